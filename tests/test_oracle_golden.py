@@ -1,0 +1,86 @@
+"""Pins the CPU oracle against fixtures produced by the reference itself
+(tests/golden/make_golden.py).  CPU only."""
+
+import json
+import os
+
+import pytest
+
+import cases
+from oracle import tsat_oracle as O
+from paper_2101_01332_b200 import bench_graphs, tensor_lang
+from paper_2101_01332_b200.cost import CostModel
+from paper_2101_01332_b200.errors import NoFiniteExtraction
+from paper_2101_01332_b200.rules import default_rules, parse_rules
+from paper_2101_01332_b200.sexpr import parse
+
+HERE = os.path.join(os.path.dirname(__file__), "golden")
+EXPLORE = json.load(open(os.path.join(HERE, "explore_golden.json")))
+GENERIC = json.load(open(os.path.join(HERE, "generic_golden.json")))
+
+
+def run_oracle_case(case):
+    g = cases.build_graph(bench_graphs, tensor_lang, case["graph"])
+    rules = cases.select_rules(default_rules(), case["rules"])
+    snaps = []
+
+    def on_it(eg, filt, rep):
+        snaps.append({"dump": eg.dump(), "filt": sorted(filt)})
+
+    eg, filt, rep = O.oracle_explore(
+        g, rules, filter_mode=case["filter_mode"],
+        allow_self_pairs=case["allow_self_pairs"], on_iteration=on_it, **case["limits"]
+    )
+    return eg, filt, rep, snaps
+
+
+@pytest.mark.parametrize("case", EXPLORE, ids=[c["id"] for c in EXPLORE])
+def test_oracle_explore_matches_reference(case):
+    eg, filt, rep, snaps = run_oracle_case(case)
+    assert len(snaps) == len(case["iterations"])
+    for i, (a, b) in enumerate(zip(snaps, case["iterations"])):
+        assert a["dump"] == b["dump"], f"iteration {i} dump"
+        assert a["filt"] == b["filt"], f"iteration {i} filter list"
+    stats = {k: v for k, v in rep.to_stats().items() if "time" not in k}
+    assert stats == case["stats"]
+    assert eg.dump() == case["final_dump"]
+    costs = O.oracle_costs(eg, CostModel())
+    assert {str(k): v for k, v in costs.items()} == case["costs"]
+    if "error" in case["greedy"]:
+        with pytest.raises(NoFiniteExtraction):
+            O.oracle_greedy(eg, costs, filt)
+    else:
+        sel, total, _ = O.oracle_greedy(eg, costs, filt)
+        assert {str(k): v for k, v in sel.items()} == case["greedy"]["selection"]
+        assert total == pytest.approx(case["greedy"]["total"], rel=1e-12)
+
+
+@pytest.mark.parametrize("rec", GENERIC["random"], ids=lambda r: f"seed{r['seed']}")
+def test_oracle_generic_egraph_matches_reference(rec):
+    eg = O.OEGraph()
+    ids = []
+    for step in cases.random_generic_ops(rec["seed"]):
+        if step[0] == "add":
+            ids.append(eg.add_enode(step[1], [ids[i] for i in step[2]]))
+        elif step[0] == "union":
+            eg.union(ids[step[1]], ids[step[2]])
+        else:
+            eg.rebuild()
+    assert ids == rec["ids"]
+    assert eg.dump() == rec["dump"]
+    for p, want in rec["matches"].items():
+        got = [[c, [list(b) for b in bs]] for c, bs in eg.ematch(parse(p))]
+        assert got == want, p
+
+
+def test_oracle_toy_saturation_matches_reference():
+    toy = parse_rules(cases.TOY_RULES_TEXT)
+    eg = O.OEGraph()
+    root = eg.add_term(parse("(div (mul a 2) 2)"))
+    eg.root = root
+    eg.add_term(parse("a"))
+    filt, rep = O.oracle_saturate(eg, toy, k_max=10)
+    want = GENERIC["toy"]
+    assert eg.dump() == want["dump"]
+    assert sorted(filt) == want["filt"]
+    assert {k: v for k, v in rep.to_stats().items() if "time" not in k} == want["stats"]
