@@ -1,0 +1,122 @@
+/*
+ * libtsat -- C-ABI of the B200 equality-saturation engine.
+ *
+ * Plain pointers and sizes only; every input array is caller-owned and copied
+ * during the call, every output goes to caller-allocated memory (query sizes
+ * first).  Status: 0 = ok, negative = error class (see TSAT_ERR_* below);
+ * tsat_last_error() has the message.  A handle is not thread-safe and every
+ * call is synchronous at return.
+ *
+ * Each entry point replaces one piece of the reference Python package
+ * (tensorsat, /root/reference/pkg/src/tensorsat); the cited file:line is the
+ * interface the call stands in for.  INTEGRATION.md shows the ctypes binding.
+ */
+#ifndef TSAT_H
+#define TSAT_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tsat_engine tsat_engine;
+
+enum {
+  TSAT_OK = 0,
+  TSAT_ERR_CUDA = -1,
+  TSAT_ERR_ARG = -2,
+  TSAT_ERR_SHAPE = -3,         /* errors.ShapeMismatch           (errors.py:22)   */
+  TSAT_ERR_SPLIT_ORIGIN = -4,  /* errors.MissingSplitOrigin      (errors.py:26)   */
+  TSAT_ERR_MERGE = -5,         /* errors.AnalysisMergeError      (errors.py:30)   */
+  TSAT_ERR_NO_FINITE = -6,     /* errors.NoFiniteExtraction      (errors.py:45)   */
+  TSAT_ERR_CAPACITY = -7,
+  TSAT_ERR_UNSUPPORTED = -8,
+  TSAT_ERR_UNKNOWN_SIG = -9,   /* errors.UnknownSignature        (errors.py:37)   */
+  TSAT_ERR_VALUE = -10,        /* ValueError (limits / filter mode, explorer.py:63-67) */
+  TSAT_ERR_STATE = -11         /* errors.TensorSatError                             */
+};
+
+typedef struct {
+  int64_t n_max, k_max, k_multi;
+  double time_limit_s; /* < 0: no limit */
+} tsat_limits;         /* explorer.ExploreLimits (explorer.py:56-67) */
+
+typedef struct {
+  int64_t iterations;
+  int32_t stop_reason; /* 0 iter-limit, 1 saturated, 2 node-limit, 3 timeout */
+  int32_t pad;
+  int64_t prefilter_checks, prefilter_rejects, postprocess_filtered, node_limit_overshoot, filter_size;
+  double time_s;
+} tsat_report;         /* explorer.ExploreReport (explorer.py:81-122) */
+
+/* lifecycle -- EGraph.__init__(analysis) (egraph.py:115-125) */
+int tsat_create(int device, int analysis, tsat_engine** out);
+void tsat_destroy(tsat_engine* h);
+const char* tsat_last_error(tsat_engine* h);
+
+/* atom table: interned ops / literals (sexpr.Atom, sexpr.py:22; Value parsing
+ * helpers tensor_lang.py:237-256).  Appends atoms [current count, n). */
+int tsat_set_atoms(tsat_engine* h, int32_t n, const int32_t* kind, const int64_t* ival,
+                   const int32_t* opcode, const int32_t* ndims, const int64_t* dims,
+                   const int32_t* nident, const int64_t* idims, const char* names,
+                   const int64_t* name_off);
+
+/* initial e-graph in build_egraph id order (tensor_lang.py:749-767) */
+int tsat_load_egraph(tsat_engine* h, uint32_t n, const uint32_t* op, const uint32_t* child_off,
+                     const uint32_t* child, uint32_t root);
+
+/* EGraph.add_term / add_enode (egraph.py:164-191): post-order programs,
+ * 4 int32 per instruction (kind 0=var/1=app, arg, atom, depth) */
+int tsat_add_terms(tsat_engine* h, int32_t ninstr, const int32_t* instr, int32_t nterm,
+                   const int32_t* term_len, int32_t nenv, const uint32_t* env, uint32_t* out_class);
+int tsat_union(tsat_engine* h, uint32_t a, uint32_t b, uint32_t* out_root); /* egraph.py:193 */
+int tsat_rebuild(tsat_engine* h);                                            /* egraph.py:216 */
+int tsat_find(tsat_engine* h, uint32_t x, uint32_t* out);                    /* egraph.py:143 */
+int tsat_set_root(tsat_engine* h, uint32_t root);                            /* EGraph.root   */
+
+/* sizes + SoA download (EGraph.nodes / classes / dump, egraph.py:127-162, 334-349) */
+int tsat_query_sizes(tsat_engine* h, uint32_t* next_id, uint32_t* live, uint32_t* nkids,
+                     uint32_t* root, uint32_t* dirty);
+int tsat_download(tsat_engine* h, uint32_t* op, uint32_t* child_off, uint32_t* child,
+                  uint32_t* cls, uint8_t* flags);
+int tsat_download_values(tsat_engine* h, void* vals, int64_t val_bytes, void* trees,
+                         int64_t tree_bytes, uint32_t* ntrees);
+int tsat_dump(tsat_engine* h, char* buf, int64_t cap, int64_t* len);
+
+/* filter list (cycles.FilterList, cycles.py:27) */
+int tsat_set_filter(tsat_engine* h, int32_t n, const uint32_t* ids, int32_t on);
+int tsat_get_filter(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n);
+
+/* compiled rule set (rules.RewriteRule + canonical patterns, rules.py:36-123) */
+int tsat_load_rules(tsat_engine* h, int64_t n, const int64_t* blob);
+
+/* explorer.saturate (explorer.py:311-365); rule_stats = nrules x 7 int64 in
+ * RuleStats field order, per_iter = 3 x k_max (enodes, alloc, eclasses) */
+int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self,
+                  tsat_report* rep, int64_t* rule_stats, int64_t* per_iter);
+
+/* EGraph.ematch of a loaded canonical pattern (egraph.py:248-262) */
+int tsat_ematch(tsat_engine* h, int32_t pattern, uint32_t* out_cls, uint32_t* out_bind, int64_t cap,
+                int64_t* n, int32_t* nb);
+
+/* cycles.break_all_cycles / dfs_get_cycles (cycles.py:172-245) */
+int tsat_break_cycles(tsat_engine* h, int64_t* added);
+int tsat_dfs_cycles(tsat_engine* h, uint32_t* nodes, int64_t cap, uint32_t* off, int64_t off_cap,
+                    int64_t* ncycles);
+
+/* cost.egraph_costs (cost.py:225-247): mode 0 synthetic, 1 table */
+int tsat_costs(tsat_engine* h, int32_t mode, int32_t strict, int32_t ntab, const char* keys,
+               const int64_t* key_off, const double* vals, double* out_by_node);
+
+/* extract.greedy_extract (extract.py:120-159); cost_by_node NULL = device
+ * vector from the last tsat_costs */
+int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, uint32_t* sel_node,
+                uint32_t* nsel, double* root_best, int64_t* rounds);
+
+/* per-phase device timings of the last saturate / greedy (ms) */
+int tsat_phase_times(tsat_engine* h, double* out, int32_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,266 @@
+// extern "C" boundary of libtsat (declared in include/tsat.h).
+#include <cstring>
+
+#include "../../include/tsat.h"
+#include "engine.cuh"
+
+struct tsat_engine {
+  Engine* e;
+  std::string err;
+};
+
+#define GUARD(h, ...)                                   \
+  do {                                                  \
+    if (!(h) || !(h)->e) return TSAT_ERR_ARG;           \
+    try {                                               \
+      __VA_ARGS__;                                      \
+      return TSAT_OK;                                   \
+    } catch (TsatException & ex) {                      \
+      (h)->err = ex.what();                             \
+      return ex.code;                                   \
+    } catch (std::exception & ex) {                     \
+      (h)->err = ex.what();                             \
+      return TSAT_ERR_STATE;                            \
+    }                                                   \
+  } while (0)
+
+extern "C" {
+
+int tsat_create(int device, int analysis, tsat_engine** out) {
+  if (!out) return TSAT_ERR_ARG;
+  *out = nullptr;
+  try {
+    tsat_engine* h = new tsat_engine();
+    h->e = new Engine(device);
+    h->e->analysis = analysis != 0;
+    *out = h;
+    return TSAT_OK;
+  } catch (TsatException& ex) {
+    return ex.code;
+  } catch (...) {
+    return TSAT_ERR_CUDA;
+  }
+}
+
+void tsat_destroy(tsat_engine* h) {
+  if (!h) return;
+  delete h->e;
+  delete h;
+}
+
+const char* tsat_last_error(tsat_engine* h) { return h ? h->err.c_str() : "null handle"; }
+
+int tsat_set_atoms(tsat_engine* h, int32_t n, const int32_t* kind, const int64_t* ival, const int32_t* opcode,
+                   const int32_t* ndims, const int64_t* dims, const int32_t* nident, const int64_t* idims,
+                   const char* names, const int64_t* name_off) {
+  GUARD(h, h->e->set_atoms(n, kind, ival, opcode, ndims, dims, nident, idims, names, name_off));
+}
+
+int tsat_load_egraph(tsat_engine* h, uint32_t n, const uint32_t* op, const uint32_t* child_off,
+                     const uint32_t* child, uint32_t root) {
+  GUARD(h, h->e->load_initial(n, op, child_off, child, root));
+}
+
+int tsat_add_terms(tsat_engine* h, int32_t ninstr, const int32_t* instr, int32_t nterm, const int32_t* term_len,
+                   int32_t nenv, const uint32_t* env, uint32_t* out_class) {
+  GUARD(h, {
+    std::vector<Instr> prog(ninstr);
+    for (int i = 0; i < ninstr; i++) {
+      prog[i].kind = instr[4 * i];
+      prog[i].arg = instr[4 * i + 1];
+      prog[i].atom = (u32)instr[4 * i + 2];
+      prog[i].depth = instr[4 * i + 3];
+    }
+    h->e->add_terms(ninstr, prog.data(), nterm, term_len, nenv, env, out_class);
+    h->e->snap.valid = false;
+  });
+}
+
+int tsat_union(tsat_engine* h, uint32_t a, uint32_t b, uint32_t* out_root) {
+  GUARD(h, {
+    *out_root = h->e->union_pair(a, b);
+    h->e->snap.valid = false;
+    if (h->e->root != TSAT_NONE) h->e->root = h->e->root;  // root tracked by node id; find() at read
+  });
+}
+
+int tsat_rebuild(tsat_engine* h) { GUARD(h, h->e->rebuild()); }
+
+int tsat_find(tsat_engine* h, uint32_t x, uint32_t* out) { GUARD(h, *out = h->e->find(x)); }
+
+int tsat_set_root(tsat_engine* h, uint32_t root) {
+  GUARD(h, {
+    if (root != TSAT_NONE && root >= h->e->h.next_id) throw TsatException(TSAT_ERR_ARG, "root out of range");
+    h->e->root = root;
+  });
+}
+
+int tsat_query_sizes(tsat_engine* h, uint32_t* next_id, uint32_t* live, uint32_t* nkids, uint32_t* root,
+                     uint32_t* dirty) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    *next_id = e.h.next_id;
+    *live = e.h.live;
+    *nkids = e.h.nkids;
+    *root = e.root == TSAT_NONE ? TSAT_NONE : e.find(e.root);
+    *dirty = e.h.dirty;
+  });
+}
+
+int tsat_download(tsat_engine* h, uint32_t* op, uint32_t* child_off, uint32_t* child, uint32_t* cls,
+                  uint8_t* flags) {
+  GUARD(h, h->e->download(op, child_off, child, cls, flags));
+}
+
+int tsat_download_values(tsat_engine* h, void* vals, int64_t val_bytes, void* trees, int64_t tree_bytes,
+                         uint32_t* ntrees) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    u64 need = (u64)e.h.next_id * sizeof(Val);
+    u32 nt;
+    CUDA_OK(cudaMemcpyAsync(&nt, e.tree_count.p, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+    e.sync();
+    *ntrees = nt;
+    if (vals) {
+      if ((u64)val_bytes < need) throw TsatException(TSAT_ERR_ARG, "value buffer too small");
+      if (need) CUDA_OK(cudaMemcpyAsync(vals, e.val.p, need, cudaMemcpyDeviceToHost, e.s));
+    }
+    if (trees) {
+      if ((u64)tree_bytes < (u64)nt * sizeof(Tree)) throw TsatException(TSAT_ERR_ARG, "tree buffer too small");
+      if (nt) CUDA_OK(cudaMemcpyAsync(trees, e.trees.p, (u64)nt * sizeof(Tree), cudaMemcpyDeviceToHost, e.s));
+    }
+    e.sync();
+  });
+}
+
+int tsat_dump(tsat_engine* h, char* buf, int64_t cap, int64_t* len) {
+  GUARD(h, {
+    std::string t = h->e->dump_text();
+    *len = (int64_t)t.size();
+    if (buf && cap >= (int64_t)t.size()) memcpy(buf, t.data(), t.size());
+  });
+}
+
+int tsat_set_filter(tsat_engine* h, int32_t n, const uint32_t* ids, int32_t on) {
+  GUARD(h, h->e->set_filter(n, ids, on));
+}
+
+int tsat_get_filter(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n) {
+  GUARD(h, {
+    std::vector<u32> f = h->e->get_filter();
+    *n = (int64_t)f.size();
+    if (out && cap >= (int64_t)f.size()) memcpy(out, f.data(), f.size() * sizeof(u32));
+  });
+}
+
+int tsat_load_rules(tsat_engine* h, int64_t n, const int64_t* blob) { GUARD(h, h->e->load_rules((int)n, blob)); }
+
+int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self, tsat_report* rep,
+                  int64_t* rule_stats, int64_t* per_iter) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    if (lim->n_max < 0 || lim->k_max < 0 || lim->k_multi < 0)
+      throw TsatException(TSAT_ERR_VALUE, "limits must be non-negative");
+    if (lim->k_multi > lim->k_max) throw TsatException(TSAT_ERR_VALUE, "k_multi must be <= k_max");
+    if (filter_mode < 0 || filter_mode > 2 || filter_mode == 1)
+      throw TsatException(TSAT_ERR_UNSUPPORTED, "filter_mode must be 'none' or 'efficient'");
+    ExploreLimitsC L{lim->n_max, lim->k_max, lim->k_multi, lim->time_limit_s};
+    e.saturate(L, filter_mode, allow_self, nullptr, 0);
+    e.snap.valid = false;
+    rep->iterations = e.report.iterations;
+    rep->stop_reason = e.report.stop_reason;
+    rep->prefilter_checks = e.report.prefilter_checks;
+    rep->prefilter_rejects = e.report.prefilter_rejects;
+    rep->postprocess_filtered = e.report.postprocess_filtered;
+    rep->node_limit_overshoot = e.report.node_limit_overshoot;
+    rep->filter_size = e.report.filter_size;
+    rep->time_s = e.report.time_s;
+    for (size_t r = 0; r < e.rstats.size(); r++) {
+      const RuleStatsH& s = e.rstats[r];
+      int64_t* o = rule_stats + 7 * r;
+      o[0] = s.found;
+      o[1] = s.applied;
+      o[2] = s.applied_noop;
+      o[3] = s.skipped_self;
+      o[4] = s.skipped_compat;
+      o[5] = s.skipped_shape;
+      o[6] = s.skipped_cycle;
+    }
+    for (size_t i = 0; i < e.enodes_per_iter.size(); i++) {
+      per_iter[3 * i] = e.enodes_per_iter[i];
+      per_iter[3 * i + 1] = e.alloc_per_iter[i];
+      per_iter[3 * i + 2] = e.eclasses_per_iter[i];
+    }
+  });
+}
+
+int tsat_ematch(tsat_engine* h, int32_t pattern, uint32_t* out_cls, uint32_t* out_bind, int64_t cap, int64_t* n,
+                int32_t* nb) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    if (pattern < 0 || pattern >= (int)e.patterns.size()) throw TsatException(TSAT_ERR_ARG, "bad pattern id");
+    e.snap.valid = false;
+    MatchSet ms;
+    e.ematch_pattern(pattern, ms);
+    *n = ms.n;
+    *nb = ms.nb;
+    if (out_cls && cap >= (int64_t)ms.n && ms.n) {
+      CUDA_OK(cudaMemcpyAsync(out_cls, ms.cls.p, ms.n * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+      if (ms.nb)
+        CUDA_OK(cudaMemcpyAsync(out_bind, ms.bind.p, (u64)ms.n * ms.nb * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+      e.sync();
+    }
+  });
+}
+
+int tsat_break_cycles(tsat_engine* h, int64_t* added) {
+  GUARD(h, {
+    h->e->snap.valid = false;
+    *added = h->e->break_all_cycles(false, nullptr);
+  });
+}
+
+int tsat_dfs_cycles(tsat_engine* h, uint32_t* nodes, int64_t cap, uint32_t* off, int64_t off_cap, int64_t* ncycles) {
+  GUARD(h, {
+    h->e->snap.valid = false;
+    std::vector<std::vector<u32>> cyc;
+    h->e->break_all_cycles(false, &cyc);
+    *ncycles = (int64_t)cyc.size();
+    int64_t tot = 0;
+    for (auto& c : cyc) tot += (int64_t)c.size();
+    if (nodes && cap >= tot && off_cap > (int64_t)cyc.size()) {
+      int64_t k = 0;
+      for (size_t i = 0; i < cyc.size(); i++) {
+        off[i] = (uint32_t)k;
+        for (u32 x : cyc[i]) nodes[k++] = x;
+      }
+      off[cyc.size()] = (uint32_t)k;
+    } else {
+      *ncycles = -tot - 1;  // buffer too small: -(total nodes) - 1
+    }
+  });
+}
+
+int tsat_costs(tsat_engine* h, int32_t mode, int32_t strict, int32_t ntab, const char* keys, const int64_t* key_off,
+               const double* vals, double* out_by_node) {
+  GUARD(h, {
+    if (!h->e->snap.valid) h->e->build_snapshot();
+    h->e->costs(mode, strict, ntab, keys, key_off, vals, out_by_node);
+  });
+}
+
+int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, uint32_t* sel_node, uint32_t* nsel,
+                double* root_best, int64_t* rounds) {
+  GUARD(h, {
+    h->e->snap.valid = false;
+    *root_best = h->e->greedy(cost_by_node, sel_cls, sel_node, nsel, rounds);
+  });
+}
+
+int tsat_phase_times(tsat_engine* h, double* out, int32_t n) {
+  GUARD(h, {
+    for (int i = 0; i < n; i++) out[i] = i < (int)h->e->phase_ms.size() ? h->e->phase_ms[i] : 0.0;
+  });
+}
+
+}  // extern "C"

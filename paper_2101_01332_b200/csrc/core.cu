@@ -1,0 +1,751 @@
+// libtsat core: buffers, loading, sequential (exact) mutation kernels,
+// parallel congruence rebuild, snapshot CSR construction, download + dump.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <sstream>
+
+#include "engine.cuh"
+
+static inline unsigned nblk(u64 n, unsigned t = 256) {
+  u64 b = (n + t - 1) / t;
+  if (b < 1) b = 1;
+  if (b > 148ull * 64) b = 148ull * 64;  // grid-stride beyond 64 CTAs per SM
+  return (unsigned)b;
+}
+
+#define GRID_STRIDE(i, n) for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < (n); i += (u64)gridDim.x * blockDim.x)
+
+u32 bits_for(u32 maxval) {
+  u32 b = 1;
+  while (b < 32 && (1ull << b) <= maxval) b++;
+  return b;
+}
+
+// ---------------------------------------------------------------- cub helpers
+
+void dev_exclusive_scan_u32(Engine& e, const u32* in, u32* out, u32 n) {
+  size_t bytes = 0;
+  CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, e.s));
+  e.temp.ensure(bytes + 16);
+  CUDA_OK(cub::DeviceScan::ExclusiveSum(e.temp.p, bytes, in, out, n, e.s));
+}
+
+void dev_sort_pairs_u32(Engine& e, u32* kin, u32* kout, u32* vin, u32* vout, u32 n, int end_bit) {
+  size_t bytes = 0;
+  CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, n, 0, end_bit, e.s));
+  e.temp.ensure(bytes + 16);
+  CUDA_OK(cub::DeviceRadixSort::SortPairs(e.temp.p, bytes, kin, kout, vin, vout, n, 0, end_bit, e.s));
+}
+
+// ---------------------------------------------------------------- lifecycle
+
+Engine::Engine(int dev) : device(dev) {
+  CUDA_OK(cudaSetDevice(dev));
+  CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cnt.alloc(1);
+  err.alloc(1);
+  dstats.alloc(1);
+  CUDA_OK(cudaMemsetAsync(cnt.p, 0, sizeof(Counters), s));
+  CUDA_OK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
+  memset(&h, 0, sizeof(h));
+  tree_cap = 1 << 16;
+  tree_hc_cap = 1 << 18;
+  trees.alloc(tree_cap);
+  tree_hc.alloc(tree_hc_cap);
+  tree_count.alloc(1);
+  CUDA_OK(cudaMemsetAsync(tree_hc.p, 0xFF, tree_hc_cap * sizeof(u32), s));
+  CUDA_OK(cudaMemsetAsync(tree_count.p, 0, sizeof(u32), s));
+  ensure_nodes(1024, 4096);
+  sync();
+}
+
+Engine::~Engine() {
+  if (s) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+}
+
+G Engine::view() {
+  G g;
+  g.op = op.p;
+  g.koff = koff.p;
+  g.kids = kids.p;
+  g.parent = parent.p;
+  g.flags = flags.p;
+  g.val = val.p;
+  g.hc = hc.p;
+  g.hc_mask = hc_cap - 1;
+  g.cap_nodes = cap_nodes;
+  g.cap_kids = cap_kids;
+  g.analysis = analysis ? 1 : 0;
+  g.atoms = atoms.p;
+  g.tt.trees = trees.p;
+  g.tt.hc = tree_hc.p;
+  g.tt.hc_mask = tree_hc_cap - 1;
+  g.tt.count = tree_count.p;
+  g.tt.cap = tree_cap;
+  g.err = err.p;
+  g.cnt = cnt.p;
+  return g;
+}
+
+void Engine::sync() { CUDA_OK(cudaStreamSynchronize(s)); }
+
+void Engine::pull_counters() {
+  CUDA_OK(cudaMemcpyAsync(&h, cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  sync();
+}
+
+void Engine::push_counters() {
+  CUDA_OK(cudaMemcpyAsync(cnt.p, &h, sizeof(Counters), cudaMemcpyHostToDevice, s));
+}
+
+static const char* status_name(int c) {
+  switch (c) {
+    case TSAT_ERR_SHAPE: return "ShapeMismatch";
+    case TSAT_ERR_SPLIT_ORIGIN: return "MissingSplitOrigin";
+    case TSAT_ERR_MERGE: return "AnalysisMergeError";
+    case TSAT_ERR_CAPACITY: return "capacity";
+    default: return "error";
+  }
+}
+
+void Engine::check_error() {
+  DevError he;
+  CUDA_OK(cudaMemcpyAsync(&he, err.p, sizeof(he), cudaMemcpyDeviceToHost, s));
+  sync();
+  if (he.code != 0) {
+    CUDA_OK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
+    std::ostringstream os;
+    os << status_name(he.code) << " (detail " << he.detail << ", " << he.a << ", " << he.b << ")";
+    if (he.code == TSAT_ERR_MERGE) {
+      os.str("");
+      os << "incompatible analyses " << value_str((u32)he.a) << " vs " << value_str((u32)he.b);
+    } else if (he.code == TSAT_ERR_SHAPE || he.code == TSAT_ERR_SPLIT_ORIGIN) {
+      os.str("");
+      std::string opn = (he.b >= 0 && (size_t)he.b < atom_names.size()) ? atom_names[he.b] : "?";
+      os << "shape inference failed for operator '" << opn << "' (node n" << he.a << ")";
+    }
+    throw TsatException(he.code, os.str());
+  }
+}
+
+// ---------------------------------------------------------------- capacity
+
+__global__ void k_hc_insert_alive(G g, u32 n) {
+  GRID_STRIDE(i, n) {
+    if (g.flags[i] & NF_ALIVE) hc_insert(g, (u32)i);
+  }
+}
+
+void Engine::rehash(u32 new_cap) {
+  hc.alloc(new_cap);
+  hc_cap = new_cap;
+  CUDA_OK(cudaMemsetAsync(hc.p, 0xFF, (size_t)new_cap * sizeof(u32), s));
+  if (h.next_id) k_hc_insert_alive<<<nblk(h.next_id), 256, 0, s>>>(view(), h.next_id);
+}
+
+void Engine::ensure_nodes(u64 extra_nodes, u64 extra_kids) {
+  u64 need_n = (u64)h.next_id + extra_nodes + 1;
+  u64 need_k = (u64)h.nkids + extra_kids + 1;
+  if (need_n >= 0xF0000000ull || need_k >= 0xF0000000ull)
+    throw TsatException(TSAT_ERR_CAPACITY, "e-graph exceeds 32-bit id space");
+  if (need_n > cap_nodes) {
+    u64 nc = cap_nodes ? cap_nodes : 1024;
+    while (nc < need_n) nc *= 2;
+    op.grow(nc, h.next_id, s);
+    koff.grow(nc + 1, (u64)h.next_id + 1, s);
+    parent.grow(nc, h.next_id, s);
+    flags.grow(nc, h.next_id, s);
+    val.grow(nc, h.next_id, s);
+    cap_nodes = (u32)std::min<u64>(nc, op.cap);
+    if (h.next_id == 0) CUDA_OK(cudaMemsetAsync(koff.p, 0, sizeof(u32), s));
+  }
+  if (need_k > cap_kids) {
+    u64 nc = cap_kids ? cap_kids : 4096;
+    while (nc < need_k) nc *= 2;
+    kids.grow(nc, h.nkids, s);
+    cap_kids = (u32)kids.cap;
+  }
+  // hashcons load factor <= 1/2 over all allocated ids
+  u64 want = 16;
+  while (want < 2 * need_n) want *= 2;
+  if (want > hc_cap) rehash((u32)want);
+}
+
+// ---------------------------------------------------------------- atoms
+
+void Engine::set_atoms(int n, const int32_t* kind, const i64* ival, const int32_t* opcode,
+                       const int32_t* ndims, const i64* dims, const int32_t* nident, const i64* idims,
+                       const char* names_blob, const i64* name_off) {
+  size_t old = h_atoms.size();
+  if ((size_t)n < old) throw TsatException(TSAT_ERR_ARG, "atom table can only grow");
+  for (int i = (int)old; i < n; i++) {
+    AtomInfo a;
+    memset(&a, 0, sizeof(a));
+    a.kind = kind[i];
+    a.opcode = opcode[i];
+    a.ival = ival[i];
+    a.ndims = ndims[i];
+    a.nident = nident[i];
+    for (int j = 0; j < 4; j++) {
+      a.dims[j] = dims[4 * (size_t)i + j];
+      a.idims[j] = idims[4 * (size_t)i + j];
+    }
+    h_atoms.push_back(a);
+    atom_names.emplace_back(names_blob + name_off[i], names_blob + name_off[i + 1]);
+  }
+  if (atoms.cap < h_atoms.size()) atoms.grow(h_atoms.size() * 2 + 16, 0, s);
+  CUDA_OK(cudaMemcpyAsync(atoms.p, h_atoms.data(), h_atoms.size() * sizeof(AtomInfo),
+                          cudaMemcpyHostToDevice, s));
+  // atom names (signature keys for cost-table lookups are rendered on device)
+  std::vector<char> blob;
+  std::vector<u32> offs;
+  for (auto& nm : atom_names) {
+    offs.push_back((u32)blob.size());
+    blob.insert(blob.end(), nm.begin(), nm.end());
+  }
+  offs.push_back((u32)blob.size());
+  sync();
+  d_names.alloc(blob.size() + 1);
+  d_name_off.alloc(offs.size());
+  if (!blob.empty())
+    CUDA_OK(cudaMemcpyAsync(d_names.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpyAsync(d_name_off.p, offs.data(), offs.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
+  sync();
+}
+
+// ---------------------------------------------------------------- bulk load
+
+__global__ void k_init_nodes(G g, u32 n) {
+  GRID_STRIDE(i, n) {
+    g.parent[i] = (u32)i;
+    g.flags[i] = NF_ALIVE;
+  }
+}
+
+// analysis values for the nodes of one depth level (children already valued)
+__global__ void k_make_level(G g, const u32* ids, u32 n) {
+  GRID_STRIDE(t, n) {
+    u32 nid = ids[t];
+    u32 a = g.koff[nid], b = g.koff[nid + 1];
+    int k = (int)(b - a);
+    Val kv[7];
+    if (k > 7) {
+      dev_set_error(g.err, TSAT_ERR_SHAPE, 3, nid, g.op[nid]);
+      continue;
+    }
+    for (int j = 0; j < k; j++) kv[j] = g.val[g.kids[a + j]];
+    Val v;
+    int st = val_make(g.op[nid], kv, k, v, g.atoms, g.tt);
+    if (st != AS_OK) {
+      dev_set_error(g.err, ana_to_status(st), 3, nid, g.op[nid]);
+      continue;
+    }
+    g.val[nid] = v;
+  }
+}
+
+void Engine::load_initial(u32 n, const u32* hop, const u32* hkoff, const u32* hkids, u32 r) {
+  if (h.next_id != 0) throw TsatException(TSAT_ERR_STATE, "load_initial on a non-empty e-graph");
+  u32 nk = hkoff[n];
+  for (u32 i = 0; i < n; i++)
+    for (u32 j = hkoff[i]; j < hkoff[i + 1]; j++)
+      if (hkids[j] >= i) throw TsatException(TSAT_ERR_ARG, "children must precede their parent");
+  ensure_nodes(n, nk);
+  CUDA_OK(cudaMemcpyAsync(op.p, hop, n * sizeof(u32), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpyAsync(koff.p, hkoff, (n + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
+  if (nk) CUDA_OK(cudaMemcpyAsync(kids.p, hkids, nk * sizeof(u32), cudaMemcpyHostToDevice, s));
+  k_init_nodes<<<nblk(n), 256, 0, s>>>(view(), n);
+  h.next_id = n;
+  h.live = n;
+  h.nkids = nk;
+  h.dirty = 0;
+  push_counters();
+  k_hc_insert_alive<<<nblk(n), 256, 0, s>>>(view(), n);
+  if (analysis) {
+    // depth levels computed on the host from the (small) initial graph
+    std::vector<u32> lvl(n, 0);
+    u32 maxl = 0;
+    for (u32 i = 0; i < n; i++) {
+      u32 l = 0;
+      for (u32 j = hkoff[i]; j < hkoff[i + 1]; j++) l = std::max(l, lvl[hkids[j]] + 1);
+      lvl[i] = l;
+      maxl = std::max(maxl, l);
+    }
+    std::vector<std::vector<u32>> by(maxl + 1);
+    for (u32 i = 0; i < n; i++) by[lvl[i]].push_back(i);
+    DevBuf<u32>& ids = scratch_u32[0];
+    ids.ensure(n + 1);
+    std::vector<u32> flat;
+    std::vector<size_t> off;
+    for (auto& v : by) {
+      off.push_back(flat.size());
+      flat.insert(flat.end(), v.begin(), v.end());
+    }
+    CUDA_OK(cudaMemcpyAsync(ids.p, flat.data(), flat.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
+    for (size_t l = 0; l < by.size(); l++)
+      if (!by[l].empty())
+        k_make_level<<<nblk(by[l].size()), 128, 0, s>>>(view(), ids.p + off[l], (u32)by[l].size());
+    sync();
+  }
+  root = r;
+  check_error();
+}
+
+// ---------------------------------------------------------------- sequential ops
+
+// run a batch of term programs (post-order Instr) against env, one thread:
+// exactly add_term (egraph.py:184-191) for each term in order.
+__global__ void k_seq_add_terms(G g, const Instr* prog, const int32_t* term_len, int nterm,
+                                const u32* env, u32* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  u32 stack[64];
+  int pc = 0;
+  for (int t = 0; t < nterm; t++) {
+    int sp = 0;
+    for (int k = 0; k < term_len[t]; k++, pc++) {
+      const Instr& in = prog[pc];
+      if (in.kind == I_VAR) {
+        stack[sp++] = uf_find(g.parent, env[in.arg]);
+      } else {
+        int na = in.arg;
+        sp -= na;
+        u32 kidsb[8];
+        for (int j = 0; j < na; j++) kidsb[j] = stack[sp + j];
+        u32 c = seq_add_enode(g, in.atom, kidsb, na);
+        if (c == TSAT_NONE) return;
+        stack[sp++] = c;
+      }
+    }
+    out[t] = stack[0];
+  }
+}
+
+void Engine::add_terms(int ninstr, const Instr* prog, int nterm, const int32_t* term_len, int nenv,
+                       const u32* env, u32* out_cls) {
+  u64 napp = 0, nk = 0;
+  for (int i = 0; i < ninstr; i++) {
+    if (prog[i].kind == I_APP) {
+      napp++;
+      nk += prog[i].arg;
+      if (prog[i].arg > 8) throw TsatException(TSAT_ERR_ARG, "arity > 8 not supported");
+    }
+  }
+  ensure_nodes(napp, nk);
+  DevBuf<Instr> dp;
+  dp.alloc(ninstr + 1);
+  DevBuf<int32_t> dl;
+  dl.alloc(nterm + 1);
+  DevBuf<u32> de, dout;
+  de.alloc(nenv + 1);
+  dout.alloc(nterm + 1);
+  CUDA_OK(cudaMemcpyAsync(dp.p, prog, ninstr * sizeof(Instr), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpyAsync(dl.p, term_len, nterm * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (nenv) CUDA_OK(cudaMemcpyAsync(de.p, env, nenv * sizeof(u32), cudaMemcpyHostToDevice, s));
+  k_seq_add_terms<<<1, 1, 0, s>>>(view(), dp.p, dl.p, nterm, de.p, dout.p);
+  CUDA_OK(cudaMemcpyAsync(out_cls, dout.p, nterm * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  pull_counters();
+  check_error();
+}
+
+__global__ void k_seq_union(G g, u32 a, u32 b, u32* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  *out = seq_union(g, a, b);
+}
+
+u32 Engine::union_pair(u32 a, u32 b) {
+  if (a >= h.next_id || b >= h.next_id) throw TsatException(TSAT_ERR_ARG, "unknown e-class id");
+  DevBuf<u32>& o = scratch_u32[7];
+  o.ensure(1);
+  k_seq_union<<<1, 1, 0, s>>>(view(), a, b, o.p);
+  u32 r;
+  CUDA_OK(cudaMemcpyAsync(&r, o.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  pull_counters();
+  check_error();
+  return r;
+}
+
+__global__ void k_find(G g, u32 x, u32* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  *out = uf_find(g.parent, x);
+}
+
+u32 Engine::find(u32 x) {
+  if (x >= h.next_id) throw TsatException(TSAT_ERR_ARG, "unknown id");
+  DevBuf<u32>& o = scratch_u32[7];
+  o.ensure(1);
+  k_find<<<1, 1, 0, s>>>(view(), x, o.p);
+  u32 r;
+  CUDA_OK(cudaMemcpyAsync(&r, o.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
+  return r;
+}
+
+// ---------------------------------------------------------------- filter list
+
+__global__ void k_set_filter(G g, const u32* ids, u32 n, int on) {
+  GRID_STRIDE(i, n) {
+    u32 x = ids[i];
+    if (on) g.flags[x] |= NF_FILT;
+    else g.flags[x] &= ~NF_FILT;
+  }
+}
+
+__global__ void k_clear_filter(G g, u32 n) {
+  GRID_STRIDE(i, n) g.flags[i] &= ~NF_FILT;
+}
+
+void Engine::set_filter(int n, const u32* ids, int on) {
+  if (on == 2) {
+    if (h.next_id) k_clear_filter<<<nblk(h.next_id), 256, 0, s>>>(view(), h.next_id);
+    sync();
+    return;
+  }
+  if (n <= 0) return;
+  for (int i = 0; i < n; i++)
+    if (ids[i] >= h.next_id) throw TsatException(TSAT_ERR_ARG, "filter id out of range");
+  DevBuf<u32> d;
+  d.alloc(n);
+  CUDA_OK(cudaMemcpyAsync(d.p, ids, n * sizeof(u32), cudaMemcpyHostToDevice, s));
+  k_set_filter<<<nblk(n), 256, 0, s>>>(view(), d.p, n, on);
+  sync();
+}
+
+std::vector<u32> Engine::get_filter() {
+  std::vector<u8> f(h.next_id);
+  if (h.next_id)
+    CUDA_OK(cudaMemcpyAsync(f.data(), flags.p, h.next_id, cudaMemcpyDeviceToHost, s));
+  sync();
+  std::vector<u32> out;
+  for (u32 i = 0; i < h.next_id; i++)
+    if (f[i] & NF_FILT) out.push_back(i);
+  return out;
+}
+
+// ---------------------------------------------------------------- rebuild
+// Congruence closure to fixpoint (reference egraph.py:216-238).  Each round:
+// canonicalise every live node's children against the frozen union-find,
+// regroup by (op, children) keeping the minimum id per key, drop the others
+// and union their classes with the survivor's.  Survivor = min id per final
+// key and the partition is the congruence closure, so the result equals the
+// reference's sequential pass (verified by the parity tests).
+
+__global__ void k_canon_kids(G g, u32 n) {
+  GRID_STRIDE(i, n) {
+    if (!(g.flags[i] & NF_ALIVE)) continue;
+    u32 a = g.koff[i], b = g.koff[i + 1];
+    for (u32 j = a; j < b; j++) g.kids[j] = uf_find(g.parent, g.kids[j]);
+  }
+}
+
+__global__ void k_dedup_insert(G g, u32 n) {
+  GRID_STRIDE(i0, n) {
+    u32 i = (u32)i0;
+    if (!(g.flags[i] & NF_ALIVE)) continue;
+    u32 slot = (u32)node_hash(g, i) & g.hc_mask;
+    while (true) {
+      u32 cur = ((volatile u32*)g.hc)[slot];
+      if (cur == TSAT_NONE) {
+        u32 prev = atomicCAS(&g.hc[slot], TSAT_NONE, i);
+        if (prev == TSAT_NONE) break;
+        cur = prev;
+      }
+      if (node_eq_node(g, cur, i)) {
+        atomicMin(&g.hc[slot], i);
+        break;
+      }
+      slot = (slot + 1) & g.hc_mask;
+    }
+  }
+}
+
+// drop non-survivors and union them with their survivor; record linked roots
+__global__ void k_dedup_drop(G g, u32 n, u32* linked, u32* nlinked, u32* dropped) {
+  GRID_STRIDE(i0, n) {
+    u32 i = (u32)i0;
+    if (!(g.flags[i] & NF_ALIVE)) continue;
+    u32 a = g.koff[i];
+    int k = (int)(g.koff[i + 1] - a);
+    u32 sv = hc_lookup(g, g.op[i], k, g.kids + a);
+    if (sv == i) continue;
+    g.flags[i] &= ~NF_ALIVE;
+    atomicAdd(dropped, 1u);
+    // union(find(sv), find(i)) with record of the root that got linked
+    u32 x = sv, y = i;
+    while (true) {
+      x = uf_find_ro(g.parent, x);
+      y = uf_find_ro(g.parent, y);
+      if (x == y) break;
+      u32 lo = x < y ? x : y, hi = x < y ? y : x;
+      if (atomicCAS(&g.parent[hi], hi, lo) == hi) {
+        linked[atomicAdd(nlinked, 1u)] = hi;
+        break;
+      }
+    }
+  }
+}
+
+__global__ void k_link_targets(G g, const u32* linked, u32 m, u32* tgt) {
+  GRID_STRIDE(i, m) tgt[i] = uf_find_ro(g.parent, linked[i]);
+}
+
+// one thread per merged group (sorted by target): fold analyses in
+__global__ void k_merge_groups(G g, const u32* tgt, const u32* src, u32 m) {
+  GRID_STRIDE(i, m) {
+    if (i > 0 && tgt[i - 1] == tgt[i]) continue;
+    u32 t = tgt[i];
+    Val acc = g.val[t];
+    for (u64 j = i; j < m && tgt[j] == t; j++) {
+      const Val& o = g.val[src[j]];
+      if (!val_same_data(acc, o)) {
+        dev_set_error(g.err, TSAT_ERR_MERGE, 4, t, src[j]);
+        break;
+      }
+      if (val_merge_into(acc, o) != AS_OK) {
+        dev_set_error(g.err, TSAT_ERR_CAPACITY, 5, t, src[j]);
+        break;
+      }
+    }
+    g.val[t] = acc;
+  }
+}
+
+void Engine::rebuild() {
+  if (!h.dirty) return;
+  u32 n = h.next_id;
+  DevBuf<u32>& linked = scratch_u32[1];
+  DevBuf<u32>& tgt = scratch_u32[2];
+  DevBuf<u32>& srt_t = scratch_u32[3];
+  DevBuf<u32>& srt_s = scratch_u32[4];
+  DevBuf<u32>& small = scratch_u32[5];
+  linked.ensure(n + 1);
+  tgt.ensure(n + 1);
+  srt_t.ensure(n + 1);
+  srt_s.ensure(n + 1);
+  small.ensure(4);
+  while (true) {
+    k_canon_kids<<<nblk(n), 256, 0, s>>>(view(), n);
+    CUDA_OK(cudaMemsetAsync(hc.p, 0xFF, (size_t)hc_cap * sizeof(u32), s));
+    k_dedup_insert<<<nblk(n), 256, 0, s>>>(view(), n);
+    CUDA_OK(cudaMemsetAsync(small.p, 0, 2 * sizeof(u32), s));
+    k_dedup_drop<<<nblk(n), 256, 0, s>>>(view(), n, linked.p, small.p, small.p + 1);
+    u32 hm[2];
+    CUDA_OK(cudaMemcpyAsync(hm, small.p, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    sync();
+    u32 m = hm[0];
+    h.live -= hm[1];
+    if (m && analysis) {
+      k_link_targets<<<nblk(m), 256, 0, s>>>(view(), linked.p, m, tgt.p);
+      dev_sort_pairs_u32(*this, tgt.p, srt_t.p, linked.p, srt_s.p, m, bits_for(n));
+      k_merge_groups<<<nblk(m), 256, 0, s>>>(view(), srt_t.p, srt_s.p, m);
+    }
+    if (m == 0) break;
+  }
+  h.dirty = 0;
+  push_counters();
+  sync();
+  check_error();
+  snap.valid = false;
+}
+
+// ---------------------------------------------------------------- snapshot CSR
+
+__global__ void k_alive_flags(G g, u32 n, u32* fl) {
+  GRID_STRIDE(i, n) fl[i] = (g.flags[i] & NF_ALIVE) ? 1u : 0u;
+}
+
+__global__ void k_compact_alive(G g, u32 n, const u32* pos, u32* ids, u32* cls, u32* opk) {
+  GRID_STRIDE(i, n) {
+    if (!(g.flags[i] & NF_ALIVE)) continue;
+    u32 p = pos[i];
+    ids[p] = (u32)i;
+    cls[p] = uf_find_ro(g.parent, (u32)i);
+    opk[p] = g.op[i];
+  }
+}
+
+__global__ void k_class_heads(const u32* scls, u32 m, u32* head) {
+  GRID_STRIDE(i, m) head[i] = (i == 0 || scls[i] != scls[i - 1]) ? 1u : 0u;
+}
+
+__global__ void k_class_index(const u32* scls, const u32* headpos, u32 m, u32* cls_off, u32* cls_ids,
+                              u32* cls_index) {
+  GRID_STRIDE(i, m) {
+    if (i == 0 || scls[i] != scls[i - 1]) {
+      u32 d = headpos[i];
+      cls_off[d] = (u32)i;
+      cls_ids[d] = scls[i];
+      cls_index[scls[i]] = d;
+    }
+  }
+}
+
+__global__ void k_set_u32(u32* p, u32 idx, u32 v) { p[idx] = v; }
+
+__global__ void k_op_hist(const u32* ops, u32 m, u32* hist) {
+  GRID_STRIDE(i, m) atomicAdd(&hist[ops[i]], 1u);
+}
+
+void Engine::build_snapshot() {
+  u32 n = h.next_id, m = h.live;
+  DevBuf<u32>& fl = scratch_u32[1];
+  DevBuf<u32>& pos = scratch_u32[2];
+  DevBuf<u32>& ids = scratch_u32[3];
+  DevBuf<u32>& cls = scratch_u32[4];
+  DevBuf<u32>& opk = scratch_u32[5];
+  DevBuf<u32>& tmp = scratch_u32[6];
+  u32 na = (u32)h_atoms.size();
+  fl.ensure(std::max(n, na) + 2);
+  pos.ensure(std::max(n, na) + 2);
+  ids.ensure(m + 1);
+  cls.ensure(m + 1);
+  opk.ensure(m + 1);
+  tmp.ensure(m + 1);
+  k_alive_flags<<<nblk(n), 256, 0, s>>>(view(), n, fl.p);
+  dev_exclusive_scan_u32(*this, fl.p, pos.p, n);
+  k_compact_alive<<<nblk(n), 256, 0, s>>>(view(), n, pos.p, ids.p, cls.p, opk.p);
+  // class CSR: stable sort (class, id) -> members grouped, ascending
+  snap.cls_nodes.ensure(m + 1);
+  snap.cls_index.ensure(n + 1);
+  CUDA_OK(cudaMemsetAsync(snap.cls_index.p, 0xFF, (size_t)(n + 1) * sizeof(u32), s));
+  u32 nb = bits_for(n);
+  dev_sort_pairs_u32(*this, cls.p, tmp.p, ids.p, snap.cls_nodes.p, m, nb);
+  // tmp = sorted class ids
+  k_class_heads<<<nblk(m), 256, 0, s>>>(tmp.p, m, fl.p);
+  dev_exclusive_scan_u32(*this, fl.p, pos.p, m);
+  u32 last_head = 0, last_pos = 0;
+  if (m) {
+    CUDA_OK(cudaMemcpyAsync(&last_head, fl.p + m - 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(&last_pos, pos.p + m - 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  }
+  sync();
+  u32 ncls = m ? last_pos + last_head : 0;
+  snap.cls_off.ensure(ncls + 1);
+  snap.cls_ids.ensure(ncls + 1);
+  k_class_index<<<nblk(m), 256, 0, s>>>(tmp.p, pos.p, m, snap.cls_off.p, snap.cls_ids.p, snap.cls_index.p);
+  k_set_u32<<<1, 1, 0, s>>>(snap.cls_off.p, ncls, m);
+  // op CSR: stable sort alive ids by op atom
+  snap.op_nodes.ensure(m + 1);
+  snap.op_off.ensure(na + 1);
+  CUDA_OK(cudaMemsetAsync(fl.p, 0, (size_t)(na + 1) * sizeof(u32), s));
+  k_op_hist<<<nblk(m), 256, 0, s>>>(opk.p, m, fl.p);
+  dev_exclusive_scan_u32(*this, fl.p, snap.op_off.p, na + 1);
+  dev_sort_pairs_u32(*this, opk.p, tmp.p, ids.p, snap.op_nodes.p, m, bits_for(na));
+  snap.n_alloc = n;
+  snap.ncls = ncls;
+  snap.valid = true;
+  sync();
+}
+
+// ---------------------------------------------------------------- download / dump
+
+void Engine::download(u32* hop, u32* hkoff, u32* hkids, u32* hcls, u8* hflags) {
+  u32 n = h.next_id;
+  std::vector<u32> par(n);
+  if (n) {
+    CUDA_OK(cudaMemcpyAsync(hop, op.p, n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(hkoff, koff.p, (n + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    if (h.nkids) CUDA_OK(cudaMemcpyAsync(hkids, kids.p, h.nkids * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(par.data(), parent.p, n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(hflags, flags.p, n, cudaMemcpyDeviceToHost, s));
+  }
+  sync();
+  for (u32 i = 0; i < n; i++) {
+    u32 r = i;
+    while (par[r] != r) r = par[r];
+    u32 x = i;
+    while (par[x] != r) {
+      u32 nx = par[x];
+      par[x] = r;
+      x = nx;
+    }
+    hcls[i] = r;
+  }
+}
+
+static void dims_str(std::ostringstream& os, const i64* d, int r) {
+  for (int i = 0; i < r; i++) {
+    if (i) os << "x";
+    os << d[i];
+  }
+}
+
+static std::string val_to_string(const Val& v, const std::vector<std::string>& names) {
+  std::ostringstream os;
+  switch (v.kind) {
+    case VK_N: os << "N:" << v.iv; break;
+    case VK_S: os << "S:" << names[v.iv]; break;
+    case VK_T: os << "T:"; dims_str(os, v.d0, v.r0); break;
+    case VK_TT:
+      os << "TT:";
+      dims_str(os, v.d0, v.r0);
+      os << "|";
+      dims_str(os, v.d1, v.r1);
+      break;
+    default: os << "?";
+  }
+  return os.str();
+}
+
+std::string Engine::value_str(u32 c) {
+  if (!analysis || c >= h.next_id) return "";
+  Val v;
+  CUDA_OK(cudaMemcpyAsync(&v, val.p + c, sizeof(Val), cudaMemcpyDeviceToHost, s));
+  sync();
+  return val_to_string(v, atom_names);
+}
+
+std::string Engine::dump_text() {
+  u32 n = h.next_id;
+  std::vector<u32> hop(n), hkoff(n + 1), hkids(h.nkids + 1), hcls(n);
+  std::vector<u8> hfl(n);
+  download(hop.data(), hkoff.data(), hkids.data(), hcls.data(), hfl.data());
+  std::vector<Val> hv;
+  if (analysis && n) {
+    hv.resize(n);
+    CUDA_OK(cudaMemcpyAsync(hv.data(), val.p, n * sizeof(Val), cudaMemcpyDeviceToHost, s));
+    sync();
+  }
+  // classes = roots of alive nodes; members ascending
+  std::vector<u32> first(n, TSAT_NONE), nxt(n, TSAT_NONE), last(n, TSAT_NONE);
+  u32 nclasses = 0, nnodes = 0;
+  std::vector<u32> order;
+  for (u32 i = 0; i < n; i++) {
+    if (!(hfl[i] & NF_ALIVE)) continue;
+    nnodes++;
+    u32 c = hcls[i];
+    if (first[c] == TSAT_NONE) {
+      first[c] = i;
+      nclasses++;
+      order.push_back(c);
+    } else {
+      nxt[last[c]] = i;
+    }
+    last[c] = i;
+  }
+  std::sort(order.begin(), order.end());
+  std::ostringstream os;
+  os << "egraph nodes=" << nnodes << " classes=" << nclasses << " root=";
+  if (root == TSAT_NONE) os << "-";
+  else os << "c" << hcls[root];
+  os << "\n";
+  for (u32 c : order) {
+    os << "c" << c;
+    if (analysis) os << " [" << val_to_string(hv[c], atom_names) << "]";
+    os << ":";
+    for (u32 i = first[c]; i != TSAT_NONE; i = nxt[i]) {
+      os << " n" << i << "=" << atom_names[hop[i]] << "(";
+      for (u32 j = hkoff[i]; j < hkoff[i + 1]; j++) {
+        if (j > hkoff[i]) os << ",";
+        os << "c" << hcls[hkids[j]];
+      }
+      os << ")";
+    }
+    os << "\n";
+  }
+  return os.str();
+}

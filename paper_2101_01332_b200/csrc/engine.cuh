@@ -1,0 +1,257 @@
+// Host-side engine object behind one C-ABI handle (include/tsat.h).
+#pragma once
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "egraph.cuh"
+
+struct TsatException : public std::runtime_error {
+  int code;
+  TsatException(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  void alloc(size_t n) {
+    release();
+    if (n) CUDA_OK(cudaMalloc((void**)&p, n * sizeof(T)));
+    cap = n;
+  }
+  // grow to at least n elements, preserving the first ``keep`` elements
+  void grow(size_t n, size_t keep, cudaStream_t s) {
+    if (n <= cap) return;
+    size_t nc = cap ? cap : 16;
+    while (nc < n) nc *= 2;
+    T* q = nullptr;
+    CUDA_OK(cudaMalloc((void**)&q, nc * sizeof(T)));
+    if (keep && p) CUDA_OK(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (p) {
+      CUDA_OK(cudaStreamSynchronize(s));
+      CUDA_OK(cudaFree(p));
+    }
+    p = q;
+    cap = nc;
+  }
+  void ensure(size_t n) {  // no preservation
+    if (n > cap) {
+      size_t nc = cap ? cap : 16;
+      while (nc < n) nc *= 2;
+      alloc(nc);
+    }
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+// pattern app node (pre-order); child[j] >= 0 -> app index, < 0 -> var -(slot+1)
+struct PatApp {
+  u32 atom;
+  int32_t nargs;
+  int32_t child[8];
+};
+
+// target instruction (post-order); I_VAR pushes env[arg], I_APP applies atom
+enum InstrKind : int32_t { I_VAR = 0, I_APP = 1 };
+struct Instr {
+  int32_t kind;
+  int32_t arg;  // var slot (I_VAR) or nargs (I_APP)
+  u32 atom;
+  int32_t depth;  // term depth of the produced request (I_APP), 1 = leaf
+};
+
+#define MAX_SRC 4
+#define MAX_PAT_APPS 8
+#define MAX_VARS 16
+#define MAX_STACK 16
+
+struct HPattern {
+  std::vector<PatApp> apps;
+  int nvars = 0;
+  std::vector<int> order;  // binding position k -> canonical var index (name-sorted)
+};
+
+struct HRule {
+  std::string name;
+  int nsrc = 0, nslots = 0;
+  int src_pat[MAX_SRC];
+  int bind_slot[MAX_SRC][MAX_VARS];  // binding position -> rule slot
+  int src_nb[MAX_SRC];
+  std::vector<std::vector<Instr>> targets;
+  std::vector<std::vector<int>> leaves;  // per target: rule slots of its variables
+  bool same_canon = false;
+  int max_req = 0;  // requests (App nodes) over all targets
+};
+
+// matches of one canonical pattern: n rows of (eclass, bindings[nb])
+struct MatchSet {
+  u32 n = 0;
+  int nb = 0;
+  DevBuf<u32> cls;
+  DevBuf<u32> bind;  // row-major n x nb
+};
+
+struct RuleStatsH {
+  i64 found = 0, applied = 0, applied_noop = 0, skipped_self = 0, skipped_compat = 0,
+      skipped_shape = 0, skipped_cycle = 0;
+};
+
+// device-side per-run statistics accumulated by the explore kernels
+struct DevStats {
+  unsigned long long found, applied, applied_noop, skipped_self, skipped_compat, skipped_shape,
+      skipped_cycle;
+  unsigned long long prefilter_checks, prefilter_rejects;
+  u32 changed;     // any applied combo this iteration
+  u32 stop;        // 1 = node limit hit
+  u32 overshoot;
+  u32 resume_set;  // capacity stop: resume position valid
+  unsigned long long resume_pos;
+};
+
+struct Snapshot {
+  u32 n_alloc = 0;  // next_id when taken
+  u32 ncls = 0;
+  DevBuf<u32> cls_index;  // node id -> dense class index (TSAT_NONE if not a class)
+  DevBuf<u32> cls_ids;    // dense -> class id
+  DevBuf<u32> cls_off;    // dense -> member range
+  DevBuf<u32> cls_nodes;  // members (alive nodes), ascending per class
+  DevBuf<u32> op_off;     // atom -> range in op_nodes
+  DevBuf<u32> op_nodes;
+  bool valid = false;
+};
+
+struct Reach {  // descendants bitset over a snapshot
+  u32 n = 0, words = 0;
+  DevBuf<u32> bits;
+  bool valid = false;
+};
+
+struct ExploreLimitsC {
+  i64 n_max, k_max, k_multi;
+  double time_limit_s;  // < 0: none
+};
+
+struct ExploreReportC {
+  i64 iterations;
+  int stop_reason;  // 0 iter-limit, 1 saturated, 2 node-limit, 3 timeout
+  i64 prefilter_checks, prefilter_rejects, postprocess_filtered, node_limit_overshoot, filter_size;
+  double time_s;
+};
+
+struct Engine {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  bool analysis = false;
+  std::string last_error;
+
+  // atoms
+  std::vector<AtomInfo> h_atoms;
+  std::vector<std::string> atom_names;
+  DevBuf<AtomInfo> atoms;
+  DevBuf<char> d_names;
+  DevBuf<u32> d_name_off;
+  DevBuf<double> d_costs;  // c_i by node id from the last costs() call
+  u32 costs_valid_for = TSAT_NONE;  // next_id when computed
+
+  // node table
+  DevBuf<u32> op, koff, kids, parent;
+  DevBuf<u8> flags;
+  DevBuf<Val> val;
+  u32 cap_nodes = 0, cap_kids = 0;
+  DevBuf<u32> hc;
+  u32 hc_cap = 0;
+
+  // cut trees
+  DevBuf<Tree> trees;
+  DevBuf<u32> tree_hc;
+  DevBuf<u32> tree_count;
+  u32 tree_cap = 0, tree_hc_cap = 0;
+
+  DevBuf<Counters> cnt;
+  Counters h{};
+  DevBuf<DevError> err;
+  u32 root = TSAT_NONE;
+
+  // rules
+  std::vector<HPattern> patterns;
+  std::vector<HRule> rules;
+  std::vector<MatchSet> matches;  // per pattern, current iteration
+  DevBuf<Instr> d_instr;
+  DevBuf<int> d_leaf;
+
+  Snapshot snap;
+  Reach reach;
+  DevBuf<u8> temp;  // cub scratch
+  DevBuf<u32> scratch_u32[8];
+  DevBuf<DevStats> dstats;
+
+  // per-rule stats of the last saturate call
+  std::vector<RuleStatsH> rstats;
+  std::vector<i64> enodes_per_iter, alloc_per_iter, eclasses_per_iter;
+  ExploreReportC report{};
+  std::vector<double> phase_ms;
+
+  Engine(int dev);
+  ~Engine();
+
+  G view();
+  void pull_counters();
+  void push_counters();
+  void check_error();
+  void sync();
+  void ensure_nodes(u64 extra_nodes, u64 extra_kids);
+  void rehash(u32 new_cap);
+
+  // construction / generic API
+  void set_atoms(int n, const int32_t* kind, const i64* ival, const int32_t* opcode,
+                 const int32_t* ndims, const i64* dims, const int32_t* nident, const i64* idims,
+                 const char* names_blob, const i64* name_off);
+  void load_initial(u32 n, const u32* op, const u32* koff, const u32* kids, u32 root);
+  void add_terms(int ninstr, const Instr* prog, int nterm, const int32_t* term_len, int nenv,
+                 const u32* env, u32* out_cls);
+  u32 union_pair(u32 a, u32 b);
+  void rebuild();
+  void set_filter(int n, const u32* ids, int on);
+  std::vector<u32> get_filter();
+  u32 find(u32 x);
+
+  // snapshot + matching
+  void build_snapshot();
+  void ematch_pattern(int pid, MatchSet& out);
+  void load_rules(int n, const i64* blob);
+
+  // cycles
+  void build_reach();
+  i64 break_all_cycles(bool precheck_only, std::vector<std::vector<u32>>* cycles_out);
+
+  // exploration
+  bool seq_changed = false, seq_stop = false;
+  std::vector<std::string> rule_names;
+  void apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P);
+  void saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self, const int* active_rule_mask,
+                int n_active);
+  void run_rule_seq(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long p0,
+                    unsigned long long p1);
+
+  // extraction
+  void costs(int mode, int strict, int ntab, const char* keys, const i64* key_off, const double* vals,
+             double* out);
+  double greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u32* nsel, i64* rounds);
+
+  // download
+  void download(u32* op, u32* koff, u32* kids, u32* cls, u8* flags);
+  std::string dump_text();
+  std::string value_str(u32 cls);
+};
+
+// cub helpers (core.cu)
+void dev_exclusive_scan_u32(Engine& e, const u32* in, u32* out, u32 n);
+void dev_sort_pairs_u32(Engine& e, u32* keys_in, u32* keys_out, u32* vals_in, u32* vals_out, u32 n,
+                        int end_bit);
+u32 bits_for(u32 maxval);

@@ -1,0 +1,400 @@
+// Exploration driver (reference: pkg/src/tensorsat/explorer.py:136-365).
+//
+// Per iteration: snapshot CSR -> (efficient) descendants bitset -> e-match
+// every unique canonical pattern on the snapshot -> rules in order over
+// their match products -> rebuild -> cycle post-processing.  The apply
+// step has two device paths: the sequential exact path in this file
+// (k_seq_rule, the reference loop run by one GPU thread) and the parallel
+// wave path (wave.cu) that handles hazard-free prefixes in bulk and falls
+// back to k_seq_rule for exactly one combo at each hazard.
+#include <chrono>
+#include <cstring>
+
+#include "rulesdev.cuh"
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ---------------------------------------------------------------- rule loading
+
+void Engine::load_rules(int n, const i64* b) {
+  (void)n;
+  size_t k = 0;
+  patterns.clear();
+  rules.clear();
+  i64 npat = b[k++];
+  for (i64 p = 0; p < npat; p++) {
+    HPattern hp;
+    int napps = (int)b[k++];
+    hp.nvars = (int)b[k++];
+    if (napps < 1 || napps > MAX_PAT_APPS || hp.nvars > MAX_VARS)
+      throw TsatException(TSAT_ERR_UNSUPPORTED, "pattern too large for the device matcher");
+    for (int i = 0; i < hp.nvars; i++) hp.order.push_back((int)b[k++]);
+    for (int a = 0; a < napps; a++) {
+      PatApp pa;
+      pa.atom = (u32)b[k++];
+      pa.nargs = (int)b[k++];
+      if (pa.nargs > 8) throw TsatException(TSAT_ERR_UNSUPPORTED, "pattern arity > 8");
+      for (int j = 0; j < 8; j++) pa.child[j] = (int32_t)b[k++];
+      hp.apps.push_back(pa);
+    }
+    patterns.push_back(hp);
+  }
+  i64 nr = b[k++];
+  std::vector<Instr> all_instr;
+  std::vector<int> all_leaf;
+  for (i64 r = 0; r < nr; r++) {
+    HRule hr;
+    hr.nsrc = (int)b[k++];
+    hr.nslots = (int)b[k++];
+    hr.same_canon = b[k++] != 0;
+    if (hr.nsrc < 1 || hr.nsrc > MAX_SRC || hr.nslots > MAX_VARS)
+      throw TsatException(TSAT_ERR_UNSUPPORTED, "rule has too many sources or variables");
+    for (int s_ = 0; s_ < hr.nsrc; s_++) {
+      hr.src_pat[s_] = (int)b[k++];
+      hr.src_nb[s_] = (int)b[k++];
+      for (int j = 0; j < hr.src_nb[s_]; j++) hr.bind_slot[s_][j] = (int)b[k++];
+    }
+    int req = 0;
+    for (int t = 0; t < hr.nsrc; t++) {
+      int ni = (int)b[k++];
+      std::vector<Instr> prog;
+      int depth = 0, maxd = 0;
+      for (int i = 0; i < ni; i++) {
+        Instr in;
+        in.kind = (int32_t)b[k++];
+        in.arg = (int32_t)b[k++];
+        in.atom = (u32)b[k++];
+        in.depth = (int32_t)b[k++];
+        if (in.kind == I_APP) {
+          req++;
+          depth -= in.arg;
+          if (in.arg > 8) throw TsatException(TSAT_ERR_UNSUPPORTED, "target arity > 8");
+        }
+        depth++;
+        maxd = std::max(maxd, depth);
+        prog.push_back(in);
+      }
+      if (maxd > MAX_STACK) throw TsatException(TSAT_ERR_UNSUPPORTED, "target too deep");
+      hr.targets.push_back(prog);
+      int nl = (int)b[k++];
+      std::vector<int> lv;
+      for (int i = 0; i < nl; i++) lv.push_back((int)b[k++]);
+      hr.leaves.push_back(lv);
+    }
+    hr.max_req = req;
+    rules.push_back(hr);
+  }
+  // flatten programs to device
+  for (auto& r : rules)
+    for (size_t t = 0; t < r.targets.size(); t++) {
+      all_instr.insert(all_instr.end(), r.targets[t].begin(), r.targets[t].end());
+      all_leaf.insert(all_leaf.end(), r.leaves[t].begin(), r.leaves[t].end());
+    }
+  d_instr.alloc(all_instr.size() + 1);
+  d_leaf.alloc(all_leaf.size() + 1);
+  if (!all_instr.empty())
+    CUDA_OK(cudaMemcpyAsync(d_instr.p, all_instr.data(), all_instr.size() * sizeof(Instr),
+                            cudaMemcpyHostToDevice, s));
+  if (!all_leaf.empty())
+    CUDA_OK(cudaMemcpyAsync(d_leaf.p, all_leaf.data(), all_leaf.size() * sizeof(int),
+                            cudaMemcpyHostToDevice, s));
+  matches.clear();
+  matches.resize(patterns.size());
+  sync();
+}
+
+RuleDev make_rule_dev(Engine& e, int ri, int filter_mode, int allow_self) {
+  RuleDev R;
+  memset(&R, 0, sizeof(R));
+  const HRule& hr = e.rules[ri];
+  R.nsrc = hr.nsrc;
+  R.nslots = hr.nslots;
+  R.same_canon = hr.same_canon;
+  R.allow_self = allow_self;
+  R.efficient = filter_mode == 2;
+  R.max_req = hr.max_req;
+  int mk = 0;
+  size_t ioff = 0, loff = 0;
+  for (int r = 0; r < ri; r++)
+    for (size_t t = 0; t < e.rules[r].targets.size(); t++) {
+      ioff += e.rules[r].targets[t].size();
+      loff += e.rules[r].leaves[t].size();
+    }
+  for (int t = 0; t < hr.nsrc; t++) {
+    const MatchSet& m = e.matches[hr.src_pat[t]];
+    R.nmatch[t] = m.n;
+    R.mcls[t] = m.cls.p;
+    R.mbind[t] = m.bind.p;
+    R.nb[t] = m.nb;
+    for (int j = 0; j < hr.src_nb[t]; j++) R.bind_slot[t][j] = hr.bind_slot[t][j];
+    R.tgt_off[t] = (int)ioff;
+    R.tgt_len[t] = (int)hr.targets[t].size();
+    R.leaf_off[t] = (int)loff;
+    R.leaf_len[t] = (int)hr.leaves[t].size();
+    for (auto& in : hr.targets[t])
+      if (in.kind == I_APP) mk += in.arg;
+    ioff += hr.targets[t].size();
+    loff += hr.leaves[t].size();
+  }
+  R.max_kids = mk;
+  R.instr = e.d_instr.p;
+  R.leaf = e.d_leaf.p;
+  return R;
+}
+
+ReachDev make_reach_dev(Engine& e) {
+  ReachDev r;
+  r.bits = e.reach.bits.p;
+  r.words = e.reach.words;
+  r.cls_index = e.snap.cls_index.p;
+  r.n_alloc = e.snap.n_alloc;
+  r.valid = e.reach.valid ? 1 : 0;
+  return r;
+}
+
+// ---------------------------------------------------------------- exact path
+
+// The reference run_rule loop (explorer.py:227-262) for product positions
+// [p0, p1), executed by a single GPU thread against the live e-graph.
+__global__ void k_seq_rule(G g, RuleDev R, ReachDev RD, DevStats* st, unsigned long long p0,
+                           unsigned long long p1, i64 n_max) {
+  if (threadIdx.x || blockIdx.x) return;
+  Counters* c = g.cnt;
+  u32 idx[MAX_SRC];
+  u32 env[MAX_VARS];
+  for (unsigned long long p = p0; p < p1; p++) {
+    if ((u64)c->next_id + R.max_req + 2 > g.cap_nodes || (u64)c->nkids + R.max_kids + 2 > g.cap_kids ||
+        2ull * ((u64)c->next_id + R.max_req + 2) > (u64)g.hc_mask + 1) {
+      st->resume_set = 1;
+      st->resume_pos = p;
+      return;
+    }
+    if ((i64)c->live >= n_max) {
+      st->stop = 1;
+      st->overshoot = (u32)((i64)c->live - n_max);
+      return;
+    }
+    st->found++;
+    decode_pos(R, p, idx);
+    if (R.nsrc > 1 && !R.allow_self && R.same_canon) {
+      bool all = true;
+      for (int i = 1; i < R.nsrc; i++) all &= idx[i] == idx[0];
+      if (all) {
+        st->skipped_self++;
+        continue;
+      }
+    }
+    // compatible() + combined_subst() with live find (rules.py:63-81)
+    for (int v = 0; v < R.nslots; v++) env[v] = TSAT_NONE;
+    bool compat = true;
+    for (int i = 0; i < R.nsrc && compat; i++)
+      for (int j = 0; j < R.nb[i]; j++) {
+        u32 cls = uf_find(g.parent, R.mbind[i][(u64)idx[i] * R.nb[i] + j]);
+        int sl = R.bind_slot[i][j];
+        if (env[sl] == TSAT_NONE) env[sl] = cls;
+        else if (env[sl] != cls) {
+          compat = false;
+          break;
+        }
+      }
+    if (!compat) {
+      st->skipped_compat++;
+      continue;
+    }
+    // shape check (rules.py:141-156)
+    if (g.analysis) {
+      bool ok = true;
+      for (int t = 0; t < R.nsrc && ok; t++) {
+        Val out;
+        int s = eval_target(g, R.instr + R.tgt_off[t], R.tgt_len[t], env, out);
+        if (s == AS_ORIGIN_OVERFLOW || s == AS_TREE_FULL) {
+          dev_set_error(g.err, TSAT_ERR_CAPACITY, 10 + s, (i64)p, t);
+          return;
+        }
+        if (s != AS_OK) ok = false;
+        else ok = val_same_data(out, g.val[uf_find(g.parent, R.mcls[t][idx[t]])]);
+      }
+      if (!ok) {
+        st->skipped_shape++;
+        continue;
+      }
+    }
+    // efficient pre-filter (explorer.py:208-225, cycles.py:151-169)
+    if (R.efficient) {
+      st->prefilter_checks++;
+      bool hit = false;
+      for (int t = 0; t < R.nsrc && !hit; t++) {
+        u32 out = uf_find(g.parent, R.mcls[t][idx[t]]);
+        for (int l = 0; l < R.leaf_len[t]; l++) {
+          u32 leaf = uf_find(g.parent, env[R.leaf[R.leaf_off[t] + l]]);
+          if (leaf == out || reach_query(RD, leaf, out)) {
+            hit = true;
+            break;
+          }
+        }
+      }
+      if (hit) {
+        st->prefilter_rejects++;
+        st->skipped_cycle++;
+        continue;
+      }
+    }
+    // _apply_combo (explorer.py:146-163)
+    u32 before = c->next_id;
+    bool did = false;
+    for (int t = 0; t < R.nsrc; t++) {
+      const Instr* ins = R.instr + R.tgt_off[t];
+      u32 stk[MAX_STACK];
+      int sp = 0;
+      for (int k = 0; k < R.tgt_len[t]; k++) {
+        const Instr& in = ins[k];
+        if (in.kind == I_VAR) {
+          stk[sp++] = uf_find(g.parent, env[in.arg]);
+        } else {
+          int na = in.arg;
+          sp -= na;
+          u32 kb[8];
+          for (int j = 0; j < na; j++) kb[j] = stk[sp + j];
+          u32 cl = seq_add_enode(g, in.atom, kb, na);
+          if (cl == TSAT_NONE) return;  // error recorded
+          stk[sp++] = cl;
+        }
+      }
+      u32 nw = stk[0];
+      u32 old = uf_find(g.parent, R.mcls[t][idx[t]]);
+      if (uf_find(g.parent, nw) != old) {
+        if (seq_union(g, old, nw) == TSAT_NONE) {
+          g.err->a = (i64)p;  // merge error: keep rule context
+          return;
+        }
+        did = true;
+      }
+    }
+    if (did || c->next_id > before) {
+      st->applied++;
+      st->changed = 1;
+    } else {
+      st->applied_noop++;
+    }
+  }
+}
+
+static void accumulate(Engine& e, int ri, const DevStats& d) {
+  RuleStatsH& r = e.rstats[ri];
+  r.found += d.found;
+  r.applied += d.applied;
+  r.applied_noop += d.applied_noop;
+  r.skipped_self += d.skipped_self;
+  r.skipped_compat += d.skipped_compat;
+  r.skipped_shape += d.skipped_shape;
+  r.skipped_cycle += d.skipped_cycle;
+  e.report.prefilter_checks += d.prefilter_checks;
+  e.report.prefilter_rejects += d.prefilter_rejects;
+}
+
+// returns through dstats; grows capacity and resumes as needed
+void Engine::run_rule_seq(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long p0,
+                          unsigned long long p1) {
+  RuleDev R = make_rule_dev(*this, ri, filter_mode, allow_self);
+  ReachDev RD = make_reach_dev(*this);
+  unsigned long long p = p0;
+  while (p < p1) {
+    CUDA_OK(cudaMemsetAsync(dstats.p, 0, sizeof(DevStats), s));
+    k_seq_rule<<<1, 1, 0, s>>>(view(), R, RD, dstats.p, p, p1, n_max);
+    DevStats d;
+    CUDA_OK(cudaMemcpyAsync(&d, dstats.p, sizeof(d), cudaMemcpyDeviceToHost, s));
+    pull_counters();
+    accumulate(*this, ri, d);
+    if (d.changed) seq_changed = true;
+    if (d.stop) {
+      seq_stop = true;
+      report.node_limit_overshoot = d.overshoot;
+    }
+    try {
+      check_error();
+    } catch (TsatException& ex) {
+      if (ex.code == TSAT_ERR_MERGE)
+        throw TsatException(ex.code, "unsound rule '" + rule_names[ri] + "': " + ex.what());
+      throw;
+    }
+    if (d.stop) return;
+    if (!d.resume_set) return;
+    p = d.resume_pos;
+    ensure_nodes(4096 + (u64)R.max_req * 64, 4096 + (u64)R.max_kids * 64);
+  }
+}
+
+// ---------------------------------------------------------------- saturate
+
+void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self, const int*, int) {
+  double t0 = now_s();
+  double deadline = lim.time_limit_s < 0 ? -1.0 : t0 + lim.time_limit_s;
+  memset(&report, 0, sizeof(report));
+  rstats.assign(rules.size(), RuleStatsH());
+  enodes_per_iter.clear();
+  alloc_per_iter.clear();
+  eclasses_per_iter.clear();
+  std::vector<int> multi, single;
+  for (size_t i = 0; i < rules.size(); i++) (rules[i].nsrc > 1 ? multi : single).push_back((int)i);
+  int stop = 0;  // iter-limit
+  for (i64 it = 0; it < lim.k_max; it++) {
+    if (!snap.valid) build_snapshot();
+    if (filter_mode == 2) build_reach();
+    else reach.valid = false;
+    std::vector<int> active;
+    if (it < lim.k_multi) active = multi;
+    active.insert(active.end(), single.begin(), single.end());
+    std::vector<char> need(patterns.size(), 0);
+    for (int ri : active)
+      for (int t = 0; t < rules[ri].nsrc; t++) need[rules[ri].src_pat[t]] = 1;
+    for (size_t p = 0; p < patterns.size(); p++)
+      if (need[p]) ematch_pattern((int)p, matches[p]);
+    seq_changed = false;
+    seq_stop = false;
+    int stop_flag = 0;
+    for (int ri : active) {
+      const HRule& hr = rules[ri];
+      unsigned long long P = 1;
+      for (int t = 0; t < hr.nsrc; t++) P *= matches[hr.src_pat[t]].n;
+      if (P == 0) continue;
+      if (deadline >= 0 && now_s() > deadline) {
+        stop_flag = 3;
+        break;
+      }
+      apply_rule(ri, filter_mode, allow_self, lim.n_max, P);
+      if (seq_stop) {
+        stop_flag = 2;
+        break;
+      }
+    }
+    snap.valid = false;
+    rebuild();
+    build_snapshot();
+    if (filter_mode != 0) report.postprocess_filtered += break_all_cycles(false, nullptr);
+    report.iterations = it + 1;
+    enodes_per_iter.push_back(h.live);
+    alloc_per_iter.push_back(h.next_id);
+    eclasses_per_iter.push_back(snap.ncls);
+    if (stop_flag) {
+      stop = stop_flag;
+      break;
+    }
+    if (!seq_changed) {
+      stop = 1;
+      break;
+    }
+    if (deadline >= 0 && now_s() > deadline) {
+      stop = 3;
+      break;
+    }
+  }
+  report.stop_reason = stop;
+  report.filter_size = (i64)get_filter().size();
+  report.time_s = now_s() - t0;
+}
+
+void Engine::apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P) {
+  run_rule_seq(ri, filter_mode, allow_self, n_max, 0, P);
+}

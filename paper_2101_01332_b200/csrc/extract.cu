@@ -1,0 +1,512 @@
+// Cost vector and greedy extraction on the GPU.
+//
+// * k_node_costs: c_i for every live e-node (reference cost.py:225-247 with
+//   CostModel.node_cost :164-174 and synthetic_node_cost :78-126).  fp64
+//   with the reference's operation order; the library is built with
+//   -fmad=false so no multiply-add is contracted.  Table mode renders the
+//   canonical signature key (cost.py:135-140) on device and probes a hash
+//   table of the normalised keys.
+// * greedy: Jacobi min-cost relaxation to fixpoint with the reference tie
+//   rule (extract.py:120-159): per class, fold members in id order starting
+//   from the previous round's (cost, node), update on total < cur - 1e-15 or
+//   |total - cur| <= 1e-15 with a smaller id.  Child totals are summed in
+//   child order.  Then a BFS over chosen nodes gives the reached selection
+//   (extract.py:74-91).
+#include <cmath>
+#include <cstring>
+
+#include "engine.cuh"
+
+static inline unsigned nblk(u64 n, unsigned t = 256) {
+  u64 b = (n + t - 1) / t;
+  if (b < 1) b = 1;
+  if (b > 148ull * 64) b = 148ull * 64;
+  return (unsigned)b;
+}
+#define GRID_STRIDE(i, n) for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < (n); i += (u64)gridDim.x * blockDim.x)
+
+struct CostTab {
+  const char* keys;
+  const i64* off;
+  const double* vals;
+  const u32* slots;
+  u32 mask;
+  int n;
+  int mode;    // 0 synthetic, 1 table
+  int strict;
+  const char* names;
+  const u32* name_off;
+};
+
+__device__ __forceinline__ u64 fnv1a(const char* p, int n) {
+  u64 h = 1469598103934665603ULL;
+  for (int i = 0; i < n; i++) {
+    h ^= (u8)p[i];
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+struct SigBuf {
+  char b[320];
+  int n = 0;
+  bool ovf = false;
+  __device__ void ch(char c) {
+    if (n < 319) b[n++] = c;
+    else ovf = true;
+  }
+  __device__ void str(const char* p, int len) {
+    for (int i = 0; i < len; i++) ch(p[i]);
+  }
+  __device__ void cstr(const char* p) {
+    while (*p) ch(*p++);
+  }
+  __device__ void num(i64 v) {
+    char t[24];
+    int k = 0;
+    bool neg = v < 0;
+    unsigned long long u = neg ? (unsigned long long)(-(v + 1)) + 1 : (unsigned long long)v;
+    do {
+      t[k++] = (char)('0' + u % 10);
+      u /= 10;
+    } while (u);
+    if (neg) ch('-');
+    while (k) ch(t[--k]);
+  }
+};
+
+// sorted-by-name parameter order per op: scalar index list + names
+__device__ const char* param_name(int op, int k, int& idx) {
+  switch (op) {
+    case OP_MATMUL: idx = 0; return "activation";
+    case OP_CONV: {
+      const int ix[4] = {3, 2, 0, 1};
+      const char* nm[4] = {"activation", "padding", "stride_h", "stride_w"};
+      idx = ix[k];
+      return nm[k];
+    }
+    case OP_POOLMAX:
+    case OP_POOLAVG: {
+      const int ix[6] = {5, 0, 1, 4, 2, 3};
+      const char* nm[6] = {"activation", "kernel_h", "kernel_w", "padding", "stride_h", "stride_w"};
+      idx = ix[k];
+      return nm[k];
+    }
+    case OP_TRANSPOSE: idx = 0; return "perm";
+    case OP_SPLIT: idx = 0; return "axis";
+    case OP_MERGE: idx = 0; return "count";
+    case OP_RESHAPE: idx = 0; return "shape";
+    case OP_INPUT:
+    case OP_WEIGHT: idx = 0; return "identifier";
+    default:
+      if (op >= OP_CONCAT2 && op <= OP_CONCAT6) {
+        idx = 0;
+        return "axis";
+      }
+  }
+  idx = -1;
+  return nullptr;
+}
+
+__device__ __forceinline__ int n_params(int op) {
+  switch (op) {
+    case OP_MATMUL: case OP_TRANSPOSE: case OP_SPLIT: case OP_MERGE: case OP_RESHAPE:
+    case OP_INPUT: case OP_WEIGHT: return 1;
+    case OP_CONV: return 4;
+    case OP_POOLMAX: case OP_POOLAVG: return 6;
+    default: return (op >= OP_CONCAT2 && op <= OP_CONCAT6) ? 1 : 0;
+  }
+}
+
+__device__ __forceinline__ i64 numel(const i64* d, int r) {
+  i64 p = 1;
+  for (int i = 0; i < r; i++) p *= d[i];
+  return p;
+}
+
+__device__ __forceinline__ double base_cost(int op) {
+  switch (op) {
+    case OP_MATMUL: case OP_CONV: return 0.05;
+    case OP_POOLMAX: case OP_POOLAVG: return 0.02;
+    case OP_EWADD: case OP_EWMUL: case OP_RELU: case OP_TANH: case OP_SIGMOID: return 0.01;
+    case OP_INPUT: case OP_WEIGHT: case OP_NOOP: return 0.0;
+    default: return 0.005;
+  }
+}
+
+#define RATE_EW 1e-7
+#define RATE_MM 1e-6
+#define FUSED_ACT 0.2
+
+__global__ void k_node_costs(G g, CostTab ct, u32 n, double* out) {
+  const double RATE_MOVE = 0.05 * 1e-7;
+  GRID_STRIDE(i0, n) {
+    u32 i = (u32)i0;
+    if (!(g.flags[i] & NF_ALIVE)) {
+      out[i] = 0.0;
+      continue;
+    }
+    u32 a = g.koff[i], b = g.koff[i + 1];
+    if (a == b) {
+      out[i] = 0.0;
+      continue;
+    }
+    const AtomInfo& ai = g.atoms[g.op[i]];
+    int op = ai.kind == 1 ? ai.opcode : -1;
+    if (op < 0) {
+      dev_set_error(g.err, TSAT_ERR_SHAPE, 20, i, g.op[i]);
+      out[i] = 0.0;
+      continue;
+    }
+    if (op == OP_INPUT || op == OP_WEIGHT || op == OP_NOOP) {
+      out[i] = 0.0;
+      continue;
+    }
+    // gather scalars / shapes from child analyses in child order
+    i64 sc[7];
+    int sk[7];  // 0 int, 1 str atom
+    int nsc = 0, nsh = 0;
+    const Val* sh[7];
+    for (u32 j = a; j < b; j++) {
+      const Val& v = g.val[uf_find_ro(g.parent, g.kids[j])];
+      if (v.kind == VK_N || v.kind == VK_S) {
+        sk[nsc] = v.kind == VK_S;
+        sc[nsc++] = v.iv;
+      } else {
+        sh[nsh++] = &v;
+      }
+    }
+    if (ct.mode == 1) {
+      SigBuf s;
+      u32 na = ct.name_off[g.op[i]], nb = ct.name_off[g.op[i] + 1];
+      s.str(ct.names + na, (int)(nb - na));
+      int np = n_params(op);
+      if (np) {
+        s.ch('[');
+        for (int k = 0; k < np; k++) {
+          int idx;
+          const char* pn = param_name(op, k, idx);
+          if (k) s.ch(',');
+          s.cstr(pn);
+          s.ch('=');
+          if (idx < nsc) {
+            if (sk[idx]) {
+              u32 x = ct.name_off[sc[idx]], y = ct.name_off[sc[idx] + 1];
+              s.str(ct.names + x, (int)(y - x));
+            } else {
+              s.num(sc[idx]);
+            }
+          }
+        }
+        s.ch(']');
+      }
+      s.ch('(');
+      for (int k = 0; k < nsh; k++) {
+        if (k) s.ch(',');
+        const Val& v = *sh[k];
+        for (int d = 0; d < v.r0; d++) {
+          if (d) s.ch('x');
+          s.num(v.d0[d]);
+        }
+        if (v.kind == VK_TT) {
+          s.ch('|');
+          for (int d = 0; d < v.r1; d++) {
+            if (d) s.ch('x');
+            s.num(v.d1[d]);
+          }
+        }
+      }
+      s.ch(')');
+      bool hit = false;
+      if (!s.ovf && ct.n > 0) {
+        u64 h = fnv1a(s.b, s.n);
+        u32 slot = (u32)h & ct.mask;
+        while (true) {
+          u32 e = ct.slots[slot];
+          if (e == TSAT_NONE) break;
+          i64 ka = ct.off[e], kb = ct.off[e + 1];
+          if (kb - ka == s.n) {
+            bool eq = true;
+            for (int q = 0; q < s.n && eq; q++) eq = ct.keys[ka + q] == s.b[q];
+            if (eq) {
+              out[i] = ct.vals[e];
+              hit = true;
+              break;
+            }
+          }
+          slot = (slot + 1) & ct.mask;
+        }
+      }
+      if (hit) continue;
+      if (ct.strict) {
+        dev_set_error(g.err, TSAT_ERR_UNKNOWN_SIG, 21, i, g.op[i]);
+        out[i] = 0.0;
+        continue;
+      }
+    }
+    double base = base_cost(op), work = 0.0;
+    switch (op) {
+      case OP_MATMUL: {
+        const Val &x = *sh[0], &y = *sh[1];
+        i64 macs = numel(x.d0, x.r0) * y.d0[y.r0 - 1];
+        work = RATE_MM * (double)macs;
+        if (sc[0] != 0)
+          work += FUSED_ACT * RATE_EW * (double)(numel(x.d0, x.r0) / x.d0[x.r0 - 1]) * (double)y.d0[y.r0 - 1];
+        break;
+      }
+      case OP_CONV: {
+        const Val &x = *sh[0], &w = *sh[1];
+        i64 oh = 0, ow = 0;
+        if (conv_out(x.d0[2], x.d0[3], w.d0[2], w.d0[3], sc[0], sc[1], sc[2], oh, ow)) {
+          dev_set_error(g.err, TSAT_ERR_SHAPE, 22, i, g.op[i]);
+          break;
+        }
+        i64 oe = x.d0[0] * w.d0[0] * oh * ow;
+        work = RATE_MM * (double)oe * (double)w.d0[1] * (double)w.d0[2] * (double)w.d0[3];
+        if (sc[3] != 0) work += FUSED_ACT * RATE_EW * (double)oe;
+        break;
+      }
+      case OP_EWADD: case OP_EWMUL: case OP_RELU: case OP_TANH: case OP_SIGMOID:
+        work = RATE_EW * (double)numel(sh[0]->d0, sh[0]->r0);
+        break;
+      case OP_POOLMAX:
+      case OP_POOLAVG: {
+        const Val& x = *sh[0];
+        i64 kh = sc[0], kw = sc[1], oh = 0, ow = 0;
+        if (conv_out(x.d0[2], x.d0[3], kh, kw, sc[2], sc[3], sc[4], oh, ow)) {
+          dev_set_error(g.err, TSAT_ERR_SHAPE, 23, i, g.op[i]);
+          break;
+        }
+        work = RATE_EW * (double)x.d0[0] * (double)x.d0[1] * (double)oh * (double)ow * (double)kh * (double)kw;
+        if (sc[5] != 0)
+          work += FUSED_ACT * RATE_EW * (double)x.d0[0] * (double)x.d0[1] * (double)oh * (double)ow;
+        break;
+      }
+      case OP_SPLIT:
+        work = RATE_MOVE * (double)numel(sh[0]->d0, sh[0]->r0);
+        break;
+      case OP_SPLIT0:
+        work = RATE_MOVE * (double)numel(sh[0]->d0, sh[0]->r0);
+        break;
+      case OP_SPLIT1:
+        work = RATE_MOVE * (double)numel(sh[0]->d1, sh[0]->r1);
+        break;
+      case OP_ENLARGE: {
+        const Val &x = *sh[0], &r = *sh[1];
+        i64 d[4] = {x.d0[0], x.d0[1], r.d0[2], r.d0[3]};
+        work = RATE_MOVE * (double)numel(d, 4);
+        break;
+      }
+      case OP_MERGE:
+        work = RATE_MOVE * (double)numel(sh[0]->d0, sh[0]->r0) * (double)sc[0];
+        break;
+      case OP_TRANSPOSE:
+      case OP_RESHAPE:
+        work = RATE_MOVE * (double)numel(sh[0]->d0, sh[0]->r0);
+        break;
+      default:
+        if (op >= OP_CONCAT2 && op <= OP_CONCAT6) {
+          i64 tot = 0;
+          for (int k = 0; k < nsh; k++) tot += numel(sh[k]->d0, sh[k]->r0);
+          work = RATE_MOVE * (double)tot;
+        }
+    }
+    out[i] = base + work;
+  }
+}
+
+static u64 fnv1a_host(const char* p, i64 n) {
+  u64 h = 1469598103934665603ULL;
+  for (i64 i = 0; i < n; i++) {
+    h ^= (u8)p[i];
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+void Engine::costs(int mode, int strict, int ntab, const char* keys, const i64* key_off, const double* vals,
+                   double* out) {
+  if (!analysis) throw TsatException(TSAT_ERR_STATE, "egraph_costs needs the tensor analysis");
+  u32 n = h.next_id;
+  DevBuf<char> dk;
+  DevBuf<i64> doff;
+  DevBuf<double> dv;
+  DevBuf<u32> dslots;
+  CostTab ct;
+  memset(&ct, 0, sizeof(ct));
+  ct.mode = mode;
+  ct.strict = strict;
+  ct.n = ntab;
+  ct.names = d_names.p;
+  ct.name_off = d_name_off.p;
+  if (mode == 1 && ntab > 0) {
+    i64 nbytes = key_off[ntab];
+    u32 cap = 16;
+    while (cap < 2u * (u32)ntab) cap *= 2;
+    std::vector<u32> slots(cap, TSAT_NONE);
+    for (int e = 0; e < ntab; e++) {
+      u32 s_ = (u32)fnv1a_host(keys + key_off[e], key_off[e + 1] - key_off[e]) & (cap - 1);
+      while (slots[s_] != TSAT_NONE) s_ = (s_ + 1) & (cap - 1);
+      slots[s_] = e;
+    }
+    dk.alloc(nbytes + 1);
+    doff.alloc(ntab + 1);
+    dv.alloc(ntab);
+    dslots.alloc(cap);
+    CUDA_OK(cudaMemcpyAsync(dk.p, keys, nbytes, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(doff.p, key_off, (ntab + 1) * sizeof(i64), cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(dv.p, vals, ntab * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(dslots.p, slots.data(), cap * sizeof(u32), cudaMemcpyHostToDevice, s));
+    ct.keys = dk.p;
+    ct.off = doff.p;
+    ct.vals = dv.p;
+    ct.slots = dslots.p;
+    ct.mask = cap - 1;
+  }
+  d_costs.ensure(n + 1);
+  k_node_costs<<<nblk(n, 128), 128, 0, s>>>(view(), ct, n, d_costs.p);
+  if (out) CUDA_OK(cudaMemcpyAsync(out, d_costs.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  sync();
+  check_error();
+  costs_valid_for = n;
+}
+
+// ---------------------------------------------------------------- greedy
+
+__global__ void k_greedy_init(double* bc, u32* bn, u32 n) {
+  GRID_STRIDE(i, n) {
+    bc[i] = INFINITY;
+    bn[i] = TSAT_NONE;
+  }
+}
+
+__global__ void k_greedy_round(G g, const u32* cls_off, const u32* cls_nodes, const u32* cls_index, u32 ncls,
+                               const double* cost, const double* pc, const u32* pn, double* nc, u32* nn,
+                               u32* changed) {
+  GRID_STRIDE(i, ncls) {
+    double bc = pc[i];
+    u32 bn = pn[i];
+    for (u32 k = cls_off[i]; k < cls_off[i + 1]; k++) {
+      u32 m = cls_nodes[k];
+      if (g.flags[m] & NF_FILT) continue;
+      double tot = cost[m];
+      for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++)
+        tot += pc[cls_index[uf_find_ro(g.parent, g.kids[j])]];
+      if (isinf(tot)) continue;
+      if (tot < bc - 1e-15 || (fabs(tot - bc) <= 1e-15 && (bn == TSAT_NONE || m < bn))) {
+        bc = tot;
+        bn = m;
+      }
+    }
+    nc[i] = bc;
+    nn[i] = bn;
+    if (bn != pn[i] || !(bc == pc[i])) *changed = 1;
+  }
+}
+
+__global__ void k_sel_step(G g, const u32* front, u32 nf, const u32* bn, const u32* cls_index, u8* mark,
+                           u32* next, u32* nn, u32* missing) {
+  GRID_STRIDE(t, nf) {
+    u32 i = front[t];
+    u32 m = bn[i];
+    if (m == TSAT_NONE) {
+      *missing = 1;
+      continue;
+    }
+    for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) {
+      u32 c = cls_index[uf_find_ro(g.parent, g.kids[j])];
+      if (!mark[c]) {
+        mark[c] = 1;
+        next[atomicAdd(nn, 1u)] = c;
+      }
+    }
+  }
+}
+
+__global__ void k_sel_collect(const u8* mark, const u32* cls_ids, const u32* bn, u32 n, u32* oc, u32* on, u32* cnt) {
+  GRID_STRIDE(i, n) {
+    if (!mark[i]) continue;
+    u32 k = atomicAdd(cnt, 1u);
+    oc[k] = cls_ids[i];
+    on[k] = bn[i];
+  }
+}
+
+double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u32* nsel, i64* rounds) {
+  if (root == TSAT_NONE) throw TsatException(TSAT_ERR_STATE, "e-graph has no root");
+  if (!snap.valid) build_snapshot();
+  u32 n = h.next_id, C = snap.ncls;
+  DevBuf<double> upl;
+  const double* cost = d_costs.p;
+  if (cost_by_node) {
+    upl.alloc(n + 1);
+    CUDA_OK(cudaMemcpyAsync(upl.p, cost_by_node, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    cost = upl.p;
+  } else if (costs_valid_for != n) {
+    throw TsatException(TSAT_ERR_STATE, "device cost vector is stale; recompute egraph_costs");
+  }
+  DevBuf<double> c0, c1;
+  DevBuf<u32> n0, n1, flag;
+  c0.alloc(C + 1);
+  c1.alloc(C + 1);
+  n0.alloc(C + 1);
+  n1.alloc(C + 1);
+  flag.alloc(4);
+  k_greedy_init<<<nblk(C), 256, 0, s>>>(c0.p, n0.p, C);
+  i64 r = 0;
+  while (true) {
+    r++;
+    CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
+    k_greedy_round<<<nblk(C, 128), 128, 0, s>>>(view(), snap.cls_off.p, snap.cls_nodes.p, snap.cls_index.p, C,
+                                               cost, c0.p, n0.p, c1.p, n1.p, flag.p);
+    u32 ch;
+    CUDA_OK(cudaMemcpyAsync(&ch, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    sync();
+    std::swap(c0.p, c1.p);
+    std::swap(n0.p, n1.p);
+    if (!ch) break;
+  }
+  *rounds = r;
+  u32 rc = find(root);
+  u32 rd;
+  CUDA_OK(cudaMemcpyAsync(&rd, snap.cls_index.p + rc, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  double rcost;
+  sync();
+  CUDA_OK(cudaMemcpyAsync(&rcost, c0.p + rd, sizeof(double), cudaMemcpyDeviceToHost, s));
+  sync();
+  if (std::isinf(rcost)) throw TsatException(TSAT_ERR_NO_FINITE, "every root selection has infinite cost");
+  DevBuf<u8> mark;
+  DevBuf<u32> fa, fb;
+  mark.alloc(C + 1);
+  fa.alloc(C + 1);
+  fb.alloc(C + 1);
+  CUDA_OK(cudaMemsetAsync(mark.p, 0, C + 1, s));
+  u8 one = 1;
+  CUDA_OK(cudaMemcpyAsync(mark.p + rd, &one, 1, cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpyAsync(fa.p, &rd, sizeof(u32), cudaMemcpyHostToDevice, s));
+  u32 nf = 1;
+  while (nf) {
+    CUDA_OK(cudaMemsetAsync(flag.p, 0, 2 * sizeof(u32), s));
+    k_sel_step<<<nblk(nf), 256, 0, s>>>(view(), fa.p, nf, n0.p, snap.cls_index.p, mark.p, fb.p, flag.p,
+                                        flag.p + 1);
+    u32 hf[2];
+    CUDA_OK(cudaMemcpyAsync(hf, flag.p, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    sync();
+    if (hf[1]) throw TsatException(TSAT_ERR_STATE, "no selected node covers a reached e-class");
+    nf = hf[0];
+    std::swap(fa.p, fb.p);
+  }
+  DevBuf<u32> oc, on;
+  oc.alloc(C + 1);
+  on.alloc(C + 1);
+  CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
+  k_sel_collect<<<nblk(C), 256, 0, s>>>(mark.p, snap.cls_ids.p, n0.p, C, oc.p, on.p, flag.p);
+  u32 k;
+  CUDA_OK(cudaMemcpyAsync(&k, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
+  CUDA_OK(cudaMemcpyAsync(sel_cls, oc.p, k * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaMemcpyAsync(sel_node, on.p, k * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
+  *nsel = k;
+  return rcost;
+}

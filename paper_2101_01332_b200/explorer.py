@@ -1,0 +1,186 @@
+"""Exploration entry points (reference: pkg/src/tensorsat/explorer.py:56-384).
+
+``explore`` / ``saturate`` keep the reference signatures and result types; the
+whole iteration loop -- e-matching, multi-pattern joins, shape and cycle
+gates, application, rebuild, cycle post-processing -- runs on the GPU in
+``tsat_saturate`` (csrc/explore.cu, csrc/wave.cu).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .egraph import EGraph, compile_ruleset
+from .errors import TensorSatError
+from .tensor_lang import TensorGraph, build_egraph
+
+FILTER_MODES = ("none", "vanilla", "efficient")
+_MODE_CODE = {"none": 0, "vanilla": 1, "efficient": 2}
+_STOPS = ("iter-limit", "saturated", "node-limit", "timeout")
+
+
+@dataclass
+class ExploreLimits:
+    n_max: int = 50000
+    k_max: int = 15
+    k_multi: int = 1
+    time_limit_s: Optional[float] = None
+
+    def __post_init__(self):
+        if min(self.n_max, self.k_max, self.k_multi) < 0:
+            raise ValueError("limits must be non-negative")
+        if self.k_multi > self.k_max:
+            raise ValueError("k_multi must be <= k_max")
+
+
+@dataclass
+class RuleStats:
+    found: int = 0
+    applied: int = 0
+    applied_noop: int = 0
+    skipped_self: int = 0
+    skipped_compat: int = 0
+    skipped_shape: int = 0
+    skipped_cycle: int = 0
+
+
+_RULE_FIELDS = ("found", "applied", "applied_noop", "skipped_self", "skipped_compat",
+                "skipped_shape", "skipped_cycle")
+
+
+@dataclass
+class ExploreReport:
+    iterations: int = 0
+    stop_reason: str = ""
+    enodes_per_iter: list = field(default_factory=list)
+    alloc_per_iter: list = field(default_factory=list)
+    eclasses_per_iter: list = field(default_factory=list)
+    rules: dict = field(default_factory=dict)
+    prefilter_checks: int = 0
+    prefilter_rejects: int = 0
+    postprocess_filtered: int = 0
+    node_limit_overshoot: int = 0
+    filter_size: int = 0
+    time_s: float = 0.0
+
+    @property
+    def saturated(self) -> bool:
+        return self.stop_reason == "saturated"
+
+    def total(self, name: str) -> int:
+        return sum(getattr(s, name) for s in self.rules.values())
+
+    def to_stats(self) -> dict:
+        out = {
+            "explore.iterations": self.iterations,
+            "explore.stop_reason": self.stop_reason,
+            "explore.enodes_per_iter": ",".join(map(str, self.enodes_per_iter)),
+            "explore.alloc_per_iter": ",".join(map(str, self.alloc_per_iter)),
+            "explore.eclasses_per_iter": ",".join(map(str, self.eclasses_per_iter)),
+            "explore.prefilter_checks": self.prefilter_checks,
+            "explore.prefilter_rejects": self.prefilter_rejects,
+            "explore.postprocess_filtered": self.postprocess_filtered,
+            "explore.node_limit_overshoot": self.node_limit_overshoot,
+            "explore.filter_size": self.filter_size,
+            "explore.time_s": self.time_s,
+        }
+        for name, s in sorted(self.rules.items()):
+            for f in _RULE_FIELDS:
+                out[f"rule.{name}.{f}"] = getattr(s, f)
+        return out
+
+
+def saturate(
+    eg: EGraph,
+    rules: Sequence,
+    limits: Optional[ExploreLimits] = None,
+    filter_mode: str = "efficient",
+    filt: Optional[set] = None,
+    on_reject: Optional[Callable] = None,
+    allow_self_pairs: bool = False,
+):
+    """Iterate rules on ``eg`` (mutated in place) until saturation or a limit.
+    Returns (filter list, ExploreReport); ``filt`` is updated in place."""
+    limits = limits or ExploreLimits()
+    if filter_mode not in FILTER_MODES:
+        raise ValueError(f"filter_mode must be one of {FILTER_MODES}")
+    if filter_mode == "vanilla":
+        raise NotImplementedError("vanilla (apply-on-clone) cycle filtering is not part of the B200 engine")
+    if on_reject is not None:
+        raise NotImplementedError("on_reject needs the live mid-iteration e-graph, which stays on the GPU")
+    filt = set() if filt is None else filt
+    rules = list(rules)
+    eg.set_filter(filt)
+    blob, _ = compile_ruleset(eg, rules)
+    lib = _lib.load()
+    _lib.check(eg._h, lib.tsat_load_rules(eg._h, len(blob), _lib.ptr(blob, C.c_int64)))
+    lim = _lib.Limits(limits.n_max, limits.k_max, limits.k_multi,
+                      -1.0 if limits.time_limit_s is None else float(limits.time_limit_s))
+    rep = _lib.Report()
+    rs = np.zeros(max(len(rules), 1) * 7, np.int64)
+    per = np.zeros(max(limits.k_max, 1) * 3, np.int64)
+    try:
+        _lib.check(eg._h, lib.tsat_saturate(eg._h, C.byref(lim), _MODE_CODE[filter_mode],
+                                            1 if allow_self_pairs else 0, C.byref(rep),
+                                            _lib.ptr(rs, C.c_int64), _lib.ptr(per, C.c_int64)))
+    finally:
+        eg._touch()
+    report = ExploreReport()
+    for i, r in enumerate(rules):
+        report.rules.setdefault(r.name, RuleStats(*[int(x) for x in rs[7 * i:7 * i + 7]]))
+    it = int(rep.iterations)
+    report.iterations = it
+    report.stop_reason = _STOPS[rep.stop_reason]
+    report.enodes_per_iter = [int(per[3 * i]) for i in range(it)]
+    report.alloc_per_iter = [int(per[3 * i + 1]) for i in range(it)]
+    report.eclasses_per_iter = [int(per[3 * i + 2]) for i in range(it)]
+    report.prefilter_checks = int(rep.prefilter_checks)
+    report.prefilter_rejects = int(rep.prefilter_rejects)
+    report.postprocess_filtered = int(rep.postprocess_filtered)
+    report.node_limit_overshoot = int(rep.node_limit_overshoot)
+    report.time_s = float(rep.time_s)
+    extra = {x for x in filt if not (0 <= int(x) < eg.allocated_nodes)}
+    filt.clear()
+    filt.update(eg.get_filter())
+    filt.update(extra)
+    report.filter_size = len(filt)
+    return filt, report
+
+
+def explore(
+    g: TensorGraph,
+    rules: Sequence,
+    limits: Optional[ExploreLimits] = None,
+    filter_mode: str = "efficient",
+    on_reject: Optional[Callable] = None,
+    allow_self_pairs: bool = False,
+    device: int = 0,
+):
+    """End-to-end exploration of a single-rooted tensor graph on the GPU."""
+    if g.root is None:
+        raise TensorSatError("graph must be single-rooted (run make_single_rooted)")
+    eg, _ = build_egraph(g, device=device)
+    filt, report = saturate(eg, rules, limits, filter_mode, on_reject=on_reject,
+                            allow_self_pairs=allow_self_pairs)
+    return eg, filt, report
+
+
+def apply_multi_pattern(eg, multi_rules, filt=None, filter_mode="none", allow_self_pairs=False) -> int:
+    """One multi-pattern pass (explorer.py:270-289)."""
+    rules = [r for r in multi_rules if r.multi]
+    filt, rep = saturate(eg, rules, ExploreLimits(n_max=1 << 62, k_max=1, k_multi=1), filter_mode,
+                         filt=set() if filt is None else filt, allow_self_pairs=allow_self_pairs)
+    return rep.total("applied")
+
+
+def apply_single_patterns(eg, single_rules, filt=None, filter_mode="none") -> int:
+    """One single-pattern pass (explorer.py:292-308)."""
+    rules = [r for r in single_rules if not r.multi]
+    filt, rep = saturate(eg, rules, ExploreLimits(n_max=1 << 62, k_max=1, k_multi=0), filter_mode,
+                         filt=set() if filt is None else filt)
+    return rep.total("applied")

@@ -1,0 +1,150 @@
+"""Extraction (reference: pkg/src/tensorsat/extract.py).
+
+``greedy_extract`` runs the min-cost relaxation and the reached-selection
+walk on the GPU (``tsat_greedy``, csrc/extract.cu).  ``reconstruct`` and the
+selection helpers are host-side format code.  ILP extraction (build_ilp /
+solve_ilp / export_lp) is out of scope for the B200 engine.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+from typing import Iterable, Mapping, Optional
+
+import numpy as np
+
+from . import _lib
+from .egraph import CostVector, EGraph
+from .errors import ExtractionError, ReconstructError
+from .tensor_lang import SIGNATURES, TensorGraph, ValueKind
+
+
+@dataclass
+class SolverStats:
+    nodes_explored: int = 0
+    lp_solves: int = 0
+    time_s: float = 0.0
+    optimal: bool = True
+    objective: float = 0.0
+
+
+@dataclass
+class ExtractionResult:
+    selection: dict
+    total_cost: float
+    graph: Optional[TensorGraph] = None
+    stats: Optional[SolverStats] = None
+    optimal: bool = True
+
+
+def selection_cost(costs: Mapping, selection: Mapping) -> float:
+    return sum(costs[n] for n in set(selection.values()))
+
+
+def selection_is_acyclic(eg: EGraph, selection: Mapping) -> bool:
+    state: dict = {}
+
+    def visit(c) -> bool:
+        c = eg.find(c)
+        s = state.get(c)
+        if s == 2:
+            return True
+        if s == 1:
+            return False
+        state[c] = 1
+        ok = all(visit(ch) for ch in eg.nodes[selection[c]].children)
+        state[c] = 2
+        return ok
+
+    return all(visit(c) for c in selection)
+
+
+def greedy_extract(eg: EGraph, costs: Mapping, filt: Iterable[int] = ()) -> ExtractionResult:
+    """Greedy fixpoint extraction on the GPU (extract.py:120-159)."""
+    if eg.root is None:
+        raise ExtractionError("e-graph has no root")
+    t0 = time.perf_counter()
+    eg.set_filter(filt)
+    lib = _lib.load()
+    n = eg.allocated_nodes
+    arr = None
+    if not (isinstance(costs, CostVector) and costs._eg is eg and len(costs.array) == n):
+        arr = np.zeros(max(n, 1), np.float64)
+        alive = eg.view.alive
+        for nid in np.nonzero(alive)[0]:
+            arr[nid] = costs[int(nid)]
+    cap = max(eg.num_classes, 1)
+    sc = np.zeros(cap, np.uint32)
+    sn = np.zeros(cap, np.uint32)
+    k = C.c_uint32()
+    best = C.c_double()
+    rounds = C.c_int64()
+    _lib.check(eg._h, lib.tsat_greedy(eg._h, _lib.ptr(arr, C.c_double), _lib.ptr(sc, C.c_uint32),
+                                      _lib.ptr(sn, C.c_uint32), C.byref(k), C.byref(best), C.byref(rounds)))
+    selection = {int(c): int(m) for c, m in zip(sc[: k.value], sn[: k.value])}
+    stats = SolverStats(nodes_explored=int(rounds.value), time_s=time.perf_counter() - t0)
+    return ExtractionResult(selection, selection_cost(costs, selection), stats=stats)
+
+
+def reconstruct(eg: EGraph, selection: Mapping) -> TensorGraph:
+    """Materialise a selection as a tensor graph (extract.py:584-639)."""
+    if eg.root is None:
+        raise ReconstructError("e-graph has no root")
+    g = TensorGraph()
+    built: dict = {}
+    onstack: set = set()
+    nodes = eg.view
+
+    def build(cid: int) -> str:
+        cid = eg.find(cid)
+        if cid in built:
+            return built[cid]
+        if cid in onstack:
+            raise ReconstructError(f"cycle through e-class c{cid}")
+        if cid not in selection:
+            raise ReconstructError(f"selection misses e-class c{cid}")
+        onstack.add(cid)
+        en = nodes.node(selection[cid])
+        sig = SIGNATURES.get(en.op) if isinstance(en.op, str) else None
+        if sig is None:
+            raise ReconstructError(f"e-node n{en.id} ({en.op!r}) is not a graph operator")
+        params: dict = {}
+        inputs: list = []
+        for (arg, kind), ch in zip(sig.args, en.children):
+            ch = eg.find(ch)
+            if kind in (ValueKind.T, ValueKind.TT):
+                inputs.append(build(ch))
+            else:
+                leaf_id = selection.get(ch)
+                if leaf_id is None:
+                    raise ReconstructError(f"selection misses parameter class c{ch}")
+                leaf = nodes.node(leaf_id)
+                if leaf.children:
+                    raise ReconstructError(f"parameter class c{ch} selected a non-literal")
+                params[arg] = leaf.op
+        onstack.discard(cid)
+        name = f"e{cid}"
+        g.add(name, en.op, tuple(inputs), **params)
+        built[cid] = name
+        return name
+
+    root_name = build(eg.root)
+
+    def flat(name: str) -> list:
+        nd = g.nodes[name]
+        if nd.op != "noop":
+            return [name]
+        return flat(nd.inputs[0]) + flat(nd.inputs[1])
+
+    g.set_outputs(flat(root_name))
+    g.root = root_name
+    return g
+
+
+def build_ilp(*a, **k):
+    raise NotImplementedError("ILP extraction is out of scope for the B200 engine (use greedy_extract)")
+
+
+solve_ilp = export_lp = parse_solution = build_ilp
