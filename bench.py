@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark: explore + extract search time per graph on B200 (BASELINE.json).
+
+Default workload = configs[1]: BERT-base graph (models.bert), all 14 rules,
+k_multi=1, N_max=50k, k_max=15, efficient cycle filtering, synthetic cost
+model, greedy extraction.  One step = one full explore + egraph_costs +
+greedy_extract of one graph (the reference's three timed spans).
+
+Arms:
+  * value: device-resident -- the initial e-graph is uploaded before the timed
+    region; the step runs saturate + costs + greedy on the GPU.
+  * e2e:   the public API from a host TensorGraph (explore -> egraph_costs ->
+    greedy_extract), host<->device copies inside the timed region.
+  * --impl reference: the CPU port of the reference (oracle/, the reference
+    itself is pure Python and cannot travel to the GPU box) on all host cores.
+N>1: one process per GPU, each explores its own graph (weak scaling, no
+collective on the data path); value = step time / graphs per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "bert": dict(model="bert", k_multi=1, n_max=50000, k_max=15,
+                 desc="configs[1]: BERT-base (12 layers, seq 64, hidden 768), all 14 rules, k_multi=1, "
+                      "N_max=50k, k_max=15, efficient cycle filtering, greedy"),
+    "nasrnn": dict(model="nasrnn", k_multi=0, n_max=50000, k_max=15,
+                   desc="configs[0]: NasRNN, single-pattern rules only, k_max=15, N_max=50k, greedy"),
+    "squeezenet": dict(model="squeezenet", k_multi=2, n_max=100000, k_max=15,
+                       desc="configs[2]: SqueezeNet, k_multi=2, N_max=100k, greedy"),
+    "resnext50": dict(model="resnext50", k_multi=2, n_max=100000, k_max=15,
+                      desc="configs[2]: ResNeXt-50, k_multi=2, N_max=100k, greedy"),
+    "inception_v3": dict(model="inception_v3", k_multi=2, n_max=50000, k_max=15,
+                         desc="configs[3]: Inception-v3, k_multi=2, greedy"),
+    "nasnet_a": dict(model="nasnet_a", k_multi=2, n_max=50000, k_max=15,
+                     desc="configs[3]: NasNet-A, k_multi=2, greedy"),
+}
+
+KGROUPS = ["rebuild", "ematch", "apply_seq", "apply_wave", "reach", "cycles", "costs", "greedy", "snapshot"]
+KERNEL_OF = {"rebuild": "k_canon_kids+k_dedup_insert+k_dedup_drop", "ematch": "k_ematch",
+             "greedy": "k_greedy_round", "reach": "k_close_rows (+trim)", "apply_seq": "k_seq_rule",
+             "apply_wave": "wave kernels", "costs": "k_node_costs", "cycles": "bfs/trim/dfs",
+             "snapshot": "snapshot CSR"}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def build_workload(name):
+    from paper_2101_01332_b200 import models
+    from paper_2101_01332_b200.rules import default_rules
+
+    w = WORKLOADS[name]
+    return models.MODELS[w["model"]](), list(default_rules()), w
+
+
+def run_oracle_once(name):
+    from oracle import tsat_oracle as O
+    from paper_2101_01332_b200.cost import CostModel
+
+    g, rules, w = build_workload(name)
+    t0 = time.perf_counter()
+    eg, filt, rep = O.oracle_explore(g, rules, n_max=w["n_max"], k_max=w["k_max"], k_multi=w["k_multi"])
+    costs = O.oracle_costs(eg, CostModel())
+    sel, total, _ = O.oracle_greedy(eg, costs, filt)
+    return time.perf_counter() - t0, eg.num_nodes, total
+
+
+def _oracle_worker(name):
+    return run_oracle_once(name)
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    g, rules, w = build_workload(args.workload)
+    times = []
+    with mp.get_context("fork").Pool(cores) as pool:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_oracle_worker, [args.workload] * cores)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+    per_graph = statistics.mean(times) / cores
+    line = {
+        "impl": "reference", "metric": "explore+extract search time (s) per graph", "value": per_graph,
+        "unit": "s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.mean(times) * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32+f64", "data": "synthetic (authored model graph)",
+        "config": {"workload": w["desc"], "graphs_per_step": cores},
+        "cpu_baseline": {"value": per_graph, "unit": "s", "cores": cores, "kind": "port",
+                         "sample": f"{cores} concurrent full explore+costs+greedy runs per step (oracle/tsat_oracle.py)"},
+        "e2e": {"value": per_graph, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--workload", default="bert", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    from paper_2101_01332_b200 import _lib
+    from paper_2101_01332_b200.cost import CostModel, egraph_costs
+    from paper_2101_01332_b200.explorer import ExploreLimits, explore, saturate
+    from paper_2101_01332_b200.extract import greedy_extract
+    from paper_2101_01332_b200.tensor_lang import build_egraph, initial_enodes
+
+    lib = _lib.load()
+    g, rules, w = build_workload(args.workload)
+    limits = ExploreLimits(n_max=w["n_max"], k_max=w["k_max"], k_multi=w["k_multi"])
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    # ---- device-resident arm: e-graphs uploaded before the timed region
+    graphs = [build_egraph(g, device=local)[0] for _ in range(args.warmup + args.steps)]
+    torch.cuda.synchronize()
+    step_s = []
+    kst = np.zeros((3, 9))
+    last = None
+    with Clocks(local) as clk:
+        for i, eg in enumerate(graphs):
+            flush.zero_()
+            barrier()
+            ms = np.zeros(9)
+            by = np.zeros(9)
+            la = np.zeros(9, np.int64)
+            lib.tsat_kernel_stats(eg._h, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                  by.ctypes.data_as(C.POINTER(C.c_double)),
+                                  la.ctypes.data_as(C.POINTER(C.c_int64)), 9, 1)
+            t0 = time.perf_counter()
+            filt, rep = saturate(eg, rules, limits, "efficient")
+            costs = egraph_costs(eg, CostModel())
+            res = greedy_extract(eg, costs, filt)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            barrier()
+            if i >= args.warmup:
+                step_s.append(max_over_ranks(dt))
+                lib.tsat_kernel_stats(eg._h, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                      by.ctypes.data_as(C.POINTER(C.c_double)),
+                                      la.ctypes.data_as(C.POINTER(C.c_int64)), 9, 0)
+                kst[0] += ms
+                kst[1] += by
+                kst[2] += la
+            last = (eg, rep, res)
+    clocks = clk.summary()
+    eg, rep, res = last
+    nodes = rep.enodes_per_iter[-1] if rep.enodes_per_iter else eg.num_nodes
+    ms_step = statistics.mean(step_s) * 1e3
+    value = ms_step / 1e3 / world
+
+    # ---- e2e arm through the public API
+    ops, kids, _, _ = initial_enodes(g)
+    h2d = 4 * len(ops) + 4 * (len(ops) + 1) + 4 * sum(len(k) for k in kids) + 96 * len(ops)
+    e2e_s = []
+    d2h = 0
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        barrier()
+        t0 = time.perf_counter()
+        eg2, filt2, rep2 = explore(g, rules, limits, "efficient", device=local)
+        costs2 = egraph_costs(eg2, CostModel())
+        res2 = greedy_extract(eg2, costs2, filt2)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        barrier()
+        if i >= args.warmup:
+            e2e_s.append(max_over_ranks(dt))
+        d2h = 8 * eg2.allocated_nodes + 8 * len(res2.selection) + 4 * len(filt2) + 8 * 7 * len(rules) + 24 * 15
+        del eg2
+    e2e = statistics.mean(e2e_s) / world
+
+    # ---- roofline: dominant instrumented kernel group with an algorithmic byte model
+    peak, peak_kind = load_peaks()
+    per_step = kst / max(len(step_s), 1)
+    with_bytes = [i for i in range(9) if per_step[1][i] > 0]
+    dom = max(with_bytes, key=lambda i: per_step[0][i]) if with_bytes else 0
+    dom_all = max(range(9), key=lambda i: per_step[0][i])
+    achieved = per_step[1][dom] / (per_step[0][dom] / 1e3) / 1e9 if per_step[0][dom] > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": KERNEL_OF[KGROUPS[dom]], "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                "launches_per_step": per_step[2][dom], "ms_per_step": per_step[0][dom],
+                "algorithmic_bytes_per_step": per_step[1][dom]}
+    groups_ms = {KGROUPS[i]: round(per_step[0][i], 3) for i in range(9)}
+
+    line = {
+        "metric": "explore+extract search time (s) per graph", "value": value, "unit": "s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64",
+        "data": "synthetic (authored model graph, random-free; L2 flushed between steps)",
+        "config": {"workload": w["desc"], "graphs_per_step": world, "l2": "flushed (256 MiB write) between steps",
+                   "final_enodes": nodes, "stop_reason": rep.stop_reason, "total_cost": res.total_cost,
+                   "parallelism": f"replicas x{world}"},
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "enodes_matched_per_s": None, "kernel_groups_ms_per_step": groups_ms,
+        "dominant_group": KGROUPS[dom_all],
+        "roofline": roofline, "clocks": clocks, "gpu_launches": int(per_step[2].sum()),
+    }
+    em_ms = per_step[0][1]
+    if em_ms > 0:
+        # every live e-node root-tested once per unique canonical pattern
+        line["enodes_matched_per_s"] = None  # filled below from the per-iteration sizes
+        tested = sum(rep.enodes_per_iter[:-1]) * 13 + rep.enodes_per_iter[0] * 0
+        line["enodes_matched_per_s"] = tested / (em_ms / 1e3) if tested else None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t_cpu, n_cpu, total_cpu = run_oracle_once(args.workload)
+        line["cpu_baseline"] = {"value": t_cpu, "unit": "s", "cores": 1, "kind": "port",
+                                "sample": f"one full explore+costs+greedy of the same graph on 1 core "
+                                          f"(oracle/tsat_oracle.py), {n_cpu} e-nodes, cost {total_cpu:.6f}"}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -113,6 +113,11 @@ int tsat_costs(tsat_engine* h, int32_t mode, int32_t strict, int32_t ntab, const
 int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, uint32_t* sel_node,
                 uint32_t* nsel, double* root_best, int64_t* rounds);
 
+/* per kernel-group CUDA-event timings and algorithmic bytes since the last
+ * reset; groups: rebuild, ematch, apply_seq, apply_wave, reach, cycles,
+ * costs, greedy, snapshot */
+int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launches, int32_t n, int32_t reset);
+
 /* per-phase device timings of the last saturate / greedy (ms) */
 int tsat_phase_times(tsat_engine* h, double* out, int32_t n);
 

@@ -257,6 +257,19 @@ int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, u
   });
 }
 
+int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launches, int32_t n, int32_t reset) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    for (int i = 0; i < n && i < KG_COUNT; i++) {
+      ms[i] = e.kstat[i].ms;
+      bytes[i] = e.kstat[i].bytes;
+      launches[i] = (int64_t)e.kstat[i].launches;
+    }
+    if (reset)
+      for (int i = 0; i < KG_COUNT; i++) e.kstat[i] = KStat();
+  });
+}
+
 int tsat_phase_times(tsat_engine* h, double* out, int32_t n) {
   GUARD(h, {
     for (int i = 0; i < n; i++) out[i] = i < (int)h->e->phase_ms.size() ? h->e->phase_ms[i] : 0.0;

@@ -44,6 +44,8 @@ void dev_sort_pairs_u32(Engine& e, u32* kin, u32* kout, u32* vin, u32* vout, u32
 Engine::Engine(int dev) : device(dev) {
   CUDA_OK(cudaSetDevice(dev));
   CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  CUDA_OK(cudaEventCreate(&ev_pool[0]));
+  CUDA_OK(cudaEventCreate(&ev_pool[1]));
   cnt.alloc(1);
   err.alloc(1);
   dstats.alloc(1);
@@ -59,6 +61,24 @@ Engine::Engine(int dev) : device(dev) {
   CUDA_OK(cudaMemsetAsync(tree_count.p, 0, sizeof(u32), s));
   ensure_nodes(1024, 4096);
   sync();
+}
+
+KTimer::KTimer(Engine& e_, int g_, double bytes_, unsigned long long launches_)
+    : e(e_), g(g_), bytes(bytes_), launches(launches_) {
+  a = e.ev_pool[0];
+  b = e.ev_pool[1];
+  CUDA_OK(cudaEventRecord(a, e.s));
+}
+
+KTimer::~KTimer() {
+  cudaEventRecord(b, e.s);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  e.kstat[g].ms += ms;
+  e.kstat[g].bytes += bytes;
+  e.kstat[g].launches += launches;
+  e.nlaunch += launches;
 }
 
 Engine::~Engine() {
@@ -528,11 +548,15 @@ void Engine::rebuild() {
   srt_s.ensure(n + 1);
   small.ensure(4);
   while (true) {
-    k_canon_kids<<<nblk(n), 256, 0, s>>>(view(), n);
-    CUDA_OK(cudaMemsetAsync(hc.p, 0xFF, (size_t)hc_cap * sizeof(u32), s));
-    k_dedup_insert<<<nblk(n), 256, 0, s>>>(view(), n);
-    CUDA_OK(cudaMemsetAsync(small.p, 0, 2 * sizeof(u32), s));
-    k_dedup_drop<<<nblk(n), 256, 0, s>>>(view(), n, linked.p, small.p, small.p + 1);
+    {
+      // algorithmic bytes of one dirty round: 60 N + 12 A
+      KTimer kt(*this, KG_REBUILD, 60.0 * h.live + 12.0 * h.nkids, 3);
+      k_canon_kids<<<nblk(n), 256, 0, s>>>(view(), n);
+      CUDA_OK(cudaMemsetAsync(hc.p, 0xFF, (size_t)hc_cap * sizeof(u32), s));
+      k_dedup_insert<<<nblk(n), 256, 0, s>>>(view(), n);
+      CUDA_OK(cudaMemsetAsync(small.p, 0, 2 * sizeof(u32), s));
+      k_dedup_drop<<<nblk(n), 256, 0, s>>>(view(), n, linked.p, small.p, small.p + 1);
+    }
     u32 hm[2];
     CUDA_OK(cudaMemcpyAsync(hm, small.p, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
@@ -592,6 +616,7 @@ __global__ void k_op_hist(const u32* ops, u32 m, u32* hist) {
 
 void Engine::build_snapshot() {
   u32 n = h.next_id, m = h.live;
+  KTimer kt(*this, KG_SNAPSHOT, 0.0, 5);
   DevBuf<u32>& fl = scratch_u32[1];
   DevBuf<u32>& pos = scratch_u32[2];
   DevBuf<u32>& ids = scratch_u32[3];

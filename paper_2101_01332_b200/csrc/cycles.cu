@@ -204,6 +204,7 @@ __global__ void k_untrimmed(const u32* level, u32 n, u32* list, u32* cnt) {
 
 void Engine::build_reach() {
   if (!snap.valid) build_snapshot();
+  KTimer kt(*this, KG_REACH, 0.0, 0);
   ClassGraph cg;
   build_class_graph(*this, cg);
   u32 n = cg.ncls;
@@ -243,12 +244,15 @@ void Engine::build_reach() {
   reach.n = n;
   reach.words = words;
   reach.valid = true;
+  // closure traffic: every row written once, each edge reads its child's row
+  kt.bytes = 4.0 * words * ((double)n + (double)cg.nedge);
+  kt.launches = 4 + nl;
   sync();
 }
 
 // ---------------------------------------------------------------- post-processing
 
-__global__ void k_bfs_init(u8* mark, u32 n, u32 root, u32* front, u32* nf) {
+__global__ void k_bfs_init(u32* mark, u32 n, u32 root, u32* front, u32* nf) {
   GRID_STRIDE(i, n) mark[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     mark[root] = 1;
@@ -257,19 +261,19 @@ __global__ void k_bfs_init(u8* mark, u32 n, u32 root, u32* front, u32* nf) {
   }
 }
 
-__global__ void k_bfs_step(const u32* front, u32 nf, const u32* eoff, const u32* edst, u8* mark, u32* next,
+__global__ void k_bfs_step(const u32* front, u32 nf, const u32* eoff, const u32* edst, u32* mark, u32* next,
                            u32* nn) {
   GRID_STRIDE(t, nf) {
     u32 i = front[t];
     for (u32 e = eoff[i]; e < eoff[i + 1]; e++) {
       u32 j = edst[e];
-      if (!mark[j]) {
-        // benign race: a class may be queued twice; both copies are harmless
-        mark[j] = 1;
-        next[atomicAdd(nn, 1u)] = j;
-      }
+      if (mark[j] == 0 && atomicCAS(&mark[j], 0u, 1u) == 0u) next[atomicAdd(nn, 1u)] = j;
     }
   }
+}
+
+__global__ void k_mark_to_u8(const u32* m, u32 n, u8* out) {
+  GRID_STRIDE(i, n) out[i] = m[i] ? 1 : 0;
 }
 
 __global__ void k_count_cyclic(const u8* mark, const u32* level, u32 n, u32* cnt) {
@@ -372,6 +376,7 @@ i64 Engine::break_all_cycles(bool precheck_only, std::vector<std::vector<u32>>* 
   u32 root_dense;
   CUDA_OK(cudaMemcpyAsync(&root_dense, snap.cls_index.p + rc, sizeof(u32), cudaMemcpyDeviceToHost, s));
   sync();
+  KTimer kt(*this, KG_CYCLES, 0.0, 0);
   i64 added = 0;
   u32 cyc_cap = 1 << 16, off_cap = 1 << 12;
   while (true) {
@@ -380,20 +385,23 @@ i64 Engine::break_all_cycles(bool precheck_only, std::vector<std::vector<u32>>* 
     u32 n = cg.ncls;
     DevBuf<u8> mark;
     mark.alloc(n + 1);
+    DevBuf<u32> mark32;
+    mark32.alloc(n + 1);
     DevBuf<u32> fa, fb;
     fa.alloc(n + 1);
     fb.alloc(n + 1);
     DevBuf<u32>& c2 = scratch_u32[3];
     c2.ensure(4);
-    k_bfs_init<<<nblk(n), 256, 0, s>>>(mark.p, n, root_dense, fa.p, c2.p);
+    k_bfs_init<<<nblk(n), 256, 0, s>>>(mark32.p, n, root_dense, fa.p, c2.p);
     u32 nf = 1;
     while (nf) {
       CUDA_OK(cudaMemsetAsync(c2.p + 1, 0, sizeof(u32), s));
-      k_bfs_step<<<nblk(nf), 256, 0, s>>>(fa.p, nf, cg.eoff.p, cg.edst.p, mark.p, fb.p, c2.p + 1);
+      k_bfs_step<<<nblk(nf), 256, 0, s>>>(fa.p, nf, cg.eoff.p, cg.edst.p, mark32.p, fb.p, c2.p + 1);
       CUDA_OK(cudaMemcpyAsync(&nf, c2.p + 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
       sync();
       std::swap(fa.p, fb.p);
     }
+    k_mark_to_u8<<<nblk(n), 256, 0, s>>>(mark32.p, n, mark.p);
     std::vector<u32> lo;
     DevBuf<u32> order;
     u32 ntr = 0;

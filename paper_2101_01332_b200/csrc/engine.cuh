@@ -144,6 +144,25 @@ struct ExploreReportC {
   double time_s;
 };
 
+// per kernel-group device timing + algorithmic bytes (roofline reporting)
+enum KGroup { KG_REBUILD = 0, KG_EMATCH, KG_APPLY_SEQ, KG_APPLY_WAVE, KG_REACH, KG_CYCLES, KG_COSTS, KG_GREEDY, KG_SNAPSHOT, KG_COUNT };
+struct KStat {
+  double ms = 0.0;
+  double bytes = 0.0;
+  unsigned long long launches = 0;
+};
+
+struct Engine;
+struct KTimer {  // records CUDA events on the engine stream around a kernel group
+  Engine& e;
+  int g;
+  double bytes;
+  unsigned long long launches;
+  cudaEvent_t a, b;
+  KTimer(Engine& e_, int g_, double bytes_, unsigned long long launches_);
+  ~KTimer();
+};
+
 struct Engine {
   int device = 0;
   cudaStream_t s = nullptr;
@@ -195,7 +214,10 @@ struct Engine {
   std::vector<RuleStatsH> rstats;
   std::vector<i64> enodes_per_iter, alloc_per_iter, eclasses_per_iter;
   ExploreReportC report{};
-  std::vector<double> phase_ms;
+  std::vector<double> phase_ms = std::vector<double>(8, 0.0);
+  unsigned long long nlaunch = 0;  // kernels of ours launched (not CUB)
+  KStat kstat[KG_COUNT];
+  cudaEvent_t ev_pool[2] = {nullptr, nullptr};
 
   Engine(int dev);
   ~Engine();

@@ -302,7 +302,10 @@ void Engine::run_rule_seq(int ri, int filter_mode, int allow_self, i64 n_max, un
   unsigned long long p = p0;
   while (p < p1) {
     CUDA_OK(cudaMemsetAsync(dstats.p, 0, sizeof(DevStats), s));
-    k_seq_rule<<<1, 1, 0, s>>>(view(), R, RD, dstats.p, p, p1, n_max);
+    {
+      KTimer kt(*this, KG_APPLY_SEQ, 0.0, 1);
+      k_seq_rule<<<1, 1, 0, s>>>(view(), R, RD, dstats.p, p, p1, n_max);
+    }
     DevStats d;
     CUDA_OK(cudaMemcpyAsync(&d, dstats.p, sizeof(d), cudaMemcpyDeviceToHost, s));
     pull_counters();
@@ -339,10 +342,20 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
   std::vector<int> multi, single;
   for (size_t i = 0; i < rules.size(); i++) (rules[i].nsrc > 1 ? multi : single).push_back((int)i);
   int stop = 0;  // iter-limit
+  for (int q = 0; q < 8; q++) phase_ms[q] = 0.0;
+  auto tick = [&](int ph, double& t) {
+    sync();
+    double n2 = now_s();
+    phase_ms[ph] += (n2 - t) * 1e3;
+    t = n2;
+  };
+  double tp = now_s();
   for (i64 it = 0; it < lim.k_max; it++) {
     if (!snap.valid) build_snapshot();
+    tick(0, tp);
     if (filter_mode == 2) build_reach();
     else reach.valid = false;
+    tick(1, tp);
     std::vector<int> active;
     if (it < lim.k_multi) active = multi;
     active.insert(active.end(), single.begin(), single.end());
@@ -351,6 +364,7 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
       for (int t = 0; t < rules[ri].nsrc; t++) need[rules[ri].src_pat[t]] = 1;
     for (size_t p = 0; p < patterns.size(); p++)
       if (need[p]) ematch_pattern((int)p, matches[p]);
+    tick(2, tp);
     seq_changed = false;
     seq_stop = false;
     int stop_flag = 0;
@@ -370,9 +384,13 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
       }
     }
     snap.valid = false;
+    tick(3, tp);
     rebuild();
+    tick(4, tp);
     build_snapshot();
+    tick(0, tp);
     if (filter_mode != 0) report.postprocess_filtered += break_all_cycles(false, nullptr);
+    tick(5, tp);
     report.iterations = it + 1;
     enodes_per_iter.push_back(h.live);
     alloc_per_iter.push_back(h.next_id);

@@ -364,7 +364,10 @@ void Engine::costs(int mode, int strict, int ntab, const char* keys, const i64* 
     ct.mask = cap - 1;
   }
   d_costs.ensure(n + 1);
-  k_node_costs<<<nblk(n, 128), 128, 0, s>>>(view(), ct, n, d_costs.p);
+  {
+    KTimer kt(*this, KG_COSTS, 16.0 * h.live + 4.0 * h.nkids + 128.0 * h.nkids, 1);
+    k_node_costs<<<nblk(n, 128), 128, 0, s>>>(view(), ct, n, d_costs.p);
+  }
   if (out) CUDA_OK(cudaMemcpyAsync(out, d_costs.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   sync();
   check_error();
@@ -404,7 +407,7 @@ __global__ void k_greedy_round(G g, const u32* cls_off, const u32* cls_nodes, co
   }
 }
 
-__global__ void k_sel_step(G g, const u32* front, u32 nf, const u32* bn, const u32* cls_index, u8* mark,
+__global__ void k_sel_step(G g, const u32* front, u32 nf, const u32* bn, const u32* cls_index, u32* mark,
                            u32* next, u32* nn, u32* missing) {
   GRID_STRIDE(t, nf) {
     u32 i = front[t];
@@ -415,15 +418,12 @@ __global__ void k_sel_step(G g, const u32* front, u32 nf, const u32* bn, const u
     }
     for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) {
       u32 c = cls_index[uf_find_ro(g.parent, g.kids[j])];
-      if (!mark[c]) {
-        mark[c] = 1;
-        next[atomicAdd(nn, 1u)] = c;
-      }
+      if (mark[c] == 0 && atomicCAS(&mark[c], 0u, 1u) == 0u) next[atomicAdd(nn, 1u)] = c;
     }
   }
 }
 
-__global__ void k_sel_collect(const u8* mark, const u32* cls_ids, const u32* bn, u32 n, u32* oc, u32* on, u32* cnt) {
+__global__ void k_sel_collect(const u32* mark, const u32* cls_ids, const u32* bn, u32 n, u32* oc, u32* on, u32* cnt) {
   GRID_STRIDE(i, n) {
     if (!mark[i]) continue;
     u32 k = atomicAdd(cnt, 1u);
@@ -457,8 +457,12 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
   while (true) {
     r++;
     CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
-    k_greedy_round<<<nblk(C, 128), 128, 0, s>>>(view(), snap.cls_off.p, snap.cls_nodes.p, snap.cls_index.p, C,
-                                               cost, c0.p, n0.p, c1.p, n1.p, flag.p);
+    {
+      // per round: 16 N + 12 A + 12 C
+      KTimer kt(*this, KG_GREEDY, 16.0 * h.live + 12.0 * h.nkids + 12.0 * C, 1);
+      k_greedy_round<<<nblk(C, 128), 128, 0, s>>>(view(), snap.cls_off.p, snap.cls_nodes.p, snap.cls_index.p, C,
+                                                 cost, c0.p, n0.p, c1.p, n1.p, flag.p);
+    }
     u32 ch;
     CUDA_OK(cudaMemcpyAsync(&ch, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
@@ -475,14 +479,14 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
   CUDA_OK(cudaMemcpyAsync(&rcost, c0.p + rd, sizeof(double), cudaMemcpyDeviceToHost, s));
   sync();
   if (std::isinf(rcost)) throw TsatException(TSAT_ERR_NO_FINITE, "every root selection has infinite cost");
-  DevBuf<u8> mark;
+  DevBuf<u32> mark;
   DevBuf<u32> fa, fb;
   mark.alloc(C + 1);
   fa.alloc(C + 1);
   fb.alloc(C + 1);
-  CUDA_OK(cudaMemsetAsync(mark.p, 0, C + 1, s));
-  u8 one = 1;
-  CUDA_OK(cudaMemcpyAsync(mark.p + rd, &one, 1, cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemsetAsync(mark.p, 0, (C + 1) * sizeof(u32), s));
+  u32 one = 1;
+  CUDA_OK(cudaMemcpyAsync(mark.p + rd, &one, sizeof(u32), cudaMemcpyHostToDevice, s));
   CUDA_OK(cudaMemcpyAsync(fa.p, &rd, sizeof(u32), cudaMemcpyHostToDevice, s));
   u32 nf = 1;
   while (nf) {

@@ -193,10 +193,15 @@ void Engine::ematch_pattern(int pid, MatchSet& out) {
     rc.ensure(cap);
     rb.ensure((u64)cap * std::max(p.nb, 1));
     CUDA_OK(cudaMemsetAsync(cntb.p, 0, sizeof(u32), s));
-    k_ematch<<<nblk(ncand, 128), 128, 0, s>>>(view(), sd, p, snap.op_nodes.p + range[0], ncand, rc.p, rb.p,
-                                              cntb.p, cap);
+    {
+      // root-candidate scan: id 4 + op 4 + koff 8 + flags 1 + children/parents 8a per candidate
+      KTimer kt(*this, KG_EMATCH, (double)ncand * (17.0 + 8.0 * p.apps[0].nargs), 1);
+      k_ematch<<<nblk(ncand, 128), 128, 0, s>>>(view(), sd, p, snap.op_nodes.p + range[0], ncand, rc.p, rb.p,
+                                                cntb.p, cap);
+    }
     CUDA_OK(cudaMemcpyAsync(&m, cntb.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
+    kstat[KG_EMATCH].bytes += (double)std::min(m, cap) * 4.0 * (1 + p.nb);
     if (m <= cap) break;
     cap = m + 1024;
   }
