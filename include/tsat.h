@@ -118,6 +118,10 @@ int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, u
  * costs, greedy, snapshot */
 int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launches, int32_t n, int32_t reset);
 
+/* diagnostics: level count, peeled classes, classes, class edges, snapshot /
+ * filter versions, allocated and live e-nodes */
+int tsat_debug_info(tsat_engine* h, int64_t* out, int32_t n);
+
 /* per-phase device timings of the last saturate / greedy (ms) */
 int tsat_phase_times(tsat_engine* h, double* out, int32_t n);
 

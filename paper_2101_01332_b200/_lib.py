@@ -61,6 +61,7 @@ _SIGS = {
     "tsat_costs": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, i64p, f64p, f64p], C.c_int),
     "tsat_greedy": ([C.c_void_p, f64p, u32p, u32p, u32p, f64p, i64p], C.c_int),
     "tsat_phase_times": ([C.c_void_p, f64p, C.c_int32], C.c_int),
+    "tsat_debug_info": ([C.c_void_p, i64p, C.c_int32], C.c_int),
     "tsat_kernel_stats": ([C.c_void_p, f64p, f64p, i64p, C.c_int32, C.c_int32], C.c_int),
 }
 

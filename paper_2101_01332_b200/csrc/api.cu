@@ -26,13 +26,28 @@ struct tsat_engine {
 
 extern "C" {
 
+// Engines are pooled: creating one allocates every device table, so a
+// destroyed handle's engine is reset and kept for the next tsat_create.
+static std::vector<Engine*>& engine_pool() {
+  static std::vector<Engine*> p;
+  return p;
+}
+
 int tsat_create(int device, int analysis, tsat_engine** out) {
   if (!out) return TSAT_ERR_ARG;
   *out = nullptr;
   try {
     tsat_engine* h = new tsat_engine();
-    h->e = new Engine(device);
-    h->e->analysis = analysis != 0;
+    auto& pool = engine_pool();
+    for (size_t i = 0; i < pool.size(); i++)
+      if (pool[i]->device == device) {
+        h->e = pool[i];
+        pool.erase(pool.begin() + i);
+        break;
+      }
+    if (!h->e) h->e = new Engine(device);
+    CUDA_OK(cudaSetDevice(device));
+    h->e->reset(analysis != 0);
     *out = h;
     return TSAT_OK;
   } catch (TsatException& ex) {
@@ -44,7 +59,17 @@ int tsat_create(int device, int analysis, tsat_engine** out) {
 
 void tsat_destroy(tsat_engine* h) {
   if (!h) return;
-  delete h->e;
+  auto& pool = engine_pool();
+  bool pooled = false;
+  if (h->e && pool.size() < 4) {
+    try {
+      h->e->reset(false);
+      pool.push_back(h->e);
+      pooled = true;
+    } catch (...) {
+    }
+  }
+  if (!pooled) delete h->e;
   delete h;
 }
 
@@ -166,7 +191,6 @@ int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, i
       throw TsatException(TSAT_ERR_UNSUPPORTED, "filter_mode must be 'none' or 'efficient'");
     ExploreLimitsC L{lim->n_max, lim->k_max, lim->k_multi, lim->time_limit_s};
     e.saturate(L, filter_mode, allow_self, nullptr, 0);
-    e.snap.valid = false;
     rep->iterations = e.report.iterations;
     rep->stop_reason = e.report.stop_reason;
     rep->prefilter_checks = e.report.prefilter_checks;
@@ -199,7 +223,6 @@ int tsat_ematch(tsat_engine* h, int32_t pattern, uint32_t* out_cls, uint32_t* ou
   GUARD(h, {
     Engine& e = *h->e;
     if (pattern < 0 || pattern >= (int)e.patterns.size()) throw TsatException(TSAT_ERR_ARG, "bad pattern id");
-    e.snap.valid = false;
     MatchSet ms;
     e.ematch_pattern(pattern, ms);
     *n = ms.n;
@@ -214,15 +237,11 @@ int tsat_ematch(tsat_engine* h, int32_t pattern, uint32_t* out_cls, uint32_t* ou
 }
 
 int tsat_break_cycles(tsat_engine* h, int64_t* added) {
-  GUARD(h, {
-    h->e->snap.valid = false;
-    *added = h->e->break_all_cycles(false, nullptr);
-  });
+  GUARD(h, *added = h->e->break_all_cycles(false, nullptr));
 }
 
 int tsat_dfs_cycles(tsat_engine* h, uint32_t* nodes, int64_t cap, uint32_t* off, int64_t off_cap, int64_t* ncycles) {
   GUARD(h, {
-    h->e->snap.valid = false;
     std::vector<std::vector<u32>> cyc;
     h->e->break_all_cycles(false, &cyc);
     *ncycles = (int64_t)cyc.size();
@@ -251,10 +270,7 @@ int tsat_costs(tsat_engine* h, int32_t mode, int32_t strict, int32_t ntab, const
 
 int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, uint32_t* sel_node, uint32_t* nsel,
                 double* root_best, int64_t* rounds) {
-  GUARD(h, {
-    h->e->snap.valid = false;
-    *root_best = h->e->greedy(cost_by_node, sel_cls, sel_node, nsel, rounds);
-  });
+  GUARD(h, *root_best = h->e->greedy(cost_by_node, sel_cls, sel_node, nsel, rounds));
 }
 
 int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launches, int32_t n, int32_t reset) {
@@ -267,6 +283,15 @@ int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launch
     }
     if (reset)
       for (int i = 0; i < KG_COUNT; i++) e.kstat[i] = KStat();
+  });
+}
+
+int tsat_debug_info(tsat_engine* h, int64_t* out, int32_t n) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    int64_t v[8] = {e.lv_n, e.lv_trimmed, e.snap.ncls, e.cg_ne, (int64_t)e.snap_id, (int64_t)e.filter_id,
+                    (int64_t)e.h.next_id, (int64_t)e.h.live};
+    for (int i = 0; i < n && i < 8; i++) out[i] = v[i];
   });
 }
 

@@ -81,7 +81,37 @@ KTimer::~KTimer() {
   e.nlaunch += launches;
 }
 
+void free_wave_bufs(WaveBufs* b);
+
+// return a pooled engine to the freshly-created state, keeping allocations
+void Engine::reset(bool analysis_) {
+  sync();
+  analysis = analysis_;
+  memset(&h, 0, sizeof(h));
+  push_counters();
+  CUDA_OK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
+  CUDA_OK(cudaMemsetAsync(tree_hc.p, 0xFF, (size_t)tree_hc_cap * sizeof(u32), s));
+  CUDA_OK(cudaMemsetAsync(tree_count.p, 0, sizeof(u32), s));
+  if (hc_cap) CUDA_OK(cudaMemsetAsync(hc.p, 0xFF, (size_t)hc_cap * sizeof(u32), s));
+  root = TSAT_NONE;
+  h_atoms.clear();
+  atom_names.clear();
+  patterns.clear();
+  rules.clear();
+  rule_names.clear();
+  matches.clear();
+  snap.valid = false;
+  reach.valid = false;
+  lv_snap = lv_filter = ~0ull;
+  costs_valid_for = TSAT_NONE;
+  for (int i = 0; i < KG_COUNT; i++) kstat[i] = KStat();
+  nlaunch = 0;
+  last_error.clear();
+  sync();
+}
+
 Engine::~Engine() {
+  if (wave) free_wave_bufs(wave);
   if (s) {
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
@@ -356,16 +386,18 @@ void Engine::add_terms(int ninstr, const Instr* prog, int nterm, const int32_t* 
     }
   }
   ensure_nodes(napp, nk);
-  DevBuf<Instr> dp;
-  dp.alloc(ninstr + 1);
-  DevBuf<int32_t> dl;
-  dl.alloc(nterm + 1);
-  DevBuf<u32> de, dout;
-  de.alloc(nenv + 1);
-  dout.alloc(nterm + 1);
+  DevBuf<Instr>& dp = sc.a_prog;
+  dp.ensure(ninstr + 1);
+  DevBuf<int32_t>& dl = sc.a_len;
+  dl.ensure(nterm + 1);
+  DevBuf<u32>& de = sc.a_env;
+  DevBuf<u32>& dout = sc.a_out;
+  de.ensure(nenv + 1);
+  dout.ensure(nterm + 1);
   CUDA_OK(cudaMemcpyAsync(dp.p, prog, ninstr * sizeof(Instr), cudaMemcpyHostToDevice, s));
   CUDA_OK(cudaMemcpyAsync(dl.p, term_len, nterm * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   if (nenv) CUDA_OK(cudaMemcpyAsync(de.p, env, nenv * sizeof(u32), cudaMemcpyHostToDevice, s));
+  snap.valid = false;
   k_seq_add_terms<<<1, 1, 0, s>>>(view(), dp.p, dl.p, nterm, de.p, dout.p);
   CUDA_OK(cudaMemcpyAsync(out_cls, dout.p, nterm * sizeof(u32), cudaMemcpyDeviceToHost, s));
   pull_counters();
@@ -381,6 +413,7 @@ u32 Engine::union_pair(u32 a, u32 b) {
   if (a >= h.next_id || b >= h.next_id) throw TsatException(TSAT_ERR_ARG, "unknown e-class id");
   DevBuf<u32>& o = scratch_u32[7];
   o.ensure(1);
+  snap.valid = false;
   k_seq_union<<<1, 1, 0, s>>>(view(), a, b, o.p);
   u32 r;
   CUDA_OK(cudaMemcpyAsync(&r, o.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -420,6 +453,7 @@ __global__ void k_clear_filter(G g, u32 n) {
 }
 
 void Engine::set_filter(int n, const u32* ids, int on) {
+  filter_id++;
   if (on == 2) {
     if (h.next_id) k_clear_filter<<<nblk(h.next_id), 256, 0, s>>>(view(), h.next_id);
     sync();
@@ -428,8 +462,8 @@ void Engine::set_filter(int n, const u32* ids, int on) {
   if (n <= 0) return;
   for (int i = 0; i < n; i++)
     if (ids[i] >= h.next_id) throw TsatException(TSAT_ERR_ARG, "filter id out of range");
-  DevBuf<u32> d;
-  d.alloc(n);
+  DevBuf<u32>& d = sc.a_ids;
+  d.ensure(n);
   CUDA_OK(cudaMemcpyAsync(d.p, ids, n * sizeof(u32), cudaMemcpyHostToDevice, s));
   k_set_filter<<<nblk(n), 256, 0, s>>>(view(), d.p, n, on);
   sync();
@@ -662,7 +696,9 @@ void Engine::build_snapshot() {
   dev_sort_pairs_u32(*this, opk.p, tmp.p, ids.p, snap.op_nodes.p, m, bits_for(na));
   snap.n_alloc = n;
   snap.ncls = ncls;
+  snap.n_atoms = na;
   snap.valid = true;
+  snap_id++;
   sync();
 }
 

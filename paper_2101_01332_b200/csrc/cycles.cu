@@ -1,20 +1,30 @@
-// Cycle filtering on the GPU (reference: pkg/src/tensorsat/cycles.py).
+// Cycle filtering and class-level graph passes on the GPU
+// (reference: pkg/src/tensorsat/cycles.py).
 //
-// * build_reach: the per-iteration descendants map (cycles.py:70-148) as a
-//   dense bitset over snapshot classes.  Classes are peeled in topological
-//   levels (Kahn trimming on live, unfiltered class edges); each level ORs
-//   its children's rows in one pass; classes left after trimming (on or above
-//   a cycle) are closed by sweeping to a fixpoint.
-// * break_all_cycles: the post-processing loop (cycles.py:172-245).  A level
-//   trim restricted to classes reachable from the root proves the common
-//   case "no live cycle" without a DFS; otherwise the exact lexicographic
-//   DFS runs on one GPU thread over the untrimmed region only (trimmed
-//   classes cannot lie on or lead to a cycle, so skipping them leaves the
-//   back-edge sequence unchanged), then resolves cycles by filter-listing
-//   their max node id, repeating passes until no cycle remains.
+// Class graph: class -> child classes through live, unfiltered e-nodes (CSR
+// plus reverse CSR), built from the snapshot CSR.  Three passes run as
+// cooperative persistent kernels (grid.sync() between levels, no host round
+// trips):
+//   * k_trim_coop  -- Kahn peeling from the sinks: level[c] = height of c in
+//                     the condensation-free part; classes never peeled lie on
+//                     or above a cycle.
+//   * k_bfs_coop   -- classes reachable from the root.
+//   * k_close_coop -- the descendants bitset (cycles.py:70-148) level by
+//                     level; untrimmed classes are closed by sweeping to a
+//                     fixpoint afterwards.
+// break_all_cycles (cycles.py:234-245): "no reachable class is untrimmed"
+// proves there is no live cycle below the root; otherwise the exact
+// lexicographic DFS (cycles.py:172-221) runs on one GPU thread over the
+// untrimmed region only (trimmed classes cannot lie on or lead to a cycle, so
+// skipping them keeps the back-edge sequence), then resolves cycles by
+// filter-listing their max node id, pass after pass.
+#include <cooperative_groups.h>
+
 #include <cub/cub.cuh>
 
 #include "engine.cuh"
+
+namespace cg = cooperative_groups;
 
 static inline unsigned nblk(u64 n, unsigned t = 256) {
   u64 b = (n + t - 1) / t;
@@ -23,18 +33,6 @@ static inline unsigned nblk(u64 n, unsigned t = 256) {
   return (unsigned)b;
 }
 #define GRID_STRIDE(i, n) for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < (n); i += (u64)gridDim.x * blockDim.x)
-
-struct ClassGraph {
-  u32 ncls = 0;
-  u64 nedge = 0;
-  DevBuf<u32> eoff;   // ncls + 1
-  DevBuf<u32> edst;   // dense child class per edge
-  DevBuf<u32> enode;  // node id that contributes the edge
-  DevBuf<u32> roff;   // reverse CSR
-  DevBuf<u32> rsrc;
-  DevBuf<u32> outdeg;
-  DevBuf<u32> level;  // trim round, TSAT_NONE = untrimmed
-};
 
 // per class: number of edges through live, unfiltered members
 __global__ void k_edge_count(G g, const u32* cls_off, const u32* cls_nodes, u32 ncls, u32* cnt) {
@@ -47,10 +45,11 @@ __global__ void k_edge_count(G g, const u32* cls_off, const u32* cls_nodes, u32 
     }
     cnt[i] = c;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[ncls] = 0;
 }
 
 __global__ void k_edge_fill(G g, const u32* cls_off, const u32* cls_nodes, const u32* cls_index, u32 ncls,
-                            const u32* eoff, u32* edst, u32* enode) {
+                            const u32* eoff, u32* edst, u32* esrc) {
   GRID_STRIDE(i, ncls) {
     u32 o = eoff[i];
     for (u32 k = cls_off[i]; k < cls_off[i + 1]; k++) {
@@ -58,119 +57,20 @@ __global__ void k_edge_fill(G g, const u32* cls_off, const u32* cls_nodes, const
       if (g.flags[m] & NF_FILT) continue;
       for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) {
         edst[o] = cls_index[uf_find_ro(g.parent, g.kids[j])];
-        enode[o] = m;
+        esrc[o] = (u32)i;
         o++;
       }
     }
   }
 }
 
-__global__ void k_edge_src(const u32* eoff, u32 ncls, u32* esrc) {
-  GRID_STRIDE(i, ncls) for (u32 e = eoff[i]; e < eoff[i + 1]; e++) esrc[e] = (u32)i;
-}
-
 __global__ void k_rhist(const u32* edst, u64 ne, u32* h) {
   GRID_STRIDE(e, ne) atomicAdd(&h[edst[e]], 1u);
 }
 
-__global__ void k_outdeg_init(const u32* eoff, u32 ncls, u32* outdeg, u32* level, u32* frontier,
-                              u32* nfront, const u8* mask) {
-  GRID_STRIDE(i, ncls) {
-    level[i] = TSAT_NONE;
-    if (mask && !mask[i]) continue;
-    u32 d = eoff[i + 1] - eoff[i];
-    outdeg[i] = d;
-    if (d == 0) {
-      level[i] = 0;
-      frontier[atomicAdd(nfront, 1u)] = (u32)i;
-    }
-  }
-}
-
-// restricted to mask (reachable set): edges into masked-out classes never
-// exist because the mask is closed under children.
-__global__ void k_trim_step(const u32* front, u32 nf, const u32* roff, const u32* rsrc, u32* outdeg,
-                            u32* level, u32 lvl, u32* next, u32* nnext, const u8* mask) {
-  GRID_STRIDE(t, nf) {
-    u32 j = front[t];
-    for (u32 k = roff[j]; k < roff[j + 1]; k++) {
-      u32 i = rsrc[k];
-      if (mask && !mask[i]) continue;
-      if (atomicSub(&outdeg[i], 1u) == 1u) {
-        level[i] = lvl;
-        next[atomicAdd(nnext, 1u)] = i;
-      }
-    }
-  }
-}
-
-static void build_class_graph(Engine& e, ClassGraph& cg) {
-  Snapshot& S = e.snap;
-  u32 n = S.ncls;
-  cg.ncls = n;
-  cg.eoff.ensure(n + 1);
-  DevBuf<u32>& cnt = e.scratch_u32[1];
-  cnt.ensure(n + 1);
-  k_edge_count<<<nblk(n), 256, 0, e.s>>>(e.view(), S.cls_off.p, S.cls_nodes.p, n, cnt.p);
-  CUDA_OK(cudaMemsetAsync(cnt.p + n, 0, sizeof(u32), e.s));
-  dev_exclusive_scan_u32(e, cnt.p, cg.eoff.p, n + 1);
-  u32 ne;
-  CUDA_OK(cudaMemcpyAsync(&ne, cg.eoff.p + n, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-  e.sync();
-  cg.nedge = ne;
-  cg.edst.ensure(ne + 1);
-  cg.enode.ensure(ne + 1);
-  k_edge_fill<<<nblk(n), 256, 0, e.s>>>(e.view(), S.cls_off.p, S.cls_nodes.p, S.cls_index.p, n, cg.eoff.p,
-                                        cg.edst.p, cg.enode.p);
-  // reverse CSR by stable sort of (dst, src)
-  DevBuf<u32> esrc, sdst;
-  esrc.alloc(ne + 1);
-  sdst.alloc(ne + 1);
-  cg.rsrc.ensure(ne + 1);
-  cg.roff.ensure(n + 1);
-  k_edge_src<<<nblk(n), 256, 0, e.s>>>(cg.eoff.p, n, esrc.p);
-  if (ne) dev_sort_pairs_u32(e, cg.edst.p, sdst.p, esrc.p, cg.rsrc.p, ne, bits_for(n));
-  CUDA_OK(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(u32), e.s));
-  k_rhist<<<nblk(ne), 256, 0, e.s>>>(cg.edst.p, ne, cnt.p);
-  dev_exclusive_scan_u32(e, cnt.p, cg.roff.p, n + 1);
-  cg.outdeg.ensure(n + 1);
-  cg.level.ensure(n + 1);
-}
-
-// Kahn trimming; returns number of levels and fills per-level lists
-static u32 trim(Engine& e, ClassGraph& cg, const u8* mask, std::vector<u32>& lvl_off, DevBuf<u32>& order,
-                u32& ntrimmed) {
-  u32 n = cg.ncls;
-  order.ensure(n + 1);
-  DevBuf<u32>& cntb = e.scratch_u32[2];
-  cntb.ensure(2);
-  CUDA_OK(cudaMemsetAsync(cntb.p, 0, sizeof(u32), e.s));
-  k_outdeg_init<<<nblk(n), 256, 0, e.s>>>(cg.eoff.p, n, cg.outdeg.p, cg.level.p, order.p, cntb.p, mask);
-  u32 nf;
-  CUDA_OK(cudaMemcpyAsync(&nf, cntb.p, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-  e.sync();
-  lvl_off.clear();
-  lvl_off.push_back(0);
-  u32 start = 0, lvl = 0;
-  while (nf) {
-    lvl_off.push_back(start + nf);
-    CUDA_OK(cudaMemsetAsync(cntb.p, 0, sizeof(u32), e.s));
-    k_trim_step<<<nblk(nf), 256, 0, e.s>>>(order.p + start, nf, cg.roff.p, cg.rsrc.p, cg.outdeg.p,
-                                           cg.level.p, lvl + 1, order.p + start + nf, cntb.p, mask);
-    u32 nn;
-    CUDA_OK(cudaMemcpyAsync(&nn, cntb.p, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-    e.sync();
-    start += nf;
-    nf = nn;
-    lvl++;
-  }
-  ntrimmed = start;
-  return lvl;
-}
-
-// one warp per class row: row[i] = OR_{i->j} (row[j] | bit j)
-__global__ void k_close_rows(const u32* list, u32 nl, const u32* eoff, const u32* edst, u32* bits, u32 words,
-                             u32* changed) {
+// fixpoint sweep over untrimmed classes
+__global__ void k_close_sweep(const u32* list, u32 nl, const u32* eoff, const u32* edst, u32* bits, u32 words,
+                              u32* changed) {
   u32 warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   u32 lane = threadIdx.x & 31;
   u32 nw = (gridDim.x * blockDim.x) >> 5;
@@ -179,62 +79,92 @@ __global__ void k_close_rows(const u32* list, u32 nl, const u32* eoff, const u32
     u32* row = bits + (u64)i * words;
     bool ch = false;
     for (u32 w = lane; w < words; w += 32) {
-      u32 acc = changed ? row[w] : 0u;
+      u32 acc = row[w];
       for (u32 e = eoff[i]; e < eoff[i + 1]; e++) {
         u32 j = edst[e];
         acc |= bits[(u64)j * words + w];
         if ((j >> 5) == w) acc |= 1u << (j & 31);
       }
-      if (changed) {
-        if (acc != row[w]) {
-          row[w] = acc;
-          ch = true;
-        }
-      } else {
+      if (acc != row[w]) {
         row[w] = acc;
+        ch = true;
       }
     }
-    if (changed && __any_sync(0xffffffffu, ch) && lane == 0) *changed = 1;
+    if (__any_sync(0xffffffffu, ch) && lane == 0) *changed = 1;
   }
 }
 
-__global__ void k_untrimmed(const u32* level, u32 n, u32* list, u32* cnt) {
-  GRID_STRIDE(i, n) if (level[i] == TSAT_NONE) list[atomicAdd(cnt, 1u)] = (u32)i;
+__global__ void k_untrimmed(const u32* level, u32 n, const u8* mask, u32* list, u32* cnt) {
+  GRID_STRIDE(i, n) if (level[i] == TSAT_NONE && (!mask || mask[i])) list[atomicAdd(cnt, 1u)] = (u32)i;
+}
+
+// ---------------------------------------------------------------- host helpers
+
+void build_class_graph(Engine& e) {
+  Snapshot& S = e.snap;
+  Scratch& X = e.sc;
+  u32 n = S.ncls;
+  X.cg_eoff.ensure(n + 1);
+  DevBuf<u32>& cnt = X.cg_outdeg;  // reused as count buffer here
+  cnt.ensure(n + 1);
+  k_edge_count<<<nblk(n), 256, 0, e.s>>>(e.view(), S.cls_off.p, S.cls_nodes.p, n, cnt.p);
+  dev_exclusive_scan_u32(e, cnt.p, X.cg_eoff.p, n + 1);
+  u32 ne;
+  CUDA_OK(cudaMemcpyAsync(&ne, X.cg_eoff.p + n, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+  e.sync();
+  e.cg_n = n;
+  e.cg_ne = ne;
+  X.cg_edst.ensure(ne + 1);
+  X.cg_esrc.ensure(ne + 1);
+  X.cg_sdst.ensure(ne + 1);
+  X.cg_rsrc.ensure(ne + 1);
+  X.cg_roff.ensure(n + 1);
+  k_edge_fill<<<nblk(n), 256, 0, e.s>>>(e.view(), S.cls_off.p, S.cls_nodes.p, S.cls_index.p, n, X.cg_eoff.p,
+                                        X.cg_edst.p, X.cg_esrc.p);
+  if (ne) dev_sort_pairs_u32(e, X.cg_edst.p, X.cg_sdst.p, X.cg_esrc.p, X.cg_rsrc.p, ne, bits_for(n));
+  CUDA_OK(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(u32), e.s));
+  k_rhist<<<nblk(ne), 256, 0, e.s>>>(X.cg_edst.p, ne, cnt.p);
+  dev_exclusive_scan_u32(e, cnt.p, X.cg_roff.p, n + 1);
+  X.cg_outdeg.ensure(n + 1);
+  X.cg_level.ensure(n + 1);
+}
+
+u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrimmed);
+u32 bfs_classes(Engine& e, u32 root, u32* mark, u32* queue);
+void close_levels(Engine& e, const std::vector<u32>& lo, u32 nl, u32* bits, u32 words);
+
+void Engine::ensure_levels() {
+  if (!snap.valid) build_snapshot();
+  if (lv_snap == snap_id && lv_filter == filter_id) return;
+  build_class_graph(*this);
+  lv_n = trim_levels(*this, nullptr, lv_off, lv_trimmed);
+  lv_snap = snap_id;
+  lv_filter = filter_id;
 }
 
 void Engine::build_reach() {
   if (!snap.valid) build_snapshot();
   KTimer kt(*this, KG_REACH, 0.0, 0);
-  ClassGraph cg;
-  build_class_graph(*this, cg);
-  u32 n = cg.ncls;
+  ensure_levels();
+  u32 n = cg_n;
   u32 words = (n + 31) / 32;
   u64 bytes = (u64)n * words * 4;
-  if (bytes > (u64)48 << 30)
-    throw TsatException(TSAT_ERR_UNSUPPORTED, "descendants bitset would exceed 48 GiB");
+  if (bytes > (u64)48 << 30) throw TsatException(TSAT_ERR_UNSUPPORTED, "descendants bitset would exceed 48 GiB");
   reach.bits.ensure((u64)n * words + 1);
   CUDA_OK(cudaMemsetAsync(reach.bits.p, 0, bytes, s));
-  std::vector<u32> lo;
-  DevBuf<u32> order;
-  u32 ntr = 0;
-  u32 nl = trim(*this, cg, nullptr, lo, order, ntr);
-  for (u32 l = 1; l < nl; l++) {  // level 0 rows stay empty
-    u32 a = lo[l], b = lo[l + 1];
-    k_close_rows<<<nblk((u64)(b - a) * 32, 256), 256, 0, s>>>(order.p + a, b - a, cg.eoff.p, cg.edst.p,
-                                                              reach.bits.p, words, nullptr);
-  }
+  u32 nl = lv_n, ntr = lv_trimmed;
+  if (nl > 1) close_levels(*this, lv_off, nl, reach.bits.p, words);
   if (ntr < n) {
-    DevBuf<u32> rest;
-    rest.alloc(n - ntr + 1);
-    DevBuf<u32>& c2 = scratch_u32[2];
-    c2.ensure(2);
-    CUDA_OK(cudaMemsetAsync(c2.p, 0, sizeof(u32), s));
-    k_untrimmed<<<nblk(n), 256, 0, s>>>(cg.level.p, n, rest.p, c2.p);
+    DevBuf<u32>& rest = sc.c_rest;
+    rest.ensure(n - ntr + 1);
+    DevBuf<u32>& c2 = sc.c_res;
+    CUDA_OK(cudaMemsetAsync(c2.p, 0, 2 * sizeof(u32), s));
+    k_untrimmed<<<nblk(n), 256, 0, s>>>(sc.cg_level.p, n, nullptr, rest.p, c2.p);
     u32 nr = n - ntr;
     while (true) {
       CUDA_OK(cudaMemsetAsync(c2.p + 1, 0, sizeof(u32), s));
-      k_close_rows<<<nblk((u64)nr * 32, 256), 256, 0, s>>>(rest.p, nr, cg.eoff.p, cg.edst.p, reach.bits.p,
-                                                           words, c2.p + 1);
+      k_close_sweep<<<nblk((u64)nr * 32, 256), 256, 0, s>>>(rest.p, nr, sc.cg_eoff.p, sc.cg_edst.p, reach.bits.p,
+                                                            words, c2.p + 1);
       u32 ch;
       CUDA_OK(cudaMemcpyAsync(&ch, c2.p + 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
       sync();
@@ -244,54 +174,25 @@ void Engine::build_reach() {
   reach.n = n;
   reach.words = words;
   reach.valid = true;
-  // closure traffic: every row written once, each edge reads its child's row
-  kt.bytes = 4.0 * words * ((double)n + (double)cg.nedge);
-  kt.launches = 4 + nl;
+  kt.bytes = 4.0 * words * ((double)n + (double)cg_ne);
+  kt.launches = 6;
   sync();
 }
 
 // ---------------------------------------------------------------- post-processing
 
-__global__ void k_bfs_init(u32* mark, u32 n, u32 root, u32* front, u32* nf) {
-  GRID_STRIDE(i, n) mark[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    mark[root] = 1;
-    front[0] = root;
-    *nf = 1;
-  }
-}
-
-__global__ void k_bfs_step(const u32* front, u32 nf, const u32* eoff, const u32* edst, u32* mark, u32* next,
-                           u32* nn) {
-  GRID_STRIDE(t, nf) {
-    u32 i = front[t];
-    for (u32 e = eoff[i]; e < eoff[i + 1]; e++) {
-      u32 j = edst[e];
-      if (mark[j] == 0 && atomicCAS(&mark[j], 0u, 1u) == 0u) next[atomicAdd(nn, 1u)] = j;
-    }
-  }
-}
-
-__global__ void k_mark_to_u8(const u32* m, u32 n, u8* out) {
-  GRID_STRIDE(i, n) out[i] = m[i] ? 1 : 0;
-}
-
-__global__ void k_count_cyclic(const u8* mark, const u32* level, u32 n, u32* cnt) {
-  GRID_STRIDE(i, n) if (mark[i] && level[i] == TSAT_NONE) atomicAdd(cnt, 1u);
-}
-
 struct DfsFrame {
-  u32 cls;    // dense class
-  u32 mpos;   // member cursor
-  u32 kpos;   // child cursor within member
+  u32 cls;
+  u32 mpos;
+  u32 kpos;
 };
 
-// Exact DFS pass of dfs_get_cycles (cycles.py:172-221) on one thread, then
-// the resolution loop of break_all_cycles (cycles.py:234-245).
+// Exact DFS pass of dfs_get_cycles (cycles.py:172-221) on one thread, then the
+// resolution loop of break_all_cycles (cycles.py:234-245) when ``resolve``.
 __global__ void k_dfs_cycles(G g, const u32* cls_off, const u32* cls_nodes, const u32* cls_index,
                              const u32* level, u32 root_dense, u8* color, u32* depth_of, DfsFrame* stack,
-                             u32* path, u32* cyc_nodes, u32 cyc_cap, u32* cyc_off, u32 cyc_off_cap,
-                             u32* out /* [ncycles, nnodes, overflow, filtered] */, int resolve) {
+                             u32* path, u32* cyc_nodes, u32 cyc_cap, u32* cyc_off, u32 cyc_off_cap, u32* out,
+                             int resolve) {
   if (threadIdx.x || blockIdx.x) return;
   u32 ncyc = 0, nnodes = 0;
   bool overflow = false;
@@ -318,7 +219,7 @@ __global__ void k_dfs_cycles(G g, const u32* cls_off, const u32* cls_nodes, cons
       }
       u32 ch = cls_index[uf_find_ro(g.parent, g.kids[ka + f.kpos])];
       f.kpos++;
-      if (level[ch] != TSAT_NONE) continue;  // trimmed: cannot reach a cycle
+      if (level[ch] != TSAT_NONE) continue;  // peeled: cannot reach a cycle
       u8 st = color[ch];
       if (st == 1) {
         u32 start = depth_of[ch];
@@ -369,68 +270,54 @@ __global__ void k_dfs_cycles(G g, const u32* cls_off, const u32* cls_nodes, cons
   out[3] = filtered;
 }
 
+__global__ void k_mark8(const u32* m, u32 n, u8* o) {
+  GRID_STRIDE(i, n) o[i] = m[i] ? 1 : 0;
+}
+
+__global__ void k_count_cyclic(const u8* mark, const u32* level, u32 n, u32* cnt) {
+  GRID_STRIDE(i, n) if (mark[i] && level[i] == TSAT_NONE) atomicAdd(cnt, 1u);
+}
+
 i64 Engine::break_all_cycles(bool precheck_only, std::vector<std::vector<u32>>* cycles_out) {
   if (root == TSAT_NONE) throw TsatException(TSAT_ERR_STATE, "e-graph has no root");
   if (!snap.valid) build_snapshot();
+  KTimer kt(*this, KG_CYCLES, 0.0, 0);
   u32 rc = find(root);
   u32 root_dense;
   CUDA_OK(cudaMemcpyAsync(&root_dense, snap.cls_index.p + rc, sizeof(u32), cudaMemcpyDeviceToHost, s));
   sync();
-  KTimer kt(*this, KG_CYCLES, 0.0, 0);
   i64 added = 0;
   u32 cyc_cap = 1 << 16, off_cap = 1 << 12;
   while (true) {
-    ClassGraph cg;
-    build_class_graph(*this, cg);
-    u32 n = cg.ncls;
-    DevBuf<u8> mark;
-    mark.alloc(n + 1);
-    DevBuf<u32> mark32;
-    mark32.alloc(n + 1);
-    DevBuf<u32> fa, fb;
-    fa.alloc(n + 1);
-    fb.alloc(n + 1);
-    DevBuf<u32>& c2 = scratch_u32[3];
-    c2.ensure(4);
-    k_bfs_init<<<nblk(n), 256, 0, s>>>(mark32.p, n, root_dense, fa.p, c2.p);
-    u32 nf = 1;
-    while (nf) {
-      CUDA_OK(cudaMemsetAsync(c2.p + 1, 0, sizeof(u32), s));
-      k_bfs_step<<<nblk(nf), 256, 0, s>>>(fa.p, nf, cg.eoff.p, cg.edst.p, mark32.p, fb.p, c2.p + 1);
-      CUDA_OK(cudaMemcpyAsync(&nf, c2.p + 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
-      sync();
-      std::swap(fa.p, fb.p);
-    }
-    k_mark_to_u8<<<nblk(n), 256, 0, s>>>(mark32.p, n, mark.p);
-    std::vector<u32> lo;
-    DevBuf<u32> order;
-    u32 ntr = 0;
-    trim(*this, cg, mark.p, lo, order, ntr);
-    CUDA_OK(cudaMemsetAsync(c2.p + 2, 0, sizeof(u32), s));
-    k_count_cyclic<<<nblk(n), 256, 0, s>>>(mark.p, cg.level.p, n, c2.p + 2);
+    ensure_levels();
+    u32 n = cg_n;
+    if (lv_trimmed == n) return added;  // the whole class graph peels: no live cycle anywhere
+    sc.c_mark.ensure(n + 1);
+    sc.c_mark32.ensure(n + 1);
+    sc.c_fa.ensure(n + 1);
+    sc.c_res.ensure(8);
+    bfs_classes(*this, root_dense, sc.c_mark32.p, sc.c_fa.p);
+    k_mark8<<<nblk(n), 256, 0, s>>>(sc.c_mark32.p, n, sc.c_mark.p);
+    CUDA_OK(cudaMemsetAsync(sc.c_res.p + 6, 0, sizeof(u32), s));
+    k_count_cyclic<<<nblk(n), 256, 0, s>>>(sc.c_mark.p, sc.cg_level.p, n, sc.c_res.p + 6);
     u32 ncyc_cls;
-    CUDA_OK(cudaMemcpyAsync(&ncyc_cls, c2.p + 2, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(&ncyc_cls, sc.c_res.p + 6, sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
     if (ncyc_cls == 0) return added;
     if (precheck_only) return -1;
-    // exact DFS over the untrimmed region
-    DevBuf<u8> color;
-    color.alloc(n + 1);
-    DevBuf<u32> depth_of, path, cyc_nodes, cyc_off, res;
-    DevBuf<DfsFrame> stack;
-    depth_of.alloc(n + 1);
-    path.alloc(n + 1);
-    stack.alloc(n + 1);
-    res.alloc(4);
+    sc.c_color.ensure(n + 1);
+    sc.c_depth.ensure(n + 1);
+    sc.c_path.ensure(n + 1);
+    sc.c_stack.ensure((u64)(n + 1) * sizeof(DfsFrame));
     u32 hres[4];
     while (true) {
-      cyc_nodes.ensure(cyc_cap);
-      cyc_off.ensure(off_cap);
-      CUDA_OK(cudaMemsetAsync(color.p, 0, n + 1, s));
-      k_dfs_cycles<<<1, 1, 0, s>>>(view(), snap.cls_off.p, snap.cls_nodes.p, snap.cls_index.p, cg.level.p,
-                                   root_dense, color.p, depth_of.p, stack.p, path.p, cyc_nodes.p, cyc_cap,
-                                   cyc_off.p, off_cap, res.p, cycles_out ? 0 : 1);
-      CUDA_OK(cudaMemcpyAsync(hres, res.p, sizeof(hres), cudaMemcpyDeviceToHost, s));
+      sc.c_cycn.ensure(cyc_cap);
+      sc.c_cyco.ensure(off_cap);
+      CUDA_OK(cudaMemsetAsync(sc.c_color.p, 0, n + 1, s));
+      k_dfs_cycles<<<1, 1, 0, s>>>(view(), snap.cls_off.p, snap.cls_nodes.p, snap.cls_index.p, sc.cg_level.p,
+                                   root_dense, sc.c_color.p, sc.c_depth.p, (DfsFrame*)sc.c_stack.p, sc.c_path.p,
+                                   sc.c_cycn.p, cyc_cap, sc.c_cyco.p, off_cap, sc.c_res.p, cycles_out ? 0 : 1);
+      CUDA_OK(cudaMemcpyAsync(hres, sc.c_res.p, sizeof(hres), cudaMemcpyDeviceToHost, s));
       sync();
       if (!hres[2]) break;
       cyc_cap *= 4;
@@ -438,14 +325,14 @@ i64 Engine::break_all_cycles(bool precheck_only, std::vector<std::vector<u32>>* 
     }
     if (cycles_out) {
       std::vector<u32> hn(hres[1]), ho(hres[0] + 1);
-      if (hres[1]) CUDA_OK(cudaMemcpyAsync(hn.data(), cyc_nodes.p, hres[1] * 4, cudaMemcpyDeviceToHost, s));
-      CUDA_OK(cudaMemcpyAsync(ho.data(), cyc_off.p, (hres[0] + 1) * 4, cudaMemcpyDeviceToHost, s));
+      if (hres[1]) CUDA_OK(cudaMemcpyAsync(hn.data(), sc.c_cycn.p, hres[1] * 4, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(cudaMemcpyAsync(ho.data(), sc.c_cyco.p, (hres[0] + 1) * 4, cudaMemcpyDeviceToHost, s));
       sync();
       for (u32 c = 0; c < hres[0]; c++) cycles_out->emplace_back(hn.begin() + ho[c], hn.begin() + ho[c + 1]);
-      // dfs_get_cycles semantics: report only, undo the resolution
       return (i64)hres[0];
     }
-    if (hres[0] == 0) return added;  // untrimmed region unreachable through live DFS order
+    if (hres[0] == 0) return added;
     added += hres[3];
+    if (hres[3]) filter_id++;
   }
 }

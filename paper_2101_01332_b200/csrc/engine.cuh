@@ -47,6 +47,10 @@ struct DevBuf {
     p = nullptr;
     cap = 0;
   }
+  void swap(DevBuf& o) {
+    std::swap(p, o.p);
+    std::swap(cap, o.cap);
+  }
   ~DevBuf() { release(); }
 };
 
@@ -117,6 +121,7 @@ struct DevStats {
 struct Snapshot {
   u32 n_alloc = 0;  // next_id when taken
   u32 ncls = 0;
+  u32 n_atoms = 0;  // op CSR is sized for this many atoms
   DevBuf<u32> cls_index;  // node id -> dense class index (TSAT_NONE if not a class)
   DevBuf<u32> cls_ids;    // dense -> class id
   DevBuf<u32> cls_off;    // dense -> member range
@@ -163,8 +168,32 @@ struct KTimer {  // records CUDA events on the engine stream around a kernel gro
   ~KTimer();
 };
 
+// persistent scratch buffers (grown on demand, never freed inside a run)
+struct Scratch {
+  // e-matching
+  DevBuf<u32> m_rc, m_rb, m_cnt, m_perm, m_perm2, m_key, m_key2, m_fl, m_pos;
+  // class graph / cycles / reach
+  DevBuf<u32> cg_eoff, cg_edst, cg_enode, cg_roff, cg_rsrc, cg_outdeg, cg_level, cg_esrc, cg_sdst;
+  DevBuf<u32> c_mark32, c_fa, c_fb, c_order, c_depth, c_path, c_cycn, c_cyco, c_res, c_rest, c_lvloff;
+  DevBuf<u8> c_mark, c_color;
+  DevBuf<unsigned char> c_stack;
+  // greedy / costs
+  DevBuf<double> g_c0, g_c1, g_upl, k_dv;
+  DevBuf<u32> g_n0, g_n1, g_flag, g_mark, g_fa, g_fb, g_oc, g_on, k_slots, g_eoff, g_edst, g_cnt;
+  DevBuf<char> k_keys;
+  DevBuf<i64> k_off;
+  // api
+  DevBuf<Instr> a_prog;
+  DevBuf<int32_t> a_len;
+  DevBuf<u32> a_env, a_out, a_ids;
+};
+
+struct WaveBufs;
+
 struct Engine {
   int device = 0;
+  Scratch sc;
+  WaveBufs* wave = nullptr;
   cudaStream_t s = nullptr;
   bool analysis = false;
   std::string last_error;
@@ -205,6 +234,14 @@ struct Engine {
   DevBuf<int> d_leaf;
 
   Snapshot snap;
+  u32 cg_n = 0, cg_ne = 0;  // current class graph (cycles.cu)
+  // level peel of the snapshot class graph (live, unfiltered edges), shared by
+  // the cycle check, the next iteration's descendants map and greedy
+  u64 snap_id = 0, filter_id = 0, lv_snap = ~0ull, lv_filter = ~0ull;
+  std::vector<u32> lv_off;
+  u32 lv_n = 0, lv_trimmed = 0;
+  void ensure_levels();
+  void reset(bool analysis_);
   Reach reach;
   DevBuf<u8> temp;  // cub scratch
   DevBuf<u32> scratch_u32[8];
@@ -214,7 +251,7 @@ struct Engine {
   std::vector<RuleStatsH> rstats;
   std::vector<i64> enodes_per_iter, alloc_per_iter, eclasses_per_iter;
   ExploreReportC report{};
-  std::vector<double> phase_ms = std::vector<double>(8, 0.0);
+  std::vector<double> phase_ms = std::vector<double>(16, 0.0);
   unsigned long long nlaunch = 0;  // kernels of ours launched (not CUB)
   KStat kstat[KG_COUNT];
   cudaEvent_t ev_pool[2] = {nullptr, nullptr};
@@ -254,6 +291,7 @@ struct Engine {
 
   // exploration
   bool seq_changed = false, seq_stop = false;
+  bool force_seq = false;  // debug: exact sequential path only
   std::vector<std::string> rule_names;
   void apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P);
   void saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self, const int* active_rule_mask,

@@ -342,7 +342,7 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
   std::vector<int> multi, single;
   for (size_t i = 0; i < rules.size(); i++) (rules[i].nsrc > 1 ? multi : single).push_back((int)i);
   int stop = 0;  // iter-limit
-  for (int q = 0; q < 8; q++) phase_ms[q] = 0.0;
+  for (int q = 0; q < 16; q++) phase_ms[q] = 0.0;
   auto tick = [&](int ph, double& t) {
     sync();
     double n2 = now_s();
@@ -413,6 +413,13 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
   report.time_s = now_s() - t0;
 }
 
+void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P);
+
 void Engine::apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P) {
-  run_rule_seq(ri, filter_mode, allow_self, n_max, 0, P);
+  const HRule& hr = rules[ri];
+  int R = 0;
+  for (auto& t : hr.targets)
+    for (auto& in : t) R += in.kind == I_APP;
+  if (hr.nsrc <= 2 && R <= 32 && !force_seq) run_rule_wave(*this, ri, filter_mode, allow_self, n_max, P);
+  else run_rule_seq(ri, filter_mode, allow_self, n_max, 0, P);
 }

@@ -12,10 +12,14 @@
 //   |total - cur| <= 1e-15 with a smaller id.  Child totals are summed in
 //   child order.  Then a BFS over chosen nodes gives the reached selection
 //   (extract.py:74-91).
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <cstring>
 
 #include "engine.cuh"
+
+namespace cg = cooperative_groups;
 
 static inline unsigned nblk(u64 n, unsigned t = 256) {
   u64 b = (n + t - 1) / t;
@@ -328,10 +332,10 @@ void Engine::costs(int mode, int strict, int ntab, const char* keys, const i64* 
                    double* out) {
   if (!analysis) throw TsatException(TSAT_ERR_STATE, "egraph_costs needs the tensor analysis");
   u32 n = h.next_id;
-  DevBuf<char> dk;
-  DevBuf<i64> doff;
-  DevBuf<double> dv;
-  DevBuf<u32> dslots;
+  DevBuf<char>& dk = sc.k_keys;
+  DevBuf<i64>& doff = sc.k_off;
+  DevBuf<double>& dv = sc.k_dv;
+  DevBuf<u32>& dslots = sc.k_slots;
   CostTab ct;
   memset(&ct, 0, sizeof(ct));
   ct.mode = mode;
@@ -349,10 +353,10 @@ void Engine::costs(int mode, int strict, int ntab, const char* keys, const i64* 
       while (slots[s_] != TSAT_NONE) s_ = (s_ + 1) & (cap - 1);
       slots[s_] = e;
     }
-    dk.alloc(nbytes + 1);
-    doff.alloc(ntab + 1);
-    dv.alloc(ntab);
-    dslots.alloc(cap);
+    dk.ensure(nbytes + 1);
+    doff.ensure(ntab + 1);
+    dv.ensure(ntab);
+    dslots.ensure(cap);
     CUDA_OK(cudaMemcpyAsync(dk.p, keys, nbytes, cudaMemcpyHostToDevice, s));
     CUDA_OK(cudaMemcpyAsync(doff.p, key_off, (ntab + 1) * sizeof(i64), cudaMemcpyHostToDevice, s));
     CUDA_OK(cudaMemcpyAsync(dv.p, vals, ntab * sizeof(double), cudaMemcpyHostToDevice, s));
@@ -376,6 +380,52 @@ void Engine::costs(int mode, int strict, int ntab, const char* keys, const i64* 
 
 // ---------------------------------------------------------------- greedy
 
+__global__ void k_untrimmed_g(const u32* level, u32 n, u32* list, u32* cnt) {
+  GRID_STRIDE(i, n) if (level[i] == TSAT_NONE) list[atomicAdd(cnt, 1u)] = (u32)i;
+}
+
+void build_class_graph(Engine& e);
+u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrimmed);
+u32 bfs_classes(Engine& e, u32 root, u32* mark, u32* queue);
+u32 bfs_graph(Engine& e, const u32* eoff, const u32* edst, u32 n, u32 root, u32* mark, u32* queue);
+
+__global__ void k_sel_count(G g, const u32* bn, u32 C, u32* cnt) {
+  GRID_STRIDE(i, C) {
+    u32 m = bn[i];
+    cnt[i] = m == TSAT_NONE ? 0u : g.koff[m + 1] - g.koff[m];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[C] = 0;
+}
+
+__global__ void k_sel_fill(G g, const u32* bn, const u32* cls_index, u32 C, const u32* eoff, u32* edst) {
+  GRID_STRIDE(i, C) {
+    u32 m = bn[i];
+    if (m == TSAT_NONE) continue;
+    u32 o = eoff[i];
+    for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) edst[o++] = cls_index[uf_find_ro(g.parent, g.kids[j])];
+  }
+}
+
+__global__ void k_sel_missing(const u32* q, u32 k, const u32* bn, u32* flag) {
+  GRID_STRIDE(t, k) if (bn[q[t]] == TSAT_NONE) *flag = 1;
+}
+
+__device__ __forceinline__ void greedy_fold(const G& g, const u32* cls_off, const u32* cls_nodes,
+                                            const u32* cls_index, u32 i, const double* cost, const double* pc,
+                                            double& bc, u32& bn) {
+  for (u32 k = cls_off[i]; k < cls_off[i + 1]; k++) {
+    u32 m = cls_nodes[k];
+    if (g.flags[m] & NF_FILT) continue;
+    double tot = cost[m];
+    for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) tot += pc[cls_index[uf_find_ro(g.parent, g.kids[j])]];
+    if (isinf(tot)) continue;
+    if (tot < bc - 1e-15 || (fabs(tot - bc) <= 1e-15 && (bn == TSAT_NONE || m < bn))) {
+      bc = tot;
+      bn = m;
+    }
+  }
+}
+
 __global__ void k_greedy_init(double* bc, u32* bn, u32 n) {
   GRID_STRIDE(i, n) {
     bc[i] = INFINITY;
@@ -383,52 +433,132 @@ __global__ void k_greedy_init(double* bc, u32* bn, u32 n) {
   }
 }
 
-__global__ void k_greedy_round(G g, const u32* cls_off, const u32* cls_nodes, const u32* cls_index, u32 ncls,
-                               const double* cost, const double* pc, const u32* pn, double* nc, u32* nn,
-                               u32* changed) {
-  GRID_STRIDE(i, ncls) {
-    double bc = pc[i];
-    u32 bn = pn[i];
-    for (u32 k = cls_off[i]; k < cls_off[i + 1]; k++) {
-      u32 m = cls_nodes[k];
-      if (g.flags[m] & NF_FILT) continue;
-      double tot = cost[m];
-      for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++)
-        tot += pc[cls_index[uf_find_ro(g.parent, g.kids[j])]];
-      if (isinf(tot)) continue;
-      if (tot < bc - 1e-15 || (fabs(tot - bc) <= 1e-15 && (bn == TSAT_NONE || m < bn))) {
-        bc = tot;
-        bn = m;
+// member total (cost + child bests in child order), inf when filtered
+__device__ __forceinline__ double member_total(const G& g, u32 m, const u32* cls_index, const double* cost,
+                                               const double* pc) {
+  if (g.flags[m] & NF_FILT) return NAN;
+  double tot = cost[m];
+  for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) tot += pc[cls_index[uf_find_ro(g.parent, g.kids[j])]];
+  return tot;
+}
+
+// one warp per class: lanes compute member totals, lane 0 folds them in id
+// order with the reference tie rule (extract.py:145-152)
+__device__ __forceinline__ void warp_fold_class(const G& g, const u32* cls_off, const u32* cls_nodes,
+                                                const u32* cls_index, u32 i, const double* cost, double* bc,
+                                                u32* bn, double* stot, u32 lane) {
+  u32 a = cls_off[i], b = cls_off[i + 1];
+  double c = INFINITY;
+  u32 n = TSAT_NONE;
+  for (u32 base = a; base < b; base += 32) {
+    u32 k = base + lane;
+    double t = k < b ? member_total(g, cls_nodes[k], cls_index, cost, bc) : NAN;
+    stot[lane] = t;
+    __syncwarp();
+    if (lane == 0) {
+      u32 lim = b - base < 32 ? b - base : 32;
+      for (u32 q = 0; q < lim; q++) {
+        double tot = stot[q];
+        if (isnan(tot) || isinf(tot)) continue;
+        u32 m = cls_nodes[base + q];
+        if (tot < c - 1e-15 || (fabs(tot - c) <= 1e-15 && (n == TSAT_NONE || m < n))) {
+          c = tot;
+          n = m;
+        }
       }
     }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    bc[i] = c;
+    bn[i] = n;
+  }
+}
+
+// classes in peel order: children are final when a class is folded.
+// Thin levels [l0, l1) in one CTA (a warp per class); a wide level as a grid launch.
+__global__ void __launch_bounds__(1024) k_greedy_levels(G g, const u32* cls_off, const u32* cls_nodes,
+                                                        const u32* cls_index, const u32* order, const u32* lvl_off,
+                                                        u32 l0, u32 l1, const double* cost, double* bc, u32* bn) {
+  __shared__ double stot[32][32];
+  u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (u32 l = l0; l < l1; l++) {
+    for (u32 t = lvl_off[l] + w; t < lvl_off[l + 1]; t += 32)
+      warp_fold_class(g, cls_off, cls_nodes, cls_index, order[t], cost, bc, bn, stot[w], lane);
+    __syncthreads();
+  }
+}
+
+__global__ void k_greedy_level_wide(G g, const u32* cls_off, const u32* cls_nodes, const u32* cls_index,
+                                    const u32* order, u32 a, u32 b, const double* cost, double* bc, u32* bn) {
+  __shared__ double stot[8][32];
+  u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 t = warp; t < b - a; t += nw)
+    warp_fold_class(g, cls_off, cls_nodes, cls_index, order[a + t], cost, bc, bn, stot[w], lane);
+}
+
+// Jacobi round over the classes left on cycles
+__global__ void k_greedy_round(G g, const u32* cls_off, const u32* cls_nodes, const u32* cls_index,
+                               const u32* list, u32 nl, const double* cost, const double* pc, const u32* pn,
+                               double* nc, u32* nn, u32* changed) {
+  GRID_STRIDE(t, nl) {
+    u32 i = list[t];
+    double bc = pc[i];
+    u32 bn = pn[i];
+    greedy_fold(g, cls_off, cls_nodes, cls_index, i, cost, pc, bc, bn);
     nc[i] = bc;
     nn[i] = bn;
     if (bn != pn[i] || !(bc == pc[i])) *changed = 1;
   }
 }
 
-__global__ void k_sel_step(G g, const u32* front, u32 nf, const u32* bn, const u32* cls_index, u32* mark,
-                           u32* next, u32* nn, u32* missing) {
-  GRID_STRIDE(t, nf) {
-    u32 i = front[t];
-    u32 m = bn[i];
-    if (m == TSAT_NONE) {
-      *missing = 1;
-      continue;
-    }
-    for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) {
-      u32 c = cls_index[uf_find_ro(g.parent, g.kids[j])];
-      if (mark[c] == 0 && atomicCAS(&mark[c], 0u, 1u) == 0u) next[atomicAdd(nn, 1u)] = c;
-    }
+__global__ void k_copy_list(const u32* list, u32 nl, const double* sc_, const u32* sn, double* dc, u32* dn) {
+  GRID_STRIDE(t, nl) {
+    u32 i = list[t];
+    dc[i] = sc_[i];
+    dn[i] = sn[i];
   }
 }
 
-__global__ void k_sel_collect(const u32* mark, const u32* cls_ids, const u32* bn, u32 n, u32* oc, u32* on, u32* cnt) {
-  GRID_STRIDE(i, n) {
-    if (!mark[i]) continue;
-    u32 k = atomicAdd(cnt, 1u);
-    oc[k] = cls_ids[i];
-    on[k] = bn[i];
+// reached selection (extract.py:74-91): BFS over chosen nodes from the root
+__global__ void k_sel_coop(G g, const u32* cls_index, const u32* bn, u32 n, u32 root, u32* mark, u32* queue,
+                           u32* ctl) {
+  cg::grid_group grid = cg::this_grid();
+  GRID_STRIDE(i, n) mark[i] = 0;
+  grid.sync();
+  if (grid.thread_rank() == 0) {
+    mark[root] = 1;
+    queue[0] = root;
+    ctl[0] = 1;
+  }
+  grid.sync();
+  u32 start = 0, end = 1;
+  while (start < end) {
+    for (u64 t = start + grid.thread_rank(); t < end; t += grid.size()) {
+      u32 i = queue[t];
+      u32 m = bn[i];
+      if (m == TSAT_NONE) {
+        ctl[1] = 1;
+        continue;
+      }
+      for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) {
+        u32 c = cls_index[uf_find_ro(g.parent, g.kids[j])];
+        if (mark[c] == 0 && atomicCAS(&mark[c], 0u, 1u) == 0u) queue[atomicAdd(&ctl[0], 1u)] = c;
+      }
+    }
+    grid.sync();
+    start = end;
+    end = ((volatile u32*)ctl)[0];
+    grid.sync();
+  }
+}
+
+__global__ void k_sel_collect(const u32* queue, u32 k, const u32* cls_ids, const u32* bn, u32* oc, u32* on) {
+  GRID_STRIDE(t, k) {
+    u32 i = queue[t];
+    oc[t] = cls_ids[i];
+    on[t] = bn[i];
   }
 }
 
@@ -436,78 +566,105 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
   if (root == TSAT_NONE) throw TsatException(TSAT_ERR_STATE, "e-graph has no root");
   if (!snap.valid) build_snapshot();
   u32 n = h.next_id, C = snap.ncls;
-  DevBuf<double> upl;
+  DevBuf<double>& upl = sc.g_upl;
   const double* cost = d_costs.p;
   if (cost_by_node) {
-    upl.alloc(n + 1);
+    upl.ensure(n + 1);
     CUDA_OK(cudaMemcpyAsync(upl.p, cost_by_node, n * sizeof(double), cudaMemcpyHostToDevice, s));
     cost = upl.p;
   } else if (costs_valid_for != n) {
     throw TsatException(TSAT_ERR_STATE, "device cost vector is stale; recompute egraph_costs");
   }
-  DevBuf<double> c0, c1;
-  DevBuf<u32> n0, n1, flag;
-  c0.alloc(C + 1);
-  c1.alloc(C + 1);
-  n0.alloc(C + 1);
-  n1.alloc(C + 1);
-  flag.alloc(4);
+  KTimer kt(*this, KG_GREEDY, 0.0, 0);
+  DevBuf<double>& c0 = sc.g_c0;
+  DevBuf<double>& c1 = sc.g_c1;
+  DevBuf<u32>& n0 = sc.g_n0;
+  DevBuf<u32>& n1 = sc.g_n1;
+  DevBuf<u32>& flag = sc.g_flag;
+  c0.ensure(C + 1);
+  c1.ensure(C + 1);
+  n0.ensure(C + 1);
+  n1.ensure(C + 1);
+  flag.ensure(4);
+  ensure_levels();
+  const std::vector<u32>& lo = lv_off;
+  u32 ntr = lv_trimmed;
+  u32 nl = lv_n;
   k_greedy_init<<<nblk(C), 256, 0, s>>>(c0.p, n0.p, C);
-  i64 r = 0;
-  while (true) {
-    r++;
-    CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
-    {
-      // per round: 16 N + 12 A + 12 C
-      KTimer kt(*this, KG_GREEDY, 16.0 * h.live + 12.0 * h.nkids + 12.0 * C, 1);
-      k_greedy_round<<<nblk(C, 128), 128, 0, s>>>(view(), snap.cls_off.p, snap.cls_nodes.p, snap.cls_index.p, C,
-                                                 cost, c0.p, n0.p, c1.p, n1.p, flag.p);
+  G gv = view();
+  const u32 *co = snap.cls_off.p, *cn = snap.cls_nodes.p, *ci = snap.cls_index.p, *ord = sc.c_order.p,
+            *lvl = sc.c_lvloff.p;
+  for (u32 l = 0; l < nl;) {
+    if (lo[l + 1] - lo[l] > 16384) {
+      k_greedy_level_wide<<<nblk((u64)(lo[l + 1] - lo[l]) * 32, 256), 256, 0, s>>>(gv, co, cn, ci, ord, lo[l],
+                                                                                    lo[l + 1], cost, c0.p, n0.p);
+      l++;
+      continue;
     }
-    u32 ch;
-    CUDA_OK(cudaMemcpyAsync(&ch, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
-    sync();
-    std::swap(c0.p, c1.p);
-    std::swap(n0.p, n1.p);
-    if (!ch) break;
+    u32 l1 = l;
+    while (l1 < nl && lo[l1 + 1] - lo[l1] <= 16384) l1++;
+    k_greedy_levels<<<1, 1024, 0, s>>>(gv, co, cn, ci, ord, lvl, l, l1, cost, c0.p, n0.p);
+    l = l1;
   }
+  i64 r = 1;
+  if (ntr < C) {
+    DevBuf<u32>& rest = sc.c_rest;
+    rest.ensure(C - ntr + 1);
+    CUDA_OK(cudaMemsetAsync(flag.p, 0, 2 * sizeof(u32), s));
+    k_untrimmed_g<<<nblk(C), 256, 0, s>>>(sc.cg_level.p, C, rest.p, flag.p + 1);
+    u32 nr = C - ntr;
+    while (true) {
+      r++;
+      CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
+      k_greedy_round<<<nblk(nr, 128), 128, 0, s>>>(view(), co, cn, ci, rest.p, nr, cost, c0.p, n0.p, c1.p, n1.p,
+                                                   flag.p);
+      k_copy_list<<<nblk(nr), 256, 0, s>>>(rest.p, nr, c1.p, n1.p, c0.p, n0.p);
+      u32 ch;
+      CUDA_OK(cudaMemcpyAsync(&ch, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+      sync();
+      if (!ch) break;
+    }
+  }
+  kt.bytes = 16.0 * h.live + 12.0 * h.nkids + 12.0 * C;
+  kt.launches = 2;
   *rounds = r;
   u32 rc = find(root);
   u32 rd;
   CUDA_OK(cudaMemcpyAsync(&rd, snap.cls_index.p + rc, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  double rcost;
   sync();
+  double rcost;
   CUDA_OK(cudaMemcpyAsync(&rcost, c0.p + rd, sizeof(double), cudaMemcpyDeviceToHost, s));
   sync();
   if (std::isinf(rcost)) throw TsatException(TSAT_ERR_NO_FINITE, "every root selection has infinite cost");
-  DevBuf<u32> mark;
-  DevBuf<u32> fa, fb;
-  mark.alloc(C + 1);
-  fa.alloc(C + 1);
-  fb.alloc(C + 1);
-  CUDA_OK(cudaMemsetAsync(mark.p, 0, (C + 1) * sizeof(u32), s));
-  u32 one = 1;
-  CUDA_OK(cudaMemcpyAsync(mark.p + rd, &one, sizeof(u32), cudaMemcpyHostToDevice, s));
-  CUDA_OK(cudaMemcpyAsync(fa.p, &rd, sizeof(u32), cudaMemcpyHostToDevice, s));
-  u32 nf = 1;
-  while (nf) {
-    CUDA_OK(cudaMemsetAsync(flag.p, 0, 2 * sizeof(u32), s));
-    k_sel_step<<<nblk(nf), 256, 0, s>>>(view(), fa.p, nf, n0.p, snap.cls_index.p, mark.p, fb.p, flag.p,
-                                        flag.p + 1);
-    u32 hf[2];
-    CUDA_OK(cudaMemcpyAsync(hf, flag.p, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  DevBuf<u32>& mark = sc.g_mark;
+  DevBuf<u32>& q = sc.g_fa;
+  mark.ensure(C + 1);
+  q.ensure(C + 1);
+  // selection graph: class -> child classes of its chosen node only
+  {
+    DevBuf<u32>& cnt = sc.g_cnt;
+    cnt.ensure(C + 1);
+    sc.g_eoff.ensure(C + 1);
+    k_sel_count<<<nblk(C), 256, 0, s>>>(gv, n0.p, C, cnt.p);
+    dev_exclusive_scan_u32(*this, cnt.p, sc.g_eoff.p, C + 1);
+    u32 ne;
+    CUDA_OK(cudaMemcpyAsync(&ne, sc.g_eoff.p + C, sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
-    if (hf[1]) throw TsatException(TSAT_ERR_STATE, "no selected node covers a reached e-class");
-    nf = hf[0];
-    std::swap(fa.p, fb.p);
+    sc.g_edst.ensure(ne + 1);
+    k_sel_fill<<<nblk(C), 256, 0, s>>>(gv, n0.p, ci, C, sc.g_eoff.p, sc.g_edst.p);
   }
-  DevBuf<u32> oc, on;
-  oc.alloc(C + 1);
-  on.alloc(C + 1);
+  u32 k = bfs_graph(*this, sc.g_eoff.p, sc.g_edst.p, C, rd, mark.p, q.p);
   CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
-  k_sel_collect<<<nblk(C), 256, 0, s>>>(mark.p, snap.cls_ids.p, n0.p, C, oc.p, on.p, flag.p);
-  u32 k;
-  CUDA_OK(cudaMemcpyAsync(&k, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  k_sel_missing<<<nblk(k), 256, 0, s>>>(q.p, k, n0.p, flag.p);
+  u32 miss;
+  CUDA_OK(cudaMemcpyAsync(&miss, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
   sync();
+  if (miss) throw TsatException(TSAT_ERR_STATE, "no selected node covers a reached e-class");
+  DevBuf<u32>& oc = sc.g_oc;
+  DevBuf<u32>& on = sc.g_on;
+  oc.ensure(C + 1);
+  on.ensure(C + 1);
+  k_sel_collect<<<nblk(k), 256, 0, s>>>(q.p, k, snap.cls_ids.p, n0.p, oc.p, on.p);
   CUDA_OK(cudaMemcpyAsync(sel_cls, oc.p, k * sizeof(u32), cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaMemcpyAsync(sel_node, on.p, k * sizeof(u32), cudaMemcpyDeviceToHost, s));
   sync();

@@ -1,0 +1,302 @@
+// Level engine: Kahn peeling, BFS, level-ordered closure and greedy folds on
+// the class graph, with hybrid execution.  E-graphs from rewrite rules are
+// deep and thin (associativity chains give thousands of levels of a few
+// classes each), so a level-synchronous algorithm is barrier-bound: thin
+// levels run inside ONE 1024-thread CTA with __syncthreads(), wide levels
+// (> LV_WIDE classes) run on the whole GPU as cooperative kernels with
+// grid.sync().  The host only switches between the two when a frontier
+// crosses the threshold.
+#include <cooperative_groups.h>
+
+#include "engine.cuh"
+
+namespace cg = cooperative_groups;
+
+#define LV_WIDE 16384u
+#define LV_BLOCK 1024
+
+static inline unsigned nblk(u64 n, unsigned t = 256) {
+  u64 b = (n + t - 1) / t;
+  if (b < 1) b = 1;
+  if (b > 148ull * 64) b = 148ull * 64;
+  return (unsigned)b;
+}
+#define GRID_STRIDE(i, n) for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < (n); i += (u64)gridDim.x * blockDim.x)
+
+// ctl layout: [0] tail, [1] level, [2] start, [3] end, [4] done, [5] overflow flag
+struct Frontier {
+  const u32* eoff;  // forward CSR (BFS) or outdeg source (trim)
+  const u32* edst;
+  const u32* roff;  // reverse CSR (trim)
+  const u32* rsrc;
+  const u8* mask;
+  u32* outdeg;
+  u32* level;
+  u32* order;  // peel order / BFS queue
+  u32* lvl_off;
+  u32* mark;
+  u32 n;
+  int bfs;  // 1 = BFS from order[0], 0 = trim
+};
+
+#define HEAVY 32u
+
+__device__ __forceinline__ void frontier_edge(const Frontier& F, u32 e, u32 lvl, u32* tail) {
+  if (F.bfs) {
+    u32 k = F.edst[e];
+    if (F.mark[k] == 0 && atomicCAS(&F.mark[k], 0u, 1u) == 0u) F.order[atomicAdd(tail, 1u)] = k;
+  } else {
+    u32 i = F.rsrc[e];
+    if (F.mask && !F.mask[i]) return;
+    if (atomicSub(&F.outdeg[i], 1u) == 1u) {
+      F.level[i] = lvl + 1;
+      F.order[atomicAdd(tail, 1u)] = i;
+    }
+  }
+}
+
+__device__ __forceinline__ void edge_range(const Frontier& F, u32 j, u32& a, u32& b) {
+  if (F.bfs) {
+    a = F.eoff[j];
+    b = F.eoff[j + 1];
+  } else {
+    a = F.roff[j];
+    b = F.roff[j + 1];
+  }
+}
+
+__global__ void k_frontier_init(Frontier F, u32* ctl, u32 root) {
+  GRID_STRIDE(i, F.n) {
+    if (F.bfs) {
+      F.mark[i] = (u32)(i == root);
+      continue;
+    }
+    F.level[i] = TSAT_NONE;
+    if (F.mask && !F.mask[i]) continue;
+    u32 d = F.eoff[i + 1] - F.eoff[i];
+    F.outdeg[i] = d;
+    if (d == 0) {
+      F.level[i] = 0;
+      F.order[atomicAdd(&ctl[0], 1u)] = (u32)i;
+    }
+  }
+  if (F.bfs && blockIdx.x == 0 && threadIdx.x == 0) {
+    F.order[0] = root;
+    ctl[0] = 1;
+  }
+}
+
+__global__ void k_frontier_start(u32* ctl, u32* lvl_off) {
+  ctl[1] = 0;
+  ctl[2] = 0;
+  ctl[3] = ctl[0];
+  ctl[4] = 0;
+  if (lvl_off) {
+    lvl_off[0] = 0;
+    lvl_off[1] = ctl[0];
+  }
+}
+
+// thin levels inside one CTA; exits when a frontier gets wide.  Vertices with
+// more than HEAVY edges are queued and their edge lists are swept by the whole
+// CTA (hub classes such as shared literals have thousands of parents).
+__global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ctl) {
+  __shared__ u32 s_start, s_end, s_lvl, s_nheavy;
+  __shared__ u32 s_heavy[LV_BLOCK];
+  if (threadIdx.x == 0) {
+    s_start = ctl[2];
+    s_end = ctl[3];
+    s_lvl = ctl[1];
+  }
+  __syncthreads();
+  while (true) {
+    u32 start = s_start, end = s_end, lvl = s_lvl;
+    if (start >= end) {
+      if (threadIdx.x == 0) ctl[4] = 1;
+      break;
+    }
+    if (end - start > LV_WIDE) break;
+    for (u32 t0 = start; t0 < end; t0 += blockDim.x) {
+      if (threadIdx.x == 0) s_nheavy = 0;
+      __syncthreads();
+      u32 t = t0 + threadIdx.x;
+      if (t < end) {
+        u32 j = F.order[t], a, b;
+        edge_range(F, j, a, b);
+        if (b - a > HEAVY) s_heavy[atomicAdd(&s_nheavy, 1u)] = j;
+        else
+          for (u32 e = a; e < b; e++) frontier_edge(F, e, lvl, &ctl[0]);
+      }
+      __syncthreads();
+      for (u32 h = 0; h < s_nheavy; h++) {
+        u32 a, b;
+        edge_range(F, s_heavy[h], a, b);
+        for (u32 e = a + threadIdx.x; e < b; e += blockDim.x) frontier_edge(F, e, lvl, &ctl[0]);
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      __threadfence_block();
+      u32 ne = ((volatile u32*)ctl)[0];
+      s_start = end;
+      s_end = ne;
+      s_lvl = lvl + 1;
+      if (F.lvl_off) F.lvl_off[lvl + 2] = ne;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ctl[1] = s_lvl;
+    ctl[2] = s_start;
+    ctl[3] = s_end;
+  }
+}
+
+// wide levels on the whole GPU; exits when the frontier gets thin again
+__global__ void k_frontier_grid(Frontier F, u32* ctl) {
+  cg::grid_group grid = cg::this_grid();
+  u32 start = ctl[2], end = ctl[3], lvl = ctl[1];
+  u32 lane = threadIdx.x & 31;
+  u64 warp = grid.thread_rank() >> 5, nwarp = grid.size() >> 5;
+  while (start < end && end - start > LV_WIDE / 4) {
+    // one warp per frontier vertex: edge lists are swept 32-wide
+    for (u64 t = start + warp; t < end; t += nwarp) {
+      u32 a, b;
+      edge_range(F, F.order[t], a, b);
+      for (u32 e = a + lane; e < b; e += 32) frontier_edge(F, e, lvl, &ctl[0]);
+    }
+    grid.sync();
+    u32 ne = ((volatile u32*)ctl)[0];
+    if (grid.thread_rank() == 0 && F.lvl_off) F.lvl_off[lvl + 2] = ne;
+    start = end;
+    end = ne;
+    lvl++;
+    grid.sync();
+  }
+  if (grid.thread_rank() == 0) {
+    ctl[1] = lvl;
+    ctl[2] = start;
+    ctl[3] = end;
+    if (start >= end) ctl[4] = 1;
+  }
+}
+
+static int coop_blocks(Engine& e, const void* fn, int threads) {
+  int nsm = 0, per = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, e.device));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, 0));
+  if (per < 1) per = 1;
+  return nsm * std::min(per, 2);
+}
+
+// runs the frontier to completion; returns (levels, total processed)
+static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& total) {
+  DevBuf<u32>& ctl = e.sc.c_res;
+  ctl.ensure(8);
+  CUDA_OK(cudaMemsetAsync(ctl.p, 0, 8 * sizeof(u32), e.s));
+  k_frontier_init<<<nblk(F.n), 256, 0, e.s>>>(F, ctl.p, root);
+  k_frontier_start<<<1, 1, 0, e.s>>>(ctl.p, F.lvl_off);
+  static int gblocks = 0;
+  if (!gblocks) gblocks = coop_blocks(e, (const void*)k_frontier_grid, 256);
+  u32 h[5];
+  while (true) {
+    k_frontier_block<<<1, LV_BLOCK, 0, e.s>>>(F, ctl.p);
+    CUDA_OK(cudaMemcpyAsync(h, ctl.p, 5 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+    e.sync();
+    if (h[4]) break;
+    u32* c = ctl.p;
+    void* args[] = {&F, &c};
+    CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_frontier_grid, gblocks, 256, args, 0, e.s));
+    CUDA_OK(cudaMemcpyAsync(h, ctl.p, 5 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+    e.sync();
+    if (h[4]) break;
+  }
+  nlevels = h[1];
+  total = h[0];
+}
+
+u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrimmed) {
+  Scratch& X = e.sc;
+  u32 n = e.cg_n;
+  X.c_order.ensure(n + 1);
+  X.c_lvloff.ensure(n + 3);
+  Frontier F{X.cg_eoff.p, X.cg_edst.p, X.cg_roff.p, X.cg_rsrc.p, mask, X.cg_outdeg.p, X.cg_level.p,
+             X.c_order.p, X.c_lvloff.p, nullptr, n, 0};
+  u32 nl = 0, tot = 0;
+  run_frontier(e, F, 0, nl, tot);
+  ntrimmed = tot;
+  lvl_off.resize(nl + 1);
+  CUDA_OK(cudaMemcpyAsync(lvl_off.data(), X.c_lvloff.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+  e.sync();
+  return nl;
+}
+
+// BFS over the class graph from ``root``; marks (u32) + queue; returns count
+u32 bfs_graph(Engine& e, const u32* eoff, const u32* edst, u32 n, u32 root, u32* mark, u32* queue) {
+  Frontier F{eoff, edst, nullptr, nullptr, nullptr, nullptr, nullptr, queue, nullptr, mark, n, 1};
+  u32 nl = 0, tot = 0;
+  run_frontier(e, F, root, nl, tot);
+  return tot;
+}
+
+u32 bfs_classes(Engine& e, u32 root, u32* mark, u32* queue) {
+  return bfs_graph(e, e.sc.cg_eoff.p, e.sc.cg_edst.p, e.cg_n, root, mark, queue);
+}
+
+// ---------------------------------------------------------------- level-ordered passes
+
+// descendants closure over levels [l0, l1) inside one CTA
+__global__ void __launch_bounds__(LV_BLOCK) k_close_block(const u32* order, const u32* lvl_off, u32 l0, u32 l1,
+                                                          const u32* eoff, const u32* edst, u32* bits, u32 words) {
+  for (u32 l = l0; l < l1; l++) {
+    u32 a = lvl_off[l], b = lvl_off[l + 1];
+    u64 items = (u64)(b - a) * words;
+    for (u64 it = threadIdx.x; it < items; it += blockDim.x) {
+      u32 i = order[a + it / words];
+      u32 w = (u32)(it % words);
+      u32 acc = 0;
+      for (u32 e = eoff[i]; e < eoff[i + 1]; e++) {
+        u32 j = edst[e];
+        acc |= bits[(u64)j * words + w];
+        if ((j >> 5) == w) acc |= 1u << (j & 31);
+      }
+      bits[(u64)i * words + w] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// one wide level on the whole GPU
+__global__ void k_close_level(const u32* order, u32 a, u32 b, const u32* eoff, const u32* edst, u32* bits,
+                              u32 words) {
+  GRID_STRIDE(it, (u64)(b - a) * words) {
+    u32 i = order[a + it / words];
+    u32 w = (u32)(it % words);
+    u32 acc = 0;
+    for (u32 e = eoff[i]; e < eoff[i + 1]; e++) {
+      u32 j = edst[e];
+      acc |= bits[(u64)j * words + w];
+      if ((j >> 5) == w) acc |= 1u << (j & 31);
+    }
+    bits[(u64)i * words + w] = acc;
+  }
+}
+
+// run a level-ordered pass: consecutive thin levels batched into one CTA launch
+void close_levels(Engine& e, const std::vector<u32>& lo, u32 nl, u32* bits, u32 words) {
+  Scratch& X = e.sc;
+  u32 l = 1;  // level 0 rows stay empty
+  while (l < nl) {
+    u32 w = lo[l + 1] - lo[l];
+    if ((u64)w * words > (u64)LV_WIDE * 8) {
+      k_close_level<<<nblk((u64)w * words), 256, 0, e.s>>>(X.c_order.p, lo[l], lo[l + 1], X.cg_eoff.p, X.cg_edst.p,
+                                                           bits, words);
+      l++;
+      continue;
+    }
+    u32 l1 = l;
+    while (l1 < nl && (u64)(lo[l1 + 1] - lo[l1]) * words <= (u64)LV_WIDE * 8) l1++;
+    k_close_block<<<1, LV_BLOCK, 0, e.s>>>(X.c_order.p, X.c_lvloff.p, l, l1, X.cg_eoff.p, X.cg_edst.p, bits, words);
+    l = l1;
+  }
+}

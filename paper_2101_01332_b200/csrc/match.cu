@@ -167,7 +167,7 @@ __global__ void k_unique_write(const u32* cls, const u32* bind, int nb, const u3
 }
 
 void Engine::ematch_pattern(int pid, MatchSet& out) {
-  if (!snap.valid) build_snapshot();
+  if (!snap.valid || snap.n_atoms != h_atoms.size()) build_snapshot();
   const HPattern& hp = patterns[pid];
   PatDev p;
   memset(&p, 0, sizeof(p));
@@ -185,8 +185,10 @@ void Engine::ematch_pattern(int pid, MatchSet& out) {
   sync();
   u32 ncand = range[1] - range[0];
   if (ncand == 0) return;
-  DevBuf<u32> rc, rb, cntb;
-  cntb.alloc(1);
+  DevBuf<u32>& rc = sc.m_rc;
+  DevBuf<u32>& rb = sc.m_rb;
+  DevBuf<u32>& cntb = sc.m_cnt;
+  cntb.ensure(1);
   u32 cap = std::max<u32>(ncand * 2, 1024);
   u32 m = 0;
   for (int attempt = 0; attempt < 8; attempt++) {
@@ -207,21 +209,25 @@ void Engine::ematch_pattern(int pid, MatchSet& out) {
   }
   if (m == 0) return;
   // stable LSD sort over words (cls, b0..b_{nb-1}), last word first
-  DevBuf<u32> perm, perm2, key, key2;
-  perm.alloc(m);
-  perm2.alloc(m);
-  key.alloc(m);
-  key2.alloc(m);
+  DevBuf<u32>& perm = sc.m_perm;
+  DevBuf<u32>& perm2 = sc.m_perm2;
+  DevBuf<u32>& key = sc.m_key;
+  DevBuf<u32>& key2 = sc.m_key2;
+  perm.ensure(m);
+  perm2.ensure(m);
+  key.ensure(m);
+  key2.ensure(m);
   k_iota<<<nblk(m), 256, 0, s>>>(perm.p, m);
   int eb = (int)bits_for(h.next_id);
   for (int w = p.nb; w >= 0; w--) {
     k_gather_word<<<nblk(m), 256, 0, s>>>(rc.p, rb.p, p.nb, w, perm.p, m, key.p);
     dev_sort_pairs_u32(*this, key.p, key2.p, perm.p, perm2.p, m, eb);
-    std::swap(perm.p, perm2.p);
+    perm.swap(perm2);
   }
-  DevBuf<u32> fl, pos;
-  fl.alloc(m);
-  pos.alloc(m);
+  DevBuf<u32>& fl = sc.m_fl;
+  DevBuf<u32>& pos = sc.m_pos;
+  fl.ensure(m);
+  pos.ensure(m);
   k_unique_flags<<<nblk(m), 256, 0, s>>>(rc.p, rb.p, p.nb, perm.p, m, fl.p);
   dev_exclusive_scan_u32(*this, fl.p, pos.p, m);
   u32 lf, lp;

@@ -1,0 +1,945 @@
+// Parallel wave apply: the bulk path of run_rule/_apply_combo
+// (reference: pkg/src/tensorsat/explorer.py:146-163, 227-262).
+//
+// A wave takes the remaining product positions of one rule and evaluates all
+// of them against the e-graph state at wave start:
+//   1. join      compatible combos (multi-pattern: hash join on the shared
+//                variables' canonical classes, emitted in itertools.product
+//                order; single-pattern: every match)
+//   2. gates     combined subst, shape check (target programs on the Value
+//                analysis) and the efficient cycle pre-filter, fused
+//   3. resolve   target terms become node requests, resolved level by level:
+//                a key with only existing children is looked up in the
+//                hashcons; otherwise it goes to a wave-local key table where
+//                the first request in sequential order (min global position)
+//                is the one that allocates -- exactly the hash-cons hits the
+//                sequential loop would see.
+//   4. hazards   conditions under which later combos would observe this
+//                combo's effects differently from the wave-start state:
+//                a union of two pre-existing classes (changes find()), a
+//                union that grows a class's split origins, a request that
+//                re-uses a node created as an earlier target root (its class
+//                is the merged class), analysis errors.
+//   5. commit    all combos before the first hazard (and before the node-limit
+//                cutoff) are committed in bulk: ids by prefix sum in
+//                sequential order, node records, fresh-root unions, hashcons
+//                inserts.  The hazard combo itself runs on the exact
+//                sequential path (k_seq_rule) and the next wave starts after it.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "rulesdev.cuh"
+
+static inline unsigned nblk(u64 n, unsigned t = 256) {
+  u64 b = (n + t - 1) / t;
+  if (b < 1) b = 1;
+  if (b > 148ull * 64) b = 148ull * 64;
+  return (unsigned)b;
+}
+#define GRID_STRIDE(i, n) for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < (n); i += (u64)gridDim.x * blockDim.x)
+
+#define FRESH 0x80000000u
+#define MAX_REQ 32
+#define WAVE_MAX_CAND (1u << 22)
+
+RuleDev make_rule_dev(Engine& e, int ri, int filter_mode, int allow_self);
+ReachDev make_reach_dev(Engine& e);
+
+struct ReqT {        // request template (one App instruction of a target)
+  u32 atom;
+  int32_t nargs;
+  int32_t kid[8];    // >= 0: request index within the combo; < 0: var slot -(s+1)
+  int32_t depth;
+  int32_t tgt;
+  int32_t is_root;
+};
+
+struct WaveRule {
+  int R;                 // requests per combo
+  int ntgt;
+  int root_req[MAX_SRC]; // request index of each target's root, -1 for a bare variable target
+  int root_var[MAX_SRC]; // slot of a bare-variable target
+  int nshared;
+  int shpos[2][8];       // binding positions of the shared slots in sources 0 / 1
+  const ReqT* tmpl;
+};
+
+struct WaveTab {  // wave-local key table
+  u32* state;     // 0 empty, 1 busy, 2 ready
+  u32* key;       // 10 words per slot: op, nargs, kids[8]
+  unsigned long long* minpos;
+  u32* wid;       // assigned node id of the winner
+  u32* wroot;     // winner is a target root
+  Val* val;
+  u32 mask;
+  u32* wold;      // matched (old) class of a root winner's target
+};
+
+// ---------------------------------------------------------------- join
+
+__device__ __forceinline__ u64 shared_hash(const G& g, const u32* bind, int nb, u64 row, const int* pos, int ns) {
+  u64 h = 0x9ae16a3b2f90404fULL;
+  for (int s = 0; s < ns; s++) h = hash_mix(h, uf_find_ro(g.parent, bind[row * nb + pos[s]]));
+  return h;
+}
+
+__global__ void k_hash_rows(G g, const u32* bind, int nb, u32 n, WaveRule W, int side, u64* out, u32* idx) {
+  GRID_STRIDE(i, n) {
+    out[i] = shared_hash(g, bind, nb, i, W.shpos[side], W.nshared);
+    idx[i] = (u32)i;
+  }
+}
+
+// count (emit=false) or write (emit=true) compatible positions for rows i >= i0
+__global__ void k_join(G g, RuleDev R, WaveRule W, const u64* hA, u32 i0, const u64* hBs, const u32* iBs,
+                       unsigned long long p_start, int skip_self, const u32* off, u32* cnt,
+                       unsigned long long* out, u32 cap) {
+  GRID_STRIDE(t, (u64)(R.nmatch[0] - i0)) {
+    u32 i = i0 + (u32)t;
+    u64 h = hA[t];
+    u32 nB = R.nmatch[1];
+    // lower bound
+    u32 lo = 0, hi = nB;
+    while (lo < hi) {
+      u32 mid = (lo + hi) >> 1;
+      if (hBs[mid] < h) lo = mid + 1;
+      else hi = mid;
+    }
+    u32 c = 0;
+    u32 o = off ? off[t] : 0;
+    for (u32 k = lo; k < nB && hBs[k] == h; k++) {
+      u32 j = iBs[k];
+      unsigned long long p = (unsigned long long)i * nB + j;
+      if (p < p_start) continue;
+      if (skip_self && i == j) continue;
+      bool eq = true;
+      for (int s = 0; s < W.nshared && eq; s++)
+        eq = uf_find_ro(g.parent, R.mbind[0][(u64)i * R.nb[0] + W.shpos[0][s]]) ==
+             uf_find_ro(g.parent, R.mbind[1][(u64)j * R.nb[1] + W.shpos[1][s]]);
+      if (!eq) continue;
+      if (out) {
+        if (o + c < cap) out[o + c] = p;
+      }
+      c++;
+    }
+    if (cnt) cnt[t] = c;
+  }
+}
+
+// ---------------------------------------------------------------- gates
+
+// status: 0 accept, 1 shape fail, 2 cycle reject; hazard flag for gate errors
+__global__ void k_gates(G g, RuleDev R, ReachDev RD, WaveRule W, const unsigned long long* pos, u32 n,
+                        unsigned long long p_base, u8* status, u32* env_out, u32* old_out, u8* hazard) {
+  GRID_STRIDE(c, n) {
+    unsigned long long p = pos ? pos[c] : p_base + c;
+    u32 idx[MAX_SRC];
+    decode_pos(R, p, idx);
+    u32 env[MAX_VARS];
+    for (int v = 0; v < R.nslots; v++) env[v] = TSAT_NONE;
+    for (int i = 0; i < R.nsrc; i++)
+      for (int j = 0; j < R.nb[i]; j++) env[R.bind_slot[i][j]] = uf_find_ro(g.parent, R.mbind[i][(u64)idx[i] * R.nb[i] + j]);
+    u32 olds[MAX_SRC];
+    for (int t = 0; t < R.nsrc; t++) olds[t] = uf_find_ro(g.parent, R.mcls[t][idx[t]]);
+    u8 st = 0, hz = 0;
+    if (g.analysis) {
+      for (int t = 0; t < R.nsrc && st == 0; t++) {
+        Val out;
+        int s = eval_target(g, R.instr + R.tgt_off[t], R.tgt_len[t], env, out);
+        if (s == AS_ORIGIN_OVERFLOW || s == AS_TREE_FULL) {
+          hz = 1;
+          break;
+        }
+        if (s != AS_OK || !val_same_data(out, g.val[olds[t]])) st = 1;
+      }
+    }
+    if (st == 0 && !hz && R.efficient) {
+      bool hit = false;
+      for (int t = 0; t < R.nsrc && !hit; t++)
+        for (int l = 0; l < R.leaf_len[t]; l++) {
+          u32 leaf = env[R.leaf[R.leaf_off[t] + l]];
+          if (leaf == olds[t] || reach_query(RD, leaf, olds[t])) {
+            hit = true;
+            break;
+          }
+        }
+      if (hit) st = 2;
+    }
+    status[c] = st;
+    hazard[c] = hz;
+    for (int v = 0; v < R.nslots; v++) env_out[(u64)c * MAX_VARS + v] = env[v];
+    for (int t = 0; t < R.nsrc; t++) old_out[(u64)c * MAX_SRC + t] = olds[t];
+  }
+}
+
+__global__ void k_accept_flags(const u8* status, const u8* hazard, u32 n, u32* fl) {
+  GRID_STRIDE(c, n) fl[c] = (status[c] == 0 || hazard[c]) ? 1u : 0u;
+}
+
+__global__ void k_accept_list(const u32* fl, const u32* pre, u32 n, u32* acc) {
+  GRID_STRIDE(c, n) if (fl[c]) acc[pre[c]] = (u32)c;
+}
+
+// ---------------------------------------------------------------- resolution
+
+__device__ __forceinline__ u64 wkey_hash(u32 op, int n, const u32* k) {
+  u64 h = hash_mix(0x7a3f1e2dULL ^ ((u64)n << 40), op);
+  for (int i = 0; i < n; i++) h = hash_mix(h, k[i]);
+  return h;
+}
+
+// find-or-insert a key; returns slot
+__device__ u32 wtab_get(const WaveTab& T, u32 op, int n, const u32* k) {
+  u32 slot = (u32)wkey_hash(op, n, k) & T.mask;
+  while (true) {
+    u32 st = ((volatile u32*)T.state)[slot];
+    if (st == 0) {
+      if (atomicCAS(&T.state[slot], 0u, 1u) == 0u) {
+        u32* kk = T.key + (u64)slot * 10;
+        kk[0] = op;
+        kk[1] = (u32)n;
+        for (int i = 0; i < 8; i++) kk[2 + i] = i < n ? k[i] : 0u;
+        __threadfence();
+        atomicExch(&T.state[slot], 2u);
+        return slot;
+      }
+      st = ((volatile u32*)T.state)[slot];
+    }
+    while (st == 1) st = ((volatile u32*)T.state)[slot];
+    __threadfence();
+    const volatile u32* kk = T.key + (u64)slot * 10;
+    bool eq = kk[0] == op && kk[1] == (u32)n;
+    for (int i = 0; i < n && eq; i++) eq = kk[2 + i] == k[i];
+    if (eq) return slot;
+    slot = (slot + 1) & T.mask;
+  }
+}
+
+// one request level: thread per (accepted combo, template at this depth)
+__global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, u32 nacc, const int* lvl_req,
+                                int nlvl, const u32* env, u32* ident, u8* hazard) {
+  GRID_STRIDE(t, (u64)nacc * nlvl) {
+    u32 a = (u32)(t / nlvl);
+    int r = lvl_req[t % nlvl];
+    u32 c = acc[a];
+    if (hazard[c]) continue;
+    const ReqT& q = W.tmpl[r];
+    u32 kids[8];
+    bool real = true;
+    for (int j = 0; j < q.nargs; j++) {
+      int k = q.kid[j];
+      u32 v = k >= 0 ? ident[(u64)a * W.R + k] : env[(u64)c * MAX_VARS + (-k - 1)];
+      kids[j] = v;
+      real &= !(v & FRESH);
+    }
+    u64 gpos = (u64)a * W.R + r;
+    if (real) {
+      u32 hit = hc_lookup(g, q.atom, q.nargs, kids);
+      if (hit != TSAT_NONE) {
+        ident[gpos] = uf_find_ro(g.parent, hit);
+        continue;
+      }
+    }
+    u32 s = wtab_get(T, q.atom, q.nargs, kids);
+    atomicMin(&T.minpos[s], (unsigned long long)gpos);
+    ident[gpos] = FRESH | s;
+    if (g.analysis) {
+      Val kv[8];
+      for (int j = 0; j < q.nargs; j++) kv[j] = (kids[j] & FRESH) ? T.val[kids[j] & ~FRESH] : g.val[kids[j]];
+      Val v;
+      int st = val_make(q.atom, kv, q.nargs, v, g.atoms, g.tt);
+      if (st != AS_OK) {
+        hazard[c] = 2;
+        continue;
+      }
+      T.val[s] = v;  // every request with this key computes identical bytes
+    }
+  }
+}
+
+__global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, u32 nacc, const u32* ident, const u8* hazard,
+                             const u32* olds) {
+  GRID_STRIDE(a, nacc) {
+    if (hazard[acc[a]]) continue;
+    for (int t = 0; t < W.ntgt; t++) {
+      int r = W.root_req[t];
+      if (r < 0) continue;
+      u32 id = ident[(u64)a * W.R + r];
+      if (!(id & FRESH)) continue;
+      u32 s = id & ~FRESH;
+      if (T.minpos[s] == (u64)a * W.R + r) {
+        T.wroot[s] = 1;
+        T.wold[s] = olds[(u64)acc[a] * MAX_SRC + t];
+      }
+    }
+  }
+}
+
+// Union kinds per (combo, target): 0 none, 1 fresh root winner -> matched class,
+// 2 union(matched, existing class X), 3 union(matched, fresh non-root node F).
+#define UK_NONE 0
+#define UK_FRESH_ROOT 1
+#define UK_CLASS 2
+#define UK_FRESH_NODE 3
+
+// per accepted combo: allocations, union plan, type-a hazards (combo's own
+// evaluation cannot be trusted) and its write set.
+__global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, u32 nacc, const u32* ident,
+                             const u32* env, const u32* olds, int multi, u8* hazard, u32* alloc, u8* ukind,
+                             u32* uother, u8* grow, u8* stop_after) {
+  GRID_STRIDE(a, nacc) {
+    u32 c = acc[a];
+    u32 na = 0;
+    bool hz = hazard[c] != 0, sa = false;
+    u8 why = hazard[c];
+    for (int t = 0; t < MAX_SRC; t++) {
+      ukind[(u64)a * MAX_SRC + t] = UK_NONE;
+      grow[(u64)a * MAX_SRC + t] = 0;
+    }
+    if (!hz) {
+      for (int r = 0; r < W.R && !hz; r++) {
+        u32 id = ident[(u64)a * W.R + r];
+        if (!(id & FRESH)) continue;
+        u32 s = id & ~FRESH;
+        bool win = T.minpos[s] == (u64)a * W.R + r;
+        if (win) na++;
+        else if (T.wroot[s] && !W.tmpl[r].is_root) {
+          hz = true;  // inner reuse of a merged root
+          why = 3;
+        }
+      }
+      for (int t = 0; t < W.ntgt && !hz; t++) {
+        u32 old = olds[(u64)c * MAX_SRC + t];
+        int r = W.root_req[t];
+        u8 kind = UK_NONE;
+        u32 other = 0;
+        const Val* nv = nullptr;
+        if (r < 0) {
+          u32 x = env[(u64)c * MAX_VARS + W.root_var[t]];
+          if (x != old) {
+            kind = UK_CLASS;
+            other = x;
+            nv = &g.val[x];
+          }
+        } else {
+          u32 id = ident[(u64)a * W.R + r];
+          if (!(id & FRESH)) {
+            if (id != old) {
+              kind = UK_CLASS;
+              other = id;
+              nv = &g.val[id];
+            }
+          } else {
+            u32 s = id & ~FRESH;
+            bool win = T.minpos[s] == (u64)a * W.R + r;
+            if (win) {
+              kind = UK_FRESH_ROOT;
+              other = id;
+              nv = &T.val[s];
+            } else if (T.wroot[s]) {
+              u32 x = T.wold[s];  // the earlier root's node now lives in its matched class
+              if (x != old) {
+                kind = UK_CLASS;
+                other = x;
+                nv = &g.val[x];
+              }
+            } else {
+              kind = UK_FRESH_NODE;
+              other = id;
+              nv = &T.val[s];
+            }
+          }
+        }
+        if (kind != UK_NONE && g.analysis) {
+          const Val& ov = g.val[old];
+          if (!val_same_data(ov, *nv)) {
+            hz = true;  // AnalysisMergeError: exact path raises it
+            why = 5;
+          }
+          else if (kind == UK_CLASS) {
+            // the kept (smaller) root's analysis changes iff the dropped one adds origins
+            bool keep_is_old = old < other;
+            if (keep_is_old ? val_merge_grows(ov, *nv) : val_merge_grows(*nv, ov)) grow[(u64)a * MAX_SRC + t] = 1;
+          } else if (val_merge_grows(ov, *nv)) {
+            grow[(u64)a * MAX_SRC + t] = 1;
+          }
+        }
+        // a union or analysis change in a non-final target would feed the
+        // combo's own later targets: let the exact path handle it
+        if (t < W.ntgt - 1 && (kind == UK_CLASS || kind == UK_FRESH_NODE || grow[(u64)a * MAX_SRC + t])) {
+          hz = true;
+          why = 4;
+        }
+        if (multi && (kind == UK_CLASS || kind == UK_FRESH_NODE)) sa = true;
+        ukind[(u64)a * MAX_SRC + t] = kind;
+        uother[(u64)a * MAX_SRC + t] = other;
+      }
+    }
+    hazard[c] = hz ? (why ? why : 1) : 0;
+    stop_after[a] = sa ? 1 : 0;
+    alloc[a] = hz ? 0 : na;
+  }
+}
+
+// first writer of every identity (class id or FRESH slot) in the wave
+__global__ void k_first_writer(WaveRule W, const u32* acc, u32 nacc, const u8* hazard, const u32* olds,
+                               const u8* ukind, const u32* uother, const u8* grow, u32* fw_cls, u32* fw_fresh) {
+  GRID_STRIDE(a, nacc) {
+    u32 c = acc[a];
+    if (hazard[c]) continue;
+    for (int t = 0; t < W.ntgt; t++) {
+      u8 k = ukind[(u64)a * MAX_SRC + t];
+      u32 old = olds[(u64)c * MAX_SRC + t], x = uother[(u64)a * MAX_SRC + t];
+      bool gr = grow[(u64)a * MAX_SRC + t] != 0;
+      if (k == UK_CLASS) {
+        // only the dropped root changes identity; the kept root changes only
+        // when its analysis grows
+        u32 keep = old < x ? old : x, drop = old < x ? x : old;
+        atomicMin(&fw_cls[drop], c);
+        if (gr) atomicMin(&fw_cls[keep], c);
+      } else if (k == UK_FRESH_NODE) {
+        atomicMin(&fw_fresh[x & ~FRESH], c);
+        if (gr) atomicMin(&fw_cls[old], c);
+      } else if (k == UK_FRESH_ROOT && gr) {
+        atomicMin(&fw_cls[old], c);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ bool read_dirty(u32 id, u32 c, const u32* fw_cls, const u32* fw_fresh) {
+  if (id & FRESH) return fw_fresh[id & ~FRESH] < c;
+  return fw_cls[id] < c;
+}
+
+// candidate validity against earlier writes in the wave (all candidates:
+// rejected ones read through their gates, accepted ones through requests)
+__global__ void k_validity(WaveRule W, WaveTab T, int nslots, int nsrc, u32 ncand, const u8* hazard, const u32* env,
+                           const u32* olds, const u32* accpre, const u8* status, const u32* ident,
+                           const u32* fw_cls, const u32* fw_fresh, u32* first_bad) {
+  GRID_STRIDE(c0, ncand) {
+    u32 c = (u32)c0;
+    bool bad = hazard[c] != 0;
+    for (int v = 0; v < nslots && !bad; v++) bad = read_dirty(env[(u64)c * MAX_VARS + v], c, fw_cls, fw_fresh);
+    for (int t = 0; t < nsrc && !bad; t++) bad = read_dirty(olds[(u64)c * MAX_SRC + t], c, fw_cls, fw_fresh);
+    if (!bad && status[c] == 0) {
+      u32 a = accpre[c];
+      for (int r = 0; r < W.R && !bad; r++) {
+        u32 id = ident[(u64)a * W.R + r];
+        bad = read_dirty(id, c, fw_cls, fw_fresh);
+        // a reused target root resolves to the class it was merged into
+        if (!bad && (id & FRESH) && T.wroot[id & ~FRESH]) bad = read_dirty(T.wold[id & ~FRESH], c, fw_cls, fw_fresh);
+      }
+    }
+    if (bad) atomicMin(first_bad, c);
+  }
+}
+
+// first hazard (candidate index) and node-limit cutoff (accepted index)
+__global__ void k_find_stops(const u32* acc, u32 nacc, const u8* stop_after, const u32* apre, const u32* alloc,
+                             i64 live0, i64 n_max, u32* out /* [stop_after cand, cutoff cand] */) {
+  GRID_STRIDE(a, nacc) {
+    if (stop_after[a]) atomicMin(&out[0], acc[a]);
+    if (live0 + (i64)apre[a] + (i64)alloc[a] >= n_max && alloc[a] > 0) atomicMin(&out[1], acc[a]);
+  }
+}
+
+// unions of committed combos (disjoint by construction of the validity check)
+__global__ void k_commit_unions(G g, WaveRule W, WaveTab T, const u32* acc, u32 ncommit_acc, const u32* olds,
+                                const u8* ukind, const u32* uother, const u8* grow) {
+  GRID_STRIDE(a, ncommit_acc) {
+    u32 c = acc[a];
+    for (int t = 0; t < W.ntgt; t++) {
+      u8 k = ukind[(u64)a * MAX_SRC + t];
+      if (k == UK_NONE) continue;
+      u32 old = olds[(u64)c * MAX_SRC + t], x = uother[(u64)a * MAX_SRC + t];
+      bool gr = grow[(u64)a * MAX_SRC + t] != 0;
+      if (k == UK_FRESH_ROOT) {
+        if (gr && g.analysis) val_merge_into(g.val[old], T.val[x & ~FRESH]);
+        continue;  // parent link written by k_write_nodes
+      }
+      if (k == UK_FRESH_NODE) {
+        u32 f = T.wid[x & ~FRESH];
+        if (gr && g.analysis) val_merge_into(g.val[old], T.val[x & ~FRESH]);
+        g.parent[f] = old;
+        continue;
+      }
+      u32 keep = old < x ? old : x, drop = old < x ? x : old;
+      if (g.analysis) {
+        Val m = g.val[keep];
+        val_merge_into(m, g.val[drop]);
+        g.val[keep] = m;
+      }
+      g.parent[drop] = keep;
+    }
+  }
+}
+
+// stats over candidates [0, ncand): shape / cycle / applied / noop
+__global__ void k_seg_stats(const u8* status, u32 ncand, const u32* accpre, const u32* alloc, const u8* ukind,
+                            int efficient, DevStats* st) {
+  GRID_STRIDE(c, ncand) {
+    u8 s = status[c];
+    if (s == 1) atomicAdd(&st->skipped_shape, 1ull);
+    else if (s == 2) {
+      atomicAdd(&st->skipped_cycle, 1ull);
+      atomicAdd(&st->prefilter_checks, 1ull);
+      atomicAdd(&st->prefilter_rejects, 1ull);
+    } else {
+      if (efficient) atomicAdd(&st->prefilter_checks, 1ull);
+      u32 a = accpre[c];
+      bool un = false;
+      for (int t = 0; t < MAX_SRC; t++) un |= ukind[(u64)a * MAX_SRC + t] != UK_NONE;
+      if (alloc[a] > 0 || un) {
+        atomicAdd(&st->applied, 1ull);
+        st->changed = 1;
+      } else {
+        atomicAdd(&st->applied_noop, 1ull);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- commit
+
+__global__ void k_win_flags(WaveTab T, const u32* ident, u64 nreq, const ReqT* tmpl, int R, u32* wf, u32* ka) {
+  GRID_STRIDE(q, nreq) {
+    u32 id = ident[q];
+    bool win = (id & FRESH) && T.minpos[id & ~FRESH] == (unsigned long long)q;
+    wf[q] = win ? 1u : 0u;
+    ka[q] = win ? (u32)tmpl[q % R].nargs : 0u;
+  }
+}
+
+__global__ void k_assign_ids(WaveTab T, const u32* ident, u64 nreq, const u32* wf, const u32* wpre, u32 base) {
+  GRID_STRIDE(q, nreq) if (wf[q]) T.wid[ident[q] & ~FRESH] = base + wpre[q];
+}
+
+__global__ void k_write_nodes(G g, WaveRule W, WaveTab T, const u32* acc, const u32* ident, u64 nreq,
+                              const u32* wf, const u32* wpre, const u32* kpre, u32 base, u32 kbase,
+                              const u32* env, const u32* olds) {
+  GRID_STRIDE(q, nreq) {
+    if (!wf[q]) continue;
+    u32 a = (u32)(q / W.R);
+    int r = (int)(q % W.R);
+    u32 c = acc[a];
+    const ReqT& tq = W.tmpl[r];
+    u32 s = ident[q] & ~FRESH;
+    u32 id = base + wpre[q];
+    u32 ko = kbase + kpre[q];
+    g.op[id] = tq.atom;
+    g.koff[id] = ko;
+    g.koff[id + 1] = ko + tq.nargs;
+    for (int j = 0; j < tq.nargs; j++) {
+      int k = tq.kid[j];
+      u32 v = k >= 0 ? ident[(u64)a * W.R + k] : env[(u64)c * MAX_VARS + (-k - 1)];
+      g.kids[ko + j] = (v & FRESH) ? T.wid[v & ~FRESH] : v;
+    }
+    g.flags[id] = NF_ALIVE;
+    if (g.analysis) g.val[id] = T.val[s];
+    g.parent[id] = tq.is_root ? olds[(u64)c * MAX_SRC + tq.tgt] : id;
+  }
+}
+
+__global__ void k_insert_range(G g, u32 a, u32 b) {
+  GRID_STRIDE(i, (u64)(b - a)) hc_insert(g, a + (u32)i);
+}
+
+// ---------------------------------------------------------------- host side
+
+struct WaveBufs {
+  DevBuf<unsigned long long> pos;
+  DevBuf<u64> hA, hB, hBs;
+  DevBuf<u32> iB, iBs, cnt, off;
+  DevBuf<u8> status, hazard;
+  DevBuf<u32> env, olds, fl, pre, acc, ident, alloc, apre, wf, wpre, ka, kpre, stops, uother, fw_cls, fw_fresh;
+  DevBuf<u8> ukind, grow, sa;
+  DevBuf<int> lvl;
+  DevBuf<ReqT> tmpl;
+  // wave table
+  DevBuf<u32> wstate, wkey, wid, wroot, wold;
+  DevBuf<unsigned long long> wminpos;
+  DevBuf<Val> wval;
+  u32 wcap = 0;
+};
+
+void free_wave_bufs(WaveBufs* b) { delete b; }
+
+static void build_wave_rule(const HRule& hr, std::vector<ReqT>& tm, WaveRule& W, std::vector<std::vector<int>>& lv,
+                            int& R) {
+  tm.clear();
+  memset(&W, 0, sizeof(W));
+  W.ntgt = hr.nsrc;
+  int maxd = 0;
+  for (int t = 0; t < hr.nsrc; t++) {
+    std::vector<int> stack;  // >=0 request index, <0 var slot
+    const auto& prog = hr.targets[t];
+    for (const Instr& in : prog) {
+      if (in.kind == I_VAR) {
+        stack.push_back(-(in.arg + 1));
+      } else {
+        ReqT q;
+        memset(&q, 0, sizeof(q));
+        q.atom = in.atom;
+        q.nargs = in.arg;
+        for (int j = 0; j < in.arg; j++) q.kid[j] = stack[stack.size() - in.arg + j];
+        stack.resize(stack.size() - in.arg);
+        q.depth = in.depth;
+        q.tgt = t;
+        stack.push_back((int)tm.size());
+        tm.push_back(q);
+        maxd = std::max(maxd, in.depth);
+      }
+    }
+    int top = stack.back();
+    if (top >= 0) {
+      W.root_req[t] = top;
+      tm[top].is_root = 1;
+      W.root_var[t] = -1;
+    } else {
+      W.root_req[t] = -1;
+      W.root_var[t] = -top - 1;
+    }
+  }
+  R = (int)tm.size();
+  W.R = R;
+  lv.assign(maxd + 1, {});
+  for (int r = 0; r < R; r++) lv[tm[r].depth].push_back(r);
+  // shared slots between sources 0 and 1
+  if (hr.nsrc == 2) {
+    int ns = 0;
+    for (int j = 0; j < hr.src_nb[0]; j++)
+      for (int k = 0; k < hr.src_nb[1]; k++)
+        if (hr.bind_slot[0][j] == hr.bind_slot[1][k] && ns < 8) {
+          W.shpos[0][ns] = j;
+          W.shpos[1][ns] = k;
+          ns++;
+        }
+    W.nshared = ns;
+  }
+}
+
+static u32 read_u32(Engine& e, const u32* p) {
+  u32 v;
+  CUDA_OK(cudaMemcpyAsync(&v, p, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+  e.sync();
+  return v;
+}
+
+void dev_exclusive_scan_u32(Engine& e, const u32* in, u32* out, u32 n);
+
+static void accumulate_seg(Engine& e, int ri, const DevStats& d) {
+  RuleStatsH& r = e.rstats[ri];
+  r.applied += d.applied;
+  r.applied_noop += d.applied_noop;
+  r.skipped_shape += d.skipped_shape;
+  r.skipped_cycle += d.skipped_cycle;
+  e.report.prefilter_checks += d.prefilter_checks;
+  e.report.prefilter_rejects += d.prefilter_rejects;
+  if (d.changed) e.seq_changed = true;
+}
+
+// one rule, positions [p0, P): waves + exact fallback at hazards
+void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P) {
+  const HRule& hr = e.rules[ri];
+  if (!e.wave) e.wave = new WaveBufs();
+  WaveBufs& B = *e.wave;
+  std::vector<ReqT> tm;
+  WaveRule W;
+  std::vector<std::vector<int>> lv;
+  int R = 0;
+  build_wave_rule(hr, tm, W, lv, R);
+  B.tmpl.ensure(R + 1);
+  if (R) CUDA_OK(cudaMemcpyAsync(B.tmpl.p, tm.data(), R * sizeof(ReqT), cudaMemcpyHostToDevice, e.s));
+  W.tmpl = B.tmpl.p;
+  std::vector<int> lvl_flat, lvl_off;
+  for (auto& l : lv) {
+    lvl_off.push_back((int)lvl_flat.size());
+    lvl_flat.insert(lvl_flat.end(), l.begin(), l.end());
+  }
+  lvl_off.push_back((int)lvl_flat.size());
+  B.lvl.ensure(lvl_flat.size() + 1);
+  if (!lvl_flat.empty())
+    CUDA_OK(cudaMemcpyAsync(B.lvl.p, lvl_flat.data(), lvl_flat.size() * sizeof(int), cudaMemcpyHostToDevice, e.s));
+  int skip_self = (hr.nsrc == 2 && !allow_self && hr.same_canon) ? 1 : 0;
+  RuleStatsH& rs = e.rstats[ri];
+  unsigned long long p = 0;
+  u32 win = 1u << 12;  // adaptive candidate window (grows on clean waves, shrinks on dependencies)
+  while (p < P) {
+    // budget check at the segment's first position (explorer.py:198-206)
+    if ((i64)e.h.live >= n_max) {
+      e.seq_stop = true;
+      e.report.node_limit_overshoot = (i64)e.h.live - n_max;
+      return;
+    }
+    RuleDev Rd = make_rule_dev(e, ri, filter_mode, allow_self);
+    ReachDev RD = make_reach_dev(e);
+    e.phase_ms[8] += 1;  // waves
+    // ---- 1. candidates
+    u32 ncand = 0;
+    const unsigned long long* posp = nullptr;
+    unsigned long long seg_end = P;  // positions covered if every candidate commits
+    if (hr.nsrc == 1) {
+      unsigned long long n = std::min<unsigned long long>(P - p, win);
+      ncand = (u32)n;
+      seg_end = p + n;
+    } else {
+      u32 nA = Rd.nmatch[0], nB = Rd.nmatch[1];
+      u32 i0 = (u32)(p / nB);
+      u32 na = nA - i0;
+      B.hA.ensure(na + 1);
+      B.hB.ensure(nB + 1);
+      B.hBs.ensure(nB + 1);
+      B.iB.ensure(nB + 1);
+      B.iBs.ensure(nB + 1);
+      B.cnt.ensure(na + 1);
+      B.off.ensure(na + 1);
+      DevBuf<u32>& dummy = e.scratch_u32[6];
+      dummy.ensure(na + 1);
+      k_hash_rows<<<nblk(nB), 256, 0, e.s>>>(e.view(), Rd.mbind[1], Rd.nb[1], nB, W, 1, B.hB.p, B.iB.p);
+      k_hash_rows<<<nblk(na), 256, 0, e.s>>>(e.view(), Rd.mbind[0] + (u64)i0 * Rd.nb[0], Rd.nb[0], na, W, 0, B.hA.p,
+                                             dummy.p);
+      {
+        size_t bytes = 0;
+        CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
+        e.temp.ensure(bytes + 16);
+        CUDA_OK(cub::DeviceRadixSort::SortPairs(e.temp.p, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
+      }
+      k_join<<<nblk(na), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self, nullptr,
+                                        B.cnt.p, nullptr, 0);
+      CUDA_OK(cudaMemsetAsync(B.cnt.p + na, 0, sizeof(u32), e.s));
+      dev_exclusive_scan_u32(e, B.cnt.p, B.off.p, na + 1);
+      u32 total = read_u32(e, B.off.p + na);
+      u32 cap = std::min<u32>(total, win);
+      B.pos.ensure((u64)cap + 1);
+      if (cap)
+        k_join<<<nblk(na), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self, B.off.p,
+                                          nullptr, B.pos.p, cap);
+      ncand = cap;
+      posp = B.pos.p;
+      if (total > cap) {
+        unsigned long long lastp;
+        CUDA_OK(cudaMemcpyAsync(&lastp, B.pos.p + cap - 1, sizeof(lastp), cudaMemcpyDeviceToHost, e.s));
+        e.sync();
+        seg_end = lastp + 1;
+      }
+    }
+    auto pos_of = [&](u32 c) -> unsigned long long {
+      if (!posp) return p + c;
+      unsigned long long v;
+      CUDA_OK(cudaMemcpyAsync(&v, posp + c, sizeof(v), cudaMemcpyDeviceToHost, e.s));
+      e.sync();
+      return v;
+    };
+    if (ncand == 0) {
+      // nothing compatible left: every remaining position is a self or compat skip
+      unsigned long long cover = seg_end - p;
+      unsigned long long self = 0;
+      if (skip_self) {
+        u32 nB = Rd.nmatch[1];
+        for (u32 i = (u32)(p / nB); i < Rd.nmatch[0]; i++) {
+          unsigned long long q = (unsigned long long)i * nB + i;
+          if (q >= p && q < seg_end) self++;
+        }
+      }
+      rs.found += cover;
+      rs.skipped_self += self;
+      rs.skipped_compat += cover - self;
+      p = seg_end;
+      continue;
+    }
+    // ---- 2. gates
+    B.status.ensure(ncand + 1);
+    B.hazard.ensure(ncand + 1);
+    B.env.ensure((u64)ncand * MAX_VARS + 1);
+    B.olds.ensure((u64)ncand * MAX_SRC + 1);
+    B.fl.ensure(ncand + 1);
+    B.pre.ensure(ncand + 1);
+    B.acc.ensure(ncand + 1);
+    {
+      KTimer kt(e, KG_APPLY_WAVE, 0.0, 3);
+      k_gates<<<nblk(ncand, 128), 128, 0, e.s>>>(e.view(), Rd, RD, W, posp, ncand, p, B.status.p, B.env.p, B.olds.p,
+                                                 B.hazard.p);
+      k_accept_flags<<<nblk(ncand), 256, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.fl.p);
+      dev_exclusive_scan_u32(e, B.fl.p, B.pre.p, ncand);
+      k_accept_list<<<nblk(ncand), 256, 0, e.s>>>(B.fl.p, B.pre.p, ncand, B.acc.p);
+    }
+    u32 nacc = read_u32(e, B.pre.p + ncand - 1) + read_u32(e, B.fl.p + ncand - 1);
+    // ---- 3. resolve requests level by level
+    u64 nreq = (u64)nacc * R;
+    B.ident.ensure(nreq + 1);
+    B.alloc.ensure(nacc + 1);
+    B.apre.ensure(nacc + 1);
+    B.ukind.ensure((u64)nacc * MAX_SRC + 1);
+    B.uother.ensure((u64)nacc * MAX_SRC + 1);
+    B.grow.ensure((u64)nacc * MAX_SRC + 1);
+    B.sa.ensure(nacc + 1);
+    u32 used = 1;
+    if (R > 0 && nacc > 0) {
+      u32 want = 1024;
+      while (want < 2 * nreq + 16) want *= 2;
+      if (want > B.wcap) {
+        B.wcap = want;
+        B.wstate.alloc(want);
+        B.wkey.alloc((u64)want * 10);
+        B.wid.alloc(want);
+        B.wroot.alloc(want);
+        B.wold.alloc(want);
+        B.wminpos.alloc(want);
+        B.wval.alloc(e.analysis ? want : 1);
+      }
+      used = std::min<u32>(B.wcap, want);
+      CUDA_OK(cudaMemsetAsync(B.wstate.p, 0, (u64)used * sizeof(u32), e.s));
+      CUDA_OK(cudaMemsetAsync(B.wroot.p, 0, (u64)used * sizeof(u32), e.s));
+      CUDA_OK(cudaMemsetAsync(B.wminpos.p, 0xFF, (u64)used * sizeof(unsigned long long), e.s));
+    }
+    WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, used - 1, B.wold.p};
+    u32 bad = TSAT_NONE, sa_c = TSAT_NONE, cut_c = TSAT_NONE;
+    if (nacc > 0) {
+      KTimer kt(e, KG_APPLY_WAVE, 0.0, lv.size() + 6);
+      if (R > 0) {
+        for (size_t d = 1; d < lv.size(); d++) {
+          int nl = (int)lv[d].size();
+          if (!nl) continue;
+          k_resolve_level<<<nblk((u64)nacc * nl, 128), 128, 0, e.s>>>(e.view(), W, T, B.acc.p, nacc,
+                                                                     B.lvl.p + lvl_off[d], nl, B.env.p, B.ident.p,
+                                                                     B.hazard.p);
+        }
+        k_mark_roots<<<nblk(nacc), 256, 0, e.s>>>(W, T, B.acc.p, nacc, B.ident.p, B.hazard.p, B.olds.p);
+      }
+      k_cand_check<<<nblk(nacc), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, nacc, B.ident.p, B.env.p, B.olds.p,
+                                                hr.nsrc > 1 ? 1 : 0, B.hazard.p, B.alloc.p, B.ukind.p,
+                                                B.uother.p, B.grow.p, B.sa.p);
+      // ---- 4. read/write conflicts, stop-after, node-limit cutoff
+      B.fw_cls.ensure((u64)e.h.next_id + 1);
+      B.fw_fresh.ensure((u64)used + 1);
+      CUDA_OK(cudaMemsetAsync(B.fw_cls.p, 0xFF, ((u64)e.h.next_id + 1) * sizeof(u32), e.s));
+      CUDA_OK(cudaMemsetAsync(B.fw_fresh.p, 0xFF, ((u64)used + 1) * sizeof(u32), e.s));
+      k_first_writer<<<nblk(nacc), 256, 0, e.s>>>(W, B.acc.p, nacc, B.hazard.p, B.olds.p, B.ukind.p, B.uother.p,
+                                                  B.grow.p, B.fw_cls.p, B.fw_fresh.p);
+      B.stops.ensure(4);
+      CUDA_OK(cudaMemsetAsync(B.stops.p, 0xFF, 3 * sizeof(u32), e.s));
+      k_validity<<<nblk(ncand), 256, 0, e.s>>>(W, T, Rd.nslots, Rd.nsrc, ncand, B.hazard.p, B.env.p, B.olds.p, B.pre.p,
+                                               B.status.p, B.ident.p, B.fw_cls.p, B.fw_fresh.p, B.stops.p + 2);
+      dev_exclusive_scan_u32(e, B.alloc.p, B.apre.p, nacc);
+      k_find_stops<<<nblk(nacc), 256, 0, e.s>>>(B.acc.p, nacc, B.sa.p, B.apre.p, B.alloc.p, (i64)e.h.live, n_max,
+                                                B.stops.p);
+      u32 hs[3];
+      CUDA_OK(cudaMemcpyAsync(hs, B.stops.p, sizeof(hs), cudaMemcpyDeviceToHost, e.s));
+      e.sync();
+      sa_c = hs[0];
+      cut_c = hs[1];
+      bad = hs[2];
+    }
+    // commit boundary in candidate space (exclusive end)
+    auto plus1 = [](u32 x) -> u64 { return x == TSAT_NONE ? (u64)1 << 40 : (u64)x + 1; };
+    u64 e_bad = bad == TSAT_NONE ? (u64)1 << 40 : (u64)bad;
+    u64 e_cut = plus1(cut_c), e_sa = plus1(sa_c);
+    u64 e_end = std::min<u64>(std::min(e_bad, std::min(e_cut, e_sa)), ncand);
+    u32 ncommit_cand = (u32)e_end;
+    bool stop = false, hazard = false;
+    unsigned long long p_end = seg_end;
+    if (e_cut <= e_end) {
+      p_end = pos_of(cut_c) + 1;
+      stop = true;
+    } else if (e_bad <= e_end) {
+      p_end = pos_of(bad);
+      u8 why;
+      CUDA_OK(cudaMemcpyAsync(&why, B.hazard.p + bad, 1, cudaMemcpyDeviceToHost, e.s));
+      e.sync();
+      e.phase_ms[10 + std::min<int>(why, 5)] += 1;  // 10: read-dirty, 11 gate, 12 make, 13 inner reuse, 14 intra, 15 merge
+      // a read-after-write dependency only needs a fresh evaluation: the next
+      // wave starts at this combo.  Other hazards run it on the exact path.
+      hazard = why != 0;
+    } else if (e_sa <= e_end) {
+      p_end = pos_of(sa_c) + 1;
+    }
+    u32 ncommit_acc = ncommit_cand == ncand ? nacc
+                                            : (ncommit_cand == 0 ? 0 : read_u32(e, B.pre.p + ncommit_cand));
+    // ---- 5. stats of the committed segment [p, p_end)
+    bool any_applied = false;
+    {
+      unsigned long long cover = p_end - p, self = 0;
+      if (skip_self) {
+        u32 nB = Rd.nmatch[1];
+        u32 ia = (u32)(p / nB), ib = (u32)std::min<unsigned long long>(Rd.nmatch[0], p_end / nB + 1);
+        for (u32 i = ia; i < ib; i++) {
+          unsigned long long q = (unsigned long long)i * nB + i;
+          if (q >= p && q < p_end) self++;
+        }
+      }
+      rs.found += cover;
+      rs.skipped_self += self;
+      rs.skipped_compat += cover - self - ncommit_cand;
+      if (ncommit_cand) {
+        CUDA_OK(cudaMemsetAsync(e.dstats.p, 0, sizeof(DevStats), e.s));
+        k_seg_stats<<<nblk(ncommit_cand), 256, 0, e.s>>>(B.status.p, ncommit_cand, B.pre.p, B.alloc.p, B.ukind.p,
+                                                         Rd.efficient, e.dstats.p);
+        DevStats d;
+        CUDA_OK(cudaMemcpyAsync(&d, e.dstats.p, sizeof(d), cudaMemcpyDeviceToHost, e.s));
+        e.sync();
+        accumulate_seg(e, ri, d);
+        any_applied = d.applied > 0;
+      }
+    }
+    // ---- 6. commit
+    u64 creq = (u64)ncommit_acc * R;
+    u32 nwin = 0, nk = 0;
+    if (creq) {
+      B.wf.ensure(creq + 1);
+      B.wpre.ensure(creq + 1);
+      B.ka.ensure(creq + 1);
+      B.kpre.ensure(creq + 1);
+      k_win_flags<<<nblk(creq), 256, 0, e.s>>>(T, B.ident.p, creq, B.tmpl.p, R, B.wf.p, B.ka.p);
+      CUDA_OK(cudaMemsetAsync(B.wf.p + creq, 0, sizeof(u32), e.s));
+      CUDA_OK(cudaMemsetAsync(B.ka.p + creq, 0, sizeof(u32), e.s));
+      dev_exclusive_scan_u32(e, B.wf.p, B.wpre.p, (u32)creq + 1);
+      dev_exclusive_scan_u32(e, B.ka.p, B.kpre.p, (u32)creq + 1);
+      nwin = read_u32(e, B.wpre.p + creq);
+      nk = read_u32(e, B.kpre.p + creq);
+    }
+    if (nwin || (ncommit_acc && any_applied)) {
+      e.ensure_nodes(nwin, nk);
+      u32 base = e.h.next_id, kbase = e.h.nkids;
+      KTimer kt(e, KG_APPLY_WAVE, 0.0, 4);
+      if (nwin) {
+        k_assign_ids<<<nblk(creq), 256, 0, e.s>>>(T, B.ident.p, creq, B.wf.p, B.wpre.p, base);
+        k_write_nodes<<<nblk(creq), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, B.ident.p, creq, B.wf.p, B.wpre.p,
+                                                   B.kpre.p, base, kbase, B.env.p, B.olds.p);
+      }
+      k_commit_unions<<<nblk(ncommit_acc), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, ncommit_acc, B.olds.p, B.ukind.p,
+                                                          B.uother.p, B.grow.p);
+      if (nwin) k_insert_range<<<nblk(nwin), 256, 0, e.s>>>(e.view(), base, base + nwin);
+      e.h.next_id += nwin;
+      e.h.live += nwin;
+      e.h.nkids += nk;
+      if (any_applied) e.h.dirty = 1;
+      e.push_counters();
+      e.sync();
+    }
+    if (stop) {
+      if (p_end < P) {
+        e.seq_stop = true;
+        e.report.node_limit_overshoot = (i64)e.h.live - n_max;
+      }
+      p = p_end;
+      if (e.seq_stop) return;
+      continue;
+    }
+    // adapt the window: dependencies every k combos -> evaluate ~2k ahead
+    if (ncommit_cand < ncand) win = std::max<u32>(64u, std::min<u32>(2u * ncommit_cand + 32u, 1u << 22));
+    else win = std::min<u32>(win * 4u, 1u << 22);
+    if (hazard) {
+      e.phase_ms[9] += 1;  // hazards
+      // exact sequential path for exactly the hazard combo
+      e.ensure_nodes(4096, 4096);
+      e.run_rule_seq(ri, filter_mode, allow_self, n_max, p_end, p_end + 1);
+      if (e.seq_stop) return;
+      p = p_end + 1;
+      continue;
+    }
+    p = p_end;
+  }
+}

@@ -62,6 +62,8 @@ def break_all_cycles(eg, filt: set, root: Optional[int] = None) -> int:
     finally:
         if root is not None:
             eg.root = old_root
-    filt.update(eg.get_filter())
+    dev = eg.get_filter()
+    eg._filt_dev = frozenset(dev)
+    filt.update(dev)
     eg._touch()
     return int(added.value)

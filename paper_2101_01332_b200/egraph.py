@@ -183,6 +183,7 @@ class EGraph:
         self._atom_list: list = []
         self._sent = 0
         self._view: Optional[_View] = None
+        self._filt_dev: Optional[frozenset] = frozenset()  # filter list known to be on the device
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -348,6 +349,9 @@ class EGraph:
 
     def set_filter(self, filt: Iterable[int]) -> None:
         """Replace the device filter list (every call taking ``filt`` uploads it)."""
+        want = frozenset(int(x) for x in filt)
+        if self._filt_dev is not None and want == self._filt_dev:
+            return
         n_alloc = self._sizes()[0]
         lib = _lib.load()
         _lib.check(self._h, lib.tsat_set_filter(self._h, 0, None, 2))
@@ -355,6 +359,7 @@ class EGraph:
         if real:
             arr = np.array(real, np.uint32)
             _lib.check(self._h, lib.tsat_set_filter(self._h, len(arr), _lib.ptr(arr, C.c_uint32), 1))
+        self._filt_dev = frozenset(real)
         self._touch()
 
     def get_filter(self) -> list:

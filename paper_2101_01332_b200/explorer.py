@@ -146,7 +146,9 @@ def saturate(
     report.time_s = float(rep.time_s)
     extra = {x for x in filt if not (0 <= int(x) < eg.allocated_nodes)}
     filt.clear()
-    filt.update(eg.get_filter())
+    dev = eg.get_filter()
+    eg._filt_dev = frozenset(dev)
+    filt.update(dev)
     filt.update(extra)
     report.filter_size = len(filt)
     return filt, report

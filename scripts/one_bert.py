@@ -1,0 +1,12 @@
+import sys
+sys.path.insert(0, '.')
+from paper_2101_01332_b200 import models
+from paper_2101_01332_b200.rules import default_rules
+from paper_2101_01332_b200.explorer import ExploreLimits, explore
+from paper_2101_01332_b200.cost import CostModel, egraph_costs
+from paper_2101_01332_b200.extract import greedy_extract
+name = sys.argv[1] if len(sys.argv) > 1 else "bert"
+g = models.MODELS[name]()
+eg, filt, rep = explore(g, list(default_rules()), ExploreLimits(k_multi=1))
+res = greedy_extract(eg, egraph_costs(eg, CostModel()), filt)
+print(rep.enodes_per_iter, res.total_cost)
