@@ -77,6 +77,8 @@ int tsat_set_root(tsat_engine* h, uint32_t root);                            /* 
 /* sizes + SoA download (EGraph.nodes / classes / dump, egraph.py:127-162, 334-349) */
 int tsat_query_sizes(tsat_engine* h, uint32_t* next_id, uint32_t* live, uint32_t* nkids,
                      uint32_t* root, uint32_t* dirty);
+int tsat_num_classes(tsat_engine* h, uint32_t* out);
+int tsat_download_flags(tsat_engine* h, uint8_t* flags);
 int tsat_download(tsat_engine* h, uint32_t* op, uint32_t* child_off, uint32_t* child,
                   uint32_t* cls, uint8_t* flags);
 int tsat_download_values(tsat_engine* h, void* vals, int64_t val_bytes, void* trees,

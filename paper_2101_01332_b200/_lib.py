@@ -48,6 +48,8 @@ _SIGS = {
     "tsat_find": ([C.c_void_p, C.c_uint32, u32p], C.c_int),
     "tsat_set_root": ([C.c_void_p, C.c_uint32], C.c_int),
     "tsat_query_sizes": ([C.c_void_p, u32p, u32p, u32p, u32p, u32p], C.c_int),
+    "tsat_num_classes": ([C.c_void_p, u32p], C.c_int),
+    "tsat_download_flags": ([C.c_void_p, u8p], C.c_int),
     "tsat_download": ([C.c_void_p, u32p, u32p, u32p, u32p, u8p], C.c_int),
     "tsat_download_values": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, u32p], C.c_int),
     "tsat_dump": ([C.c_void_p, C.c_char_p, C.c_int64, i64p], C.c_int),

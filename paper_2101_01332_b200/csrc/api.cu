@@ -117,6 +117,7 @@ int tsat_set_root(tsat_engine* h, uint32_t root) {
   GUARD(h, {
     if (root != TSAT_NONE && root >= h->e->h.next_id) throw TsatException(TSAT_ERR_ARG, "root out of range");
     h->e->root = root;
+    h->e->root_ver = ~0ull;
   });
 }
 
@@ -127,8 +128,24 @@ int tsat_query_sizes(tsat_engine* h, uint32_t* next_id, uint32_t* live, uint32_t
     *next_id = e.h.next_id;
     *live = e.h.live;
     *nkids = e.h.nkids;
-    *root = e.root == TSAT_NONE ? TSAT_NONE : e.find(e.root);
+    *root = e.root == TSAT_NONE ? TSAT_NONE : e.root_class();
     *dirty = e.h.dirty;
+  });
+}
+
+int tsat_num_classes(tsat_engine* h, uint32_t* out) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    if (!e.snap.valid) e.build_snapshot();
+    *out = e.snap.ncls;
+  });
+}
+
+int tsat_download_flags(tsat_engine* h, uint8_t* flags) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    if (e.h.next_id) CUDA_OK(cudaMemcpyAsync(flags, e.flags.p, e.h.next_id, cudaMemcpyDeviceToHost, e.s));
+    e.sync();
   });
 }
 

@@ -343,6 +343,7 @@ void Engine::load_initial(u32 n, const u32* hop, const u32* hkoff, const u32* hk
     sync();
   }
   root = r;
+  root_ver = ~0ull;
   check_error();
 }
 

@@ -279,6 +279,17 @@ struct Engine {
   void set_filter(int n, const u32* ids, int on);
   std::vector<u32> get_filter();
   u32 find(u32 x);
+  u64 root_ver = ~0ull;
+  u32 root_cls_cache = TSAT_NONE;
+  u32 root_class() {
+    // snapshot id changes whenever the union-find can have changed
+    if (!snap.valid) build_snapshot();
+    if (root_ver != snap_id) {
+      root_cls_cache = find(root);
+      root_ver = snap_id;
+    }
+    return root_cls_cache;
+  }
 
   // snapshot + matching
   void build_snapshot();

@@ -47,6 +47,11 @@ static inline unsigned nblk(u64 n, unsigned t = 256) {
 RuleDev make_rule_dev(Engine& e, int ri, int filter_mode, int allow_self);
 ReachDev make_reach_dev(Engine& e);
 
+struct WaveState {
+  u32 nacc, ncommit_cand, ncommit_acc, nwin, nk, base, kbase, stop, hazard, why, any_applied, pad;
+  unsigned long long p_end;
+};
+
 struct ReqT {        // request template (one App instruction of a target)
   u32 atom;
   int32_t nargs;
@@ -218,8 +223,9 @@ __device__ u32 wtab_get(const WaveTab& T, u32 op, int n, const u32* k) {
 }
 
 // one request level: thread per (accepted combo, template at this depth)
-__global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, u32 nacc, const int* lvl_req,
+__global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const int* lvl_req,
                                 int nlvl, const u32* env, u32* ident, u8* hazard) {
+  u32 nacc = ws->nacc;
   GRID_STRIDE(t, (u64)nacc * nlvl) {
     u32 a = (u32)(t / nlvl);
     int r = lvl_req[t % nlvl];
@@ -259,8 +265,9 @@ __global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, u32 
   }
 }
 
-__global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, u32 nacc, const u32* ident, const u8* hazard,
-                             const u32* olds) {
+__global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const u32* ident,
+                             const u8* hazard, const u32* olds) {
+  u32 nacc = ws->nacc;
   GRID_STRIDE(a, nacc) {
     if (hazard[acc[a]]) continue;
     for (int t = 0; t < W.ntgt; t++) {
@@ -286,10 +293,17 @@ __global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, u32 nacc, co
 
 // per accepted combo: allocations, union plan, type-a hazards (combo's own
 // evaluation cannot be trusted) and its write set.
-__global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, u32 nacc, const u32* ident,
-                             const u32* env, const u32* olds, int multi, u8* hazard, u32* alloc, u8* ukind,
-                             u32* uother, u8* grow, u8* stop_after) {
-  GRID_STRIDE(a, nacc) {
+__global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, u32 ncand,
+                             const u32* ident, const u32* env, const u32* olds, int multi, u8* hazard, u32* alloc,
+                             u8* ukind, u32* uother, u8* grow, u8* stop_after) {
+  u32 nacc = ws->nacc;
+  GRID_STRIDE(a0, ncand) {
+    u32 a = (u32)a0;
+    if (a >= nacc) {
+      alloc[a] = 0;
+      stop_after[a] = 0;
+      continue;
+    }
     u32 c = acc[a];
     u32 na = 0;
     bool hz = hazard[c] != 0, sa = false;
@@ -384,8 +398,9 @@ __global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, u32 nac
 }
 
 // first writer of every identity (class id or FRESH slot) in the wave
-__global__ void k_first_writer(WaveRule W, const u32* acc, u32 nacc, const u8* hazard, const u32* olds,
+__global__ void k_first_writer(WaveRule W, const u32* acc, const WaveState* ws, const u8* hazard, const u32* olds,
                                const u8* ukind, const u32* uother, const u8* grow, u32* fw_cls, u32* fw_fresh) {
+  u32 nacc = ws->nacc;
   GRID_STRIDE(a, nacc) {
     u32 c = acc[a];
     if (hazard[c]) continue;
@@ -438,8 +453,11 @@ __global__ void k_validity(WaveRule W, WaveTab T, int nslots, int nsrc, u32 ncan
 }
 
 // first hazard (candidate index) and node-limit cutoff (accepted index)
-__global__ void k_find_stops(const u32* acc, u32 nacc, const u8* stop_after, const u32* apre, const u32* alloc,
-                             i64 live0, i64 n_max, u32* out /* [stop_after cand, cutoff cand] */) {
+__global__ void k_find_stops(const u32* acc, const WaveState* ws, const u8* stop_after, const u32* apre,
+                             const u32* alloc, const Counters* cnt, i64 n_max,
+                             u32* out /* [stop_after cand, cutoff cand] */) {
+  u32 nacc = ws->nacc;
+  i64 live0 = (i64)cnt->live;
   GRID_STRIDE(a, nacc) {
     if (stop_after[a]) atomicMin(&out[0], acc[a]);
     if (live0 + (i64)apre[a] + (i64)alloc[a] >= n_max && alloc[a] > 0) atomicMin(&out[1], acc[a]);
@@ -447,8 +465,9 @@ __global__ void k_find_stops(const u32* acc, u32 nacc, const u8* stop_after, con
 }
 
 // unions of committed combos (disjoint by construction of the validity check)
-__global__ void k_commit_unions(G g, WaveRule W, WaveTab T, const u32* acc, u32 ncommit_acc, const u32* olds,
+__global__ void k_commit_unions(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const u32* olds,
                                 const u8* ukind, const u32* uother, const u8* grow) {
+  u32 ncommit_acc = ws->ncommit_acc;
   GRID_STRIDE(a, ncommit_acc) {
     u32 c = acc[a];
     for (int t = 0; t < W.ntgt; t++) {
@@ -478,9 +497,11 @@ __global__ void k_commit_unions(G g, WaveRule W, WaveTab T, const u32* acc, u32 
 }
 
 // stats over candidates [0, ncand): shape / cycle / applied / noop
-__global__ void k_seg_stats(const u8* status, u32 ncand, const u32* accpre, const u32* alloc, const u8* ukind,
-                            int efficient, DevStats* st) {
+__global__ void k_seg_stats(const u8* status, WaveState* ws, u32 ncand, const u32* accpre, const u32* alloc,
+                            const u8* ukind, int efficient, DevStats* st) {
+  u32 ncommit = ws->ncommit_cand;
   GRID_STRIDE(c, ncand) {
+    if (c >= ncommit) continue;
     u8 s = status[c];
     if (s == 1) atomicAdd(&st->skipped_shape, 1ull);
     else if (s == 2) {
@@ -495,6 +516,7 @@ __global__ void k_seg_stats(const u8* status, u32 ncand, const u32* accpre, cons
       if (alloc[a] > 0 || un) {
         atomicAdd(&st->applied, 1ull);
         st->changed = 1;
+        ws->any_applied = 1;
       } else {
         atomicAdd(&st->applied_noop, 1ull);
       }
@@ -504,22 +526,27 @@ __global__ void k_seg_stats(const u8* status, u32 ncand, const u32* accpre, cons
 
 // ---------------------------------------------------------------- commit
 
-__global__ void k_win_flags(WaveTab T, const u32* ident, u64 nreq, const ReqT* tmpl, int R, u32* wf, u32* ka) {
+__global__ void k_win_flags(WaveTab T, const u32* ident, u64 nreq, const ReqT* tmpl, int R, const WaveState* ws,
+                            u32* wf, u32* ka) {
+  u64 lim = (u64)ws->ncommit_acc * R;
   GRID_STRIDE(q, nreq) {
-    u32 id = ident[q];
-    bool win = (id & FRESH) && T.minpos[id & ~FRESH] == (unsigned long long)q;
+    u32 id = q < lim ? ident[q] : 0u;
+    bool win = q < lim && (id & FRESH) && T.minpos[id & ~FRESH] == (unsigned long long)q;
     wf[q] = win ? 1u : 0u;
     ka[q] = win ? (u32)tmpl[q % R].nargs : 0u;
   }
 }
 
-__global__ void k_assign_ids(WaveTab T, const u32* ident, u64 nreq, const u32* wf, const u32* wpre, u32 base) {
+__global__ void k_assign_ids(WaveTab T, const u32* ident, u64 nreq, const u32* wf, const u32* wpre,
+                             const WaveState* ws) {
+  u32 base = ws->base;
   GRID_STRIDE(q, nreq) if (wf[q]) T.wid[ident[q] & ~FRESH] = base + wpre[q];
 }
 
 __global__ void k_write_nodes(G g, WaveRule W, WaveTab T, const u32* acc, const u32* ident, u64 nreq,
-                              const u32* wf, const u32* wpre, const u32* kpre, u32 base, u32 kbase,
+                              const u32* wf, const u32* wpre, const u32* kpre, const WaveState* ws,
                               const u32* env, const u32* olds) {
+  u32 base = ws->base, kbase = ws->kbase;
   GRID_STRIDE(q, nreq) {
     if (!wf[q]) continue;
     u32 a = (u32)(q / W.R);
@@ -543,8 +570,114 @@ __global__ void k_write_nodes(G g, WaveRule W, WaveTab T, const u32* acc, const 
   }
 }
 
-__global__ void k_insert_range(G g, u32 a, u32 b) {
-  GRID_STRIDE(i, (u64)(b - a)) hc_insert(g, a + (u32)i);
+__global__ void k_insert_range(G g, const WaveState* ws, u64 bound) {
+  u32 a = ws->base, n = ws->nwin;
+  GRID_STRIDE(i, bound) if (i < n) hc_insert(g, a + (u32)i);
+}
+
+
+// ---------------------------------------------------------------- device-side wave control
+
+
+// single-CTA exclusive scan with the total at out[n] (small arrays; CUB's two
+// kernels cost more than the work at wave sizes)
+__global__ void __launch_bounds__(1024) k_scan_block(const u32* in, u32* out, u32 n) {
+  typedef cub::BlockScan<u32, 1024> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ u32 carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u32 base = 0; base < n; base += 1024) {
+    u32 i = base + threadIdx.x;
+    u32 v = i < n ? in[i] : 0u, x, tot;
+    BS(tmp).ExclusiveSum(v, x, tot);
+    if (i < n) out[i] = carry + x;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+// accepted list (status 0 or flagged) in candidate order; ws->nacc
+__global__ void __launch_bounds__(1024) k_accept_scan(const u8* status, const u8* hazard, u32 n, u32* pre, u32* acc,
+                                                      WaveState* ws) {
+  typedef cub::BlockScan<u32, 1024> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ u32 carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u32 base = 0; base < n; base += 1024) {
+    u32 c = base + threadIdx.x;
+    u32 f = (c < n && (status[c] == 0 || hazard[c])) ? 1u : 0u, x, tot;
+    BS(tmp).ExclusiveSum(f, x, tot);
+    if (c < n) {
+      pre[c] = carry + x;
+      if (f) acc[carry + x] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pre[n] = carry;
+    ws->nacc = carry;
+  }
+}
+
+// commit boundary: stops = [stop_after cand, cutoff cand, first bad cand]
+__global__ void k_boundary(WaveState* ws, const u32* stops, u32 ncand, const unsigned long long* pos,
+                           unsigned long long p, unsigned long long seg_end, const u32* pre, const u8* hazard) {
+  if (threadIdx.x || blockIdx.x) return;
+  const u64 INF = (u64)1 << 40;
+  u64 e_sa = stops[0] == TSAT_NONE ? INF : (u64)stops[0] + 1;
+  u64 e_cut = stops[1] == TSAT_NONE ? INF : (u64)stops[1] + 1;
+  u64 e_bad = stops[2] == TSAT_NONE ? INF : (u64)stops[2];
+  u64 e_end = e_bad < e_cut ? e_bad : e_cut;
+  e_end = e_end < e_sa ? e_end : e_sa;
+  e_end = e_end < ncand ? e_end : ncand;
+  auto posf = [&](u32 c) -> unsigned long long { return pos ? pos[c] : p + c; };
+  ws->stop = 0;
+  ws->hazard = 0;
+  ws->why = 0;
+  ws->p_end = seg_end;
+  if (e_cut <= e_end) {
+    ws->p_end = posf(stops[1]) + 1;
+    ws->stop = 1;
+  } else if (e_bad <= e_end) {
+    ws->p_end = posf(stops[2]);
+    ws->why = hazard[stops[2]];
+    ws->hazard = ws->why != 0;
+  } else if (e_sa <= e_end) {
+    ws->p_end = posf(stops[0]) + 1;
+  }
+  ws->ncommit_cand = (u32)e_end;
+  ws->ncommit_acc = pre[e_end];
+  ws->any_applied = 0;
+}
+
+__global__ void k_commit_prep(WaveState* ws, const u32* wpre, const u32* kpre, u64 nq, const Counters* cnt) {
+  if (threadIdx.x || blockIdx.x) return;
+  ws->nwin = wpre[nq];
+  ws->nk = kpre[nq];
+  ws->base = cnt->next_id;
+  ws->kbase = cnt->nkids;
+}
+
+__global__ void k_zero_commit(WaveState* ws, const Counters* cnt) {
+  if (threadIdx.x || blockIdx.x) return;
+  ws->nwin = 0;
+  ws->nk = 0;
+  ws->base = cnt->next_id;
+  ws->kbase = cnt->nkids;
+}
+
+__global__ void k_counters_commit(WaveState* ws, Counters* cnt) {
+  if (threadIdx.x || blockIdx.x) return;
+  cnt->next_id += ws->nwin;
+  cnt->live += ws->nwin;
+  cnt->nkids += ws->nk;
+  if (ws->any_applied) cnt->dirty = 1;
 }
 
 // ---------------------------------------------------------------- host side
@@ -556,6 +689,8 @@ struct WaveBufs {
   DevBuf<u8> status, hazard;
   DevBuf<u32> env, olds, fl, pre, acc, ident, alloc, apre, wf, wpre, ka, kpre, stops, uother, fw_cls, fw_fresh;
   DevBuf<u8> ukind, grow, sa;
+  DevBuf<WaveState> ws;
+  DevBuf<DevStats> wstats;
   DevBuf<int> lvl;
   DevBuf<ReqT> tmpl;
   // wave table
@@ -665,6 +800,8 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     CUDA_OK(cudaMemcpyAsync(B.lvl.p, lvl_flat.data(), lvl_flat.size() * sizeof(int), cudaMemcpyHostToDevice, e.s));
   int skip_self = (hr.nsrc == 2 && !allow_self && hr.same_canon) ? 1 : 0;
   RuleStatsH& rs = e.rstats[ri];
+  B.wstats.ensure(1);
+  CUDA_OK(cudaMemsetAsync(B.wstats.p, 0, sizeof(DevStats), e.s));
   unsigned long long p = 0;
   u32 win = 1u << 12;  // adaptive candidate window (grows on clean waves, shrinks on dependencies)
   while (p < P) {
@@ -726,13 +863,6 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         seg_end = lastp + 1;
       }
     }
-    auto pos_of = [&](u32 c) -> unsigned long long {
-      if (!posp) return p + c;
-      unsigned long long v;
-      CUDA_OK(cudaMemcpyAsync(&v, posp + c, sizeof(v), cudaMemcpyDeviceToHost, e.s));
-      e.sync();
-      return v;
-    };
     if (ncand == 0) {
       // nothing compatible left: every remaining position is a self or compat skip
       unsigned long long cover = seg_end - p;
@@ -750,36 +880,30 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       p = seg_end;
       continue;
     }
-    // ---- 2. gates
+    // ---- 2. gates + accepted list
+    int Kmax = 0;
+    for (auto& q : tm) Kmax += q.nargs;
+    e.ensure_nodes((u64)ncand * R + 2, (u64)ncand * Kmax + 2);
     B.status.ensure(ncand + 1);
     B.hazard.ensure(ncand + 1);
     B.env.ensure((u64)ncand * MAX_VARS + 1);
     B.olds.ensure((u64)ncand * MAX_SRC + 1);
-    B.fl.ensure(ncand + 1);
     B.pre.ensure(ncand + 1);
     B.acc.ensure(ncand + 1);
-    {
-      KTimer kt(e, KG_APPLY_WAVE, 0.0, 3);
-      k_gates<<<nblk(ncand, 128), 128, 0, e.s>>>(e.view(), Rd, RD, W, posp, ncand, p, B.status.p, B.env.p, B.olds.p,
-                                                 B.hazard.p);
-      k_accept_flags<<<nblk(ncand), 256, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.fl.p);
-      dev_exclusive_scan_u32(e, B.fl.p, B.pre.p, ncand);
-      k_accept_list<<<nblk(ncand), 256, 0, e.s>>>(B.fl.p, B.pre.p, ncand, B.acc.p);
-    }
-    u32 nacc = read_u32(e, B.pre.p + ncand - 1) + read_u32(e, B.fl.p + ncand - 1);
-    // ---- 3. resolve requests level by level
-    u64 nreq = (u64)nacc * R;
-    B.ident.ensure(nreq + 1);
-    B.alloc.ensure(nacc + 1);
-    B.apre.ensure(nacc + 1);
-    B.ukind.ensure((u64)nacc * MAX_SRC + 1);
-    B.uother.ensure((u64)nacc * MAX_SRC + 1);
-    B.grow.ensure((u64)nacc * MAX_SRC + 1);
-    B.sa.ensure(nacc + 1);
+    B.ws.ensure(1);
+    WaveState* ws = B.ws.p;
+    u64 nreq_max = (u64)ncand * R;
+    B.ident.ensure(nreq_max + 1);
+    B.alloc.ensure(ncand + 1);
+    B.apre.ensure(ncand + 2);
+    B.ukind.ensure((u64)ncand * MAX_SRC + 1);
+    B.uother.ensure((u64)ncand * MAX_SRC + 1);
+    B.grow.ensure((u64)ncand * MAX_SRC + 1);
+    B.sa.ensure(ncand + 1);
     u32 used = 1;
-    if (R > 0 && nacc > 0) {
+    if (R > 0) {
       u32 want = 1024;
-      while (want < 2 * nreq + 16) want *= 2;
+      while (want < 2 * nreq_max + 16) want *= 2;
       if (want > B.wcap) {
         B.wcap = want;
         B.wstate.alloc(want);
@@ -788,78 +912,86 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         B.wroot.alloc(want);
         B.wold.alloc(want);
         B.wminpos.alloc(want);
-        B.wval.alloc(e.analysis ? want : 1);
+        B.wval.alloc(want);
       }
-      used = std::min<u32>(B.wcap, want);
+      used = want;
       CUDA_OK(cudaMemsetAsync(B.wstate.p, 0, (u64)used * sizeof(u32), e.s));
       CUDA_OK(cudaMemsetAsync(B.wroot.p, 0, (u64)used * sizeof(u32), e.s));
       CUDA_OK(cudaMemsetAsync(B.wminpos.p, 0xFF, (u64)used * sizeof(unsigned long long), e.s));
     }
     WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, used - 1, B.wold.p};
-    u32 bad = TSAT_NONE, sa_c = TSAT_NONE, cut_c = TSAT_NONE;
-    if (nacc > 0) {
-      KTimer kt(e, KG_APPLY_WAVE, 0.0, lv.size() + 6);
+    {
+      KTimer kt(e, KG_APPLY_WAVE, 0.0, 16 + lv.size());
+      k_gates<<<nblk(ncand, 128), 128, 0, e.s>>>(e.view(), Rd, RD, W, posp, ncand, p, B.status.p, B.env.p, B.olds.p,
+                                                 B.hazard.p);
+      k_accept_scan<<<1, 1024, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.pre.p, B.acc.p, ws);
+      // ---- 3. resolve requests level by level
       if (R > 0) {
         for (size_t d = 1; d < lv.size(); d++) {
           int nl = (int)lv[d].size();
           if (!nl) continue;
-          k_resolve_level<<<nblk((u64)nacc * nl, 128), 128, 0, e.s>>>(e.view(), W, T, B.acc.p, nacc,
-                                                                     B.lvl.p + lvl_off[d], nl, B.env.p, B.ident.p,
-                                                                     B.hazard.p);
+          k_resolve_level<<<nblk((u64)ncand * nl, 128), 128, 0, e.s>>>(e.view(), W, T, B.acc.p, ws,
+                                                                      B.lvl.p + lvl_off[d], nl, B.env.p, B.ident.p,
+                                                                      B.hazard.p);
         }
-        k_mark_roots<<<nblk(nacc), 256, 0, e.s>>>(W, T, B.acc.p, nacc, B.ident.p, B.hazard.p, B.olds.p);
+        k_mark_roots<<<nblk(ncand), 256, 0, e.s>>>(W, T, B.acc.p, ws, B.ident.p, B.hazard.p, B.olds.p);
       }
-      k_cand_check<<<nblk(nacc), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, nacc, B.ident.p, B.env.p, B.olds.p,
-                                                hr.nsrc > 1 ? 1 : 0, B.hazard.p, B.alloc.p, B.ukind.p,
-                                                B.uother.p, B.grow.p, B.sa.p);
-      // ---- 4. read/write conflicts, stop-after, node-limit cutoff
+      k_cand_check<<<nblk(ncand), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, ws, ncand, B.ident.p, B.env.p, B.olds.p,
+                                                 hr.nsrc > 1 ? 1 : 0, B.hazard.p, B.alloc.p, B.ukind.p, B.uother.p,
+                                                 B.grow.p, B.sa.p);
+      // ---- 4. read/write conflicts, stop-after, node-limit cutoff, boundary
       B.fw_cls.ensure((u64)e.h.next_id + 1);
       B.fw_fresh.ensure((u64)used + 1);
       CUDA_OK(cudaMemsetAsync(B.fw_cls.p, 0xFF, ((u64)e.h.next_id + 1) * sizeof(u32), e.s));
       CUDA_OK(cudaMemsetAsync(B.fw_fresh.p, 0xFF, ((u64)used + 1) * sizeof(u32), e.s));
-      k_first_writer<<<nblk(nacc), 256, 0, e.s>>>(W, B.acc.p, nacc, B.hazard.p, B.olds.p, B.ukind.p, B.uother.p,
-                                                  B.grow.p, B.fw_cls.p, B.fw_fresh.p);
+      k_first_writer<<<nblk(ncand), 256, 0, e.s>>>(W, B.acc.p, ws, B.hazard.p, B.olds.p, B.ukind.p, B.uother.p,
+                                                   B.grow.p, B.fw_cls.p, B.fw_fresh.p);
       B.stops.ensure(4);
       CUDA_OK(cudaMemsetAsync(B.stops.p, 0xFF, 3 * sizeof(u32), e.s));
       k_validity<<<nblk(ncand), 256, 0, e.s>>>(W, T, Rd.nslots, Rd.nsrc, ncand, B.hazard.p, B.env.p, B.olds.p, B.pre.p,
                                                B.status.p, B.ident.p, B.fw_cls.p, B.fw_fresh.p, B.stops.p + 2);
-      dev_exclusive_scan_u32(e, B.alloc.p, B.apre.p, nacc);
-      k_find_stops<<<nblk(nacc), 256, 0, e.s>>>(B.acc.p, nacc, B.sa.p, B.apre.p, B.alloc.p, (i64)e.h.live, n_max,
-                                                B.stops.p);
-      u32 hs[3];
-      CUDA_OK(cudaMemcpyAsync(hs, B.stops.p, sizeof(hs), cudaMemcpyDeviceToHost, e.s));
-      e.sync();
-      sa_c = hs[0];
-      cut_c = hs[1];
-      bad = hs[2];
+      k_scan_block<<<1, 1024, 0, e.s>>>(B.alloc.p, B.apre.p, ncand);
+      k_find_stops<<<nblk(ncand), 256, 0, e.s>>>(B.acc.p, ws, B.sa.p, B.apre.p, B.alloc.p, e.cnt.p, n_max, B.stops.p);
+      k_boundary<<<1, 1, 0, e.s>>>(ws, B.stops.p, ncand, posp, p, seg_end, B.pre.p, B.hazard.p);
+      // ---- 5. statistics of the committed segment (device accumulators)
+      k_seg_stats<<<nblk(ncand), 256, 0, e.s>>>(B.status.p, ws, ncand, B.pre.p, B.alloc.p, B.ukind.p, Rd.efficient,
+                                                B.wstats.p);
+      // ---- 6. commit
+      if (nreq_max) {
+        B.wf.ensure(nreq_max + 2);
+        B.wpre.ensure(nreq_max + 2);
+        B.ka.ensure(nreq_max + 2);
+        B.kpre.ensure(nreq_max + 2);
+        k_win_flags<<<nblk(nreq_max), 256, 0, e.s>>>(T, B.ident.p, nreq_max, B.tmpl.p, R, ws, B.wf.p, B.ka.p);
+        if (nreq_max <= (1u << 20)) {
+          k_scan_block<<<1, 1024, 0, e.s>>>(B.wf.p, B.wpre.p, (u32)nreq_max);
+          k_scan_block<<<1, 1024, 0, e.s>>>(B.ka.p, B.kpre.p, (u32)nreq_max);
+        } else {
+          CUDA_OK(cudaMemsetAsync(B.wf.p + nreq_max, 0, sizeof(u32), e.s));
+          CUDA_OK(cudaMemsetAsync(B.ka.p + nreq_max, 0, sizeof(u32), e.s));
+          dev_exclusive_scan_u32(e, B.wf.p, B.wpre.p, (u32)nreq_max + 1);
+          dev_exclusive_scan_u32(e, B.ka.p, B.kpre.p, (u32)nreq_max + 1);
+        }
+        k_commit_prep<<<1, 1, 0, e.s>>>(ws, B.wpre.p, B.kpre.p, nreq_max, e.cnt.p);
+        k_assign_ids<<<nblk(nreq_max), 256, 0, e.s>>>(T, B.ident.p, nreq_max, B.wf.p, B.wpre.p, ws);
+        k_write_nodes<<<nblk(nreq_max), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, B.ident.p, nreq_max, B.wf.p, B.wpre.p,
+                                                       B.kpre.p, ws, B.env.p, B.olds.p);
+      } else {
+        k_zero_commit<<<1, 1, 0, e.s>>>(ws, e.cnt.p);
+      }
+      k_commit_unions<<<nblk(ncand), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, ws, B.olds.p, B.ukind.p, B.uother.p,
+                                                    B.grow.p);
+      if (nreq_max) k_insert_range<<<nblk(nreq_max), 256, 0, e.s>>>(e.view(), ws, nreq_max);
+      k_counters_commit<<<1, 1, 0, e.s>>>(ws, e.cnt.p);
     }
-    // commit boundary in candidate space (exclusive end)
-    auto plus1 = [](u32 x) -> u64 { return x == TSAT_NONE ? (u64)1 << 40 : (u64)x + 1; };
-    u64 e_bad = bad == TSAT_NONE ? (u64)1 << 40 : (u64)bad;
-    u64 e_cut = plus1(cut_c), e_sa = plus1(sa_c);
-    u64 e_end = std::min<u64>(std::min(e_bad, std::min(e_cut, e_sa)), ncand);
-    u32 ncommit_cand = (u32)e_end;
-    bool stop = false, hazard = false;
-    unsigned long long p_end = seg_end;
-    if (e_cut <= e_end) {
-      p_end = pos_of(cut_c) + 1;
-      stop = true;
-    } else if (e_bad <= e_end) {
-      p_end = pos_of(bad);
-      u8 why;
-      CUDA_OK(cudaMemcpyAsync(&why, B.hazard.p + bad, 1, cudaMemcpyDeviceToHost, e.s));
-      e.sync();
-      e.phase_ms[10 + std::min<int>(why, 5)] += 1;  // 10: read-dirty, 11 gate, 12 make, 13 inner reuse, 14 intra, 15 merge
-      // a read-after-write dependency only needs a fresh evaluation: the next
-      // wave starts at this combo.  Other hazards run it on the exact path.
-      hazard = why != 0;
-    } else if (e_sa <= e_end) {
-      p_end = pos_of(sa_c) + 1;
-    }
-    u32 ncommit_acc = ncommit_cand == ncand ? nacc
-                                            : (ncommit_cand == 0 ? 0 : read_u32(e, B.pre.p + ncommit_cand));
-    // ---- 5. stats of the committed segment [p, p_end)
-    bool any_applied = false;
+    WaveState hw;
+    CUDA_OK(cudaMemcpyAsync(&hw, ws, sizeof(hw), cudaMemcpyDeviceToHost, e.s));
+    CUDA_OK(cudaMemcpyAsync(&e.h, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
+    e.sync();
+    u32 ncommit_cand = hw.ncommit_cand;
+    unsigned long long p_end = hw.p_end;
+    bool stop = hw.stop != 0, hazard = hw.hazard != 0;
+    if (hw.ncommit_cand < ncand && !stop) e.phase_ms[10 + std::min<int>(hw.why, 5)] += 1;
     {
       unsigned long long cover = p_end - p, self = 0;
       if (skip_self) {
@@ -873,51 +1005,6 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       rs.found += cover;
       rs.skipped_self += self;
       rs.skipped_compat += cover - self - ncommit_cand;
-      if (ncommit_cand) {
-        CUDA_OK(cudaMemsetAsync(e.dstats.p, 0, sizeof(DevStats), e.s));
-        k_seg_stats<<<nblk(ncommit_cand), 256, 0, e.s>>>(B.status.p, ncommit_cand, B.pre.p, B.alloc.p, B.ukind.p,
-                                                         Rd.efficient, e.dstats.p);
-        DevStats d;
-        CUDA_OK(cudaMemcpyAsync(&d, e.dstats.p, sizeof(d), cudaMemcpyDeviceToHost, e.s));
-        e.sync();
-        accumulate_seg(e, ri, d);
-        any_applied = d.applied > 0;
-      }
-    }
-    // ---- 6. commit
-    u64 creq = (u64)ncommit_acc * R;
-    u32 nwin = 0, nk = 0;
-    if (creq) {
-      B.wf.ensure(creq + 1);
-      B.wpre.ensure(creq + 1);
-      B.ka.ensure(creq + 1);
-      B.kpre.ensure(creq + 1);
-      k_win_flags<<<nblk(creq), 256, 0, e.s>>>(T, B.ident.p, creq, B.tmpl.p, R, B.wf.p, B.ka.p);
-      CUDA_OK(cudaMemsetAsync(B.wf.p + creq, 0, sizeof(u32), e.s));
-      CUDA_OK(cudaMemsetAsync(B.ka.p + creq, 0, sizeof(u32), e.s));
-      dev_exclusive_scan_u32(e, B.wf.p, B.wpre.p, (u32)creq + 1);
-      dev_exclusive_scan_u32(e, B.ka.p, B.kpre.p, (u32)creq + 1);
-      nwin = read_u32(e, B.wpre.p + creq);
-      nk = read_u32(e, B.kpre.p + creq);
-    }
-    if (nwin || (ncommit_acc && any_applied)) {
-      e.ensure_nodes(nwin, nk);
-      u32 base = e.h.next_id, kbase = e.h.nkids;
-      KTimer kt(e, KG_APPLY_WAVE, 0.0, 4);
-      if (nwin) {
-        k_assign_ids<<<nblk(creq), 256, 0, e.s>>>(T, B.ident.p, creq, B.wf.p, B.wpre.p, base);
-        k_write_nodes<<<nblk(creq), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, B.ident.p, creq, B.wf.p, B.wpre.p,
-                                                   B.kpre.p, base, kbase, B.env.p, B.olds.p);
-      }
-      k_commit_unions<<<nblk(ncommit_acc), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, ncommit_acc, B.olds.p, B.ukind.p,
-                                                          B.uother.p, B.grow.p);
-      if (nwin) k_insert_range<<<nblk(nwin), 256, 0, e.s>>>(e.view(), base, base + nwin);
-      e.h.next_id += nwin;
-      e.h.live += nwin;
-      e.h.nkids += nk;
-      if (any_applied) e.h.dirty = 1;
-      e.push_counters();
-      e.sync();
     }
     if (stop) {
       if (p_end < P) {
@@ -925,7 +1012,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         e.report.node_limit_overshoot = (i64)e.h.live - n_max;
       }
       p = p_end;
-      if (e.seq_stop) return;
+      if (e.seq_stop) break;
       continue;
     }
     // adapt the window: dependencies every k combos -> evaluate ~2k ahead
@@ -936,10 +1023,14 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       // exact sequential path for exactly the hazard combo
       e.ensure_nodes(4096, 4096);
       e.run_rule_seq(ri, filter_mode, allow_self, n_max, p_end, p_end + 1);
-      if (e.seq_stop) return;
+      if (e.seq_stop) break;
       p = p_end + 1;
       continue;
     }
     p = p_end;
   }
+  DevStats d;
+  CUDA_OK(cudaMemcpyAsync(&d, B.wstats.p, sizeof(d), cudaMemcpyDeviceToHost, e.s));
+  e.sync();
+  accumulate_seg(e, ri, d);
 }

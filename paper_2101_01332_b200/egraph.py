@@ -239,7 +239,15 @@ class EGraph:
 
     @property
     def num_classes(self) -> int:
-        return len(self.view.classes)
+        out = C.c_uint32()
+        _lib.check(self._h, _lib.load().tsat_num_classes(self._h, C.byref(out)))
+        return out.value
+
+    def _alive_flags(self) -> np.ndarray:
+        n = self._sizes()[0]
+        fl = np.zeros(max(n, 1), np.uint8)
+        _lib.check(self._h, _lib.load().tsat_download_flags(self._h, _lib.ptr(fl, C.c_uint8)))
+        return (fl[:n] & 1).astype(bool)
 
     @property
     def allocated_nodes(self) -> int:
@@ -451,29 +459,40 @@ class EGraph:
                                                _lib.ptr(out, C.c_double)))
         else:
             _lib.check(self._h, lib.tsat_costs(self._h, 0, 0, 0, b"\0", None, None, _lib.ptr(out, C.c_double)))
-        return CostVector(self, out[:n], self.view.alive.copy())
+        return CostVector(self, out[:n], None)
 
 
 class CostVector(Mapping):
-    """c_i per live node id (dict-like), backed by the device vector."""
+    """c_i per live node id (dict-like), backed by the device vector; the
+    live-node index is fetched lazily (only flags are downloaded)."""
 
-    def __init__(self, eg: EGraph, arr: np.ndarray, alive: np.ndarray):
+    def __init__(self, eg: EGraph, arr: np.ndarray, alive):
         self._eg = eg
         self.array = arr
         self._alive = alive
-        self._ids = np.nonzero(alive)[0]
+        self._ids = None
+
+    def _index(self):
+        if self._alive is None:
+            self._alive = self._eg._alive_flags()[: len(self.array)]
+        if self._ids is None:
+            self._ids = np.nonzero(self._alive)[0]
+        return self._ids
 
     def __getitem__(self, nid):
         nid = int(nid)
-        if nid < 0 or nid >= len(self.array) or not self._alive[nid]:
+        if nid < 0 or nid >= len(self.array):
+            raise KeyError(nid)
+        self._index()
+        if not self._alive[nid]:
             raise KeyError(nid)
         return float(self.array[nid])
 
     def __iter__(self):
-        return (int(i) for i in self._ids)
+        return (int(i) for i in self._index())
 
     def __len__(self):
-        return len(self._ids)
+        return len(self._index())
 
 
 def _slot(v: str, env, slots: dict, envl: list) -> int:

@@ -144,7 +144,8 @@ def saturate(
     report.postprocess_filtered = int(rep.postprocess_filtered)
     report.node_limit_overshoot = int(rep.node_limit_overshoot)
     report.time_s = float(rep.time_s)
-    extra = {x for x in filt if not (0 <= int(x) < eg.allocated_nodes)}
+    n_alloc = eg.allocated_nodes
+    extra = {x for x in filt if not (0 <= int(x) < n_alloc)}
     filt.clear()
     dev = eg.get_filter()
     eg._filt_dev = frozenset(dev)

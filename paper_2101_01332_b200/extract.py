@@ -72,8 +72,7 @@ def greedy_extract(eg: EGraph, costs: Mapping, filt: Iterable[int] = ()) -> Extr
     arr = None
     if not (isinstance(costs, CostVector) and costs._eg is eg and len(costs.array) == n):
         arr = np.zeros(max(n, 1), np.float64)
-        alive = eg.view.alive
-        for nid in np.nonzero(alive)[0]:
+        for nid in np.nonzero(eg._alive_flags())[0]:
             arr[nid] = costs[int(nid)]
     cap = max(eg.num_classes, 1)
     sc = np.zeros(cap, np.uint32)
@@ -83,9 +82,13 @@ def greedy_extract(eg: EGraph, costs: Mapping, filt: Iterable[int] = ()) -> Extr
     rounds = C.c_int64()
     _lib.check(eg._h, lib.tsat_greedy(eg._h, _lib.ptr(arr, C.c_double), _lib.ptr(sc, C.c_uint32),
                                       _lib.ptr(sn, C.c_uint32), C.byref(k), C.byref(best), C.byref(rounds)))
-    selection = {int(c): int(m) for c, m in zip(sc[: k.value], sn[: k.value])}
+    selection = dict(zip(sc[: k.value].tolist(), sn[: k.value].tolist()))
+    if isinstance(costs, CostVector) and costs._eg is eg:
+        total = float(sum(costs.array[list(set(selection.values()))].tolist()))
+    else:
+        total = selection_cost(costs, selection)
     stats = SolverStats(nodes_explored=int(rounds.value), time_s=time.perf_counter() - t0)
-    return ExtractionResult(selection, selection_cost(costs, selection), stats=stats)
+    return ExtractionResult(selection, total, stats=stats)
 
 
 def reconstruct(eg: EGraph, selection: Mapping) -> TensorGraph:
