@@ -71,6 +71,9 @@ int tsat_add_terms(tsat_engine* h, int32_t ninstr, const int32_t* instr, int32_t
                    const int32_t* term_len, int32_t nenv, const uint32_t* env, uint32_t* out_class);
 int tsat_union(tsat_engine* h, uint32_t a, uint32_t b, uint32_t* out_root); /* egraph.py:193 */
 int tsat_rebuild(tsat_engine* h);                                            /* egraph.py:216 */
+/* benchmark hooks: one full congruence round even when clean; a batch of unions */
+int tsat_force_rebuild(tsat_engine* h);
+int tsat_union_batch(tsat_engine* h, int64_t n, const uint32_t* a, const uint32_t* b);
 int tsat_find(tsat_engine* h, uint32_t x, uint32_t* out);                    /* egraph.py:143 */
 int tsat_set_root(tsat_engine* h, uint32_t root);                            /* EGraph.root   */
 

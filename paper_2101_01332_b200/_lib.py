@@ -45,6 +45,8 @@ _SIGS = {
     "tsat_add_terms": ([C.c_void_p, C.c_int32, i32p, C.c_int32, i32p, C.c_int32, u32p, u32p], C.c_int),
     "tsat_union": ([C.c_void_p, C.c_uint32, C.c_uint32, u32p], C.c_int),
     "tsat_rebuild": ([C.c_void_p], C.c_int),
+    "tsat_force_rebuild": ([C.c_void_p], C.c_int),
+    "tsat_union_batch": ([C.c_void_p, C.c_int64, u32p, u32p], C.c_int),
     "tsat_find": ([C.c_void_p, C.c_uint32, u32p], C.c_int),
     "tsat_set_root": ([C.c_void_p, C.c_uint32], C.c_int),
     "tsat_query_sizes": ([C.c_void_p, u32p, u32p, u32p, u32p, u32p], C.c_int),

@@ -111,6 +111,22 @@ int tsat_union(tsat_engine* h, uint32_t a, uint32_t b, uint32_t* out_root) {
 
 int tsat_rebuild(tsat_engine* h) { GUARD(h, h->e->rebuild()); }
 
+int tsat_force_rebuild(tsat_engine* h) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    e.h.dirty = 1;
+    e.push_counters();
+    e.rebuild();
+  });
+}
+
+int tsat_union_batch(tsat_engine* h, int64_t n, const uint32_t* a, const uint32_t* b) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    for (int64_t i = 0; i < n; i++) e.union_pair(a[i], b[i]);
+  });
+}
+
 int tsat_find(tsat_engine* h, uint32_t x, uint32_t* out) { GUARD(h, *out = h->e->find(x)); }
 
 int tsat_set_root(tsat_engine* h, uint32_t root) {

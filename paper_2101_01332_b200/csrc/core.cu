@@ -277,6 +277,32 @@ __global__ void k_init_nodes(G g, u32 n) {
   }
 }
 
+__device__ __forceinline__ void make_one(const G& g, u32 nid) {
+  u32 a = g.koff[nid], b = g.koff[nid + 1];
+  int k = (int)(b - a);
+  Val kv[7];
+  if (k > 7) {
+    dev_set_error(g.err, TSAT_ERR_SHAPE, 3, nid, g.op[nid]);
+    return;
+  }
+  for (int j = 0; j < k; j++) kv[j] = g.val[g.kids[a + j]];
+  Val v;
+  int st = val_make(g.op[nid], kv, k, v, g.atoms, g.tt);
+  if (st != AS_OK) {
+    dev_set_error(g.err, ana_to_status(st), 3, nid, g.op[nid]);
+    return;
+  }
+  g.val[nid] = v;
+}
+
+// consecutive thin levels [l0, l1) in one CTA (deep noop chains are common)
+__global__ void __launch_bounds__(256) k_make_levels(G g, const u32* ids, const u32* off, u32 l0, u32 l1) {
+  for (u32 l = l0; l < l1; l++) {
+    for (u32 t = off[l] + threadIdx.x; t < off[l + 1]; t += blockDim.x) make_one(g, ids[t]);
+    __syncthreads();
+  }
+}
+
 // analysis values for the nodes of one depth level (children already valued)
 __global__ void k_make_level(G g, const u32* ids, u32 n) {
   GRID_STRIDE(t, n) {
@@ -337,9 +363,22 @@ void Engine::load_initial(u32 n, const u32* hop, const u32* hkoff, const u32* hk
       flat.insert(flat.end(), v.begin(), v.end());
     }
     CUDA_OK(cudaMemcpyAsync(ids.p, flat.data(), flat.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
-    for (size_t l = 0; l < by.size(); l++)
-      if (!by[l].empty())
+    off.push_back(flat.size());
+    std::vector<u32> off32(off.begin(), off.end());
+    DevBuf<u32>& doff = scratch_u32[1];
+    doff.ensure(off32.size() + 1);
+    CUDA_OK(cudaMemcpyAsync(doff.p, off32.data(), off32.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
+    for (size_t l = 0; l < by.size();) {
+      if (by[l].size() > 256) {
         k_make_level<<<nblk(by[l].size()), 128, 0, s>>>(view(), ids.p + off[l], (u32)by[l].size());
+        l++;
+        continue;
+      }
+      size_t l1 = l;
+      while (l1 < by.size() && by[l1].size() <= 256) l1++;
+      k_make_levels<<<1, 256, 0, s>>>(view(), ids.p, doff.p, (u32)l, (u32)l1);
+      l = l1;
+    }
     sync();
   }
   root = r;
@@ -645,8 +684,22 @@ __global__ void k_class_index(const u32* scls, const u32* headpos, u32 m, u32* c
 
 __global__ void k_set_u32(u32* p, u32 idx, u32 v) { p[idx] = v; }
 
-__global__ void k_op_hist(const u32* ops, u32 m, u32* hist) {
-  GRID_STRIDE(i, m) atomicAdd(&hist[ops[i]], 1u);
+// off[a] = first position of key >= a in a sorted key array (CSR offsets)
+__global__ void k_lower_bounds(const u32* sorted, u32 m, u32 nkeys, u32* off) {
+  GRID_STRIDE(a, (u64)nkeys + 1) {
+    u32 lo = 0, hi = m;
+    while (lo < hi) {
+      u32 mid = (lo + hi) >> 1;
+      if (sorted[mid] < (u32)a) lo = mid + 1;
+      else hi = mid;
+    }
+    off[a] = lo;
+  }
+}
+
+// dense class index of every member position (for member-parallel passes)
+__global__ void k_member_class(const u32* head, const u32* pos, u32 m, u32* cls_of) {
+  GRID_STRIDE(i, m) cls_of[i] = pos[i] + head[i] - 1;
 }
 
 void Engine::build_snapshot() {
@@ -688,13 +741,13 @@ void Engine::build_snapshot() {
   snap.cls_ids.ensure(ncls + 1);
   k_class_index<<<nblk(m), 256, 0, s>>>(tmp.p, pos.p, m, snap.cls_off.p, snap.cls_ids.p, snap.cls_index.p);
   k_set_u32<<<1, 1, 0, s>>>(snap.cls_off.p, ncls, m);
+  snap.cls_of.ensure(m + 1);
+  k_member_class<<<nblk(m), 256, 0, s>>>(fl.p, pos.p, m, snap.cls_of.p);
   // op CSR: stable sort alive ids by op atom
   snap.op_nodes.ensure(m + 1);
   snap.op_off.ensure(na + 1);
-  CUDA_OK(cudaMemsetAsync(fl.p, 0, (size_t)(na + 1) * sizeof(u32), s));
-  k_op_hist<<<nblk(m), 256, 0, s>>>(opk.p, m, fl.p);
-  dev_exclusive_scan_u32(*this, fl.p, snap.op_off.p, na + 1);
   dev_sort_pairs_u32(*this, opk.p, tmp.p, ids.p, snap.op_nodes.p, m, bits_for(na));
+  k_lower_bounds<<<nblk((u64)na + 1), 256, 0, s>>>(tmp.p, m, na, snap.op_off.p);
   snap.n_alloc = n;
   snap.ncls = ncls;
   snap.n_atoms = na;

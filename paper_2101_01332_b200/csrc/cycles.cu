@@ -34,33 +34,42 @@ static inline unsigned nblk(u64 n, unsigned t = 256) {
 }
 #define GRID_STRIDE(i, n) for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < (n); i += (u64)gridDim.x * blockDim.x)
 
-// per class: number of edges through live, unfiltered members
-__global__ void k_edge_count(G g, const u32* cls_off, const u32* cls_nodes, u32 ncls, u32* cnt) {
-  GRID_STRIDE(i, ncls) {
-    u32 c = 0;
-    for (u32 k = cls_off[i]; k < cls_off[i + 1]; k++) {
-      u32 m = cls_nodes[k];
-      if (g.flags[m] & NF_FILT) continue;
-      c += g.koff[m + 1] - g.koff[m];
-    }
-    cnt[i] = c;
+// edges through live, unfiltered members: member-parallel (classes can have
+// thousands of members)
+__global__ void k_member_deg(G g, const u32* cls_nodes, u32 m, u32* deg) {
+  GRID_STRIDE(k, m) {
+    u32 x = cls_nodes[k];
+    deg[k] = (g.flags[x] & NF_FILT) ? 0u : g.koff[x + 1] - g.koff[x];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[ncls] = 0;
 }
 
-__global__ void k_edge_fill(G g, const u32* cls_off, const u32* cls_nodes, const u32* cls_index, u32 ncls,
-                            const u32* eoff, u32* edst, u32* esrc) {
-  GRID_STRIDE(i, ncls) {
-    u32 o = eoff[i];
-    for (u32 k = cls_off[i]; k < cls_off[i + 1]; k++) {
-      u32 m = cls_nodes[k];
-      if (g.flags[m] & NF_FILT) continue;
-      for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) {
-        edst[o] = cls_index[uf_find_ro(g.parent, g.kids[j])];
-        esrc[o] = (u32)i;
-        o++;
-      }
+__global__ void k_member_fill(G g, const u32* cls_nodes, const u32* cls_of, const u32* cls_index, u32 m,
+                              const u32* moff, u32* edst, u32* esrc) {
+  GRID_STRIDE(k, m) {
+    u32 x = cls_nodes[k];
+    if (g.flags[x] & NF_FILT) continue;
+    u32 o = moff[k], c = cls_of[k];
+    for (u32 j = g.koff[x]; j < g.koff[x + 1]; j++) {
+      edst[o] = cls_index[uf_find_ro(g.parent, g.kids[j])];
+      esrc[o] = c;
+      o++;
     }
+  }
+}
+
+__global__ void k_class_eoff(const u32* cls_off, const u32* moff, u32 n, u32* eoff) {
+  GRID_STRIDE(c, (u64)n + 1) eoff[c] = moff[cls_off[c]];
+}
+
+__global__ void k_lower_bounds2(const u32* sorted, u32 m, u32 nkeys, u32* off) {
+  GRID_STRIDE(a, (u64)nkeys + 1) {
+    u32 lo = 0, hi = m;
+    while (lo < hi) {
+      u32 mid = (lo + hi) >> 1;
+      if (sorted[mid] < (u32)a) lo = mid + 1;
+      else hi = mid;
+    }
+    off[a] = lo;
   }
 }
 
@@ -103,14 +112,16 @@ __global__ void k_untrimmed(const u32* level, u32 n, const u8* mask, u32* list, 
 void build_class_graph(Engine& e) {
   Snapshot& S = e.snap;
   Scratch& X = e.sc;
-  u32 n = S.ncls;
+  u32 n = S.ncls, m = e.h.live;
   X.cg_eoff.ensure(n + 1);
-  DevBuf<u32>& cnt = X.cg_outdeg;  // reused as count buffer here
-  cnt.ensure(n + 1);
-  k_edge_count<<<nblk(n), 256, 0, e.s>>>(e.view(), S.cls_off.p, S.cls_nodes.p, n, cnt.p);
-  dev_exclusive_scan_u32(e, cnt.p, X.cg_eoff.p, n + 1);
+  X.cg_mdeg.ensure(m + 1);
+  X.cg_moff.ensure(m + 1);
+  k_member_deg<<<nblk(m), 256, 0, e.s>>>(e.view(), S.cls_nodes.p, m, X.cg_mdeg.p);
+  CUDA_OK(cudaMemsetAsync(X.cg_mdeg.p + m, 0, sizeof(u32), e.s));
+  dev_exclusive_scan_u32(e, X.cg_mdeg.p, X.cg_moff.p, m + 1);
+  k_class_eoff<<<nblk((u64)n + 1), 256, 0, e.s>>>(S.cls_off.p, X.cg_moff.p, n, X.cg_eoff.p);
   u32 ne;
-  CUDA_OK(cudaMemcpyAsync(&ne, X.cg_eoff.p + n, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+  CUDA_OK(cudaMemcpyAsync(&ne, X.cg_moff.p + m, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
   e.sync();
   e.cg_n = n;
   e.cg_ne = ne;
@@ -119,12 +130,10 @@ void build_class_graph(Engine& e) {
   X.cg_sdst.ensure(ne + 1);
   X.cg_rsrc.ensure(ne + 1);
   X.cg_roff.ensure(n + 1);
-  k_edge_fill<<<nblk(n), 256, 0, e.s>>>(e.view(), S.cls_off.p, S.cls_nodes.p, S.cls_index.p, n, X.cg_eoff.p,
-                                        X.cg_edst.p, X.cg_esrc.p);
+  k_member_fill<<<nblk(m), 256, 0, e.s>>>(e.view(), S.cls_nodes.p, S.cls_of.p, S.cls_index.p, m, X.cg_moff.p,
+                                          X.cg_edst.p, X.cg_esrc.p);
   if (ne) dev_sort_pairs_u32(e, X.cg_edst.p, X.cg_sdst.p, X.cg_esrc.p, X.cg_rsrc.p, ne, bits_for(n));
-  CUDA_OK(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(u32), e.s));
-  k_rhist<<<nblk(ne), 256, 0, e.s>>>(X.cg_edst.p, ne, cnt.p);
-  dev_exclusive_scan_u32(e, cnt.p, X.cg_roff.p, n + 1);
+  k_lower_bounds2<<<nblk((u64)n + 1), 256, 0, e.s>>>(X.cg_sdst.p, ne, n, X.cg_roff.p);
   X.cg_outdeg.ensure(n + 1);
   X.cg_level.ensure(n + 1);
 }
@@ -295,13 +304,13 @@ i64 Engine::break_all_cycles(bool precheck_only, std::vector<std::vector<u32>>* 
     sc.c_mark.ensure(n + 1);
     sc.c_mark32.ensure(n + 1);
     sc.c_fa.ensure(n + 1);
-    sc.c_res.ensure(8);
+    sc.c_res.ensure(16);
     bfs_classes(*this, root_dense, sc.c_mark32.p, sc.c_fa.p);
     k_mark8<<<nblk(n), 256, 0, s>>>(sc.c_mark32.p, n, sc.c_mark.p);
-    CUDA_OK(cudaMemsetAsync(sc.c_res.p + 6, 0, sizeof(u32), s));
-    k_count_cyclic<<<nblk(n), 256, 0, s>>>(sc.c_mark.p, sc.cg_level.p, n, sc.c_res.p + 6);
+    CUDA_OK(cudaMemsetAsync(sc.c_res.p + 12, 0, sizeof(u32), s));
+    k_count_cyclic<<<nblk(n), 256, 0, s>>>(sc.c_mark.p, sc.cg_level.p, n, sc.c_res.p + 12);
     u32 ncyc_cls;
-    CUDA_OK(cudaMemcpyAsync(&ncyc_cls, sc.c_res.p + 6, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(&ncyc_cls, sc.c_res.p + 12, sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
     if (ncyc_cls == 0) return added;
     if (precheck_only) return -1;

@@ -126,6 +126,7 @@ struct Snapshot {
   DevBuf<u32> cls_ids;    // dense -> class id
   DevBuf<u32> cls_off;    // dense -> member range
   DevBuf<u32> cls_nodes;  // members (alive nodes), ascending per class
+  DevBuf<u32> cls_of;     // dense class of each member position
   DevBuf<u32> op_off;     // atom -> range in op_nodes
   DevBuf<u32> op_nodes;
   bool valid = false;
@@ -173,8 +174,8 @@ struct Scratch {
   // e-matching
   DevBuf<u32> m_rc, m_rb, m_cnt, m_perm, m_perm2, m_key, m_key2, m_fl, m_pos;
   // class graph / cycles / reach
-  DevBuf<u32> cg_eoff, cg_edst, cg_enode, cg_roff, cg_rsrc, cg_outdeg, cg_level, cg_esrc, cg_sdst;
-  DevBuf<u32> c_mark32, c_fa, c_fb, c_order, c_depth, c_path, c_cycn, c_cyco, c_res, c_rest, c_lvloff;
+  DevBuf<u32> cg_eoff, cg_edst, cg_enode, cg_roff, cg_rsrc, cg_outdeg, cg_level, cg_esrc, cg_sdst, cg_moff, cg_mdeg;
+  DevBuf<u32> c_heavy, c_mark32, c_fa, c_fb, c_order, c_depth, c_path, c_cycn, c_cyco, c_res, c_rest, c_lvloff;
   DevBuf<u8> c_mark, c_color;
   DevBuf<unsigned char> c_stack;
   // greedy / costs

@@ -595,14 +595,14 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
   const u32 *co = snap.cls_off.p, *cn = snap.cls_nodes.p, *ci = snap.cls_index.p, *ord = sc.c_order.p,
             *lvl = sc.c_lvloff.p;
   for (u32 l = 0; l < nl;) {
-    if (lo[l + 1] - lo[l] > 16384) {
+    if (lo[l + 1] - lo[l] > 64) {
       k_greedy_level_wide<<<nblk((u64)(lo[l + 1] - lo[l]) * 32, 256), 256, 0, s>>>(gv, co, cn, ci, ord, lo[l],
                                                                                     lo[l + 1], cost, c0.p, n0.p);
       l++;
       continue;
     }
     u32 l1 = l;
-    while (l1 < nl && lo[l1 + 1] - lo[l1] <= 16384) l1++;
+    while (l1 < nl && lo[l1 + 1] - lo[l1] <= 64) l1++;
     k_greedy_levels<<<1, 1024, 0, s>>>(gv, co, cn, ci, ord, lvl, l, l1, cost, c0.p, n0.p);
     l = l1;
   }

@@ -23,7 +23,8 @@ static inline unsigned nblk(u64 n, unsigned t = 256) {
 }
 #define GRID_STRIDE(i, n) for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < (n); i += (u64)gridDim.x * blockDim.x)
 
-// ctl layout: [0] tail, [1] level, [2] start, [3] end, [4] done, [5] overflow flag
+// ctl layout: [0] tail, [1] level, [2] start, [3] end, [4] done, [5] unused,
+// [6] edge count of the current frontier, [7] of the next frontier, [8] heavy list size
 struct Frontier {
   const u32* eoff;  // forward CSR (BFS) or outdeg source (trim)
   const u32* edst;
@@ -41,16 +42,25 @@ struct Frontier {
 
 #define HEAVY 32u
 
-__device__ __forceinline__ void frontier_edge(const Frontier& F, u32 e, u32 lvl, u32* tail) {
+__device__ __forceinline__ u32 vdeg(const Frontier& F, u32 j) {
+  return F.bfs ? F.eoff[j + 1] - F.eoff[j] : F.roff[j + 1] - F.roff[j];
+}
+
+// ctl[0] = queue tail, ctl[7] = edge count of the next frontier
+__device__ __forceinline__ void frontier_edge(const Frontier& F, u32 e, u32 lvl, u32* ctl) {
   if (F.bfs) {
     u32 k = F.edst[e];
-    if (F.mark[k] == 0 && atomicCAS(&F.mark[k], 0u, 1u) == 0u) F.order[atomicAdd(tail, 1u)] = k;
+    if (F.mark[k] == 0 && atomicCAS(&F.mark[k], 0u, 1u) == 0u) {
+      F.order[atomicAdd(&ctl[0], 1u)] = k;
+      atomicAdd(&ctl[7], vdeg(F, k));
+    }
   } else {
     u32 i = F.rsrc[e];
     if (F.mask && !F.mask[i]) return;
     if (atomicSub(&F.outdeg[i], 1u) == 1u) {
       F.level[i] = lvl + 1;
-      F.order[atomicAdd(tail, 1u)] = i;
+      F.order[atomicAdd(&ctl[0], 1u)] = i;
+      atomicAdd(&ctl[7], vdeg(F, i));
     }
   }
 }
@@ -78,11 +88,13 @@ __global__ void k_frontier_init(Frontier F, u32* ctl, u32 root) {
     if (d == 0) {
       F.level[i] = 0;
       F.order[atomicAdd(&ctl[0], 1u)] = (u32)i;
+      atomicAdd(&ctl[7], vdeg(F, (u32)i));
     }
   }
   if (F.bfs && blockIdx.x == 0 && threadIdx.x == 0) {
     F.order[0] = root;
     ctl[0] = 1;
+    ctl[7] = vdeg(F, root);
   }
 }
 
@@ -91,22 +103,26 @@ __global__ void k_frontier_start(u32* ctl, u32* lvl_off) {
   ctl[2] = 0;
   ctl[3] = ctl[0];
   ctl[4] = 0;
+  ctl[6] = ctl[7];
+  ctl[7] = 0;
   if (lvl_off) {
     lvl_off[0] = 0;
     lvl_off[1] = ctl[0];
   }
 }
 
-// thin levels inside one CTA; exits when a frontier gets wide.  Vertices with
-// more than HEAVY edges are queued and their edge lists are swept by the whole
-// CTA (hub classes such as shared literals have thousands of parents).
+// thin levels inside one CTA; exits when a frontier gets wide (by edges).
+// Vertices with more than HEAVY edges are queued and their edge lists are
+// swept by the whole CTA.
+#define LV_EDGES 65536u
 __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ctl) {
-  __shared__ u32 s_start, s_end, s_lvl, s_nheavy;
+  __shared__ u32 s_start, s_end, s_lvl, s_nheavy, s_edges;
   __shared__ u32 s_heavy[LV_BLOCK];
   if (threadIdx.x == 0) {
     s_start = ctl[2];
     s_end = ctl[3];
     s_lvl = ctl[1];
+    s_edges = ctl[6];
   }
   __syncthreads();
   while (true) {
@@ -115,7 +131,7 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
       if (threadIdx.x == 0) ctl[4] = 1;
       break;
     }
-    if (end - start > LV_WIDE) break;
+    if (end - start > LV_WIDE || s_edges > LV_EDGES) break;
     for (u32 t0 = start; t0 < end; t0 += blockDim.x) {
       if (threadIdx.x == 0) s_nheavy = 0;
       __syncthreads();
@@ -125,13 +141,13 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
         edge_range(F, j, a, b);
         if (b - a > HEAVY) s_heavy[atomicAdd(&s_nheavy, 1u)] = j;
         else
-          for (u32 e = a; e < b; e++) frontier_edge(F, e, lvl, &ctl[0]);
+          for (u32 e = a; e < b; e++) frontier_edge(F, e, lvl, ctl);
       }
       __syncthreads();
       for (u32 h = 0; h < s_nheavy; h++) {
         u32 a, b;
         edge_range(F, s_heavy[h], a, b);
-        for (u32 e = a + threadIdx.x; e < b; e += blockDim.x) frontier_edge(F, e, lvl, &ctl[0]);
+        for (u32 e = a + threadIdx.x; e < b; e += blockDim.x) frontier_edge(F, e, lvl, ctl);
       }
       __syncthreads();
     }
@@ -141,6 +157,8 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
       s_start = end;
       s_end = ne;
       s_lvl = lvl + 1;
+      s_edges = ((volatile u32*)ctl)[7];
+      ctl[7] = 0;
       if (F.lvl_off) F.lvl_off[lvl + 2] = ne;
     }
     __syncthreads();
@@ -149,34 +167,54 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
     ctl[1] = s_lvl;
     ctl[2] = s_start;
     ctl[3] = s_end;
+    ctl[6] = s_edges;
   }
 }
 
-// wide levels on the whole GPU; exits when the frontier gets thin again
-__global__ void k_frontier_grid(Frontier F, u32* ctl) {
+// wide levels on the whole GPU; exits when the frontier gets thin again.
+// Light vertices: one warp each.  Heavy vertices (> 1024 edges, e.g. shared
+// literals with millions of parents): the whole grid sweeps their edges.
+__global__ void k_frontier_grid(Frontier F, u32* ctl, u32* heavy) {
   cg::grid_group grid = cg::this_grid();
-  u32 start = ctl[2], end = ctl[3], lvl = ctl[1];
+  u32 start = ctl[2], end = ctl[3], lvl = ctl[1], edges = ctl[6];
   u32 lane = threadIdx.x & 31;
   u64 warp = grid.thread_rank() >> 5, nwarp = grid.size() >> 5;
-  while (start < end && end - start > LV_WIDE / 4) {
-    // one warp per frontier vertex: edge lists are swept 32-wide
+  while (start < end && (end - start > LV_WIDE / 4 || edges > LV_EDGES / 4)) {
+    if (grid.thread_rank() == 0) ctl[8] = 0;
+    grid.sync();
     for (u64 t = start + warp; t < end; t += nwarp) {
+      u32 j = F.order[t], a, b;
+      edge_range(F, j, a, b);
+      if (b - a > 1024) {
+        if (lane == 0) heavy[atomicAdd(&ctl[8], 1u)] = j;
+        continue;
+      }
+      for (u32 e = a + lane; e < b; e += 32) frontier_edge(F, e, lvl, ctl);
+    }
+    grid.sync();
+    u32 nh = ((volatile u32*)ctl)[8];
+    for (u32 h = 0; h < nh; h++) {
       u32 a, b;
-      edge_range(F, F.order[t], a, b);
-      for (u32 e = a + lane; e < b; e += 32) frontier_edge(F, e, lvl, &ctl[0]);
+      edge_range(F, heavy[h], a, b);
+      for (u64 e = a + grid.thread_rank(); e < b; e += grid.size()) frontier_edge(F, (u32)e, lvl, ctl);
     }
     grid.sync();
     u32 ne = ((volatile u32*)ctl)[0];
+    u32 ned = ((volatile u32*)ctl)[7];
     if (grid.thread_rank() == 0 && F.lvl_off) F.lvl_off[lvl + 2] = ne;
     start = end;
     end = ne;
+    edges = ned;
     lvl++;
+    grid.sync();
+    if (grid.thread_rank() == 0) ctl[7] = 0;
     grid.sync();
   }
   if (grid.thread_rank() == 0) {
     ctl[1] = lvl;
     ctl[2] = start;
     ctl[3] = end;
+    ctl[6] = edges;
     if (start >= end) ctl[4] = 1;
   }
 }
@@ -192,8 +230,10 @@ static int coop_blocks(Engine& e, const void* fn, int threads) {
 // runs the frontier to completion; returns (levels, total processed)
 static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& total) {
   DevBuf<u32>& ctl = e.sc.c_res;
-  ctl.ensure(8);
-  CUDA_OK(cudaMemsetAsync(ctl.p, 0, 8 * sizeof(u32), e.s));
+  ctl.ensure(16);
+  CUDA_OK(cudaMemsetAsync(ctl.p, 0, 16 * sizeof(u32), e.s));
+  DevBuf<u32>& heavy = e.sc.c_heavy;
+  heavy.ensure(F.n + 1);
   k_frontier_init<<<nblk(F.n), 256, 0, e.s>>>(F, ctl.p, root);
   k_frontier_start<<<1, 1, 0, e.s>>>(ctl.p, F.lvl_off);
   static int gblocks = 0;
@@ -205,7 +245,8 @@ static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& tot
     e.sync();
     if (h[4]) break;
     u32* c = ctl.p;
-    void* args[] = {&F, &c};
+    u32* hv = heavy.p;
+    void* args[] = {&F, &c, &hv};
     CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_frontier_grid, gblocks, 256, args, 0, e.s));
     CUDA_OK(cudaMemcpyAsync(h, ctl.p, 5 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
     e.sync();

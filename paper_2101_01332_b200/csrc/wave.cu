@@ -48,7 +48,7 @@ RuleDev make_rule_dev(Engine& e, int ri, int filter_mode, int allow_self);
 ReachDev make_reach_dev(Engine& e);
 
 struct WaveState {
-  u32 nacc, ncommit_cand, ncommit_acc, nwin, nk, base, kbase, stop, hazard, why, any_applied, pad;
+  u32 nacc, ncommit_cand, ncommit_acc, nwin, nk, base, kbase, stop, hazard, why, any_applied, sa_hit;
   unsigned long long p_end;
 };
 
@@ -97,39 +97,50 @@ __global__ void k_hash_rows(G g, const u32* bind, int nb, u32 n, WaveRule W, int
   }
 }
 
-// count (emit=false) or write (emit=true) compatible positions for rows i >= i0
+// Compatible positions for rows i >= i0, one warp per row: lanes test 32
+// candidates of the equal-hash range at a time, a ballot keeps the emitted
+// positions in j order (itertools.product order).  count pass: cnt[row];
+// emit pass: out[off[row] + k] (capped at cap).
 __global__ void k_join(G g, RuleDev R, WaveRule W, const u64* hA, u32 i0, const u64* hBs, const u32* iBs,
                        unsigned long long p_start, int skip_self, const u32* off, u32* cnt,
                        unsigned long long* out, u32 cap) {
-  GRID_STRIDE(t, (u64)(R.nmatch[0] - i0)) {
+  u32 lane = threadIdx.x & 31;
+  u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  u32 nB = R.nmatch[1];
+  for (u64 t = warp; t < (u64)(R.nmatch[0] - i0); t += nw) {
     u32 i = i0 + (u32)t;
     u64 h = hA[t];
-    u32 nB = R.nmatch[1];
-    // lower bound
     u32 lo = 0, hi = nB;
     while (lo < hi) {
       u32 mid = (lo + hi) >> 1;
       if (hBs[mid] < h) lo = mid + 1;
       else hi = mid;
     }
+    u32 ahead[8];
+    for (int s = 0; s < W.nshared; s++)
+      ahead[s] = uf_find_ro(g.parent, R.mbind[0][(u64)i * R.nb[0] + W.shpos[0][s]]);
     u32 c = 0;
     u32 o = off ? off[t] : 0;
-    for (u32 k = lo; k < nB && hBs[k] == h; k++) {
-      u32 j = iBs[k];
-      unsigned long long p = (unsigned long long)i * nB + j;
-      if (p < p_start) continue;
-      if (skip_self && i == j) continue;
-      bool eq = true;
-      for (int s = 0; s < W.nshared && eq; s++)
-        eq = uf_find_ro(g.parent, R.mbind[0][(u64)i * R.nb[0] + W.shpos[0][s]]) ==
-             uf_find_ro(g.parent, R.mbind[1][(u64)j * R.nb[1] + W.shpos[1][s]]);
-      if (!eq) continue;
-      if (out) {
-        if (o + c < cap) out[o + c] = p;
+    for (u32 k0 = lo; k0 < nB; k0 += 32) {
+      u32 k = k0 + lane;
+      bool inr = k < nB && hBs[k] == h;
+      bool ok = false;
+      if (inr) {
+        u32 j = iBs[k];
+        unsigned long long p = (unsigned long long)i * nB + j;
+        ok = p >= p_start && !(skip_self && i == j);
+        for (int s = 0; s < W.nshared && ok; s++)
+          ok = ahead[s] == uf_find_ro(g.parent, R.mbind[1][(u64)j * R.nb[1] + W.shpos[1][s]]);
       }
-      c++;
+      u32 m = __ballot_sync(0xffffffffu, ok);
+      if (ok && out) {
+        u32 q = o + c + __popc(m & ((1u << lane) - 1));
+        if (q < cap) out[q] = (unsigned long long)i * nB + iBs[k];
+      }
+      c += __popc(m);
+      if (!__any_sync(0xffffffffu, inr)) break;
     }
-    if (cnt) cnt[t] = c;
+    if (cnt && lane == 0) cnt[t] = c;
   }
 }
 
@@ -640,6 +651,7 @@ __global__ void k_boundary(WaveState* ws, const u32* stops, u32 ncand, const uns
   ws->stop = 0;
   ws->hazard = 0;
   ws->why = 0;
+  ws->sa_hit = 0;
   ws->p_end = seg_end;
   if (e_cut <= e_end) {
     ws->p_end = posf(stops[1]) + 1;
@@ -650,6 +662,7 @@ __global__ void k_boundary(WaveState* ws, const u32* stops, u32 ncand, const uns
     ws->hazard = ws->why != 0;
   } else if (e_sa <= e_end) {
     ws->p_end = posf(stops[0]) + 1;
+    ws->sa_hit = 1;
   }
   ws->ncommit_cand = (u32)e_end;
   ws->ncommit_acc = pre[e_end];
@@ -662,6 +675,11 @@ __global__ void k_commit_prep(WaveState* ws, const u32* wpre, const u32* kpre, u
   ws->nk = kpre[nq];
   ws->base = cnt->next_id;
   ws->kbase = cnt->nkids;
+}
+
+__global__ void k_set_nacc(const u32* pre, u32 n, WaveState* ws) {
+  if (threadIdx.x || blockIdx.x) return;
+  ws->nacc = pre[n];
 }
 
 __global__ void k_zero_commit(WaveState* ws, const Counters* cnt) {
@@ -802,6 +820,11 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
   RuleStatsH& rs = e.rstats[ri];
   B.wstats.ensure(1);
   CUDA_OK(cudaMemsetAsync(B.wstats.p, 0, sizeof(DevStats), e.s));
+  // multi-pattern join cache: compatible positions stay valid until a union of
+  // existing classes changes find() (stop-after waves / exact-path combos)
+  bool jvalid = false, jcomplete = true;
+  u32 jtotal = 0, jcursor = 0;
+  const u32 JCAP = 1u << 24;
   unsigned long long p = 0;
   u32 win = 1u << 12;  // adaptive candidate window (grows on clean waves, shrinks on dependencies)
   while (p < P) {
@@ -824,43 +847,53 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       seg_end = p + n;
     } else {
       u32 nA = Rd.nmatch[0], nB = Rd.nmatch[1];
-      u32 i0 = (u32)(p / nB);
-      u32 na = nA - i0;
-      B.hA.ensure(na + 1);
-      B.hB.ensure(nB + 1);
-      B.hBs.ensure(nB + 1);
-      B.iB.ensure(nB + 1);
-      B.iBs.ensure(nB + 1);
-      B.cnt.ensure(na + 1);
-      B.off.ensure(na + 1);
-      DevBuf<u32>& dummy = e.scratch_u32[6];
-      dummy.ensure(na + 1);
-      k_hash_rows<<<nblk(nB), 256, 0, e.s>>>(e.view(), Rd.mbind[1], Rd.nb[1], nB, W, 1, B.hB.p, B.iB.p);
-      k_hash_rows<<<nblk(na), 256, 0, e.s>>>(e.view(), Rd.mbind[0] + (u64)i0 * Rd.nb[0], Rd.nb[0], na, W, 0, B.hA.p,
-                                             dummy.p);
-      {
-        size_t bytes = 0;
-        CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
-        e.temp.ensure(bytes + 16);
-        CUDA_OK(cub::DeviceRadixSort::SortPairs(e.temp.p, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
+      if (!jvalid) {
+        u32 i0 = (u32)(p / nB);
+        u32 na = nA - i0;
+        B.hA.ensure(na + 1);
+        B.hB.ensure(nB + 1);
+        B.hBs.ensure(nB + 1);
+        B.iB.ensure(nB + 1);
+        B.iBs.ensure(nB + 1);
+        B.cnt.ensure(na + 1);
+        B.off.ensure(na + 1);
+        DevBuf<u32>& dummy = e.scratch_u32[6];
+        dummy.ensure(na + 1);
+        k_hash_rows<<<nblk(nB), 256, 0, e.s>>>(e.view(), Rd.mbind[1], Rd.nb[1], nB, W, 1, B.hB.p, B.iB.p);
+        k_hash_rows<<<nblk(na), 256, 0, e.s>>>(e.view(), Rd.mbind[0] + (u64)i0 * Rd.nb[0], Rd.nb[0], na, W, 0,
+                                               B.hA.p, dummy.p);
+        {
+          size_t bytes = 0;
+          CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
+          e.temp.ensure(bytes + 16);
+          CUDA_OK(cub::DeviceRadixSort::SortPairs(e.temp.p, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
+        }
+        k_join<<<nblk((u64)na * 32), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self,
+                                                   nullptr, B.cnt.p, nullptr, 0);
+        CUDA_OK(cudaMemsetAsync(B.cnt.p + na, 0, sizeof(u32), e.s));
+        dev_exclusive_scan_u32(e, B.cnt.p, B.off.p, na + 1);
+        u32 total = read_u32(e, B.off.p + na);
+        jtotal = std::min<u32>(total, JCAP);
+        jcomplete = total <= JCAP;
+        B.pos.ensure((u64)jtotal + 1);
+        if (jtotal)
+          k_join<<<nblk((u64)na * 32), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self,
+                                                     B.off.p, nullptr, B.pos.p, jtotal);
+        jcursor = 0;
+        jvalid = true;
       }
-      k_join<<<nblk(na), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self, nullptr,
-                                        B.cnt.p, nullptr, 0);
-      CUDA_OK(cudaMemsetAsync(B.cnt.p + na, 0, sizeof(u32), e.s));
-      dev_exclusive_scan_u32(e, B.cnt.p, B.off.p, na + 1);
-      u32 total = read_u32(e, B.off.p + na);
-      u32 cap = std::min<u32>(total, win);
-      B.pos.ensure((u64)cap + 1);
-      if (cap)
-        k_join<<<nblk(na), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self, B.off.p,
-                                          nullptr, B.pos.p, cap);
-      ncand = cap;
-      posp = B.pos.p;
-      if (total > cap) {
-        unsigned long long lastp;
-        CUDA_OK(cudaMemcpyAsync(&lastp, B.pos.p + cap - 1, sizeof(lastp), cudaMemcpyDeviceToHost, e.s));
+      u32 remain = jtotal - jcursor;
+      ncand = std::min<u32>(remain, win);
+      posp = B.pos.p + jcursor;
+      if (ncand < remain) {
+        // coverage ends right before the next cached candidate
+        CUDA_OK(cudaMemcpyAsync(&seg_end, B.pos.p + jcursor + ncand, sizeof(seg_end), cudaMemcpyDeviceToHost, e.s));
         e.sync();
-        seg_end = lastp + 1;
+      } else if (!jcomplete) {
+        CUDA_OK(cudaMemcpyAsync(&seg_end, B.pos.p + jtotal - 1, sizeof(seg_end), cudaMemcpyDeviceToHost, e.s));
+        e.sync();
+        seg_end += 1;
+        jvalid = false;  // re-join after the capped list
       }
     }
     if (ncand == 0) {
@@ -924,7 +957,16 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       KTimer kt(e, KG_APPLY_WAVE, 0.0, 16 + lv.size());
       k_gates<<<nblk(ncand, 128), 128, 0, e.s>>>(e.view(), Rd, RD, W, posp, ncand, p, B.status.p, B.env.p, B.olds.p,
                                                  B.hazard.p);
-      k_accept_scan<<<1, 1024, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.pre.p, B.acc.p, ws);
+      if (ncand <= 65536) {
+        k_accept_scan<<<1, 1024, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.pre.p, B.acc.p, ws);
+      } else {
+        B.fl.ensure(ncand + 1);
+        k_accept_flags<<<nblk(ncand), 256, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.fl.p);
+        CUDA_OK(cudaMemsetAsync(B.fl.p + ncand, 0, sizeof(u32), e.s));
+        dev_exclusive_scan_u32(e, B.fl.p, B.pre.p, ncand + 1);
+        k_accept_list<<<nblk(ncand), 256, 0, e.s>>>(B.fl.p, B.pre.p, ncand, B.acc.p);
+        k_set_nacc<<<1, 1, 0, e.s>>>(B.pre.p, ncand, ws);
+      }
       // ---- 3. resolve requests level by level
       if (R > 0) {
         for (size_t d = 1; d < lv.size(); d++) {
@@ -950,7 +992,12 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       CUDA_OK(cudaMemsetAsync(B.stops.p, 0xFF, 3 * sizeof(u32), e.s));
       k_validity<<<nblk(ncand), 256, 0, e.s>>>(W, T, Rd.nslots, Rd.nsrc, ncand, B.hazard.p, B.env.p, B.olds.p, B.pre.p,
                                                B.status.p, B.ident.p, B.fw_cls.p, B.fw_fresh.p, B.stops.p + 2);
-      k_scan_block<<<1, 1024, 0, e.s>>>(B.alloc.p, B.apre.p, ncand);
+      if (ncand <= 65536) {
+        k_scan_block<<<1, 1024, 0, e.s>>>(B.alloc.p, B.apre.p, ncand);
+      } else {
+        CUDA_OK(cudaMemsetAsync(B.alloc.p + ncand, 0, sizeof(u32), e.s));
+        dev_exclusive_scan_u32(e, B.alloc.p, B.apre.p, ncand + 1);
+      }
       k_find_stops<<<nblk(ncand), 256, 0, e.s>>>(B.acc.p, ws, B.sa.p, B.apre.p, B.alloc.p, e.cnt.p, n_max, B.stops.p);
       k_boundary<<<1, 1, 0, e.s>>>(ws, B.stops.p, ncand, posp, p, seg_end, B.pre.p, B.hazard.p);
       // ---- 5. statistics of the committed segment (device accumulators)
@@ -963,7 +1010,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         B.ka.ensure(nreq_max + 2);
         B.kpre.ensure(nreq_max + 2);
         k_win_flags<<<nblk(nreq_max), 256, 0, e.s>>>(T, B.ident.p, nreq_max, B.tmpl.p, R, ws, B.wf.p, B.ka.p);
-        if (nreq_max <= (1u << 20)) {
+        if (nreq_max <= 65536) {
           k_scan_block<<<1, 1024, 0, e.s>>>(B.wf.p, B.wpre.p, (u32)nreq_max);
           k_scan_block<<<1, 1024, 0, e.s>>>(B.ka.p, B.kpre.p, (u32)nreq_max);
         } else {
@@ -988,6 +1035,19 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     CUDA_OK(cudaMemcpyAsync(&hw, ws, sizeof(hw), cudaMemcpyDeviceToHost, e.s));
     CUDA_OK(cudaMemcpyAsync(&e.h, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
     e.sync();
+    {
+      // algorithmic bytes of the wave (what the apply must touch at least):
+      // candidates: match rows + subst/olds writes + analyses read by the shape check;
+      // requests: hashcons probe (slot + key) + wave-table key/pos + analysis write;
+      // committed nodes: op, koff, kids, parent, flags, analysis, hashcons slot
+      double nb = 0;
+      for (int t = 0; t < Rd.nsrc; t++) nb += 4.0 * (1 + Rd.nb[t]);
+      double per_cand = nb + 4.0 * (Rd.nslots + Rd.nsrc) + (e.analysis ? 128.0 * Rd.nslots : 0.0);
+      double per_req = 4.0 + 16.0 + 4.0 * 2 + 48.0 + (e.analysis ? 128.0 : 0.0);
+      double per_node = 21.0 + (e.analysis ? 128.0 : 0.0);
+      e.kstat[KG_APPLY_WAVE].bytes += per_cand * ncand + per_req * (double)hw.nacc * R + per_node * hw.nwin +
+                                      4.0 * hw.nk;
+    }
     u32 ncommit_cand = hw.ncommit_cand;
     unsigned long long p_end = hw.p_end;
     bool stop = hw.stop != 0, hazard = hw.hazard != 0;
@@ -1005,6 +1065,11 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       rs.found += cover;
       rs.skipped_self += self;
       rs.skipped_compat += cover - self - ncommit_cand;
+    }
+    if (hr.nsrc > 1) {
+      jcursor += ncommit_cand;
+      // a union of existing classes (stop-after) or an exact-path combo can change compatibility
+      if (hazard || hw.sa_hit) jvalid = false;
     }
     if (stop) {
       if (p_end < P) {
