@@ -369,7 +369,8 @@ void Engine::costs(int mode, int strict, int ntab, const char* keys, const i64* 
   }
   d_costs.ensure(n + 1);
   {
-    KTimer kt(*this, KG_COSTS, 16.0 * h.live + 4.0 * h.nkids + 128.0 * h.nkids, 1);
+    // node: op 4 + koff 8 + flag 1 + cost 8; child: id 4 + parent 4 + analysis fields 48
+    KTimer kt(*this, KG_COSTS, 21.0 * h.live + 56.0 * h.nkids, 1);
     k_node_costs<<<nblk(n, 128), 128, 0, s>>>(view(), ct, n, d_costs.p);
   }
   if (out) CUDA_OK(cudaMemcpyAsync(out, d_costs.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));

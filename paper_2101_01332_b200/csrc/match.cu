@@ -185,6 +185,9 @@ void Engine::ematch_pattern(int pid, MatchSet& out) {
   sync();
   u32 ncand = range[1] - range[0];
   if (ncand == 0) return;
+  // whole e-match (root scan + ordering + dedup) timed as one group; bytes per
+  // candidates + match rows + a (1+v)-word sort of the matches
+  KTimer kt_all(*this, KG_EMATCH, 0.0, 0);
   DevBuf<u32>& rc = sc.m_rc;
   DevBuf<u32>& rb = sc.m_rb;
   DevBuf<u32>& cntb = sc.m_cnt;
@@ -195,18 +198,15 @@ void Engine::ematch_pattern(int pid, MatchSet& out) {
     rc.ensure(cap);
     rb.ensure((u64)cap * std::max(p.nb, 1));
     CUDA_OK(cudaMemsetAsync(cntb.p, 0, sizeof(u32), s));
-    {
-      // root-candidate scan: id 4 + op 4 + koff 8 + flags 1 + children/parents 8a per candidate
-      KTimer kt(*this, KG_EMATCH, (double)ncand * (17.0 + 8.0 * p.apps[0].nargs), 1);
-      k_ematch<<<nblk(ncand, 128), 128, 0, s>>>(view(), sd, p, snap.op_nodes.p + range[0], ncand, rc.p, rb.p,
-                                                cntb.p, cap);
-    }
+    k_ematch<<<nblk(ncand, 128), 128, 0, s>>>(view(), sd, p, snap.op_nodes.p + range[0], ncand, rc.p, rb.p, cntb.p,
+                                              cap);
     CUDA_OK(cudaMemcpyAsync(&m, cntb.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
-    kstat[KG_EMATCH].bytes += (double)std::min(m, cap) * 4.0 * (1 + p.nb);
     if (m <= cap) break;
     cap = m + 1024;
   }
+  kt_all.bytes = (double)ncand * (17.0 + 8.0 * p.apps[0].nargs) + (double)m * 4.0 * (1 + p.nb) * 2.0;
+  kt_all.launches = 1;
   if (m == 0) return;
   // stable LSD sort over words (cls, b0..b_{nb-1}), last word first
   DevBuf<u32>& perm = sc.m_perm;
