@@ -72,7 +72,7 @@ __device__ __forceinline__ u32 uf_find(u32* parent, u32 x) {
   }
 }
 
-__device__ __forceinline__ u32 uf_find_ro(const u32* __restrict__ parent, u32 x) {
+__device__ __forceinline__ u32 uf_find_ro(const u32* parent, u32 x) {
   u32 p;
   while ((p = parent[x]) != x) x = p;
   return x;

@@ -71,15 +71,16 @@ struct WaveRule {
   const ReqT* tmpl;
 };
 
-struct WaveTab {  // wave-local key table
-  u32* state;     // 0 empty, 1 busy, 2 ready
+struct WaveTab {  // wave-local key table; every tag carries the wave's epoch
+  u32* state;     // epoch << 2 | {1 busy, 2 ready}; another epoch = empty
   u32* key;       // 10 words per slot: op, nargs, kids[8]
-  unsigned long long* minpos;
+  unsigned long long* minpos;  // (~epoch << 32) | min request position
   u32* wid;       // assigned node id of the winner
-  u32* wroot;     // winner is a target root
+  u32* wroot;     // == epoch: winner is a target root
   Val* val;
   u32 mask;
   u32* wold;      // matched (old) class of a root winner's target
+  u32 epoch;
 };
 
 // ---------------------------------------------------------------- join
@@ -144,21 +145,51 @@ __global__ void k_join(G g, RuleDev R, WaveRule W, const u64* hA, u32 i0, const 
   }
 }
 
-// ---------------------------------------------------------------- gates
+// ---------------------------------------------------------------- phases
+//
+// Every wave phase is a __device__ function over an index range striped by
+// (tid, nth).  The grid path wraps each one in its own kernel
+// (tid = global thread, nth = grid size); the single-CTA path (k_wave_cta)
+// runs them back to back inside one block with __syncthreads() between
+// phases, so a small wave costs one block's worth of barriers instead of
+// ~20 kernel launches.  Per-wave tables are epoch-tagged (no clearing).
+
+#define TID_LOOP(i, n) for (u64 i = tid; i < (u64)(n); i += nth)
+
+// union-find read that is safe inside a kernel that also writes parent[]
+// (no read-only cache path)
+__device__ __forceinline__ u32 uf_find_rw(const u32* parent, u32 x) {
+  u32 p;
+  while ((p = parent[x]) != x) x = p;
+  return x;
+}
+
+__device__ __forceinline__ unsigned long long mp_tag(u32 epoch, u64 gpos) {
+  return ((unsigned long long)(~epoch) << 32) | gpos;
+}
+__device__ __forceinline__ unsigned long long fw_tag(u32 epoch, u32 c) {
+  return ((unsigned long long)(~epoch) << 32) | c;
+}
+__device__ __forceinline__ bool is_winner(const WaveTab& T, u32 s, u64 gpos) {
+  return T.minpos[s] == mp_tag(T.epoch, gpos);
+}
+__device__ __forceinline__ bool is_wroot(const WaveTab& T, u32 s) { return T.wroot[s] == T.epoch; }
 
 // status: 0 accept, 1 shape fail, 2 cycle reject; hazard flag for gate errors
-__global__ void k_gates(G g, RuleDev R, ReachDev RD, WaveRule W, const unsigned long long* pos, u32 n,
-                        unsigned long long p_base, u8* status, u32* env_out, u32* old_out, u8* hazard) {
-  GRID_STRIDE(c, n) {
+__device__ __forceinline__ void d_gates(u64 tid, u64 nth, const G& g, const RuleDev& R, const ReachDev& RD,
+                                        const unsigned long long* pos, u32 n, unsigned long long p_base, u8* status,
+                                        u32* env_out, u32* old_out, u8* hazard) {
+  TID_LOOP(c, n) {
     unsigned long long p = pos ? pos[c] : p_base + c;
     u32 idx[MAX_SRC];
     decode_pos(R, p, idx);
     u32 env[MAX_VARS];
     for (int v = 0; v < R.nslots; v++) env[v] = TSAT_NONE;
     for (int i = 0; i < R.nsrc; i++)
-      for (int j = 0; j < R.nb[i]; j++) env[R.bind_slot[i][j]] = uf_find_ro(g.parent, R.mbind[i][(u64)idx[i] * R.nb[i] + j]);
+      for (int j = 0; j < R.nb[i]; j++)
+        env[R.bind_slot[i][j]] = uf_find_rw(g.parent, R.mbind[i][(u64)idx[i] * R.nb[i] + j]);
     u32 olds[MAX_SRC];
-    for (int t = 0; t < R.nsrc; t++) olds[t] = uf_find_ro(g.parent, R.mcls[t][idx[t]]);
+    for (int t = 0; t < R.nsrc; t++) olds[t] = uf_find_rw(g.parent, R.mcls[t][idx[t]]);
     u8 st = 0, hz = 0;
     if (g.analysis) {
       for (int t = 0; t < R.nsrc && st == 0; t++) {
@@ -190,14 +221,6 @@ __global__ void k_gates(G g, RuleDev R, ReachDev RD, WaveRule W, const unsigned 
   }
 }
 
-__global__ void k_accept_flags(const u8* status, const u8* hazard, u32 n, u32* fl) {
-  GRID_STRIDE(c, n) fl[c] = (status[c] == 0 || hazard[c]) ? 1u : 0u;
-}
-
-__global__ void k_accept_list(const u32* fl, const u32* pre, u32 n, u32* acc) {
-  GRID_STRIDE(c, n) if (fl[c]) acc[pre[c]] = (u32)c;
-}
-
 // ---------------------------------------------------------------- resolution
 
 __device__ __forceinline__ u64 wkey_hash(u32 op, int n, const u32* k) {
@@ -206,24 +229,26 @@ __device__ __forceinline__ u64 wkey_hash(u32 op, int n, const u32* k) {
   return h;
 }
 
-// find-or-insert a key; returns slot
+// find-or-insert a key; returns slot.  state = epoch << 2 | {1 busy, 2 ready};
+// a slot whose epoch is not the current one is empty.
 __device__ u32 wtab_get(const WaveTab& T, u32 op, int n, const u32* k) {
   u32 slot = (u32)wkey_hash(op, n, k) & T.mask;
+  const u32 busy = (T.epoch << 2) | 1u, ready = (T.epoch << 2) | 2u;
   while (true) {
     u32 st = ((volatile u32*)T.state)[slot];
-    if (st == 0) {
-      if (atomicCAS(&T.state[slot], 0u, 1u) == 0u) {
+    if ((st >> 2) != T.epoch) {
+      if (atomicCAS(&T.state[slot], st, busy) == st) {
         u32* kk = T.key + (u64)slot * 10;
         kk[0] = op;
         kk[1] = (u32)n;
         for (int i = 0; i < 8; i++) kk[2 + i] = i < n ? k[i] : 0u;
         __threadfence();
-        atomicExch(&T.state[slot], 2u);
+        atomicExch(&T.state[slot], ready);
         return slot;
       }
       st = ((volatile u32*)T.state)[slot];
     }
-    while (st == 1) st = ((volatile u32*)T.state)[slot];
+    while (st == busy) st = ((volatile u32*)T.state)[slot];
     __threadfence();
     const volatile u32* kk = T.key + (u64)slot * 10;
     bool eq = kk[0] == op && kk[1] == (u32)n;
@@ -234,10 +259,10 @@ __device__ u32 wtab_get(const WaveTab& T, u32 op, int n, const u32* k) {
 }
 
 // one request level: thread per (accepted combo, template at this depth)
-__global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const int* lvl_req,
-                                int nlvl, const u32* env, u32* ident, u8* hazard) {
-  u32 nacc = ws->nacc;
-  GRID_STRIDE(t, (u64)nacc * nlvl) {
+__device__ __forceinline__ void d_resolve_level(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
+                                                const u32* acc, u32 nacc, const int* lvl_req, int nlvl,
+                                                const u32* env, u32* ident, u8* hazard) {
+  TID_LOOP(t, (u64)nacc * nlvl) {
     u32 a = (u32)(t / nlvl);
     int r = lvl_req[t % nlvl];
     u32 c = acc[a];
@@ -255,12 +280,12 @@ __global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, cons
     if (real) {
       u32 hit = hc_lookup(g, q.atom, q.nargs, kids);
       if (hit != TSAT_NONE) {
-        ident[gpos] = uf_find_ro(g.parent, hit);
+        ident[gpos] = uf_find_rw(g.parent, hit);
         continue;
       }
     }
     u32 s = wtab_get(T, q.atom, q.nargs, kids);
-    atomicMin(&T.minpos[s], (unsigned long long)gpos);
+    atomicMin(&T.minpos[s], mp_tag(T.epoch, gpos));
     ident[gpos] = FRESH | s;
     if (g.analysis) {
       Val kv[8];
@@ -276,10 +301,9 @@ __global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, cons
   }
 }
 
-__global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const u32* ident,
-                             const u8* hazard, const u32* olds) {
-  u32 nacc = ws->nacc;
-  GRID_STRIDE(a, nacc) {
+__device__ __forceinline__ void d_mark_roots(u64 tid, u64 nth, const WaveRule& W, const WaveTab& T, const u32* acc,
+                                             u32 nacc, const u32* ident, const u8* hazard, const u32* olds) {
+  TID_LOOP(a, nacc) {
     if (hazard[acc[a]]) continue;
     for (int t = 0; t < W.ntgt; t++) {
       int r = W.root_req[t];
@@ -287,8 +311,8 @@ __global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, const WaveSt
       u32 id = ident[(u64)a * W.R + r];
       if (!(id & FRESH)) continue;
       u32 s = id & ~FRESH;
-      if (T.minpos[s] == (u64)a * W.R + r) {
-        T.wroot[s] = 1;
+      if (is_winner(T, s, (u64)a * W.R + r)) {
+        T.wroot[s] = T.epoch;
         T.wold[s] = olds[(u64)acc[a] * MAX_SRC + t];
       }
     }
@@ -304,11 +328,11 @@ __global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, const WaveSt
 
 // per accepted combo: allocations, union plan, type-a hazards (combo's own
 // evaluation cannot be trusted) and its write set.
-__global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, u32 ncand,
-                             const u32* ident, const u32* env, const u32* olds, int multi, u8* hazard, u32* alloc,
-                             u8* ukind, u32* uother, u8* grow, u8* stop_after) {
-  u32 nacc = ws->nacc;
-  GRID_STRIDE(a0, ncand) {
+__device__ __forceinline__ void d_cand_check(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
+                                             const u32* acc, u32 nacc, u32 ncand, const u32* ident, const u32* env,
+                                             const u32* olds, int multi, u8* hazard, u32* alloc, u8* ukind,
+                                             u32* uother, u8* grow, u8* stop_after) {
+  TID_LOOP(a0, ncand) {
     u32 a = (u32)a0;
     if (a >= nacc) {
       alloc[a] = 0;
@@ -328,9 +352,9 @@ __global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, const W
         u32 id = ident[(u64)a * W.R + r];
         if (!(id & FRESH)) continue;
         u32 s = id & ~FRESH;
-        bool win = T.minpos[s] == (u64)a * W.R + r;
+        bool win = is_winner(T, s, (u64)a * W.R + r);
         if (win) na++;
-        else if (T.wroot[s] && !W.tmpl[r].is_root) {
+        else if (is_wroot(T, s) && !W.tmpl[r].is_root) {
           hz = true;  // inner reuse of a merged root
           why = 3;
         }
@@ -358,12 +382,12 @@ __global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, const W
             }
           } else {
             u32 s = id & ~FRESH;
-            bool win = T.minpos[s] == (u64)a * W.R + r;
+            bool win = is_winner(T, s, (u64)a * W.R + r);
             if (win) {
               kind = UK_FRESH_ROOT;
               other = id;
               nv = &T.val[s];
-            } else if (T.wroot[s]) {
+            } else if (is_wroot(T, s)) {
               u32 x = T.wold[s];  // the earlier root's node now lives in its matched class
               if (x != old) {
                 kind = UK_CLASS;
@@ -382,8 +406,7 @@ __global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, const W
           if (!val_same_data(ov, *nv)) {
             hz = true;  // AnalysisMergeError: exact path raises it
             why = 5;
-          }
-          else if (kind == UK_CLASS) {
+          } else if (kind == UK_CLASS) {
             // the kept (smaller) root's analysis changes iff the dropped one adds origins
             bool keep_is_old = old < other;
             if (keep_is_old ? val_merge_grows(ov, *nv) : val_merge_grows(*nv, ov)) grow[(u64)a * MAX_SRC + t] = 1;
@@ -409,12 +432,14 @@ __global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, const W
 }
 
 // first writer of every identity (class id or FRESH slot) in the wave
-__global__ void k_first_writer(WaveRule W, const u32* acc, const WaveState* ws, const u8* hazard, const u32* olds,
-                               const u8* ukind, const u32* uother, const u8* grow, u32* fw_cls, u32* fw_fresh) {
-  u32 nacc = ws->nacc;
-  GRID_STRIDE(a, nacc) {
+__device__ __forceinline__ void d_first_writer(u64 tid, u64 nth, const WaveRule& W, u32 epoch, const u32* acc,
+                                               u32 nacc, const u8* hazard, const u32* olds, const u8* ukind,
+                                               const u32* uother, const u8* grow, unsigned long long* fw_cls,
+                                               unsigned long long* fw_fresh) {
+  TID_LOOP(a, nacc) {
     u32 c = acc[a];
     if (hazard[c]) continue;
+    unsigned long long tag = fw_tag(epoch, c);
     for (int t = 0; t < W.ntgt; t++) {
       u8 k = ukind[(u64)a * MAX_SRC + t];
       u32 old = olds[(u64)c * MAX_SRC + t], x = uother[(u64)a * MAX_SRC + t];
@@ -423,40 +448,45 @@ __global__ void k_first_writer(WaveRule W, const u32* acc, const WaveState* ws, 
         // only the dropped root changes identity; the kept root changes only
         // when its analysis grows
         u32 keep = old < x ? old : x, drop = old < x ? x : old;
-        atomicMin(&fw_cls[drop], c);
-        if (gr) atomicMin(&fw_cls[keep], c);
+        atomicMin(&fw_cls[drop], tag);
+        if (gr) atomicMin(&fw_cls[keep], tag);
       } else if (k == UK_FRESH_NODE) {
-        atomicMin(&fw_fresh[x & ~FRESH], c);
-        if (gr) atomicMin(&fw_cls[old], c);
+        atomicMin(&fw_fresh[x & ~FRESH], tag);
+        if (gr) atomicMin(&fw_cls[old], tag);
       } else if (k == UK_FRESH_ROOT && gr) {
-        atomicMin(&fw_cls[old], c);
+        atomicMin(&fw_cls[old], tag);
       }
     }
   }
 }
 
-__device__ __forceinline__ bool read_dirty(u32 id, u32 c, const u32* fw_cls, const u32* fw_fresh) {
-  if (id & FRESH) return fw_fresh[id & ~FRESH] < c;
-  return fw_cls[id] < c;
+__device__ __forceinline__ bool read_dirty(u32 id, u32 c, u32 epoch, const unsigned long long* fw_cls,
+                                           const unsigned long long* fw_fresh) {
+  unsigned long long v = (id & FRESH) ? fw_fresh[id & ~FRESH] : fw_cls[id];
+  return (u32)(v >> 32) == ~epoch && (u32)v < c;
 }
 
 // candidate validity against earlier writes in the wave (all candidates:
 // rejected ones read through their gates, accepted ones through requests)
-__global__ void k_validity(WaveRule W, WaveTab T, int nslots, int nsrc, u32 ncand, const u8* hazard, const u32* env,
-                           const u32* olds, const u32* accpre, const u8* status, const u32* ident,
-                           const u32* fw_cls, const u32* fw_fresh, u32* first_bad) {
-  GRID_STRIDE(c0, ncand) {
+__device__ __forceinline__ void d_validity(u64 tid, u64 nth, const WaveRule& W, const WaveTab& T, int nslots,
+                                           int nsrc, u32 ncand, const u8* hazard, const u32* env, const u32* olds,
+                                           const u32* accpre, const u8* status, const u32* ident,
+                                           const unsigned long long* fw_cls, const unsigned long long* fw_fresh,
+                                           u32* first_bad) {
+  u32 ep = T.epoch;
+  TID_LOOP(c0, ncand) {
     u32 c = (u32)c0;
     bool bad = hazard[c] != 0;
-    for (int v = 0; v < nslots && !bad; v++) bad = read_dirty(env[(u64)c * MAX_VARS + v], c, fw_cls, fw_fresh);
-    for (int t = 0; t < nsrc && !bad; t++) bad = read_dirty(olds[(u64)c * MAX_SRC + t], c, fw_cls, fw_fresh);
+    for (int v = 0; v < nslots && !bad; v++) bad = read_dirty(env[(u64)c * MAX_VARS + v], c, ep, fw_cls, fw_fresh);
+    for (int t = 0; t < nsrc && !bad; t++) bad = read_dirty(olds[(u64)c * MAX_SRC + t], c, ep, fw_cls, fw_fresh);
     if (!bad && status[c] == 0) {
       u32 a = accpre[c];
       for (int r = 0; r < W.R && !bad; r++) {
         u32 id = ident[(u64)a * W.R + r];
-        bad = read_dirty(id, c, fw_cls, fw_fresh);
+        bad = read_dirty(id, c, ep, fw_cls, fw_fresh);
         // a reused target root resolves to the class it was merged into
-        if (!bad && (id & FRESH) && T.wroot[id & ~FRESH]) bad = read_dirty(T.wold[id & ~FRESH], c, fw_cls, fw_fresh);
+        if (!bad && (id & FRESH) && is_wroot(T, id & ~FRESH))
+          bad = read_dirty(T.wold[id & ~FRESH], c, ep, fw_cls, fw_fresh);
       }
     }
     if (bad) atomicMin(first_bad, c);
@@ -464,22 +494,20 @@ __global__ void k_validity(WaveRule W, WaveTab T, int nslots, int nsrc, u32 ncan
 }
 
 // first hazard (candidate index) and node-limit cutoff (accepted index)
-__global__ void k_find_stops(const u32* acc, const WaveState* ws, const u8* stop_after, const u32* apre,
-                             const u32* alloc, const Counters* cnt, i64 n_max,
-                             u32* out /* [stop_after cand, cutoff cand] */) {
-  u32 nacc = ws->nacc;
-  i64 live0 = (i64)cnt->live;
-  GRID_STRIDE(a, nacc) {
+__device__ __forceinline__ void d_find_stops(u64 tid, u64 nth, const u32* acc, u32 nacc, const u8* stop_after,
+                                             const u32* apre, const u32* alloc, i64 live0, i64 n_max,
+                                             u32* out /* [stop_after cand, cutoff cand] */) {
+  TID_LOOP(a, nacc) {
     if (stop_after[a]) atomicMin(&out[0], acc[a]);
     if (live0 + (i64)apre[a] + (i64)alloc[a] >= n_max && alloc[a] > 0) atomicMin(&out[1], acc[a]);
   }
 }
 
 // unions of committed combos (disjoint by construction of the validity check)
-__global__ void k_commit_unions(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const u32* olds,
-                                const u8* ukind, const u32* uother, const u8* grow) {
-  u32 ncommit_acc = ws->ncommit_acc;
-  GRID_STRIDE(a, ncommit_acc) {
+__device__ __forceinline__ void d_commit_unions(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
+                                                const u32* acc, u32 ncommit_acc, const u32* olds, const u8* ukind,
+                                                const u32* uother, const u8* grow) {
+  TID_LOOP(a, ncommit_acc) {
     u32 c = acc[a];
     for (int t = 0; t < W.ntgt; t++) {
       u8 k = ukind[(u64)a * MAX_SRC + t];
@@ -507,12 +535,11 @@ __global__ void k_commit_unions(G g, WaveRule W, WaveTab T, const u32* acc, cons
   }
 }
 
-// stats over candidates [0, ncand): shape / cycle / applied / noop
-__global__ void k_seg_stats(const u8* status, WaveState* ws, u32 ncand, const u32* accpre, const u32* alloc,
-                            const u8* ukind, int efficient, DevStats* st) {
-  u32 ncommit = ws->ncommit_cand;
-  GRID_STRIDE(c, ncand) {
-    if (c >= ncommit) continue;
+// stats over candidates [0, ncommit): shape / cycle / applied / noop
+__device__ __forceinline__ void d_seg_stats(u64 tid, u64 nth, const u8* status, WaveState* ws, u32 ncommit,
+                                            const u32* accpre, const u32* alloc, const u8* ukind, int efficient,
+                                            DevStats* st) {
+  TID_LOOP(c, ncommit) {
     u8 s = status[c];
     if (s == 1) atomicAdd(&st->skipped_shape, 1ull);
     else if (s == 2) {
@@ -537,28 +564,26 @@ __global__ void k_seg_stats(const u8* status, WaveState* ws, u32 ncand, const u3
 
 // ---------------------------------------------------------------- commit
 
-__global__ void k_win_flags(WaveTab T, const u32* ident, u64 nreq, const ReqT* tmpl, int R, const WaveState* ws,
-                            u32* wf, u32* ka) {
-  u64 lim = (u64)ws->ncommit_acc * R;
-  GRID_STRIDE(q, nreq) {
+__device__ __forceinline__ void d_win_flags(u64 tid, u64 nth, const WaveTab& T, const u32* ident, u64 nreq,
+                                            const ReqT* tmpl, int R, u64 lim, u32* wf, u32* ka) {
+  TID_LOOP(q, nreq) {
     u32 id = q < lim ? ident[q] : 0u;
-    bool win = q < lim && (id & FRESH) && T.minpos[id & ~FRESH] == (unsigned long long)q;
+    bool win = q < lim && (id & FRESH) && is_winner(T, id & ~FRESH, q);
     wf[q] = win ? 1u : 0u;
     ka[q] = win ? (u32)tmpl[q % R].nargs : 0u;
   }
 }
 
-__global__ void k_assign_ids(WaveTab T, const u32* ident, u64 nreq, const u32* wf, const u32* wpre,
-                             const WaveState* ws) {
-  u32 base = ws->base;
-  GRID_STRIDE(q, nreq) if (wf[q]) T.wid[ident[q] & ~FRESH] = base + wpre[q];
+__device__ __forceinline__ void d_assign_ids(u64 tid, u64 nth, const WaveTab& T, const u32* ident, u64 nreq,
+                                             const u32* wf, const u32* wpre, u32 base) {
+  TID_LOOP(q, nreq) if (wf[q]) T.wid[ident[q] & ~FRESH] = base + wpre[q];
 }
 
-__global__ void k_write_nodes(G g, WaveRule W, WaveTab T, const u32* acc, const u32* ident, u64 nreq,
-                              const u32* wf, const u32* wpre, const u32* kpre, const WaveState* ws,
-                              const u32* env, const u32* olds) {
-  u32 base = ws->base, kbase = ws->kbase;
-  GRID_STRIDE(q, nreq) {
+__device__ __forceinline__ void d_write_nodes(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
+                                              const u32* acc, const u32* ident, u64 nreq, const u32* wf,
+                                              const u32* wpre, const u32* kpre, u32 base, u32 kbase, const u32* env,
+                                              const u32* olds) {
+  TID_LOOP(q, nreq) {
     if (!wf[q]) continue;
     u32 a = (u32)(q / W.R);
     int r = (int)(q % W.R);
@@ -581,65 +606,10 @@ __global__ void k_write_nodes(G g, WaveRule W, WaveTab T, const u32* acc, const 
   }
 }
 
-__global__ void k_insert_range(G g, const WaveState* ws, u64 bound) {
-  u32 a = ws->base, n = ws->nwin;
-  GRID_STRIDE(i, bound) if (i < n) hc_insert(g, a + (u32)i);
-}
-
-
-// ---------------------------------------------------------------- device-side wave control
-
-
-// single-CTA exclusive scan with the total at out[n] (small arrays; CUB's two
-// kernels cost more than the work at wave sizes)
-__global__ void __launch_bounds__(1024) k_scan_block(const u32* in, u32* out, u32 n) {
-  typedef cub::BlockScan<u32, 1024> BS;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ u32 carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (u32 base = 0; base < n; base += 1024) {
-    u32 i = base + threadIdx.x;
-    u32 v = i < n ? in[i] : 0u, x, tot;
-    BS(tmp).ExclusiveSum(v, x, tot);
-    if (i < n) out[i] = carry + x;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) out[n] = carry;
-}
-
-// accepted list (status 0 or flagged) in candidate order; ws->nacc
-__global__ void __launch_bounds__(1024) k_accept_scan(const u8* status, const u8* hazard, u32 n, u32* pre, u32* acc,
-                                                      WaveState* ws) {
-  typedef cub::BlockScan<u32, 1024> BS;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ u32 carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (u32 base = 0; base < n; base += 1024) {
-    u32 c = base + threadIdx.x;
-    u32 f = (c < n && (status[c] == 0 || hazard[c])) ? 1u : 0u, x, tot;
-    BS(tmp).ExclusiveSum(f, x, tot);
-    if (c < n) {
-      pre[c] = carry + x;
-      if (f) acc[carry + x] = c;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    pre[n] = carry;
-    ws->nacc = carry;
-  }
-}
-
 // commit boundary: stops = [stop_after cand, cutoff cand, first bad cand]
-__global__ void k_boundary(WaveState* ws, const u32* stops, u32 ncand, const unsigned long long* pos,
-                           unsigned long long p, unsigned long long seg_end, const u32* pre, const u8* hazard) {
-  if (threadIdx.x || blockIdx.x) return;
+__device__ __forceinline__ void d_boundary(WaveState* ws, const u32* stops, u32 ncand, const unsigned long long* pos,
+                                           unsigned long long p, unsigned long long seg_end, const u32* pre,
+                                           const u8* hazard) {
   const u64 INF = (u64)1 << 40;
   u64 e_sa = stops[0] == TSAT_NONE ? INF : (u64)stops[0] + 1;
   u64 e_cut = stops[1] == TSAT_NONE ? INF : (u64)stops[1] + 1;
@@ -667,6 +637,138 @@ __global__ void k_boundary(WaveState* ws, const u32* stops, u32 ncand, const uns
   ws->ncommit_cand = (u32)e_end;
   ws->ncommit_acc = pre[e_end];
   ws->any_applied = 0;
+}
+
+// ---------------------------------------------------------------- grid kernels
+
+#define GTID (blockIdx.x * (u64)blockDim.x + threadIdx.x)
+#define GNTH ((u64)gridDim.x * blockDim.x)
+
+__global__ void k_gates(G g, RuleDev R, ReachDev RD, WaveRule W, const unsigned long long* pos, u32 n,
+                        unsigned long long p_base, u8* status, u32* env_out, u32* old_out, u8* hazard) {
+  d_gates(GTID, GNTH, g, R, RD, pos, n, p_base, status, env_out, old_out, hazard);
+}
+
+__global__ void k_accept_flags(const u8* status, const u8* hazard, u32 n, u32* fl) {
+  GRID_STRIDE(c, n) fl[c] = (status[c] == 0 || hazard[c]) ? 1u : 0u;
+}
+
+__global__ void k_accept_list(const u32* fl, const u32* pre, u32 n, u32* acc) {
+  GRID_STRIDE(c, n) if (fl[c]) acc[pre[c]] = (u32)c;
+}
+
+__global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const int* lvl_req,
+                                int nlvl, const u32* env, u32* ident, u8* hazard) {
+  d_resolve_level(GTID, GNTH, g, W, T, acc, ws->nacc, lvl_req, nlvl, env, ident, hazard);
+}
+
+__global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const u32* ident,
+                             const u8* hazard, const u32* olds) {
+  d_mark_roots(GTID, GNTH, W, T, acc, ws->nacc, ident, hazard, olds);
+}
+
+__global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, u32 ncand,
+                             const u32* ident, const u32* env, const u32* olds, int multi, u8* hazard, u32* alloc,
+                             u8* ukind, u32* uother, u8* grow, u8* stop_after) {
+  d_cand_check(GTID, GNTH, g, W, T, acc, ws->nacc, ncand, ident, env, olds, multi, hazard, alloc, ukind, uother, grow,
+               stop_after);
+}
+
+__global__ void k_first_writer(WaveRule W, u32 epoch, const u32* acc, const WaveState* ws, const u8* hazard,
+                               const u32* olds, const u8* ukind, const u32* uother, const u8* grow,
+                               unsigned long long* fw_cls, unsigned long long* fw_fresh) {
+  d_first_writer(GTID, GNTH, W, epoch, acc, ws->nacc, hazard, olds, ukind, uother, grow, fw_cls, fw_fresh);
+}
+
+__global__ void k_validity(WaveRule W, WaveTab T, int nslots, int nsrc, u32 ncand, const u8* hazard, const u32* env,
+                           const u32* olds, const u32* accpre, const u8* status, const u32* ident,
+                           const unsigned long long* fw_cls, const unsigned long long* fw_fresh, u32* first_bad) {
+  d_validity(GTID, GNTH, W, T, nslots, nsrc, ncand, hazard, env, olds, accpre, status, ident, fw_cls, fw_fresh,
+             first_bad);
+}
+
+__global__ void k_find_stops(const u32* acc, const WaveState* ws, const u8* stop_after, const u32* apre,
+                             const u32* alloc, const Counters* cnt, i64 n_max, u32* out) {
+  d_find_stops(GTID, GNTH, acc, ws->nacc, stop_after, apre, alloc, (i64)cnt->live, n_max, out);
+}
+
+__global__ void k_commit_unions(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const u32* olds,
+                                const u8* ukind, const u32* uother, const u8* grow) {
+  d_commit_unions(GTID, GNTH, g, W, T, acc, ws->ncommit_acc, olds, ukind, uother, grow);
+}
+
+__global__ void k_seg_stats(const u8* status, WaveState* ws, u32 ncand, const u32* accpre, const u32* alloc,
+                            const u8* ukind, int efficient, DevStats* st) {
+  u32 nc = ws->ncommit_cand;
+  d_seg_stats(GTID, GNTH, status, ws, nc < ncand ? nc : ncand, accpre, alloc, ukind, efficient, st);
+}
+
+__global__ void k_win_flags(WaveTab T, const u32* ident, u64 nreq, const ReqT* tmpl, int R, const WaveState* ws,
+                            u32* wf, u32* ka) {
+  d_win_flags(GTID, GNTH, T, ident, nreq, tmpl, R, (u64)ws->ncommit_acc * R, wf, ka);
+}
+
+__global__ void k_assign_ids(WaveTab T, const u32* ident, u64 nreq, const u32* wf, const u32* wpre,
+                             const WaveState* ws) {
+  d_assign_ids(GTID, GNTH, T, ident, nreq, wf, wpre, ws->base);
+}
+
+__global__ void k_write_nodes(G g, WaveRule W, WaveTab T, const u32* acc, const u32* ident, u64 nreq,
+                              const u32* wf, const u32* wpre, const u32* kpre, const WaveState* ws,
+                              const u32* env, const u32* olds) {
+  d_write_nodes(GTID, GNTH, g, W, T, acc, ident, nreq, wf, wpre, kpre, ws->base, ws->kbase, env, olds);
+}
+
+__global__ void k_insert_range(G g, const WaveState* ws, u64 bound) {
+  u32 a = ws->base, n = ws->nwin;
+  GRID_STRIDE(i, bound) if (i < n) hc_insert(g, a + (u32)i);
+}
+
+// ---------------------------------------------------------------- device-side wave control
+
+// block-wide exclusive scan of f(i), i < n, with the total at out[n]
+// (all threads of the block must call it)
+template <int BT, class F>
+__device__ __forceinline__ u32 block_scan(u32 n, u32* out, F f) {
+  typedef cub::BlockScan<u32, BT> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ u32 carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u32 base = 0; base < n; base += BT) {
+    u32 i = base + threadIdx.x;
+    u32 v = i < n ? f(i) : 0u, x, tot;
+    BS(tmp).ExclusiveSum(v, x, tot);
+    if (i < n) out[i] = carry + x;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  u32 total = carry;
+  if (threadIdx.x == 0) out[n] = total;
+  __syncthreads();
+  return total;
+}
+
+// single-CTA exclusive scan with the total at out[n] (small arrays; CUB's two
+// kernels cost more than the work at wave sizes)
+__global__ void __launch_bounds__(1024) k_scan_block(const u32* in, u32* out, u32 n) {
+  block_scan<1024>(n, out, [&](u32 i) { return in[i]; });
+}
+
+// accepted list (status 0 or flagged) in candidate order; ws->nacc
+__global__ void __launch_bounds__(1024) k_accept_scan(const u8* status, const u8* hazard, u32 n, u32* pre, u32* acc,
+                                                      WaveState* ws) {
+  u32 tot = block_scan<1024>(n, pre, [&](u32 c) { return (status[c] == 0 || hazard[c]) ? 1u : 0u; });
+  for (u32 c = threadIdx.x; c < n; c += 1024)
+    if (status[c] == 0 || hazard[c]) acc[pre[c]] = c;
+  if (threadIdx.x == 0) ws->nacc = tot;
+}
+
+__global__ void k_boundary(WaveState* ws, const u32* stops, u32 ncand, const unsigned long long* pos,
+                           unsigned long long p, unsigned long long seg_end, const u32* pre, const u8* hazard) {
+  if (threadIdx.x || blockIdx.x) return;
+  d_boundary(ws, stops, ncand, pos, p, seg_end, pre, hazard);
 }
 
 __global__ void k_commit_prep(WaveState* ws, const u32* wpre, const u32* kpre, u64 nq, const Counters* cnt) {
@@ -698,6 +800,262 @@ __global__ void k_counters_commit(WaveState* ws, Counters* cnt) {
   if (ws->any_applied) cnt->dirty = 1;
 }
 
+// ---------------------------------------------------------------- single-CTA wave loop
+
+// Buffers of one wave (device pointers).
+struct WaveIO {
+  u8 *status, *hazard, *ukind, *grow, *sa;
+  u32 *env, *olds, *pre, *acc, *ident, *alloc, *apre, *wf, *wpre, *ka, *kpre, *uother, *stops;
+  unsigned long long *fw_cls, *fw_fresh;
+  WaveState* ws;
+  DevStats* wstats;
+  const int* lvl;
+};
+
+// reasons the CTA loop returns to the host
+#define CR_DONE 0     // positions exhausted
+#define CR_HAZARD 1   // exact path for position p, then resume at p + 1
+#define CR_STOP 2     // node limit: iteration stops
+#define CR_REJOIN 3   // multi-pattern join cache invalid (or capped list exhausted)
+#define CR_CAPACITY 4 // grow node / kid / hashcons capacity, then resume
+#define CR_WIDE 5     // clean full windows: continue on the grid path
+#define CR_ERROR 6    // analysis/table capacity error (exact path reports it)
+
+struct CtaCtl {
+  unsigned long long p, P;
+  u32 win, epoch;
+  u32 jcursor, jtotal;
+  int jcomplete;
+  u32 reason;
+  u32 waves, clean_full;
+  u32 cuts[6];
+  unsigned long long found, self, compat;
+  unsigned long long s_cand, s_req, s_win, s_nk;
+  i64 overshoot;
+  u32 seq_stop;
+};
+
+struct CtaArgs {
+  int nlv;                 // request levels (depth 1 .. nlv-1)
+  int lvl_off[12];
+  int nlvl[12];
+  int skip_self, multi, Kmax;
+  u32 nA, nB;
+  i64 n_max;
+  u32 cta_win;
+  const unsigned long long* pos;  // cached join list (multi)
+};
+
+__device__ __forceinline__ unsigned long long self_in(u32 nA, u32 nB, unsigned long long p0, unsigned long long p1) {
+  // #{i < nA : p0 <= i * (nB + 1) < p1}
+  unsigned long long d = (unsigned long long)nB + 1;
+  unsigned long long lo = (p0 + d - 1) / d, hi = (p1 + d - 1) / d;
+  if (hi > nA) hi = nA;
+  return hi > lo ? hi - lo : 0;
+}
+
+#define CTA_T 512
+
+__global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev RD, WaveRule W, WaveTab T, WaveIO io,
+                                                       CtaArgs A, CtaCtl* ctl) {
+  __shared__ unsigned long long s_p, s_seg_end;
+  __shared__ u32 s_ncand, s_jcur, s_exit, s_epoch, s_nacc, s_ncacc, s_base, s_kbase;
+  __shared__ int s_rejoin_after;
+  const u64 tid = threadIdx.x, nth = CTA_T;
+  if (tid == 0) {
+    s_p = ctl->p;
+    s_jcur = ctl->jcursor;
+    s_epoch = ctl->epoch;
+  }
+  __syncthreads();
+  while (true) {
+    if (tid == 0) {
+      s_exit = 0xFFFFFFFFu;
+      s_rejoin_after = 0;
+      unsigned long long p = s_p, P = ctl->P;
+      Counters* cn = g.cnt;
+      if (p >= P) {
+        s_exit = CR_DONE;
+      } else if ((i64)cn->live >= A.n_max) {
+        ctl->seq_stop = 1;
+        ctl->overshoot = (i64)cn->live - A.n_max;
+        s_exit = CR_STOP;
+      } else {
+        u32 win = ctl->win;
+        u32 ncand;
+        unsigned long long seg_end = P;
+        if (!A.multi) {
+          unsigned long long n = P - p < win ? P - p : win;
+          ncand = (u32)n;
+          seg_end = p + n;
+        } else {
+          u32 remain = ctl->jtotal - s_jcur;
+          ncand = remain < win ? remain : win;
+          if (ncand < remain) seg_end = A.pos[s_jcur + ncand];
+          else if (!ctl->jcomplete) {
+            seg_end = A.pos[ctl->jtotal - 1] + 1;
+            s_rejoin_after = 1;
+          }
+        }
+        if (ncand == 0) {
+          unsigned long long cover = seg_end - p, self = A.skip_self ? self_in(A.nA, A.nB, p, seg_end) : 0;
+          ctl->found += cover;
+          ctl->self += self;
+          ctl->compat += cover - self;
+          s_p = seg_end;
+          s_exit = s_rejoin_after ? CR_REJOIN : 0xFFFFFFFEu;  // continue
+        } else {
+          u64 need_n = (u64)cn->next_id + (u64)ncand * W.R + 2;
+          u64 need_k = (u64)cn->nkids + (u64)ncand * A.Kmax + 2;
+          if (need_n + 1 > g.cap_nodes || need_k + 1 > g.cap_kids || 2 * need_n > (u64)g.hc_mask + 1) {
+            s_exit = CR_CAPACITY;
+          } else {
+            s_ncand = ncand;
+            s_seg_end = seg_end;
+            s_epoch += 1;
+            ctl->waves += 1;
+            io.stops[0] = io.stops[1] = io.stops[2] = TSAT_NONE;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    {
+      u32 ex = s_exit;
+      __syncthreads();
+      if (ex == 0xFFFFFFFEu) continue;
+      if (ex != 0xFFFFFFFFu) break;
+    }
+    const u32 ncand = s_ncand;
+    const unsigned long long p = s_p;
+    const unsigned long long* posp = A.multi ? A.pos + s_jcur : nullptr;
+    WaveTab Tw = T;
+    Tw.epoch = s_epoch;
+    // ---- gates + accepted list
+    d_gates(tid, nth, g, R, RD, posp, ncand, p, io.status, io.env, io.olds, io.hazard);
+    __syncthreads();
+    {
+      u32 tot = block_scan<CTA_T>(ncand, io.pre,
+                                  [&](u32 c) { return (io.status[c] == 0 || io.hazard[c]) ? 1u : 0u; });
+      for (u32 c = tid; c < ncand; c += CTA_T)
+        if (io.status[c] == 0 || io.hazard[c]) io.acc[io.pre[c]] = c;
+      if (tid == 0) s_nacc = tot;
+      __syncthreads();
+    }
+    const u32 nacc = s_nacc;
+    // ---- resolve requests level by level
+    if (W.R > 0) {
+      for (int d = 1; d < A.nlv; d++) {
+        if (!A.nlvl[d]) continue;
+        d_resolve_level(tid, nth, g, W, Tw, io.acc, nacc, io.lvl + A.lvl_off[d], A.nlvl[d], io.env, io.ident,
+                        io.hazard);
+        __syncthreads();
+      }
+      d_mark_roots(tid, nth, W, Tw, io.acc, nacc, io.ident, io.hazard, io.olds);
+      __syncthreads();
+    }
+    d_cand_check(tid, nth, g, W, Tw, io.acc, nacc, ncand, io.ident, io.env, io.olds, A.multi, io.hazard, io.alloc,
+                 io.ukind, io.uother, io.grow, io.sa);
+    __syncthreads();
+    // ---- conflicts, stop-after, node-limit cutoff, boundary
+    d_first_writer(tid, nth, W, Tw.epoch, io.acc, nacc, io.hazard, io.olds, io.ukind, io.uother, io.grow, io.fw_cls,
+                   io.fw_fresh);
+    __syncthreads();
+    d_validity(tid, nth, W, Tw, R.nslots, R.nsrc, ncand, io.hazard, io.env, io.olds, io.pre, io.status, io.ident,
+               io.fw_cls, io.fw_fresh, io.stops + 2);
+    block_scan<CTA_T>(ncand, io.apre, [&](u32 c) { return io.alloc[c]; });
+    d_find_stops(tid, nth, io.acc, nacc, io.sa, io.apre, io.alloc, (i64)g.cnt->live, A.n_max, io.stops);
+    __syncthreads();
+    if (tid == 0) {
+      d_boundary(io.ws, io.stops, ncand, posp, p, s_seg_end, io.pre, io.hazard);
+      s_ncacc = io.ws->ncommit_acc;
+      s_base = g.cnt->next_id;
+      s_kbase = g.cnt->nkids;
+    }
+    __syncthreads();
+    const u32 ncacc = s_ncacc;
+    d_seg_stats(tid, nth, io.status, io.ws, io.ws->ncommit_cand, io.pre, io.alloc, io.ukind, R.efficient, io.wstats);
+    // ---- commit (requests of committed combos only)
+    const u64 lim = (u64)ncacc * W.R;
+    u32 nwin = 0, nk = 0;
+    if (lim) {
+      d_win_flags(tid, nth, Tw, io.ident, lim, W.tmpl, W.R, lim, io.wf, io.ka);
+      __syncthreads();
+      nwin = block_scan<CTA_T>((u32)lim, io.wpre, [&](u32 q) { return io.wf[q]; });
+      nk = block_scan<CTA_T>((u32)lim, io.kpre, [&](u32 q) { return io.ka[q]; });
+      d_assign_ids(tid, nth, Tw, io.ident, lim, io.wf, io.wpre, s_base);
+      __syncthreads();
+      d_write_nodes(tid, nth, g, W, Tw, io.acc, io.ident, lim, io.wf, io.wpre, io.kpre, s_base, s_kbase, io.env,
+                    io.olds);
+      __syncthreads();  // unions overwrite parent[] of fresh non-root nodes
+    }
+    d_commit_unions(tid, nth, g, W, Tw, io.acc, ncacc, io.olds, io.ukind, io.uother, io.grow);
+    __syncthreads();
+    for (u32 i = tid; i < nwin; i += CTA_T) hc_insert(g, s_base + i);
+    __syncthreads();
+    // ---- bookkeeping (thread 0)
+    if (tid == 0) {
+      WaveState* ws = io.ws;
+      Counters* cn = g.cnt;
+      cn->next_id += nwin;
+      cn->live += nwin;
+      cn->nkids += nk;
+      if (ws->any_applied) cn->dirty = 1;
+      ctl->s_cand += ncand;
+      ctl->s_req += (unsigned long long)nacc * W.R;
+      ctl->s_win += nwin;
+      ctl->s_nk += nk;
+      u32 ncommit = ws->ncommit_cand;
+      unsigned long long p_end = ws->p_end;
+      bool stop = ws->stop != 0, hazard = ws->hazard != 0;
+      if (ncommit < ncand && !stop) ctl->cuts[ws->why < 5 ? ws->why : 5] += 1;
+      unsigned long long cover = p_end - p, self = A.skip_self ? self_in(A.nA, A.nB, p, p_end) : 0;
+      ctl->found += cover;
+      ctl->self += self;
+      ctl->compat += cover - self - ncommit;
+      if (A.multi) s_jcur += ncommit;
+      s_p = p_end;
+      u32 exitr = 0xFFFFFFFFu;
+      if (stop) {
+        if (p_end < ctl->P) {
+          ctl->seq_stop = 1;
+          ctl->overshoot = (i64)cn->live - A.n_max;
+          exitr = CR_STOP;
+        }
+      } else {
+        u32 win = ctl->win;
+        if (ncommit < ncand) {
+          u32 w2 = 2u * ncommit + 32u;
+          win = w2 < 64u ? 64u : w2;
+          ctl->clean_full = 0;
+        } else {
+          win = win * 4u;
+          if (ncand >= A.cta_win) ctl->clean_full += 1;
+        }
+        if (win > A.cta_win) win = A.cta_win;
+        ctl->win = win;
+        if (hazard) exitr = CR_HAZARD;
+        else if (A.multi && ws->sa_hit) exitr = CR_REJOIN;
+        else if (s_rejoin_after) exitr = CR_REJOIN;
+        else if (ctl->clean_full >= 2) exitr = CR_WIDE;
+      }
+      s_exit = exitr;
+    }
+    __syncthreads();
+    {
+      u32 ex = s_exit;
+      __syncthreads();
+      if (ex != 0xFFFFFFFFu) break;
+    }
+  }
+  if (tid == 0) {
+    ctl->p = s_p;
+    ctl->jcursor = s_jcur;
+    ctl->epoch = s_epoch;
+    ctl->reason = s_exit;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 struct WaveBufs {
@@ -705,7 +1063,9 @@ struct WaveBufs {
   DevBuf<u64> hA, hB, hBs;
   DevBuf<u32> iB, iBs, cnt, off;
   DevBuf<u8> status, hazard;
-  DevBuf<u32> env, olds, fl, pre, acc, ident, alloc, apre, wf, wpre, ka, kpre, stops, uother, fw_cls, fw_fresh;
+  DevBuf<u32> env, olds, fl, pre, acc, ident, alloc, apre, wf, wpre, ka, kpre, stops, uother;
+  DevBuf<unsigned long long> fw_cls, fw_fresh;  // epoch-tagged first writers
+  DevBuf<CtaCtl> ctl;
   DevBuf<u8> ukind, grow, sa;
   DevBuf<WaveState> ws;
   DevBuf<DevStats> wstats;
@@ -716,6 +1076,8 @@ struct WaveBufs {
   DevBuf<unsigned long long> wminpos;
   DevBuf<Val> wval;
   u32 wcap = 0;
+  u32 epoch = 0;  // per-wave tag of the wave table / first-writer arrays
+  u64 cand_cap = 0;
 };
 
 void free_wave_bufs(WaveBufs* b) { delete b; }
@@ -794,7 +1156,84 @@ static void accumulate_seg(Engine& e, int ri, const DevStats& d) {
   if (d.changed) e.seq_changed = true;
 }
 
-// one rule, positions [p0, P): waves + exact fallback at hazards
+
+#define CTA_WIN 2048u
+
+// per-candidate buffers, wave table and first-writer arrays for windows of up
+// to ncand candidates (grown only; fresh tag arrays are set to "no epoch")
+static void ensure_cand_bufs(Engine& e, WaveBufs& B, u64 ncand, int R) {
+  if (ncand > B.cand_cap) {
+    u64 n = std::max<u64>(ncand, 1024);
+    B.status.ensure(n + 1);
+    B.hazard.ensure(n + 1);
+    B.env.ensure(n * MAX_VARS + 1);
+    B.olds.ensure(n * MAX_SRC + 1);
+    B.pre.ensure(n + 1);
+    B.acc.ensure(n + 1);
+    B.alloc.ensure(n + 1);
+    B.apre.ensure(n + 2);
+    B.ukind.ensure(n * MAX_SRC + 1);
+    B.uother.ensure(n * MAX_SRC + 1);
+    B.grow.ensure(n * MAX_SRC + 1);
+    B.sa.ensure(n + 1);
+    B.fl.ensure(n + 1);
+    B.cand_cap = n;
+  }
+  u64 nreq = ncand * (u64)R;
+  B.ident.ensure(nreq + 1);
+  B.wf.ensure(nreq + 2);
+  B.wpre.ensure(nreq + 2);
+  B.ka.ensure(nreq + 2);
+  B.kpre.ensure(nreq + 2);
+  B.ws.ensure(1);
+  B.stops.ensure(4);
+  B.ctl.ensure(1);
+  u64 want = 1024;
+  while (want < 2 * nreq + 16) want *= 2;
+  if (want > B.wcap) {
+    B.wcap = (u32)want;
+    B.wstate.alloc(want);
+    B.wkey.alloc(want * 10);
+    B.wid.alloc(want);
+    B.wroot.alloc(want);
+    B.wold.alloc(want);
+    B.wminpos.alloc(want);
+    B.wval.alloc(want);
+    B.fw_fresh.alloc(want + 1);
+    CUDA_OK(cudaMemsetAsync(B.wstate.p, 0, want * sizeof(u32), e.s));
+    CUDA_OK(cudaMemsetAsync(B.wroot.p, 0, want * sizeof(u32), e.s));
+    CUDA_OK(cudaMemsetAsync(B.wminpos.p, 0xFF, want * sizeof(unsigned long long), e.s));
+    CUDA_OK(cudaMemsetAsync(B.fw_fresh.p, 0xFF, (want + 1) * sizeof(unsigned long long), e.s));
+  }
+  if (B.fw_cls.cap < (u64)e.cap_nodes + 1) {
+    B.fw_cls.alloc((u64)e.cap_nodes + 1);
+    CUDA_OK(cudaMemsetAsync(B.fw_cls.p, 0xFF, ((u64)e.cap_nodes + 1) * sizeof(unsigned long long), e.s));
+  }
+}
+
+static unsigned long long self_in_host(u32 nA, u32 nB, unsigned long long p0, unsigned long long p1) {
+  unsigned long long d = (unsigned long long)nB + 1;
+  unsigned long long lo = (p0 + d - 1) / d, hi = (p1 + d - 1) / d;
+  if (hi > nA) hi = nA;
+  return hi > lo ? hi - lo : 0;
+}
+
+// algorithmic bytes of a wave (what the apply must touch at least):
+// candidates: match rows + subst/olds writes + analyses read by the shape check;
+// requests: hashcons probe (slot + key) + wave-table key/pos + analysis write;
+// committed nodes: op, koff, kids, parent, flags, analysis, hashcons slot
+static double wave_bytes(const Engine& e, const RuleDev& Rd, double ncand, double nreq, double nwin, double nk) {
+  double nb = 0;
+  for (int t = 0; t < Rd.nsrc; t++) nb += 4.0 * (1 + Rd.nb[t]);
+  double per_cand = nb + 4.0 * (Rd.nslots + Rd.nsrc) + (e.analysis ? 128.0 * Rd.nslots : 0.0);
+  double per_req = 4.0 + 16.0 + 4.0 * 2 + 48.0 + (e.analysis ? 128.0 : 0.0);
+  double per_node = 21.0 + (e.analysis ? 128.0 : 0.0);
+  return per_cand * ncand + per_req * nreq + per_node * nwin + 4.0 * nk;
+}
+
+// one rule, positions [0, P): waves + exact fallback at hazards.  Windows of
+// up to CTA_WIN candidates run inside k_wave_cta (one launch for a whole run
+// of waves); larger windows run as grid waves.
 void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P) {
   const HRule& hr = e.rules[ri];
   if (!e.wave) e.wave = new WaveBufs();
@@ -813,10 +1252,14 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     lvl_flat.insert(lvl_flat.end(), l.begin(), l.end());
   }
   lvl_off.push_back((int)lvl_flat.size());
+  if (lv.size() > 12) throw TsatException(TSAT_ERR_UNSUPPORTED, "target deeper than the wave engine supports");
   B.lvl.ensure(lvl_flat.size() + 1);
   if (!lvl_flat.empty())
     CUDA_OK(cudaMemcpyAsync(B.lvl.p, lvl_flat.data(), lvl_flat.size() * sizeof(int), cudaMemcpyHostToDevice, e.s));
+  int Kmax = 0;
+  for (auto& q : tm) Kmax += q.nargs;
   int skip_self = (hr.nsrc == 2 && !allow_self && hr.same_canon) ? 1 : 0;
+  const bool multi = hr.nsrc > 1;
   RuleStatsH& rs = e.rstats[ri];
   B.wstats.ensure(1);
   CUDA_OK(cudaMemsetAsync(B.wstats.p, 0, sizeof(DevStats), e.s));
@@ -832,60 +1275,132 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     if ((i64)e.h.live >= n_max) {
       e.seq_stop = true;
       e.report.node_limit_overshoot = (i64)e.h.live - n_max;
-      return;
+      break;
     }
     RuleDev Rd = make_rule_dev(e, ri, filter_mode, allow_self);
     ReachDev RD = make_reach_dev(e);
+    // ---- 1. compatible positions of a multi-pattern rule (cached)
+    if (multi && !jvalid) {
+      u32 nA = Rd.nmatch[0], nB = Rd.nmatch[1];
+      u32 i0 = (u32)(p / nB);
+      u32 na = nA - i0;
+      B.hA.ensure(na + 1);
+      B.hB.ensure(nB + 1);
+      B.hBs.ensure(nB + 1);
+      B.iB.ensure(nB + 1);
+      B.iBs.ensure(nB + 1);
+      B.cnt.ensure(na + 1);
+      B.off.ensure(na + 1);
+      DevBuf<u32>& dummy = e.scratch_u32[6];
+      dummy.ensure(na + 1);
+      k_hash_rows<<<nblk(nB), 256, 0, e.s>>>(e.view(), Rd.mbind[1], Rd.nb[1], nB, W, 1, B.hB.p, B.iB.p);
+      k_hash_rows<<<nblk(na), 256, 0, e.s>>>(e.view(), Rd.mbind[0] + (u64)i0 * Rd.nb[0], Rd.nb[0], na, W, 0, B.hA.p,
+                                             dummy.p);
+      {
+        size_t bytes = 0;
+        CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
+        e.temp.ensure(bytes + 16);
+        CUDA_OK(cub::DeviceRadixSort::SortPairs(e.temp.p, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
+      }
+      k_join<<<nblk((u64)na * 32), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self,
+                                                 nullptr, B.cnt.p, nullptr, 0);
+      CUDA_OK(cudaMemsetAsync(B.cnt.p + na, 0, sizeof(u32), e.s));
+      dev_exclusive_scan_u32(e, B.cnt.p, B.off.p, na + 1);
+      u32 total = read_u32(e, B.off.p + na);
+      jtotal = std::min<u32>(total, JCAP);
+      jcomplete = total <= JCAP;
+      B.pos.ensure((u64)jtotal + 1);
+      if (jtotal)
+        k_join<<<nblk((u64)na * 32), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self,
+                                                   B.off.p, nullptr, B.pos.p, jtotal);
+      jcursor = 0;
+      jvalid = true;
+    }
+    u64 remain = multi ? (u64)(jtotal - jcursor) : (u64)(P - p);
+    if (std::min<u64>(remain, win) <= CTA_WIN) {
+      // ---- single-CTA run of waves
+      e.ensure_nodes((u64)CTA_WIN * R + 2, (u64)CTA_WIN * Kmax + 2);
+      ensure_cand_bufs(e, B, CTA_WIN, R);
+      CtaCtl c;
+      memset(&c, 0, sizeof(c));
+      c.p = p;
+      c.P = P;
+      c.win = std::min<u32>(win, CTA_WIN);
+      c.epoch = B.epoch;
+      c.jcursor = jcursor;
+      c.jtotal = jtotal;
+      c.jcomplete = jcomplete ? 1 : 0;
+      c.reason = CR_DONE;
+      CUDA_OK(cudaMemcpyAsync(B.ctl.p, &c, sizeof(c), cudaMemcpyHostToDevice, e.s));
+      WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0};
+      WaveIO io{B.status.p, B.hazard.p, B.ukind.p, B.grow.p, B.sa.p, B.env.p, B.olds.p, B.pre.p, B.acc.p,
+                B.ident.p, B.alloc.p, B.apre.p, B.wf.p, B.wpre.p, B.ka.p, B.kpre.p, B.uother.p, B.stops.p,
+                B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, B.lvl.p};
+      CtaArgs A;
+      memset(&A, 0, sizeof(A));
+      A.nlv = (int)lv.size();
+      for (size_t d = 0; d < lv.size(); d++) {
+        A.lvl_off[d] = lvl_off[d];
+        A.nlvl[d] = (int)lv[d].size();
+      }
+      A.skip_self = skip_self;
+      A.multi = multi ? 1 : 0;
+      A.Kmax = Kmax;
+      A.nA = Rd.nmatch[0];
+      A.nB = multi ? Rd.nmatch[1] : 1;
+      A.n_max = n_max;
+      A.cta_win = CTA_WIN;
+      A.pos = B.pos.p;
+      {
+        KTimer kt(e, KG_APPLY_WAVE, 0.0, 1);
+        k_wave_cta<<<1, CTA_T, 0, e.s>>>(e.view(), Rd, RD, W, T, io, A, B.ctl.p);
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaMemcpyAsync(&c, B.ctl.p, sizeof(c), cudaMemcpyDeviceToHost, e.s));
+        CUDA_OK(cudaMemcpyAsync(&e.h, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
+        e.sync();
+        kt.bytes = wave_bytes(e, Rd, (double)c.s_cand, (double)c.s_req, (double)c.s_win, (double)c.s_nk);
+      }
+      B.epoch = c.epoch;
+      rs.found += c.found;
+      rs.skipped_self += c.self;
+      rs.skipped_compat += c.compat;
+      e.phase_ms[8] += c.waves;
+      for (int k = 0; k < 6; k++) e.phase_ms[10 + k] += c.cuts[k];
+      p = c.p;
+      jcursor = c.jcursor;
+      win = c.win;
+      if (c.reason == CR_STOP) {
+        e.seq_stop = true;
+        e.report.node_limit_overshoot = c.overshoot;
+        break;
+      } else if (c.reason == CR_HAZARD) {
+        e.phase_ms[9] += 1;
+        if (multi) jvalid = false;
+        e.ensure_nodes(4096, 4096);
+        e.run_rule_seq(ri, filter_mode, allow_self, n_max, p, p + 1);
+        if (e.seq_stop) break;
+        p = p + 1;
+      } else if (c.reason == CR_REJOIN) {
+        jvalid = false;
+      } else if (c.reason == CR_WIDE) {
+        win = 4 * CTA_WIN;
+      }
+      continue;
+    }
     e.phase_ms[8] += 1;  // waves
-    // ---- 1. candidates
+    // ---- candidates of a grid wave
     u32 ncand = 0;
     const unsigned long long* posp = nullptr;
     unsigned long long seg_end = P;  // positions covered if every candidate commits
-    if (hr.nsrc == 1) {
+    if (!multi) {
       unsigned long long n = std::min<unsigned long long>(P - p, win);
       ncand = (u32)n;
       seg_end = p + n;
     } else {
-      u32 nA = Rd.nmatch[0], nB = Rd.nmatch[1];
-      if (!jvalid) {
-        u32 i0 = (u32)(p / nB);
-        u32 na = nA - i0;
-        B.hA.ensure(na + 1);
-        B.hB.ensure(nB + 1);
-        B.hBs.ensure(nB + 1);
-        B.iB.ensure(nB + 1);
-        B.iBs.ensure(nB + 1);
-        B.cnt.ensure(na + 1);
-        B.off.ensure(na + 1);
-        DevBuf<u32>& dummy = e.scratch_u32[6];
-        dummy.ensure(na + 1);
-        k_hash_rows<<<nblk(nB), 256, 0, e.s>>>(e.view(), Rd.mbind[1], Rd.nb[1], nB, W, 1, B.hB.p, B.iB.p);
-        k_hash_rows<<<nblk(na), 256, 0, e.s>>>(e.view(), Rd.mbind[0] + (u64)i0 * Rd.nb[0], Rd.nb[0], na, W, 0,
-                                               B.hA.p, dummy.p);
-        {
-          size_t bytes = 0;
-          CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
-          e.temp.ensure(bytes + 16);
-          CUDA_OK(cub::DeviceRadixSort::SortPairs(e.temp.p, bytes, B.hB.p, B.hBs.p, B.iB.p, B.iBs.p, nB, 0, 64, e.s));
-        }
-        k_join<<<nblk((u64)na * 32), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self,
-                                                   nullptr, B.cnt.p, nullptr, 0);
-        CUDA_OK(cudaMemsetAsync(B.cnt.p + na, 0, sizeof(u32), e.s));
-        dev_exclusive_scan_u32(e, B.cnt.p, B.off.p, na + 1);
-        u32 total = read_u32(e, B.off.p + na);
-        jtotal = std::min<u32>(total, JCAP);
-        jcomplete = total <= JCAP;
-        B.pos.ensure((u64)jtotal + 1);
-        if (jtotal)
-          k_join<<<nblk((u64)na * 32), 256, 0, e.s>>>(e.view(), Rd, W, B.hA.p, i0, B.hBs.p, B.iBs.p, p, skip_self,
-                                                     B.off.p, nullptr, B.pos.p, jtotal);
-        jcursor = 0;
-        jvalid = true;
-      }
-      u32 remain = jtotal - jcursor;
-      ncand = std::min<u32>(remain, win);
+      u32 rem = jtotal - jcursor;
+      ncand = std::min<u32>(rem, win);
       posp = B.pos.p + jcursor;
-      if (ncand < remain) {
+      if (ncand < rem) {
         // coverage ends right before the next cached candidate
         CUDA_OK(cudaMemcpyAsync(&seg_end, B.pos.p + jcursor + ncand, sizeof(seg_end), cudaMemcpyDeviceToHost, e.s));
         e.sync();
@@ -896,63 +1411,12 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         jvalid = false;  // re-join after the capped list
       }
     }
-    if (ncand == 0) {
-      // nothing compatible left: every remaining position is a self or compat skip
-      unsigned long long cover = seg_end - p;
-      unsigned long long self = 0;
-      if (skip_self) {
-        u32 nB = Rd.nmatch[1];
-        for (u32 i = (u32)(p / nB); i < Rd.nmatch[0]; i++) {
-          unsigned long long q = (unsigned long long)i * nB + i;
-          if (q >= p && q < seg_end) self++;
-        }
-      }
-      rs.found += cover;
-      rs.skipped_self += self;
-      rs.skipped_compat += cover - self;
-      p = seg_end;
-      continue;
-    }
     // ---- 2. gates + accepted list
-    int Kmax = 0;
-    for (auto& q : tm) Kmax += q.nargs;
     e.ensure_nodes((u64)ncand * R + 2, (u64)ncand * Kmax + 2);
-    B.status.ensure(ncand + 1);
-    B.hazard.ensure(ncand + 1);
-    B.env.ensure((u64)ncand * MAX_VARS + 1);
-    B.olds.ensure((u64)ncand * MAX_SRC + 1);
-    B.pre.ensure(ncand + 1);
-    B.acc.ensure(ncand + 1);
-    B.ws.ensure(1);
+    ensure_cand_bufs(e, B, ncand, R);
     WaveState* ws = B.ws.p;
     u64 nreq_max = (u64)ncand * R;
-    B.ident.ensure(nreq_max + 1);
-    B.alloc.ensure(ncand + 1);
-    B.apre.ensure(ncand + 2);
-    B.ukind.ensure((u64)ncand * MAX_SRC + 1);
-    B.uother.ensure((u64)ncand * MAX_SRC + 1);
-    B.grow.ensure((u64)ncand * MAX_SRC + 1);
-    B.sa.ensure(ncand + 1);
-    u32 used = 1;
-    if (R > 0) {
-      u32 want = 1024;
-      while (want < 2 * nreq_max + 16) want *= 2;
-      if (want > B.wcap) {
-        B.wcap = want;
-        B.wstate.alloc(want);
-        B.wkey.alloc((u64)want * 10);
-        B.wid.alloc(want);
-        B.wroot.alloc(want);
-        B.wold.alloc(want);
-        B.wminpos.alloc(want);
-        B.wval.alloc(want);
-      }
-      used = want;
-      CUDA_OK(cudaMemsetAsync(B.wstate.p, 0, (u64)used * sizeof(u32), e.s));
-      CUDA_OK(cudaMemsetAsync(B.wroot.p, 0, (u64)used * sizeof(u32), e.s));
-      CUDA_OK(cudaMemsetAsync(B.wminpos.p, 0xFF, (u64)used * sizeof(unsigned long long), e.s));
-    }
-    WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, used - 1, B.wold.p};
+    WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, ++B.epoch};
     {
       KTimer kt(e, KG_APPLY_WAVE, 0.0, 16 + lv.size());
       k_gates<<<nblk(ncand, 128), 128, 0, e.s>>>(e.view(), Rd, RD, W, posp, ncand, p, B.status.p, B.env.p, B.olds.p,
@@ -960,7 +1424,6 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       if (ncand <= 65536) {
         k_accept_scan<<<1, 1024, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.pre.p, B.acc.p, ws);
       } else {
-        B.fl.ensure(ncand + 1);
         k_accept_flags<<<nblk(ncand), 256, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.fl.p);
         CUDA_OK(cudaMemsetAsync(B.fl.p + ncand, 0, sizeof(u32), e.s));
         dev_exclusive_scan_u32(e, B.fl.p, B.pre.p, ncand + 1);
@@ -979,16 +1442,11 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         k_mark_roots<<<nblk(ncand), 256, 0, e.s>>>(W, T, B.acc.p, ws, B.ident.p, B.hazard.p, B.olds.p);
       }
       k_cand_check<<<nblk(ncand), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, ws, ncand, B.ident.p, B.env.p, B.olds.p,
-                                                 hr.nsrc > 1 ? 1 : 0, B.hazard.p, B.alloc.p, B.ukind.p, B.uother.p,
+                                                 multi ? 1 : 0, B.hazard.p, B.alloc.p, B.ukind.p, B.uother.p,
                                                  B.grow.p, B.sa.p);
       // ---- 4. read/write conflicts, stop-after, node-limit cutoff, boundary
-      B.fw_cls.ensure((u64)e.h.next_id + 1);
-      B.fw_fresh.ensure((u64)used + 1);
-      CUDA_OK(cudaMemsetAsync(B.fw_cls.p, 0xFF, ((u64)e.h.next_id + 1) * sizeof(u32), e.s));
-      CUDA_OK(cudaMemsetAsync(B.fw_fresh.p, 0xFF, ((u64)used + 1) * sizeof(u32), e.s));
-      k_first_writer<<<nblk(ncand), 256, 0, e.s>>>(W, B.acc.p, ws, B.hazard.p, B.olds.p, B.ukind.p, B.uother.p,
-                                                   B.grow.p, B.fw_cls.p, B.fw_fresh.p);
-      B.stops.ensure(4);
+      k_first_writer<<<nblk(ncand), 256, 0, e.s>>>(W, T.epoch, B.acc.p, ws, B.hazard.p, B.olds.p, B.ukind.p,
+                                                   B.uother.p, B.grow.p, B.fw_cls.p, B.fw_fresh.p);
       CUDA_OK(cudaMemsetAsync(B.stops.p, 0xFF, 3 * sizeof(u32), e.s));
       k_validity<<<nblk(ncand), 256, 0, e.s>>>(W, T, Rd.nslots, Rd.nsrc, ncand, B.hazard.p, B.env.p, B.olds.p, B.pre.p,
                                                B.status.p, B.ident.p, B.fw_cls.p, B.fw_fresh.p, B.stops.p + 2);
@@ -1005,10 +1463,6 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
                                                 B.wstats.p);
       // ---- 6. commit
       if (nreq_max) {
-        B.wf.ensure(nreq_max + 2);
-        B.wpre.ensure(nreq_max + 2);
-        B.ka.ensure(nreq_max + 2);
-        B.kpre.ensure(nreq_max + 2);
         k_win_flags<<<nblk(nreq_max), 256, 0, e.s>>>(T, B.ident.p, nreq_max, B.tmpl.p, R, ws, B.wf.p, B.ka.p);
         if (nreq_max <= 65536) {
           k_scan_block<<<1, 1024, 0, e.s>>>(B.wf.p, B.wpre.p, (u32)nreq_max);
@@ -1035,38 +1489,18 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     CUDA_OK(cudaMemcpyAsync(&hw, ws, sizeof(hw), cudaMemcpyDeviceToHost, e.s));
     CUDA_OK(cudaMemcpyAsync(&e.h, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
     e.sync();
-    {
-      // algorithmic bytes of the wave (what the apply must touch at least):
-      // candidates: match rows + subst/olds writes + analyses read by the shape check;
-      // requests: hashcons probe (slot + key) + wave-table key/pos + analysis write;
-      // committed nodes: op, koff, kids, parent, flags, analysis, hashcons slot
-      double nb = 0;
-      for (int t = 0; t < Rd.nsrc; t++) nb += 4.0 * (1 + Rd.nb[t]);
-      double per_cand = nb + 4.0 * (Rd.nslots + Rd.nsrc) + (e.analysis ? 128.0 * Rd.nslots : 0.0);
-      double per_req = 4.0 + 16.0 + 4.0 * 2 + 48.0 + (e.analysis ? 128.0 : 0.0);
-      double per_node = 21.0 + (e.analysis ? 128.0 : 0.0);
-      e.kstat[KG_APPLY_WAVE].bytes += per_cand * ncand + per_req * (double)hw.nacc * R + per_node * hw.nwin +
-                                      4.0 * hw.nk;
-    }
+    e.kstat[KG_APPLY_WAVE].bytes += wave_bytes(e, Rd, ncand, (double)hw.nacc * R, hw.nwin, hw.nk);
     u32 ncommit_cand = hw.ncommit_cand;
     unsigned long long p_end = hw.p_end;
     bool stop = hw.stop != 0, hazard = hw.hazard != 0;
     if (hw.ncommit_cand < ncand && !stop) e.phase_ms[10 + std::min<int>(hw.why, 5)] += 1;
     {
-      unsigned long long cover = p_end - p, self = 0;
-      if (skip_self) {
-        u32 nB = Rd.nmatch[1];
-        u32 ia = (u32)(p / nB), ib = (u32)std::min<unsigned long long>(Rd.nmatch[0], p_end / nB + 1);
-        for (u32 i = ia; i < ib; i++) {
-          unsigned long long q = (unsigned long long)i * nB + i;
-          if (q >= p && q < p_end) self++;
-        }
-      }
+      unsigned long long cover = p_end - p, self = skip_self ? self_in_host(Rd.nmatch[0], Rd.nmatch[1], p, p_end) : 0;
       rs.found += cover;
       rs.skipped_self += self;
       rs.skipped_compat += cover - self - ncommit_cand;
     }
-    if (hr.nsrc > 1) {
+    if (multi) {
       jcursor += ncommit_cand;
       // a union of existing classes (stop-after) or an exact-path combo can change compatibility
       if (hazard || hw.sa_hit) jvalid = false;
