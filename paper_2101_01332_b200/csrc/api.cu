@@ -256,8 +256,8 @@ int tsat_ematch(tsat_engine* h, int32_t pattern, uint32_t* out_cls, uint32_t* ou
   GUARD(h, {
     Engine& e = *h->e;
     if (pattern < 0 || pattern >= (int)e.patterns.size()) throw TsatException(TSAT_ERR_ARG, "bad pattern id");
-    MatchSet ms;
-    e.ematch_pattern(pattern, ms);
+    e.ematch_batch(std::vector<int>{pattern});
+    MatchSet& ms = e.matches[pattern];
     *n = ms.n;
     *nb = ms.nb;
     if (out_cls && cap >= (int64_t)ms.n && ms.n) {

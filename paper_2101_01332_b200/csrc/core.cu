@@ -666,6 +666,10 @@ __global__ void k_compact_alive(G g, u32 n, const u32* pos, u32* ids, u32* cls, 
   }
 }
 
+__global__ void k_gather_op(G g, const u32* ids, u32 m, u32* opk) {
+  GRID_STRIDE(i, m) opk[i] = g.op[ids[i]];
+}
+
 __global__ void k_class_heads(const u32* scls, u32 m, u32* head) {
   GRID_STRIDE(i, m) head[i] = (i == 0 || scls[i] != scls[i - 1]) ? 1u : 0u;
 }
@@ -743,11 +747,15 @@ void Engine::build_snapshot() {
   k_set_u32<<<1, 1, 0, s>>>(snap.cls_off.p, ncls, m);
   snap.cls_of.ensure(m + 1);
   k_member_class<<<nblk(m), 256, 0, s>>>(fl.p, pos.p, m, snap.cls_of.p);
-  // op CSR: stable sort alive ids by op atom
+  // op CSR in (op, class, id) order: stable sort of the class-ordered members
+  // by op atom, so e-matching emits each pattern's matches grouped by class
   snap.op_nodes.ensure(m + 1);
   snap.op_off.ensure(na + 1);
-  dev_sort_pairs_u32(*this, opk.p, tmp.p, ids.p, snap.op_nodes.p, m, bits_for(na));
+  k_gather_op<<<nblk(m), 256, 0, s>>>(view(), snap.cls_nodes.p, m, opk.p);
+  dev_sort_pairs_u32(*this, opk.p, tmp.p, snap.cls_nodes.p, snap.op_nodes.p, m, bits_for(na));
   k_lower_bounds<<<nblk((u64)na + 1), 256, 0, s>>>(tmp.p, m, na, snap.op_off.p);
+  snap.op_off_h.resize(na + 1);
+  CUDA_OK(cudaMemcpyAsync(snap.op_off_h.data(), snap.op_off.p, (na + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
   snap.n_alloc = n;
   snap.ncls = ncls;
   snap.n_atoms = na;

@@ -77,30 +77,70 @@ __global__ void k_rhist(const u32* edst, u64 ne, u32* h) {
   GRID_STRIDE(e, ne) atomicAdd(&h[edst[e]], 1u);
 }
 
-// fixpoint sweep over untrimmed classes
-__global__ void k_close_sweep(const u32* list, u32 nl, const u32* eoff, const u32* edst, u32* bits, u32 words,
-                              u32* changed) {
-  u32 warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  u32 lane = threadIdx.x & 31;
-  u32 nw = (gridDim.x * blockDim.x) >> 5;
-  for (u32 t = warp; t < nl; t += nw) {
-    u32 i = list[t];
-    u32* row = bits + (u64)i * words;
-    bool ch = false;
-    for (u32 w = lane; w < words; w += 32) {
-      u32 acc = row[w];
-      for (u32 e = eoff[i]; e < eoff[i + 1]; e++) {
+// Descendants closure, column-parallel.  The bitset is stored word-major
+// (bitsT[w * n + i] = word w of class i's descendant set), and word w of a
+// class depends only on word w of its children, so the closure splits into
+// independent column groups: each CTA owns WPB words for ALL classes, walks
+// the peel levels in order with only __syncthreads() between levels (no grid
+// or host synchronisation), then sweeps the untrimmed (cyclic) remainder to a
+// fixpoint.  Columns live in shared memory when they fit, else in HBM.
+__global__ void __launch_bounds__(512) k_close_cols(const u32* order, const u32* lvl_off, u32 nl, const u32* eoff,
+                                                    const u32* edst, const u32* rest, u32 nrest, u32 n, u32 words,
+                                                    int wpb, int in_smem, u32* bitsT) {
+  extern __shared__ u32 smem_col[];
+  __shared__ u32 s_changed;
+  const u32 w0 = blockIdx.x * (u32)wpb;
+  const int nk = (int)min((u32)wpb, words - w0);
+  u32* col = in_smem ? smem_col : bitsT + (u64)w0 * n;
+  if (in_smem)
+    for (u64 i = threadIdx.x; i < (u64)nk * n; i += blockDim.x) col[i] = 0;
+  __syncthreads();
+  for (u32 l = 1; l < nl; l++) {
+    u32 a = lvl_off[l], b = lvl_off[l + 1];
+    u64 items = (u64)(b - a) * nk;
+    for (u64 it = threadIdx.x; it < items; it += blockDim.x) {
+      u32 i = order[a + it / nk];
+      int k = (int)(it % nk);
+      u32 w = w0 + k;
+      const u32* ck = col + (u64)k * n;
+      u32 acc = 0;
+      for (u32 e = eoff[i], e1 = eoff[i + 1]; e < e1; e++) {
         u32 j = edst[e];
-        acc |= bits[(u64)j * words + w];
+        acc |= ck[j];
         if ((j >> 5) == w) acc |= 1u << (j & 31);
       }
-      if (acc != row[w]) {
-        row[w] = acc;
-        ch = true;
-      }
+      col[(u64)k * n + i] = acc;
     }
-    if (__any_sync(0xffffffffu, ch) && lane == 0) *changed = 1;
+    __syncthreads();
   }
+  if (nrest) {
+    while (true) {
+      if (threadIdx.x == 0) s_changed = 0;
+      __syncthreads();
+      for (u64 it = threadIdx.x; it < (u64)nrest * nk; it += blockDim.x) {
+        u32 i = rest[it / nk];
+        int k = (int)(it % nk);
+        u32 w = w0 + k;
+        u32* ck = col + (u64)k * n;
+        u32 acc = ck[i], old = acc;
+        for (u32 e = eoff[i], e1 = eoff[i + 1]; e < e1; e++) {
+          u32 j = edst[e];
+          acc |= ck[j];
+          if ((j >> 5) == w) acc |= 1u << (j & 31);
+        }
+        if (acc != old) {
+          atomicOr(&ck[i], acc);
+          s_changed = 1;
+        }
+      }
+      __syncthreads();
+      u32 ch = s_changed;
+      __syncthreads();
+      if (!ch) break;
+    }
+  }
+  if (in_smem)
+    for (u64 i = threadIdx.x; i < (u64)nk * n; i += blockDim.x) bitsT[(u64)w0 * n + i] = col[i];
 }
 
 __global__ void k_untrimmed(const u32* level, u32 n, const u8* mask, u32* list, u32* cnt) {
@@ -140,7 +180,6 @@ void build_class_graph(Engine& e) {
 
 u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrimmed);
 u32 bfs_classes(Engine& e, u32 root, u32* mark, u32* queue);
-void close_levels(Engine& e, const std::vector<u32>& lo, u32 nl, u32* bits, u32 words);
 
 void Engine::ensure_levels() {
   if (!snap.valid) build_snapshot();
@@ -160,31 +199,39 @@ void Engine::build_reach() {
   u64 bytes = (u64)n * words * 4;
   if (bytes > (u64)48 << 30) throw TsatException(TSAT_ERR_UNSUPPORTED, "descendants bitset would exceed 48 GiB");
   reach.bits.ensure((u64)n * words + 1);
-  CUDA_OK(cudaMemsetAsync(reach.bits.p, 0, bytes, s));
   u32 nl = lv_n, ntr = lv_trimmed;
-  if (nl > 1) close_levels(*this, lv_off, nl, reach.bits.p, words);
-  if (ntr < n) {
-    DevBuf<u32>& rest = sc.c_rest;
-    rest.ensure(n - ntr + 1);
+  DevBuf<u32>& rest = sc.c_rest;
+  u32 nr = n - ntr;
+  if (nr) {
+    rest.ensure(nr + 1);
     DevBuf<u32>& c2 = sc.c_res;
-    CUDA_OK(cudaMemsetAsync(c2.p, 0, 2 * sizeof(u32), s));
+    CUDA_OK(cudaMemsetAsync(c2.p, 0, sizeof(u32), s));
     k_untrimmed<<<nblk(n), 256, 0, s>>>(sc.cg_level.p, n, nullptr, rest.p, c2.p);
-    u32 nr = n - ntr;
-    while (true) {
-      CUDA_OK(cudaMemsetAsync(c2.p + 1, 0, sizeof(u32), s));
-      k_close_sweep<<<nblk((u64)nr * 32, 256), 256, 0, s>>>(rest.p, nr, sc.cg_eoff.p, sc.cg_edst.p, reach.bits.p,
-                                                            words, c2.p + 1);
-      u32 ch;
-      CUDA_OK(cudaMemcpyAsync(&ch, c2.p + 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
-      sync();
-      if (!ch) break;
+  }
+  if (n) {
+    // words per CTA: as many columns as fit in shared memory, but enough CTAs
+    // to cover the SMs
+    const u64 SMEM = 200u << 10;
+    static int smem_set = 0;
+    if (!smem_set) {
+      CUDA_OK(cudaFuncSetAttribute(k_close_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+      smem_set = 1;
     }
+    u64 fit = SMEM / (4ull * n);
+    int in_smem = fit >= 1;
+    u64 wpb = std::max<u64>(1, std::min<u64>(in_smem ? fit : 1, (words + 147) / 148));
+    if (!in_smem) CUDA_OK(cudaMemsetAsync(reach.bits.p, 0, bytes, s));
+    u32 grid = (u32)((words + wpb - 1) / wpb);
+    size_t sm = in_smem ? (size_t)wpb * n * 4 : 0;
+    k_close_cols<<<grid, 512, sm, s>>>(sc.c_order.p, sc.c_lvloff.p, nl, sc.cg_eoff.p, sc.cg_edst.p, rest.p, nr, n,
+                                        words, (int)wpb, in_smem, reach.bits.p);
+    CUDA_OK(cudaGetLastError());
   }
   reach.n = n;
   reach.words = words;
   reach.valid = true;
   kt.bytes = 4.0 * words * ((double)n + (double)cg_ne);
-  kt.launches = 6;
+  kt.launches = 2;
   sync();
 }
 

@@ -128,7 +128,8 @@ struct Snapshot {
   DevBuf<u32> cls_nodes;  // members (alive nodes), ascending per class
   DevBuf<u32> cls_of;     // dense class of each member position
   DevBuf<u32> op_off;     // atom -> range in op_nodes
-  DevBuf<u32> op_nodes;
+  DevBuf<u32> op_nodes;   // alive nodes in (op, class, id) order
+  std::vector<u32> op_off_h;  // host copy of op_off
   bool valid = false;
 };
 
@@ -173,6 +174,7 @@ struct KTimer {  // records CUDA events on the engine stream around a kernel gro
 struct Scratch {
   // e-matching
   DevBuf<u32> m_rc, m_rb, m_cnt, m_perm, m_perm2, m_key, m_key2, m_fl, m_pos;
+  DevBuf<u32> m_bnd, m_big, m_head, m_bpos, m_L, m_bh, m_gex, m_bperm, m_bperm2, m_bkey, m_bkey2;
   // class graph / cycles / reach
   DevBuf<u32> cg_eoff, cg_edst, cg_enode, cg_roff, cg_rsrc, cg_outdeg, cg_level, cg_esrc, cg_sdst, cg_moff, cg_mdeg;
   DevBuf<u32> c_heavy, c_mark32, c_fa, c_fb, c_order, c_depth, c_path, c_cycn, c_cyco, c_res, c_rest, c_lvloff;
@@ -252,7 +254,7 @@ struct Engine {
   std::vector<RuleStatsH> rstats;
   std::vector<i64> enodes_per_iter, alloc_per_iter, eclasses_per_iter;
   ExploreReportC report{};
-  std::vector<double> phase_ms = std::vector<double>(16, 0.0);
+  std::vector<double> phase_ms = std::vector<double>(32, 0.0);
   unsigned long long nlaunch = 0;  // kernels of ours launched (not CUB)
   KStat kstat[KG_COUNT];
   cudaEvent_t ev_pool[2] = {nullptr, nullptr};
@@ -294,7 +296,7 @@ struct Engine {
 
   // snapshot + matching
   void build_snapshot();
-  void ematch_pattern(int pid, MatchSet& out);
+  void ematch_batch(const std::vector<int>& pids);
   void load_rules(int n, const i64* blob);
 
   // cycles

@@ -148,6 +148,7 @@ ReachDev make_reach_dev(Engine& e) {
   ReachDev r;
   r.bits = e.reach.bits.p;
   r.words = e.reach.words;
+  r.n = e.reach.n;
   r.cls_index = e.snap.cls_index.p;
   r.n_alloc = e.snap.n_alloc;
   r.valid = e.reach.valid ? 1 : 0;
@@ -342,7 +343,7 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
   std::vector<int> multi, single;
   for (size_t i = 0; i < rules.size(); i++) (rules[i].nsrc > 1 ? multi : single).push_back((int)i);
   int stop = 0;  // iter-limit
-  for (int q = 0; q < 16; q++) phase_ms[q] = 0.0;
+  for (int q = 0; q < 32; q++) phase_ms[q] = 0.0;
   auto tick = [&](int ph, double& t) {
     sync();
     double n2 = now_s();
@@ -362,8 +363,10 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
     std::vector<char> need(patterns.size(), 0);
     for (int ri : active)
       for (int t = 0; t < rules[ri].nsrc; t++) need[rules[ri].src_pat[t]] = 1;
+    std::vector<int> todo;
     for (size_t p = 0; p < patterns.size(); p++)
-      if (need[p]) ematch_pattern((int)p, matches[p]);
+      if (need[p]) todo.push_back((int)p);
+    ematch_batch(todo);
     tick(2, tp);
     seq_changed = false;
     seq_stop = false;

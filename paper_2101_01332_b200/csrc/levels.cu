@@ -284,60 +284,3 @@ u32 bfs_classes(Engine& e, u32 root, u32* mark, u32* queue) {
   return bfs_graph(e, e.sc.cg_eoff.p, e.sc.cg_edst.p, e.cg_n, root, mark, queue);
 }
 
-// ---------------------------------------------------------------- level-ordered passes
-
-// descendants closure over levels [l0, l1) inside one CTA
-__global__ void __launch_bounds__(LV_BLOCK) k_close_block(const u32* order, const u32* lvl_off, u32 l0, u32 l1,
-                                                          const u32* eoff, const u32* edst, u32* bits, u32 words) {
-  for (u32 l = l0; l < l1; l++) {
-    u32 a = lvl_off[l], b = lvl_off[l + 1];
-    u64 items = (u64)(b - a) * words;
-    for (u64 it = threadIdx.x; it < items; it += blockDim.x) {
-      u32 i = order[a + it / words];
-      u32 w = (u32)(it % words);
-      u32 acc = 0;
-      for (u32 e = eoff[i]; e < eoff[i + 1]; e++) {
-        u32 j = edst[e];
-        acc |= bits[(u64)j * words + w];
-        if ((j >> 5) == w) acc |= 1u << (j & 31);
-      }
-      bits[(u64)i * words + w] = acc;
-    }
-    __syncthreads();
-  }
-}
-
-// one wide level on the whole GPU
-__global__ void k_close_level(const u32* order, u32 a, u32 b, const u32* eoff, const u32* edst, u32* bits,
-                              u32 words) {
-  GRID_STRIDE(it, (u64)(b - a) * words) {
-    u32 i = order[a + it / words];
-    u32 w = (u32)(it % words);
-    u32 acc = 0;
-    for (u32 e = eoff[i]; e < eoff[i + 1]; e++) {
-      u32 j = edst[e];
-      acc |= bits[(u64)j * words + w];
-      if ((j >> 5) == w) acc |= 1u << (j & 31);
-    }
-    bits[(u64)i * words + w] = acc;
-  }
-}
-
-// run a level-ordered pass: consecutive thin levels batched into one CTA launch
-void close_levels(Engine& e, const std::vector<u32>& lo, u32 nl, u32* bits, u32 words) {
-  Scratch& X = e.sc;
-  u32 l = 1;  // level 0 rows stay empty
-  while (l < nl) {
-    u32 w = lo[l + 1] - lo[l];
-    if ((u64)w * words > (u64)LV_WIDE * 8) {
-      k_close_level<<<nblk((u64)w * words), 256, 0, e.s>>>(X.c_order.p, lo[l], lo[l + 1], X.cg_eoff.p, X.cg_edst.p,
-                                                           bits, words);
-      l++;
-      continue;
-    }
-    u32 l1 = l;
-    while (l1 < nl && (u64)(lo[l1 + 1] - lo[l1]) * words <= (u64)LV_WIDE * 8) l1++;
-    k_close_block<<<1, LV_BLOCK, 0, e.s>>>(X.c_order.p, X.c_lvloff.p, l, l1, X.cg_eoff.p, X.cg_edst.p, bits, words);
-    l = l1;
-  }
-}

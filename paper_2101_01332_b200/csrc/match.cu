@@ -1,12 +1,23 @@
 // E-matching on the GPU (reference: pkg/src/tensorsat/egraph.py:248-293).
 //
-// One thread per root candidate: candidates come from the per-operator CSR
-// (snapshot.op_nodes), i.e. a relational scan of the root operator's table;
-// nested pattern nodes are joined through the class CSR (class -> members,
-// ascending ids) with filter-list, op and arity checks and nonlinear-variable
-// equality.  Results are deduplicated and ordered by (eclass, bindings in
-// variable-name order) with a stable LSD radix sort over the tuple words,
-// reproducing _match_sorted (egraph.py:107-112).
+// All unique canonical patterns of an iteration are matched in ONE batch.
+// The root candidates of every pattern form one flat list: pattern p scans
+// the per-operator table of its root atom (snapshot.op_nodes, stored in
+// (op, class, id) order).  Nested pattern nodes are joined through the class
+// CSR (class -> members, ascending ids) with filter-list, op and arity checks
+// and nonlinear-variable equality.
+//
+//   count   one thread per candidate: number of matches (DFS over the join)
+//   scan    per-candidate output offsets (one pass for the whole batch)
+//   emit    the same DFS writes rows (eclass, bindings in var-name order) at
+//           the candidate's offset -- rows come out grouped by eclass, with
+//           eclasses ascending, because candidates are class-ordered
+//   rank    rows of one eclass are ordered by bindings and deduplicated
+//           (_match_sorted, egraph.py:107-112): small groups (<= 32 rows,
+//           the common case) by a per-row rank, larger groups by one CTA each
+//   compact keep first-of-equal rows, write each pattern's MatchSet
+//
+// Two host synchronisations per batch (row counts, unique counts).
 #include <cub/cub.cuh>
 
 #include "engine.cuh"
@@ -30,8 +41,33 @@ struct SnapDev {
   const u32* cls_index;
   const u32* cls_off;
   const u32* cls_nodes;
+  const u32* op_nodes;
   u32 n_alloc;
 };
+
+#define MAX_BATCH 24
+#define SMALL_GROUP 32u
+
+struct Batch {
+  int npat;
+  int stride;                 // words per binding row (max nb of the batch, >= 1)
+  PatDev pat[MAX_BATCH];
+  u32 cbase[MAX_BATCH + 1];   // flat candidate ranges
+  u32 obase[MAX_BATCH];       // op_nodes offset of each pattern's root atom
+  u32 rbase[MAX_BATCH + 1];   // raw row ranges (after the count scan)
+  u32* out_cls[MAX_BATCH];
+  u32* out_bind[MAX_BATCH];
+};
+
+__device__ __forceinline__ int seg_of(const u32* base, int n, u32 t) {
+  int lo = 0, hi = n;  // largest p with base[p] <= t
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (base[mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
 
 __device__ __forceinline__ bool node_ok(const G& g, u32 nid, const PatApp& a) {
   if (g.flags[nid] & NF_FILT) return false;
@@ -69,175 +105,317 @@ __device__ __forceinline__ void unbind(int t, u32* env, int8_t* bound_at) {
     }
 }
 
-__global__ void k_ematch(G g, SnapDev sd, PatDev p, const u32* cand, u32 ncand, u32* out_cls,
-                         u32* out_bind, u32* count, u32 cap) {
-  GRID_STRIDE(ci, ncand) {
-    u32 r = cand[ci];
-    if (!node_ok(g, r, p.apps[0])) continue;
-    u32 env[MAX_VARS];
-    int8_t bound_at[MAX_VARS];
-    u32 cls_app[MAX_PAT_APPS];
-    u32 pos[MAX_PAT_APPS], end[MAX_PAT_APPS];
-    for (int v = 0; v < MAX_VARS; v++) {
-      env[v] = TSAT_NONE;
-      bound_at[v] = -1;
-    }
-    if (!bind_node(g, p.apps[0], r, 0, env, bound_at, cls_app)) continue;
-    u32 rc = uf_find_ro(g.parent, r);
-    int level = 1;
-    bool init = true;
-    while (true) {
-      if (level == p.napps) {
-        u32 slot = atomicAdd(count, 1u);
-        if (slot < cap) {
-          out_cls[slot] = rc;
-          for (int k = 0; k < p.nb; k++) out_bind[(u64)slot * p.nb + k] = env[p.order[k]];
-        }
-        level--;
-        if (level == 0) break;
-        unbind(level, env, bound_at);
-        init = false;
-        continue;
-      }
-      if (init) {
-        u32 c = cls_app[level];
-        u32 d = c < sd.n_alloc ? sd.cls_index[c] : TSAT_NONE;
-        if (d == TSAT_NONE) {
-          pos[level] = end[level] = 0;
-        } else {
-          pos[level] = sd.cls_off[d];
-          end[level] = sd.cls_off[d + 1];
-        }
-      }
-      bool found = false;
-      const PatApp& a = p.apps[level];
-      while (pos[level] < end[level]) {
-        u32 m = sd.cls_nodes[pos[level]++];
-        if (!node_ok(g, m, a)) continue;
-        if (bind_node(g, a, m, level, env, bound_at, cls_app)) {
-          found = true;
-          break;
-        }
-        unbind(level, env, bound_at);
-      }
-      if (found) {
-        level++;
-        init = true;
-      } else {
-        level--;
-        if (level == 0) break;
-        unbind(level, env, bound_at);
-        init = false;
-      }
-    }
+// DFS over the pattern's join for root node r; emit(k, rc, env) per match.
+template <class F>
+__device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const PatDev& p, u32 r, F emit) {
+  if (!node_ok(g, r, p.apps[0])) return 0;
+  u32 env[MAX_VARS];
+  int8_t bound_at[MAX_VARS];
+  u32 cls_app[MAX_PAT_APPS];
+  u32 pos[MAX_PAT_APPS], end[MAX_PAT_APPS];
+  for (int v = 0; v < MAX_VARS; v++) {
+    env[v] = TSAT_NONE;
+    bound_at[v] = -1;
   }
-}
-
-__global__ void k_iota(u32* p, u32 n) { GRID_STRIDE(i, n) p[i] = (u32)i; }
-
-__global__ void k_gather_word(const u32* cls, const u32* bind, int nb, int w, const u32* perm, u32 n,
-                              u32* out) {
-  GRID_STRIDE(i, n) {
-    u32 r = perm[i];
-    out[i] = w == 0 ? cls[r] : bind[(u64)r * nb + (w - 1)];
-  }
-}
-
-__global__ void k_unique_flags(const u32* cls, const u32* bind, int nb, const u32* perm, u32 n, u32* fl) {
-  GRID_STRIDE(i, n) {
-    if (i == 0) {
-      fl[i] = 1;
+  if (!bind_node(g, p.apps[0], r, 0, env, bound_at, cls_app)) return 0;
+  u32 rc = uf_find_ro(g.parent, r);
+  u32 count = 0;
+  int level = 1;
+  bool init = true;
+  while (true) {
+    if (level == p.napps) {
+      emit(count, rc, env);
+      count++;
+      level--;
+      if (level == 0) break;
+      unbind(level, env, bound_at);
+      init = false;
       continue;
     }
-    u32 a = perm[i], b = perm[i - 1];
-    bool same = cls[a] == cls[b];
-    for (int k = 0; k < nb && same; k++) same = bind[(u64)a * nb + k] == bind[(u64)b * nb + k];
-    fl[i] = same ? 0u : 1u;
+    if (init) {
+      u32 c = cls_app[level];
+      u32 d = c < sd.n_alloc ? sd.cls_index[c] : TSAT_NONE;
+      if (d == TSAT_NONE) {
+        pos[level] = end[level] = 0;
+      } else {
+        pos[level] = sd.cls_off[d];
+        end[level] = sd.cls_off[d + 1];
+      }
+    }
+    bool found = false;
+    const PatApp& a = p.apps[level];
+    while (pos[level] < end[level]) {
+      u32 m = sd.cls_nodes[pos[level]++];
+      if (!node_ok(g, m, a)) continue;
+      if (bind_node(g, a, m, level, env, bound_at, cls_app)) {
+        found = true;
+        break;
+      }
+      unbind(level, env, bound_at);
+    }
+    if (found) {
+      level++;
+      init = true;
+    } else {
+      level--;
+      if (level == 0) break;
+      unbind(level, env, bound_at);
+      init = false;
+    }
+  }
+  return count;
+}
+
+__global__ void k_em_count(G g, SnapDev sd, Batch B, u32 ntot, u32* cnt) {
+  GRID_STRIDE(t, ntot) {
+    int p = seg_of(B.cbase, B.npat, (u32)t);
+    u32 r = sd.op_nodes[B.obase[p] + ((u32)t - B.cbase[p])];
+    cnt[t] = match_root(g, sd, B.pat[p], r, [](u32, u32, const u32*) {});
   }
 }
 
-__global__ void k_unique_write(const u32* cls, const u32* bind, int nb, const u32* perm, const u32* fl,
-                               const u32* pos, u32 n, u32* ocls, u32* obind) {
-  GRID_STRIDE(i, n) {
-    if (!fl[i]) continue;
-    u32 r = perm[i], o = pos[i];
-    ocls[o] = cls[r];
-    for (int k = 0; k < nb; k++) obind[(u64)o * nb + k] = bind[(u64)r * nb + k];
+__global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u32* rc, u32* rb) {
+  GRID_STRIDE(t, ntot) {
+    int p = seg_of(B.cbase, B.npat, (u32)t);
+    const PatDev& pd = B.pat[p];
+    u32 r = sd.op_nodes[B.obase[p] + ((u32)t - B.cbase[p])];
+    u32 o = off[t];
+    const int S = B.stride;
+    match_root(g, sd, pd, r, [&](u32 k, u32 cls, const u32* env) {
+      rc[o + k] = cls;
+      for (int j = 0; j < S; j++) rb[(u64)(o + k) * S + j] = j < pd.nb ? env[pd.order[j]] : 0u;
+    });
   }
 }
 
-void Engine::ematch_pattern(int pid, MatchSet& out) {
+__global__ void k_em_bounds(const u32* off, Batch B, u32* out) {
+  int p = threadIdx.x;
+  if (p <= B.npat) out[p] = off[B.cbase[p]];
+}
+
+// row a < row b within one eclass group: bindings lexicographic, ties by index
+__device__ __forceinline__ int row_cmp(const u32* rb, int S, int nb, u32 a, u32 b) {
+  for (int j = 0; j < nb; j++) {
+    u32 x = rb[(u64)a * S + j], y = rb[(u64)b * S + j];
+    if (x != y) return x < y ? -1 : 1;
+  }
+  return 0;
+}
+
+__device__ __forceinline__ void put_row(const u32* rc, const u32* rb, int S, int nb, u32 src, u32 dst, u32* sc,
+                                        u32* sb) {
+  sc[dst] = rc[src];
+  for (int j = 0; j < nb; j++) sb[(u64)dst * S + j] = rb[(u64)src * S + j];
+}
+
+// small groups: per-row rank + scatter; rows of larger groups are flagged
+// (big[k] = 1, head[k] = first row of its group) for the radix path
+__global__ void k_em_rank(Batch B, u32 nrows, const u32* rc, const u32* rb, u32* sc, u32* sb, u32* big,
+                          u32* head) {
+  GRID_STRIDE(k0, nrows) {
+    u32 k = (u32)k0;
+    int p = seg_of(B.rbase, B.npat, k);
+    u32 lo = B.rbase[p], hi = B.rbase[p + 1];
+    u32 c = rc[k];
+    u32 gs = k, ge = k + 1;
+    while (gs > lo && rc[gs - 1] == c && k - gs < SMALL_GROUP) gs--;
+    while (ge < hi && rc[ge] == c && ge - k <= SMALL_GROUP) ge++;
+    bool is_big = ge - gs > SMALL_GROUP || (gs > lo && rc[gs - 1] == c);
+    big[k] = is_big ? 1u : 0u;
+    head[k] = (k == lo || rc[k - 1] != c) ? 1u : 0u;
+    if (is_big) continue;
+    const int nb = B.pat[p].nb, S = B.stride;
+    u32 rank = 0;
+    for (u32 j = gs; j < ge; j++) {
+      if (j == k) continue;
+      int cmp = row_cmp(rb, S, nb, j, k);
+      if (cmp < 0 || (cmp == 0 && j < k)) rank++;
+    }
+    put_row(rc, rb, S, nb, k, gs + rank, sc, sb);
+  }
+}
+
+// big rows, ascending: L[i] = row, bh[i] = group head flag, perm = identity
+__global__ void k_em_big_list(u32 nrows, const u32* big, const u32* bpos, const u32* head, u32* L, u32* bh,
+                              u32* perm) {
+  GRID_STRIDE(k, nrows) {
+    if (!big[k]) continue;
+    u32 i = bpos[k];
+    L[i] = (u32)k;
+    bh[i] = head[k];
+    perm[i] = i;
+  }
+}
+
+// radix key of pass w (binding word w, or the group index when w < 0)
+__global__ void k_em_big_key(u32 nbig, const u32* L, const u32* perm, const u32* rb, int S, int w, const u32* bh,
+                             const u32* gex, u32* key) {
+  GRID_STRIDE(i, nbig) {
+    u32 q = perm[i];
+    key[i] = w >= 0 ? rb[(u64)L[q] * S + w] : gex[q] + bh[q] - 1;
+  }
+}
+
+// sorted big rows go to the big-row slots in ascending order (groups keep
+// their positions and sizes)
+__global__ void k_em_big_scatter(u32 nbig, const u32* L, const u32* perm, const u32* rc, const u32* rb, int S,
+                                 u32* sc, u32* sb) {
+  GRID_STRIDE(i, nbig) put_row(rc, rb, S, S, L[perm[i]], L[i], sc, sb);
+}
+
+__global__ void k_em_keep(Batch B, u32 nrows, const u32* sc, const u32* sb, u32* keep) {
+  GRID_STRIDE(k0, nrows) {
+    u32 k = (u32)k0;
+    int p = seg_of(B.rbase, B.npat, k);
+    bool kp = k == B.rbase[p] || sc[k] != sc[k - 1] || row_cmp(sb, B.stride, B.pat[p].nb, k - 1, k) != 0;
+    keep[k] = kp ? 1u : 0u;
+  }
+}
+
+__global__ void k_em_compact(Batch B, u32 nrows, const u32* sc, const u32* sb, const u32* keep, const u32* upos) {
+  GRID_STRIDE(k0, nrows) {
+    u32 k = (u32)k0;
+    if (!keep[k]) continue;
+    int p = seg_of(B.rbase, B.npat, k);
+    u32 d = upos[k] - upos[B.rbase[p]];
+    const int nb = B.pat[p].nb;
+    B.out_cls[p][d] = sc[k];
+    for (int j = 0; j < nb; j++) B.out_bind[p][(u64)d * nb + j] = sb[(u64)k * B.stride + j];
+  }
+}
+
+__global__ void k_em_ubounds(const u32* upos, Batch B, u32* out) {
+  int p = threadIdx.x;
+  if (p <= B.npat) out[p] = upos[B.rbase[p]];
+}
+
+void Engine::ematch_batch(const std::vector<int>& pids_all) {
   if (!snap.valid || snap.n_atoms != h_atoms.size()) build_snapshot();
-  const HPattern& hp = patterns[pid];
-  PatDev p;
-  memset(&p, 0, sizeof(p));
-  p.napps = (int)hp.apps.size();
-  p.nb = hp.nvars;
-  for (int i = 0; i < p.napps; i++) p.apps[i] = hp.apps[i];
-  for (int k = 0; k < hp.nvars; k++) p.order[k] = hp.order[k];
-  SnapDev sd{snap.cls_index.p, snap.cls_off.p, snap.cls_nodes.p, snap.n_alloc};
-  u32 ra = p.apps[0].atom;
-  out.nb = p.nb;
-  out.n = 0;
-  if (ra >= h_atoms.size()) return;
-  u32 range[2];
-  CUDA_OK(cudaMemcpyAsync(range, snap.op_off.p + ra, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
-  sync();
-  u32 ncand = range[1] - range[0];
-  if (ncand == 0) return;
-  // whole e-match (root scan + ordering + dedup) timed as one group; bytes per
-  // candidates + match rows + a (1+v)-word sort of the matches
-  KTimer kt_all(*this, KG_EMATCH, 0.0, 0);
-  DevBuf<u32>& rc = sc.m_rc;
-  DevBuf<u32>& rb = sc.m_rb;
-  DevBuf<u32>& cntb = sc.m_cnt;
-  cntb.ensure(1);
-  u32 cap = std::max<u32>(ncand * 2, 1024);
-  u32 m = 0;
-  for (int attempt = 0; attempt < 8; attempt++) {
-    rc.ensure(cap);
-    rb.ensure((u64)cap * std::max(p.nb, 1));
-    CUDA_OK(cudaMemsetAsync(cntb.p, 0, sizeof(u32), s));
-    k_ematch<<<nblk(ncand, 128), 128, 0, s>>>(view(), sd, p, snap.op_nodes.p + range[0], ncand, rc.p, rb.p, cntb.p,
-                                              cap);
-    CUDA_OK(cudaMemcpyAsync(&m, cntb.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  for (size_t c0 = 0; c0 < pids_all.size(); c0 += MAX_BATCH) {
+    std::vector<int> pids(pids_all.begin() + c0, pids_all.begin() + std::min(pids_all.size(), c0 + MAX_BATCH));
+    Batch B;
+    memset(&B, 0, sizeof(B));
+    std::vector<int> live;  // patterns with candidates
+    u32 ntot = 0;
+    int stride = 1;
+    double cand_bytes = 0;
+    for (int pid : pids) {
+      const HPattern& hp = patterns[pid];
+      MatchSet& ms = matches[pid];
+      ms.nb = hp.nvars;
+      ms.n = 0;
+      u32 ra = hp.apps[0].atom;
+      if (ra + 1 >= snap.op_off_h.size()) continue;
+      u32 lo = snap.op_off_h[ra], hi = snap.op_off_h[ra + 1];
+      if (hi == lo) continue;
+      int b = (int)live.size();
+      PatDev& p = B.pat[b];
+      p.napps = (int)hp.apps.size();
+      p.nb = hp.nvars;
+      for (int i = 0; i < p.napps; i++) p.apps[i] = hp.apps[i];
+      for (int k = 0; k < hp.nvars; k++) p.order[k] = hp.order[k];
+      B.cbase[b] = ntot;
+      B.obase[b] = lo;
+      ntot += hi - lo;
+      stride = std::max(stride, hp.nvars);
+      cand_bytes += (double)(hi - lo) * (17.0 + 8.0 * hp.apps[0].nargs);
+      live.push_back(pid);
+    }
+    if (live.empty()) continue;
+    int np = (int)live.size();
+    B.npat = np;
+    B.cbase[np] = ntot;
+    B.stride = stride;
+    KTimer kt(*this, KG_EMATCH, 0.0, 0);
+    SnapDev sd{snap.cls_index.p, snap.cls_off.p, snap.cls_nodes.p, snap.op_nodes.p, snap.n_alloc};
+    DevBuf<u32>& cnt = sc.m_cnt;
+    DevBuf<u32>& off = sc.m_pos;
+    DevBuf<u32>& bnd = sc.m_bnd;
+    cnt.ensure(ntot + 1);
+    off.ensure(ntot + 1);
+    bnd.ensure(2 * (MAX_BATCH + 1));
+    k_em_count<<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p);
+    CUDA_OK(cudaMemsetAsync(cnt.p + ntot, 0, sizeof(u32), s));
+    dev_exclusive_scan_u32(*this, cnt.p, off.p, ntot + 1);
+    k_em_bounds<<<1, 32, 0, s>>>(off.p, B, bnd.p);
+    CUDA_OK(cudaMemcpyAsync(B.rbase, bnd.p, (np + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
-    if (m <= cap) break;
-    cap = m + 1024;
+    u32 nrows = B.rbase[np];
+    for (int b = 0; b < np; b++) {
+      MatchSet& ms = matches[live[b]];
+      u32 raw = B.rbase[b + 1] - B.rbase[b];
+      ms.cls.ensure(raw + 1);
+      ms.bind.ensure((u64)(raw + 1) * std::max(ms.nb, 1));
+      B.out_cls[b] = ms.cls.p;
+      B.out_bind[b] = ms.bind.p;
+    }
+    u32 nuniq[MAX_BATCH + 1] = {0};
+    if (nrows) {
+      DevBuf<u32>& rc = sc.m_rc;
+      DevBuf<u32>& rb = sc.m_rb;
+      DevBuf<u32>& scl = sc.m_key;
+      DevBuf<u32>& sbd = sc.m_perm;
+      DevBuf<u32>& keep = sc.m_fl;
+      DevBuf<u32>& upos = sc.m_perm2;
+      rc.ensure(nrows);
+      rb.ensure((u64)nrows * stride);
+      scl.ensure(nrows);
+      sbd.ensure((u64)nrows * stride);
+      keep.ensure(nrows + 1);
+      upos.ensure(nrows + 1);
+      DevBuf<u32>& big = sc.m_big;
+      DevBuf<u32>& head = sc.m_head;
+      DevBuf<u32>& bpos = sc.m_bpos;
+      bpos.ensure(nrows + 1);
+      big.ensure(nrows + 1);
+      head.ensure(nrows + 1);
+      k_em_emit<<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p);
+      k_em_rank<<<nblk(nrows), 256, 0, s>>>(B, nrows, rc.p, rb.p, scl.p, sbd.p, big.p, head.p);
+      // large groups: stable LSD radix sort of their rows by (group, bindings)
+      CUDA_OK(cudaMemsetAsync(big.p + nrows, 0, sizeof(u32), s));
+      dev_exclusive_scan_u32(*this, big.p, bpos.p, nrows + 1);
+      u32 nbigrows = 0;
+      CUDA_OK(cudaMemcpyAsync(&nbigrows, bpos.p + nrows, sizeof(u32), cudaMemcpyDeviceToHost, s));
+      sync();
+      if (nbigrows) {
+        DevBuf<u32>& L = sc.m_L;
+        DevBuf<u32>& bh = sc.m_bh;
+        DevBuf<u32>& gex = sc.m_gex;
+        DevBuf<u32>& perm = sc.m_bperm;
+        DevBuf<u32>& perm2 = sc.m_bperm2;
+        DevBuf<u32>& key = sc.m_bkey;
+        DevBuf<u32>& key2 = sc.m_bkey2;
+        L.ensure(nbigrows + 1);
+        bh.ensure(nbigrows + 1);
+        gex.ensure(nbigrows + 1);
+        perm.ensure(nbigrows + 1);
+        perm2.ensure(nbigrows + 1);
+        key.ensure(nbigrows + 1);
+        key2.ensure(nbigrows + 1);
+        k_em_big_list<<<nblk(nrows), 256, 0, s>>>(nrows, big.p, bpos.p, head.p, L.p, bh.p, perm.p);
+        dev_exclusive_scan_u32(*this, bh.p, gex.p, nbigrows);
+        int eb = (int)bits_for(h.next_id);
+        for (int w = stride - 1; w >= -1; w--) {
+          k_em_big_key<<<nblk(nbigrows), 256, 0, s>>>(nbigrows, L.p, perm.p, rb.p, stride, w, bh.p, gex.p, key.p);
+          dev_sort_pairs_u32(*this, key.p, key2.p, perm.p, perm2.p, nbigrows, w >= 0 ? eb : (int)bits_for(nbigrows));
+          perm.swap(perm2);
+        }
+        k_em_big_scatter<<<nblk(nbigrows), 256, 0, s>>>(nbigrows, L.p, perm.p, rc.p, rb.p, stride, scl.p, sbd.p);
+      }
+      k_em_keep<<<nblk(nrows), 256, 0, s>>>(B, nrows, scl.p, sbd.p, keep.p);
+      CUDA_OK(cudaMemsetAsync(keep.p + nrows, 0, sizeof(u32), s));
+      dev_exclusive_scan_u32(*this, keep.p, upos.p, nrows + 1);
+      k_em_compact<<<nblk(nrows), 256, 0, s>>>(B, nrows, scl.p, sbd.p, keep.p, upos.p);
+      k_em_ubounds<<<1, 32, 0, s>>>(upos.p, B, bnd.p);
+      CUDA_OK(cudaMemcpyAsync(nuniq, bnd.p, (np + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      sync();
+    }
+    for (int b = 0; b < np; b++) matches[live[b]].n = nuniq[b + 1] - nuniq[b];
+    // algorithmic bytes: candidate scan + match rows written,
+    // ordered and compacted
+    double rows_bytes = 0;
+    for (int b = 0; b < np; b++) rows_bytes += (double)(B.rbase[b + 1] - B.rbase[b]) * 4.0 * (1 + B.pat[b].nb);
+    kt.bytes = cand_bytes + 2.0 * rows_bytes;
+    kt.launches = 9;
   }
-  kt_all.bytes = (double)ncand * (17.0 + 8.0 * p.apps[0].nargs) + (double)m * 4.0 * (1 + p.nb) * 2.0;
-  kt_all.launches = 1;
-  if (m == 0) return;
-  // stable LSD sort over words (cls, b0..b_{nb-1}), last word first
-  DevBuf<u32>& perm = sc.m_perm;
-  DevBuf<u32>& perm2 = sc.m_perm2;
-  DevBuf<u32>& key = sc.m_key;
-  DevBuf<u32>& key2 = sc.m_key2;
-  perm.ensure(m);
-  perm2.ensure(m);
-  key.ensure(m);
-  key2.ensure(m);
-  k_iota<<<nblk(m), 256, 0, s>>>(perm.p, m);
-  int eb = (int)bits_for(h.next_id);
-  for (int w = p.nb; w >= 0; w--) {
-    k_gather_word<<<nblk(m), 256, 0, s>>>(rc.p, rb.p, p.nb, w, perm.p, m, key.p);
-    dev_sort_pairs_u32(*this, key.p, key2.p, perm.p, perm2.p, m, eb);
-    perm.swap(perm2);
-  }
-  DevBuf<u32>& fl = sc.m_fl;
-  DevBuf<u32>& pos = sc.m_pos;
-  fl.ensure(m);
-  pos.ensure(m);
-  k_unique_flags<<<nblk(m), 256, 0, s>>>(rc.p, rb.p, p.nb, perm.p, m, fl.p);
-  dev_exclusive_scan_u32(*this, fl.p, pos.p, m);
-  u32 lf, lp;
-  CUDA_OK(cudaMemcpyAsync(&lf, fl.p + m - 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  CUDA_OK(cudaMemcpyAsync(&lp, pos.p + m - 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  sync();
-  u32 nu = lf + lp;
-  out.cls.ensure(nu);
-  out.bind.ensure((u64)nu * std::max(p.nb, 1));
-  k_unique_write<<<nblk(m), 256, 0, s>>>(rc.p, rb.p, p.nb, perm.p, fl.p, pos.p, m, out.cls.p, out.bind.p);
-  out.n = nu;
-  sync();
 }

@@ -16,8 +16,8 @@ struct RuleDev {
 };
 
 struct ReachDev {
-  const u32* bits;
-  u32 words;
+  const u32* bits;  // word-major: bits[w * n + i] = word w of class i's descendants
+  u32 words, n;
   const u32* cls_index;
   u32 n_alloc;
   int valid;
@@ -28,7 +28,7 @@ __device__ __forceinline__ bool reach_query(const ReachDev& r, u32 a, u32 b) {
   u32 ia = a < r.n_alloc ? r.cls_index[a] : TSAT_NONE;
   u32 ib = b < r.n_alloc ? r.cls_index[b] : TSAT_NONE;
   if (ia == TSAT_NONE || ib == TSAT_NONE) return false;
-  return (r.bits[(u64)ia * r.words + (ib >> 5)] >> (ib & 31)) & 1u;
+  return (r.bits[(u64)(ib >> 5) * r.n + ia] >> (ib & 31)) & 1u;
 }
 
 // decode product position -> per-source match indices (itertools.product order)

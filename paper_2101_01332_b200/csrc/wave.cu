@@ -833,6 +833,7 @@ struct CtaCtl {
   unsigned long long s_cand, s_req, s_win, s_nk;
   i64 overshoot;
   u32 seq_stop;
+  unsigned long long prof[12];  // ns per wave phase (thread 0's view)
 };
 
 struct CtaArgs {
@@ -856,12 +857,25 @@ __device__ __forceinline__ unsigned long long self_in(u32 nA, u32 nB, unsigned l
 
 #define CTA_T 512
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define WPROF(k)                          \
+  if (tid == 0) {                         \
+    unsigned long long t_ = gtimer();     \
+    ctl->prof[k] += t_ - t_last;          \
+    t_last = t_;                          \
+  }
+
 __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev RD, WaveRule W, WaveTab T, WaveIO io,
                                                        CtaArgs A, CtaCtl* ctl) {
   __shared__ unsigned long long s_p, s_seg_end;
   __shared__ u32 s_ncand, s_jcur, s_exit, s_epoch, s_nacc, s_ncacc, s_base, s_kbase;
   __shared__ int s_rejoin_after;
   const u64 tid = threadIdx.x, nth = CTA_T;
+  unsigned long long t_last = tid == 0 ? gtimer() : 0;
   if (tid == 0) {
     s_p = ctl->p;
     s_jcur = ctl->jcursor;
@@ -927,6 +941,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
       if (ex != 0xFFFFFFFFu) break;
     }
     const u32 ncand = s_ncand;
+    WPROF(11);
     const unsigned long long p = s_p;
     const unsigned long long* posp = A.multi ? A.pos + s_jcur : nullptr;
     WaveTab Tw = T;
@@ -934,6 +949,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     // ---- gates + accepted list
     d_gates(tid, nth, g, R, RD, posp, ncand, p, io.status, io.env, io.olds, io.hazard);
     __syncthreads();
+    WPROF(0);
     {
       u32 tot = block_scan<CTA_T>(ncand, io.pre,
                                   [&](u32 c) { return (io.status[c] == 0 || io.hazard[c]) ? 1u : 0u; });
@@ -942,6 +958,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
       if (tid == 0) s_nacc = tot;
       __syncthreads();
     }
+    WPROF(1);
     const u32 nacc = s_nacc;
     // ---- resolve requests level by level
     if (W.R > 0) {
@@ -954,18 +971,22 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
       d_mark_roots(tid, nth, W, Tw, io.acc, nacc, io.ident, io.hazard, io.olds);
       __syncthreads();
     }
+    WPROF(2);
     d_cand_check(tid, nth, g, W, Tw, io.acc, nacc, ncand, io.ident, io.env, io.olds, A.multi, io.hazard, io.alloc,
                  io.ukind, io.uother, io.grow, io.sa);
     __syncthreads();
+    WPROF(3);
     // ---- conflicts, stop-after, node-limit cutoff, boundary
     d_first_writer(tid, nth, W, Tw.epoch, io.acc, nacc, io.hazard, io.olds, io.ukind, io.uother, io.grow, io.fw_cls,
                    io.fw_fresh);
     __syncthreads();
+    WPROF(4);
     d_validity(tid, nth, W, Tw, R.nslots, R.nsrc, ncand, io.hazard, io.env, io.olds, io.pre, io.status, io.ident,
                io.fw_cls, io.fw_fresh, io.stops + 2);
     block_scan<CTA_T>(ncand, io.apre, [&](u32 c) { return io.alloc[c]; });
     d_find_stops(tid, nth, io.acc, nacc, io.sa, io.apre, io.alloc, (i64)g.cnt->live, A.n_max, io.stops);
     __syncthreads();
+    WPROF(5);
     if (tid == 0) {
       d_boundary(io.ws, io.stops, ncand, posp, p, s_seg_end, io.pre, io.hazard);
       s_ncacc = io.ws->ncommit_acc;
@@ -973,6 +994,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
       s_kbase = g.cnt->nkids;
     }
     __syncthreads();
+    WPROF(6);
     const u32 ncacc = s_ncacc;
     d_seg_stats(tid, nth, io.status, io.ws, io.ws->ncommit_cand, io.pre, io.alloc, io.ukind, R.efficient, io.wstats);
     // ---- commit (requests of committed combos only)
@@ -989,10 +1011,13 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
                     io.olds);
       __syncthreads();  // unions overwrite parent[] of fresh non-root nodes
     }
+    WPROF(7);
     d_commit_unions(tid, nth, g, W, Tw, io.acc, ncacc, io.olds, io.ukind, io.uother, io.grow);
     __syncthreads();
+    WPROF(8);
     for (u32 i = tid; i < nwin; i += CTA_T) hc_insert(g, s_base + i);
     __syncthreads();
+    WPROF(9);
     // ---- bookkeeping (thread 0)
     if (tid == 0) {
       WaveState* ws = io.ws;
@@ -1042,6 +1067,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
       s_exit = exitr;
     }
     __syncthreads();
+    WPROF(10);
     {
       u32 ex = s_exit;
       __syncthreads();
@@ -1366,6 +1392,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       rs.skipped_compat += c.compat;
       e.phase_ms[8] += c.waves;
       for (int k = 0; k < 6; k++) e.phase_ms[10 + k] += c.cuts[k];
+      for (int k = 0; k < 12; k++) e.phase_ms[16 + k] += c.prof[k] * 1e-6;
       p = c.p;
       jcursor = c.jcursor;
       win = c.win;
