@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Cost vector and greedy extraction on the GPU.
 //
 // * k_node_costs: c_i for every live e-node (reference cost.py:225-247 with
@@ -490,6 +491,84 @@ __global__ void __launch_bounds__(1024) k_greedy_levels(G g, const u32* cls_off,
   }
 }
 
+// Greedy over the peel levels of a small class graph in ONE CTA.
+// A prologue lays the trimmed classes' members out in peel order (q index):
+// node id, cost (NaN when filtered) and child classes (the class graph's
+// member edges, child order kept so the fp64 sums match the reference).
+// Per level: (A) one thread per member computes its total from the children's
+// best costs held in shared memory; (B) one thread per class folds its
+// members in id order with the reference rule (extract.py:145-152: a member
+// replaces the running best only when cheaper by more than 1e-15; with
+// ascending ids the tie clause never fires).
+__global__ void k_gq_count(const u32* order, u32 ntr, const u32* cls_off, u32* cnt) {
+  GRID_STRIDE(t, ntr) {
+    u32 i = order[t];
+    cnt[t] = cls_off[i + 1] - cls_off[i];
+  }
+}
+
+__global__ void k_gq_fill(G g, const u32* order, u32 ntr, const u32* cls_off, const u32* cls_nodes, const u32* moff,
+                          const u32* lvm_off, const double* cost, u32* qk, u32* qnode, double* qcost, u32* qdeg) {
+  GRID_STRIDE(t, ntr) {
+    u32 i = order[t];
+    u32 q = lvm_off[t];
+    for (u32 k = cls_off[i]; k < cls_off[i + 1]; k++, q++) {
+      u32 m = cls_nodes[k];
+      qk[q] = k;
+      qnode[q] = m;
+      bool f = (g.flags[m] & NF_FILT) != 0;
+      qcost[q] = f ? NAN : cost[m];
+      qdeg[q] = moff[k + 1] - moff[k];
+    }
+  }
+}
+
+__global__ void k_gq_edges(u32 nq, const u32* qk, const u32* moff, const u32* edst, const u32* qeoff, u32* qedst) {
+  GRID_STRIDE(q, nq) {
+    u32 k = qk[q], o = qeoff[q];
+    for (u32 e = moff[k]; e < moff[k + 1]; e++) qedst[o++] = edst[e];
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_greedy_cta(const u32* order, const u32* lvl_off, u32 nl, u32 ntr,
+                                                     const u32* lvm_off, const u32* qnode, const double* qcost,
+                                                     const u32* qeoff, const u32* qedst, double* qtot, double* bc_g,
+                                                     u32* bn) {
+  extern __shared__ double s_bc[];
+  for (u32 l = 0; l < nl; l++) {
+    u32 a = lvl_off[l], b = lvl_off[l + 1];
+    u32 qa = lvm_off[a], qb = lvm_off[b];
+    for (u32 q = qa + threadIdx.x; q < qb; q += blockDim.x) {
+      double tot = qcost[q];
+      if (!isnan(tot))
+        for (u32 e = qeoff[q], e1 = qeoff[q + 1]; e < e1; e++) tot += s_bc[qedst[e]];
+      qtot[q] = tot;
+    }
+    __syncthreads();
+    for (u32 t = a + threadIdx.x; t < b; t += blockDim.x) {
+      u32 q0 = lvm_off[t], q1 = lvm_off[t + 1];
+      double c = INFINITY;
+      u32 best = TSAT_NONE;
+      for (u32 q = q0; q < q1; q++) {
+        double tot = qtot[q];
+        if (isnan(tot) || isinf(tot)) continue;
+        if (tot < c - 1e-15) {
+          c = tot;
+          best = q;
+        }
+      }
+      u32 i = order[t];
+      s_bc[i] = c;
+      bn[i] = best == TSAT_NONE ? TSAT_NONE : qnode[best];
+    }
+    __syncthreads();
+  }
+  for (u32 t = threadIdx.x; t < ntr; t += blockDim.x) {
+    u32 i = order[t];
+    bc_g[i] = s_bc[i];
+  }
+}
+
 __global__ void k_greedy_level_wide(G g, const u32* cls_off, const u32* cls_nodes, const u32* cls_index,
                                     const u32* order, u32 a, u32 b, const double* cost, double* bc, u32* bn) {
   __shared__ double stot[8][32];
@@ -595,7 +674,41 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
   G gv = view();
   const u32 *co = snap.cls_off.p, *cn = snap.cls_nodes.p, *ci = snap.cls_index.p, *ord = sc.c_order.p,
             *lvl = sc.c_lvloff.p;
-  for (u32 l = 0; l < nl;) {
+  const u64 GREEDY_SMEM = 200u << 10;
+  bool cta = (u64)C * sizeof(double) <= GREEDY_SMEM;
+  if (cta) {
+    static int smem_set = 0;
+    if (!smem_set) {
+      CUDA_OK(cudaFuncSetAttribute(k_greedy_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GREEDY_SMEM));
+      smem_set = 1;
+    }
+    Scratch& X = sc;
+    X.gq_lvm.ensure(ntr + 1);
+    X.gq_cnt.ensure(ntr + 1);
+    k_gq_count<<<nblk(ntr), 256, 0, s>>>(ord, ntr, co, X.gq_cnt.p);
+    CUDA_OK(cudaMemsetAsync(X.gq_cnt.p + ntr, 0, sizeof(u32), s));
+    dev_exclusive_scan_u32(*this, X.gq_cnt.p, X.gq_lvm.p, ntr + 1);
+    u32 nq = 0;
+    CUDA_OK(cudaMemcpyAsync(&nq, X.gq_lvm.p + ntr, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    sync();
+    X.gq_k.ensure(nq + 1);
+    X.gq_node.ensure(nq + 1);
+    X.gq_cost.ensure(nq + 1);
+    X.gq_tot.ensure(nq + 1);
+    X.gq_deg.ensure(nq + 1);
+    X.gq_eoff.ensure(nq + 1);
+    k_gq_fill<<<nblk(ntr), 256, 0, s>>>(gv, ord, ntr, co, cn, sc.cg_moff.p, X.gq_lvm.p, cost, X.gq_k.p, X.gq_node.p,
+                                        X.gq_cost.p, X.gq_deg.p);
+    CUDA_OK(cudaMemsetAsync(X.gq_deg.p + nq, 0, sizeof(u32), s));
+    dev_exclusive_scan_u32(*this, X.gq_deg.p, X.gq_eoff.p, nq + 1);
+    X.gq_edst.ensure((u64)cg_ne + 1);
+    k_gq_edges<<<nblk(nq), 256, 0, s>>>(nq, X.gq_k.p, sc.cg_moff.p, sc.cg_edst.p, X.gq_eoff.p, X.gq_edst.p);
+    k_greedy_cta<<<1, 1024, (size_t)C * sizeof(double), s>>>(ord, lvl, nl, ntr, X.gq_lvm.p, X.gq_node.p,
+                                                              X.gq_cost.p, X.gq_eoff.p, X.gq_edst.p, X.gq_tot.p, c0.p,
+                                                              n0.p);
+    CUDA_OK(cudaGetLastError());
+  }
+  for (u32 l = 0; l < nl && !cta;) {
     if (lo[l + 1] - lo[l] > 64) {
       k_greedy_level_wide<<<nblk((u64)(lo[l + 1] - lo[l]) * 32, 256), 256, 0, s>>>(gv, co, cn, ci, ord, lo[l],
                                                                                     lo[l + 1], cost, c0.p, n0.p);

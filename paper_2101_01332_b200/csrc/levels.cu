@@ -46,21 +46,22 @@ __device__ __forceinline__ u32 vdeg(const Frontier& F, u32 j) {
   return F.bfs ? F.eoff[j + 1] - F.eoff[j] : F.roff[j + 1] - F.roff[j];
 }
 
-// ctl[0] = queue tail, ctl[7] = edge count of the next frontier
-__device__ __forceinline__ void frontier_edge(const Frontier& F, u32 e, u32 lvl, u32* ctl) {
+// deg = mark (BFS) or outdeg (trim) array; tail / nedges = queue tail and edge
+// count of the next frontier (global ctl words, or shared-memory copies)
+__device__ __forceinline__ void frontier_edge(const Frontier& F, u32 e, u32 lvl, u32* deg, u32* tail, u32* nedges) {
   if (F.bfs) {
     u32 k = F.edst[e];
-    if (F.mark[k] == 0 && atomicCAS(&F.mark[k], 0u, 1u) == 0u) {
-      F.order[atomicAdd(&ctl[0], 1u)] = k;
-      atomicAdd(&ctl[7], vdeg(F, k));
+    if (deg[k] == 0 && atomicCAS(&deg[k], 0u, 1u) == 0u) {
+      F.order[atomicAdd(tail, 1u)] = k;
+      atomicAdd(nedges, vdeg(F, k));
     }
   } else {
     u32 i = F.rsrc[e];
     if (F.mask && !F.mask[i]) return;
-    if (atomicSub(&F.outdeg[i], 1u) == 1u) {
+    if (atomicSub(&deg[i], 1u) == 1u) {
       F.level[i] = lvl + 1;
-      F.order[atomicAdd(&ctl[0], 1u)] = i;
-      atomicAdd(&ctl[7], vdeg(F, i));
+      F.order[atomicAdd(tail, 1u)] = i;
+      atomicAdd(nedges, vdeg(F, i));
     }
   }
 }
@@ -113,16 +114,27 @@ __global__ void k_frontier_start(u32* ctl, u32* lvl_off) {
 
 // thin levels inside one CTA; exits when a frontier gets wide (by edges).
 // Vertices with more than HEAVY edges are queued and their edge lists are
-// swept by the whole CTA.
+// swept by the whole CTA.  With ``use_smem`` the mark / out-degree array and
+// the queue counters live in shared memory (small graphs), so a level costs
+// a couple of dependent global loads plus shared-memory atomics.
 #define LV_EDGES 65536u
-__global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ctl) {
-  __shared__ u32 s_start, s_end, s_lvl, s_nheavy, s_edges;
+__global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ctl, int use_smem) {
+  extern __shared__ u32 s_deg[];
+  __shared__ u32 s_start, s_end, s_lvl, s_nheavy, s_edges, s_tail, s_ned;
   __shared__ u32 s_heavy[LV_BLOCK];
+  u32* gdeg = F.bfs ? F.mark : F.outdeg;
+  u32* deg = use_smem ? s_deg : gdeg;
+  u32* tail = use_smem ? &s_tail : &ctl[0];
+  u32* ned = use_smem ? &s_ned : &ctl[7];
+  if (use_smem)
+    for (u32 i = threadIdx.x; i < F.n; i += blockDim.x) s_deg[i] = gdeg[i];
   if (threadIdx.x == 0) {
     s_start = ctl[2];
     s_end = ctl[3];
     s_lvl = ctl[1];
     s_edges = ctl[6];
+    s_tail = ctl[0];
+    s_ned = ctl[7];
   }
   __syncthreads();
   while (true) {
@@ -141,33 +153,39 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
         edge_range(F, j, a, b);
         if (b - a > HEAVY) s_heavy[atomicAdd(&s_nheavy, 1u)] = j;
         else
-          for (u32 e = a; e < b; e++) frontier_edge(F, e, lvl, ctl);
+          for (u32 e = a; e < b; e++) frontier_edge(F, e, lvl, deg, tail, ned);
       }
       __syncthreads();
       for (u32 h = 0; h < s_nheavy; h++) {
         u32 a, b;
         edge_range(F, s_heavy[h], a, b);
-        for (u32 e = a + threadIdx.x; e < b; e += blockDim.x) frontier_edge(F, e, lvl, ctl);
+        for (u32 e = a + threadIdx.x; e < b; e += blockDim.x) frontier_edge(F, e, lvl, deg, tail, ned);
       }
       __syncthreads();
     }
     if (threadIdx.x == 0) {
       __threadfence_block();
-      u32 ne = ((volatile u32*)ctl)[0];
+      u32 ne = ((volatile u32*)tail)[0];
       s_start = end;
       s_end = ne;
       s_lvl = lvl + 1;
-      s_edges = ((volatile u32*)ctl)[7];
-      ctl[7] = 0;
+      s_edges = ((volatile u32*)ned)[0];
+      *ned = 0;
       if (F.lvl_off) F.lvl_off[lvl + 2] = ne;
     }
     __syncthreads();
   }
+  if (use_smem)
+    for (u32 i = threadIdx.x; i < F.n; i += blockDim.x) gdeg[i] = s_deg[i];
   if (threadIdx.x == 0) {
     ctl[1] = s_lvl;
     ctl[2] = s_start;
     ctl[3] = s_end;
     ctl[6] = s_edges;
+    if (use_smem) {
+      ctl[0] = s_tail;
+      ctl[7] = s_ned;
+    }
   }
 }
 
@@ -189,14 +207,15 @@ __global__ void k_frontier_grid(Frontier F, u32* ctl, u32* heavy) {
         if (lane == 0) heavy[atomicAdd(&ctl[8], 1u)] = j;
         continue;
       }
-      for (u32 e = a + lane; e < b; e += 32) frontier_edge(F, e, lvl, ctl);
+      for (u32 e = a + lane; e < b; e += 32) frontier_edge(F, e, lvl, F.bfs ? F.mark : F.outdeg, &ctl[0], &ctl[7]);
     }
     grid.sync();
     u32 nh = ((volatile u32*)ctl)[8];
     for (u32 h = 0; h < nh; h++) {
       u32 a, b;
       edge_range(F, heavy[h], a, b);
-      for (u64 e = a + grid.thread_rank(); e < b; e += grid.size()) frontier_edge(F, (u32)e, lvl, ctl);
+      for (u64 e = a + grid.thread_rank(); e < b; e += grid.size())
+        frontier_edge(F, (u32)e, lvl, F.bfs ? F.mark : F.outdeg, &ctl[0], &ctl[7]);
     }
     grid.sync();
     u32 ne = ((volatile u32*)ctl)[0];
@@ -239,8 +258,15 @@ static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& tot
   static int gblocks = 0;
   if (!gblocks) gblocks = coop_blocks(e, (const void*)k_frontier_grid, 256);
   u32 h[5];
+  const u32 FR_SMEM = 160u << 10;
+  int use_smem = (u64)F.n * 4 <= FR_SMEM;
+  static int smem_set = 0;
+  if (!smem_set) {
+    CUDA_OK(cudaFuncSetAttribute(k_frontier_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FR_SMEM));
+    smem_set = 1;
+  }
   while (true) {
-    k_frontier_block<<<1, LV_BLOCK, 0, e.s>>>(F, ctl.p);
+    k_frontier_block<<<1, LV_BLOCK, use_smem ? (size_t)F.n * 4 : 0, e.s>>>(F, ctl.p, use_smem);
     CUDA_OK(cudaMemcpyAsync(h, ctl.p, 5 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
     e.sync();
     if (h[4]) break;
