@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "rulesdev.cuh"
@@ -231,6 +232,13 @@ __device__ __forceinline__ u64 wkey_hash(u32 op, int n, const u32* k) {
 
 // find-or-insert a key; returns slot.  state = epoch << 2 | {1 busy, 2 ready};
 // a slot whose epoch is not the current one is empty.
+template <bool CTA>
+__device__ __forceinline__ void wfence() {
+  if (CTA) __threadfence_block();
+  else __threadfence();
+}
+
+template <bool CTA>
 __device__ u32 wtab_get(const WaveTab& T, u32 op, int n, const u32* k) {
   u32 slot = (u32)wkey_hash(op, n, k) & T.mask;
   const u32 busy = (T.epoch << 2) | 1u, ready = (T.epoch << 2) | 2u;
@@ -242,14 +250,14 @@ __device__ u32 wtab_get(const WaveTab& T, u32 op, int n, const u32* k) {
         kk[0] = op;
         kk[1] = (u32)n;
         for (int i = 0; i < 8; i++) kk[2 + i] = i < n ? k[i] : 0u;
-        __threadfence();
+        wfence<CTA>();
         atomicExch(&T.state[slot], ready);
         return slot;
       }
       st = ((volatile u32*)T.state)[slot];
     }
     while (st == busy) st = ((volatile u32*)T.state)[slot];
-    __threadfence();
+    wfence<CTA>();
     const volatile u32* kk = T.key + (u64)slot * 10;
     bool eq = kk[0] == op && kk[1] == (u32)n;
     for (int i = 0; i < n && eq; i++) eq = kk[2 + i] == k[i];
@@ -259,6 +267,7 @@ __device__ u32 wtab_get(const WaveTab& T, u32 op, int n, const u32* k) {
 }
 
 // one request level: thread per (accepted combo, template at this depth)
+template <bool CTA>
 __device__ __forceinline__ void d_resolve_level(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
                                                 const u32* acc, u32 nacc, const int* lvl_req, int nlvl,
                                                 const u32* env, u32* ident, u8* hazard) {
@@ -284,7 +293,7 @@ __device__ __forceinline__ void d_resolve_level(u64 tid, u64 nth, const G& g, co
         continue;
       }
     }
-    u32 s = wtab_get(T, q.atom, q.nargs, kids);
+    u32 s = wtab_get<CTA>(T, q.atom, q.nargs, kids);
     atomicMin(&T.minpos[s], mp_tag(T.epoch, gpos));
     ident[gpos] = FRESH | s;
     if (g.analysis) {
@@ -659,7 +668,7 @@ __global__ void k_accept_list(const u32* fl, const u32* pre, u32 n, u32* acc) {
 
 __global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const int* lvl_req,
                                 int nlvl, const u32* env, u32* ident, u8* hazard) {
-  d_resolve_level(GTID, GNTH, g, W, T, acc, ws->nacc, lvl_req, nlvl, env, ident, hazard);
+  d_resolve_level<false>(GTID, GNTH, g, W, T, acc, ws->nacc, lvl_req, nlvl, env, ident, hazard);
 }
 
 __global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const u32* ident,
@@ -964,7 +973,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     if (W.R > 0) {
       for (int d = 1; d < A.nlv; d++) {
         if (!A.nlvl[d]) continue;
-        d_resolve_level(tid, nth, g, W, Tw, io.acc, nacc, io.lvl + A.lvl_off[d], A.nlvl[d], io.env, io.ident,
+        d_resolve_level<true>(tid, nth, g, W, Tw, io.acc, nacc, io.lvl + A.lvl_off[d], A.nlvl[d], io.env, io.ident,
                         io.hazard);
         __syncthreads();
       }
@@ -1287,6 +1296,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
   int skip_self = (hr.nsrc == 2 && !allow_self && hr.same_canon) ? 1 : 0;
   const bool multi = hr.nsrc > 1;
   RuleStatsH& rs = e.rstats[ri];
+  const double dbg_w0 = e.phase_ms[8], dbg_c0 = e.phase_ms[10];
   B.wstats.ensure(1);
   CUDA_OK(cudaMemsetAsync(B.wstats.p, 0, sizeof(DevStats), e.s));
   // multi-pattern join cache: compatible positions stay valid until a union of
@@ -1559,4 +1569,8 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
   CUDA_OK(cudaMemcpyAsync(&d, B.wstats.p, sizeof(d), cudaMemcpyDeviceToHost, e.s));
   e.sync();
   accumulate_seg(e, ri, d);
+  if (getenv("TSAT_DEBUG_WAVES"))
+    fprintf(stderr, "rule %d %s P=%llu waves=%.0f cuts=%.0f applied=%llu live=%u\n", ri,
+            ri < (int)e.rule_names.size() ? e.rule_names[ri].c_str() : "?", P, e.phase_ms[8] - dbg_w0,
+            e.phase_ms[10] - dbg_c0, (unsigned long long)d.applied, e.h.live);
 }
