@@ -118,6 +118,18 @@ int tsat_costs(tsat_engine* h, int32_t mode, int32_t strict, int32_t ntab, const
 int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, uint32_t* sel_node,
                 uint32_t* nsel, double* root_best, int64_t* rounds);
 
+/* Multi-GPU e-matching shards.  Rank r of ``world`` e-matches
+ * root candidates whose e-class id lies in [lo_r, hi_r) (tsat_shard_range of
+ * the allocated-node count) and the per-pattern match lists are all-gathered
+ * over NCCL, rank-order concatenation being the global (eclass, bindings)
+ * order of EGraph.ematch (egraph.py:107-112, 248-262).  The NCCL unique id is
+ * created by rank 0 (tsat_nccl_unique_id) and distributed by the caller.
+ * world == 1 disables sharding; nccl_id == NULL with world > 1 computes this
+ * rank's part only, without the exchange (diagnostics / single-GPU tests). */
+int tsat_shard_setup(tsat_engine* h, int32_t rank, int32_t world, const void* nccl_id, int32_t id_bytes);
+int tsat_nccl_unique_id(void* out, int32_t cap, int32_t* len);
+int tsat_shard_range(uint64_t n_alloc, int32_t rank, int32_t world, uint32_t* lo, uint32_t* hi);
+
 /* per kernel-group CUDA-event timings and algorithmic bytes since the last
  * reset; groups: rebuild, ematch, apply_seq, apply_wave, reach, cycles,
  * costs, greedy, snapshot */

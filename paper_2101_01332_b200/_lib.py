@@ -67,6 +67,9 @@ _SIGS = {
     "tsat_phase_times": ([C.c_void_p, f64p, C.c_int32], C.c_int),
     "tsat_debug_info": ([C.c_void_p, i64p, C.c_int32], C.c_int),
     "tsat_kernel_stats": ([C.c_void_p, f64p, f64p, i64p, C.c_int32, C.c_int32], C.c_int),
+    "tsat_shard_setup": ([C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_int32], C.c_int),
+    "tsat_nccl_unique_id": ([C.c_char_p, C.c_int32, i32p], C.c_int),
+    "tsat_shard_range": ([C.c_uint64, C.c_int32, C.c_int32, u32p, u32p], C.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

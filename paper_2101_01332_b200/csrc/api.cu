@@ -306,6 +306,30 @@ int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, u
   GUARD(h, *root_best = h->e->greedy(cost_by_node, sel_cls, sel_node, nsel, rounds));
 }
 
+int tsat_shard_setup(tsat_engine* h, int32_t rank, int32_t world, const void* nccl_id, int32_t id_bytes) {
+  GUARD(h, {
+    if (world > 1 && nccl_id && id_bytes != 128) throw TsatException(TSAT_ERR_ARG, "need a 128-byte NCCL unique id");
+    h->e->shard_setup(rank, world, nccl_id);
+  });
+}
+
+int tsat_nccl_unique_id(void* out, int32_t cap, int32_t* len) {
+  if (!out || !len || cap < 128) return TSAT_ERR_ARG;
+  try {
+    nccl_unique_id(out);
+    *len = 128;
+    return TSAT_OK;
+  } catch (TsatException& ex) {
+    return ex.code;
+  }
+}
+
+int tsat_shard_range(uint64_t n_alloc, int32_t rank, int32_t world, uint32_t* lo, uint32_t* hi) {
+  if (!lo || !hi || world < 1 || rank < 0 || rank >= world) return TSAT_ERR_ARG;
+  shard_range(n_alloc, rank, world, *lo, *hi);
+  return TSAT_OK;
+}
+
 int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launches, int32_t n, int32_t reset) {
   GUARD(h, {
     Engine& e = *h->e;

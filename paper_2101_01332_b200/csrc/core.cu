@@ -86,6 +86,7 @@ void free_wave_bufs(WaveBufs* b);
 // return a pooled engine to the freshly-created state, keeping allocations
 void Engine::reset(bool analysis_) {
   sync();
+  shard_teardown();
   analysis = analysis_;
   memset(&h, 0, sizeof(h));
   push_counters();
@@ -111,6 +112,10 @@ void Engine::reset(bool analysis_) {
 }
 
 Engine::~Engine() {
+  try {
+    shard_teardown();
+  } catch (...) {
+  }
   if (wave) free_wave_bufs(wave);
   if (s) {
     cudaStreamSynchronize(s);

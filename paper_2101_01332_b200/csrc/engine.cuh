@@ -175,6 +175,9 @@ struct Scratch {
   // e-matching
   DevBuf<u32> m_rc, m_rb, m_cnt, m_perm, m_perm2, m_key, m_key2, m_fl, m_pos;
   DevBuf<u32> m_bnd, m_big, m_head, m_bpos, m_L, m_bh, m_gex, m_bperm, m_bperm2, m_bkey, m_bkey2;
+  // sharding (shard.cu)
+  DevBuf<u32> sh_rng, sh_cnt, sh_pack, sh_recv;
+  DevBuf<unsigned char> sh_segs;
   // class graph / cycles / reach
   DevBuf<u32> cg_eoff, cg_edst, cg_enode, cg_roff, cg_rsrc, cg_outdeg, cg_level, cg_esrc, cg_sdst, cg_moff, cg_mdeg;
   DevBuf<u32> c_heavy, c_mark32, c_fa, c_fb, c_order, c_depth, c_path, c_cycn, c_cyco, c_res, c_rest, c_lvloff;
@@ -299,6 +302,14 @@ struct Engine {
   // snapshot + matching
   void build_snapshot();
   void ematch_batch(const std::vector<int>& pids);
+
+  // multi-GPU e-matching shards (shard.cu)
+  int shard_rank = 0, shard_world = 1;
+  void* comm = nullptr;  // ncclComm_t
+  void shard_setup(int rank, int world, const void* nccl_id);
+  void shard_teardown();
+  void shard_candidate_ranges(std::vector<u32>& rng);
+  void shard_gather_matches(const std::vector<int>& pids);
   void load_rules(int n, const i64* blob);
 
   // cycles
@@ -331,3 +342,5 @@ void dev_exclusive_scan_u32(Engine& e, const u32* in, u32* out, u32 n);
 void dev_sort_pairs_u32(Engine& e, u32* keys_in, u32* keys_out, u32* vals_in, u32* vals_out, u32 n,
                         int end_bit);
 u32 bits_for(u32 maxval);
+void shard_range(u64 n_alloc, int rank, int world, u32& lo, u32& hi);
+void nccl_unique_id(void* out);

@@ -299,14 +299,23 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
     u32 ntot = 0;
     int stride = 1;
     double cand_bytes = 0;
-    for (int pid : pids) {
+    // root candidate ranges (this rank's class range when sharded, shard.cu)
+    std::vector<u32> rng(2 * pids.size(), 0);
+    for (size_t q = 0; q < pids.size(); q++) {
+      u32 ra = patterns[pids[q]].apps[0].atom;
+      if (ra + 1 < snap.op_off_h.size()) {
+        rng[2 * q] = snap.op_off_h[ra];
+        rng[2 * q + 1] = snap.op_off_h[ra + 1];
+      }
+    }
+    shard_candidate_ranges(rng);
+    for (size_t q = 0; q < pids.size(); q++) {
+      int pid = pids[q];
       const HPattern& hp = patterns[pid];
       MatchSet& ms = matches[pid];
       ms.nb = hp.nvars;
       ms.n = 0;
-      u32 ra = hp.apps[0].atom;
-      if (ra + 1 >= snap.op_off_h.size()) continue;
-      u32 lo = snap.op_off_h[ra], hi = snap.op_off_h[ra + 1];
+      u32 lo = rng[2 * q], hi = rng[2 * q + 1];
       if (hi == lo) continue;
       int b = (int)live.size();
       PatDev& p = B.pat[b];
@@ -321,7 +330,10 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
       cand_bytes += (double)(hi - lo) * (17.0 + 8.0 * hp.apps[0].nargs);
       live.push_back(pid);
     }
-    if (live.empty()) continue;
+    if (live.empty()) {
+      shard_gather_matches(pids);
+      continue;
+    }
     int np = (int)live.size();
     B.npat = np;
     B.cbase[np] = ntot;
@@ -417,5 +429,6 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
     for (int b = 0; b < np; b++) rows_bytes += (double)(B.rbase[b + 1] - B.rbase[b]) * 4.0 * (1 + B.pat[b].nb);
     kt.bytes = cand_bytes + 2.0 * rows_bytes;
     kt.launches = 9;
+    shard_gather_matches(pids);
   }
 }

@@ -10,6 +10,8 @@ global insertion counter; ``dump`` byte-identical).
 
 from __future__ import annotations
 
+import functools
+
 import ctypes as C
 from dataclasses import dataclass
 from typing import Any, Iterable, Iterator, Mapping, Optional
@@ -45,6 +47,7 @@ class EClass:
     analysis: Any = None
 
 
+@functools.lru_cache(maxsize=None, typed=True)
 def _atom_info(a: Atom):
     """(kind, ival, opcode, ndims, dims, nident, idims) for the device atom table;
     string parsing mirrors tensor_lang.parse_dims / parse_identifier."""

@@ -163,11 +163,19 @@ def explore(
     on_reject: Optional[Callable] = None,
     allow_self_pairs: bool = False,
     device: int = 0,
+    shard_group=None,
 ):
-    """End-to-end exploration of a single-rooted tensor graph on the GPU."""
+    """End-to-end exploration of a single-rooted tensor graph on the GPU.
+    ``shard_group``: a torch.distributed process group whose ranks (one per GPU)
+    split e-matching by e-class range (shard.py); results are identical on
+    every rank and to the single-GPU run."""
     if g.root is None:
         raise TensorSatError("graph must be single-rooted (run make_single_rooted)")
     eg, _ = build_egraph(g, device=device)
+    if shard_group is not None:
+        from .shard import attach_group
+
+        attach_group(eg, None if shard_group is True else shard_group)
     filt, report = saturate(eg, rules, limits, filter_mode, on_reject=on_reject,
                             allow_self_pairs=allow_self_pairs)
     return eg, filt, report

@@ -1,0 +1,91 @@
+"""Multi-GPU e-matching shards.
+
+One process per GPU; every rank holds a replica of the e-graph.  Rank ``r``
+of ``world`` e-matches only root candidates whose e-class id lies in the
+contiguous id range :func:`class_range` of the allocated-node count (class id
+= min node id, reference ``egraph.py:64``).  Matches are ordered by
+``(eclass, bindings)`` (``egraph.py:107-112``), so the rank-order
+concatenation of the ranks' sorted lists *is* the global sorted list
+(:func:`concat_rank_matches`): the device exchange is one NCCL all-gather of
+packed per-pattern lists plus an in-order unpack (``csrc/shard.cu``).
+Apply / rebuild / cycle filtering / greedy then run on identical inputs on
+every rank.
+
+``torch.distributed`` is plumbing only: it carries the NCCL unique id from
+rank 0 to the others (:func:`attach_group`) and runs the CPU (gloo) tests of
+the partition logic.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Sequence, Tuple
+
+from . import _lib
+
+
+def class_range(n_alloc: int, rank: int, world: int) -> Tuple[int, int]:
+    """[lo, hi) of e-class ids owned by ``rank`` (same formula as tsat_shard_range)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world size")
+    return n_alloc * rank // world, n_alloc * (rank + 1) // world
+
+
+def shard_matches(matches: Sequence, n_alloc: int, rank: int, world: int) -> list:
+    """The part of a sorted match list (``Match``-like, ``.eclass`` or tuple
+    head) this rank produces."""
+    lo, hi = class_range(n_alloc, rank, world)
+    return [m for m in matches if lo <= _eclass(m) < hi]
+
+
+def concat_rank_matches(parts: Sequence[Sequence]) -> list:
+    """Global match list from the ranks' lists (rank order)."""
+    out: list = []
+    for p in parts:
+        out.extend(p)
+    return out
+
+
+def _eclass(m) -> int:
+    return m.eclass if hasattr(m, "eclass") else m[0]
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 calls this)."""
+    lib = _lib.load()
+    buf = C.create_string_buffer(128)
+    n = C.c_int32()
+    st = lib.tsat_nccl_unique_id(buf, 128, C.byref(n))
+    if st != 0:
+        raise _lib.E.DeviceError(f"tsat_nccl_unique_id failed with status {st}")
+    return buf.raw[: n.value]
+
+
+def attach(eg, rank: int, world: int, uid: bytes = b"") -> None:
+    """Make ``eg`` rank ``rank`` of a ``world``-GPU e-matching shard group.
+    Without ``uid`` the engine computes its own shard only (no exchange)."""
+    lib = _lib.load()
+    _lib.check(eg._h, lib.tsat_shard_setup(eg._h, rank, world, uid or None, len(uid)))
+
+
+def attach_group(eg, group=None) -> None:
+    """Shard ``eg`` over the ranks of a torch.distributed process group."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    obj: List = [nccl_unique_id() if rank == 0 and world > 1 else b""]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+    attach(eg, rank, world, obj[0])
+
+
+def lib_class_range(n_alloc: int, rank: int, world: int) -> Tuple[int, int]:
+    """tsat_shard_range through the C-ABI (pure host function, no device)."""
+    lib = _lib.load()
+    lo, hi = C.c_uint32(), C.c_uint32()
+    st = lib.tsat_shard_range(n_alloc, rank, world, C.byref(lo), C.byref(hi))
+    if st != 0:
+        raise ValueError("bad rank / world size")
+    return lo.value, hi.value
