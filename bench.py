@@ -185,6 +185,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--workload", default="bert", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: the ranks explore ONE graph together, e-matching split by e-class range "
+                         "with an NCCL all-gather of the match lists (SURVEY 8(e)); default: one graph per GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
@@ -198,6 +201,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
+    shard_mode = args.shard and world > 1
     if world > 1:
         import torch.distributed as dist
 
@@ -234,6 +238,10 @@ def main():
     with Clocks(local) as clk:
         for i in range(args.warmup + args.steps):
             eg = build_egraph(g, device=local)[0]
+            if shard_mode:
+                from paper_2101_01332_b200.shard import attach_group
+
+                attach_group(eg)
             flush.zero_()
             barrier()
             ms = np.zeros(9)
@@ -263,7 +271,7 @@ def main():
     eg, rep, res = last
     nodes = rep.enodes_per_iter[-1] if rep.enodes_per_iter else eg.num_nodes
     ms_step = statistics.mean(step_s) * 1e3
-    value = ms_step / 1e3 / world
+    value = ms_step / 1e3 / (1 if shard_mode else world)
 
     # ---- e2e arm through the public API
     ops, kids, _, _ = initial_enodes(g)
@@ -274,7 +282,8 @@ def main():
         flush.zero_()
         barrier()
         t0 = time.perf_counter()
-        eg2, filt2, rep2 = explore(g, rules, limits, "efficient", device=local)
+        eg2, filt2, rep2 = explore(g, rules, limits, "efficient", device=local,
+                                   shard_group=True if shard_mode else None)
         costs2 = egraph_costs(eg2, CostModel())
         res2 = greedy_extract(eg2, costs2, filt2)
         torch.cuda.synchronize()
@@ -284,7 +293,7 @@ def main():
             e2e_s.append(max_over_ranks(dt))
         d2h = 8 * eg2.allocated_nodes + 8 * len(res2.selection) + 4 * len(filt2) + 8 * 7 * len(rules) + 24 * 15
         del eg2
-    e2e = statistics.mean(e2e_s) / world
+    e2e = statistics.mean(e2e_s) / (1 if shard_mode else world)
 
     # ---- roofline: dominant instrumented kernel group with an algorithmic byte model
     peak, peak_kind = load_peaks()
@@ -302,11 +311,13 @@ def main():
     line = {
         "metric": "explore+extract search time (s) per graph", "value": value, "unit": "s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64",
+        "higher_is_better": False, "scaling": "strong" if shard_mode else "weak", "vs_baseline": None,
+        "dtype": "int32+f64",
         "data": "synthetic (authored model graph, random-free; L2 flushed between steps)",
-        "config": {"workload": w["desc"], "graphs_per_step": world, "l2": "flushed (256 MiB write) between steps",
+        "config": {"workload": w["desc"], "graphs_per_step": 1 if shard_mode else world,
+                   "l2": "flushed (256 MiB write) between steps",
                    "final_enodes": nodes, "stop_reason": rep.stop_reason, "total_cost": res.total_cost,
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": f"ematch-shard x{world}" if shard_mode else f"replicas x{world}"},
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "enodes_matched_per_s": None, "kernel_groups_ms_per_step": groups_ms,
         "dominant_group": KGROUPS[dom_all],

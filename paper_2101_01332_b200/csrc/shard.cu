@@ -68,24 +68,51 @@ void nccl_unique_id(void* out) {
   memcpy(out, &id, sizeof(id));
 }
 
+// Communicators are shared by every engine of the process that was set up
+// with the same unique id (one NCCL init per process group, not per e-graph).
+struct CommEntry {
+  std::string uid;
+  int rank, world, device;
+  ncclComm_t comm;
+  int refs;
+};
+static std::vector<CommEntry>& comm_cache() {
+  static std::vector<CommEntry> c;
+  return c;
+}
+
 void Engine::shard_setup(int rank_, int world_, const void* id) {
   if (world_ < 1 || rank_ < 0 || rank_ >= world_) throw TsatException(TSAT_ERR_ARG, "bad rank / world size");
   shard_teardown();
   shard_rank = rank_;
   shard_world = world_;
   if (world_ == 1 || !id) return;  // no id: local shard only (no exchange; tests)
+  std::string key((const char*)id, NCCL_UNIQUE_ID_BYTES);
+  for (auto& ce : comm_cache())
+    if (ce.uid == key && ce.rank == rank_ && ce.world == world_ && ce.device == device) {
+      ce.refs++;
+      comm = (void*)ce.comm;
+      return;
+    }
   ncclUniqueId uid;
   memcpy(&uid, id, sizeof(uid));
   ncclComm_t c = nullptr;
   CUDA_OK(cudaSetDevice(device));
   NCCL_OK(nccl().CommInitRank(&c, world_, uid, rank_));
+  comm_cache().push_back(CommEntry{key, rank_, world_, device, c, 1});
   comm = (void*)c;
 }
 
 void Engine::shard_teardown() {
   if (comm) {
     sync();
-    nccl().CommDestroy((ncclComm_t)comm);
+    auto& cc = comm_cache();
+    for (size_t i = 0; i < cc.size(); i++)
+      if ((void*)cc[i].comm == comm && --cc[i].refs == 0) {
+        nccl().CommDestroy(cc[i].comm);
+        cc.erase(cc.begin() + i);
+        break;
+      }
     comm = nullptr;
   }
   shard_rank = 0;

@@ -68,17 +68,31 @@ def attach(eg, rank: int, world: int, uid: bytes = b"") -> None:
     _lib.check(eg._h, lib.tsat_shard_setup(eg._h, rank, world, uid or None, len(uid)))
 
 
+_GROUP_UID: dict = {}
+
+
+def group_uid(group=None) -> bytes:
+    """The NCCL unique id of a torch.distributed group (created by its first
+    rank once, then cached: every e-graph of the group shares one communicator)."""
+    import torch.distributed as dist
+
+    key = id(group)
+    if key not in _GROUP_UID:
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        obj: List = [nccl_unique_id() if rank == 0 and world > 1 else b""]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+        _GROUP_UID[key] = obj[0]
+    return _GROUP_UID[key]
+
+
 def attach_group(eg, group=None) -> None:
     """Shard ``eg`` over the ranks of a torch.distributed process group."""
     import torch.distributed as dist
 
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    obj: List = [nccl_unique_id() if rank == 0 and world > 1 else b""]
-    if world > 1:
-        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
-                                   group=group)
-    attach(eg, rank, world, obj[0])
+    attach(eg, dist.get_rank(group), dist.get_world_size(group), group_uid(group))
 
 
 def lib_class_range(n_alloc: int, rank: int, world: int) -> Tuple[int, int]:
