@@ -136,7 +136,8 @@ int tsat_shard_range(uint64_t n_alloc, int32_t rank, int32_t world, uint32_t* lo
 int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launches, int32_t n, int32_t reset);
 
 /* diagnostics: level count, peeled classes, classes, class edges, snapshot /
- * filter versions, allocated and live e-nodes */
+ * filter versions, allocated and live e-nodes, device blocks allocated by the
+ * block cache (count, bytes), engines constructed */
 int tsat_debug_info(tsat_engine* h, int64_t* out, int32_t n);
 
 /* per-phase device timings of the last saturate / greedy (ms) */

@@ -12,6 +12,7 @@ struct tsat_engine {
 #define GUARD(h, ...)                                   \
   do {                                                  \
     if (!(h) || !(h)->e) return TSAT_ERR_ARG;           \
+    tl_stream = (h)->e->s;                              \
     try {                                               \
       __VA_ARGS__;                                      \
       return TSAT_OK;                                   \
@@ -47,6 +48,7 @@ int tsat_create(int device, int analysis, tsat_engine** out) {
       }
     if (!h->e) h->e = new Engine(device);
     CUDA_OK(cudaSetDevice(device));
+    tl_stream = h->e->s;
     h->e->reset(analysis != 0);
     *out = h;
     return TSAT_OK;
@@ -61,6 +63,7 @@ void tsat_destroy(tsat_engine* h) {
   if (!h) return;
   auto& pool = engine_pool();
   bool pooled = false;
+  if (h->e) tl_stream = h->e->s;
   if (h->e && pool.size() < 4) {
     try {
       h->e->reset(false);
@@ -346,9 +349,10 @@ int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launch
 int tsat_debug_info(tsat_engine* h, int64_t* out, int32_t n) {
   GUARD(h, {
     Engine& e = *h->e;
-    int64_t v[8] = {e.lv_n, e.lv_trimmed, e.snap.ncls, e.cg_ne, (int64_t)e.snap_id, (int64_t)e.filter_id,
-                    (int64_t)e.h.next_id, (int64_t)e.h.live};
-    for (int i = 0; i < n && i < 8; i++) out[i] = v[i];
+    int64_t v[11] = {e.lv_n, e.lv_trimmed, e.snap.ncls, e.cg_ne, (int64_t)e.snap_id, (int64_t)e.filter_id,
+                     (int64_t)e.h.next_id, (int64_t)e.h.live, (int64_t)g_dev_allocs, (int64_t)g_dev_alloc_bytes,
+                     (int64_t)g_engines};
+    for (int i = 0; i < n && i < 11; i++) out[i] = v[i];
   });
 }
 

@@ -6,6 +6,8 @@
 #include <cstring>
 #include <sstream>
 
+#include <mutex>
+
 #include "engine.cuh"
 
 static inline unsigned nblk(u64 n, unsigned t = 256) {
@@ -44,6 +46,8 @@ void dev_sort_pairs_u32(Engine& e, u32* kin, u32* kout, u32* vin, u32* vout, u32
 Engine::Engine(int dev) : device(dev) {
   CUDA_OK(cudaSetDevice(dev));
   CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  tl_stream = s;
+  g_engines++;
   CUDA_OK(cudaEventCreate(&ev_pool[0]));
   CUDA_OK(cudaEventCreate(&ev_pool[1]));
   cnt.alloc(1);
@@ -100,7 +104,7 @@ void Engine::reset(bool analysis_) {
   patterns.clear();
   rules.clear();
   rule_names.clear();
-  matches.clear();
+  for (auto& m : matches) m.n = 0;  // keep the device buffers for the next graph
   snap.valid = false;
   reach.valid = false;
   lv_snap = lv_filter = ~0ull;
@@ -116,9 +120,12 @@ Engine::~Engine() {
     shard_teardown();
   } catch (...) {
   }
+  if (s) cudaStreamSynchronize(s);
+  // everything this engine released is idle now; members released below too
+  tl_stream = nullptr;
   if (wave) free_wave_bufs(wave);
   if (s) {
-    cudaStreamSynchronize(s);
+    dev_cache_forget_stream(s);
     cudaStreamDestroy(s);
   }
 }
@@ -145,6 +152,84 @@ G Engine::view() {
   g.err = err.p;
   g.cnt = cnt.p;
   return g;
+}
+
+unsigned long long g_dev_allocs = 0, g_dev_alloc_bytes = 0, g_engines = 0;
+thread_local cudaStream_t tl_stream = nullptr;
+
+// ---------------------------------------------------------------- device block cache
+namespace {
+struct CachedBlock {
+  void* p;
+  cudaStream_t s;  // stream of the last user (nullptr: idle)
+};
+struct DevCache {
+  std::mutex mu;
+  std::vector<CachedBlock> free_[64];  // bucket b holds blocks of 2^b bytes
+};
+DevCache& dev_cache() {
+  static DevCache* c = new DevCache();  // never destroyed: blocks outlive static teardown
+  return *c;
+}
+int bucket_of(size_t bytes) {
+  int b = 8;  // >= 256 B
+  while (((size_t)1 << b) < bytes) b++;
+  return b;
+}
+}  // namespace
+
+void* dev_cache_get(size_t bytes) {
+  int b = bucket_of(bytes);
+  DevCache& c = dev_cache();
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    auto& fl = c.free_[b];
+    for (size_t i = fl.size(); i-- > 0;) {
+      if (fl[i].s == tl_stream || fl[i].s == nullptr) {
+        void* p = fl[i].p;
+        fl.erase(fl.begin() + i);
+        return p;
+      }
+    }
+    if (!fl.empty()) {
+      CachedBlock blk = fl.back();
+      fl.pop_back();
+      CUDA_OK(cudaStreamSynchronize(blk.s));  // last user may still read it
+      return blk.p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, (size_t)1 << b);
+  if (e != cudaSuccess) {
+    // out of memory: release idle cached blocks and retry once
+    cudaGetLastError();
+    {
+      std::lock_guard<std::mutex> g(c.mu);
+      CUDA_OK(cudaDeviceSynchronize());
+      for (auto& fl : c.free_) {
+        for (auto& blk : fl) cudaFree(blk.p);
+        fl.clear();
+      }
+    }
+    CUDA_OK(cudaMalloc(&p, (size_t)1 << b));
+  }
+  g_dev_allocs++;
+  g_dev_alloc_bytes += (size_t)1 << b;
+  return p;
+}
+
+void dev_cache_put(void* p, size_t bytes) {
+  DevCache& c = dev_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  c.free_[bucket_of(bytes)].push_back(CachedBlock{p, tl_stream});
+}
+
+void dev_cache_forget_stream(cudaStream_t s) {
+  DevCache& c = dev_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  for (auto& fl : c.free_)
+    for (auto& blk : fl)
+      if (blk.s == s) blk.s = nullptr;
 }
 
 void Engine::sync() { CUDA_OK(cudaStreamSynchronize(s)); }
@@ -265,8 +350,8 @@ void Engine::set_atoms(int n, const int32_t* kind, const i64* ival, const int32_
   }
   offs.push_back((u32)blob.size());
   sync();
-  d_names.alloc(blob.size() + 1);
-  d_name_off.alloc(offs.size());
+  d_names.ensure(blob.size() + 1);
+  d_name_off.ensure(offs.size());
   if (!blob.empty())
     CUDA_OK(cudaMemcpyAsync(d_names.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
   CUDA_OK(cudaMemcpyAsync(d_name_off.p, offs.data(), offs.size() * sizeof(u32), cudaMemcpyHostToDevice, s));

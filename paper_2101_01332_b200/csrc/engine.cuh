@@ -11,13 +11,43 @@ struct TsatException : public std::runtime_error {
   TsatException(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 
+// Caching device allocator behind every DevBuf.  Blocks are power-of-two
+// sized and recycled instead of cudaFree'd: cudaMalloc / cudaFree cost
+// milliseconds and cudaFree synchronises the whole device, which made run
+// times erratic whenever a fresh engine or a growing buffer allocated inside
+// a timed phase.  A block is tagged with the stream of the engine that
+// released it (thread-local "current stream", set at every C-ABI entry);
+// reuse under a different stream first synchronises the tagged stream.
+extern unsigned long long g_dev_allocs, g_dev_alloc_bytes, g_engines;  // diagnostics (tsat_debug_info)
+void* dev_cache_get(size_t bytes);
+void dev_cache_put(void* p, size_t bytes);
+void dev_cache_forget_stream(cudaStream_t s);  // stream about to be destroyed (already synced)
+extern thread_local cudaStream_t tl_stream;
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;  // owning: moves only
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) {
+    o.p = nullptr;
+    o.cap = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      cap = o.cap;
+      o.p = nullptr;
+      o.cap = 0;
+    }
+    return *this;
+  }
   void alloc(size_t n) {
     release();
-    if (n) CUDA_OK(cudaMalloc((void**)&p, n * sizeof(T)));
+    if (n) p = (T*)dev_cache_get(n * sizeof(T));
     cap = n;
   }
   // grow to at least n elements, preserving the first ``keep`` elements
@@ -25,13 +55,9 @@ struct DevBuf {
     if (n <= cap) return;
     size_t nc = cap ? cap : 16;
     while (nc < n) nc *= 2;
-    T* q = nullptr;
-    CUDA_OK(cudaMalloc((void**)&q, nc * sizeof(T)));
+    T* q = (T*)dev_cache_get(nc * sizeof(T));
     if (keep && p) CUDA_OK(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
-    if (p) {
-      CUDA_OK(cudaStreamSynchronize(s));
-      CUDA_OK(cudaFree(p));
-    }
+    release();
     p = q;
     cap = nc;
   }
@@ -43,7 +69,7 @@ struct DevBuf {
     }
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_cache_put(p, cap * sizeof(T));
     p = nullptr;
     cap = 0;
   }

@@ -92,16 +92,18 @@ void Engine::load_rules(int n, const i64* b) {
       all_instr.insert(all_instr.end(), r.targets[t].begin(), r.targets[t].end());
       all_leaf.insert(all_leaf.end(), r.leaves[t].begin(), r.leaves[t].end());
     }
-  d_instr.alloc(all_instr.size() + 1);
-  d_leaf.alloc(all_leaf.size() + 1);
+  d_instr.ensure(all_instr.size() + 1);
+  d_leaf.ensure(all_leaf.size() + 1);
   if (!all_instr.empty())
     CUDA_OK(cudaMemcpyAsync(d_instr.p, all_instr.data(), all_instr.size() * sizeof(Instr),
                             cudaMemcpyHostToDevice, s));
   if (!all_leaf.empty())
     CUDA_OK(cudaMemcpyAsync(d_leaf.p, all_leaf.data(), all_leaf.size() * sizeof(int),
                             cudaMemcpyHostToDevice, s));
-  matches.clear();
-  matches.resize(patterns.size());
+  // match sets keep their device buffers across rule loads (no per-run
+  // cudaMalloc / cudaFree, whose implicit syncs made run times erratic)
+  if (matches.size() < patterns.size()) matches.resize(patterns.size());
+  for (auto& m : matches) m.n = 0;
   sync();
 }
 

@@ -66,6 +66,39 @@ __device__ __forceinline__ void frontier_edge(const Frontier& F, u32 e, u32 lvl,
   }
 }
 
+// warp-uniform variant for the grid kernel: all 32 lanes call it (valid = lane
+// holds an edge); the queue tail and the next-frontier edge count are bumped
+// once per warp (ballot + popc) instead of once per vertex -- a 1M-vertex
+// level otherwise serialises on the single tail counter.
+__device__ __forceinline__ void frontier_edge_warp(const Frontier& F, bool valid, u32 e, u32 lvl, u32* deg,
+                                                   u32* tail, u32* nedges) {
+  u32 v = TSAT_NONE;
+  if (valid) {
+    if (F.bfs) {
+      u32 k = F.edst[e];
+      if (deg[k] == 0 && atomicCAS(&deg[k], 0u, 1u) == 0u) v = k;
+    } else {
+      u32 i = F.rsrc[e];
+      if ((!F.mask || F.mask[i]) && atomicSub(&deg[i], 1u) == 1u) {
+        F.level[i] = lvl + 1;
+        v = i;
+      }
+    }
+  }
+  u32 lane = threadIdx.x & 31;
+  unsigned m = __ballot_sync(0xffffffffu, v != TSAT_NONE);
+  if (!m) return;
+  u32 d = v != TSAT_NONE ? vdeg(F, v) : 0u;
+  for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  u32 base = 0;
+  if (lane == 0) {
+    base = atomicAdd(tail, (u32)__popc(m));
+    atomicAdd(nedges, d);
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (v != TSAT_NONE) F.order[base + __popc(m & ((1u << lane) - 1))] = v;
+}
+
 __device__ __forceinline__ void edge_range(const Frontier& F, u32 j, u32& a, u32& b) {
   if (F.bfs) {
     a = F.eoff[j];
@@ -144,6 +177,86 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
       break;
     }
     if (end - start > LV_WIDE || s_edges > LV_EDGES) break;
+    if (end - start <= 32 && s_edges <= 64) {
+      // Very thin levels (deep chains): warp 0 alone walks level after level
+      // with __syncwarp() only; the queue tail lives in a register.
+      if (threadIdx.x < 32) {
+        const u32 lane = threadIdx.x;
+        u32 st = start, en = end, lv = lvl, ed = s_edges, tl = *(volatile u32*)tail;
+        // the frontier stays in registers: lane q holds vertex st + q and its
+        // edge range, handed over by shuffles from the lane that queued it
+        u32 a = 0, b = 0;
+        if (st + lane < en) edge_range(F, F.order[st + lane], a, b);
+        while (st < en && en - st <= 32 && ed <= 64) {
+          u32 md = b - a;
+          for (int o = 16; o; o >>= 1) md = max(md, __shfl_xor_sync(0xffffffffu, md, o));
+          if (md > 16) break;  // a fat vertex: let the whole CTA take this level
+          const u32 nst = tl;
+          u32 nd = 0, na = 0, nb = 0;
+          for (u32 k = 0; k < md; k++) {
+            u32 v = TSAT_NONE, va = 0, vb = 0;
+            if (a + k < b) {
+              u32 e = a + k;
+              if (F.bfs) {
+                u32 x = F.edst[e];
+                if (deg[x] == 0 && atomicCAS(&deg[x], 0u, 1u) == 0u) v = x;
+              } else {
+                u32 i = F.rsrc[e];
+                if ((!F.mask || F.mask[i]) && atomicSub(&deg[i], 1u) == 1u) {
+                  F.level[i] = lv + 1;
+                  v = i;
+                }
+              }
+            }
+            unsigned m = __ballot_sync(0xffffffffu, v != TSAT_NONE);
+            if (v != TSAT_NONE) {
+              F.order[tl + __popc(m & ((1u << lane) - 1))] = v;
+              edge_range(F, v, va, vb);
+              nd += vb - va;
+            }
+            // hand (va, vb) to the lane that owns the new position
+            int q = (int)lane - (int)(tl - nst);
+            u32 cnt = __popc(m);
+            u32 src = lane;
+            if (q >= 0 && (u32)q < cnt) {
+              u32 mm = m;
+              for (int i = 0; i < q; i++) mm &= mm - 1;  // drop the q lowest set bits
+              src = (u32)(__ffs(mm) - 1);
+            }
+            u32 ga = __shfl_sync(0xffffffffu, va, src), gb = __shfl_sync(0xffffffffu, vb, src);
+            if (q >= 0 && (u32)q < cnt) {
+              na = ga;
+              nb = gb;
+            }
+            tl += cnt;
+          }
+          for (int o = 16; o; o >>= 1) nd += __shfl_xor_sync(0xffffffffu, nd, o);
+          if (F.lvl_off && lane == 0) F.lvl_off[lv + 2] = tl;
+          st = en;
+          en = tl;
+          ed = nd;
+          lv++;
+          if (en - st > 32) break;
+          a = na;
+          b = nb;
+          __syncwarp();
+        }
+        if (lane == 0) {
+          s_start = st;
+          s_end = en;
+          s_lvl = lv;
+          s_edges = ed;
+          *tail = tl;
+          *ned = 0;
+        }
+      }
+      __syncthreads();
+      if (s_start == start) {
+        // no progress in warp mode (fat vertex): fall through to the CTA path
+      } else {
+        continue;
+      }
+    }
     for (u32 t0 = start; t0 < end; t0 += blockDim.x) {
       if (threadIdx.x == 0) s_nheavy = 0;
       __syncthreads();
@@ -190,32 +303,64 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
 }
 
 // wide levels on the whole GPU; exits when the frontier gets thin again.
-// Light vertices: one warp each.  Heavy vertices (> 1024 edges, e.g. shared
-// literals with millions of parents): the whole grid sweeps their edges.
+// Three vertex tiers, every queue append warp-aggregated (ballot + popc, one
+// atomic per warp step -- a 1M-vertex level otherwise serialises on the tail):
+//   light  (<= 32 edges): one thread per vertex, lanes step their edge lists
+//   medium (<= 4096):     listed, then one warp per vertex
+//   heavy  (> 4096, e.g. shared literals with a million parents): listed,
+//                         then the whole grid sweeps each edge list
 __global__ void k_frontier_grid(Frontier F, u32* ctl, u32* heavy) {
   cg::grid_group grid = cg::this_grid();
   u32 start = ctl[2], end = ctl[3], lvl = ctl[1], edges = ctl[6];
   u32 lane = threadIdx.x & 31;
   u64 warp = grid.thread_rank() >> 5, nwarp = grid.size() >> 5;
+  u32* medium = heavy + F.n + 1;
+  u32* deg = F.bfs ? F.mark : F.outdeg;
   while (start < end && (end - start > LV_WIDE / 4 || edges > LV_EDGES / 4)) {
-    if (grid.thread_rank() == 0) ctl[8] = 0;
-    grid.sync();
-    for (u64 t = start + warp; t < end; t += nwarp) {
-      u32 j = F.order[t], a, b;
-      edge_range(F, j, a, b);
-      if (b - a > 1024) {
-        if (lane == 0) heavy[atomicAdd(&ctl[8], 1u)] = j;
-        continue;
-      }
-      for (u32 e = a + lane; e < b; e += 32) frontier_edge(F, e, lvl, F.bfs ? F.mark : F.outdeg, &ctl[0], &ctl[7]);
+    if (grid.thread_rank() == 0) {
+      ctl[8] = 0;
+      ctl[9] = 0;
     }
     grid.sync();
+    for (u64 t0 = start + warp * 32; t0 < end; t0 += nwarp * 32) {
+      u64 t = t0 + lane;
+      u32 a = 0, b = 0, j = TSAT_NONE;
+      if (t < end) {
+        j = F.order[t];
+        edge_range(F, j, a, b);
+      }
+      u32 d = b - a;
+      bool med = j != TSAT_NONE && d > 32 && d <= 4096, hv = j != TSAT_NONE && d > 4096;
+      unsigned mm = __ballot_sync(0xffffffffu, med), mh = __ballot_sync(0xffffffffu, hv);
+      if (mm | mh) {
+        u32 bm = 0, bh = 0;
+        if (lane == 0) {
+          if (mm) bm = atomicAdd(&ctl[9], (u32)__popc(mm));
+          if (mh) bh = atomicAdd(&ctl[8], (u32)__popc(mh));
+        }
+        bm = __shfl_sync(0xffffffffu, bm, 0);
+        bh = __shfl_sync(0xffffffffu, bh, 0);
+        if (med) medium[bm + __popc(mm & ((1u << lane) - 1))] = j;
+        if (hv) heavy[bh + __popc(mh & ((1u << lane) - 1))] = j;
+      }
+      if (med || hv) b = a;
+      u32 md = b - a;
+      for (int o = 16; o; o >>= 1) md = max(md, __shfl_xor_sync(0xffffffffu, md, o));
+      for (u32 k = 0; k < md; k++) frontier_edge_warp(F, a + k < b, a + k, lvl, deg, &ctl[0], &ctl[7]);
+    }
+    grid.sync();
+    u32 nm = ((volatile u32*)ctl)[9];
+    for (u64 q = warp; q < nm; q += nwarp) {
+      u32 a, b;
+      edge_range(F, medium[q], a, b);
+      for (u32 e0 = a; e0 < b; e0 += 32) frontier_edge_warp(F, e0 + lane < b, e0 + lane, lvl, deg, &ctl[0], &ctl[7]);
+    }
     u32 nh = ((volatile u32*)ctl)[8];
     for (u32 h = 0; h < nh; h++) {
       u32 a, b;
       edge_range(F, heavy[h], a, b);
-      for (u64 e = a + grid.thread_rank(); e < b; e += grid.size())
-        frontier_edge(F, (u32)e, lvl, F.bfs ? F.mark : F.outdeg, &ctl[0], &ctl[7]);
+      for (u64 e0 = a + warp * 32; e0 < b; e0 += nwarp * 32)
+        frontier_edge_warp(F, e0 + lane < b, (u32)(e0 + lane), lvl, deg, &ctl[0], &ctl[7]);
     }
     grid.sync();
     u32 ne = ((volatile u32*)ctl)[0];
@@ -252,7 +397,7 @@ static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& tot
   ctl.ensure(16);
   CUDA_OK(cudaMemsetAsync(ctl.p, 0, 16 * sizeof(u32), e.s));
   DevBuf<u32>& heavy = e.sc.c_heavy;
-  heavy.ensure(F.n + 1);
+  heavy.ensure(2 * ((u64)F.n + 1));
   k_frontier_init<<<nblk(F.n), 256, 0, e.s>>>(F, ctl.p, root);
   k_frontier_start<<<1, 1, 0, e.s>>>(ctl.p, F.lvl_off);
   static int gblocks = 0;

@@ -20,6 +20,9 @@
 // Two host synchronisations per batch (row counts, unique counts).
 #include <cub/cub.cuh>
 
+#include <chrono>
+#include <cstdlib>
+
 #include "engine.cuh"
 
 static inline unsigned nblk(u64 n, unsigned t = 256) {
@@ -289,7 +292,13 @@ __global__ void k_em_ubounds(const u32* upos, Batch B, u32* out) {
   if (p <= B.npat) out[p] = upos[B.rbase[p]];
 }
 
+static double wall_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void Engine::ematch_batch(const std::vector<int>& pids_all) {
+  const bool dbg = getenv("TSAT_DEBUG_EMATCH") != nullptr;
+  double w0 = wall_ms();
   if (!snap.valid || snap.n_atoms != h_atoms.size()) build_snapshot();
   for (size_t c0 = 0; c0 < pids_all.size(); c0 += MAX_BATCH) {
     std::vector<int> pids(pids_all.begin() + c0, pids_all.begin() + std::min(pids_all.size(), c0 + MAX_BATCH));
@@ -353,6 +362,15 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
     CUDA_OK(cudaMemcpyAsync(B.rbase, bnd.p, (np + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
     u32 nrows = B.rbase[np];
+    double w1 = wall_ms();
+    if (dbg && ntot) {
+      std::vector<u32> hc(ntot);
+      CUDA_OK(cudaMemcpy(hc.data(), cnt.p, ntot * 4, cudaMemcpyDeviceToHost));
+      u32 mx = 0;
+      for (u32 x : hc) mx = std::max(mx, x);
+      fprintf(stderr, "  max matches per candidate %u\n", mx);
+      w1 = wall_ms();
+    }
     for (int b = 0; b < np; b++) {
       MatchSet& ms = matches[live[b]];
       u32 raw = B.rbase[b + 1] - B.rbase[b];
@@ -389,6 +407,9 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
       u32 nbigrows = 0;
       CUDA_OK(cudaMemcpyAsync(&nbigrows, bpos.p + nrows, sizeof(u32), cudaMemcpyDeviceToHost, s));
       sync();
+      double w2 = wall_ms();
+      if (dbg) fprintf(stderr, "  count+scan %.3f ms, emit+rank %.3f ms\n", w1 - w0, w2 - w1);
+      if (dbg) fprintf(stderr, "  big rows %u (stride %d)\n", nbigrows, stride);
       if (nbigrows) {
         DevBuf<u32>& L = sc.m_L;
         DevBuf<u32>& bh = sc.m_bh;
@@ -423,6 +444,9 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
       sync();
     }
     for (int b = 0; b < np; b++) matches[live[b]].n = nuniq[b + 1] - nuniq[b];
+    if (dbg)
+      fprintf(stderr, "ematch batch: %d patterns, %u candidates, %u rows, %u unique, %.3f ms\n", np, ntot, nrows,
+              nuniq[np], wall_ms() - w0);
     // algorithmic bytes: candidate scan + match rows written,
     // ordered and compacted
     double rows_bytes = 0;

@@ -98,7 +98,6 @@ class _View:
         self.atoms = eg._atom_list
         self._nodes = None
         self._classes = None
-        self._eg = eg
         self.values = None
         if eg.analysis is not None:
             self.values = np.zeros(n, VAL_DTYPE)
@@ -444,7 +443,10 @@ class EGraph:
             memo[key] = out
             return out
 
-        return go(cid, depth_limit)
+        try:
+            return go(cid, depth_limit)
+        finally:
+            go = None  # break the recursive closure's cycle (it references self)
 
     # ---------------------------------------------------------------- costs (cost.py)
     def _device_costs(self, model) -> "CostVector":
@@ -523,6 +525,7 @@ def compile_term(term: Term, atom_id, slot_of) -> list:
         return d + 1
 
     go(term)
+    go = None  # break the closure's self-reference (it holds atom_id, a bound method of the e-graph)
     return prog
 
 
@@ -546,6 +549,7 @@ def _compile_pattern(pat: Term, atom_id) -> list:
         return idx
 
     go(pat)
+    go = None  # see compile_term
     names = sorted(f"v{i}" for i in range(nvars))
     out = [len(apps), nvars] + [int(n[1:]) for n in names]
     for atom, nargs, ch in apps:

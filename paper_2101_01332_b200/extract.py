@@ -58,7 +58,10 @@ def selection_is_acyclic(eg: EGraph, selection: Mapping) -> bool:
         state[c] = 2
         return ok
 
-    return all(visit(c) for c in selection)
+    try:
+        return all(visit(c) for c in selection)
+    finally:
+        visit = None  # break the recursive closure's cycle (it references eg)
 
 
 def greedy_extract(eg: EGraph, costs: Mapping, filt: Iterable[int] = ()) -> ExtractionResult:
@@ -134,6 +137,7 @@ def reconstruct(eg: EGraph, selection: Mapping) -> TensorGraph:
         return name
 
     root_name = build(eg.root)
+    build = None  # break the recursive closure's cycle (it references eg)
 
     def flat(name: str) -> list:
         nd = g.nodes[name]
