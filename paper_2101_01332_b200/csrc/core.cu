@@ -97,7 +97,8 @@ void Engine::reset(bool analysis_) {
   CUDA_OK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
   CUDA_OK(cudaMemsetAsync(tree_hc.p, 0xFF, (size_t)tree_hc_cap * sizeof(u32), s));
   CUDA_OK(cudaMemsetAsync(tree_count.p, 0, sizeof(u32), s));
-  if (hc_cap) CUDA_OK(cudaMemsetAsync(hc.p, 0xFF, (size_t)hc_cap * sizeof(u32), s));
+  if (hc_cap) CUDA_OK(cudaMemsetAsync(hc.p, 0, (size_t)hc_cap * sizeof(unsigned long long), s));
+  hc_epoch = 1;
   root = TSAT_NONE;
   h_atoms.clear();
   atom_names.clear();
@@ -140,6 +141,7 @@ G Engine::view() {
   g.val = val.p;
   g.hc = hc.p;
   g.hc_mask = hc_cap - 1;
+  g.hc_epoch = hc_epoch;
   g.cap_nodes = cap_nodes;
   g.cap_kids = cap_kids;
   g.analysis = analysis ? 1 : 0;
@@ -281,10 +283,19 @@ __global__ void k_hc_insert_alive(G g, u32 n) {
   }
 }
 
+// the next hashcons epoch: an empty table without a clear (a clear every 255)
+void Engine::hc_new_epoch() {
+  if (++hc_epoch > 255) {
+    CUDA_OK(cudaMemsetAsync(hc.p, 0, (size_t)hc_cap * sizeof(unsigned long long), s));
+    hc_epoch = 1;
+  }
+}
+
 void Engine::rehash(u32 new_cap) {
   hc.alloc(new_cap);
   hc_cap = new_cap;
-  CUDA_OK(cudaMemsetAsync(hc.p, 0xFF, (size_t)new_cap * sizeof(u32), s));
+  hc_epoch = 1;
+  CUDA_OK(cudaMemsetAsync(hc.p, 0, (size_t)new_cap * sizeof(unsigned long long), s));
   if (h.next_id) k_hc_insert_alive<<<nblk(h.next_id), 256, 0, s>>>(view(), h.next_id);
 }
 
@@ -618,48 +629,60 @@ std::vector<u32> Engine::get_filter() {
 // key and the partition is the congruence closure, so the result equals the
 // reference's sequential pass (verified by the parity tests).
 
-__global__ void k_canon_kids(G g, u32 n) {
-  GRID_STRIDE(i, n) {
-    if (!(g.flags[i] & NF_ALIVE)) continue;
-    u32 a = g.koff[i], b = g.koff[i + 1];
-    for (u32 j = a; j < b; j++) g.kids[j] = uf_find(g.parent, g.kids[j]);
-  }
+// One congruence round, fused: every live node canonicalises its children
+// against the union-find (writing them back), hashes the canonical key and
+// claims its hashcons slot in the round's fresh epoch.  A node meeting an equal
+// key (fingerprint first, then the other node's children through find()) does
+// atomicMin on the slot: the larger of the two ids is a non-survivor and is
+// dropped and unioned on the spot -- each non-minimum of a key group loses
+// exactly once, the minimum never does, so no second pass is needed.  Unions
+// made during the round only make later keys fresher; the round loop runs to
+// a fixpoint (no union), whose final round leaves exactly the live nodes in
+// the table under their canonical keys.
+__device__ __forceinline__ bool key_eq_canon(const G& g, u32 other, u32 op, u32 a, u32 n) {
+  if (g.op[other] != op) return false;
+  u32 ao = g.koff[other];
+  if (g.koff[other + 1] - ao != n) return false;
+  for (u32 j = 0; j < n; j++)
+    if (uf_find_ro(g.parent, g.kids[ao + j]) != g.kids[a + j]) return false;
+  return true;
 }
 
-__global__ void k_dedup_insert(G g, u32 n) {
+__global__ void k_rebuild_round(G g, u32 lo, u32 n, u32* linked, u32* nlinked, u32* dropped) {
   GRID_STRIDE(i0, n) {
-    u32 i = (u32)i0;
+    u32 i = lo + (u32)i0;
     if (!(g.flags[i] & NF_ALIVE)) continue;
-    u32 slot = (u32)node_hash(g, i) & g.hc_mask;
+    u32 a = g.koff[i], b = g.koff[i + 1];
+    u32 op = g.op[i];
+    u64 h = hash_mix(0x2545f4914f6cdd1dULL ^ ((u64)(b - a) << 32), op);
+    for (u32 j = a; j < b; j++) {
+      u32 k = g.kids[j], c = uf_find(g.parent, k);
+      if (c != k) g.kids[j] = c;
+      h = hash_mix(h, c);
+    }
+    u32 slot = (u32)h & g.hc_mask;
+    u32 tag = hc_tag(g.hc_epoch, h);
+    unsigned long long mine = ((unsigned long long)tag << 32) | i;
+    u32 loser = TSAT_NONE, winner = TSAT_NONE;
     while (true) {
-      u32 cur = ((volatile u32*)g.hc)[slot];
-      if (cur == TSAT_NONE) {
-        u32 prev = atomicCAS(&g.hc[slot], TSAT_NONE, i);
-        if (prev == TSAT_NONE) break;
-        cur = prev;
+      unsigned long long e = ((volatile unsigned long long*)g.hc)[slot];
+      if (!hc_live(g, e)) {
+        if (atomicCAS(&g.hc[slot], e, mine) == e) break;
+        continue;
       }
-      if (node_eq_node(g, cur, i)) {
-        atomicMin(&g.hc[slot], i);
+      if ((u32)(e >> 32) == tag && key_eq_canon(g, (u32)e, op, a, b - a)) {
+        unsigned long long old = atomicMin(&g.hc[slot], mine);
+        u32 o = (u32)old;
+        loser = o > i ? o : i;
+        winner = o > i ? i : o;
         break;
       }
       slot = (slot + 1) & g.hc_mask;
     }
-  }
-}
-
-// drop non-survivors and union them with their survivor; record linked roots
-__global__ void k_dedup_drop(G g, u32 n, u32* linked, u32* nlinked, u32* dropped) {
-  GRID_STRIDE(i0, n) {
-    u32 i = (u32)i0;
-    if (!(g.flags[i] & NF_ALIVE)) continue;
-    u32 a = g.koff[i];
-    int k = (int)(g.koff[i + 1] - a);
-    u32 sv = hc_lookup(g, g.op[i], k, g.kids + a);
-    if (sv == i) continue;
-    g.flags[i] &= ~NF_ALIVE;
+    if (loser == TSAT_NONE) continue;
+    g.flags[loser] &= ~NF_ALIVE;
     atomicAdd(dropped, 1u);
-    // union(find(sv), find(i)) with record of the root that got linked
-    u32 x = sv, y = i;
+    u32 x = winner, y = loser;
     while (true) {
       x = uf_find_ro(g.parent, x);
       y = uf_find_ro(g.parent, y);
@@ -714,12 +737,10 @@ void Engine::rebuild() {
   while (true) {
     {
       // algorithmic bytes of one dirty round: 60 N + 12 A
-      KTimer kt(*this, KG_REBUILD, 60.0 * h.live + 12.0 * h.nkids, 3);
-      k_canon_kids<<<nblk(n), 256, 0, s>>>(view(), n);
-      CUDA_OK(cudaMemsetAsync(hc.p, 0xFF, (size_t)hc_cap * sizeof(u32), s));
-      k_dedup_insert<<<nblk(n), 256, 0, s>>>(view(), n);
+      KTimer kt(*this, KG_REBUILD, 60.0 * h.live + 12.0 * h.nkids, 1);
+      hc_new_epoch();
       CUDA_OK(cudaMemsetAsync(small.p, 0, 2 * sizeof(u32), s));
-      k_dedup_drop<<<nblk(n), 256, 0, s>>>(view(), n, linked.p, small.p, small.p + 1);
+      k_rebuild_round<<<nblk(n), 256, 0, s>>>(view(), 0, n, linked.p, small.p, small.p + 1);
     }
     u32 hm[2];
     CUDA_OK(cudaMemcpyAsync(hm, small.p, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));

@@ -8,8 +8,12 @@
 //   parent[n]  u32  union-find parent; root = class id = min node id
 //   flags[n]   u8   NF_ALIVE | NF_FILT (filter list)
 //   val[n]     Val  analysis of the class rooted at n (valid for roots)
-// Hashcons: open-addressing table of node ids keyed by (op, kids[koff..]).
-// Every live node is in it under its stored key, so keys need no storage.
+// Hashcons: open-addressing table keyed by (op, kids[koff..]); a slot is
+//   (epoch:8 | fingerprint:24) << 32 | node id
+// so a probe compares the key hash's fingerprint before touching the node
+// table, and a new epoch empties the table without clearing it (each
+// congruence round starts a new epoch).  Every live node is in it under its
+// stored key, so keys need no storage.
 #pragma once
 #include "analysis.cuh"
 
@@ -29,8 +33,9 @@ struct G {
   u32* parent;
   u8* flags;
   Val* val;
-  u32* hc;
+  unsigned long long* hc;
   u32 hc_mask;
+  u32 hc_epoch;  // 1..255; slots of other epochs are empty
   u32 cap_nodes;
   u32 cap_kids;
   int analysis;
@@ -71,22 +76,32 @@ __device__ __forceinline__ bool node_eq_node(const G& g, u32 x, u32 y) {
   return true;
 }
 
+__device__ __forceinline__ u32 hc_tag(u32 epoch, u64 h) { return (epoch << 24) | (u32)(h >> 40); }
+__device__ __forceinline__ bool hc_live(const G& g, unsigned long long e) { return (u32)(e >> 56) == g.hc_epoch; }
+
 // hashcons lookup of a (canonical) key; TSAT_NONE on miss
 __device__ __forceinline__ u32 hc_lookup(const G& g, u32 op, int n, const u32* kids) {
-  u32 slot = (u32)key_hash(op, n, kids) & g.hc_mask;
+  u64 h = key_hash(op, n, kids);
+  u32 slot = (u32)h & g.hc_mask, tag = hc_tag(g.hc_epoch, h);
   while (true) {
-    u32 cand = g.hc[slot];
-    if (cand == TSAT_NONE) return TSAT_NONE;
-    if (node_key_eq(g, cand, op, n, kids)) return cand;
+    unsigned long long e = g.hc[slot];
+    if (!hc_live(g, e)) return TSAT_NONE;
+    if ((u32)(e >> 32) == tag && node_key_eq(g, (u32)e, op, n, kids)) return (u32)e;
     slot = (slot + 1) & g.hc_mask;
   }
 }
 
 // insert node id (its key must be absent); lock-free
 __device__ __forceinline__ void hc_insert(const G& g, u32 nid) {
-  u32 slot = (u32)node_hash(g, nid) & g.hc_mask;
+  u64 h = node_hash(g, nid);
+  u32 slot = (u32)h & g.hc_mask;
+  unsigned long long v = ((unsigned long long)hc_tag(g.hc_epoch, h) << 32) | nid;
   while (true) {
-    if (g.hc[slot] == TSAT_NONE && atomicCAS(&g.hc[slot], TSAT_NONE, nid) == TSAT_NONE) return;
+    unsigned long long e = ((volatile unsigned long long*)g.hc)[slot];
+    if (!hc_live(g, e)) {
+      if (atomicCAS(&g.hc[slot], e, v) == e) return;
+      continue;  // re-read the same slot
+    }
     slot = (slot + 1) & g.hc_mask;
   }
 }

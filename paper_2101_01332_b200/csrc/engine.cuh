@@ -246,8 +246,10 @@ struct Engine {
   DevBuf<u8> flags;
   DevBuf<Val> val;
   u32 cap_nodes = 0, cap_kids = 0;
-  DevBuf<u32> hc;
+  DevBuf<unsigned long long> hc;
   u32 hc_cap = 0;
+  u32 hc_epoch = 1;
+  void hc_new_epoch();
 
   // cut trees
   DevBuf<Tree> trees;
