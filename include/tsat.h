@@ -104,6 +104,10 @@ int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, i
 int tsat_ematch(tsat_engine* h, int32_t pattern, uint32_t* out_cls, uint32_t* out_bind, int64_t cap,
                 int64_t* n, int32_t* nb);
 
+/* all patterns of one iteration in one batch (the saturate path); match counts
+ * per pattern, lists stay on the device */
+int tsat_ematch_batch(tsat_engine* h, int32_t npat, const int32_t* pids, int64_t* counts);
+
 /* cycles.break_all_cycles / dfs_get_cycles (cycles.py:172-245) */
 int tsat_break_cycles(tsat_engine* h, int64_t* added);
 int tsat_dfs_cycles(tsat_engine* h, uint32_t* nodes, int64_t cap, uint32_t* off, int64_t off_cap,

@@ -272,6 +272,19 @@ int tsat_ematch(tsat_engine* h, int32_t pattern, uint32_t* out_cls, uint32_t* ou
   });
 }
 
+int tsat_ematch_batch(tsat_engine* h, int32_t npat, const int32_t* pids, int64_t* counts) {
+  GUARD(h, {
+    Engine& e = *h->e;
+    std::vector<int> v;
+    for (int i = 0; i < npat; i++) {
+      if (pids[i] < 0 || pids[i] >= (int)e.patterns.size()) throw TsatException(TSAT_ERR_ARG, "bad pattern id");
+      v.push_back(pids[i]);
+    }
+    e.ematch_batch(v);
+    for (int i = 0; i < npat; i++) counts[i] = e.matches[pids[i]].n;
+  });
+}
+
 int tsat_break_cycles(tsat_engine* h, int64_t* added) {
   GUARD(h, *added = h->e->break_all_cycles(false, nullptr));
 }

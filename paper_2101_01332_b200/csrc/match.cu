@@ -38,6 +38,12 @@ struct PatDev {
   int napps;
   int nb;
   int order[MAX_VARS];
+  // single-app patterns (the common case): binding k = root child src[k];
+  // children eq[i][0] and eq[i][1] must be the same class (repeated variable)
+  int8_t src[MAX_VARS];
+  int8_t fast;  // the single-app plan below is valid
+  int8_t neq;
+  int8_t eq[8][2];
 };
 
 struct SnapDev {
@@ -100,23 +106,50 @@ __device__ __forceinline__ bool bind_node(const G& g, const PatApp& a, u32 nid, 
   return true;
 }
 
+template <int MV>
 __device__ __forceinline__ void unbind(int t, u32* env, int8_t* bound_at) {
-  for (int v = 0; v < MAX_VARS; v++)
+  for (int v = 0; v < MV; v++)
     if (bound_at[v] == t) {
       bound_at[v] = -1;
       env[v] = TSAT_NONE;
     }
 }
 
+__device__ __forceinline__ u32 sel8(const u32* kc, int i) {
+  // register select (no local-memory indexing)
+  u32 v = kc[0];
+#pragma unroll
+  for (int j = 1; j < 8; j++) v = i == j ? kc[j] : v;
+  return v;
+}
+
+// single-app pattern: at most one match per root, state in registers.
+// Counting (EMIT = false) of a pattern without repeated variables only needs
+// the root's op / arity / filter flag.
+template <bool EMIT, class F>
+__device__ __forceinline__ u32 match_root1(const G& g, const PatDev& p, u32 r, F emit) {
+  const PatApp& a = p.apps[0];
+  if (!node_ok(g, r, a)) return 0;
+  if (!EMIT && p.neq == 0) return 1;
+  u32 base = g.koff[r];
+  u32 kc[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) kc[j] = j < a.nargs ? uf_find_ro(g.parent, g.kids[base + j]) : 0u;
+  for (int i = 0; i < p.neq; i++)
+    if (sel8(kc, p.eq[i][0]) != sel8(kc, p.eq[i][1])) return 0;
+  if (EMIT) emit(uf_find_ro(g.parent, r), kc);
+  return 1;
+}
+
 // DFS over the pattern's join for root node r; emit(k, rc, env) per match.
-template <class F>
+template <int MV, int MA, class F>
 __device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const PatDev& p, u32 r, F emit) {
   if (!node_ok(g, r, p.apps[0])) return 0;
-  u32 env[MAX_VARS];
-  int8_t bound_at[MAX_VARS];
-  u32 cls_app[MAX_PAT_APPS];
-  u32 pos[MAX_PAT_APPS], end[MAX_PAT_APPS];
-  for (int v = 0; v < MAX_VARS; v++) {
+  u32 env[MV];
+  int8_t bound_at[MV];
+  u32 cls_app[MA];
+  u32 pos[MA], end[MA];
+  for (int v = 0; v < MV; v++) {
     env[v] = TSAT_NONE;
     bound_at[v] = -1;
   }
@@ -131,7 +164,7 @@ __device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const P
       count++;
       level--;
       if (level == 0) break;
-      unbind(level, env, bound_at);
+      unbind<MV>(level, env, bound_at);
       init = false;
       continue;
     }
@@ -154,7 +187,7 @@ __device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const P
         found = true;
         break;
       }
-      unbind(level, env, bound_at);
+      unbind<MV>(level, env, bound_at);
     }
     if (found) {
       level++;
@@ -162,21 +195,27 @@ __device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const P
     } else {
       level--;
       if (level == 0) break;
-      unbind(level, env, bound_at);
+      unbind<MV>(level, env, bound_at);
       init = false;
     }
   }
   return count;
 }
 
+// MV / MA: DFS state sizes (small instantiation keeps the state in few
+// registers + little local memory; the large one covers any loadable pattern)
+template <int MV, int MA>
 __global__ void k_em_count(G g, SnapDev sd, Batch B, u32 ntot, u32* cnt) {
   GRID_STRIDE(t, ntot) {
     int p = seg_of(B.cbase, B.npat, (u32)t);
     u32 r = sd.op_nodes[B.obase[p] + ((u32)t - B.cbase[p])];
-    cnt[t] = match_root(g, sd, B.pat[p], r, [](u32, u32, const u32*) {});
+    const PatDev& pd = B.pat[p];
+    cnt[t] = pd.fast ? match_root1<false>(g, pd, r, [](u32, const u32*) {})
+                           : match_root<MV, MA>(g, sd, pd, r, [](u32, u32, const u32*) {});
   }
 }
 
+template <int MV, int MA>
 __global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u32* rc, u32* rb) {
   GRID_STRIDE(t, ntot) {
     int p = seg_of(B.cbase, B.npat, (u32)t);
@@ -184,7 +223,14 @@ __global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u3
     u32 r = sd.op_nodes[B.obase[p] + ((u32)t - B.cbase[p])];
     u32 o = off[t];
     const int S = B.stride;
-    match_root(g, sd, pd, r, [&](u32 k, u32 cls, const u32* env) {
+    if (pd.fast) {
+      match_root1<true>(g, pd, r, [&](u32 cls, const u32* kc) {
+        rc[o] = cls;
+        for (int j = 0; j < S; j++) rb[(u64)o * S + j] = j < pd.nb ? sel8(kc, pd.src[j]) : 0u;
+      });
+      continue;
+    }
+    match_root<MV, MA>(g, sd, pd, r, [&](u32 k, u32 cls, const u32* env) {
       rc[o + k] = cls;
       for (int j = 0; j < S; j++) rb[(u64)(o + k) * S + j] = j < pd.nb ? env[pd.order[j]] : 0u;
     });
@@ -305,6 +351,7 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
     Batch B;
     memset(&B, 0, sizeof(B));
     std::vector<int> live;  // patterns with candidates
+    int maxapps = 0;
     u32 ntot = 0;
     int stride = 1;
     double cand_bytes = 0;
@@ -332,6 +379,30 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
       p.nb = hp.nvars;
       for (int i = 0; i < p.napps; i++) p.apps[i] = hp.apps[i];
       for (int k = 0; k < hp.nvars; k++) p.order[k] = hp.order[k];
+      if (p.napps == 1 && p.apps[0].nargs <= 8) {
+        // binding position k <- first root child carrying var order[k]; repeats must agree
+        int first[MAX_VARS];
+        for (int v = 0; v < MAX_VARS; v++) first[v] = -1;
+        bool ok = true;
+        for (int j = 0; j < p.apps[0].nargs && ok; j++) {
+          int v = -p.apps[0].child[j] - 1;
+          if (v < 0 || v >= MAX_VARS) ok = false;
+          else if (first[v] < 0) first[v] = j;
+          else if (p.neq < 8) {
+            p.eq[(int)p.neq][0] = (int8_t)first[v];
+            p.eq[(int)p.neq][1] = (int8_t)j;
+            p.neq++;
+          } else {
+            ok = false;  // too many repeats: general DFS
+          }
+        }
+        for (int k = 0; k < hp.nvars && ok; k++) {
+          if (first[hp.order[k]] < 0) ok = false;
+          else p.src[k] = (int8_t)first[hp.order[k]];
+        }
+        p.fast = ok ? 1 : 0;
+      }
+      if (p.napps > maxapps) maxapps = p.napps;
       B.cbase[b] = ntot;
       B.obase[b] = lo;
       ntot += hi - lo;
@@ -355,7 +426,10 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
     cnt.ensure(ntot + 1);
     off.ensure(ntot + 1);
     bnd.ensure(2 * (MAX_BATCH + 1));
-    k_em_count<<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p);
+    bool small = maxapps <= 4 && stride <= 8;
+    for (int b = 0; b < np; b++) small &= B.pat[b].nb <= 8;
+    if (small) k_em_count<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p);
+    else k_em_count<MAX_VARS, MAX_PAT_APPS><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p);
     CUDA_OK(cudaMemsetAsync(cnt.p + ntot, 0, sizeof(u32), s));
     dev_exclusive_scan_u32(*this, cnt.p, off.p, ntot + 1);
     k_em_bounds<<<1, 32, 0, s>>>(off.p, B, bnd.p);
@@ -399,7 +473,8 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
       bpos.ensure(nrows + 1);
       big.ensure(nrows + 1);
       head.ensure(nrows + 1);
-      k_em_emit<<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p);
+      if (small) k_em_emit<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p);
+      else k_em_emit<MAX_VARS, MAX_PAT_APPS><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p);
       k_em_rank<<<nblk(nrows), 256, 0, s>>>(B, nrows, rc.p, rb.p, scl.p, sbd.p, big.p, head.p);
       // large groups: stable LSD radix sort of their rows by (group, bindings)
       CUDA_OK(cudaMemsetAsync(big.p + nrows, 0, sizeof(u32), s));

@@ -53,10 +53,11 @@ def run(n=1415, reps=3):
         blob, pidx = compile_ruleset(eg, list(default_rules()))
         lib.tsat_load_rules(eg._h, len(blob), blob.ctypes.data_as(C.POINTER(C.c_int64)))
         kstats(lib, eg)
-        cnt = C.c_int64(); nb = C.c_int32(); matched = 0
-        for p in range(len(pidx)):
-            _lib.check(eg._h, lib.tsat_ematch(eg._h, p, None, None, 0, C.byref(cnt), C.byref(nb)))
-            matched += cnt.value
+        pids = np.arange(len(pidx), dtype=np.int32)
+        counts = np.zeros(len(pidx), np.int64)
+        _lib.check(eg._h, lib.tsat_ematch_batch(eg._h, len(pids), pids.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                counts.ctypes.data_as(C.POINTER(C.c_int64))))
+        matched = int(counts.sum())
         em = kstats(lib, eg)["ematch"]
         # (ii) forced full rebuild, then a congruence cascade: w_{2k} ~ w_{2k+1}
         _lib.check(eg._h, lib.tsat_force_rebuild(eg._h))
