@@ -18,6 +18,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cub/cub.cuh>
+
 #include "engine.cuh"
 
 namespace cg = cooperative_groups;
@@ -435,62 +437,6 @@ __global__ void k_greedy_init(double* bc, u32* bn, u32 n) {
   }
 }
 
-// member total (cost + child bests in child order), inf when filtered
-__device__ __forceinline__ double member_total(const G& g, u32 m, const u32* cls_index, const double* cost,
-                                               const double* pc) {
-  if (g.flags[m] & NF_FILT) return NAN;
-  double tot = cost[m];
-  for (u32 j = g.koff[m]; j < g.koff[m + 1]; j++) tot += pc[cls_index[uf_find_ro(g.parent, g.kids[j])]];
-  return tot;
-}
-
-// one warp per class: lanes compute member totals, lane 0 folds them in id
-// order with the reference tie rule (extract.py:145-152)
-__device__ __forceinline__ void warp_fold_class(const G& g, const u32* cls_off, const u32* cls_nodes,
-                                                const u32* cls_index, u32 i, const double* cost, double* bc,
-                                                u32* bn, double* stot, u32 lane) {
-  u32 a = cls_off[i], b = cls_off[i + 1];
-  double c = INFINITY;
-  u32 n = TSAT_NONE;
-  for (u32 base = a; base < b; base += 32) {
-    u32 k = base + lane;
-    double t = k < b ? member_total(g, cls_nodes[k], cls_index, cost, bc) : NAN;
-    stot[lane] = t;
-    __syncwarp();
-    if (lane == 0) {
-      u32 lim = b - base < 32 ? b - base : 32;
-      for (u32 q = 0; q < lim; q++) {
-        double tot = stot[q];
-        if (isnan(tot) || isinf(tot)) continue;
-        u32 m = cls_nodes[base + q];
-        if (tot < c - 1e-15 || (fabs(tot - c) <= 1e-15 && (n == TSAT_NONE || m < n))) {
-          c = tot;
-          n = m;
-        }
-      }
-    }
-    __syncwarp();
-  }
-  if (lane == 0) {
-    bc[i] = c;
-    bn[i] = n;
-  }
-}
-
-// classes in peel order: children are final when a class is folded.
-// Thin levels [l0, l1) in one CTA (a warp per class); a wide level as a grid launch.
-__global__ void __launch_bounds__(1024) k_greedy_levels(G g, const u32* cls_off, const u32* cls_nodes,
-                                                        const u32* cls_index, const u32* order, const u32* lvl_off,
-                                                        u32 l0, u32 l1, const double* cost, double* bc, u32* bn) {
-  __shared__ double stot[32][32];
-  u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (u32 l = l0; l < l1; l++) {
-    for (u32 t = lvl_off[l] + w; t < lvl_off[l + 1]; t += 32)
-      warp_fold_class(g, cls_off, cls_nodes, cls_index, order[t], cost, bc, bn, stot[w], lane);
-    __syncthreads();
-  }
-}
-
 // Greedy over the peel levels of a small class graph in ONE CTA.
 // A prologue lays the trimmed classes' members out in peel order (q index):
 // node id, cost (NaN when filtered) and child classes (the class graph's
@@ -500,6 +446,10 @@ __global__ void __launch_bounds__(1024) k_greedy_levels(G g, const u32* cls_off,
 // members in id order with the reference rule (extract.py:145-152: a member
 // replaces the running best only when cheaper by more than 1e-15; with
 // ascending ids the tie clause never fires).
+__global__ void k_gather_at(const u32* src, const u32* idx, u32 n, u32* out) {
+  GRID_STRIDE(i, n) out[i] = src[idx[i]];
+}
+
 __global__ void k_gq_count(const u32* order, u32 ntr, const u32* cls_off, u32* cnt) {
   GRID_STRIDE(t, ntr) {
     u32 i = order[t];
@@ -507,19 +457,27 @@ __global__ void k_gq_count(const u32* order, u32 ntr, const u32* cls_off, u32* c
   }
 }
 
-__global__ void k_gq_fill(G g, const u32* order, u32 ntr, const u32* cls_off, const u32* cls_nodes, const u32* moff,
-                          const u32* lvm_off, const double* cost, u32* qk, u32* qnode, double* qcost, u32* qdeg) {
+// member-parallel fill: slot_of[q] (the peel-order class slot of member q)
+// comes from a max-scan of the slot heads, so big classes do not serialise
+__global__ void k_gq_heads(const u32* lvm_off, u32 ntr, u32* head) {
   GRID_STRIDE(t, ntr) {
-    u32 i = order[t];
-    u32 q = lvm_off[t];
-    for (u32 k = cls_off[i]; k < cls_off[i + 1]; k++, q++) {
-      u32 m = cls_nodes[k];
-      qk[q] = k;
-      qnode[q] = m;
-      bool f = (g.flags[m] & NF_FILT) != 0;
-      qcost[q] = f ? NAN : cost[m];
-      qdeg[q] = moff[k + 1] - moff[k];
-    }
+    if (lvm_off[t + 1] > lvm_off[t]) head[lvm_off[t]] = (u32)t;
+  }
+}
+
+__global__ void k_gq_fill(G g, const u32* order, u32 nq, const u32* slot_of, const u32* cls_off, const u32* cls_nodes,
+                          const u32* moff, const u32* lvm_off, const double* cost, u32* qk, u32* qnode,
+                          double* qcost, u32* qdeg) {
+  GRID_STRIDE(q0, nq) {
+    u32 q = (u32)q0;
+    u32 t = slot_of[q];
+    u32 k = cls_off[order[t]] + (q - lvm_off[t]);
+    u32 m = cls_nodes[k];
+    qk[q] = k;
+    qnode[q] = m;
+    bool f = (g.flags[m] & NF_FILT) != 0;
+    qcost[q] = f ? NAN : cost[m];
+    qdeg[q] = moff[k + 1] - moff[k];
   }
 }
 
@@ -530,52 +488,71 @@ __global__ void k_gq_edges(u32 nq, const u32* qk, const u32* moff, const u32* ed
   }
 }
 
-__global__ void __launch_bounds__(1024) k_greedy_cta(const u32* order, const u32* lvl_off, u32 nl, u32 ntr,
-                                                     const u32* lvm_off, const u32* qnode, const double* qcost,
-                                                     const u32* qeoff, const u32* qedst, double* qtot, double* bc_g,
-                                                     u32* bn) {
-  extern __shared__ double s_bc[];
-  for (u32 l = 0; l < nl; l++) {
-    u32 a = lvl_off[l], b = lvl_off[l + 1];
-    u32 qa = lvm_off[a], qb = lvm_off[b];
-    for (u32 q = qa + threadIdx.x; q < qb; q += blockDim.x) {
-      double tot = qcost[q];
-      if (!isnan(tot))
-        for (u32 e = qeoff[q], e1 = qeoff[q + 1]; e < e1; e++) tot += s_bc[qedst[e]];
-      qtot[q] = tot;
-    }
-    __syncthreads();
-    for (u32 t = a + threadIdx.x; t < b; t += blockDim.x) {
-      u32 q0 = lvm_off[t], q1 = lvm_off[t + 1];
-      double c = INFINITY;
-      u32 best = TSAT_NONE;
-      for (u32 q = q0; q < q1; q++) {
-        double tot = qtot[q];
-        if (isnan(tot) || isinf(tot)) continue;
-        if (tot < c - 1e-15) {
-          c = tot;
-          best = q;
-        }
-      }
-      u32 i = order[t];
-      s_bc[i] = c;
-      bn[i] = best == TSAT_NONE ? TSAT_NONE : qnode[best];
-    }
-    __syncthreads();
-  }
-  for (u32 t = threadIdx.x; t < ntr; t += blockDim.x) {
-    u32 i = order[t];
-    bc_g[i] = s_bc[i];
+// phase A: member totals (children's best costs); phase B: per-class fold
+__device__ __forceinline__ void gq_totals(u32 qa, u32 qb, u64 tid, u64 nth, const double* qcost, const u32* qeoff,
+                                          const u32* qedst, const double* bc, double* qtot) {
+  for (u64 q = qa + tid; q < qb; q += nth) {
+    double tot = qcost[q];
+    if (!isnan(tot))
+      for (u32 e = qeoff[q], e1 = qeoff[q + 1]; e < e1; e++) tot += bc[qedst[e]];
+    qtot[q] = tot;
   }
 }
 
-__global__ void k_greedy_level_wide(G g, const u32* cls_off, const u32* cls_nodes, const u32* cls_index,
-                                    const u32* order, u32 a, u32 b, const double* cost, double* bc, u32* bn) {
-  __shared__ double stot[8][32];
-  u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
-  for (u64 t = warp; t < b - a; t += nw)
-    warp_fold_class(g, cls_off, cls_nodes, cls_index, order[a + t], cost, bc, bn, stot[w], lane);
+__device__ __forceinline__ void gq_fold(u32 a, u32 b, u64 tid, u64 nth, const u32* order, const u32* lvm_off,
+                                        const u32* qnode, const double* qtot, double* bc, u32* bn) {
+  for (u64 t = a + tid; t < b; t += nth) {
+    u32 q0 = lvm_off[t], q1 = lvm_off[t + 1];
+    double c = INFINITY;
+    u32 best = TSAT_NONE;
+    for (u32 q = q0; q < q1; q++) {
+      double tot = qtot[q];
+      if (isnan(tot) || isinf(tot)) continue;
+      if (tot < c - 1e-15) {
+        c = tot;
+        best = q;
+      }
+    }
+    u32 i = order[t];
+    bc[i] = c;
+    bn[i] = best == TSAT_NONE ? TSAT_NONE : qnode[best];
+  }
+}
+
+// levels [l0, l1) in ONE CTA (thin levels: a barrier per phase instead of a
+// launch); best costs in shared memory when the whole class set fits
+// (``smem``: then this launch covers every level), else in HBM
+__global__ void __launch_bounds__(1024) k_greedy_cta(const u32* order, const u32* lvl_off, u32 l0, u32 l1, u32 ntr,
+                                                     const u32* lvm_off, const u32* qnode, const double* qcost,
+                                                     const u32* qeoff, const u32* qedst, double* qtot, double* bc_g,
+                                                     u32* bn, int smem) {
+  extern __shared__ double s_bc[];
+  double* bc = smem ? s_bc : bc_g;
+  for (u32 l = l0; l < l1; l++) {
+    u32 a = lvl_off[l], b = lvl_off[l + 1];
+    gq_totals(lvm_off[a], lvm_off[b], threadIdx.x, blockDim.x, qcost, qeoff, qedst, bc, qtot);
+    __syncthreads();
+    gq_fold(a, b, threadIdx.x, blockDim.x, order, lvm_off, qnode, qtot, bc, bn);
+    __syncthreads();
+  }
+  if (smem)
+    for (u32 t = threadIdx.x; t < ntr; t += blockDim.x) {
+      u32 i = order[t];
+      bc_g[i] = s_bc[i];
+    }
+}
+
+// one wide level on the whole GPU (two launches: totals, then folds)
+__global__ void k_gq_totals_wide(u32 qa, u32 qb, const double* qcost, const u32* qeoff, const u32* qedst,
+                                 const double* bc, double* qtot) {
+  gq_totals(qa, qb, blockIdx.x * (u64)blockDim.x + threadIdx.x, (u64)gridDim.x * blockDim.x, qcost, qeoff, qedst, bc,
+            qtot);
+}
+
+__global__ void k_gq_fold_wide(u32 a, u32 b, const u32* order, const u32* lvm_off, const u32* qnode,
+                               const double* qtot, double* bc, u32* bn) {
+  gq_fold(a, b, blockIdx.x * (u64)blockDim.x + threadIdx.x, (u64)gridDim.x * blockDim.x, order, lvm_off, qnode, qtot,
+          bc, bn);
 }
 
 // Jacobi round over the classes left on cycles
@@ -674,52 +651,80 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
   G gv = view();
   const u32 *co = snap.cls_off.p, *cn = snap.cls_nodes.p, *ci = snap.cls_index.p, *ord = sc.c_order.p,
             *lvl = sc.c_lvloff.p;
-  const u64 GREEDY_SMEM = 200u << 10;
-  bool cta = (u64)C * sizeof(double) <= GREEDY_SMEM;
-  if (cta) {
-    static int smem_set = 0;
-    if (!smem_set) {
-      CUDA_OK(cudaFuncSetAttribute(k_greedy_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GREEDY_SMEM));
-      smem_set = 1;
-    }
-    Scratch& X = sc;
-    X.gq_lvm.ensure(ntr + 1);
-    X.gq_cnt.ensure(ntr + 1);
-    k_gq_count<<<nblk(ntr), 256, 0, s>>>(ord, ntr, co, X.gq_cnt.p);
-    CUDA_OK(cudaMemsetAsync(X.gq_cnt.p + ntr, 0, sizeof(u32), s));
-    dev_exclusive_scan_u32(*this, X.gq_cnt.p, X.gq_lvm.p, ntr + 1);
-    u32 nq = 0;
-    CUDA_OK(cudaMemcpyAsync(&nq, X.gq_lvm.p + ntr, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  // peel-order member layout (q index): node, cost (NaN when filtered), child classes
+  Scratch& X = sc;
+  X.gq_lvm.ensure(ntr + 1);
+  X.gq_cnt.ensure(ntr + 1);
+  k_gq_count<<<nblk(ntr), 256, 0, s>>>(ord, ntr, co, X.gq_cnt.p);
+  CUDA_OK(cudaMemsetAsync(X.gq_cnt.p + ntr, 0, sizeof(u32), s));
+  dev_exclusive_scan_u32(*this, X.gq_cnt.p, X.gq_lvm.p, ntr + 1);
+  std::vector<u32> lvm(nl + 1);
+  {
+    // member offsets at level boundaries (host: picks thin runs / wide levels)
+    DevBuf<u32>& lb = X.gq_lb;
+    lb.ensure(nl + 1);
+    k_gather_at<<<nblk(nl + 1), 256, 0, s>>>(X.gq_lvm.p, lvl, nl + 1, lb.p);
+    CUDA_OK(cudaMemcpyAsync(lvm.data(), lb.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
-    X.gq_k.ensure(nq + 1);
-    X.gq_node.ensure(nq + 1);
-    X.gq_cost.ensure(nq + 1);
-    X.gq_tot.ensure(nq + 1);
-    X.gq_deg.ensure(nq + 1);
-    X.gq_eoff.ensure(nq + 1);
-    k_gq_fill<<<nblk(ntr), 256, 0, s>>>(gv, ord, ntr, co, cn, sc.cg_moff.p, X.gq_lvm.p, cost, X.gq_k.p, X.gq_node.p,
-                                        X.gq_cost.p, X.gq_deg.p);
-    CUDA_OK(cudaMemsetAsync(X.gq_deg.p + nq, 0, sizeof(u32), s));
-    dev_exclusive_scan_u32(*this, X.gq_deg.p, X.gq_eoff.p, nq + 1);
-    X.gq_edst.ensure((u64)cg_ne + 1);
-    k_gq_edges<<<nblk(nq), 256, 0, s>>>(nq, X.gq_k.p, sc.cg_moff.p, sc.cg_edst.p, X.gq_eoff.p, X.gq_edst.p);
-    k_greedy_cta<<<1, 1024, (size_t)C * sizeof(double), s>>>(ord, lvl, nl, ntr, X.gq_lvm.p, X.gq_node.p,
-                                                              X.gq_cost.p, X.gq_eoff.p, X.gq_edst.p, X.gq_tot.p, c0.p,
-                                                              n0.p);
-    CUDA_OK(cudaGetLastError());
   }
-  for (u32 l = 0; l < nl && !cta;) {
-    if (lo[l + 1] - lo[l] > 64) {
-      k_greedy_level_wide<<<nblk((u64)(lo[l + 1] - lo[l]) * 32, 256), 256, 0, s>>>(gv, co, cn, ci, ord, lo[l],
-                                                                                    lo[l + 1], cost, c0.p, n0.p);
-      l++;
-      continue;
+  u32 nq = lvm[nl];
+  X.gq_k.ensure(nq + 1);
+  X.gq_node.ensure(nq + 1);
+  X.gq_cost.ensure(nq + 1);
+  X.gq_tot.ensure(nq + 1);
+  X.gq_deg.ensure(nq + 1);
+  X.gq_eoff.ensure(nq + 1);
+  {
+    DevBuf<u32>& head = X.gq_head;
+    DevBuf<u32>& slot = X.gq_slot;
+    head.ensure(nq + 1);
+    slot.ensure(nq + 1);
+    CUDA_OK(cudaMemsetAsync(head.p, 0, (nq + 1) * sizeof(u32), s));
+    k_gq_heads<<<nblk(ntr), 256, 0, s>>>(X.gq_lvm.p, ntr, head.p);
+    if (nq) {
+      size_t bytes = 0;
+      CUDA_OK(cub::DeviceScan::InclusiveScan(nullptr, bytes, head.p, slot.p, cuda::maximum<>{}, nq, s));
+      temp.ensure(bytes + 16);
+      CUDA_OK(cub::DeviceScan::InclusiveScan(temp.p, bytes, head.p, slot.p, cuda::maximum<>{}, nq, s));
     }
-    u32 l1 = l;
-    while (l1 < nl && lo[l1 + 1] - lo[l1] <= 64) l1++;
-    k_greedy_levels<<<1, 1024, 0, s>>>(gv, co, cn, ci, ord, lvl, l, l1, cost, c0.p, n0.p);
-    l = l1;
+    k_gq_fill<<<nblk(nq), 256, 0, s>>>(gv, ord, nq, slot.p, co, cn, sc.cg_moff.p, X.gq_lvm.p, cost, X.gq_k.p,
+                                       X.gq_node.p, X.gq_cost.p, X.gq_deg.p);
   }
+  CUDA_OK(cudaMemsetAsync(X.gq_deg.p + nq, 0, sizeof(u32), s));
+  dev_exclusive_scan_u32(*this, X.gq_deg.p, X.gq_eoff.p, nq + 1);
+  X.gq_edst.ensure((u64)cg_ne + 1);
+  k_gq_edges<<<nblk(nq), 256, 0, s>>>(nq, X.gq_k.p, sc.cg_moff.p, sc.cg_edst.p, X.gq_eoff.p, X.gq_edst.p);
+  const u64 GREEDY_SMEM = 200u << 10;
+  static int smem_set = 0;
+  if (!smem_set) {
+    CUDA_OK(cudaFuncSetAttribute(k_greedy_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GREEDY_SMEM));
+    smem_set = 1;
+  }
+  if ((u64)C * sizeof(double) <= GREEDY_SMEM) {
+    k_greedy_cta<<<1, 1024, (size_t)C * sizeof(double), s>>>(ord, lvl, 0, nl, ntr, X.gq_lvm.p, X.gq_node.p,
+                                                              X.gq_cost.p, X.gq_eoff.p, X.gq_edst.p, X.gq_tot.p, c0.p,
+                                                              n0.p, 1);
+  } else {
+    // thin runs in one CTA, wide levels (> WIDE members or classes) on the grid
+    const u32 WIDE = 8192;
+    for (u32 l = 0; l < nl;) {
+      u32 wm = lvm[l + 1] - lvm[l], wc = lo[l + 1] - lo[l];
+      if (wm > WIDE || wc > WIDE) {
+        k_gq_totals_wide<<<nblk(wm), 256, 0, s>>>(lvm[l], lvm[l + 1], X.gq_cost.p, X.gq_eoff.p, X.gq_edst.p, c0.p,
+                                                   X.gq_tot.p);
+        k_gq_fold_wide<<<nblk(wc), 256, 0, s>>>(lo[l], lo[l + 1], ord, X.gq_lvm.p, X.gq_node.p, X.gq_tot.p, c0.p,
+                                                n0.p);
+        l++;
+        continue;
+      }
+      u32 l1 = l;
+      while (l1 < nl && lvm[l1 + 1] - lvm[l1] <= WIDE && lo[l1 + 1] - lo[l1] <= WIDE) l1++;
+      k_greedy_cta<<<1, 1024, 0, s>>>(ord, lvl, l, l1, ntr, X.gq_lvm.p, X.gq_node.p, X.gq_cost.p, X.gq_eoff.p,
+                                      X.gq_edst.p, X.gq_tot.p, c0.p, n0.p, 0);
+      l = l1;
+    }
+  }
+  CUDA_OK(cudaGetLastError());
   i64 r = 1;
   if (ntr < C) {
     DevBuf<u32>& rest = sc.c_rest;

@@ -195,16 +195,30 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
           u32 nd = 0, na = 0, nb = 0;
           for (u32 k = 0; k < md; k++) {
             u32 v = TSAT_NONE, va = 0, vb = 0;
+            // warp mode: this warp is the only writer of deg[], so plain
+            // loads / stores with lanes of equal targets combined by
+            // __match_any_sync replace the L2 atomics (one round trip less
+            // per level on long chains)
+            u32 tgt = TSAT_NONE;
             if (a + k < b) {
               u32 e = a + k;
+              tgt = F.bfs ? F.edst[e] : F.rsrc[e];
+              if (!F.bfs && F.mask && !F.mask[tgt]) tgt = TSAT_NONE;
+            }
+            unsigned same = __match_any_sync(0xffffffffu, tgt);
+            bool leader = tgt != TSAT_NONE && (u32)(__ffs(same) - 1) == lane;
+            if (leader) {
               if (F.bfs) {
-                u32 x = F.edst[e];
-                if (deg[x] == 0 && atomicCAS(&deg[x], 0u, 1u) == 0u) v = x;
+                if (deg[tgt] == 0) {
+                  deg[tgt] = 1;
+                  v = tgt;
+                }
               } else {
-                u32 i = F.rsrc[e];
-                if ((!F.mask || F.mask[i]) && atomicSub(&deg[i], 1u) == 1u) {
-                  F.level[i] = lv + 1;
-                  v = i;
+                u32 dd = deg[tgt], dec = (u32)__popc(same);
+                deg[tgt] = dd - dec;
+                if (dd == dec) {
+                  F.level[tgt] = lv + 1;
+                  v = tgt;
                 }
               }
             }
