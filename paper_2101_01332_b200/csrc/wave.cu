@@ -1153,6 +1153,42 @@ static void build_wave_rule(const HRule& hr, std::vector<ReqT>& tm, WaveRule& W,
       W.root_var[t] = -top - 1;
     }
   }
+  // Shared inner subterms (e.g. the split / matmul / concat_2 that both
+  // targets of a merge rule contain) are ONE request: sequentially, the second
+  // target's add_term hits the node the first one created, so resolving it
+  // once is the same.  Target roots are never merged (a later reuse of a root
+  // sees its merged class -- the wave's hazard path handles that case).
+  {
+    const int R0 = (int)tm.size();
+    std::vector<int> canon(R0), newidx(R0, -1);
+    for (int r = 0; r < R0; r++) {
+      for (int j = 0; j < tm[r].nargs; j++)
+        if (tm[r].kid[j] >= 0) tm[r].kid[j] = canon[tm[r].kid[j]];
+      canon[r] = r;
+      if (tm[r].is_root) continue;
+      for (int q = 0; q < r; q++) {
+        if (tm[q].is_root || canon[q] != q || tm[q].atom != tm[r].atom || tm[q].nargs != tm[r].nargs) continue;
+        bool same = true;
+        for (int j = 0; j < tm[r].nargs && same; j++) same = tm[q].kid[j] == tm[r].kid[j];
+        if (same) {
+          canon[r] = q;
+          break;
+        }
+      }
+    }
+    std::vector<ReqT> uq;
+    for (int r = 0; r < R0; r++)
+      if (canon[r] == r) {
+        newidx[r] = (int)uq.size();
+        uq.push_back(tm[r]);
+      }
+    for (auto& q : uq)
+      for (int j = 0; j < q.nargs; j++)
+        if (q.kid[j] >= 0) q.kid[j] = newidx[q.kid[j]];
+    for (int t = 0; t < hr.nsrc; t++)
+      if (W.root_req[t] >= 0) W.root_req[t] = newidx[W.root_req[t]];
+    tm.swap(uq);
+  }
   R = (int)tm.size();
   W.R = R;
   lv.assign(maxd + 1, {});
