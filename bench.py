@@ -185,6 +185,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--workload", default="bert", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] 10M-node kernel sweep")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: the ranks explore ONE graph together, e-matching split by e-class range "
                          "with an NCCL all-gather of the match lists (SURVEY 8(e)); default: one graph per GPU")
@@ -334,11 +335,31 @@ def main():
         starts = [n0] + rep.enodes_per_iter[:-1]
         tested = sum(n * (len(pats_all) if i < w["k_multi"] else len(pats_single)) for i, n in enumerate(starts))
         line["enodes_matched_per_s"] = tested / (em_ms / 1e3)
-    if w["model"] == "synth10m" and rank == 0:
+    if rank == 0 and (w["model"] == "synth10m" or not args.no_sweep):
+        # configs[4] kernel sweep on the 10M-node e-graph: the north star's
+        # roofline targets (e-matching and rebuild vs HBM), with the ncu DRAM
+        # traffic of the same kernels from the committed captures (profiles/)
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         import synth_sweep
 
-        line["sweep"] = synth_sweep.run(1415, reps=2)
+        sw = synth_sweep.run(1415, reps=3)
+        if w["model"] == "synth10m":
+            line["sweep"] = sw
+        else:
+            ncu = {}
+            try:
+                ncu = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+            except Exception:
+                pass
+            line["config5_kernels"] = {
+                k: {"ms": round(sw[k]["ms"], 4), "algorithmic_GB": round(sw[k]["bytes"] / 1e9, 4),
+                    "achieved_GBps": round(sw[k]["GBps"], 1), "frac": round(sw[k]["frac"], 4),
+                    "ncu_dram_GB_per_launch": ncu.get(k, {}).get("dram_GB"),
+                    "ncu_dram_GBps": ncu.get(k, {}).get("dram_GBps")}
+                for k in ("ematch_13", "rebuild_forced", "rebuild_cascade", "costs", "greedy", "apply_wave") if k in sw}
+            line["config5_kernels"]["graph"] = {"nodes": sw["nodes"], "classes": sw["classes"],
+                                                "peak_GBps": sw["peak_GBps"],
+                                                "enodes_matched_per_s": sw["enodes_matched_per_s"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         t_cpu, n_cpu, total_cpu = run_oracle_once(args.workload)
         if "sample_n" in w:

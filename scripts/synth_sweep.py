@@ -79,7 +79,7 @@ def run(n=1415, reps=3):
                     best[k] = v
             else:
                 out[k] = v
-        del eg
+        del eg, costs, res, filt
     for k, v in best.items():
         v["GBps"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else 0.0
         v["frac"] = v["GBps"] / peak
