@@ -261,8 +261,15 @@ __device__ __forceinline__ int conv_out(i64 h, i64 w, i64 kh, i64 kw, i64 sh, i6
 
 // ---------------------------------------------------------------- infer_shape
 
+// Argument values by reference: an array of pointers into the node table /
+// wave table (no 128-byte copies into local memory).
+struct ValRefs {
+  const Val* const* p;
+  __device__ __forceinline__ const Val& operator[](int i) const { return *p[i]; }
+};
+
 // Output value of operator ``op`` for argument values ``a`` (n of them).
-static __device__ int infer_shape_dev(int op, const Val* a, int n, Val& out, const AtomInfo* atoms,
+static __device__ int infer_shape_dev(int op, ValRefs a, int n, Val& out, const AtomInfo* atoms,
                                const TreeTab& tt) {
   if (op < 0 || op >= OP_COUNT) return AS_SHAPE;
   if (n != c_sig_n[op]) return AS_SHAPE;
@@ -379,7 +386,7 @@ static __device__ int infer_shape_dev(int op, const Val* a, int n, Val& out, con
     case OP_CONCAT5:
     case OP_CONCAT6: {
       int k = n - 1;
-      const Val* in = a + 1;
+      ValRefs in{a.p + 1};
       int r = in[0].r0;
       i64 axis = a[0].iv;
       if (!in_range(axis, 0, r - 1)) return AS_SHAPE;
@@ -503,7 +510,7 @@ static __device__ int infer_shape_dev(int op, const Val* a, int n, Val& out, con
 }
 
 // TensorAnalysis.make (tensor_lang.py:734-743)
-__device__ __forceinline__ int val_make(u32 atom, const Val* kids, int n, Val& out,
+__device__ __forceinline__ int val_make(u32 atom, ValRefs kids, int n, Val& out,
                                         const AtomInfo* atoms, const TreeTab& tt) {
   const AtomInfo& ai = atoms[atom];
   if (n == 0) {

@@ -381,14 +381,14 @@ __global__ void k_init_nodes(G g, u32 n) {
 __device__ __forceinline__ void make_one(const G& g, u32 nid) {
   u32 a = g.koff[nid], b = g.koff[nid + 1];
   int k = (int)(b - a);
-  Val kv[7];
+  const Val* kv[8];
   if (k > 7) {
     dev_set_error(g.err, TSAT_ERR_SHAPE, 3, nid, g.op[nid]);
     return;
   }
-  for (int j = 0; j < k; j++) kv[j] = g.val[g.kids[a + j]];
+  for (int j = 0; j < k; j++) kv[j] = &g.val[g.kids[a + j]];
   Val v;
-  int st = val_make(g.op[nid], kv, k, v, g.atoms, g.tt);
+  int st = val_make(g.op[nid], ValRefs{kv}, k, v, g.atoms, g.tt);
   if (st != AS_OK) {
     dev_set_error(g.err, ana_to_status(st), 3, nid, g.op[nid]);
     return;
@@ -410,14 +410,14 @@ __global__ void k_make_level(G g, const u32* ids, u32 n) {
     u32 nid = ids[t];
     u32 a = g.koff[nid], b = g.koff[nid + 1];
     int k = (int)(b - a);
-    Val kv[7];
+    const Val* kv[8];
     if (k > 7) {
       dev_set_error(g.err, TSAT_ERR_SHAPE, 3, nid, g.op[nid]);
       continue;
     }
-    for (int j = 0; j < k; j++) kv[j] = g.val[g.kids[a + j]];
+    for (int j = 0; j < k; j++) kv[j] = &g.val[g.kids[a + j]];
     Val v;
-    int st = val_make(g.op[nid], kv, k, v, g.atoms, g.tt);
+    int st = val_make(g.op[nid], ValRefs{kv}, k, v, g.atoms, g.tt);
     if (st != AS_OK) {
       dev_set_error(g.err, ana_to_status(st), 3, nid, g.op[nid]);
       continue;

@@ -129,9 +129,9 @@ static __device__ u32 seq_add_enode(const G& g, u32 op, u32* kids, int n) {
   u32 nid = c->next_id;
   Val v;
   if (g.analysis) {
-    Val kv[7];
-    for (int i = 0; i < n && i < 7; i++) kv[i] = g.val[kids[i]];
-    int st = n > 7 ? AS_SHAPE : val_make(op, kv, n, v, g.atoms, g.tt);
+    const Val* kv[8];
+    for (int i = 0; i < n && i < 8; i++) kv[i] = &g.val[kids[i]];
+    int st = n > 7 ? AS_SHAPE : val_make(op, ValRefs{kv}, n, v, g.atoms, g.tt);
     if (st != AS_OK) {
       c->next_id = nid + 1;  // the reference bumps the counter before make()
       dev_set_error(g.err, ana_to_status(st), 1, nid, op);

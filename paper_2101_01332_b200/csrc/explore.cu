@@ -209,15 +209,16 @@ __global__ void k_seq_rule(G g, RuleDev R, ReachDev RD, DevStats* st, unsigned l
     // shape check (rules.py:141-156)
     if (g.analysis) {
       bool ok = true;
+      Val scratch[MAX_STACK];
       for (int t = 0; t < R.nsrc && ok; t++) {
-        Val out;
-        int s = eval_target(g, R.instr + R.tgt_off[t], R.tgt_len[t], env, out);
+        const Val* outp = nullptr;
+        int s = eval_target(g, R.instr + R.tgt_off[t], R.tgt_len[t], env, scratch, outp);
         if (s == AS_ORIGIN_OVERFLOW || s == AS_TREE_FULL) {
           dev_set_error(g.err, TSAT_ERR_CAPACITY, 10 + s, (i64)p, t);
           return;
         }
         if (s != AS_OK) ok = false;
-        else ok = val_same_data(out, g.val[uf_find(g.parent, R.mcls[t][idx[t]])]);
+        else ok = val_same_data(*outp, g.val[uf_find(g.parent, R.mcls[t][idx[t]])]);
       }
       if (!ok) {
         st->skipped_shape++;

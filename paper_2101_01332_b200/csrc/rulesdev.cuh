@@ -39,23 +39,27 @@ __device__ __forceinline__ void decode_pos(const RuleDev& R, unsigned long long 
   }
 }
 
-// eval_pattern of one target under env (reference rules.py:126-138)
-static __device__ int eval_target(const G& g, const Instr* ins, int len, const u32* env, Val& out) {
-  Val st[MAX_STACK];
-  int sp = 0;
+// eval_pattern of one target under env (reference rules.py:126-138).
+// Variables are referenced in place (node-table analyses); only the results of
+// the target's App nodes are materialised, in ``scratch`` (MAX_STACK entries).
+// *outp points at the target's value (a node-table entry for a bare variable).
+static __device__ int eval_target(const G& g, const Instr* ins, int len, const u32* env, Val* scratch,
+                                  const Val*& outp) {
+  const Val* st[MAX_STACK];
+  int sp = 0, nr = 0;
   for (int k = 0; k < len; k++) {
     const Instr& in = ins[k];
     if (in.kind == I_VAR) {
-      st[sp++] = g.val[uf_find_ro(g.parent, env[in.arg])];
+      st[sp++] = &g.val[uf_find_ro(g.parent, env[in.arg])];
     } else {
       int na = in.arg;
       sp -= na;
-      Val r;
-      int s = val_make(in.atom, st + sp, na, r, g.atoms, g.tt);
+      Val& r = scratch[nr++];
+      int s = val_make(in.atom, ValRefs{st + sp}, na, r, g.atoms, g.tt);
       if (s != AS_OK) return s;
-      st[sp++] = r;
+      st[sp++] = &r;
     }
   }
-  out = st[0];
+  outp = st[0];
   return AS_OK;
 }

@@ -193,14 +193,15 @@ __device__ __forceinline__ void d_gates(u64 tid, u64 nth, const G& g, const Rule
     for (int t = 0; t < R.nsrc; t++) olds[t] = uf_find_rw(g.parent, R.mcls[t][idx[t]]);
     u8 st = 0, hz = 0;
     if (g.analysis) {
+      Val scratch[MAX_STACK];
       for (int t = 0; t < R.nsrc && st == 0; t++) {
-        Val out;
-        int s = eval_target(g, R.instr + R.tgt_off[t], R.tgt_len[t], env, out);
+        const Val* out = nullptr;
+        int s = eval_target(g, R.instr + R.tgt_off[t], R.tgt_len[t], env, scratch, out);
         if (s == AS_ORIGIN_OVERFLOW || s == AS_TREE_FULL) {
           hz = 1;
           break;
         }
-        if (s != AS_OK || !val_same_data(out, g.val[olds[t]])) st = 1;
+        if (s != AS_OK || !val_same_data(*out, g.val[olds[t]])) st = 1;
       }
     }
     if (st == 0 && !hz && R.efficient) {
@@ -297,10 +298,10 @@ __device__ __forceinline__ void d_resolve_level(u64 tid, u64 nth, const G& g, co
     atomicMin(&T.minpos[s], mp_tag(T.epoch, gpos));
     ident[gpos] = FRESH | s;
     if (g.analysis) {
-      Val kv[8];
-      for (int j = 0; j < q.nargs; j++) kv[j] = (kids[j] & FRESH) ? T.val[kids[j] & ~FRESH] : g.val[kids[j]];
+      const Val* kv[8];
+      for (int j = 0; j < q.nargs; j++) kv[j] = (kids[j] & FRESH) ? &T.val[kids[j] & ~FRESH] : &g.val[kids[j]];
       Val v;
-      int st = val_make(q.atom, kv, q.nargs, v, g.atoms, g.tt);
+      int st = val_make(q.atom, ValRefs{kv}, q.nargs, v, g.atoms, g.tt);
       if (st != AS_OK) {
         hazard[c] = 2;
         continue;
