@@ -75,6 +75,7 @@ int tsat_rebuild(tsat_engine* h);                                            /* 
 int tsat_force_rebuild(tsat_engine* h);
 int tsat_union_batch(tsat_engine* h, int64_t n, const uint32_t* a, const uint32_t* b);
 int tsat_find(tsat_engine* h, uint32_t x, uint32_t* out);                    /* egraph.py:143 */
+int tsat_find_batch(tsat_engine* h, uint32_t n, const uint32_t* ids, uint32_t* out); /* many finds, one sync */
 int tsat_set_root(tsat_engine* h, uint32_t root);                            /* EGraph.root   */
 
 /* sizes + SoA download (EGraph.nodes / classes / dump, egraph.py:127-162, 334-349) */
@@ -84,6 +85,11 @@ int tsat_num_classes(tsat_engine* h, uint32_t* out);
 int tsat_download_flags(tsat_engine* h, uint8_t* flags);
 int tsat_download(tsat_engine* h, uint32_t* op, uint32_t* child_off, uint32_t* child,
                   uint32_t* cls, uint8_t* flags);
+/* selected nodes only (extract.reconstruct, extract.py:584-639): ops, child
+ * offsets (n+1) and canonical children; *nchild > child_cap means retry with a
+ * larger buffer */
+int tsat_download_nodes(tsat_engine* h, uint32_t n, const uint32_t* ids, uint32_t* op, uint32_t* child_off,
+                        uint32_t* child, uint64_t child_cap, uint64_t* nchild);
 int tsat_download_values(tsat_engine* h, void* vals, int64_t val_bytes, void* trees,
                          int64_t tree_bytes, uint32_t* ntrees);
 int tsat_dump(tsat_engine* h, char* buf, int64_t cap, int64_t* len);

@@ -53,6 +53,9 @@ _SIGS = {
     "tsat_num_classes": ([C.c_void_p, u32p], C.c_int),
     "tsat_download_flags": ([C.c_void_p, u8p], C.c_int),
     "tsat_download": ([C.c_void_p, u32p, u32p, u32p, u32p, u8p], C.c_int),
+    "tsat_find_batch": ([C.c_void_p, C.c_uint32, u32p, u32p], C.c_int),
+    "tsat_download_nodes": ([C.c_void_p, C.c_uint32, u32p, u32p, u32p, u32p, C.c_uint64,
+                             C.POINTER(C.c_uint64)], C.c_int),
     "tsat_download_values": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, u32p], C.c_int),
     "tsat_dump": ([C.c_void_p, C.c_char_p, C.c_int64, i64p], C.c_int),
     "tsat_set_filter": ([C.c_void_p, C.c_int32, u32p, C.c_int32], C.c_int),

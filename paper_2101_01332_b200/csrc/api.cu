@@ -173,6 +173,15 @@ int tsat_download(tsat_engine* h, uint32_t* op, uint32_t* child_off, uint32_t* c
   GUARD(h, h->e->download(op, child_off, child, cls, flags));
 }
 
+int tsat_find_batch(tsat_engine* h, uint32_t n, const uint32_t* ids, uint32_t* out) {
+  GUARD(h, h->e->find_batch(n, ids, out));
+}
+
+int tsat_download_nodes(tsat_engine* h, uint32_t n, const uint32_t* ids, uint32_t* op, uint32_t* child_off,
+                        uint32_t* child, uint64_t child_cap, uint64_t* nchild) {
+  GUARD(h, h->e->download_nodes(n, ids, op, child_off, child, child_cap, nchild));
+}
+
 int tsat_download_values(tsat_engine* h, void* vals, int64_t val_bytes, void* trees, int64_t tree_bytes,
                          uint32_t* ntrees) {
   GUARD(h, {

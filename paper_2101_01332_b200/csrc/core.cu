@@ -877,6 +877,67 @@ void Engine::build_snapshot() {
 
 // ---------------------------------------------------------------- download / dump
 
+// selected nodes only (reconstruct): op, arity prefix, canonical children
+__global__ void k_sub_arity(G g, const u32* ids, u32 n, u32* op_out, u32* deg) {
+  GRID_STRIDE(i, n) {
+    u32 x = ids[i];
+    op_out[i] = g.op[x];
+    deg[i] = g.koff[x + 1] - g.koff[x];
+  }
+}
+
+__global__ void k_sub_kids(G g, const u32* ids, u32 n, const u32* off, u32* kids_out) {
+  GRID_STRIDE(i, n) {
+    u32 x = ids[i], a = g.koff[x], b = g.koff[x + 1], o = off[i];
+    for (u32 j = a; j < b; j++) kids_out[o++] = uf_find_ro(g.parent, g.kids[j]);
+  }
+}
+
+__global__ void k_find_batch(G g, const u32* ids, u32 n, u32* out) {
+  GRID_STRIDE(i, n) out[i] = uf_find_ro(g.parent, ids[i]);
+}
+
+void Engine::find_batch(u32 n, const u32* ids, u32* out) {
+  for (u32 i = 0; i < n; i++)
+    if (ids[i] >= h.next_id) throw TsatException(TSAT_ERR_ARG, "node id out of range");
+  DevBuf<u32>& di = scratch_u32[0];
+  DevBuf<u32>& dout = scratch_u32[1];
+  di.ensure(n + 1);
+  dout.ensure(n + 1);
+  if (!n) return;
+  CUDA_OK(cudaMemcpyAsync(di.p, ids, n * sizeof(u32), cudaMemcpyHostToDevice, s));
+  k_find_batch<<<nblk(n), 256, 0, s>>>(view(), di.p, n, dout.p);
+  CUDA_OK(cudaMemcpyAsync(out, dout.p, n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
+}
+
+void Engine::download_nodes(u32 n, const u32* ids, u32* hop, u32* hoff, u32* hkids, u64 kids_cap, u64* nkids) {
+  for (u32 i = 0; i < n; i++)
+    if (ids[i] >= h.next_id) throw TsatException(TSAT_ERR_ARG, "node id out of range");
+  DevBuf<u32>& di = scratch_u32[0];
+  DevBuf<u32>& dop = scratch_u32[1];
+  DevBuf<u32>& ddeg = scratch_u32[2];
+  DevBuf<u32>& doff = scratch_u32[3];
+  DevBuf<u32>& dk = scratch_u32[4];
+  di.ensure(n + 1);
+  dop.ensure(n + 1);
+  ddeg.ensure(n + 1);
+  doff.ensure(n + 1);
+  if (n) CUDA_OK(cudaMemcpyAsync(di.p, ids, n * sizeof(u32), cudaMemcpyHostToDevice, s));
+  k_sub_arity<<<nblk(n), 256, 0, s>>>(view(), di.p, n, dop.p, ddeg.p);
+  CUDA_OK(cudaMemsetAsync(ddeg.p + n, 0, sizeof(u32), s));
+  dev_exclusive_scan_u32(*this, ddeg.p, doff.p, n + 1);
+  CUDA_OK(cudaMemcpyAsync(hoff, doff.p, (n + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  if (n) CUDA_OK(cudaMemcpyAsync(hop, dop.p, n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
+  *nkids = hoff[n];
+  if (hoff[n] > kids_cap) return;  // caller retries with a larger buffer
+  dk.ensure((u64)hoff[n] + 1);
+  k_sub_kids<<<nblk(n), 256, 0, s>>>(view(), di.p, n, doff.p, dk.p);
+  if (hoff[n]) CUDA_OK(cudaMemcpyAsync(hkids, dk.p, (u64)hoff[n] * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
+}
+
 void Engine::download(u32* hop, u32* hkoff, u32* hkids, u32* hcls, u8* hflags) {
   u32 n = h.next_id;
   std::vector<u32> par(n);

@@ -361,6 +361,8 @@ struct Engine {
 
   // download
   void download(u32* op, u32* koff, u32* kids, u32* cls, u8* flags);
+  void download_nodes(u32 n, const u32* ids, u32* op, u32* off, u32* kids, u64 kids_cap, u64* nkids);
+  void find_batch(u32 n, const u32* ids, u32* out);
   std::string dump_text();
   std::string value_str(u32 cls);
 };

@@ -94,6 +94,28 @@ def greedy_extract(eg: EGraph, costs: Mapping, filt: Iterable[int] = ()) -> Extr
     return ExtractionResult(selection, total, stats=stats)
 
 
+def _selected_nodes(eg: EGraph, ids) -> dict:
+    """(op atom, canonical children) of the selected e-nodes only: one gather on
+    the device instead of materialising the whole e-graph."""
+    lib = _lib.load()
+    ids = np.array(sorted(set(int(x) for x in ids)), np.uint32)
+    n = len(ids)
+    op = np.zeros(max(n, 1), np.uint32)
+    off = np.zeros(n + 1, np.uint32)
+    cap = max(4 * n, 16)
+    while True:
+        kids = np.zeros(cap, np.uint32)
+        nk = C.c_uint64()
+        _lib.check(eg._h, lib.tsat_download_nodes(eg._h, n, _lib.ptr(ids, C.c_uint32), _lib.ptr(op, C.c_uint32),
+                                                  _lib.ptr(off, C.c_uint32), _lib.ptr(kids, C.c_uint32), cap,
+                                                  C.byref(nk)))
+        if nk.value <= cap:
+            break
+        cap = int(nk.value)
+    atoms = eg._atom_list
+    return {int(x): (atoms[int(op[i])], tuple(int(k) for k in kids[off[i]:off[i + 1]])) for i, x in enumerate(ids)}
+
+
 def reconstruct(eg: EGraph, selection: Mapping) -> TensorGraph:
     """Materialise a selection as a tensor graph (extract.py:584-639)."""
     if eg.root is None:
@@ -101,10 +123,28 @@ def reconstruct(eg: EGraph, selection: Mapping) -> TensorGraph:
     g = TensorGraph()
     built: dict = {}
     onstack: set = set()
-    nodes = eg.view
+    if any(not 0 <= int(v) < eg.allocated_nodes for v in selection.values()):
+        raise ReconstructError("selection names an unknown e-node")
+    sel_nodes = _selected_nodes(eg, selection.values())
+    keys = np.array([int(c) for c in selection] + [int(eg.root)], np.uint32)
+    if (keys >= eg.allocated_nodes).any():
+        raise ReconstructError("selection names an unknown e-class")
+    found = np.zeros(max(len(keys), 1), np.uint32)
+    _lib.check(eg._h, _lib.load().tsat_find_batch(eg._h, len(keys), _lib.ptr(keys, C.c_uint32),
+                                                  _lib.ptr(found, C.c_uint32)))
+    canon = {int(k): int(f) for k, f in zip(keys[:-1], found[:-1])}
+    root_cls = int(found[len(keys) - 1])
+    selection = {canon[int(c)]: int(v) for c, v in selection.items()}
+
+    class _EN:
+        __slots__ = ("id", "op", "children")
+
+        def __init__(self, nid):
+            self.id = nid
+            self.op, self.children = sel_nodes[nid]
 
     def build(cid: int) -> str:
-        cid = eg.find(cid)
+        cid = canon.get(cid, cid)
         if cid in built:
             return built[cid]
         if cid in onstack:
@@ -112,21 +152,21 @@ def reconstruct(eg: EGraph, selection: Mapping) -> TensorGraph:
         if cid not in selection:
             raise ReconstructError(f"selection misses e-class c{cid}")
         onstack.add(cid)
-        en = nodes.node(selection[cid])
+        en = _EN(selection[cid])
         sig = SIGNATURES.get(en.op) if isinstance(en.op, str) else None
         if sig is None:
             raise ReconstructError(f"e-node n{en.id} ({en.op!r}) is not a graph operator")
         params: dict = {}
         inputs: list = []
         for (arg, kind), ch in zip(sig.args, en.children):
-            ch = eg.find(ch)
+            ch = canon.get(ch, ch)
             if kind in (ValueKind.T, ValueKind.TT):
                 inputs.append(build(ch))
             else:
                 leaf_id = selection.get(ch)
                 if leaf_id is None:
                     raise ReconstructError(f"selection misses parameter class c{ch}")
-                leaf = nodes.node(leaf_id)
+                leaf = _EN(leaf_id)
                 if leaf.children:
                     raise ReconstructError(f"parameter class c{ch} selected a non-literal")
                 params[arg] = leaf.op
@@ -136,7 +176,7 @@ def reconstruct(eg: EGraph, selection: Mapping) -> TensorGraph:
         built[cid] = name
         return name
 
-    root_name = build(eg.root)
+    root_name = build(root_cls)
     build = None  # break the recursive closure's cycle (it references eg)
 
     def flat(name: str) -> list:
