@@ -341,16 +341,17 @@ __device__ __forceinline__ void d_mark_roots(u64 tid, u64 nth, const WaveRule& W
 __device__ __forceinline__ void d_cand_check(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
                                              const u32* acc, u32 nacc, u32 ncand, const u32* ident, const u32* env,
                                              const u32* olds, int multi, u8* hazard, u32* alloc, u8* ukind,
-                                             u32* uother, u8* grow, u8* stop_after) {
+                                             u32* uother, u8* grow, u8* stop_after, u32* akid) {
   TID_LOOP(a0, ncand) {
     u32 a = (u32)a0;
     if (a >= nacc) {
       alloc[a] = 0;
+      akid[a] = 0;
       stop_after[a] = 0;
       continue;
     }
     u32 c = acc[a];
-    u32 na = 0;
+    u32 na = 0, nk = 0;
     bool hz = hazard[c] != 0, sa = false;
     u8 why = hazard[c];
     for (int t = 0; t < MAX_SRC; t++) {
@@ -363,8 +364,10 @@ __device__ __forceinline__ void d_cand_check(u64 tid, u64 nth, const G& g, const
         if (!(id & FRESH)) continue;
         u32 s = id & ~FRESH;
         bool win = is_winner(T, s, (u64)a * W.R + r);
-        if (win) na++;
-        else if (is_wroot(T, s) && !W.tmpl[r].is_root) {
+        if (win) {
+          na++;
+          nk += (u32)W.tmpl[r].nargs;
+        } else if (is_wroot(T, s) && !W.tmpl[r].is_root) {
           hz = true;  // inner reuse of a merged root
           why = 3;
         }
@@ -438,6 +441,7 @@ __device__ __forceinline__ void d_cand_check(u64 tid, u64 nth, const G& g, const
     hazard[c] = hz ? (why ? why : 1) : 0;
     stop_after[a] = sa ? 1 : 0;
     alloc[a] = hz ? 0 : na;
+    akid[a] = hz ? 0 : nk;
   }
 }
 
@@ -616,6 +620,51 @@ __device__ __forceinline__ void d_write_nodes(u64 tid, u64 nth, const G& g, cons
   }
 }
 
+// per-combo commit (single-CTA path): node ids / kid offsets from the
+// per-combo prefixes of winners and winners' children, requests in order
+__device__ __forceinline__ void d_assign_combos(u64 tid, u64 nth, const WaveRule& W, const WaveTab& T, u32 ncacc,
+                                                const u32* ident, const u32* apre, u32 base) {
+  TID_LOOP(a, ncacc) {
+    u32 id = base + apre[a];
+    for (int r = 0; r < W.R; r++) {
+      u64 q = a * (u64)W.R + r;
+      u32 v = ident[q];
+      if ((v & FRESH) && is_winner(T, v & ~FRESH, q)) T.wid[v & ~FRESH] = id++;
+    }
+  }
+}
+
+__device__ __forceinline__ void d_write_combos(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
+                                               const u32* acc, u32 ncacc, const u32* ident, const u32* apre,
+                                               const u32* kpre, u32 base, u32 kbase, const u32* env,
+                                               const u32* olds) {
+  TID_LOOP(a, ncacc) {
+    u32 id = base + apre[a], ko = kbase + kpre[a];
+    u32 c = acc[a];
+    for (int r = 0; r < W.R; r++) {
+      u64 q = a * (u64)W.R + r;
+      u32 v0 = ident[q];
+      if (!(v0 & FRESH)) continue;
+      u32 s = v0 & ~FRESH;
+      if (!is_winner(T, s, q)) continue;
+      const ReqT& tq = W.tmpl[r];
+      g.op[id] = tq.atom;
+      g.koff[id] = ko;
+      g.koff[id + 1] = ko + tq.nargs;
+      for (int j = 0; j < tq.nargs; j++) {
+        int k = tq.kid[j];
+        u32 v = k >= 0 ? ident[a * (u64)W.R + k] : env[(u64)c * MAX_VARS + (-k - 1)];
+        g.kids[ko + j] = (v & FRESH) ? T.wid[v & ~FRESH] : v;
+      }
+      g.flags[id] = NF_ALIVE;
+      if (g.analysis) g.val[id] = T.val[s];
+      g.parent[id] = tq.is_root ? olds[(u64)c * MAX_SRC + tq.tgt] : id;
+      ko += tq.nargs;
+      id++;
+    }
+  }
+}
+
 // commit boundary: stops = [stop_after cand, cutoff cand, first bad cand]
 __device__ __forceinline__ void d_boundary(WaveState* ws, const u32* stops, u32 ncand, const unsigned long long* pos,
                                            unsigned long long p, unsigned long long seg_end, const u32* pre,
@@ -679,9 +728,9 @@ __global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, const WaveSt
 
 __global__ void k_cand_check(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, u32 ncand,
                              const u32* ident, const u32* env, const u32* olds, int multi, u8* hazard, u32* alloc,
-                             u8* ukind, u32* uother, u8* grow, u8* stop_after) {
+                             u8* ukind, u32* uother, u8* grow, u8* stop_after, u32* akid) {
   d_cand_check(GTID, GNTH, g, W, T, acc, ws->nacc, ncand, ident, env, olds, multi, hazard, alloc, ukind, uother, grow,
-               stop_after);
+               stop_after, akid);
 }
 
 __global__ void k_first_writer(WaveRule W, u32 epoch, const u32* acc, const WaveState* ws, const u8* hazard,
@@ -760,6 +809,34 @@ __device__ __forceinline__ u32 block_scan(u32 n, u32* out, F f) {
   return total;
 }
 
+// block-wide exclusive scan of two counters at once (packed in a u64):
+// out_a / out_b get the prefixes of fa / fb, totals at [n]
+template <int BT, class F>
+__device__ __forceinline__ void block_scan2(u32 n, u32* out_a, u32* out_b, F f) {
+  typedef cub::BlockScan<unsigned long long, BT> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u32 base = 0; base < n; base += BT) {
+    u32 i = base + threadIdx.x;
+    unsigned long long v = i < n ? f(i) : 0ull, x, tot;
+    BS(tmp).ExclusiveSum(v, x, tot);
+    if (i < n) {
+      out_a[i] = (u32)((carry + x) >> 32);
+      out_b[i] = (u32)(carry + x);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out_a[n] = (u32)(carry >> 32);
+    out_b[n] = (u32)carry;
+  }
+  __syncthreads();
+}
+
 // single-CTA exclusive scan with the total at out[n] (small arrays; CUB's two
 // kernels cost more than the work at wave sizes)
 __global__ void __launch_bounds__(1024) k_scan_block(const u32* in, u32* out, u32 n) {
@@ -815,7 +892,7 @@ __global__ void k_counters_commit(WaveState* ws, Counters* cnt) {
 // Buffers of one wave (device pointers).
 struct WaveIO {
   u8 *status, *hazard, *ukind, *grow, *sa;
-  u32 *env, *olds, *pre, *acc, *ident, *alloc, *apre, *wf, *wpre, *ka, *kpre, *uother, *stops;
+  u32 *env, *olds, *pre, *acc, *ident, *alloc, *apre, *wf, *wpre, *ka, *kpre, *uother, *stops, *akid, *ckpre;
   unsigned long long *fw_cls, *fw_fresh;
   WaveState* ws;
   DevStats* wstats;
@@ -983,7 +1060,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     }
     WPROF(2);
     d_cand_check(tid, nth, g, W, Tw, io.acc, nacc, ncand, io.ident, io.env, io.olds, A.multi, io.hazard, io.alloc,
-                 io.ukind, io.uother, io.grow, io.sa);
+                 io.ukind, io.uother, io.grow, io.sa, io.akid);
     __syncthreads();
     WPROF(3);
     // ---- conflicts, stop-after, node-limit cutoff, boundary
@@ -993,7 +1070,8 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     WPROF(4);
     d_validity(tid, nth, W, Tw, R.nslots, R.nsrc, ncand, io.hazard, io.env, io.olds, io.pre, io.status, io.ident,
                io.fw_cls, io.fw_fresh, io.stops + 2);
-    block_scan<CTA_T>(ncand, io.apre, [&](u32 c) { return io.alloc[c]; });
+    block_scan2<CTA_T>(ncand, io.apre, io.ckpre,
+                       [&](u32 c) { return ((unsigned long long)io.alloc[c] << 32) | io.akid[c]; });
     d_find_stops(tid, nth, io.acc, nacc, io.sa, io.apre, io.alloc, (i64)g.cnt->live, A.n_max, io.stops);
     __syncthreads();
     WPROF(5);
@@ -1008,17 +1086,11 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     const u32 ncacc = s_ncacc;
     d_seg_stats(tid, nth, io.status, io.ws, io.ws->ncommit_cand, io.pre, io.alloc, io.ukind, R.efficient, io.wstats);
     // ---- commit (requests of committed combos only)
-    const u64 lim = (u64)ncacc * W.R;
-    u32 nwin = 0, nk = 0;
-    if (lim) {
-      d_win_flags(tid, nth, Tw, io.ident, lim, W.tmpl, W.R, lim, io.wf, io.ka);
+    const u32 nwin = io.apre[ncacc], nk = io.ckpre[ncacc];
+    if (nwin) {
+      d_assign_combos(tid, nth, W, Tw, ncacc, io.ident, io.apre, s_base);
       __syncthreads();
-      nwin = block_scan<CTA_T>((u32)lim, io.wpre, [&](u32 q) { return io.wf[q]; });
-      nk = block_scan<CTA_T>((u32)lim, io.kpre, [&](u32 q) { return io.ka[q]; });
-      d_assign_ids(tid, nth, Tw, io.ident, lim, io.wf, io.wpre, s_base);
-      __syncthreads();
-      d_write_nodes(tid, nth, g, W, Tw, io.acc, io.ident, lim, io.wf, io.wpre, io.kpre, s_base, s_kbase, io.env,
-                    io.olds);
+      d_write_combos(tid, nth, g, W, Tw, io.acc, ncacc, io.ident, io.apre, io.ckpre, s_base, s_kbase, io.env, io.olds);
       __syncthreads();  // unions overwrite parent[] of fresh non-root nodes
     }
     WPROF(7);
@@ -1099,7 +1171,7 @@ struct WaveBufs {
   DevBuf<u64> hA, hB, hBs;
   DevBuf<u32> iB, iBs, cnt, off;
   DevBuf<u8> status, hazard;
-  DevBuf<u32> env, olds, fl, pre, acc, ident, alloc, apre, wf, wpre, ka, kpre, stops, uother;
+  DevBuf<u32> env, olds, fl, pre, acc, ident, alloc, apre, wf, wpre, ka, kpre, stops, uother, akid, ckpre;
   DevBuf<unsigned long long> fw_cls, fw_fresh;  // epoch-tagged first writers
   DevBuf<CtaCtl> ctl;
   DevBuf<u8> ukind, grow, sa;
@@ -1244,6 +1316,8 @@ static void ensure_cand_bufs(Engine& e, WaveBufs& B, u64 ncand, int R) {
     B.acc.ensure(n + 1);
     B.alloc.ensure(n + 1);
     B.apre.ensure(n + 2);
+    B.akid.ensure(n + 1);
+    B.ckpre.ensure(n + 2);
     B.ukind.ensure(n * MAX_SRC + 1);
     B.uother.ensure(n * MAX_SRC + 1);
     B.grow.ensure(n * MAX_SRC + 1);
@@ -1408,7 +1482,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0};
       WaveIO io{B.status.p, B.hazard.p, B.ukind.p, B.grow.p, B.sa.p, B.env.p, B.olds.p, B.pre.p, B.acc.p,
                 B.ident.p, B.alloc.p, B.apre.p, B.wf.p, B.wpre.p, B.ka.p, B.kpre.p, B.uother.p, B.stops.p,
-                B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, B.lvl.p};
+                B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, B.lvl.p};
       CtaArgs A;
       memset(&A, 0, sizeof(A));
       A.nlv = (int)lv.size();
@@ -1517,7 +1591,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       }
       k_cand_check<<<nblk(ncand), 256, 0, e.s>>>(e.view(), W, T, B.acc.p, ws, ncand, B.ident.p, B.env.p, B.olds.p,
                                                  multi ? 1 : 0, B.hazard.p, B.alloc.p, B.ukind.p, B.uother.p,
-                                                 B.grow.p, B.sa.p);
+                                                 B.grow.p, B.sa.p, B.akid.p);
       // ---- 4. read/write conflicts, stop-after, node-limit cutoff, boundary
       k_first_writer<<<nblk(ncand), 256, 0, e.s>>>(W, T.epoch, B.acc.p, ws, B.hazard.p, B.olds.p, B.ukind.p,
                                                    B.uother.p, B.grow.p, B.fw_cls.p, B.fw_fresh.p);
