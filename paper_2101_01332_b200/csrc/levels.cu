@@ -8,6 +8,8 @@
 // crosses the threshold.
 #include <cooperative_groups.h>
 
+#include <cub/cub.cuh>
+
 #include "engine.cuh"
 
 namespace cg = cooperative_groups;
@@ -151,16 +153,32 @@ __global__ void k_frontier_start(u32* ctl, u32* lvl_off) {
 // the queue counters live in shared memory (small graphs), so a level costs
 // a couple of dependent global loads plus shared-memory atomics.
 #define LV_EDGES 65536u
-__global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ctl, int use_smem) {
+// use_smem: 0 = all state in HBM, 1 = degree / mark array in shared memory,
+// 2 = also the CSR offsets and the queue (small graphs: a level then costs one
+// HBM round trip, the edge-list read)
+__global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier Fg, u32* ctl, int use_smem) {
   extern __shared__ u32 s_deg[];
-  __shared__ u32 s_start, s_end, s_lvl, s_nheavy, s_edges, s_tail, s_ned;
+  __shared__ u32 s_start, s_end, s_lvl, s_edges, s_tail, s_ned;
   __shared__ u32 s_heavy[LV_BLOCK];
+  __shared__ u32 s_estart[LV_BLOCK];
+  Frontier F = Fg;
   u32* gdeg = F.bfs ? F.mark : F.outdeg;
   u32* deg = use_smem ? s_deg : gdeg;
   u32* tail = use_smem ? &s_tail : &ctl[0];
   u32* ned = use_smem ? &s_ned : &ctl[7];
+  const u32 t_init = ctl[0];
   if (use_smem)
     for (u32 i = threadIdx.x; i < F.n; i += blockDim.x) s_deg[i] = gdeg[i];
+  if (use_smem == 2) {
+    u32* s_off = s_deg + F.n;
+    u32* s_ord = s_off + F.n + 1;
+    const u32* goff = F.bfs ? F.eoff : F.roff;
+    for (u32 i = threadIdx.x; i <= F.n; i += blockDim.x) s_off[i] = goff[i];
+    for (u32 i = ctl[2] + threadIdx.x; i < t_init; i += blockDim.x) s_ord[i] = Fg.order[i];
+    if (F.bfs) F.eoff = s_off;
+    else F.roff = s_off;
+    F.order = s_ord;
+  }
   if (threadIdx.x == 0) {
     s_start = ctl[2];
     s_end = ctl[3];
@@ -271,22 +289,29 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
         continue;
       }
     }
+    // the level's edges are flattened: a block scan of the frontier vertices'
+    // degrees, then one thread per edge (vertex found by binary search of the
+    // prefix) -- no thread walks a long edge list alone
     for (u32 t0 = start; t0 < end; t0 += blockDim.x) {
-      if (threadIdx.x == 0) s_nheavy = 0;
-      __syncthreads();
       u32 t = t0 + threadIdx.x;
-      if (t < end) {
-        u32 j = F.order[t], a, b;
-        edge_range(F, j, a, b);
-        if (b - a > HEAVY) s_heavy[atomicAdd(&s_nheavy, 1u)] = j;
-        else
-          for (u32 e = a; e < b; e++) frontier_edge(F, e, lvl, deg, tail, ned);
-      }
+      u32 a = 0, b = 0;
+      if (t < end) edge_range(F, F.order[t], a, b);
+      u32 d = b - a, x, tot;
+      typedef cub::BlockScan<u32, LV_BLOCK> BS;
+      __shared__ typename BS::TempStorage scan_tmp;
+      BS(scan_tmp).ExclusiveSum(d, x, tot);
+      s_heavy[threadIdx.x] = x;  // prefix of the chunk's degrees
+      s_estart[threadIdx.x] = a;
       __syncthreads();
-      for (u32 h = 0; h < s_nheavy; h++) {
-        u32 a, b;
-        edge_range(F, s_heavy[h], a, b);
-        for (u32 e = a + threadIdx.x; e < b; e += blockDim.x) frontier_edge(F, e, lvl, deg, tail, ned);
+      u32 nv = min((u32)blockDim.x, end - t0);
+      for (u32 k = threadIdx.x; k < tot; k += blockDim.x) {
+        u32 lo = 0, hi = nv;  // last vertex slot with prefix <= k
+        while (hi - lo > 1) {
+          u32 mid = (lo + hi) >> 1;
+          if (s_heavy[mid] <= k) lo = mid;
+          else hi = mid;
+        }
+        frontier_edge(F, s_estart[lo] + (k - s_heavy[lo]), lvl, deg, tail, ned);
       }
       __syncthreads();
     }
@@ -304,6 +329,8 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier F, u32* ct
   }
   if (use_smem)
     for (u32 i = threadIdx.x; i < F.n; i += blockDim.x) gdeg[i] = s_deg[i];
+  if (use_smem == 2)
+    for (u32 i = t_init + threadIdx.x; i < s_tail; i += blockDim.x) Fg.order[i] = F.order[i];
   if (threadIdx.x == 0) {
     ctl[1] = s_lvl;
     ctl[2] = s_start;
@@ -417,15 +444,16 @@ static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& tot
   static int gblocks = 0;
   if (!gblocks) gblocks = coop_blocks(e, (const void*)k_frontier_grid, 256);
   u32 h[5];
-  const u32 FR_SMEM = 160u << 10;
-  int use_smem = (u64)F.n * 4 <= FR_SMEM;
+  const u64 FR_SMEM = 200u << 10;
+  int use_smem = (12ull * F.n + 4 <= FR_SMEM) ? 2 : ((u64)F.n * 4 <= FR_SMEM ? 1 : 0);
+  size_t smem_bytes = use_smem == 2 ? (size_t)(3ull * F.n + 1) * 4 : use_smem == 1 ? (size_t)F.n * 4 : 0;
   static int smem_set = 0;
   if (!smem_set) {
     CUDA_OK(cudaFuncSetAttribute(k_frontier_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FR_SMEM));
     smem_set = 1;
   }
   while (true) {
-    k_frontier_block<<<1, LV_BLOCK, use_smem ? (size_t)F.n * 4 : 0, e.s>>>(F, ctl.p, use_smem);
+    k_frontier_block<<<1, LV_BLOCK, smem_bytes, e.s>>>(F, ctl.p, use_smem);
     CUDA_OK(cudaMemcpyAsync(h, ctl.p, 5 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
     e.sync();
     if (h[4]) break;
