@@ -499,23 +499,75 @@ __device__ __forceinline__ void gq_totals(u32 qa, u32 qb, u64 tid, u64 nth, cons
   }
 }
 
+// sequential fold over members [q0, q1) in id order (extract.py:145-152)
+__device__ __forceinline__ void gq_fold_seq(u32 q0, u32 q1, const double* qtot, double& c, u32& best) {
+  c = INFINITY;
+  best = TSAT_NONE;
+  for (u32 q = q0; q < q1; q++) {
+    double tot = qtot[q];
+    if (isnan(tot) || isinf(tot)) continue;
+    if (tot < c - 1e-15) {
+      c = tot;
+      best = q;
+    }
+  }
+}
+
+// Classes with more than 32 members are folded by a warp: the sequential
+// rule picks the first member attaining the minimum unless some total lies in
+// (min, min + 1e-15] (then the chain of near-ties decides: lane 0 replays the
+// sequential fold).  Smaller classes: one thread each.
+#define GQ_BIG 32u
 __device__ __forceinline__ void gq_fold(u32 a, u32 b, u64 tid, u64 nth, const u32* order, const u32* lvm_off,
-                                        const u32* qnode, const double* qtot, double* bc, u32* bn) {
+                                        const u32* qnode, const double* qtot, double* bc, u32* bn, bool big) {
   for (u64 t = a + tid; t < b; t += nth) {
     u32 q0 = lvm_off[t], q1 = lvm_off[t + 1];
-    double c = INFINITY;
-    u32 best = TSAT_NONE;
-    for (u32 q = q0; q < q1; q++) {
-      double tot = qtot[q];
-      if (isnan(tot) || isinf(tot)) continue;
-      if (tot < c - 1e-15) {
-        c = tot;
-        best = q;
-      }
-    }
+    if (q1 - q0 > GQ_BIG) continue;
+    double c;
+    u32 best;
+    gq_fold_seq(q0, q1, qtot, c, best);
     u32 i = order[t];
     bc[i] = c;
     bn[i] = best == TSAT_NONE ? TSAT_NONE : qnode[best];
+  }
+  if (!big) return;  // no class of this level has more than GQ_BIG members
+  const u32 lane = (u32)(tid & 31);
+  for (u64 t = a + (tid >> 5); t < b; t += nth >> 5) {
+    u32 q0 = lvm_off[t], q1 = lvm_off[t + 1];
+    if (q1 - q0 <= GQ_BIG) continue;
+    double m = INFINITY;
+    u32 mi = TSAT_NONE;
+    for (u32 q = q0 + lane; q < q1; q += 32) {
+      double tot = qtot[q];
+      if (isnan(tot) || isinf(tot)) continue;
+      if (tot < m) {  // lanes walk ascending q: keeps the first occurrence
+        m = tot;
+        mi = q;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      u32 i2 = __shfl_xor_sync(0xffffffffu, mi, o);
+      if (m2 < m || (m2 == m && i2 < mi)) {
+        m = m2;
+        mi = i2;
+      }
+    }
+    bool near = false;
+    if (mi != TSAT_NONE)
+      for (u32 q = q0 + lane; q < q1; q += 32) {
+        double tot = qtot[q];
+        if (!isnan(tot) && !isinf(tot) && tot > m && tot <= m + 1e-15) near = true;
+      }
+    near = __any_sync(0xffffffffu, near);
+    if (lane == 0) {
+      double c = m;
+      u32 best = mi;
+      if (near) gq_fold_seq(q0, q1, qtot, c, best);
+      u32 i = order[t];
+      bc[i] = best == TSAT_NONE ? INFINITY : c;
+      bn[i] = best == TSAT_NONE ? TSAT_NONE : qnode[best];
+    }
   }
 }
 
@@ -525,14 +577,14 @@ __device__ __forceinline__ void gq_fold(u32 a, u32 b, u64 tid, u64 nth, const u3
 __global__ void __launch_bounds__(1024) k_greedy_cta(const u32* order, const u32* lvl_off, u32 l0, u32 l1, u32 ntr,
                                                      const u32* lvm_off, const u32* qnode, const double* qcost,
                                                      const u32* qeoff, const u32* qedst, double* qtot, double* bc_g,
-                                                     u32* bn, int smem) {
+                                                     u32* bn, int smem, const u32* bigflag) {
   extern __shared__ double s_bc[];
   double* bc = smem ? s_bc : bc_g;
   for (u32 l = l0; l < l1; l++) {
     u32 a = lvl_off[l], b = lvl_off[l + 1];
     gq_totals(lvm_off[a], lvm_off[b], threadIdx.x, blockDim.x, qcost, qeoff, qedst, bc, qtot);
     __syncthreads();
-    gq_fold(a, b, threadIdx.x, blockDim.x, order, lvm_off, qnode, qtot, bc, bn);
+    gq_fold(a, b, threadIdx.x, blockDim.x, order, lvm_off, qnode, qtot, bc, bn, bigflag[l] != 0);
     __syncthreads();
   }
   if (smem)
@@ -550,9 +602,16 @@ __global__ void k_gq_totals_wide(u32 qa, u32 qb, const double* qcost, const u32*
 }
 
 __global__ void k_gq_fold_wide(u32 a, u32 b, const u32* order, const u32* lvm_off, const u32* qnode,
-                               const double* qtot, double* bc, u32* bn) {
+                               const double* qtot, double* bc, u32* bn, int big) {
   gq_fold(a, b, blockIdx.x * (u64)blockDim.x + threadIdx.x, (u64)gridDim.x * blockDim.x, order, lvm_off, qnode, qtot,
-          bc, bn);
+          bc, bn, big != 0);
+}
+
+// levels holding a class with more than GQ_BIG members
+__global__ void k_gq_bigflags(const u32* order, const u32* lvm_off, u32 ntr, const u32* level, u32* flag) {
+  GRID_STRIDE(t, ntr) {
+    if (lvm_off[t + 1] - lvm_off[t] > GQ_BIG) flag[level[order[t]]] = 1;
+  }
 }
 
 // Jacobi round over the classes left on cycles
@@ -658,13 +717,18 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
   k_gq_count<<<nblk(ntr), 256, 0, s>>>(ord, ntr, co, X.gq_cnt.p);
   CUDA_OK(cudaMemsetAsync(X.gq_cnt.p + ntr, 0, sizeof(u32), s));
   dev_exclusive_scan_u32(*this, X.gq_cnt.p, X.gq_lvm.p, ntr + 1);
-  std::vector<u32> lvm(nl + 1);
+  std::vector<u32> lvm(nl + 1), bigf(nl + 1);
+  DevBuf<u32>& bflag = X.gq_big;
+  bflag.ensure(nl + 1);
   {
     // member offsets at level boundaries (host: picks thin runs / wide levels)
     DevBuf<u32>& lb = X.gq_lb;
     lb.ensure(nl + 1);
     k_gather_at<<<nblk(nl + 1), 256, 0, s>>>(X.gq_lvm.p, lvl, nl + 1, lb.p);
+    CUDA_OK(cudaMemsetAsync(bflag.p, 0, (nl + 1) * sizeof(u32), s));
+    k_gq_bigflags<<<nblk(ntr), 256, 0, s>>>(ord, X.gq_lvm.p, ntr, sc.cg_level.p, bflag.p);
     CUDA_OK(cudaMemcpyAsync(lvm.data(), lb.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(bigf.data(), bflag.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
     sync();
   }
   u32 nq = lvm[nl];
@@ -703,7 +767,7 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
   if ((u64)C * sizeof(double) <= GREEDY_SMEM) {
     k_greedy_cta<<<1, 1024, (size_t)C * sizeof(double), s>>>(ord, lvl, 0, nl, ntr, X.gq_lvm.p, X.gq_node.p,
                                                               X.gq_cost.p, X.gq_eoff.p, X.gq_edst.p, X.gq_tot.p, c0.p,
-                                                              n0.p, 1);
+                                                              n0.p, 1, bflag.p);
   } else {
     // thin runs in one CTA, wide levels (> WIDE members or classes) on the grid
     const u32 WIDE = 8192;
@@ -712,15 +776,15 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
       if (wm > WIDE || wc > WIDE) {
         k_gq_totals_wide<<<nblk(wm), 256, 0, s>>>(lvm[l], lvm[l + 1], X.gq_cost.p, X.gq_eoff.p, X.gq_edst.p, c0.p,
                                                    X.gq_tot.p);
-        k_gq_fold_wide<<<nblk(wc), 256, 0, s>>>(lo[l], lo[l + 1], ord, X.gq_lvm.p, X.gq_node.p, X.gq_tot.p, c0.p,
-                                                n0.p);
+        k_gq_fold_wide<<<nblk(bigf[l] ? (u64)wc * 32 : wc), 256, 0, s>>>(lo[l], lo[l + 1], ord, X.gq_lvm.p,
+                                                                         X.gq_node.p, X.gq_tot.p, c0.p, n0.p, bigf[l]);
         l++;
         continue;
       }
       u32 l1 = l;
       while (l1 < nl && lvm[l1 + 1] - lvm[l1] <= WIDE && lo[l1 + 1] - lo[l1] <= WIDE) l1++;
       k_greedy_cta<<<1, 1024, 0, s>>>(ord, lvl, l, l1, ntr, X.gq_lvm.p, X.gq_node.p, X.gq_cost.p, X.gq_eoff.p,
-                                      X.gq_edst.p, X.gq_tot.p, c0.p, n0.p, 0);
+                                      X.gq_edst.p, X.gq_tot.p, c0.p, n0.p, 0, bflag.p);
       l = l1;
     }
   }
