@@ -214,6 +214,7 @@ struct Scratch {
   DevBuf<u32> g_n0, g_n1, g_flag, g_mark, g_fa, g_fb, g_oc, g_on, k_slots, g_eoff, g_edst, g_cnt;
   DevBuf<char> k_keys;
   DevBuf<u32> gq_lvm, gq_cnt, gq_k, gq_node, gq_deg, gq_eoff, gq_edst, gq_lb, gq_head, gq_slot, gq_big;
+  DevBuf<double> gq_pack, gq_recv;  // sharded wide levels: {best cost, node} records
   DevBuf<double> gq_cost, gq_tot;
   DevBuf<i64> k_off;
   // api
@@ -338,6 +339,7 @@ struct Engine {
   void shard_teardown();
   void shard_candidate_ranges(std::vector<u32>& rng);
   void shard_gather_matches(const std::vector<int>& pids);
+  void shard_allgather_bytes(const void* send, void* recv, size_t bytes);
   void load_rules(int n, const i64* blob);
 
   // cycles

@@ -607,6 +607,39 @@ __global__ void k_gq_fold_wide(u32 a, u32 b, const u32* order, const u32* lvm_of
           bc, bn, big != 0);
 }
 
+// Sharded wide level (extraction relaxation partitioned by
+// e-class range, class-cost vectors all-gathered): rank r folds the level's
+// class slots [a + r*chunk, ...) -- member totals for members of those slots
+// only -- and packs {best cost, node} per slot; after the all-gather every
+// rank scatters the whole level back into its best-cost arrays.
+__global__ void k_gq_totals_slots(u32 qa, u32 qb, u32 t_lo, u32 t_hi, const u32* slot_of, const double* qcost,
+                                  const u32* qeoff, const u32* qedst, const double* bc, double* qtot) {
+  GRID_STRIDE(q0, (u64)(qb - qa)) {
+    u32 q = qa + (u32)q0, t = slot_of[q];
+    if (t < t_lo || t >= t_hi) continue;
+    double tot = qcost[q];
+    if (!isnan(tot))
+      for (u32 e = qeoff[q], e1 = qeoff[q + 1]; e < e1; e++) tot += bc[qedst[e]];
+    qtot[q] = tot;
+  }
+}
+
+__global__ void k_gq_pack(u32 t_lo, u32 t_hi, const u32* order, const double* bc, const u32* bn, double* rec) {
+  GRID_STRIDE(k, (u64)(t_hi - t_lo)) {
+    u32 i = order[t_lo + k];
+    rec[2 * k] = bc[i];
+    rec[2 * k + 1] = __longlong_as_double((long long)bn[i]);
+  }
+}
+
+__global__ void k_gq_unpack(u32 a, u32 b, const u32* order, const double* rec, double* bc, u32* bn) {
+  GRID_STRIDE(k, (u64)(b - a)) {
+    u32 i = order[a + k];
+    bc[i] = rec[2 * k];
+    bn[i] = (u32)__double_as_longlong(rec[2 * k + 1]);
+  }
+}
+
 // levels holding a class with more than GQ_BIG members
 __global__ void k_gq_bigflags(const u32* order, const u32* lvm_off, u32 ntr, const u32* level, u32* flag) {
   GRID_STRIDE(t, ntr) {
@@ -773,6 +806,30 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
     const u32 WIDE = 8192;
     for (u32 l = 0; l < nl;) {
       u32 wm = lvm[l + 1] - lvm[l], wc = lo[l + 1] - lo[l];
+      if ((wm > WIDE || wc > WIDE) && shard_world > 1) {
+        // class slots split across the shard ranks, {cost, node} all-gathered.
+        // Without a communicator (single-GPU shard tests) every rank's slice
+        // is computed here in turn -- the same slicing, packing and unpacking.
+        const u32 W = (u32)shard_world, a = lo[l], b = lo[l + 1], chunk = (wc + W - 1) / W;
+        X.gq_pack.ensure(2ull * chunk + 2);
+        X.gq_recv.ensure(2ull * chunk * W + 2);
+        for (u32 r = 0; r < W; r++) {
+          if (comm && (int)r != shard_rank) continue;
+          u32 ta = std::min(b, a + r * chunk), tb = std::min(b, ta + chunk);
+          if (tb > ta) {
+            k_gq_totals_slots<<<nblk(wm), 256, 0, s>>>(lvm[l], lvm[l + 1], ta, tb, X.gq_slot.p, X.gq_cost.p,
+                                                        X.gq_eoff.p, X.gq_edst.p, c0.p, X.gq_tot.p);
+            k_gq_fold_wide<<<nblk(bigf[l] ? (u64)(tb - ta) * 32 : tb - ta), 256, 0, s>>>(
+                ta, tb, ord, X.gq_lvm.p, X.gq_node.p, X.gq_tot.p, c0.p, n0.p, bigf[l]);
+          }
+          double* dst = comm ? X.gq_pack.p : X.gq_recv.p + 2ull * chunk * r;
+          if (tb > ta) k_gq_pack<<<nblk(tb - ta), 256, 0, s>>>(ta, tb, ord, c0.p, n0.p, dst);
+        }
+        if (comm) shard_allgather_bytes(X.gq_pack.p, X.gq_recv.p, 2ull * chunk * sizeof(double));
+        k_gq_unpack<<<nblk(wc), 256, 0, s>>>(a, b, ord, X.gq_recv.p, c0.p, n0.p);
+        l++;
+        continue;
+      }
       if (wm > WIDE || wc > WIDE) {
         k_gq_totals_wide<<<nblk(wm), 256, 0, s>>>(lvm[l], lvm[l + 1], X.gq_cost.p, X.gq_eoff.p, X.gq_edst.p, c0.p,
                                                    X.gq_tot.p);

@@ -240,3 +240,9 @@ void Engine::shard_gather_matches(const std::vector<int>& pids) {
   copy_segs(*this, segs);
   sync();
 }
+
+// plain all-gather of ``bytes`` from every rank into recv (rank order)
+void Engine::shard_allgather_bytes(const void* send, void* recv, size_t bytes) {
+  if (shard_world <= 1 || !comm) throw TsatException(TSAT_ERR_STATE, "no shard communicator");
+  NCCL_OK(nccl().AllGather(send, recv, bytes, ncclUint8, (ncclComm_t)comm, s));
+}

@@ -44,3 +44,23 @@ def test_shards_concat_to_global(name, world):
         om = oeg.ematch(pat, frozenset(ofilt))
         assert [(m.eclass, tuple(x for _, x in m.bindings)) for m in full] == \
                [(c, tuple(x for _, x in b)) for c, b in om]
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_greedy_wide_levels_match(world):
+    """Greedy's wide levels split by class slot across W ranks (emulated on one
+    GPU without an NCCL id: every slice computed, packed and unpacked) must
+    give the unsharded selection and total."""
+    from paper_2101_01332_b200.cost import CostModel, egraph_costs
+    from paper_2101_01332_b200.extract import greedy_extract
+
+    g = bench_graphs.matmul_chain(150)  # 112k e-nodes, 67k classes: HBM path with wide levels
+    merge = [r for r in default_rules() if r.name == "matmul-merge-shared-lhs"]
+    eg, filt, rep = explore(g, merge, ExploreLimits(n_max=10**9, k_max=1, k_multi=1))
+    costs = egraph_costs(eg, CostModel())
+    ref = greedy_extract(eg, costs, filt)
+    shard.attach(eg, world - 1, world)
+    res = greedy_extract(eg, costs, filt)
+    shard.attach(eg, 0, 1)
+    assert res.selection == ref.selection
+    assert res.total_cost == ref.total_cost
