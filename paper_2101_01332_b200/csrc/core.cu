@@ -396,11 +396,30 @@ __device__ __forceinline__ void make_one(const G& g, u32 nid) {
   g.val[nid] = v;
 }
 
-// consecutive thin levels [l0, l1) in one CTA (deep noop chains are common)
+// consecutive thin levels [l0, l1) in one CTA (deep noop chains are common);
+// levels of at most 32 nodes are walked by warp 0 alone with __syncwarp only
 __global__ void __launch_bounds__(256) k_make_levels(G g, const u32* ids, const u32* off, u32 l0, u32 l1) {
-  for (u32 l = l0; l < l1; l++) {
+  __shared__ u32 s_next;
+  for (u32 l = l0; l < l1;) {
+    if (off[l + 1] - off[l] <= 32) {
+      if (threadIdx.x < 32) {
+        u32 ll = l;
+        while (ll < l1 && off[ll + 1] - off[ll] <= 32) {
+          u32 t = off[ll] + threadIdx.x;
+          if (t < off[ll + 1]) make_one(g, ids[t]);
+          __syncwarp();
+          ll++;
+        }
+        if (threadIdx.x == 0) s_next = ll;
+      }
+      __syncthreads();
+      l = s_next;
+      __syncthreads();
+      continue;
+    }
     for (u32 t = off[l] + threadIdx.x; t < off[l + 1]; t += blockDim.x) make_one(g, ids[t]);
     __syncthreads();
+    l++;
   }
 }
 

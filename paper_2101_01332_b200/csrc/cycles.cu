@@ -94,24 +94,46 @@ __global__ void __launch_bounds__(512) k_close_cols(const u32* order, const u32*
   u32* col = in_smem ? smem_col : bitsT + (u64)w0 * n;
   if (in_smem)
     for (u64 i = threadIdx.x; i < (u64)nk * n; i += blockDim.x) col[i] = 0;
+  __shared__ u32 s_next;
   __syncthreads();
-  for (u32 l = 1; l < nl; l++) {
+  auto item = [&](u32 a, u64 it) {
+    u32 i = order[a + it / nk];
+    int k = (int)(it % nk);
+    u32 w = w0 + k;
+    const u32* ck = col + (u64)k * n;
+    u32 acc = 0;
+    for (u32 e = eoff[i], e1 = eoff[i + 1]; e < e1; e++) {
+      u32 j = edst[e];
+      acc |= ck[j];
+      if ((j >> 5) == w) acc |= 1u << (j & 31);
+    }
+    col[(u64)k * n + i] = acc;
+  };
+  for (u32 l = 1; l < nl;) {
     u32 a = lvl_off[l], b = lvl_off[l + 1];
     u64 items = (u64)(b - a) * nk;
-    for (u64 it = threadIdx.x; it < items; it += blockDim.x) {
-      u32 i = order[a + it / nk];
-      int k = (int)(it % nk);
-      u32 w = w0 + k;
-      const u32* ck = col + (u64)k * n;
-      u32 acc = 0;
-      for (u32 e = eoff[i], e1 = eoff[i + 1]; e < e1; e++) {
-        u32 j = edst[e];
-        acc |= ck[j];
-        if ((j >> 5) == w) acc |= 1u << (j & 31);
+    if (items <= 32) {
+      // a run of thin levels (deep chains): warp 0 alone, __syncwarp only
+      if (threadIdx.x < 32) {
+        u32 ll = l;
+        while (ll < nl) {
+          u32 a2 = lvl_off[ll], b2 = lvl_off[ll + 1];
+          u64 it2 = (u64)(b2 - a2) * nk;
+          if (it2 > 32) break;
+          if (threadIdx.x < it2) item(a2, threadIdx.x);
+          __syncwarp();
+          ll++;
+        }
+        if (threadIdx.x == 0) s_next = ll;
       }
-      col[(u64)k * n + i] = acc;
+      __syncthreads();
+      l = s_next;
+      __syncthreads();
+      continue;
     }
+    for (u64 it = threadIdx.x; it < items; it += blockDim.x) item(a, it);
     __syncthreads();
+    l++;
   }
   if (nrest) {
     while (true) {

@@ -169,12 +169,22 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier Fg, u32* c
   const u32 t_init = ctl[0];
   if (use_smem)
     for (u32 i = threadIdx.x; i < F.n; i += blockDim.x) s_deg[i] = gdeg[i];
-  if (use_smem == 2) {
+  if (use_smem >= 2) {
     u32* s_off = s_deg + F.n;
     u32* s_ord = s_off + F.n + 1;
     const u32* goff = F.bfs ? F.eoff : F.roff;
     for (u32 i = threadIdx.x; i <= F.n; i += blockDim.x) s_off[i] = goff[i];
     for (u32 i = ctl[2] + threadIdx.x; i < t_init; i += blockDim.x) s_ord[i] = Fg.order[i];
+    if (use_smem == 3) {
+      // the edge list too (tiny graphs with deep chains: a level is then all
+      // shared-memory work)
+      u32* s_edge = s_ord + F.n;
+      u32 ne = goff[F.n];
+      const u32* gedge = F.bfs ? F.edst : F.rsrc;
+      for (u32 i = threadIdx.x; i < ne; i += blockDim.x) s_edge[i] = gedge[i];
+      if (F.bfs) F.edst = s_edge;
+      else F.rsrc = s_edge;
+    }
     if (F.bfs) F.eoff = s_off;
     else F.roff = s_off;
     F.order = s_ord;
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier Fg, u32* c
   }
   if (use_smem)
     for (u32 i = threadIdx.x; i < F.n; i += blockDim.x) gdeg[i] = s_deg[i];
-  if (use_smem == 2)
+  if (use_smem >= 2)
     for (u32 i = t_init + threadIdx.x; i < s_tail; i += blockDim.x) Fg.order[i] = F.order[i];
   if (threadIdx.x == 0) {
     ctl[1] = s_lvl;
@@ -445,8 +455,15 @@ static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& tot
   if (!gblocks) gblocks = coop_blocks(e, (const void*)k_frontier_grid, 256);
   u32 h[5];
   const u64 FR_SMEM = 200u << 10;
-  int use_smem = (12ull * F.n + 4 <= FR_SMEM) ? 2 : ((u64)F.n * 4 <= FR_SMEM ? 1 : 0);
-  size_t smem_bytes = use_smem == 2 ? (size_t)(3ull * F.n + 1) * 4 : use_smem == 1 ? (size_t)F.n * 4 : 0;
+  u32 ne = 0;
+  CUDA_OK(cudaMemcpyAsync(&ne, (F.bfs ? F.eoff : F.roff) + F.n, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+  e.sync();
+  int use_smem = (12ull * F.n + 4 + 4ull * ne <= FR_SMEM) ? 3
+                 : (12ull * F.n + 4 <= FR_SMEM) ? 2 : ((u64)F.n * 4 <= FR_SMEM ? 1 : 0);
+  size_t smem_bytes = use_smem == 3   ? (size_t)(3ull * F.n + 1 + ne) * 4
+                      : use_smem == 2 ? (size_t)(3ull * F.n + 1) * 4
+                      : use_smem == 1 ? (size_t)F.n * 4
+                                      : 0;
   static int smem_set = 0;
   if (!smem_set) {
     CUDA_OK(cudaFuncSetAttribute(k_frontier_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FR_SMEM));
