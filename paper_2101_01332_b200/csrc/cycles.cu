@@ -2,16 +2,15 @@
 // (reference: pkg/src/tensorsat/cycles.py).
 //
 // Class graph: class -> child classes through live, unfiltered e-nodes (CSR
-// plus reverse CSR), built from the snapshot CSR.  Three passes run as
-// cooperative persistent kernels (grid.sync() between levels, no host round
-// trips):
-//   * k_trim_coop  -- Kahn peeling from the sinks: level[c] = height of c in
-//                     the condensation-free part; classes never peeled lie on
-//                     or above a cycle.
-//   * k_bfs_coop   -- classes reachable from the root.
-//   * k_close_coop -- the descendants bitset (cycles.py:70-148) level by
-//                     level; untrimmed classes are closed by sweeping to a
-//                     fixpoint afterwards.
+// plus reverse CSR), built from the snapshot CSR (build_class_graph).  On it:
+//   * the Kahn peel from the sinks (levels.cu: trim_levels): level[c] =
+//     height of c; classes never peeled lie on or above a cycle.  The peel is
+//     cached per (snapshot, filter) and shared by the cycle check, the next
+//     iteration's descendants map and greedy;
+//   * BFS from the root (levels.cu: bfs_classes);
+//   * the descendants bitset (cycles.py:70-148), column-parallel
+//     (k_close_cols): word-major bitset, one CTA per column group walking
+//     every level, untrimmed classes swept to a fixpoint afterwards.
 // break_all_cycles (cycles.py:234-245): "no reachable class is untrimmed"
 // proves there is no live cycle below the root; otherwise the exact
 // lexicographic DFS (cycles.py:172-221) runs on one GPU thread over the

@@ -1,10 +1,17 @@
-// Level engine: Kahn peeling, BFS, level-ordered closure and greedy folds on
-// the class graph, with hybrid execution.  E-graphs from rewrite rules are
-// deep and thin (associativity chains give thousands of levels of a few
-// classes each), so a level-synchronous algorithm is barrier-bound: thin
-// levels run inside ONE 1024-thread CTA with __syncthreads(), wide levels
-// (> LV_WIDE classes) run on the whole GPU as cooperative kernels with
-// grid.sync().  The host only switches between the two when a frontier
+// Level engine: Kahn peeling and BFS on the class graph, with hybrid
+// execution.  E-graphs from rewrite rules are deep and thin (associativity
+// chains and the make_single_rooted noop fold give hundreds to thousands of
+// levels of a few classes each), so a level-synchronous algorithm is
+// latency bound:
+//   * very thin levels (<= 32 vertices, <= 64 edges): warp 0 alone, frontier
+//     carried in registers, plain shared-memory updates (no atomics);
+//   * thin levels (<= LV_WIDE vertices): one 1024-thread CTA, the level's edges
+//     flattened by a block scan of the frontier degrees, degree / mark arrays
+//     (and for small graphs the CSR offsets, queue and edge list) in shared
+//     memory;
+//   * wide levels: the whole GPU as a cooperative kernel with grid.sync(),
+//     light / medium / heavy vertex tiers, warp-aggregated queue appends.
+// The host only switches between the CTA and the grid kernel when a frontier
 // crosses the threshold.
 #include <cooperative_groups.h>
 
