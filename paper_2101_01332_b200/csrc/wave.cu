@@ -932,7 +932,54 @@ struct CtaArgs {
   i64 n_max;
   u32 cta_win;
   const unsigned long long* pos;  // cached join list (multi)
+  int smem;  // per-candidate wave arrays in shared memory (window <= cta_win)
 };
+
+// shared-memory carve-out of the per-candidate wave arrays (window of `win`
+// candidates, R requests each); returns the byte size when out == nullptr
+__host__ __device__ inline size_t wave_smem_layout(u32 win, int R, unsigned char* base, WaveIO* out) {
+  size_t o = 0;
+  auto take = [&](size_t bytes) -> void* {
+    void* p = base ? (void*)(base + o) : nullptr;
+    o += (bytes + 15) & ~(size_t)15;
+    return p;
+  };
+  void* status = take(win + 1);
+  void* hazard = take(win + 1);
+  void* sa = take(win + 1);
+  void* ukind = take((size_t)win * MAX_SRC + 1);
+  void* grow = take((size_t)win * MAX_SRC + 1);
+  void* env = take(((size_t)win * MAX_VARS + 1) * 4);
+  void* olds = take(((size_t)win * MAX_SRC + 1) * 4);
+  void* uother = take(((size_t)win * MAX_SRC + 1) * 4);
+  void* pre = take(((size_t)win + 2) * 4);
+  void* acc = take(((size_t)win + 1) * 4);
+  void* ident = take(((size_t)win * (R > 0 ? R : 1) + 1) * 4);
+  void* alloc = take(((size_t)win + 2) * 4);
+  void* apre = take(((size_t)win + 2) * 4);
+  void* akid = take(((size_t)win + 2) * 4);
+  void* ckpre = take(((size_t)win + 2) * 4);
+  void* stops = take(16);
+  if (out) {
+    out->status = (u8*)status;
+    out->hazard = (u8*)hazard;
+    out->sa = (u8*)sa;
+    out->ukind = (u8*)ukind;
+    out->grow = (u8*)grow;
+    out->env = (u32*)env;
+    out->olds = (u32*)olds;
+    out->uother = (u32*)uother;
+    out->pre = (u32*)pre;
+    out->acc = (u32*)acc;
+    out->ident = (u32*)ident;
+    out->alloc = (u32*)alloc;
+    out->apre = (u32*)apre;
+    out->akid = (u32*)akid;
+    out->ckpre = (u32*)ckpre;
+    out->stops = (u32*)stops;
+  }
+  return o;
+}
 
 __device__ __forceinline__ unsigned long long self_in(u32 nA, u32 nB, unsigned long long p0, unsigned long long p1) {
   // #{i < nA : p0 <= i * (nB + 1) < p1}
@@ -958,6 +1005,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev RD, WaveRule W, WaveTab T, WaveIO io,
                                                        CtaArgs A, CtaCtl* ctl) {
+  extern __shared__ __align__(16) unsigned char wsm[];
+  // per-candidate arrays in shared memory: each phase reads what the previous
+  // one wrote, so this removes an L2 round trip from most phase chains
+  if (A.smem) wave_smem_layout(A.cta_win, W.R, wsm, &io);
   __shared__ unsigned long long s_p, s_seg_end;
   __shared__ u32 s_ncand, s_jcur, s_exit, s_epoch, s_nacc, s_ncacc, s_base, s_kbase;
   __shared__ int s_rejoin_after;
@@ -1498,9 +1549,30 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       A.n_max = n_max;
       A.cta_win = CTA_WIN;
       A.pos = B.pos.p;
+      size_t smem_bytes = 0;
+      {
+        // a small window keeps most of the SM's L1 for the node table / analyses
+        const size_t WSMEM = 160u << 10;
+        u32 SWIN = 512;
+        size_t need = wave_smem_layout(SWIN, R, nullptr, nullptr);
+        if (need <= WSMEM) {
+          static int smem_set = 0;
+          if (!smem_set) {
+            CUDA_OK(cudaFuncSetAttribute(k_wave_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM));
+            smem_set = 1;
+          }
+          A.smem = 1;
+          A.cta_win = SWIN;
+          smem_bytes = need;
+          if (c.win > SWIN) {
+            c.win = SWIN;
+            CUDA_OK(cudaMemcpyAsync(B.ctl.p, &c, sizeof(c), cudaMemcpyHostToDevice, e.s));
+          }
+        }
+      }
       {
         KTimer kt(e, KG_APPLY_WAVE, 0.0, 1);
-        k_wave_cta<<<1, CTA_T, 0, e.s>>>(e.view(), Rd, RD, W, T, io, A, B.ctl.p);
+        k_wave_cta<<<1, CTA_T, smem_bytes, e.s>>>(e.view(), Rd, RD, W, T, io, A, B.ctl.p);
         CUDA_OK(cudaGetLastError());
         CUDA_OK(cudaMemcpyAsync(&c, B.ctl.p, sizeof(c), cudaMemcpyDeviceToHost, e.s));
         CUDA_OK(cudaMemcpyAsync(&e.h, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
