@@ -292,7 +292,9 @@ def main():
         barrier()
         if i >= args.warmup:
             e2e_s.append(max_over_ranks(dt))
-        d2h = 8 * eg2.allocated_nodes + 8 * len(res2.selection) + 4 * len(filt2) + 8 * 7 * len(rules) + 24 * 15
+        # selection (class, node) + the selected nodes' costs + filter ids + rule stats / per-iteration counts
+        d2h = (8 * len(res2.selection) + 8 * len(set(res2.selection.values())) + 4 * len(filt2)
+               + 8 * 7 * len(rules) + 24 * 15)
         del eg2
     e2e = statistics.mean(e2e_s) / (1 if shard_mode else world)
 

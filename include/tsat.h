@@ -123,6 +123,10 @@ int tsat_dfs_cycles(tsat_engine* h, uint32_t* nodes, int64_t cap, uint32_t* off,
 int tsat_costs(tsat_engine* h, int32_t mode, int32_t strict, int32_t ntab, const char* keys,
                const int64_t* key_off, const double* vals, double* out_by_node);
 
+/* entries of the device cost vector of the last tsat_costs (ids NULL: the
+ * first n); lets callers skip downloading c_i for every node */
+int tsat_costs_gather(tsat_engine* h, uint32_t n, const uint32_t* ids, double* out);
+
 /* extract.greedy_extract (extract.py:120-159); cost_by_node NULL = device
  * vector from the last tsat_costs */
 int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, uint32_t* sel_node,

@@ -67,6 +67,7 @@ _SIGS = {
     "tsat_break_cycles": ([C.c_void_p, i64p], C.c_int),
     "tsat_dfs_cycles": ([C.c_void_p, u32p, C.c_int64, u32p, C.c_int64, i64p], C.c_int),
     "tsat_costs": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, i64p, f64p, f64p], C.c_int),
+    "tsat_costs_gather": ([C.c_void_p, C.c_uint32, u32p, f64p], C.c_int),
     "tsat_greedy": ([C.c_void_p, f64p, u32p, u32p, u32p, f64p, i64p], C.c_int),
     "tsat_phase_times": ([C.c_void_p, f64p, C.c_int32], C.c_int),
     "tsat_debug_info": ([C.c_void_p, i64p, C.c_int32], C.c_int),

@@ -326,6 +326,10 @@ int tsat_costs(tsat_engine* h, int32_t mode, int32_t strict, int32_t ntab, const
   });
 }
 
+int tsat_costs_gather(tsat_engine* h, uint32_t n, const uint32_t* ids, double* out) {
+  GUARD(h, h->e->costs_gather(n, ids, out));
+}
+
 int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, uint32_t* sel_node, uint32_t* nsel,
                 double* root_best, int64_t* rounds) {
   GUARD(h, *root_best = h->e->greedy(cost_by_node, sel_cls, sel_node, nsel, rounds));

@@ -629,14 +629,37 @@ void Engine::set_filter(int n, const u32* ids, int on) {
   sync();
 }
 
+__global__ void k_filt_flags(const u8* flags, u32 n, u32* fl) {
+  GRID_STRIDE(i, n) fl[i] = (flags[i] & NF_FILT) ? 1u : 0u;
+}
+
+__global__ void k_filt_compact(const u32* fl, const u32* pos, u32 n, u32* out) {
+  GRID_STRIDE(i, n) if (fl[i]) out[pos[i]] = (u32)i;
+}
+
+// filter-listed node ids, ascending: compacted on the device (only the ids
+// cross PCIe, not a flag byte per node)
 std::vector<u32> Engine::get_filter() {
-  std::vector<u8> f(h.next_id);
-  if (h.next_id)
-    CUDA_OK(cudaMemcpyAsync(f.data(), flags.p, h.next_id, cudaMemcpyDeviceToHost, s));
-  sync();
+  u32 n = h.next_id;
   std::vector<u32> out;
-  for (u32 i = 0; i < h.next_id; i++)
-    if (f[i] & NF_FILT) out.push_back(i);
+  if (!n) return out;
+  DevBuf<u32>& fl = scratch_u32[1];
+  DevBuf<u32>& pos = scratch_u32[2];
+  DevBuf<u32>& ids = scratch_u32[3];
+  fl.ensure(n + 1);
+  pos.ensure(n + 1);
+  k_filt_flags<<<nblk(n), 256, 0, s>>>(flags.p, n, fl.p);
+  CUDA_OK(cudaMemsetAsync(fl.p + n, 0, sizeof(u32), s));
+  dev_exclusive_scan_u32(*this, fl.p, pos.p, n + 1);
+  u32 cnt = 0;
+  CUDA_OK(cudaMemcpyAsync(&cnt, pos.p + n, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
+  if (!cnt) return out;
+  ids.ensure(cnt + 1);
+  k_filt_compact<<<nblk(n), 256, 0, s>>>(fl.p, pos.p, n, ids.p);
+  out.resize(cnt);
+  CUDA_OK(cudaMemcpyAsync(out.data(), ids.p, cnt * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
   return out;
 }
 

@@ -360,6 +360,7 @@ struct Engine {
   void costs(int mode, int strict, int ntab, const char* keys, const i64* key_off, const double* vals,
              double* out);
   double greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u32* nsel, i64* rounds);
+  void costs_gather(u32 n, const u32* ids, double* out);
 
   // download
   void download(u32* op, u32* koff, u32* kids, u32* cls, u8* flags);

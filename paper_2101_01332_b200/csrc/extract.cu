@@ -331,6 +331,32 @@ static u64 fnv1a_host(const char* p, i64 n) {
   return h;
 }
 
+__global__ void k_gather_f64(const double* src, const u32* ids, u32 n, double* out) {
+  GRID_STRIDE(i, n) out[i] = src[ids[i]];
+}
+
+// c_i of selected nodes (ids == nullptr: the first n entries)
+void Engine::costs_gather(u32 n, const u32* ids, double* out) {
+  if (costs_valid_for != h.next_id) throw TsatException(TSAT_ERR_STATE, "device cost vector is stale");
+  if (!n) return;
+  if (!ids) {
+    if (n > h.next_id) throw TsatException(TSAT_ERR_ARG, "more entries than nodes");
+    CUDA_OK(cudaMemcpyAsync(out, d_costs.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    sync();
+    return;
+  }
+  for (u32 i = 0; i < n; i++)
+    if (ids[i] >= h.next_id) throw TsatException(TSAT_ERR_ARG, "node id out of range");
+  DevBuf<u32>& di = scratch_u32[0];
+  DevBuf<double>& dv = sc.g_c1;
+  di.ensure(n + 1);
+  dv.ensure(n + 1);
+  CUDA_OK(cudaMemcpyAsync(di.p, ids, n * sizeof(u32), cudaMemcpyHostToDevice, s));
+  k_gather_f64<<<nblk(n), 256, 0, s>>>(d_costs.p, di.p, n, dv.p);
+  CUDA_OK(cudaMemcpyAsync(out, dv.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  sync();
+}
+
 void Engine::costs(int mode, int strict, int ntab, const char* keys, const i64* key_off, const double* vals,
                    double* out) {
   if (!analysis) throw TsatException(TSAT_ERR_STATE, "egraph_costs needs the tensor analysis");

@@ -375,10 +375,13 @@ class EGraph:
     def get_filter(self) -> list:
         lib = _lib.load()
         n = C.c_int64()
-        _lib.check(self._h, lib.tsat_get_filter(self._h, None, 0, C.byref(n)))
-        out = np.zeros(max(n.value, 1), np.uint32)
-        _lib.check(self._h, lib.tsat_get_filter(self._h, _lib.ptr(out, C.c_uint32), len(out), C.byref(n)))
-        return [int(x) for x in out[: n.value]]
+        cap = 1024
+        while True:
+            out = np.zeros(cap, np.uint32)
+            _lib.check(self._h, lib.tsat_get_filter(self._h, _lib.ptr(out, C.c_uint32), cap, C.byref(n)))
+            if n.value <= cap:
+                return out[: n.value].tolist()
+            cap = int(n.value)
 
     def ematch(self, pattern: Term, filt=frozenset()) -> list:
         """All matches of ``pattern`` (egraph.py:248-262), computed on the GPU."""
@@ -452,7 +455,7 @@ class EGraph:
     def _device_costs(self, model) -> "CostVector":
         lib = _lib.load()
         n = self._sizes()[0]
-        out = np.zeros(max(n, 1), np.float64)
+        out = None  # the vector stays on the device; CostVector downloads it lazily
         if model.mode == "table":
             keys = [k.encode() for k in model.table]
             off = np.zeros(len(keys) + 1, np.int64)
@@ -460,33 +463,52 @@ class EGraph:
             vals = np.array(list(model.table.values()) or [0.0], np.float64)
             blob = b"".join(keys) + b"\0"
             _lib.check(self._h, lib.tsat_costs(self._h, 1, 1 if model.strict else 0, len(keys), blob,
-                                               _lib.ptr(off, C.c_int64), _lib.ptr(vals, C.c_double),
-                                               _lib.ptr(out, C.c_double)))
+                                               _lib.ptr(off, C.c_int64), _lib.ptr(vals, C.c_double), None))
         else:
-            _lib.check(self._h, lib.tsat_costs(self._h, 0, 0, 0, b"\0", None, None, _lib.ptr(out, C.c_double)))
-        return CostVector(self, out[:n], None)
+            _lib.check(self._h, lib.tsat_costs(self._h, 0, 0, 0, b"\0", None, None, None))
+        return CostVector(self, None, None, n)
 
 
 class CostVector(Mapping):
     """c_i per live node id (dict-like), backed by the device vector; the
-    live-node index is fetched lazily (only flags are downloaded)."""
+    host copy and the live-node index are fetched lazily, and ``gather`` reads
+    selected entries only (greedy_extract's total)."""
 
-    def __init__(self, eg: EGraph, arr: np.ndarray, alive):
+    def __init__(self, eg: EGraph, arr: Optional[np.ndarray], alive, n: Optional[int] = None):
         self._eg = eg
-        self.array = arr
+        self._arr = arr
+        self._n = len(arr) if arr is not None else int(n)
         self._alive = alive
         self._ids = None
 
+    @property
+    def array(self) -> np.ndarray:
+        if self._arr is None:
+            out = np.zeros(max(self._n, 1), np.float64)
+            _lib.check(self._eg._h, _lib.load().tsat_costs_gather(self._eg._h, self._n, None,
+                                                                  _lib.ptr(out, C.c_double)))
+            self._arr = out[: self._n]
+        return self._arr
+
+    def gather(self, ids) -> np.ndarray:
+        ids = np.asarray(ids, np.uint32)
+        if self._arr is not None:
+            return self._arr[ids]
+        out = np.zeros(max(len(ids), 1), np.float64)
+        _lib.check(self._eg._h, _lib.load().tsat_costs_gather(self._eg._h, len(ids), _lib.ptr(ids, C.c_uint32),
+                                                              _lib.ptr(out, C.c_double)))
+        return out[: len(ids)]
+
     def _index(self):
         if self._alive is None:
-            self._alive = self._eg._alive_flags()[: len(self.array)]
+            self._alive = self._eg._alive_flags()[: self._n]
         if self._ids is None:
             self._ids = np.nonzero(self._alive)[0]
         return self._ids
 
     def __getitem__(self, nid):
         nid = int(nid)
-        if nid < 0 or nid >= len(self.array):
+        if nid < 0 or nid >= self._n:
             raise KeyError(nid)
         self._index()
         if not self._alive[nid]:

@@ -73,7 +73,8 @@ def greedy_extract(eg: EGraph, costs: Mapping, filt: Iterable[int] = ()) -> Extr
     lib = _lib.load()
     n = eg.allocated_nodes
     arr = None
-    if not (isinstance(costs, CostVector) and costs._eg is eg and len(costs.array) == n):
+    on_device = isinstance(costs, CostVector) and costs._eg is eg and costs._n == n
+    if not on_device:
         arr = np.zeros(max(n, 1), np.float64)
         for nid in np.nonzero(eg._alive_flags())[0]:
             arr[nid] = costs[int(nid)]
@@ -86,8 +87,9 @@ def greedy_extract(eg: EGraph, costs: Mapping, filt: Iterable[int] = ()) -> Extr
     _lib.check(eg._h, lib.tsat_greedy(eg._h, _lib.ptr(arr, C.c_double), _lib.ptr(sc, C.c_uint32),
                                       _lib.ptr(sn, C.c_uint32), C.byref(k), C.byref(best), C.byref(rounds)))
     selection = dict(zip(sc[: k.value].tolist(), sn[: k.value].tolist()))
-    if isinstance(costs, CostVector) and costs._eg is eg:
-        total = float(sum(costs.array[list(set(selection.values()))].tolist()))
+    if on_device:
+        # the reference sums c_i over the Python set of selected nodes (extract.py:112-114)
+        total = float(sum(costs.gather(list(set(selection.values()))).tolist()))
     else:
         total = selection_cost(costs, selection)
     stats = SolverStats(nodes_explored=int(rounds.value), time_s=time.perf_counter() - t0)
