@@ -579,8 +579,38 @@ def _compile_pattern(pat: Term, atom_id) -> list:
     return out
 
 
+_RULESET_CACHE: dict = {}
+
+
 def compile_ruleset(eg: EGraph, rules, extra_patterns=()):
-    """Lower rules to the int64 blob of tsat_load_rules.  Returns (blob, pattern ids)."""
+    """Lower rules to the int64 blob of tsat_load_rules.  Returns (blob, pattern ids).
+
+    The blob depends on the rules and on the atom ids the e-graph has interned
+    so far; repeated explorations of the same graph with the same rule set
+    (pooled engines) reuse the compiled blob and replay the atom interning."""
+    atoms = getattr(eg, "_atom_list", None)
+    try:
+        key = None if atoms is None else ((type(eg).__name__,) + tuple((type(a) is int, a) for a in atoms),
+                                          tuple(rules), tuple(extra_patterns))
+        hit = None if key is None else _RULESET_CACHE.get(key)
+    except TypeError:  # unhashable rule / pattern objects: compile every time
+        key, hit = None, None
+    if hit is not None:
+        blob, pidx, new_atoms = hit
+        for a in new_atoms:
+            eg._atom(a)
+        eg._flush_atoms()
+        return blob, dict(pidx)
+    n_before = len(atoms) if atoms is not None else 0
+    blob, pidx = _compile_ruleset(eg, rules, extra_patterns)
+    if key is not None:
+        if len(_RULESET_CACHE) > 64:
+            _RULESET_CACHE.clear()
+        _RULESET_CACHE[key] = (blob, dict(pidx), list(eg._atom_list[n_before:]))
+    return blob, pidx
+
+
+def _compile_ruleset(eg: EGraph, rules, extra_patterns=()):
     pats: list = list(extra_patterns)
     pidx = {p: i for i, p in enumerate(pats)}
     rule_parts: list = []
