@@ -305,8 +305,15 @@ def main():
     with_bytes = [i for i in range(9) if per_step[1][i] > 0]
     dom = dom_all if per_step[1][dom_all] > 0 else (max(with_bytes, key=lambda i: per_step[0][i]) if with_bytes else 0)
     achieved = per_step[1][dom] / (per_step[0][dom] / 1e3) / 1e9 if per_step[0][dom] > 0 else 0.0
+    traffic = None
+    try:  # ncu DRAM bytes per launch of the same kernel group (committed capture)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+        if w["model"] == "bert" and KGROUPS[dom] in tr:
+            traffic = tr[KGROUPS[dom]]["dram_GB"] * 1e9
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": KERNEL_OF[KGROUPS[dom]], "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                 "launches_per_step": per_step[2][dom], "ms_per_step": per_step[0][dom],
                 "algorithmic_bytes_per_step": per_step[1][dom]}
     groups_ms = {KGROUPS[i]: round(per_step[0][i], 3) for i in range(9)}
