@@ -266,6 +266,7 @@ struct Engine {
   // rules
   std::vector<HPattern> patterns;
   std::vector<HRule> rules;
+  u64 rules_gen = 0;  // bumped by load_rules (wave templates are cached per generation)
   std::vector<MatchSet> matches;  // per pattern, current iteration
   DevBuf<Instr> d_instr;
   DevBuf<int> d_leaf;

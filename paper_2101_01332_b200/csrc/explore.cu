@@ -104,6 +104,7 @@ void Engine::load_rules(int n, const i64* b) {
   // cudaMalloc / cudaFree, whose implicit syncs made run times erratic)
   if (matches.size() < patterns.size()) matches.resize(patterns.size());
   for (auto& m : matches) m.n = 0;
+  rules_gen++;
   sync();
 }
 

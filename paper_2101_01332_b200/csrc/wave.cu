@@ -1237,6 +1237,25 @@ struct WaveBufs {
   u32 wcap = 0;
   u32 epoch = 0;  // per-wave tag of the wave table / first-writer arrays
   u64 cand_cap = 0;
+  // per-rule request templates, built once per loaded rule set
+  struct RuleWave {
+    std::vector<ReqT> tm;
+    WaveRule W;
+    std::vector<std::vector<int>> lv;
+    std::vector<int> lvl_off;
+    int R = 0, Kmax = 0;
+    size_t tmpl_base = 0, lvl_base = 0;
+  };
+  std::vector<RuleWave> rw;
+  u64 rw_gen = ~0ull;
+  DevBuf<ReqT> tmpl_all;
+  DevBuf<int> lvl_all;
+  CtaCtl* hctl = nullptr;       // pinned
+  Counters* hcnt = nullptr;     // pinned
+  ~WaveBufs() {
+    if (hctl) cudaFreeHost(hctl);
+    if (hcnt) cudaFreeHost(hcnt);
+  }
 };
 
 void free_wave_bufs(WaveBufs* b) { delete b; }
@@ -1435,26 +1454,46 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
   const HRule& hr = e.rules[ri];
   if (!e.wave) e.wave = new WaveBufs();
   WaveBufs& B = *e.wave;
-  std::vector<ReqT> tm;
-  WaveRule W;
-  std::vector<std::vector<int>> lv;
-  int R = 0;
-  build_wave_rule(hr, tm, W, lv, R);
-  B.tmpl.ensure(R + 1);
-  if (R) CUDA_OK(cudaMemcpyAsync(B.tmpl.p, tm.data(), R * sizeof(ReqT), cudaMemcpyHostToDevice, e.s));
-  W.tmpl = B.tmpl.p;
-  std::vector<int> lvl_flat, lvl_off;
-  for (auto& l : lv) {
-    lvl_off.push_back((int)lvl_flat.size());
-    lvl_flat.insert(lvl_flat.end(), l.begin(), l.end());
+  if (!B.hctl) {
+    CUDA_OK(cudaMallocHost((void**)&B.hctl, sizeof(CtaCtl)));
+    CUDA_OK(cudaMallocHost((void**)&B.hcnt, sizeof(Counters)));
   }
-  lvl_off.push_back((int)lvl_flat.size());
+  if (B.rw_gen != e.rules_gen) {
+    // templates of every rule of the loaded set, uploaded once
+    B.rw.assign(e.rules.size(), WaveBufs::RuleWave());
+    std::vector<ReqT> tall;
+    std::vector<int> lall;
+    for (size_t r = 0; r < e.rules.size(); r++) {
+      WaveBufs::RuleWave& x = B.rw[r];
+      if (e.rules[r].nsrc > MAX_SRC) continue;
+      build_wave_rule(e.rules[r], x.tm, x.W, x.lv, x.R);
+      for (auto& q : x.tm) x.Kmax += q.nargs;
+      x.tmpl_base = tall.size();
+      tall.insert(tall.end(), x.tm.begin(), x.tm.end());
+      x.lvl_base = lall.size();
+      for (auto& l : x.lv) {
+        x.lvl_off.push_back((int)(lall.size() - x.lvl_base));
+        lall.insert(lall.end(), l.begin(), l.end());
+      }
+      x.lvl_off.push_back((int)(lall.size() - x.lvl_base));
+    }
+    B.tmpl_all.ensure(tall.size() + 1);
+    B.lvl_all.ensure(lall.size() + 1);
+    if (!tall.empty())
+      CUDA_OK(cudaMemcpyAsync(B.tmpl_all.p, tall.data(), tall.size() * sizeof(ReqT), cudaMemcpyHostToDevice, e.s));
+    if (!lall.empty())
+      CUDA_OK(cudaMemcpyAsync(B.lvl_all.p, lall.data(), lall.size() * sizeof(int), cudaMemcpyHostToDevice, e.s));
+    B.rw_gen = e.rules_gen;
+  }
+  WaveBufs::RuleWave& RWc = B.rw[ri];
+  WaveRule W = RWc.W;
+  const std::vector<std::vector<int>>& lv = RWc.lv;
+  const int R = RWc.R;
+  W.tmpl = B.tmpl_all.p + RWc.tmpl_base;
+  const std::vector<int>& lvl_off = RWc.lvl_off;
   if (lv.size() > 12) throw TsatException(TSAT_ERR_UNSUPPORTED, "target deeper than the wave engine supports");
-  B.lvl.ensure(lvl_flat.size() + 1);
-  if (!lvl_flat.empty())
-    CUDA_OK(cudaMemcpyAsync(B.lvl.p, lvl_flat.data(), lvl_flat.size() * sizeof(int), cudaMemcpyHostToDevice, e.s));
-  int Kmax = 0;
-  for (auto& q : tm) Kmax += q.nargs;
+  int* lvl_dev = B.lvl_all.p + RWc.lvl_base;
+  const int Kmax = RWc.Kmax;
   int skip_self = (hr.nsrc == 2 && !allow_self && hr.same_canon) ? 1 : 0;
   const bool multi = hr.nsrc > 1;
   RuleStatsH& rs = e.rstats[ri];
@@ -1529,11 +1568,12 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       c.jtotal = jtotal;
       c.jcomplete = jcomplete ? 1 : 0;
       c.reason = CR_DONE;
-      CUDA_OK(cudaMemcpyAsync(B.ctl.p, &c, sizeof(c), cudaMemcpyHostToDevice, e.s));
+      *B.hctl = c;
+      CUDA_OK(cudaMemcpyAsync(B.ctl.p, B.hctl, sizeof(c), cudaMemcpyHostToDevice, e.s));
       WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0};
       WaveIO io{B.status.p, B.hazard.p, B.ukind.p, B.grow.p, B.sa.p, B.env.p, B.olds.p, B.pre.p, B.acc.p,
                 B.ident.p, B.alloc.p, B.apre.p, B.wf.p, B.wpre.p, B.ka.p, B.kpre.p, B.uother.p, B.stops.p,
-                B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, B.lvl.p};
+                B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, lvl_dev};
       CtaArgs A;
       memset(&A, 0, sizeof(A));
       A.nlv = (int)lv.size();
@@ -1566,7 +1606,8 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
           smem_bytes = need;
           if (c.win > SWIN) {
             c.win = SWIN;
-            CUDA_OK(cudaMemcpyAsync(B.ctl.p, &c, sizeof(c), cudaMemcpyHostToDevice, e.s));
+            *B.hctl = c;
+            CUDA_OK(cudaMemcpyAsync(B.ctl.p, B.hctl, sizeof(c), cudaMemcpyHostToDevice, e.s));
           }
         }
       }
@@ -1574,9 +1615,11 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         KTimer kt(e, KG_APPLY_WAVE, 0.0, 1);
         k_wave_cta<<<1, CTA_T, smem_bytes, e.s>>>(e.view(), Rd, RD, W, T, io, A, B.ctl.p);
         CUDA_OK(cudaGetLastError());
-        CUDA_OK(cudaMemcpyAsync(&c, B.ctl.p, sizeof(c), cudaMemcpyDeviceToHost, e.s));
-        CUDA_OK(cudaMemcpyAsync(&e.h, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
+        CUDA_OK(cudaMemcpyAsync(B.hctl, B.ctl.p, sizeof(c), cudaMemcpyDeviceToHost, e.s));
+        CUDA_OK(cudaMemcpyAsync(B.hcnt, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
         e.sync();
+        c = *B.hctl;
+        e.h = *B.hcnt;
         kt.bytes = wave_bytes(e, Rd, (double)c.s_cand, (double)c.s_req, (double)c.s_win, (double)c.s_nk);
       }
       B.epoch = c.epoch;
@@ -1656,7 +1699,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
           int nl = (int)lv[d].size();
           if (!nl) continue;
           k_resolve_level<<<nblk((u64)ncand * nl, 128), 128, 0, e.s>>>(e.view(), W, T, B.acc.p, ws,
-                                                                      B.lvl.p + lvl_off[d], nl, B.env.p, B.ident.p,
+                                                                      lvl_dev + lvl_off[d], nl, B.env.p, B.ident.p,
                                                                       B.hazard.p);
         }
         k_mark_roots<<<nblk(ncand), 256, 0, e.s>>>(W, T, B.acc.p, ws, B.ident.p, B.hazard.p, B.olds.p);
@@ -1683,7 +1726,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
                                                 B.wstats.p);
       // ---- 6. commit
       if (nreq_max) {
-        k_win_flags<<<nblk(nreq_max), 256, 0, e.s>>>(T, B.ident.p, nreq_max, B.tmpl.p, R, ws, B.wf.p, B.ka.p);
+        k_win_flags<<<nblk(nreq_max), 256, 0, e.s>>>(T, B.ident.p, nreq_max, W.tmpl, R, ws, B.wf.p, B.ka.p);
         if (nreq_max <= 65536) {
           k_scan_block<<<1, 1024, 0, e.s>>>(B.wf.p, B.wpre.p, (u32)nreq_max);
           k_scan_block<<<1, 1024, 0, e.s>>>(B.ka.p, B.kpre.p, (u32)nreq_max);
