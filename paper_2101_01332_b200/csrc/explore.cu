@@ -354,6 +354,13 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
     phase_ms[ph] += (n2 - t) * 1e3;
     t = n2;
   };
+  // a bounded search reserves its node / kid / hashcons capacity up front: a
+  // mid-apply growth (copy + rehash) costs more than the whole reservation
+  if (lim.n_max > 0 && lim.n_max < (1ll << 26) && (i64)h.next_id < 2 * lim.n_max) {
+    u64 extra = (u64)(2 * lim.n_max - (i64)h.next_id);
+    u64 avg_k = h.next_id ? ((u64)h.nkids + h.next_id - 1) / h.next_id : 2;
+    ensure_nodes(extra, extra * std::max<u64>(avg_k + 1, 3));
+  }
   double tp = now_s();
   for (i64 it = 0; it < lim.k_max; it++) {
     if (!snap.valid) build_snapshot();

@@ -25,9 +25,11 @@
 //                sequential order, node records, fresh-root unions, hashcons
 //                inserts.  The hazard combo itself runs on the exact
 //                sequential path (k_seq_rule) and the next wave starts after it.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 
@@ -480,31 +482,182 @@ __device__ __forceinline__ bool read_dirty(u32 id, u32 c, u32 epoch, const unsig
   return (u32)(v >> 32) == ~epoch && (u32)v < c;
 }
 
+#ifdef WAVE_DBG
+__device__ unsigned long long g_wdbg_first = ~0ull;
+__device__ unsigned long long g_wdbg_cnt[32];
+#define WDBG_CAT(k) \
+  if (bad && !dbg_cat) dbg_cat = (k)
+#define WDBG_SET(k) dbg_cat = (k)
+#else
+#define WDBG_CAT(k)
+#define WDBG_SET(k)
+#endif
+
+// class of a wave-start root at candidate c's turn: follow the drops of the
+// earlier first writers (each identity has at most one writer before the
+// first conflict, so the chain is exact up to there).  *grown: the root's
+// analysis was extended earlier in the wave.  TSAT_NONE if the chain is long.
+__device__ __forceinline__ u32 soft_find(u32 id, u32 c, u32 ep, const WaveRule& W, const unsigned long long* fw_cls,
+                                         const u32* accpre, const u32* olds, const u8* ukind, const u32* uother,
+                                         bool* grown) {
+  *grown = false;
+  for (int hop = 0; hop < 32; hop++) {
+    unsigned long long v = fw_cls[id];
+    if ((u32)(v >> 32) != ~ep || (u32)v >= c) return id;
+    u32 w = (u32)v, a = accpre[w], nxt = id;
+    for (int t = 0; t < W.ntgt; t++) {
+      if (ukind[(u64)a * MAX_SRC + t] != UK_CLASS) continue;
+      u32 o = olds[(u64)w * MAX_SRC + t], x = uother[(u64)a * MAX_SRC + t];
+      if ((o > x ? o : x) == id) nxt = o < x ? o : x;
+    }
+    if (nxt == id) {
+      *grown = true;
+      return id;
+    }
+    id = nxt;
+  }
+  return TSAT_NONE;
+}
+
+__device__ __forceinline__ bool cycle_hit(const RuleDev& R, const ReachDev& RD, const u32* env, const u32* outs) {
+  for (int t = 0; t < R.nsrc; t++)
+    for (int l = 0; l < R.leaf_len[t]; l++) {
+      u32 leaf = env[R.leaf[R.leaf_off[t] + l]];
+      if (leaf == outs[t] || reach_query(RD, leaf, outs[t])) return true;
+    }
+  return false;
+}
+
 // candidate validity against earlier writes in the wave (all candidates:
-// rejected ones read through their gates, accepted ones through requests)
-__device__ __forceinline__ void d_validity(u64 tid, u64 nth, const WaveRule& W, const WaveTab& T, int nslots,
-                                           int nsrc, u32 ncand, const u8* hazard, const u32* env, const u32* olds,
-                                           const u32* accpre, const u8* status, const u32* ident,
+// rejected ones read through their gates, accepted ones through requests).
+//
+// Reads of the classes a target is unioned with (the matched class and, for a
+// class merge, the class the target root resolved to) are soft: sequentially
+// the combo unions find(old) with find(other), so an earlier merge changes
+// only which roots meet, not what the combo builds.  A combo whose soft reads
+// are dirty is still exact here when it writes nothing:
+//   * a shape-rejected combo compared only the class's data (merges keep it);
+//   * a no-op target (its root resolved to the matched class) stays a no-op;
+//   * a fresh target root without analysis growth just joins the class
+//     (its parent may point at the old root: find() is the same);
+//   * the efficient cycle pre-filter is re-run with the current roots
+//     (reference cycles.py:163-168) and must give the gates' answer.
+// A combo that does write (class merge, fresh-node union, growth) is a soft
+// writer: with first_soft the caller resolves it (d_resolve_soft) and
+// re-runs the conflict pass; without, it ends the prefix like any conflict.
+// Reads of everything else (substitution classes, inner request classes)
+// are hard: an earlier write ends the prefix.
+__device__ __forceinline__ void d_validity(u64 tid, u64 nth, const WaveRule& W, const WaveTab& T, u32 ep,
+                                           const RuleDev& R, const ReachDev& RD, u32 ncand, const u8* hazard,
+                                           const u32* env, const u32* olds, const u32* accpre, const u8* status,
+                                           const u32* ident, const u8* ukind, const u8* grow, const u32* uother,
                                            const unsigned long long* fw_cls, const unsigned long long* fw_fresh,
-                                           u32* first_bad) {
-  u32 ep = T.epoch;
+                                           u32* first_bad, u32* first_soft) {
   TID_LOOP(c0, ncand) {
     u32 c = (u32)c0;
-    bool bad = hazard[c] != 0;
-    for (int v = 0; v < nslots && !bad; v++) bad = read_dirty(env[(u64)c * MAX_VARS + v], c, ep, fw_cls, fw_fresh);
-    for (int t = 0; t < nsrc && !bad; t++) bad = read_dirty(olds[(u64)c * MAX_SRC + t], c, ep, fw_cls, fw_fresh);
-    if (!bad && status[c] == 0) {
-      u32 a = accpre[c];
+    u8 st = status[c];
+    bool bad = hazard[c] != 0 || st > 2;
+#ifdef WAVE_DBG
+    int dbg_cat = 0;
+#endif
+    WDBG_CAT(1);
+    for (int v = 0; v < R.nslots && !bad; v++) bad = read_dirty(env[(u64)c * MAX_VARS + v], c, ep, fw_cls, fw_fresh);
+    WDBG_CAT(2);
+    u32 a = st == 0 ? accpre[c] : 0u;
+    bool writer = false, recheck = false;
+    for (int t = 0; t < R.nsrc && !bad; t++) {
+      u32 o = olds[(u64)c * MAX_SRC + t];
+      u8 k = st == 0 ? ukind[(u64)a * MAX_SRC + t] : (u8)UK_NONE;
+      bool dirty = read_dirty(o, c, ep, fw_cls, fw_fresh);
+      if (k == UK_CLASS) dirty |= read_dirty(uother[(u64)a * MAX_SRC + t], c, ep, fw_cls, fw_fresh);
+      if (!dirty) continue;
+      if (st == 0 && (k == UK_CLASS || k == UK_FRESH_NODE || (k == UK_FRESH_ROOT && grow[(u64)a * MAX_SRC + t])))
+        writer = true;
+      else if (st != 1)
+        recheck = true;
+    }
+    if (!bad && !writer && recheck && R.efficient) {  // cycle pre-filter at c's turn
+      u32 outs[MAX_SRC];
+      for (int t = 0; t < R.nsrc && !bad; t++) {
+        bool gr;
+        outs[t] = soft_find(olds[(u64)c * MAX_SRC + t], c, ep, W, fw_cls, accpre, olds, ukind, uother, &gr);
+        bad = outs[t] == TSAT_NONE;
+      }
+      if (!bad) bad = cycle_hit(R, RD, env + (u64)c * MAX_VARS, outs) != (st == 2);
+      WDBG_CAT(5);
+    }
+    if (!bad && st == 0) {
       for (int r = 0; r < W.R && !bad; r++) {
+        const ReqT& q = W.tmpl[r];
+        // a target root's class is a union side (above) unless it is a fresh
+        // node another combo may have merged
+        if (q.is_root && ukind[(u64)a * MAX_SRC + q.tgt] != UK_FRESH_NODE) continue;
         u32 id = ident[(u64)a * W.R + r];
         bad = read_dirty(id, c, ep, fw_cls, fw_fresh);
+        WDBG_CAT(q.is_root ? 7 : 6);
         // a reused target root resolves to the class it was merged into
         if (!bad && (id & FRESH) && is_wroot(T, id & ~FRESH))
           bad = read_dirty(T.wold[id & ~FRESH], c, ep, fw_cls, fw_fresh);
+        WDBG_CAT(8);
       }
     }
+    if (!bad && writer) {
+      if (first_soft) atomicMin(first_soft, c);
+      else bad = true;
+      WDBG_CAT(9);
+    }
     if (bad) atomicMin(first_bad, c);
+#ifdef WAVE_DBG
+    if (bad) atomicMin(&g_wdbg_first, ((unsigned long long)c << 8) | (dbg_cat ? dbg_cat : 31));
+#endif
   }
+}
+
+// Resolve soft writer c (one thread; every earlier writer is exact): its
+// union sides become the roots at its turn, its union kind / growth are
+// recomputed from them (a merge of two classes already joined is a no-op),
+// and the cycle pre-filter is re-checked.  false: not resolvable here (an
+// analysis that changed earlier in the wave, a merged fresh node, a change
+// in a non-final target) -- the prefix ends at c.
+__device__ bool d_resolve_soft(const G& g, const WaveRule& W, const WaveTab& T, u32 ep, const RuleDev& R,
+                               const ReachDev& RD, u32 c, const u32* env, u32* olds, const u32* accpre, u8* ukind,
+                               u32* uother, u8* grow, const unsigned long long* fw_cls,
+                               const unsigned long long* fw_fresh) {
+  u32 a = accpre[c];
+  u32 outs[MAX_SRC];
+  for (int t = 0; t < R.nsrc; t++) {
+    u64 ia = (u64)a * MAX_SRC + t, ic = (u64)c * MAX_SRC + t;
+    bool gro, grx;
+    u32 ro = soft_find(olds[ic], c, ep, W, fw_cls, accpre, olds, ukind, uother, &gro);
+    if (ro == TSAT_NONE) return false;
+    outs[t] = ro;
+    u8 k = ukind[ia];
+    if (k == UK_NONE) continue;
+    if (gro) return false;
+    u32 x = uother[ia];
+    u8 nk = k, ng = 0;
+    if (k == UK_CLASS) {
+      u32 rx = soft_find(x, c, ep, W, fw_cls, accpre, olds, ukind, uother, &grx);
+      if (rx == TSAT_NONE || grx) return false;
+      if (rx == ro) {
+        nk = UK_NONE;
+      } else {
+        u32 keep = ro < rx ? ro : rx, drop = ro < rx ? rx : ro;
+        ng = g.analysis && val_merge_grows(g.val[keep], g.val[drop]);
+      }
+      x = rx;
+    } else {
+      if (k == UK_FRESH_NODE && read_dirty(x, c, ep, fw_cls, fw_fresh)) return false;
+      ng = g.analysis && val_merge_grows(g.val[ro], T.val[x & ~FRESH]);
+    }
+    if (t < W.ntgt - 1 && (nk == UK_CLASS || nk == UK_FRESH_NODE || ng)) return false;
+    olds[ic] = ro;
+    ukind[ia] = nk;
+    uother[ia] = x;
+    grow[ia] = ng;
+  }
+  if (R.efficient && cycle_hit(R, RD, env + (u64)c * MAX_VARS, outs)) return false;
+  return true;
 }
 
 // first hazard (candidate index) and node-limit cutoff (accepted index)
@@ -739,11 +892,45 @@ __global__ void k_first_writer(WaveRule W, u32 epoch, const u32* acc, const Wave
   d_first_writer(GTID, GNTH, W, epoch, acc, ws->nacc, hazard, olds, ukind, uother, grow, fw_cls, fw_fresh);
 }
 
-__global__ void k_validity(WaveRule W, WaveTab T, int nslots, int nsrc, u32 ncand, const u8* hazard, const u32* env,
-                           const u32* olds, const u32* accpre, const u8* status, const u32* ident,
-                           const unsigned long long* fw_cls, const unsigned long long* fw_fresh, u32* first_bad) {
-  d_validity(GTID, GNTH, W, T, nslots, nsrc, ncand, hazard, env, olds, accpre, status, ident, fw_cls, fw_fresh,
-             first_bad);
+__global__ void k_validity(WaveRule W, WaveTab T, RuleDev R, ReachDev RD, u32 ncand, const u8* hazard,
+                           const u32* env, const u32* olds, const u32* accpre, const u8* status, const u32* ident,
+                           const u8* ukind, const u8* grow, const u32* uother, const unsigned long long* fw_cls,
+                           const unsigned long long* fw_fresh, u32* first_bad) {
+  d_validity(GTID, GNTH, W, T, T.epoch, R, RD, ncand, hazard, env, olds, accpre, status, ident, ukind, grow, uother,
+             fw_cls, fw_fresh, first_bad, nullptr);
+}
+
+// Conflict pass of a grid wave, iterated like the single-CTA loop: first
+// writers, validity, and (one thread) resolution of the first soft writer,
+// with grid-wide barriers in between (cooperative launch, co-resident grid).
+// Epochs ep0 .. ep0 + max_it tag the first-writer arrays.
+__global__ void k_conflicts_grid(G g, WaveRule W, WaveTab T, RuleDev R, ReachDev RD, const u32* acc,
+                                 const WaveState* ws, u32 ncand, u8* hazard, const u32* env, u32* olds,
+                                 const u32* accpre, u8* status, const u32* ident, u8* ukind, u8* grow, u32* uother,
+                                 unsigned long long* fw_cls, unsigned long long* fw_fresh, u32* stops, u32 ep0,
+                                 u32 max_it, u32* nresolved) {
+  cooperative_groups::grid_group gg = cooperative_groups::this_grid();
+  const u32 nacc = ws->nacc;
+  for (u32 it = 0;; it++) {
+    const u32 ep = ep0 + it;
+    d_first_writer(GTID, GNTH, W, ep, acc, nacc, hazard, olds, ukind, uother, grow, fw_cls, fw_fresh);
+    gg.sync();
+    d_validity(GTID, GNTH, W, T, ep, R, RD, ncand, hazard, env, olds, accpre, status, ident, ukind, grow, uother,
+               fw_cls, fw_fresh, stops + 2, stops + 3);
+    gg.sync();
+    const u32 fb = ((volatile u32*)stops)[2], sw = ((volatile u32*)stops)[3];
+    gg.sync();
+    if (sw == TSAT_NONE || sw >= fb) break;
+    if (GTID == 0) {
+      if (it + 1 >= max_it || !d_resolve_soft(g, W, T, ep, R, RD, sw, env, olds, accpre, ukind, uother, grow, fw_cls,
+                                              fw_fresh))
+        status[sw] = 3;
+      else
+        *nresolved += 1;
+      stops[2] = stops[3] = TSAT_NONE;
+    }
+    gg.sync();
+  }
 }
 
 __global__ void k_find_stops(const u32* acc, const WaveState* ws, const u8* stop_after, const u32* apre,
@@ -916,6 +1103,7 @@ struct CtaCtl {
   u32 reason;
   u32 waves, clean_full;
   u32 cuts[6];
+  u32 resolved;  // soft writers resolved inside waves
   unsigned long long found, self, compat;
   unsigned long long s_cand, s_req, s_win, s_nk;
   i64 overshoot;
@@ -933,6 +1121,7 @@ struct CtaArgs {
   u32 cta_win;
   const unsigned long long* pos;  // cached join list (multi)
   int smem;  // per-candidate wave arrays in shared memory (window <= cta_win)
+  u32 wide_after;  // clean full windows before handing over to the grid path
 };
 
 // shared-memory carve-out of the per-candidate wave arrays (window of `win`
@@ -1012,6 +1201,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
   __shared__ unsigned long long s_p, s_seg_end;
   __shared__ u32 s_ncand, s_jcur, s_exit, s_epoch, s_nacc, s_ncacc, s_base, s_kbase;
   __shared__ int s_rejoin_after;
+  __shared__ u32 s_wres;  // soft writers resolved in the current wave
   const u64 tid = threadIdx.x, nth = CTA_T;
   unsigned long long t_last = tid == 0 ? gtimer() : 0;
   if (tid == 0) {
@@ -1065,8 +1255,9 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
             s_ncand = ncand;
             s_seg_end = seg_end;
             s_epoch += 1;
+            s_wres = 0;
             ctl->waves += 1;
-            io.stops[0] = io.stops[1] = io.stops[2] = TSAT_NONE;
+            io.stops[0] = io.stops[1] = io.stops[2] = io.stops[3] = TSAT_NONE;
           }
         }
       }
@@ -1114,13 +1305,33 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
                  io.ukind, io.uother, io.grow, io.sa, io.akid);
     __syncthreads();
     WPROF(3);
-    // ---- conflicts, stop-after, node-limit cutoff, boundary
-    d_first_writer(tid, nth, W, Tw.epoch, io.acc, nacc, io.hazard, io.olds, io.ukind, io.uother, io.grow, io.fw_cls,
-                   io.fw_fresh);
-    __syncthreads();
+    // ---- conflicts (re-run while the first one is a soft writer that
+    // resolves), stop-after, node-limit cutoff, boundary
+    for (int it = 0;; it++) {
+      const u32 fwep = s_epoch;
+      d_first_writer(tid, nth, W, fwep, io.acc, nacc, io.hazard, io.olds, io.ukind, io.uother, io.grow, io.fw_cls,
+                     io.fw_fresh);
+      __syncthreads();
+      d_validity(tid, nth, W, Tw, fwep, R, RD, ncand, io.hazard, io.env, io.olds, io.pre, io.status, io.ident,
+                 io.ukind, io.grow, io.uother, io.fw_cls, io.fw_fresh, io.stops + 2, io.stops + 3);
+      __syncthreads();
+      const u32 fb = io.stops[2], sw = io.stops[3];
+      __syncthreads();
+      if (sw == TSAT_NONE || sw >= fb) break;
+      if (tid == 0) {
+        if (it >= 64 || !d_resolve_soft(g, W, Tw, fwep, R, RD, sw, io.env, io.olds, io.pre, io.ukind, io.uother,
+                                         io.grow, io.fw_cls, io.fw_fresh))
+          io.status[sw] = 3;  // ends the prefix
+        else {
+          ctl->resolved += 1;
+          s_wres += 1;
+        }
+        io.stops[2] = io.stops[3] = TSAT_NONE;
+        s_epoch += 1;  // fresh first-writer tags
+      }
+      __syncthreads();
+    }
     WPROF(4);
-    d_validity(tid, nth, W, Tw, R.nslots, R.nsrc, ncand, io.hazard, io.env, io.olds, io.pre, io.status, io.ident,
-               io.fw_cls, io.fw_fresh, io.stops + 2);
     block_scan2<CTA_T>(ncand, io.apre, io.ckpre,
                        [&](u32 c) { return ((unsigned long long)io.alloc[c] << 32) | io.akid[c]; });
     d_find_stops(tid, nth, io.acc, nacc, io.sa, io.apre, io.alloc, (i64)g.cnt->live, A.n_max, io.stops);
@@ -1128,6 +1339,11 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     WPROF(5);
     if (tid == 0) {
       d_boundary(io.ws, io.stops, ncand, posp, p, s_seg_end, io.pre, io.hazard);
+#ifdef WAVE_DBG
+      if (io.stops[2] != TSAT_NONE && io.ws->ncommit_cand == io.stops[2] && (g_wdbg_first >> 8) == io.stops[2])
+        g_wdbg_cnt[g_wdbg_first & 31] += 1;
+      g_wdbg_first = ~0ull;
+#endif
       s_ncacc = io.ws->ncommit_acc;
       s_base = g.cnt->next_id;
       s_kbase = g.cnt->nkids;
@@ -1188,14 +1404,17 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
           ctl->clean_full = 0;
         } else {
           win = win * 4u;
-          if (ncand >= A.cta_win) ctl->clean_full += 1;
+          // a wave that needed soft-writer resolutions would be cut on the
+          // grid path (which resolves only a few): stay here
+          if (s_wres) ctl->clean_full = 0;
+          else if (ncand >= A.cta_win) ctl->clean_full += 1;
         }
         if (win > A.cta_win) win = A.cta_win;
         ctl->win = win;
         if (hazard) exitr = CR_HAZARD;
         else if (A.multi && ws->sa_hit) exitr = CR_REJOIN;
         else if (s_rejoin_after) exitr = CR_REJOIN;
-        else if (ctl->clean_full >= 2) exitr = CR_WIDE;
+        else if (ctl->clean_full >= A.wide_after) exitr = CR_WIDE;
       }
       s_exit = exitr;
     }
@@ -1402,7 +1621,7 @@ static void ensure_cand_bufs(Engine& e, WaveBufs& B, u64 ncand, int R) {
   B.ka.ensure(nreq + 2);
   B.kpre.ensure(nreq + 2);
   B.ws.ensure(1);
-  B.stops.ensure(4);
+  B.stops.ensure(6);
   B.ctl.ensure(1);
   u64 want = 1024;
   while (want < 2 * nreq + 16) want *= 2;
@@ -1498,8 +1717,16 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
   const bool multi = hr.nsrc > 1;
   RuleStatsH& rs = e.rstats[ri];
   const double dbg_w0 = e.phase_ms[8], dbg_c0 = e.phase_ms[10];
+  static const bool dbg_waves = getenv("TSAT_DEBUG_WAVES") != nullptr;
+  std::chrono::steady_clock::time_point dbg_t0;
+  if (dbg_waves) {
+    e.sync();
+    dbg_t0 = std::chrono::steady_clock::now();
+  }
   B.wstats.ensure(1);
   CUDA_OK(cudaMemsetAsync(B.wstats.p, 0, sizeof(DevStats), e.s));
+  B.stops.ensure(6);
+  CUDA_OK(cudaMemsetAsync(B.stops.p + 4, 0, sizeof(u32), e.s));  // grid-wave soft writers resolved
   // multi-pattern join cache: compatible positions stay valid until a union of
   // existing classes changes find() (stop-after waves / exact-path combos)
   bool jvalid = false, jcomplete = true;
@@ -1588,6 +1815,10 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       A.nB = multi ? Rd.nmatch[1] : 1;
       A.n_max = n_max;
       A.cta_win = CTA_WIN;
+      {
+        static const char* wa = getenv("TSAT_WIDE_AFTER");
+        A.wide_after = wa ? (u32)atoi(wa) : 2u;
+      }
       A.pos = B.pos.p;
       size_t smem_bytes = 0;
       {
@@ -1622,6 +1853,10 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         e.h = *B.hcnt;
         kt.bytes = wave_bytes(e, Rd, (double)c.s_cand, (double)c.s_req, (double)c.s_win, (double)c.s_nk);
       }
+      if (dbg_waves)
+        fprintf(stderr, "   cta: reason %u waves %u cand %llu resolved %u p %llu/%llu prof %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f | %.3f ms\n", c.reason, c.waves,
+                c.s_cand, c.resolved, c.p, P, c.prof[0]*1e-6, c.prof[1]*1e-6, c.prof[2]*1e-6, c.prof[3]*1e-6, c.prof[4]*1e-6, c.prof[5]*1e-6, c.prof[6]*1e-6, c.prof[7]*1e-6, c.prof[8]*1e-6, c.prof[9]*1e-6, c.prof[10]*1e-6, c.prof[11]*1e-6,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0).count());
       B.epoch = c.epoch;
       rs.found += c.found;
       rs.skipped_self += c.self;
@@ -1629,6 +1864,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       e.phase_ms[8] += c.waves;
       for (int k = 0; k < 6; k++) e.phase_ms[10 + k] += c.cuts[k];
       for (int k = 0; k < 12; k++) e.phase_ms[16 + k] += c.prof[k] * 1e-6;
+      e.phase_ms[28] += c.resolved;
       p = c.p;
       jcursor = c.jcursor;
       win = c.win;
@@ -1675,8 +1911,20 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       }
     }
     // ---- 2. gates + accepted list
+    double dbg_ens = 0;
+    unsigned long long dbg_al = g_dev_allocs;
+    if (dbg_waves) {
+      e.sync();
+      dbg_ens = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0).count();
+    }
     e.ensure_nodes((u64)ncand * R + 2, (u64)ncand * Kmax + 2);
     ensure_cand_bufs(e, B, ncand, R);
+    if (dbg_waves) {
+      e.sync();
+      fprintf(stderr, "   grid: ensure %.3f ms (cap_nodes %u, %llu cudaMallocs)\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0).count() - dbg_ens,
+              e.cap_nodes, g_dev_allocs - dbg_al);
+    }
     WaveState* ws = B.ws.p;
     u64 nreq_max = (u64)ncand * R;
     WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, ++B.epoch};
@@ -1708,11 +1956,30 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
                                                  multi ? 1 : 0, B.hazard.p, B.alloc.p, B.ukind.p, B.uother.p,
                                                  B.grow.p, B.sa.p, B.akid.p);
       // ---- 4. read/write conflicts, stop-after, node-limit cutoff, boundary
-      k_first_writer<<<nblk(ncand), 256, 0, e.s>>>(W, T.epoch, B.acc.p, ws, B.hazard.p, B.olds.p, B.ukind.p,
-                                                   B.uother.p, B.grow.p, B.fw_cls.p, B.fw_fresh.p);
-      CUDA_OK(cudaMemsetAsync(B.stops.p, 0xFF, 3 * sizeof(u32), e.s));
-      k_validity<<<nblk(ncand), 256, 0, e.s>>>(W, T, Rd.nslots, Rd.nsrc, ncand, B.hazard.p, B.env.p, B.olds.p, B.pre.p,
-                                               B.status.p, B.ident.p, B.fw_cls.p, B.fw_fresh.p, B.stops.p + 2);
+      CUDA_OK(cudaMemsetAsync(B.stops.p, 0xFF, 4 * sizeof(u32), e.s));
+      {
+        static int coop_blocks = 0;
+        if (!coop_blocks) {
+          int per_sm = 0, nsm = 0, dev = 0;
+          CUDA_OK(cudaGetDevice(&dev));
+          CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+          CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conflicts_grid, 256, 0));
+          coop_blocks = std::max(1, std::min(per_sm, 4)) * nsm;
+        }
+        const u32 max_it = 4;
+        u32 ep0 = ++B.epoch;
+        B.epoch += max_it;
+        G gv = e.view();
+        const u32* accp = B.acc.p;
+        u32 nc = ncand;
+        u32* resp = B.stops.p + 4;
+        void* args[] = {&gv,       &W,         &T,         &Rd,      &RD,      &accp,    &ws,
+                        &nc,       &B.hazard.p, &B.env.p,  &B.olds.p, &B.pre.p, &B.status.p, &B.ident.p,
+                        &B.ukind.p, &B.grow.p,  &B.uother.p, &B.fw_cls.p, &B.fw_fresh.p, &B.stops.p, &ep0,
+                        (void*)&max_it, &resp};
+        unsigned nb = (unsigned)std::min<u64>((u64)coop_blocks, std::max<u64>(1, ((u64)ncand + 255) / 256));
+        CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_conflicts_grid, nb, 256, args, 0, e.s));
+      }
       if (ncand <= 65536) {
         k_scan_block<<<1, 1024, 0, e.s>>>(B.alloc.p, B.apre.p, ncand);
       } else {
@@ -1755,6 +2022,10 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     e.kstat[KG_APPLY_WAVE].bytes += wave_bytes(e, Rd, ncand, (double)hw.nacc * R, hw.nwin, hw.nk);
     u32 ncommit_cand = hw.ncommit_cand;
     unsigned long long p_end = hw.p_end;
+    if (dbg_waves)
+      fprintf(stderr, "   grid: ncand %u nacc %u commit %u why %u p %llu/%llu | %.3f ms\n", ncand, hw.nacc,
+              hw.ncommit_cand, hw.why, p_end, P,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0).count());
     bool stop = hw.stop != 0, hazard = hw.hazard != 0;
     if (hw.ncommit_cand < ncand && !stop) e.phase_ms[10 + std::min<int>(hw.why, 5)] += 1;
     {
@@ -1792,11 +2063,25 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     p = p_end;
   }
   DevStats d;
+  u32 gres = 0;
   CUDA_OK(cudaMemcpyAsync(&d, B.wstats.p, sizeof(d), cudaMemcpyDeviceToHost, e.s));
+  CUDA_OK(cudaMemcpyAsync(&gres, B.stops.p + 4, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
   e.sync();
+  e.phase_ms[29] += gres;
   accumulate_seg(e, ri, d);
-  if (getenv("TSAT_DEBUG_WAVES"))
-    fprintf(stderr, "rule %d %s P=%llu waves=%.0f cuts=%.0f applied=%llu live=%u\n", ri,
+  if (dbg_waves)
+    fprintf(stderr, "rule %d %s P=%llu waves=%.0f cuts=%.0f applied=%llu live=%u %.3f ms\n", ri,
             ri < (int)e.rule_names.size() ? e.rule_names[ri].c_str() : "?", P, e.phase_ms[8] - dbg_w0,
-            e.phase_ms[10] - dbg_c0, (unsigned long long)d.applied, e.h.live);
+            e.phase_ms[10] - dbg_c0, (unsigned long long)d.applied, e.h.live,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0).count());
+#ifdef WAVE_DBG
+  if (getenv("TSAT_DEBUG_WAVES")) {
+    unsigned long long cnt[32];
+    CUDA_OK(cudaMemcpyFromSymbol(cnt, g_wdbg_cnt, sizeof(cnt)));
+    fprintf(stderr, "  bad-read categories:");
+    for (int i = 0; i < 32; i++)
+      if (cnt[i]) fprintf(stderr, " %d:%llu", i, cnt[i]);
+    fprintf(stderr, "\n");
+  }
+#endif
 }

@@ -38,9 +38,9 @@ for i in range(int(__import__("os").environ.get("REPS", "4"))):
     f(0)
     print(f"[{i}] saturate {1e3*(t1-t0):.1f} costs {1e3*(t2-t1):.1f} greedy {1e3*(t3-t2):.1f} total {1e3*(t3-t0):.1f} ms nodes {rep.enodes_per_iter} iters {rep.iterations}")
     print("   levels %d peeled %d classes %d class-edges %d alloc %d live %d | cudaMallocs so far %d (%.1f MB) engines %d" % (dbg[0], dbg[1], dbg[2], dbg[3], dbg[6], dbg[7], dbg[8], dbg[9] / 1e6, dbg[10]))
-    print("   phases(ms) snap %.2f reach %.2f ematch %.2f apply %.2f rebuild %.2f cycles %.2f | waves %d hazards %d why %s" % (
-        ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[8], ph[9], ph[10:16].astype(int).tolist()))
-    names = ["gates", "accept", "resolve", "candchk", "firstw", "valid+stops", "boundary", "commit", "unions", "insert", "bookkeep", "top"]
+    print("   phases(ms) snap %.2f reach %.2f ematch %.2f apply %.2f rebuild %.2f cycles %.2f | waves %d hazards %d why %s resolved %d+%d" % (
+        ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[8], ph[9], ph[10:16].astype(int).tolist(), ph[28], ph[29]))
+    names = ["gates", "accept", "resolve", "candchk", "conflicts", "stops", "boundary", "commit", "unions", "insert", "bookkeep", "top"]
     print("   wave-cta phases(ms): " + " ".join(f"{n} {ph[16+k]:.2f}" for k, n in enumerate(names)))
     print("   kgroups(ms/launches): " + "  ".join(f"{G[k]} {ms[k]:.2f}/{la[k]}" for k in range(9)))
     del eg

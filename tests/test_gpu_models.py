@@ -18,10 +18,12 @@ CASES = [
     ("nasrnn", 0, 50000),        # configs[0]: single-pattern rules only
     ("bert", 1, 6000),           # configs[1] at a reduced node limit (oracle time)
     ("bert", 1, 20000),
+    ("bert", 1, 50000),          # configs[1] as benchmarked (soft-writer resolution in every wave)
     ("squeezenet", 2, 100000),   # configs[2]
     ("resnext50", 2, 100000),
     ("inception_v3", 2, 6000),   # configs[3]
     ("inception_v3", 2, 15000),
+    ("inception_v3", 2, 50000),
     ("nasnet_a", 2, 50000),
 ]
 
