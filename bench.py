@@ -56,7 +56,7 @@ KERNEL_OF = {"rebuild": "rebuild round (k_canon_kids+k_dedup_insert+k_dedup_drop
              "ematch": "e-match (k_ematch + radix ordering + unique)",
              "greedy": "greedy (k_greedy_levels/_wide + selection BFS)",
              "reach": "descendants bitset (peel + k_close_block/level)", "apply_seq": "k_seq_rule",
-             "apply_wave": "wave apply (k_wave_cta single-CTA waves; grid waves: k_gates, k_resolve_level, k_cand_check, k_validity, commit kernels)",
+             "apply_wave": "wave apply (k_wave_cta single-CTA waves; grid waves: k_gates, k_resolve_level, k_cand_check, k_conflicts_grid, commit kernels)",
              "costs": "k_node_costs", "cycles": "cycle check (peel/BFS/DFS)", "snapshot": "snapshot CSR"}
 
 

@@ -7,6 +7,7 @@
 // (k_seq_rule, the reference loop run by one GPU thread) and the parallel
 // wave path (wave.cu) that handles hazard-free prefixes in bulk and falls
 // back to k_seq_rule for exactly one combo at each hazard.
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 
@@ -406,6 +407,18 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
     if (filter_mode != 0) report.postprocess_filtered += break_all_cycles(false, nullptr);
     tick(5, tp);
     report.iterations = it + 1;
+    {
+      static const bool dbg_it = getenv("TSAT_DEBUG_ITERS") != nullptr;
+      static double last[6];
+      if (dbg_it) {
+        if (it == 0)
+          for (int q = 0; q < 6; q++) last[q] = 0;
+        fprintf(stderr, "iter %lld: snap %.3f reach %.3f ematch %.3f apply %.3f rebuild %.3f cycles %.3f ms live %u\n",
+                (long long)it, phase_ms[0] - last[0], phase_ms[1] - last[1], phase_ms[2] - last[2],
+                phase_ms[3] - last[3], phase_ms[4] - last[4], phase_ms[5] - last[5], h.live);
+        for (int q = 0; q < 6; q++) last[q] = phase_ms[q];
+      }
+    }
     enodes_per_iter.push_back(h.live);
     alloc_per_iter.push_back(h.next_id);
     eclasses_per_iter.push_back(snap.ncls);

@@ -1024,16 +1024,51 @@ __device__ __forceinline__ void block_scan2(u32 n, u32* out_a, u32* out_b, F f) 
   __syncthreads();
 }
 
+// block-wide exclusive scan over tiles of BT * IT elements, IT consecutive
+// elements per thread (independent loads in flight); total at out[n]
+template <int BT, int IT, class F>
+__device__ __forceinline__ u32 block_scan_tiled(u32 n, u32* out, F f) {
+  typedef cub::BlockScan<u32, BT> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ u32 carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u32 base = 0; base < n; base += BT * IT) {
+    u32 i0 = base + threadIdx.x * IT;
+    u32 v[IT], sum = 0;
+#pragma unroll
+    for (int k = 0; k < IT; k++) {
+      v[k] = i0 + k < n ? f(i0 + k) : 0u;
+      sum += v[k];
+    }
+    u32 x, tot;
+    BS(tmp).ExclusiveSum(sum, x, tot);
+    x += carry;
+#pragma unroll
+    for (int k = 0; k < IT; k++) {
+      if (i0 + k < n) out[i0 + k] = x;
+      x += v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  u32 total = carry;
+  if (threadIdx.x == 0) out[n] = total;
+  __syncthreads();
+  return total;
+}
+
 // single-CTA exclusive scan with the total at out[n] (small arrays; CUB's two
 // kernels cost more than the work at wave sizes)
 __global__ void __launch_bounds__(1024) k_scan_block(const u32* in, u32* out, u32 n) {
-  block_scan<1024>(n, out, [&](u32 i) { return in[i]; });
+  block_scan_tiled<1024, 8>(n, out, [&](u32 i) { return in[i]; });
 }
 
 // accepted list (status 0 or flagged) in candidate order; ws->nacc
 __global__ void __launch_bounds__(1024) k_accept_scan(const u8* status, const u8* hazard, u32 n, u32* pre, u32* acc,
                                                       WaveState* ws) {
-  u32 tot = block_scan<1024>(n, pre, [&](u32 c) { return (status[c] == 0 || hazard[c]) ? 1u : 0u; });
+  u32 tot = block_scan_tiled<1024, 8>(n, pre, [&](u32 c) { return (status[c] == 0 || hazard[c]) ? 1u : 0u; });
   for (u32 c = threadIdx.x; c < n; c += 1024)
     if (status[c] == 0 || hazard[c]) acc[pre[c]] = c;
   if (threadIdx.x == 0) ws->nacc = tot;
@@ -1966,7 +2001,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
           CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conflicts_grid, 256, 0));
           coop_blocks = std::max(1, std::min(per_sm, 4)) * nsm;
         }
-        const u32 max_it = 4;
+        static const u32 max_it = getenv("TSAT_GRID_RESOLVE") ? (u32)atoi(getenv("TSAT_GRID_RESOLVE")) : 4u;
         u32 ep0 = ++B.epoch;
         B.epoch += max_it;
         G gv = e.view();
