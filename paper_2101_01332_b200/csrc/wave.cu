@@ -84,6 +84,8 @@ struct WaveTab {  // wave-local key table; every tag carries the wave's epoch
   u32 mask;
   u32* wold;      // matched (old) class of a root winner's target
   u32 epoch;
+  unsigned long long* tag;  // grid waves: (epoch << 32) | key-hash high word per slot
+  u32* own;                 // grid waves: request that claimed the slot
 };
 
 // ---------------------------------------------------------------- join
@@ -309,6 +311,111 @@ __device__ __forceinline__ void d_resolve_level(u64 tid, u64 nth, const G& g, co
         continue;
       }
       T.val[s] = v;  // every request with this key computes identical bytes
+    }
+  }
+}
+
+// Grid waves resolve a level in two kernels instead of one fenced insert:
+//   claim   — a request whose key is not in the hashcons claims a slot by a
+//             CAS of (epoch, key hash) (equal hashes share the slot; the CAS
+//             winner records itself as the slot's owner);
+//   verify  — after the kernel boundary every sharer compares its key with the
+//             owner's (recomputed from the owner's request), takes part in the
+//             min-position election, and the owner stores the slot's analysis.
+// No key is stored and no fence is needed: the launch boundary orders both
+// passes.  A 64-bit hash collision between different keys marks the combo
+// for the exact path.
+__device__ __forceinline__ int req_key(const WaveRule& W, const u32* ident, const u32* env, u32 a, u32 c, int r,
+                                       u32* kids) {
+  const ReqT& q = W.tmpl[r];
+  for (int j = 0; j < q.nargs; j++) {
+    int k = q.kid[j];
+    kids[j] = k >= 0 ? ident[(u64)a * W.R + k] : env[(u64)c * MAX_VARS + (-k - 1)];
+  }
+  return q.nargs;
+}
+
+__global__ void k_resolve_claim(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws,
+                                const int* lvl_req, int nlvl, const u32* env, u32* ident, const u8* hazard) {
+  const u32 nacc = ws->nacc;
+  GRID_STRIDE(t, (u64)nacc * nlvl) {
+    u32 a = (u32)(t / nlvl);
+    int r = lvl_req[t % nlvl];
+    u32 c = acc[a];
+    u64 gpos = (u64)a * W.R + r;
+    if (hazard[c]) {
+      ident[gpos] = TSAT_NONE;
+      continue;
+    }
+    const ReqT& q = W.tmpl[r];
+    u32 kids[8];
+    int n = req_key(W, ident, env, a, c, r, kids);
+    bool real = true;
+    for (int j = 0; j < n; j++) real &= !(kids[j] & FRESH);
+    if (real) {
+      u32 hit = hc_lookup(g, q.atom, n, kids);
+      if (hit != TSAT_NONE) {
+        ident[gpos] = uf_find_rw(g.parent, hit);
+        continue;
+      }
+    }
+    u64 h = wkey_hash(q.atom, n, kids);
+    unsigned long long mine = ((unsigned long long)T.epoch << 32) | (u32)(h >> 32);
+    u32 slot = (u32)h & T.mask;
+    while (true) {
+      unsigned long long cur = T.tag[slot];
+      if ((u32)(cur >> 32) != T.epoch) {
+        unsigned long long prev = atomicCAS(&T.tag[slot], cur, mine);
+        if (prev == cur) {
+          T.own[slot] = (u32)gpos;
+          break;
+        }
+        cur = prev;
+      }
+      if (cur == mine) break;
+      slot = (slot + 1) & T.mask;
+    }
+    ident[gpos] = FRESH | slot;
+  }
+}
+
+__global__ void k_resolve_verify(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws,
+                                 const int* lvl_req, int nlvl, const u32* env, const u32* ident, u8* hazard) {
+  const u32 nacc = ws->nacc;
+  GRID_STRIDE(t, (u64)nacc * nlvl) {
+    u32 a = (u32)(t / nlvl);
+    int r = lvl_req[t % nlvl];
+    u64 gpos = (u64)a * W.R + r;
+    u32 id = ident[gpos];
+    if (id == TSAT_NONE || !(id & FRESH)) continue;
+    u32 s = id & ~FRESH, c = acc[a];
+    const ReqT& q = W.tmpl[r];
+    u32 kids[8];
+    int n = req_key(W, ident, env, a, c, r, kids);
+    u32 own = T.own[s];
+    if (own != (u32)gpos) {
+      u32 ao = own / (u32)W.R;
+      int ro = (int)(own % (u32)W.R);
+      const ReqT& qo = W.tmpl[ro];
+      bool eq = qo.atom == q.atom && qo.nargs == q.nargs;
+      if (eq) {
+        u32 ko[8];
+        req_key(W, ident, env, ao, acc[ao], ro, ko);
+        for (int j = 0; j < n && eq; j++) eq = ko[j] == kids[j];
+      }
+      if (!eq) {
+        hazard[c] = 2;  // hash collision: the exact path decides
+        continue;
+      }
+    }
+    atomicMin(&T.minpos[s], mp_tag(T.epoch, gpos));
+    if (g.analysis) {
+      const Val* kv[8];
+      for (int j = 0; j < n; j++) kv[j] = (kids[j] & FRESH) ? &T.val[kids[j] & ~FRESH] : &g.val[kids[j]];
+      Val v;
+      int st = val_make(q.atom, ValRefs{kv}, n, v, g.atoms, g.tt);
+      if (st != AS_OK) hazard[c] = 2;
+      else if (own == (u32)gpos) T.val[s] = v;
     }
   }
 }
@@ -1485,7 +1592,8 @@ struct WaveBufs {
   DevBuf<int> lvl;
   DevBuf<ReqT> tmpl;
   // wave table
-  DevBuf<u32> wstate, wkey, wid, wroot, wold;
+  DevBuf<u32> wstate, wkey, wid, wroot, wold, wown;
+  DevBuf<unsigned long long> wtag;
   DevBuf<unsigned long long> wminpos;
   DevBuf<Val> wval;
   u32 wcap = 0;
@@ -1670,6 +1778,9 @@ static void ensure_cand_bufs(Engine& e, WaveBufs& B, u64 ncand, int R) {
     B.wminpos.alloc(want);
     B.wval.alloc(want);
     B.fw_fresh.alloc(want + 1);
+    B.wtag.alloc(want);
+    B.wown.alloc(want);
+    CUDA_OK(cudaMemsetAsync(B.wtag.p, 0, want * sizeof(unsigned long long), e.s));
     CUDA_OK(cudaMemsetAsync(B.wstate.p, 0, want * sizeof(u32), e.s));
     CUDA_OK(cudaMemsetAsync(B.wroot.p, 0, want * sizeof(u32), e.s));
     CUDA_OK(cudaMemsetAsync(B.wminpos.p, 0xFF, want * sizeof(unsigned long long), e.s));
@@ -1832,7 +1943,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       c.reason = CR_DONE;
       *B.hctl = c;
       CUDA_OK(cudaMemcpyAsync(B.ctl.p, B.hctl, sizeof(c), cudaMemcpyHostToDevice, e.s));
-      WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0};
+      WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0, B.wtag.p, B.wown.p};
       WaveIO io{B.status.p, B.hazard.p, B.ukind.p, B.grow.p, B.sa.p, B.env.p, B.olds.p, B.pre.p, B.acc.p,
                 B.ident.p, B.alloc.p, B.apre.p, B.wf.p, B.wpre.p, B.ka.p, B.kpre.p, B.uother.p, B.stops.p,
                 B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, lvl_dev};
@@ -1962,7 +2073,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     }
     WaveState* ws = B.ws.p;
     u64 nreq_max = (u64)ncand * R;
-    WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, ++B.epoch};
+    WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, ++B.epoch, B.wtag.p, B.wown.p};
     {
       KTimer kt(e, KG_APPLY_WAVE, 0.0, 16 + lv.size());
       k_gates<<<nblk(ncand, 128), 128, 0, e.s>>>(e.view(), Rd, RD, W, posp, ncand, p, B.status.p, B.env.p, B.olds.p,
@@ -1981,9 +2092,12 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         for (size_t d = 1; d < lv.size(); d++) {
           int nl = (int)lv[d].size();
           if (!nl) continue;
-          k_resolve_level<<<nblk((u64)ncand * nl, 128), 128, 0, e.s>>>(e.view(), W, T, B.acc.p, ws,
+          k_resolve_claim<<<nblk((u64)ncand * nl, 128), 128, 0, e.s>>>(e.view(), W, T, B.acc.p, ws,
                                                                       lvl_dev + lvl_off[d], nl, B.env.p, B.ident.p,
                                                                       B.hazard.p);
+          k_resolve_verify<<<nblk((u64)ncand * nl, 128), 128, 0, e.s>>>(e.view(), W, T, B.acc.p, ws,
+                                                                       lvl_dev + lvl_off[d], nl, B.env.p, B.ident.p,
+                                                                       B.hazard.p);
         }
         k_mark_roots<<<nblk(ncand), 256, 0, e.s>>>(W, T, B.acc.p, ws, B.ident.p, B.hazard.p, B.olds.p);
       }
