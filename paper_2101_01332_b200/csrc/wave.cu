@@ -75,8 +75,6 @@ struct WaveRule {
 };
 
 struct WaveTab {  // wave-local key table; every tag carries the wave's epoch
-  u32* state;     // epoch << 2 | {1 busy, 2 ready}; another epoch = empty
-  u32* key;       // 10 words per slot: op, nargs, kids[8]
   unsigned long long* minpos;  // (~epoch << 32) | min request position
   u32* wid;       // assigned node id of the winner
   u32* wroot;     // == epoch: winner is a target root
@@ -84,8 +82,8 @@ struct WaveTab {  // wave-local key table; every tag carries the wave's epoch
   u32 mask;
   u32* wold;      // matched (old) class of a root winner's target
   u32 epoch;
-  unsigned long long* tag;  // grid waves: (epoch << 32) | key-hash high word per slot
-  u32* own;                 // grid waves: request that claimed the slot
+  unsigned long long* tag;  // (epoch << 32) | key-hash high word per slot
+  u32* own;                 // request that claimed the slot
 };
 
 // ---------------------------------------------------------------- join
@@ -235,95 +233,15 @@ __device__ __forceinline__ u64 wkey_hash(u32 op, int n, const u32* k) {
   return h;
 }
 
-// find-or-insert a key; returns slot.  state = epoch << 2 | {1 busy, 2 ready};
-// a slot whose epoch is not the current one is empty.
-template <bool CTA>
-__device__ __forceinline__ void wfence() {
-  if (CTA) __threadfence_block();
-  else __threadfence();
-}
-
-template <bool CTA>
-__device__ u32 wtab_get(const WaveTab& T, u32 op, int n, const u32* k) {
-  u32 slot = (u32)wkey_hash(op, n, k) & T.mask;
-  const u32 busy = (T.epoch << 2) | 1u, ready = (T.epoch << 2) | 2u;
-  while (true) {
-    u32 st = ((volatile u32*)T.state)[slot];
-    if ((st >> 2) != T.epoch) {
-      if (atomicCAS(&T.state[slot], st, busy) == st) {
-        u32* kk = T.key + (u64)slot * 10;
-        kk[0] = op;
-        kk[1] = (u32)n;
-        for (int i = 0; i < 8; i++) kk[2 + i] = i < n ? k[i] : 0u;
-        wfence<CTA>();
-        atomicExch(&T.state[slot], ready);
-        return slot;
-      }
-      st = ((volatile u32*)T.state)[slot];
-    }
-    while (st == busy) st = ((volatile u32*)T.state)[slot];
-    wfence<CTA>();
-    const volatile u32* kk = T.key + (u64)slot * 10;
-    bool eq = kk[0] == op && kk[1] == (u32)n;
-    for (int i = 0; i < n && eq; i++) eq = kk[2 + i] == k[i];
-    if (eq) return slot;
-    slot = (slot + 1) & T.mask;
-  }
-}
-
-// one request level: thread per (accepted combo, template at this depth)
-template <bool CTA>
-__device__ __forceinline__ void d_resolve_level(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
-                                                const u32* acc, u32 nacc, const int* lvl_req, int nlvl,
-                                                const u32* env, u32* ident, u8* hazard) {
-  TID_LOOP(t, (u64)nacc * nlvl) {
-    u32 a = (u32)(t / nlvl);
-    int r = lvl_req[t % nlvl];
-    u32 c = acc[a];
-    if (hazard[c]) continue;
-    const ReqT& q = W.tmpl[r];
-    u32 kids[8];
-    bool real = true;
-    for (int j = 0; j < q.nargs; j++) {
-      int k = q.kid[j];
-      u32 v = k >= 0 ? ident[(u64)a * W.R + k] : env[(u64)c * MAX_VARS + (-k - 1)];
-      kids[j] = v;
-      real &= !(v & FRESH);
-    }
-    u64 gpos = (u64)a * W.R + r;
-    if (real) {
-      u32 hit = hc_lookup(g, q.atom, q.nargs, kids);
-      if (hit != TSAT_NONE) {
-        ident[gpos] = uf_find_rw(g.parent, hit);
-        continue;
-      }
-    }
-    u32 s = wtab_get<CTA>(T, q.atom, q.nargs, kids);
-    atomicMin(&T.minpos[s], mp_tag(T.epoch, gpos));
-    ident[gpos] = FRESH | s;
-    if (g.analysis) {
-      const Val* kv[8];
-      for (int j = 0; j < q.nargs; j++) kv[j] = (kids[j] & FRESH) ? &T.val[kids[j] & ~FRESH] : &g.val[kids[j]];
-      Val v;
-      int st = val_make(q.atom, ValRefs{kv}, q.nargs, v, g.atoms, g.tt);
-      if (st != AS_OK) {
-        hazard[c] = 2;
-        continue;
-      }
-      T.val[s] = v;  // every request with this key computes identical bytes
-    }
-  }
-}
-
-// Grid waves resolve a level in two kernels instead of one fenced insert:
+// A request level resolves in two passes instead of one fenced key insert:
 //   claim   — a request whose key is not in the hashcons claims a slot by a
 //             CAS of (epoch, key hash) (equal hashes share the slot; the CAS
 //             winner records itself as the slot's owner);
-//   verify  — after the kernel boundary every sharer compares its key with the
+//   verify  — after the barrier every sharer compares its key with the
 //             owner's (recomputed from the owner's request), takes part in the
 //             min-position election, and the owner stores the slot's analysis.
-// No key is stored and no fence is needed: the launch boundary orders both
-// passes.  A 64-bit hash collision between different keys marks the combo
+// No key is stored and no fence is needed: the barrier between the passes
+// (kernel boundary on grid waves, __syncthreads in k_wave_cta) orders them.  A 64-bit hash collision between different keys marks the combo
 // for the exact path.
 __device__ __forceinline__ int req_key(const WaveRule& W, const u32* ident, const u32* env, u32 a, u32 c, int r,
                                        u32* kids) {
@@ -335,10 +253,10 @@ __device__ __forceinline__ int req_key(const WaveRule& W, const u32* ident, cons
   return q.nargs;
 }
 
-__global__ void k_resolve_claim(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws,
-                                const int* lvl_req, int nlvl, const u32* env, u32* ident, const u8* hazard) {
-  const u32 nacc = ws->nacc;
-  GRID_STRIDE(t, (u64)nacc * nlvl) {
+__device__ __forceinline__ void d_resolve_claim(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
+                                                const u32* acc, u32 nacc, const int* lvl_req, int nlvl,
+                                                const u32* env, u32* ident, const u8* hazard) {
+  TID_LOOP(t, (u64)nacc * nlvl) {
     u32 a = (u32)(t / nlvl);
     int r = lvl_req[t % nlvl];
     u32 c = acc[a];
@@ -379,10 +297,10 @@ __global__ void k_resolve_claim(G g, WaveRule W, WaveTab T, const u32* acc, cons
   }
 }
 
-__global__ void k_resolve_verify(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws,
-                                 const int* lvl_req, int nlvl, const u32* env, const u32* ident, u8* hazard) {
-  const u32 nacc = ws->nacc;
-  GRID_STRIDE(t, (u64)nacc * nlvl) {
+__device__ __forceinline__ void d_resolve_verify(u64 tid, u64 nth, const G& g, const WaveRule& W, const WaveTab& T,
+                                                 const u32* acc, u32 nacc, const int* lvl_req, int nlvl,
+                                                 const u32* env, const u32* ident, u8* hazard) {
+  TID_LOOP(t, (u64)nacc * nlvl) {
     u32 a = (u32)(t / nlvl);
     int r = lvl_req[t % nlvl];
     u64 gpos = (u64)a * W.R + r;
@@ -976,9 +894,14 @@ __global__ void k_accept_list(const u32* fl, const u32* pre, u32 n, u32* acc) {
   GRID_STRIDE(c, n) if (fl[c]) acc[pre[c]] = (u32)c;
 }
 
-__global__ void k_resolve_level(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const int* lvl_req,
-                                int nlvl, const u32* env, u32* ident, u8* hazard) {
-  d_resolve_level<false>(GTID, GNTH, g, W, T, acc, ws->nacc, lvl_req, nlvl, env, ident, hazard);
+__global__ void k_resolve_claim(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const int* lvl_req,
+                                int nlvl, const u32* env, u32* ident, const u8* hazard) {
+  d_resolve_claim(GTID, GNTH, g, W, T, acc, ws->nacc, lvl_req, nlvl, env, ident, hazard);
+}
+
+__global__ void k_resolve_verify(G g, WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const int* lvl_req,
+                                 int nlvl, const u32* env, const u32* ident, u8* hazard) {
+  d_resolve_verify(GTID, GNTH, g, W, T, acc, ws->nacc, lvl_req, nlvl, env, ident, hazard);
 }
 
 __global__ void k_mark_roots(WaveRule W, WaveTab T, const u32* acc, const WaveState* ws, const u32* ident,
@@ -1435,8 +1358,11 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     if (W.R > 0) {
       for (int d = 1; d < A.nlv; d++) {
         if (!A.nlvl[d]) continue;
-        d_resolve_level<true>(tid, nth, g, W, Tw, io.acc, nacc, io.lvl + A.lvl_off[d], A.nlvl[d], io.env, io.ident,
+        d_resolve_claim(tid, nth, g, W, Tw, io.acc, nacc, io.lvl + A.lvl_off[d], A.nlvl[d], io.env, io.ident,
                         io.hazard);
+        __syncthreads();
+        d_resolve_verify(tid, nth, g, W, Tw, io.acc, nacc, io.lvl + A.lvl_off[d], A.nlvl[d], io.env, io.ident,
+                         io.hazard);
         __syncthreads();
       }
       d_mark_roots(tid, nth, W, Tw, io.acc, nacc, io.ident, io.hazard, io.olds);
@@ -1592,7 +1518,7 @@ struct WaveBufs {
   DevBuf<int> lvl;
   DevBuf<ReqT> tmpl;
   // wave table
-  DevBuf<u32> wstate, wkey, wid, wroot, wold, wown;
+  DevBuf<u32> wid, wroot, wold, wown;
   DevBuf<unsigned long long> wtag;
   DevBuf<unsigned long long> wminpos;
   DevBuf<Val> wval;
@@ -1770,8 +1696,6 @@ static void ensure_cand_bufs(Engine& e, WaveBufs& B, u64 ncand, int R) {
   while (want < 2 * nreq + 16) want *= 2;
   if (want > B.wcap) {
     B.wcap = (u32)want;
-    B.wstate.alloc(want);
-    B.wkey.alloc(want * 10);
     B.wid.alloc(want);
     B.wroot.alloc(want);
     B.wold.alloc(want);
@@ -1781,7 +1705,6 @@ static void ensure_cand_bufs(Engine& e, WaveBufs& B, u64 ncand, int R) {
     B.wtag.alloc(want);
     B.wown.alloc(want);
     CUDA_OK(cudaMemsetAsync(B.wtag.p, 0, want * sizeof(unsigned long long), e.s));
-    CUDA_OK(cudaMemsetAsync(B.wstate.p, 0, want * sizeof(u32), e.s));
     CUDA_OK(cudaMemsetAsync(B.wroot.p, 0, want * sizeof(u32), e.s));
     CUDA_OK(cudaMemsetAsync(B.wminpos.p, 0xFF, want * sizeof(unsigned long long), e.s));
     CUDA_OK(cudaMemsetAsync(B.fw_fresh.p, 0xFF, (want + 1) * sizeof(unsigned long long), e.s));
@@ -1943,7 +1866,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       c.reason = CR_DONE;
       *B.hctl = c;
       CUDA_OK(cudaMemcpyAsync(B.ctl.p, B.hctl, sizeof(c), cudaMemcpyHostToDevice, e.s));
-      WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0, B.wtag.p, B.wown.p};
+      WaveTab T{B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0, B.wtag.p, B.wown.p};
       WaveIO io{B.status.p, B.hazard.p, B.ukind.p, B.grow.p, B.sa.p, B.env.p, B.olds.p, B.pre.p, B.acc.p,
                 B.ident.p, B.alloc.p, B.apre.p, B.wf.p, B.wpre.p, B.ka.p, B.kpre.p, B.uother.p, B.stops.p,
                 B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, lvl_dev};
@@ -2073,7 +1996,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     }
     WaveState* ws = B.ws.p;
     u64 nreq_max = (u64)ncand * R;
-    WaveTab T{B.wstate.p, B.wkey.p, B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, ++B.epoch, B.wtag.p, B.wown.p};
+    WaveTab T{B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, ++B.epoch, B.wtag.p, B.wown.p};
     {
       KTimer kt(e, KG_APPLY_WAVE, 0.0, 16 + lv.size());
       k_gates<<<nblk(ncand, 128), 128, 0, e.s>>>(e.view(), Rd, RD, W, posp, ncand, p, B.status.p, B.env.p, B.olds.p,
