@@ -519,9 +519,13 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
       sync();
     }
     for (int b = 0; b < np; b++) matches[live[b]].n = nuniq[b + 1] - nuniq[b];
-    if (dbg)
+    if (dbg) {
       fprintf(stderr, "ematch batch: %d patterns, %u candidates, %u rows, %u unique, %.3f ms\n", np, ntot, nrows,
               nuniq[np], wall_ms() - w0);
+      fprintf(stderr, "  per pattern (id:rows):");
+      for (int b = 0; b < np; b++) fprintf(stderr, " %d:%u", pids[b], B.rbase[b + 1] - B.rbase[b]);
+      fprintf(stderr, "\n");
+    }
     // algorithmic bytes: candidate scan + match rows written,
     // ordered and compacted
     double rows_bytes = 0;

@@ -1243,7 +1243,7 @@ __device__ __forceinline__ unsigned long long self_in(u32 nA, u32 nB, unsigned l
   return hi > lo ? hi - lo : 0;
 }
 
-#define CTA_T 512
+#define CTA_T 1024
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -1802,7 +1802,8 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
   u32 jtotal = 0, jcursor = 0;
   const u32 JCAP = 1u << 24;
   unsigned long long p = 0;
-  u32 win = 1u << 12;  // adaptive candidate window (grows on clean waves, shrinks on dependencies)
+  static const u32 win0 = getenv("TSAT_WIN0") ? (u32)atoi(getenv("TSAT_WIN0")) : (1u << 12);
+  u32 win = win0;  // adaptive candidate window (grows on clean waves, shrinks on dependencies)
   while (p < P) {
     // budget check at the segment's first position (explorer.py:198-206)
     if ((i64)e.h.live >= n_max) {
@@ -1886,14 +1887,14 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       A.cta_win = CTA_WIN;
       {
         static const char* wa = getenv("TSAT_WIDE_AFTER");
-        A.wide_after = wa ? (u32)atoi(wa) : 2u;
+        A.wide_after = wa ? (u32)atoi(wa) : 8u;
       }
       A.pos = B.pos.p;
       size_t smem_bytes = 0;
       {
         // a small window keeps most of the SM's L1 for the node table / analyses
         const size_t WSMEM = 160u << 10;
-        u32 SWIN = 512;
+        u32 SWIN = wave_smem_layout(CTA_T, R, nullptr, nullptr) <= WSMEM ? CTA_T : 512u;
         size_t need = wave_smem_layout(SWIN, R, nullptr, nullptr);
         if (need <= WSMEM) {
           static int smem_set = 0;
