@@ -105,6 +105,16 @@ int tsat_load_rules(tsat_engine* h, int64_t n, const int64_t* blob);
  * RuleStats field order, per_iter = 3 x k_max (enodes, alloc, eclasses) */
 int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self,
                   tsat_report* rep, int64_t* rule_stats, int64_t* per_iter);
+/* filter_mode: 0 "none", 1 "vanilla" (apply on a checkpoint + cycle check per combo,
+ * cycles.py:248-254), 2 "efficient" (descendants pre-filter, cycles.py:151-169) */
+
+/* on_reject support (explorer.py:223-224): with recording on, tsat_saturate keeps
+ * every cycle-rejected combo as [rule, nsrc, (eclass, nb, bindings[nb]) x nsrc]
+ * (bindings in sorted canonical-variable order); tsat_rejects copies them out
+ * (size query with out = NULL).  Efficient mode records through the exact
+ * sequential path. */
+int tsat_set_record_rejects(tsat_engine* h, int32_t on);
+int tsat_rejects(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n);
 
 /* EGraph.ematch of a loaded canonical pattern (egraph.py:248-262) */
 int tsat_ematch(tsat_engine* h, int32_t pattern, uint32_t* out_cls, uint32_t* out_bind, int64_t cap,

@@ -223,6 +223,19 @@ int tsat_get_filter(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n) {
   });
 }
 
+int tsat_set_record_rejects(tsat_engine* h, int32_t on) { GUARD(h, h->e->record_rejects = on != 0); }
+
+int tsat_rejects(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n) {
+  GUARD(h, {
+    const std::vector<u32>& r = h->e->rejects;
+    *n = (int64_t)r.size();
+    if (out) {
+      if (cap < (int64_t)r.size()) throw TsatException(TSAT_ERR_VALUE, "reject buffer too small");
+      if (!r.empty()) memcpy(out, r.data(), r.size() * sizeof(u32));
+    }
+  });
+}
+
 int tsat_load_rules(tsat_engine* h, int64_t n, const int64_t* blob) { GUARD(h, h->e->load_rules((int)n, blob)); }
 
 int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self, tsat_report* rep,
@@ -232,8 +245,9 @@ int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, i
     if (lim->n_max < 0 || lim->k_max < 0 || lim->k_multi < 0)
       throw TsatException(TSAT_ERR_VALUE, "limits must be non-negative");
     if (lim->k_multi > lim->k_max) throw TsatException(TSAT_ERR_VALUE, "k_multi must be <= k_max");
-    if (filter_mode < 0 || filter_mode > 2 || filter_mode == 1)
-      throw TsatException(TSAT_ERR_UNSUPPORTED, "filter_mode must be 'none' or 'efficient'");
+    if (filter_mode < 0 || filter_mode > 2)
+      throw TsatException(TSAT_ERR_VALUE, "filter_mode must be 'none', 'vanilla' or 'efficient'");
+    e.rejects.clear();
     ExploreLimitsC L{lim->n_max, lim->k_max, lim->k_multi, lim->time_limit_s};
     e.saturate(L, filter_mode, allow_self, nullptr, 0);
     rep->iterations = e.report.iterations;

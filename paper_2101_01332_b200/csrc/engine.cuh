@@ -142,6 +142,8 @@ struct DevStats {
   u32 overshoot;
   u32 resume_set;  // capacity stop: resume position valid
   unsigned long long resume_pos;
+  u32 vpend;       // vanilla: combo at resume_pos awaits its apply-on-checkpoint check
+  u32 nrej;        // entries written to RuleDev::rej_log
 };
 
 struct Snapshot {
@@ -217,6 +219,10 @@ struct Scratch {
   DevBuf<double> gq_pack, gq_recv;  // sharded wide levels: {best cost, node} records
   DevBuf<double> gq_cost, gq_tot;
   DevBuf<i64> k_off;
+  // vanilla checkpoint (explore.cu run_rule_vanilla)
+  DevBuf<u32> v_parent, v_rej;
+  DevBuf<Val> v_val;
+  DevBuf<unsigned long long> v_hc;
   // api
   DevBuf<Instr> a_prog;
   DevBuf<int32_t> a_len;
@@ -356,6 +362,12 @@ struct Engine {
                 int n_active);
   void run_rule_seq(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long p0,
                     unsigned long long p1);
+  void run_rule_vanilla(int ri, int allow_self, i64 n_max, unsigned long long P);
+  // on_reject support: rejected combos of the last saturate, flattened as
+  // [rule, nsrc, (eclass, nb, bindings[nb]) x nsrc] (snapshot match rows)
+  bool record_rejects = false;
+  std::vector<u32> rejects;
+  void record_reject(int ri, unsigned long long p);
 
   // extraction
   void costs(int mode, int strict, int ntab, const char* keys, const i64* key_off, const double* vals,

@@ -118,6 +118,8 @@ RuleDev make_rule_dev(Engine& e, int ri, int filter_mode, int allow_self) {
   R.same_canon = hr.same_canon;
   R.allow_self = allow_self;
   R.efficient = filter_mode == 2;
+  R.vanilla = filter_mode == 1;
+  R.vanilla_go = ~0ull;
   R.max_req = hr.max_req;
   int mk = 0;
   size_t ioff = 0, loff = 0;
@@ -244,8 +246,30 @@ __global__ void k_seq_rule(G g, RuleDev R, ReachDev RD, DevStats* st, unsigned l
       if (hit) {
         st->prefilter_rejects++;
         st->skipped_cycle++;
+        if (R.rej_log) {
+          if (st->nrej >= R.rej_cap) {  // log full: resume here after the host drains it
+            st->prefilter_rejects--;
+            st->skipped_cycle--;
+            st->prefilter_checks--;
+            st->found--;
+            st->resume_set = 1;
+            st->resume_pos = p;
+            return;
+          }
+          R.rej_log[2 * st->nrej] = (u32)(p >> 32);
+          R.rej_log[2 * st->nrej + 1] = (u32)p;
+          st->nrej++;
+        }
         continue;
       }
+    }
+    // vanilla (cycles.py:248-254): the host applies this combo on a
+    // checkpoint and runs the cycle check from the root
+    if (R.vanilla && p != R.vanilla_go) {
+      st->found--;  // counted again by the apply launch
+      st->vpend = 1;
+      st->resume_pos = p;
+      return;
     }
     // _apply_combo (explorer.py:146-163)
     u32 before = c->next_id;
@@ -305,6 +329,11 @@ void Engine::run_rule_seq(int ri, int filter_mode, int allow_self, i64 n_max, un
                           unsigned long long p1) {
   RuleDev R = make_rule_dev(*this, ri, filter_mode, allow_self);
   ReachDev RD = make_reach_dev(*this);
+  if (record_rejects && R.efficient) {
+    R.rej_cap = 4096;
+    sc.v_rej.ensure(2 * R.rej_cap);
+    R.rej_log = sc.v_rej.p;
+  }
   unsigned long long p = p0;
   while (p < p1) {
     CUDA_OK(cudaMemsetAsync(dstats.p, 0, sizeof(DevStats), s));
@@ -328,10 +357,126 @@ void Engine::run_rule_seq(int ri, int filter_mode, int allow_self, i64 n_max, un
         throw TsatException(ex.code, "unsound rule '" + rule_names[ri] + "': " + ex.what());
       throw;
     }
+    if (d.nrej) {
+      std::vector<u32> lg(2 * (size_t)d.nrej);
+      CUDA_OK(cudaMemcpyAsync(lg.data(), R.rej_log, lg.size() * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      sync();
+      for (u32 k = 0; k < d.nrej; k++) record_reject(ri, ((unsigned long long)lg[2 * k] << 32) | lg[2 * k + 1]);
+    }
     if (d.stop) return;
     if (!d.resume_set) return;
     p = d.resume_pos;
     ensure_nodes(4096 + (u64)R.max_req * 64, 4096 + (u64)R.max_kids * 64);
+  }
+}
+
+// One rejected combo -> [rule, nsrc, (eclass, nb, bindings) x nsrc] from the
+// iteration's match rows (the reference hands on_reject the Match objects).
+void Engine::record_reject(int ri, unsigned long long p) {
+  const HRule& hr = rules[ri];
+  rejects.push_back((u32)ri);
+  rejects.push_back((u32)hr.nsrc);
+  unsigned long long q = p;
+  u32 idx[MAX_SRC];
+  for (int t = hr.nsrc - 1; t >= 0; t--) {  // itertools.product: last source fastest
+    u32 n = matches[hr.src_pat[t]].n;
+    idx[t] = (u32)(q % n);
+    q /= n;
+  }
+  for (int t = 0; t < hr.nsrc; t++) {
+    const MatchSet& m = matches[hr.src_pat[t]];
+    u32 row[1 + MAX_VARS];
+    CUDA_OK(cudaMemcpyAsync(row, m.cls.p + idx[t], sizeof(u32), cudaMemcpyDeviceToHost, s));
+    if (m.nb)
+      CUDA_OK(cudaMemcpyAsync(row + 1, m.bind.p + (u64)idx[t] * m.nb, m.nb * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    sync();
+    rejects.push_back(row[0]);
+    rejects.push_back((u32)m.nb);
+    for (int j = 0; j < m.nb; j++) rejects.push_back(row[1 + j]);
+  }
+}
+
+// filter_mode "vanilla" (explorer.py:218-220, cycles.py:248-254): every combo
+// that passes the self / compat / shape gates is applied on the live e-graph
+// after a device-to-device checkpoint of the mutable state (union-find
+// parents, analysis values, hashcons, counters); a cycle check from the root
+// over the un-rebuilt result (peel + reachability, the precheck of
+// break_all_cycles) decides, and a cycle restores the checkpoint.  Applying
+// on the original instead of a clone gives the same e-graph: the apply is
+// deterministic.  Cost: O(N) device work per checked combo, by design (the
+// paper's baseline that the efficient pre-filter replaces).
+void Engine::run_rule_vanilla(int ri, int allow_self, i64 n_max, unsigned long long P) {
+  RuleDev R = make_rule_dev(*this, ri, 1, allow_self);
+  ReachDev RD = make_reach_dev(*this);
+  auto launch = [&](const RuleDev& Rx, unsigned long long a, unsigned long long b, DevStats& d) {
+    CUDA_OK(cudaMemsetAsync(dstats.p, 0, sizeof(DevStats), s));
+    {
+      KTimer kt(*this, KG_APPLY_SEQ, 0.0, 1);
+      k_seq_rule<<<1, 1, 0, s>>>(view(), Rx, RD, dstats.p, a, b, n_max);
+    }
+    CUDA_OK(cudaMemcpyAsync(&d, dstats.p, sizeof(d), cudaMemcpyDeviceToHost, s));
+    pull_counters();
+    try {
+      check_error();
+    } catch (TsatException& ex) {
+      if (ex.code == TSAT_ERR_MERGE)
+        throw TsatException(ex.code, "unsound rule '" + rule_names[ri] + "': " + ex.what());
+      throw;
+    }
+  };
+  unsigned long long p = 0;
+  while (p < P) {
+    DevStats d;
+    launch(R, p, P, d);
+    accumulate(*this, ri, d);
+    if (d.stop) {
+      seq_stop = true;
+      report.node_limit_overshoot = d.overshoot;
+      return;
+    }
+    if (d.resume_set) {  // capacity
+      p = d.resume_pos;
+      ensure_nodes(4096 + (u64)R.max_req * 64, 4096 + (u64)R.max_kids * 64);
+      continue;
+    }
+    if (!d.vpend) return;
+    const unsigned long long q = d.resume_pos;
+    ensure_nodes(4096 + (u64)R.max_req * 64, 4096 + (u64)R.max_kids * 64);
+    // checkpoint
+    const u32 n0 = h.next_id;
+    const Counters h0 = h;
+    sc.v_parent.ensure(n0 + 1);
+    sc.v_hc.ensure((size_t)hc_cap);
+    CUDA_OK(cudaMemcpyAsync(sc.v_parent.p, parent.p, (size_t)n0 * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(sc.v_hc.p, hc.p, (size_t)hc_cap * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    if (analysis) {
+      sc.v_val.ensure(n0 + 1);
+      CUDA_OK(cudaMemcpyAsync(sc.v_val.p, val.p, (size_t)n0 * sizeof(Val), cudaMemcpyDeviceToDevice, s));
+    }
+    RuleDev R1 = R;
+    R1.vanilla_go = q;
+    DevStats d1;
+    launch(R1, q, q + 1, d1);
+    if (d1.resume_set || d1.stop || d1.vpend)
+      throw TsatException(TSAT_ERR_STATE, "vanilla check: unexpected stop of the single-combo apply");
+    snap.valid = false;
+    bool cyc = break_all_cycles(true, nullptr) < 0;
+    if (cyc) {
+      CUDA_OK(cudaMemcpyAsync(parent.p, sc.v_parent.p, (size_t)n0 * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+      CUDA_OK(cudaMemcpyAsync(hc.p, sc.v_hc.p, (size_t)hc_cap * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+      if (analysis)
+        CUDA_OK(cudaMemcpyAsync(val.p, sc.v_val.p, (size_t)n0 * sizeof(Val), cudaMemcpyDeviceToDevice, s));
+      h = h0;
+      push_counters();
+      snap.valid = false;
+      rstats[ri].found++;
+      rstats[ri].skipped_cycle++;
+      if (record_rejects) record_reject(ri, q);
+    } else {
+      accumulate(*this, ri, d1);
+      if (d1.changed) seq_changed = true;
+    }
+    p = q + 1;
   }
 }
 
@@ -447,6 +592,8 @@ void Engine::apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsi
   int R = 0;
   for (auto& t : hr.targets)
     for (auto& in : t) R += in.kind == I_APP;
-  if (hr.nsrc <= 2 && R <= 32 && !force_seq) run_rule_wave(*this, ri, filter_mode, allow_self, n_max, P);
+  if (filter_mode == 1) run_rule_vanilla(ri, allow_self, n_max, P);
+  else if (hr.nsrc <= 2 && R <= 32 && !force_seq && !(record_rejects && filter_mode == 2))
+    run_rule_wave(*this, ri, filter_mode, allow_self, n_max, P);
   else run_rule_seq(ri, filter_mode, allow_self, n_max, 0, P);
 }

@@ -13,6 +13,10 @@ struct RuleDev {
   int leaf_off[MAX_SRC], leaf_len[MAX_SRC];
   const Instr* instr;
   const int* leaf;
+  int vanilla;                     // filter_mode "vanilla": stop before the cycle gate
+  unsigned long long vanilla_go;   // ... except at this position (apply it)
+  u32* rej_log;                    // efficient-mode reject positions (on_reject), or null
+  u32 rej_cap;
 };
 
 struct ReachDev {

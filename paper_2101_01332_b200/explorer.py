@@ -17,6 +17,7 @@ import numpy as np
 from . import _lib
 from .egraph import EGraph, compile_ruleset
 from .errors import TensorSatError
+from .rules import Match
 from .tensor_lang import TensorGraph, build_egraph
 
 FILTER_MODES = ("none", "vanilla", "efficient")
@@ -105,14 +106,19 @@ def saturate(
     allow_self_pairs: bool = False,
 ):
     """Iterate rules on ``eg`` (mutated in place) until saturation or a limit.
-    Returns (filter list, ExploreReport); ``filt`` is updated in place."""
+    Returns (filter list, ExploreReport); ``filt`` is updated in place.
+
+    ``filter_mode="vanilla"`` checks each combo by applying it on a device
+    checkpoint and running the cycle check from the root (cycles.py:248-254).
+    ``on_reject(eg, filt, rule, matches)`` is the post-saturation variant of
+    the reference hook (explorer.py:223-224): the device records every
+    cycle-rejected combo (rule + snapshot Match per source, in rejection
+    order) and the callbacks run after the search, with the final e-graph;
+    the live mid-iteration e-graph never leaves the GPU.  Recording routes
+    efficient-mode rules through the exact sequential path."""
     limits = limits or ExploreLimits()
     if filter_mode not in FILTER_MODES:
         raise ValueError(f"filter_mode must be one of {FILTER_MODES}")
-    if filter_mode == "vanilla":
-        raise NotImplementedError("vanilla (apply-on-clone) cycle filtering is not part of the B200 engine")
-    if on_reject is not None:
-        raise NotImplementedError("on_reject needs the live mid-iteration e-graph, which stays on the GPU")
     filt = set() if filt is None else filt
     rules = list(rules)
     eg.set_filter(filt)
@@ -124,12 +130,17 @@ def saturate(
     rep = _lib.Report()
     rs = np.zeros(max(len(rules), 1) * 7, np.int64)
     per = np.zeros(max(limits.k_max, 1) * 3, np.int64)
+    if on_reject is not None:
+        _lib.check(eg._h, lib.tsat_set_record_rejects(eg._h, 1))
     try:
         _lib.check(eg._h, lib.tsat_saturate(eg._h, C.byref(lim), _MODE_CODE[filter_mode],
                                             1 if allow_self_pairs else 0, C.byref(rep),
                                             _lib.ptr(rs, C.c_int64), _lib.ptr(per, C.c_int64)))
     finally:
         eg._touch()
+        if on_reject is not None:
+            _lib.check(eg._h, lib.tsat_set_record_rejects(eg._h, 0))
+    rejected = _rejected_combos(eg, rules) if on_reject is not None else []
     report = ExploreReport()
     for i, r in enumerate(rules):
         report.rules.setdefault(r.name, RuleStats(*[int(x) for x in rs[7 * i:7 * i + 7]]))
@@ -152,7 +163,36 @@ def saturate(
     filt.update(dev)
     filt.update(extra)
     report.filter_size = len(filt)
+    for rule, matches in rejected:
+        on_reject(eg, filt, rule, matches)
     return filt, report
+
+
+def _rejected_combos(eg: EGraph, rules) -> list:
+    """(rule, [Match per source]) for every cycle-rejected combo of the last
+    tsat_saturate, in rejection order.  The device records the snapshot match
+    rows; bindings are re-keyed by the rule's original variable names like
+    run_rule's decanonicalize (explorer.py:231-233)."""
+    lib = _lib.load()
+    n = C.c_int64()
+    _lib.check(eg._h, lib.tsat_rejects(eg._h, None, 0, C.byref(n)))
+    buf = np.zeros(max(n.value, 1), np.uint32)
+    _lib.check(eg._h, lib.tsat_rejects(eg._h, _lib.ptr(buf, C.c_uint32), len(buf), C.byref(n)))
+    out, i = [], 0
+    while i < n.value:
+        rule = rules[int(buf[i])]
+        nsrc = int(buf[i + 1])
+        i += 2
+        matches = []
+        for t in range(nsrc):
+            cls, nb = int(buf[i]), int(buf[i + 1])
+            b = buf[i + 2:i + 2 + nb]
+            i += 2 + nb
+            names = sorted(f"v{k}" for k in range(nb))
+            back = {c: o for o, c in rule.canonical_sources[t].rename}
+            matches.append(Match(cls, tuple(sorted((back[names[k]], int(b[k])) for k in range(nb)))))
+        out.append((rule, matches))
+    return out
 
 
 def explore(

@@ -139,6 +139,13 @@ EXPLORE_CASES = [
     ("rand_incep_4", ["generate", "inception-block", 1, 4], "all", _L(k_max=3), "efficient", False),
     ("k0_none", ["matmul_chain", [2]], MERGE_LHS, _L(k_max=0, k_multi=0), "efficient", False),
     ("empty_rules", ["matmul_chain", [2]], [], _L(), "efficient", False),
+    # vanilla (apply-on-clone) cycle filtering, cycles.py:248-254
+    ("chain3_lhs_vanilla", ["matmul_chain", [3]], MERGE_LHS, _L(k_max=2), "vanilla", False),
+    ("feedback2_lhs_vanilla", ["matmul_feedback", [2]], MERGE_LHS, _L(), "vanilla", False),
+    ("feedback3_both_vanilla", ["matmul_feedback", [3]], MERGE_BOTH, _L(k_max=2), "vanilla", False),
+    ("rnn2_all_vanilla", ["rnn_cell_stack", [2]], "all", _L(k_max=3), "vanilla", False),
+    ("ew_mix_vanilla", ["custom", "ew_mix"], "all", _L(k_multi=0, k_max=4), "vanilla", False),
+    ("chain4_limit60_vanilla", ["matmul_chain", [4]], MERGE_LHS, _L(n_max=60, k_multi=3, k_max=5), "vanilla", False),
 ]
 
 

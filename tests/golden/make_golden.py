@@ -41,10 +41,16 @@ def run_explore_case(case):
         orig_end(self)
         snaps.append({"dump": self.eg.dump(), "filt": sorted(self.filt)})
 
+    rejects = []
+
+    def on_reject(_eg, _filt, rule, matches):
+        rejects.append([rule.name, [[m.eclass, [list(b) for b in m.bindings]] for m in matches]])
+
     rexp._Engine.end_iteration = end_iteration
     try:
         eg, filt, rep = rexp.explore(
-            g, rules, rexp.ExploreLimits(**limits), mode, allow_self_pairs=self_pairs
+            g, rules, rexp.ExploreLimits(**limits), mode, allow_self_pairs=self_pairs,
+            on_reject=on_reject,
         )
     finally:
         rexp._Engine.end_iteration = orig_end
@@ -52,7 +58,7 @@ def run_explore_case(case):
     out = {"id": cid, "graph": gspec, "rules": names, "limits": limits,
            "filter_mode": mode, "allow_self_pairs": self_pairs,
            "iterations": snaps, "stats": stats, "final_dump": eg.dump(),
-           "final_filt": sorted(filt)}
+           "final_filt": sorted(filt), "rejects": rejects}
     costs = egraph_costs(eg, CostModel())
     out["costs"] = {str(k): v for k, v in sorted(costs.items())}
     try:

@@ -144,3 +144,45 @@ def test_feedback_cycles_filtered_match_oracle():
         assert eg.dump() == oeg.dump()
         assert sorted(filt) == sorted(ofilt)
         assert _stats(rep) == {k: v for k, v in orep.to_stats().items() if "time" not in k}
+
+
+_FILTERED = [c for c in EXPLORE if c["filter_mode"] != "none"]
+
+
+@pytest.mark.parametrize("case", _FILTERED, ids=[c["id"] for c in _FILTERED])
+def test_on_reject_matches_reference(case):
+    """on_reject (post-saturation variant) sees the reference's rejected combos
+    in the reference's order; recording (efficient: exact sequential path)
+    leaves the result unchanged."""
+    g = cases.build_graph(bench_graphs, tensor_lang, case["graph"])
+    rules = cases.select_rules(default_rules(), case["rules"])
+    got = []
+
+    def on_reject(_eg, _filt, rule, matches):
+        got.append([rule.name, [[m.eclass, [list(b) for b in m.bindings]] for m in matches]])
+
+    eg, filt, rep = explore(g, rules, ExploreLimits(**case["limits"]), case["filter_mode"],
+                            on_reject=on_reject, allow_self_pairs=case["allow_self_pairs"])
+    assert got == case["rejects"]
+    assert eg.dump() == case["final_dump"]
+    assert sorted(filt) == case["final_filt"]
+    assert _stats(rep) == case["stats"]
+
+
+def test_vanilla_against_oracle_and_slower_than_efficient():
+    """C5 shape (pkg/tests/test_acceptance.py:240-253): one k_multi iteration of
+    matmul-merge-shared-lhs on matmul_chain(33) in both modes; each equals the
+    oracle, and the efficient pre-filter beats per-combo apply-and-check."""
+    g = bench_graphs.matmul_chain(33)
+    rules = cases.select_rules(default_rules(), cases.MERGE_LHS)
+    lim = ExploreLimits(k_multi=1, k_max=1)
+    out = {}
+    for mode in ("efficient", "vanilla"):
+        eg, filt, rep = explore(g, rules, lim, mode)
+        oeg, ofilt, orep = O.oracle_explore(g, rules, filter_mode=mode, n_max=lim.n_max, k_max=1, k_multi=1)
+        assert eg.dump() == oeg.dump(), mode
+        assert sorted(filt) == sorted(ofilt), mode
+        assert _stats(rep) == {k: v for k, v in orep.to_stats().items() if "time" not in k}, mode
+        out[mode] = rep
+    assert out["efficient"].rules["matmul-merge-shared-lhs"].found >= 1000
+    assert out["efficient"].time_s < out["vanilla"].time_s
