@@ -113,6 +113,16 @@ int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, i
  * (bindings in sorted canonical-variable order); tsat_rejects copies them out
  * (size query with out = NULL).  Efficient mode records through the exact
  * sequential path. */
+/* ILP model skeleton (extract.reachable_classes + build_ilp, extract.py:198-322) over the
+ * current filter list.  sizes = {classes, x variables, live members, pick rows}.
+ * download: classes (root first, then ascending id), x nodes (alive members of those
+ * classes, ascending id), live_off[classes+1] / live (non-filtered members per class,
+ * ascending), pick_off[live+1] / pick_child (distinct child classes of each live member
+ * as positions in classes, ascending class id).  Any out pointer may be NULL. */
+int tsat_ilp_build(tsat_engine* h, uint32_t* sizes);
+int tsat_ilp_download(tsat_engine* h, uint32_t* classes, uint32_t* nodes, uint32_t* live_off, uint32_t* live,
+                      uint32_t* pick_off, uint32_t* pick_child);
+
 int tsat_set_record_rejects(tsat_engine* h, int32_t on);
 int tsat_rejects(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n);
 

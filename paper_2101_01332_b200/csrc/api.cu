@@ -223,6 +223,13 @@ int tsat_get_filter(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n) {
   });
 }
 
+int tsat_ilp_build(tsat_engine* h, uint32_t* sizes) { GUARD(h, h->e->ilp_build(sizes)); }
+
+int tsat_ilp_download(tsat_engine* h, uint32_t* classes, uint32_t* nodes, uint32_t* live_off, uint32_t* live,
+                      uint32_t* pick_off, uint32_t* pick_child) {
+  GUARD(h, h->e->ilp_download(classes, nodes, live_off, live, pick_off, pick_child));
+}
+
 int tsat_set_record_rejects(tsat_engine* h, int32_t on) { GUARD(h, h->e->record_rejects = on != 0); }
 
 int tsat_rejects(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n) {

@@ -223,6 +223,9 @@ struct Scratch {
   DevBuf<u32> v_parent, v_rej;
   DevBuf<Val> v_val;
   DevBuf<unsigned long long> v_hc;
+  // ILP model skeleton (ilp.cu)
+  DevBuf<u32> il_mark, il_queue, il_f, il_scan, il_pos, il_classes, il_sel, il_soff, il_nodes, il_tmp, il_tmp2;
+  DevBuf<u32> il_loff, il_lcnt, il_live, il_pcnt, il_poff, il_pchild;
   // api
   DevBuf<Instr> a_prog;
   DevBuf<int32_t> a_len;
@@ -374,6 +377,11 @@ struct Engine {
              double* out);
   double greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u32* nsel, i64* rounds);
   void costs_gather(u32 n, const u32* ids, double* out);
+
+  // ILP model skeleton (ilp.cu): sizes = {classes, x nodes, live members, pick rows}
+  u32 il_sizes[4] = {0, 0, 0, 0};
+  void ilp_build(u32* sizes);
+  void ilp_download(u32* classes, u32* nodes, u32* live_off, u32* live, u32* pick_off, u32* pick_child);
 
   // download
   void download(u32* op, u32* koff, u32* kids, u32* cls, u8* flags);
