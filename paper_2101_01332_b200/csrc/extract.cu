@@ -605,13 +605,97 @@ __global__ void __launch_bounds__(1024) k_greedy_cta(const u32* order, const u32
                                                      const u32* qeoff, const u32* qedst, double* qtot, double* bc_g,
                                                      u32* bn, int smem, const u32* bigflag) {
   extern __shared__ double s_bc[];
+  __shared__ double s_run[32];
+  __shared__ u32 s_cls[32], s_len, s_next;
   double* bc = smem ? s_bc : bc_g;
-  for (u32 l = l0; l < l1; l++) {
+  u32 next_check = l0;
+  for (u32 l = l0; l < l1;) {
+    // Runs of single-member levels (deep chains such as the noop spine of
+    // make_single_rooted): warp 0 prefetches up to 32 levels at once -- one
+    // level per lane, its member, cost and the child best costs that lie
+    // below the run -- then folds them in level order with __syncwarp only,
+    // in-run children read from shared memory.  Same fp64 sums in the same
+    // order as gq_totals / gq_fold_seq.
+    if (l >= next_check) {
+    if (threadIdx.x < 32) {
+      const u32 lane = threadIdx.x, lv = l + lane;
+      u32 q = 0, deg = 0, ea = 0, cls = TSAT_NONE;
+      bool one = false;
+      if (lv < l1) {
+        u32 a = lvl_off[lv];
+        if (lvl_off[lv + 1] == a + 1) {
+          q = lvm_off[a];
+          if (lvm_off[a + 1] == q + 1) {
+            ea = qeoff[q];
+            deg = qeoff[q + 1] - ea;
+            cls = order[a];
+            one = deg <= 8;
+          }
+        }
+      }
+      unsigned good = __ballot_sync(0xffffffffu, one), bad = ~good;
+      u32 len = bad ? (u32)(__ffs(bad) - 1) : 32u;
+      unsigned pairs = good & (good >> 1);
+      if (len >= 2) {
+        s_cls[lane] = cls;
+        __syncwarp();
+        double cst = 0.0, val[8];
+        int src[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          src[j] = -1;
+          val[j] = 0.0;
+        }
+        if (lane < len) {
+          cst = qcost[q];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            if ((u32)j < deg) {
+              u32 d = qedst[ea + j];
+              for (u32 k = 0; k < lane; k++)
+                if (s_cls[k] == d) src[j] = (int)k;
+              if (src[j] < 0) val[j] = bc[d];
+            }
+          }
+        }
+        for (u32 k = 0; k < len; k++) {
+          if (lane == k) {
+            double tot = cst;
+            if (!isnan(tot))
+#pragma unroll
+              for (int j = 0; j < 8; j++)
+                if ((u32)j < deg) tot += src[j] >= 0 ? s_run[src[j]] : val[j];
+            bool ok = !(isnan(tot) || isinf(tot));
+            double c = ok ? tot : INFINITY;
+            s_run[k] = c;
+            qtot[q] = tot;
+            bc[cls] = c;
+            bn[cls] = ok ? qnode[q] : TSAT_NONE;
+          }
+          __syncwarp();
+        }
+      }
+      if (lane == 0) {
+        s_len = len;
+        s_next = pairs ? l + (u32)(__ffs(pairs) - 1) : l + 31;
+      }
+    }
+    __syncthreads();
+    const u32 len = s_len, nxt = s_next;
+    __syncthreads();
+    if (len >= 2) {
+      l += len;
+      next_check = l;
+      continue;
+    }
+    next_check = nxt;
+    }
     u32 a = lvl_off[l], b = lvl_off[l + 1];
     gq_totals(lvm_off[a], lvm_off[b], threadIdx.x, blockDim.x, qcost, qeoff, qedst, bc, qtot);
     __syncthreads();
     gq_fold(a, b, threadIdx.x, blockDim.x, order, lvm_off, qnode, qtot, bc, bn, bigflag[l] != 0);
     __syncthreads();
+    l++;
   }
   if (smem)
     for (u32 t = threadIdx.x; t < ntr; t += blockDim.x) {
@@ -726,6 +810,119 @@ __global__ void k_sel_coop(G g, const u32* cls_index, const u32* bn, u32 n, u32 
     start = end;
     end = ((volatile u32*)ctl)[0];
     grid.sync();
+  }
+}
+
+// Reached selection by a top-down sweep of the peel levels (a chosen node's
+// children sit on strictly lower levels), instead of a BFS whose depth is the
+// selection's depth (the 1,416-level noop spine at config 5).  One CTA walks
+// levels [lo, hi) downwards; runs of single-class levels go to warp 0, which
+// loads up to 32 levels at once (class, mark, children) and propagates marks
+// through the run in shared memory; other levels: one barrier each.
+__global__ void __launch_bounds__(1024) k_sel_cta(const u32* order, const u32* lvl_off, u32 lo, u32 hi,
+                                                  const u32* eoff, const u32* edst, u32* mark) {
+  __shared__ u32 s_cls[32], s_mk[32], s_len, s_next;
+  u32 next_check = hi;  // levels at or below this index get a run check
+  for (u32 l = hi; l > lo;) {
+    if (l <= next_check) {
+      if (threadIdx.x < 32) {
+        const u32 lane = threadIdx.x;
+        const long long lvs = (long long)l - 1 - lane;
+        u32 cls = TSAT_NONE, ea = 0, deg = 0;
+        bool one = false;
+        if (lvs >= (long long)lo) {
+          u32 a = lvl_off[lvs];
+          if (lvl_off[lvs + 1] == a + 1) {
+            cls = order[a];
+            ea = eoff[cls];
+            deg = eoff[cls + 1] - ea;
+            one = deg <= 8;
+          }
+        }
+        unsigned good = __ballot_sync(0xffffffffu, one), bad = ~good;
+        u32 len = bad ? (u32)(__ffs(bad) - 1) : 32u;
+        unsigned pairs = good & (good >> 1);
+        if (len >= 2) {
+          s_cls[lane] = cls;
+          s_mk[lane] = 0;
+          u32 gm = lane < len ? mark[cls] : 0u;
+          u32 d[8];
+          int src[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            d[j] = TSAT_NONE;
+            src[j] = -1;
+          }
+          __syncwarp();
+          if (lane < len) {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+              if ((u32)j < deg) {
+                d[j] = edst[ea + j];
+                for (u32 k = lane + 1; k < len; k++)
+                  if (s_cls[k] == d[j]) src[j] = (int)k;
+              }
+          }
+          for (u32 k = 0; k < len; k++) {
+            if (lane == k && (gm || s_mk[k])) {
+#pragma unroll
+              for (int j = 0; j < 8; j++)
+                if ((u32)j < deg) {
+                  if (src[j] >= 0) s_mk[src[j]] = 1;
+                  else mark[d[j]] = 1;
+                }
+              if (!gm) mark[cls] = 1;
+            }
+            __syncwarp();
+          }
+        }
+        if (lane == 0) {
+          s_len = len;
+          s_next = pairs ? l - 1 - (u32)(__ffs(pairs) - 1) : (l > 31 ? l - 31 : 0);
+        }
+      }
+      __syncthreads();
+      const u32 len = s_len, nxt = s_next;
+      __syncthreads();
+      if (len >= 2) {
+        l -= len;
+        next_check = l;
+        continue;
+      }
+      next_check = nxt + 1;
+    }
+    const u32 a = lvl_off[l - 1], b = lvl_off[l];
+    for (u32 t = a + threadIdx.x; t < b; t += blockDim.x) {
+      u32 i = order[t];
+      if (mark[i])
+        for (u32 e = eoff[i], e1 = eoff[i + 1]; e < e1; e++) mark[edst[e]] = 1;
+    }
+    __syncthreads();
+    l--;
+  }
+}
+
+// one wide level of the top-down sweep on the whole GPU
+__global__ void k_sel_wide(const u32* order, u32 a, u32 b, const u32* eoff, const u32* edst, u32* mark) {
+  GRID_STRIDE(t0, (u64)(b - a)) {
+    u32 i = order[a + (u32)t0];
+    if (mark[i])
+      for (u32 e = eoff[i], e1 = eoff[i + 1]; e < e1; e++) mark[edst[e]] = 1;
+  }
+}
+
+__global__ void k_sel_flags(const u32* mark, u32 C, u32* fl) {
+  GRID_STRIDE(i, (u64)C + 1) fl[i] = (i < C && mark[i]) ? 1u : 0u;
+}
+
+__global__ void k_sel_compact(const u32* mark, const u32* pos, u32 C, const u32* cls_ids, const u32* bn, u32* oc,
+                              u32* on, u32* missing) {
+  GRID_STRIDE(i, C) {
+    if (!mark[i]) continue;
+    u32 p = pos[i];
+    oc[p] = cls_ids[i];
+    on[p] = bn[i];
+    if (bn[i] == TSAT_NONE) *missing = 1;
   }
 }
 
@@ -919,18 +1116,57 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
     sc.g_edst.ensure(ne + 1);
     k_sel_fill<<<nblk(C), 256, 0, s>>>(gv, n0.p, ci, C, sc.g_eoff.p, sc.g_edst.p);
   }
-  u32 k = bfs_graph(*this, sc.g_eoff.p, sc.g_edst.p, C, rd, mark.p, q.p);
-  CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
-  k_sel_missing<<<nblk(k), 256, 0, s>>>(q.p, k, n0.p, flag.p);
-  u32 miss;
-  CUDA_OK(cudaMemcpyAsync(&miss, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  sync();
-  if (miss) throw TsatException(TSAT_ERR_STATE, "no selected node covers a reached e-class");
   DevBuf<u32>& oc = sc.g_oc;
   DevBuf<u32>& on = sc.g_on;
   oc.ensure(C + 1);
   on.ensure(C + 1);
-  k_sel_collect<<<nblk(k), 256, 0, s>>>(q.p, k, snap.cls_ids.p, n0.p, oc.p, on.p);
+  u32 k;
+  static const int sel_mode = getenv("TSAT_SEL") ? atoi(getenv("TSAT_SEL")) : 0;  // debug: 1 BFS, 2 sweep
+  u32 single_lv = 0;
+  for (u32 l = 0; l < nl; l++) single_lv += lo[l + 1] - lo[l] == 1;
+  if (getenv("TSAT_SEL_DEBUG")) fprintf(stderr, "greedy levels %u single %u classes %u\n", nl, single_lv, C);
+  bool sweep = ntr == C && (sel_mode == 2 || (sel_mode == 0 && single_lv >= 256));
+  if (sweep) {
+    // every class peeled: top-down level sweep (k_sel_cta / k_sel_wide)
+    CUDA_OK(cudaMemsetAsync(mark.p, 0, (size_t)(C + 1) * sizeof(u32), s));
+    const u32 one = 1;
+    CUDA_OK(cudaMemcpyAsync(mark.p + rd, &one, sizeof(u32), cudaMemcpyHostToDevice, s));
+    const u32 WIDE = 8192;
+    for (u32 l = nl; l > 0;) {
+      u32 wc = lo[l] - lo[l - 1];
+      if (wc > WIDE) {
+        k_sel_wide<<<nblk(wc), 256, 0, s>>>(ord, lo[l - 1], lo[l], sc.g_eoff.p, sc.g_edst.p, mark.p);
+        l--;
+        continue;
+      }
+      u32 l0 = l;
+      while (l0 > 0 && lo[l0] - lo[l0 - 1] <= WIDE) l0--;
+      k_sel_cta<<<1, 1024, 0, s>>>(ord, lvl, l0, l, sc.g_eoff.p, sc.g_edst.p, mark.p);
+      l = l0;
+    }
+    DevBuf<u32>& fl = sc.g_cnt;
+    fl.ensure(C + 2);
+    q.ensure(C + 2);
+    k_sel_flags<<<nblk((u64)C + 1), 256, 0, s>>>(mark.p, C, fl.p);
+    dev_exclusive_scan_u32(*this, fl.p, q.p, C + 1);
+    CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
+    k_sel_compact<<<nblk(C), 256, 0, s>>>(mark.p, q.p, C, snap.cls_ids.p, n0.p, oc.p, on.p, flag.p);
+    u32 hk[2];
+    CUDA_OK(cudaMemcpyAsync(&hk[0], q.p + C, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(&hk[1], flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    sync();
+    k = hk[0];
+    if (hk[1]) throw TsatException(TSAT_ERR_STATE, "no selected node covers a reached e-class");
+  } else {
+    k = bfs_graph(*this, sc.g_eoff.p, sc.g_edst.p, C, rd, mark.p, q.p);
+    CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
+    k_sel_missing<<<nblk(k), 256, 0, s>>>(q.p, k, n0.p, flag.p);
+    u32 miss;
+    CUDA_OK(cudaMemcpyAsync(&miss, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    sync();
+    if (miss) throw TsatException(TSAT_ERR_STATE, "no selected node covers a reached e-class");
+    k_sel_collect<<<nblk(k), 256, 0, s>>>(q.p, k, snap.cls_ids.p, n0.p, oc.p, on.p);
+  }
   CUDA_OK(cudaMemcpyAsync(sel_cls, oc.p, k * sizeof(u32), cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaMemcpyAsync(sel_node, on.p, k * sizeof(u32), cudaMemcpyDeviceToHost, s));
   sync();
