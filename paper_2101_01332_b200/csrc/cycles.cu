@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(512) k_close_cols(const u32* order, const u32*
   u32* col = in_smem ? smem_col : bitsT + (u64)w0 * n;
   if (in_smem)
     for (u64 i = threadIdx.x; i < (u64)nk * n; i += blockDim.x) col[i] = 0;
-  __shared__ u32 s_next;
+  __shared__ u32 s_next, s_rcls[32], s_rw[4][32];
   __syncthreads();
   auto item = [&](u32 a, u64 it) {
     u32 i = order[a + it / nk];
@@ -114,8 +114,72 @@ __global__ void __launch_bounds__(512) k_close_cols(const u32* order, const u32*
     if (items <= 32) {
       // a run of thin levels (deep chains): warp 0 alone, __syncwarp only
       if (threadIdx.x < 32) {
-        u32 ll = l;
+        const u32 lane = threadIdx.x;
+        u32 ll = l, next_check = l;
         while (ll < nl) {
+          if (nk <= 4 && ll >= next_check) {
+            // runs of single-class levels: one lane per level loads its
+            // children and their column words up front, then the lanes OR
+            // them in level order (in-run children through shared memory)
+            u32 lv = ll + lane, ci = TSAT_NONE, ea = 0, deg = 0;
+            bool one = false;
+            if (lv < nl) {
+              u32 a3 = lvl_off[lv];
+              if (lvl_off[lv + 1] == a3 + 1) {
+                ci = order[a3];
+                ea = eoff[ci];
+                deg = eoff[ci + 1] - ea;
+                one = deg <= 8;
+              }
+            }
+            unsigned good = __ballot_sync(0xffffffffu, one), bad = ~good;
+            u32 len = bad ? (u32)(__ffs(bad) - 1) : 32u;
+            unsigned pairs = good & (good >> 1);
+            if (len >= 2) {
+              s_rcls[lane] = ci;
+              __syncwarp();
+              u32 d[8], v[4][8];
+              int src[8];
+#pragma unroll
+              for (int j = 0; j < 8; j++) {
+                d[j] = 0;
+                src[j] = -1;
+#pragma unroll
+                for (int w = 0; w < 4; w++) v[w][j] = 0;
+                if (lane < len && (u32)j < deg) {
+                  d[j] = edst[ea + j];
+                  for (u32 k = 0; k < lane; k++)
+                    if (s_rcls[k] == d[j]) src[j] = (int)k;
+                  if (src[j] < 0)
+#pragma unroll
+                    for (int w = 0; w < 4; w++)
+                      if (w < nk) v[w][j] = col[(u64)w * n + d[j]];
+                }
+              }
+              for (u32 k = 0; k < len; k++) {
+                if (lane == k) {
+#pragma unroll
+                  for (int w = 0; w < 4; w++) {
+                    if (w >= nk) break;
+                    u32 acc = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                      if ((u32)j >= deg) break;
+                      acc |= src[j] >= 0 ? s_rw[w][src[j]] : v[w][j];
+                      if ((d[j] >> 5) == w0 + w) acc |= 1u << (d[j] & 31);
+                    }
+                    s_rw[w][k] = acc;
+                    col[(u64)w * n + ci] = acc;
+                  }
+                }
+                __syncwarp();
+              }
+              ll += len;
+              next_check = ll;
+              continue;
+            }
+            next_check = pairs ? ll + (u32)(__ffs(pairs) - 1) : ll + 31;
+          }
           u32 a2 = lvl_off[ll], b2 = lvl_off[ll + 1];
           u64 it2 = (u64)(b2 - a2) * nk;
           if (it2 > 32) break;
@@ -221,6 +285,11 @@ void Engine::build_reach() {
   if (bytes > (u64)48 << 30) throw TsatException(TSAT_ERR_UNSUPPORTED, "descendants bitset would exceed 48 GiB");
   reach.bits.ensure((u64)n * words + 1);
   u32 nl = lv_n, ntr = lv_trimmed;
+  if (getenv("TSAT_SEL_DEBUG")) {
+    u32 single = 0;
+    for (u32 l = 0; l < nl; l++) single += lv_off[l + 1] - lv_off[l] == 1;
+    fprintf(stderr, "reach classes %u levels %u single %u trimmed %u\n", cg_n, nl, single, ntr);
+  }
   DevBuf<u32>& rest = sc.c_rest;
   u32 nr = n - ntr;
   if (nr) {
