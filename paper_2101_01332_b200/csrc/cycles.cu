@@ -83,9 +83,19 @@ __global__ void k_rhist(const u32* edst, u64 ne, u32* h) {
 // the peel levels in order with only __syncthreads() between levels (no grid
 // or host synchronisation), then sweeps the untrimmed (cyclic) remainder to a
 // fixpoint.  Columns live in shared memory when they fit, else in HBM.
+// Staged variant (oeoff != nullptr): the class edges are laid out in peel
+// order (oeoff / oedst by level position), and batches of consecutive levels
+// -- their level offsets, classes and edge lists -- are copied to shared
+// memory with coalesced loads before the batch is walked, so a level costs a
+// barrier plus shared-memory work instead of three dependent L2 round trips.
+#define CC_LV 512u
+#define CC_T 2048u
+#define CC_E 8192u
+#define CC_STAGE_WORDS (CC_LV + 1 + CC_T + 1 + CC_T + CC_E)
 __global__ void __launch_bounds__(512) k_close_cols(const u32* order, const u32* lvl_off, u32 nl, const u32* eoff,
                                                     const u32* edst, const u32* rest, u32 nrest, u32 n, u32 words,
-                                                    int wpb, int in_smem, u32* bitsT) {
+                                                    int wpb, int in_smem, u32* bitsT, const u32* oeoff,
+                                                    const u32* oedst, const u32* batch, u32 nbatch) {
   extern __shared__ u32 smem_col[];
   __shared__ u32 s_changed;
   const u32 w0 = blockIdx.x * (u32)wpb;
@@ -108,7 +118,72 @@ __global__ void __launch_bounds__(512) k_close_cols(const u32* order, const u32*
     }
     col[(u64)k * n + i] = acc;
   };
-  for (u32 l = 1; l < nl;) {
+  if (oeoff) {
+    u32* s_lv = smem_col + (in_smem ? (u64)nk * n : 0);
+    u32* s_off = s_lv + CC_LV + 1;
+    u32* s_ord = s_off + CC_T + 1;
+    u32* s_ed = s_ord + CC_T;
+    for (u32 bi = 0; bi < nbatch; bi++) {
+      const u32 lb = batch[3 * bi], le = batch[3 * bi + 1], staged = batch[3 * bi + 2];
+      const u32 t0 = lvl_off[lb], t1 = lvl_off[le];
+      const u32 e0 = oeoff[t0], e1 = oeoff[t1];
+      const u32 *LV = lvl_off, *OFF = oeoff, *ORD = order, *ED = oedst;
+      u32 lbase = 0, tbase = 0, ebase = 0;
+      if (staged) {
+        for (u32 x = threadIdx.x; x <= le - lb; x += blockDim.x) s_lv[x] = lvl_off[lb + x];
+        for (u32 x = threadIdx.x; x <= t1 - t0; x += blockDim.x) s_off[x] = oeoff[t0 + x];
+        for (u32 x = threadIdx.x; x < t1 - t0; x += blockDim.x) s_ord[x] = order[t0 + x];
+        for (u32 x = threadIdx.x; x < e1 - e0; x += blockDim.x) s_ed[x] = oedst[e0 + x];
+        __syncthreads();
+        LV = s_lv;
+        OFF = s_off;
+        ORD = s_ord;
+        ED = s_ed;
+        lbase = lb;
+        tbase = t0;
+        ebase = e0;
+      }
+      auto sitem = [&](u32 t, int k) {
+        u32 i = ORD[t - tbase];
+        u32 w = w0 + k;
+        const u32* ck = col + (u64)k * n;
+        u32 acc = 0;
+        for (u32 e = OFF[t - tbase], e1_ = OFF[t + 1 - tbase]; e < e1_; e++) {
+          u32 j = ED[e - ebase];
+          acc |= ck[j];
+          if ((j >> 5) == w) acc |= 1u << (j & 31);
+        }
+        col[(u64)k * n + i] = acc;
+      };
+      for (u32 l = lb; l < le;) {
+        u32 a = LV[l - lbase], b = LV[l + 1 - lbase];
+        u32 items = (b - a) * (u32)nk;
+        if (items <= 32) {
+          if (threadIdx.x < 32) {  // thin levels: warp 0 alone, __syncwarp only
+            u32 ll = l;
+            while (ll < le) {
+              u32 a2 = LV[ll - lbase], b2 = LV[ll + 1 - lbase];
+              u32 it2 = (b2 - a2) * (u32)nk;
+              if (it2 > 32) break;
+              if (threadIdx.x < it2) sitem(a2 + threadIdx.x / nk, (int)(threadIdx.x % nk));
+              __syncwarp();
+              ll++;
+            }
+            if (threadIdx.x == 0) s_next = ll;
+          }
+          __syncthreads();
+          l = s_next;
+          __syncthreads();
+          continue;
+        }
+        for (u32 it = threadIdx.x; it < items; it += blockDim.x) sitem(a + it / nk, (int)(it % nk));
+        __syncthreads();
+        l++;
+      }
+      __syncthreads();
+    }
+  }
+  for (u32 l = oeoff ? nl : 1; l < nl;) {
     u32 a = lvl_off[l], b = lvl_off[l + 1];
     u64 items = (u64)(b - a) * nk;
     if (items <= 32) {
@@ -228,6 +303,28 @@ __global__ void __launch_bounds__(512) k_close_cols(const u32* order, const u32*
     for (u64 i = threadIdx.x; i < (u64)nk * n; i += blockDim.x) bitsT[(u64)w0 * n + i] = col[i];
 }
 
+__global__ void k_ord_deg(const u32* order, u32 ntr, const u32* eoff, u32* deg) {
+  GRID_STRIDE(t, (u64)ntr + 1) {
+    if (t < ntr) {
+      u32 i = order[t];
+      deg[t] = eoff[i + 1] - eoff[i];
+    } else {
+      deg[t] = 0;
+    }
+  }
+}
+
+__global__ void k_ord_fill(const u32* order, u32 ntr, const u32* eoff, const u32* edst, const u32* oeoff, u32* oedst) {
+  GRID_STRIDE(t, ntr) {
+    u32 i = order[t], o = oeoff[t];
+    for (u32 e = eoff[i]; e < eoff[i + 1]; e++) oedst[o++] = edst[e];
+  }
+}
+
+__global__ void k_gather_bnd(const u32* src, const u32* idx, u32 n, u32* out) {
+  GRID_STRIDE(k, n) out[k] = src[idx[k]];
+}
+
 __global__ void k_untrimmed(const u32* level, u32 n, const u8* mask, u32* list, u32* cnt) {
   GRID_STRIDE(i, n) if (level[i] == TSAT_NONE && (!mask || mask[i])) list[atomicAdd(cnt, 1u)] = (u32)i;
 }
@@ -307,14 +404,48 @@ void Engine::build_reach() {
       CUDA_OK(cudaFuncSetAttribute(k_close_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
       smem_set = 1;
     }
-    u64 fit = SMEM / (4ull * n);
+    // level-ordered edge lists + batches of levels that fit the stage area
+    static const bool no_stage = getenv("TSAT_CLOSE_NOSTAGE") != nullptr;
+    const u64 STAGE = no_stage ? 0 : (u64)CC_STAGE_WORDS * 4;
+    u32 nbatch = 0;
+    if (!no_stage && nl > 1) {
+      Scratch& X = sc;
+      X.c_odeg.ensure(ntr + 2);
+      X.c_oeoff.ensure(ntr + 2);
+      X.c_oedst.ensure((u64)cg_ne + 1);
+      X.c_obnd.ensure(nl + 2);
+      k_ord_deg<<<nblk((u64)ntr + 1), 256, 0, s>>>(sc.c_order.p, ntr, sc.cg_eoff.p, X.c_odeg.p);
+      dev_exclusive_scan_u32(*this, X.c_odeg.p, X.c_oeoff.p, ntr + 1);
+      k_ord_fill<<<nblk(ntr), 256, 0, s>>>(sc.c_order.p, ntr, sc.cg_eoff.p, sc.cg_edst.p, X.c_oeoff.p, X.c_oedst.p);
+      k_gather_bnd<<<nblk((u64)nl + 1), 256, 0, s>>>(X.c_oeoff.p, sc.c_lvloff.p, nl + 1, X.c_obnd.p);
+      std::vector<u32> eb(nl + 1);
+      CUDA_OK(cudaMemcpyAsync(eb.data(), X.c_obnd.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      sync();
+      std::vector<u32> bt;
+      for (u32 l = 1; l < nl;) {
+        u32 le = l;
+        while (le < nl && le + 1 - l <= CC_LV && lv_off[le + 1] - lv_off[l] <= CC_T && eb[le + 1] - eb[l] <= CC_E) le++;
+        if (le == l) {  // one level beyond the stage area: walked from global memory
+          bt.insert(bt.end(), {l, l + 1, 0u});
+          l++;
+        } else {
+          bt.insert(bt.end(), {l, le, 1u});
+          l = le;
+        }
+      }
+      nbatch = (u32)(bt.size() / 3);
+      X.c_batch.ensure(bt.size() + 1);
+      CUDA_OK(cudaMemcpyAsync(X.c_batch.p, bt.data(), bt.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
+    }
+    u64 fit = (SMEM - STAGE) / (4ull * n);
     int in_smem = fit >= 1;
     u64 wpb = std::max<u64>(1, std::min<u64>(in_smem ? fit : 1, (words + 147) / 148));
     if (!in_smem) CUDA_OK(cudaMemsetAsync(reach.bits.p, 0, bytes, s));
     u32 grid = (u32)((words + wpb - 1) / wpb);
-    size_t sm = in_smem ? (size_t)wpb * n * 4 : 0;
+    size_t sm = (in_smem ? (size_t)wpb * n * 4 : 0) + (size_t)STAGE;
     k_close_cols<<<grid, 512, sm, s>>>(sc.c_order.p, sc.c_lvloff.p, nl, sc.cg_eoff.p, sc.cg_edst.p, rest.p, nr, n,
-                                        words, (int)wpb, in_smem, reach.bits.p);
+                                        words, (int)wpb, in_smem, reach.bits.p, nbatch ? sc.c_oeoff.p : nullptr,
+                                        sc.c_oedst.p, sc.c_batch.p, nbatch);
     CUDA_OK(cudaGetLastError());
   }
   reach.n = n;

@@ -209,6 +209,7 @@ struct Scratch {
   // class graph / cycles / reach
   DevBuf<u32> cg_eoff, cg_edst, cg_enode, cg_roff, cg_rsrc, cg_outdeg, cg_level, cg_esrc, cg_sdst, cg_moff, cg_mdeg;
   DevBuf<u32> c_heavy, c_mark32, c_fa, c_fb, c_order, c_depth, c_path, c_cycn, c_cyco, c_res, c_rest, c_lvloff;
+  DevBuf<u32> c_odeg, c_oeoff, c_oedst, c_obnd, c_batch;  // level-ordered class edges (staged closure)
   DevBuf<u8> c_mark, c_color;
   DevBuf<unsigned char> c_stack;
   // greedy / costs
