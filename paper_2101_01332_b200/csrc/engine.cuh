@@ -216,6 +216,7 @@ struct Scratch {
   DevBuf<double> g_c0, g_c1, g_upl, k_dv;
   DevBuf<u32> g_n0, g_n1, g_flag, g_mark, g_fa, g_fb, g_oc, g_on, k_slots, g_eoff, g_edst, g_cnt;
   DevBuf<char> k_keys;
+  DevBuf<u32> gq_batch;
   DevBuf<u32> gq_lvm, gq_cnt, gq_k, gq_node, gq_deg, gq_eoff, gq_edst, gq_lb, gq_head, gq_slot, gq_big;
   DevBuf<double> gq_pack, gq_recv;  // sharded wide levels: {best cost, node} records
   DevBuf<double> gq_cost, gq_tot;

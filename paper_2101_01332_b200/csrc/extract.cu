@@ -600,14 +600,10 @@ __device__ __forceinline__ void gq_fold(u32 a, u32 b, u64 tid, u64 nth, const u3
 // levels [l0, l1) in ONE CTA (thin levels: a barrier per phase instead of a
 // launch); best costs in shared memory when the whole class set fits
 // (``smem``: then this launch covers every level), else in HBM
-__global__ void __launch_bounds__(1024) k_greedy_cta(const u32* order, const u32* lvl_off, u32 l0, u32 l1, u32 ntr,
-                                                     const u32* lvm_off, const u32* qnode, const double* qcost,
-                                                     const u32* qeoff, const u32* qedst, double* qtot, double* bc_g,
-                                                     u32* bn, int smem, const u32* bigflag) {
-  extern __shared__ double s_bc[];
-  __shared__ double s_run[32];
-  __shared__ u32 s_cls[32], s_len, s_next;
-  double* bc = smem ? s_bc : bc_g;
+__device__ __forceinline__ void greedy_range(u32 l0, u32 l1, const u32* order, const u32* lvl_off,
+                                             const u32* lvm_off, const u32* qnode, const double* qcost,
+                                             const u32* qeoff, const u32* qedst, double* qtot, double* bc, u32* bn,
+                                             const u32* bigflag, double* s_run, u32* s_cls, u32& s_len, u32& s_next) {
   u32 next_check = l0;
   for (u32 l = l0; l < l1;) {
     // Runs of single-member levels (deep chains such as the noop spine of
@@ -697,13 +693,77 @@ __global__ void __launch_bounds__(1024) k_greedy_cta(const u32* order, const u32
     __syncthreads();
     l++;
   }
+}
+
+// Stage area of k_greedy_cta (batches of levels copied to shared memory)
+#define GQ_LV 512u
+#define GQ_T 1024u
+#define GQ_Q 2048u
+#define GQ_E 4096u
+#define GQ_STAGE_BYTES (2u * GQ_Q * 8u + 4u * (GQ_LV + 1 + GQ_T + 1 + GQ_T + GQ_Q + 1 + GQ_Q + GQ_E))
+
+// levels [l0, l1) in ONE CTA (thin levels: a barrier per phase instead of a
+// launch); best costs in shared memory when the whole class set fits
+// (``smem``: then this launch covers every level), else in HBM.  With
+// ``nbatch``, batches of levels -- their class / member offsets, member
+// costs, nodes and child lists, all contiguous in peel order -- are copied to
+// shared memory with coalesced loads first, so a level costs barriers and
+// shared-memory work instead of dependent L2 round trips.
+__global__ void __launch_bounds__(1024) k_greedy_cta(const u32* order, const u32* lvl_off, u32 l0, u32 l1, u32 ntr,
+                                                     const u32* lvm_off, const u32* qnode, const double* qcost,
+                                                     const u32* qeoff, const u32* qedst, double* qtot, double* bc_g,
+                                                     u32* bn, int smem, const u32* bigflag, u32 ncls_smem,
+                                                     const u32* batch, u32 nbatch) {
+  extern __shared__ double s_bc[];
+  __shared__ double s_run[32];
+  __shared__ u32 s_cls[32], s_len, s_next;
+  double* bc = smem ? s_bc : bc_g;
+  if (nbatch) {
+    double* s_qcost = s_bc + (smem ? ncls_smem : 0);
+    double* s_qtot = s_qcost + GQ_Q;
+    u32* s_lv = (u32*)(s_qtot + GQ_Q);
+    u32* s_lvm = s_lv + GQ_LV + 1;
+    u32* s_ord = s_lvm + GQ_T + 1;
+    u32* s_qeoff = s_ord + GQ_T;
+    u32* s_qnode = s_qeoff + GQ_Q + 1;
+    u32* s_qedst = s_qnode + GQ_Q;
+    for (u32 bi = 0; bi < nbatch; bi++) {
+      const u32 lb = batch[3 * bi], le = batch[3 * bi + 1];
+      if (!batch[3 * bi + 2]) {
+        greedy_range(lb, le, order, lvl_off, lvm_off, qnode, qcost, qeoff, qedst, qtot, bc, bn, bigflag, s_run,
+                     s_cls, s_len, s_next);
+        __syncthreads();
+        continue;
+      }
+      const u32 t0 = lvl_off[lb], t1 = lvl_off[le];
+      const u32 q0 = lvm_off[t0], q1 = lvm_off[t1];
+      const u32 e0 = qeoff[q0], e1 = qeoff[q1];
+      for (u32 x = threadIdx.x; x <= le - lb; x += blockDim.x) s_lv[x] = lvl_off[lb + x];
+      for (u32 x = threadIdx.x; x <= t1 - t0; x += blockDim.x) s_lvm[x] = lvm_off[t0 + x];
+      for (u32 x = threadIdx.x; x < t1 - t0; x += blockDim.x) s_ord[x] = order[t0 + x];
+      for (u32 x = threadIdx.x; x <= q1 - q0; x += blockDim.x) s_qeoff[x] = qeoff[q0 + x];
+      for (u32 x = threadIdx.x; x < q1 - q0; x += blockDim.x) {
+        s_qcost[x] = qcost[q0 + x];
+        s_qnode[x] = qnode[q0 + x];
+      }
+      for (u32 x = threadIdx.x; x < e1 - e0; x += blockDim.x) s_qedst[x] = qedst[e0 + x];
+      __syncthreads();
+      // base-shifted views: the level code indexes with global positions
+      greedy_range(lb, le, s_ord - t0, s_lv - lb, s_lvm - t0, s_qnode - q0, s_qcost - q0, s_qeoff - q0,
+                   s_qedst - e0, s_qtot - q0, bc, bn, bigflag, s_run, s_cls, s_len, s_next);
+      __syncthreads();
+    }
+  } else {
+    greedy_range(l0, l1, order, lvl_off, lvm_off, qnode, qcost, qeoff, qedst, qtot, bc, bn, bigflag, s_run, s_cls,
+                 s_len, s_next);
+  }
+  __syncthreads();
   if (smem)
     for (u32 t = threadIdx.x; t < ntr; t += blockDim.x) {
       u32 i = order[t];
       bc_g[i] = s_bc[i];
     }
 }
-
 // one wide level on the whole GPU (two launches: totals, then folds)
 __global__ void k_gq_totals_wide(u32 qa, u32 qb, const double* qcost, const u32* qeoff, const u32* qedst,
                                  const double* bc, double* qtot) {
@@ -1021,9 +1081,37 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
     smem_set = 1;
   }
   if ((u64)C * sizeof(double) <= GREEDY_SMEM) {
-    k_greedy_cta<<<1, 1024, (size_t)C * sizeof(double), s>>>(ord, lvl, 0, nl, ntr, X.gq_lvm.p, X.gq_node.p,
-                                                              X.gq_cost.p, X.gq_eoff.p, X.gq_edst.p, X.gq_tot.p, c0.p,
-                                                              n0.p, 1, bflag.p);
+    static const bool no_stage = getenv("TSAT_GREEDY_NOSTAGE") != nullptr;
+    u32 nbatch = 0;
+    if (!no_stage && (u64)C * sizeof(double) + GQ_STAGE_BYTES <= GREEDY_SMEM && nl) {
+      // edge offsets at level boundaries -> batches of levels that fit the stage area
+      DevBuf<u32>& eb_d = X.gq_head;  // free after the member fill
+      eb_d.ensure(nl + 2);
+      k_gather_at<<<nblk(nl + 1), 256, 0, s>>>(X.gq_eoff.p, X.gq_lb.p, nl + 1, eb_d.p);
+      std::vector<u32> eb(nl + 1);
+      CUDA_OK(cudaMemcpyAsync(eb.data(), eb_d.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      sync();
+      std::vector<u32> bt;
+      for (u32 l = 0; l < nl;) {
+        u32 le = l;
+        while (le < nl && le + 1 - l <= GQ_LV && lo[le + 1] - lo[l] <= GQ_T && lvm[le + 1] - lvm[l] <= GQ_Q &&
+               eb[le + 1] - eb[l] <= GQ_E)
+          le++;
+        if (le == l) {
+          bt.insert(bt.end(), {l, l + 1, 0u});
+          l++;
+        } else {
+          bt.insert(bt.end(), {l, le, 1u});
+          l = le;
+        }
+      }
+      nbatch = (u32)(bt.size() / 3);
+      X.gq_batch.ensure(bt.size() + 1);
+      CUDA_OK(cudaMemcpyAsync(X.gq_batch.p, bt.data(), bt.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
+    }
+    size_t dyn = (size_t)C * sizeof(double) + (nbatch ? GQ_STAGE_BYTES : 0);
+    k_greedy_cta<<<1, 1024, dyn, s>>>(ord, lvl, 0, nl, ntr, X.gq_lvm.p, X.gq_node.p, X.gq_cost.p, X.gq_eoff.p,
+                                      X.gq_edst.p, X.gq_tot.p, c0.p, n0.p, 1, bflag.p, C, X.gq_batch.p, nbatch);
   } else {
     // thin runs in one CTA, wide levels (> WIDE members or classes) on the grid
     const u32 WIDE = 8192;
@@ -1064,7 +1152,7 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
       u32 l1 = l;
       while (l1 < nl && lvm[l1 + 1] - lvm[l1] <= WIDE && lo[l1 + 1] - lo[l1] <= WIDE) l1++;
       k_greedy_cta<<<1, 1024, 0, s>>>(ord, lvl, l, l1, ntr, X.gq_lvm.p, X.gq_node.p, X.gq_cost.p, X.gq_eoff.p,
-                                      X.gq_edst.p, X.gq_tot.p, c0.p, n0.p, 0, bflag.p);
+                                      X.gq_edst.p, X.gq_tot.p, c0.p, n0.p, 0, bflag.p, 0, nullptr, 0);
       l = l1;
     }
   }
