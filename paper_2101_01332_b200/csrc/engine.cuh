@@ -222,7 +222,7 @@ struct Scratch {
   DevBuf<double> gq_cost, gq_tot;
   DevBuf<i64> k_off;
   // vanilla checkpoint (explore.cu run_rule_vanilla)
-  DevBuf<u32> v_parent, v_rej;
+  DevBuf<u32> v_parent, v_rej, v_tree_hc;
   DevBuf<Val> v_val;
   DevBuf<unsigned long long> v_hc;
   // ILP model skeleton (ilp.cu)

@@ -399,7 +399,7 @@ void Engine::record_reject(int ri, unsigned long long p) {
 // filter_mode "vanilla" (explorer.py:218-220, cycles.py:248-254): every combo
 // that passes the self / compat / shape gates is applied on the live e-graph
 // after a device-to-device checkpoint of the mutable state (union-find
-// parents, analysis values, hashcons, counters); a cycle check from the root
+// parents, analysis values, interned cut trees, hashcons, counters); a cycle check from the root
 // over the un-rebuilt result (peel + reachability, the precheck of
 // break_all_cycles) decides, and a cycle restores the checkpoint.  Applying
 // on the original instead of a clone gives the same e-graph: the apply is
@@ -452,6 +452,10 @@ void Engine::run_rule_vanilla(int ri, int allow_self, i64 n_max, unsigned long l
     if (analysis) {
       sc.v_val.ensure(n0 + 1);
       CUDA_OK(cudaMemcpyAsync(sc.v_val.p, val.p, (size_t)n0 * sizeof(Val), cudaMemcpyDeviceToDevice, s));
+      // interned cut trees (analysis.cuh): table + count, so rejected applies leave no trace
+      sc.v_tree_hc.ensure((size_t)tree_hc_cap + 1);
+      CUDA_OK(cudaMemcpyAsync(sc.v_tree_hc.p, tree_hc.p, (size_t)tree_hc_cap * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+      CUDA_OK(cudaMemcpyAsync(sc.v_tree_hc.p + tree_hc_cap, tree_count.p, sizeof(u32), cudaMemcpyDeviceToDevice, s));
     }
     RuleDev R1 = R;
     R1.vanilla_go = q;
@@ -464,8 +468,11 @@ void Engine::run_rule_vanilla(int ri, int allow_self, i64 n_max, unsigned long l
     if (cyc) {
       CUDA_OK(cudaMemcpyAsync(parent.p, sc.v_parent.p, (size_t)n0 * sizeof(u32), cudaMemcpyDeviceToDevice, s));
       CUDA_OK(cudaMemcpyAsync(hc.p, sc.v_hc.p, (size_t)hc_cap * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-      if (analysis)
+      if (analysis) {
         CUDA_OK(cudaMemcpyAsync(val.p, sc.v_val.p, (size_t)n0 * sizeof(Val), cudaMemcpyDeviceToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(tree_hc.p, sc.v_tree_hc.p, (size_t)tree_hc_cap * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(tree_count.p, sc.v_tree_hc.p + tree_hc_cap, sizeof(u32), cudaMemcpyDeviceToDevice, s));
+      }
       h = h0;
       push_counters();
       snap.valid = false;
