@@ -503,7 +503,12 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
         k_em_big_list<<<nblk(nrows), 256, 0, s>>>(nrows, big.p, bpos.p, head.p, L.p, bh.p, perm.p);
         dev_exclusive_scan_u32(*this, bh.p, gex.p, nbigrows);
         int eb = (int)bits_for(h.next_id);
-        for (int w = stride - 1; w >= -1; w--) {
+        // binding words past the widest pattern that can own a big group are
+        // zero padding for every big row: their passes would be no-ops
+        int wmax = 0;
+        for (int b = 0; b < np; b++)
+          if (B.rbase[b + 1] - B.rbase[b] > SMALL_GROUP) wmax = std::max(wmax, (int)B.pat[b].nb);
+        for (int w = std::min(wmax, stride) - 1; w >= -1; w--) {
           k_em_big_key<<<nblk(nbigrows), 256, 0, s>>>(nbigrows, L.p, perm.p, rb.p, stride, w, bh.p, gex.p, key.p);
           dev_sort_pairs_u32(*this, key.p, key2.p, perm.p, perm2.p, nbigrows, w >= 0 ? eb : (int)bits_for(nbigrows));
           perm.swap(perm2);
