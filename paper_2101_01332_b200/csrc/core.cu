@@ -841,6 +841,13 @@ __global__ void k_class_index(const u32* scls, const u32* headpos, u32 m, u32* c
 
 __global__ void k_set_u32(u32* p, u32 idx, u32 v) { p[idx] = v; }
 
+// number of classes from the head flags / their scan; closes the class CSR
+__global__ void k_close_cls_off(const u32* head, const u32* pos, u32 m, u32* cls_off, u32* ncls) {
+  u32 c = m ? pos[m - 1] + head[m - 1] : 0u;
+  cls_off[c] = m;
+  *ncls = c;
+}
+
 // off[a] = first position of key >= a in a sorted key array (CSR offsets)
 __global__ void k_lower_bounds(const u32* sorted, u32 m, u32 nkeys, u32* off) {
   GRID_STRIDE(a, (u64)nkeys + 1) {
@@ -887,17 +894,13 @@ void Engine::build_snapshot() {
   // tmp = sorted class ids
   k_class_heads<<<nblk(m), 256, 0, s>>>(tmp.p, m, fl.p);
   dev_exclusive_scan_u32(*this, fl.p, pos.p, m);
-  u32 last_head = 0, last_pos = 0;
-  if (m) {
-    CUDA_OK(cudaMemcpyAsync(&last_head, fl.p + m - 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
-    CUDA_OK(cudaMemcpyAsync(&last_pos, pos.p + m - 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  }
-  sync();
-  u32 ncls = m ? last_pos + last_head : 0;
-  snap.cls_off.ensure(ncls + 1);
-  snap.cls_ids.ensure(ncls + 1);
+  // class count stays on the device until the single sync at the end
+  // (buffers sized by the member count, an upper bound)
+  snap.cls_off.ensure(m + 2);
+  snap.cls_ids.ensure(m + 1);
+  snap.d_ncls.ensure(2);
   k_class_index<<<nblk(m), 256, 0, s>>>(tmp.p, pos.p, m, snap.cls_off.p, snap.cls_ids.p, snap.cls_index.p);
-  k_set_u32<<<1, 1, 0, s>>>(snap.cls_off.p, ncls, m);
+  k_close_cls_off<<<1, 1, 0, s>>>(fl.p, pos.p, m, snap.cls_off.p, snap.d_ncls.p);
   snap.cls_of.ensure(m + 1);
   k_member_class<<<nblk(m), 256, 0, s>>>(fl.p, pos.p, m, snap.cls_of.p);
   // op CSR in (op, class, id) order: stable sort of the class-ordered members
@@ -909,12 +912,14 @@ void Engine::build_snapshot() {
   k_lower_bounds<<<nblk((u64)na + 1), 256, 0, s>>>(tmp.p, m, na, snap.op_off.p);
   snap.op_off_h.resize(na + 1);
   CUDA_OK(cudaMemcpyAsync(snap.op_off_h.data(), snap.op_off.p, (na + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  u32 ncls = 0;
+  CUDA_OK(cudaMemcpyAsync(&ncls, snap.d_ncls.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
   snap.n_alloc = n;
   snap.ncls = ncls;
   snap.n_atoms = na;
   snap.valid = true;
   snap_id++;
-  sync();
 }
 
 // ---------------------------------------------------------------- download / dump

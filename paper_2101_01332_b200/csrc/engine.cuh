@@ -158,6 +158,7 @@ struct Snapshot {
   DevBuf<u32> op_off;     // atom -> range in op_nodes
   DevBuf<u32> op_nodes;   // alive nodes in (op, class, id) order
   std::vector<u32> op_off_h;  // host copy of op_off
+  DevBuf<u32> d_ncls;         // class count, read back with op_off_h
   bool valid = false;
 };
 
