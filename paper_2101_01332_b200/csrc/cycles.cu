@@ -559,16 +559,18 @@ i64 Engine::break_all_cycles(bool precheck_only, std::vector<std::vector<u32>>* 
   if (root == TSAT_NONE) throw TsatException(TSAT_ERR_STATE, "e-graph has no root");
   if (!snap.valid) build_snapshot();
   KTimer kt(*this, KG_CYCLES, 0.0, 0);
-  u32 rc = find(root);
-  u32 root_dense;
-  CUDA_OK(cudaMemcpyAsync(&root_dense, snap.cls_index.p + rc, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  sync();
+  u32 root_dense = TSAT_NONE;  // looked up only when some class fails to peel
   i64 added = 0;
   u32 cyc_cap = 1 << 16, off_cap = 1 << 12;
   while (true) {
     ensure_levels();
     u32 n = cg_n;
     if (lv_trimmed == n) return added;  // the whole class graph peels: no live cycle anywhere
+    if (root_dense == TSAT_NONE) {
+      u32 rc = find(root);
+      CUDA_OK(cudaMemcpyAsync(&root_dense, snap.cls_index.p + rc, sizeof(u32), cudaMemcpyDeviceToHost, s));
+      sync();
+    }
     sc.c_mark.ensure(n + 1);
     sc.c_mark32.ensure(n + 1);
     sc.c_fa.ensure(n + 1);

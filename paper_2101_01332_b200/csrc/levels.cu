@@ -450,7 +450,7 @@ static int coop_blocks(Engine& e, const void* fn, int threads) {
 }
 
 // runs the frontier to completion; returns (levels, total processed)
-static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& total) {
+static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& total, u32 ne_known = TSAT_NONE) {
   DevBuf<u32>& ctl = e.sc.c_res;
   ctl.ensure(16);
   CUDA_OK(cudaMemsetAsync(ctl.p, 0, 16 * sizeof(u32), e.s));
@@ -462,9 +462,11 @@ static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& tot
   if (!gblocks) gblocks = coop_blocks(e, (const void*)k_frontier_grid, 256);
   u32 h[5];
   const u64 FR_SMEM = 200u << 10;
-  u32 ne = 0;
-  CUDA_OK(cudaMemcpyAsync(&ne, (F.bfs ? F.eoff : F.roff) + F.n, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-  e.sync();
+  u32 ne = ne_known;
+  if (ne == TSAT_NONE) {
+    CUDA_OK(cudaMemcpyAsync(&ne, (F.bfs ? F.eoff : F.roff) + F.n, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+    e.sync();
+  }
   int use_smem = (12ull * F.n + 4 + 4ull * ne <= FR_SMEM) ? 3
                  : (12ull * F.n + 4 <= FR_SMEM) ? 2 : ((u64)F.n * 4 <= FR_SMEM ? 1 : 0);
   size_t smem_bytes = use_smem == 3   ? (size_t)(3ull * F.n + 1 + ne) * 4
@@ -501,7 +503,7 @@ u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrim
   Frontier F{X.cg_eoff.p, X.cg_edst.p, X.cg_roff.p, X.cg_rsrc.p, mask, X.cg_outdeg.p, X.cg_level.p,
              X.c_order.p, X.c_lvloff.p, nullptr, n, 0};
   u32 nl = 0, tot = 0;
-  run_frontier(e, F, 0, nl, tot);
+  run_frontier(e, F, 0, nl, tot, e.cg_ne);  // class graph: reverse edges = forward edges
   ntrimmed = tot;
   lvl_off.resize(nl + 1);
   CUDA_OK(cudaMemcpyAsync(lvl_off.data(), X.c_lvloff.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
@@ -518,6 +520,9 @@ u32 bfs_graph(Engine& e, const u32* eoff, const u32* edst, u32 n, u32 root, u32*
 }
 
 u32 bfs_classes(Engine& e, u32 root, u32* mark, u32* queue) {
-  return bfs_graph(e, e.sc.cg_eoff.p, e.sc.cg_edst.p, e.cg_n, root, mark, queue);
+  Frontier F{e.sc.cg_eoff.p, e.sc.cg_edst.p, nullptr, nullptr, nullptr, nullptr, nullptr, queue, nullptr, mark, e.cg_n, 1};
+  u32 nl = 0, tot = 0;
+  run_frontier(e, F, root, nl, tot, e.cg_ne);
+  return tot;
 }
 
