@@ -453,7 +453,6 @@ void Engine::build_reach() {
   reach.valid = true;
   kt.bytes = 4.0 * words * ((double)n + (double)cg_ne);
   kt.launches = 2;
-  sync();
 }
 
 // ---------------------------------------------------------------- post-processing

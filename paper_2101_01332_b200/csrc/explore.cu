@@ -501,8 +501,12 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
   for (size_t i = 0; i < rules.size(); i++) (rules[i].nsrc > 1 ? multi : single).push_back((int)i);
   int stop = 0;  // iter-limit
   for (int q = 0; q < 32; q++) phase_ms[q] = 0.0;
+  // host-side phase clocks (tsat_phase_times) need a stream sync per phase:
+  // only when asked for (TSAT_PHASE_SYNC / TSAT_DEBUG_ITERS); the kernel-group
+  // clocks are CUDA events and need none
+  static const bool phase_sync = getenv("TSAT_PHASE_SYNC") || getenv("TSAT_DEBUG_ITERS");
   auto tick = [&](int ph, double& t) {
-    sync();
+    if (phase_sync) sync();
     double n2 = now_s();
     phase_ms[ph] += (n2 - t) * 1e3;
     t = n2;
