@@ -798,8 +798,7 @@ void Engine::rebuild() {
   }
   h.dirty = 0;
   push_counters();
-  sync();
-  check_error();
+  check_error();  // syncs the stream
   snap.valid = false;
 }
 
