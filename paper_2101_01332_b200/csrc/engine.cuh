@@ -214,7 +214,7 @@ struct Scratch {
   DevBuf<u8> c_mark, c_color;
   DevBuf<unsigned char> c_stack;
   // greedy / costs
-  DevBuf<double> g_c0, g_c1, g_upl, k_dv;
+  DevBuf<double> g_c0, g_c1, g_upl, k_dv, g_rinfo;
   DevBuf<u32> g_n0, g_n1, g_flag, g_mark, g_fa, g_fb, g_oc, g_on, k_slots, g_eoff, g_edst, g_cnt;
   DevBuf<char> k_keys;
   DevBuf<u32> gq_batch;

@@ -986,6 +986,18 @@ __global__ void k_sel_compact(const u32* mark, const u32* pos, u32 C, const u32*
   }
 }
 
+__global__ void k_root_info(G g, u32 root, const u32* cls_index, const double* bc, double* out) {
+  u32 rd = cls_index[uf_find_ro(g.parent, root)];
+  out[0] = __longlong_as_double((long long)rd);
+  out[1] = bc[rd];
+}
+
+static inline long long __double_as_longlong_host(double d) {
+  long long x;
+  memcpy(&x, &d, sizeof(x));
+  return x;
+}
+
 __global__ void k_sel_collect(const u32* queue, u32 k, const u32* cls_ids, const u32* bn, u32* oc, u32* on) {
   GRID_STRIDE(t, k) {
     u32 i = queue[t];
@@ -1179,13 +1191,15 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
   kt.bytes = 16.0 * h.live + 12.0 * h.nkids + 12.0 * C;
   kt.launches = 2;
   *rounds = r;
-  u32 rc = find(root);
-  u32 rd;
-  CUDA_OK(cudaMemcpyAsync(&rd, snap.cls_index.p + rc, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  // root class (dense) and its best cost in one round trip
+  DevBuf<double>& rinfo = sc.g_rinfo;
+  rinfo.ensure(2);
+  k_root_info<<<1, 1, 0, s>>>(view(), root, snap.cls_index.p, c0.p, rinfo.p);
+  double hri[2];
+  CUDA_OK(cudaMemcpyAsync(hri, rinfo.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
   sync();
-  double rcost;
-  CUDA_OK(cudaMemcpyAsync(&rcost, c0.p + rd, sizeof(double), cudaMemcpyDeviceToHost, s));
-  sync();
+  const u32 rd = (u32)__double_as_longlong_host(hri[0]);
+  const double rcost = hri[1];
   if (std::isinf(rcost)) throw TsatException(TSAT_ERR_NO_FINITE, "every root selection has infinite cost");
   DevBuf<u32>& mark = sc.g_mark;
   DevBuf<u32>& q = sc.g_fa;
