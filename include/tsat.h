@@ -105,6 +105,11 @@ int tsat_load_rules(tsat_engine* h, int64_t n, const int64_t* blob);
  * RuleStats field order, per_iter = 3 x k_max (enodes, alloc, eclasses) */
 int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self,
                   tsat_report* rep, int64_t* rule_stats, int64_t* per_iter);
+/* one iteration of saturate, iteration number iter_idx of the caller's loop: multi-pattern
+ * rules active iff iter_idx < lim->k_multi (explorer.py:338-352); lim->k_max is ignored.
+ * Per-iteration parity driver (SURVEY 8(b) tsat_iterate). */
+int tsat_iterate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self, int64_t iter_idx,
+                 tsat_report* rep, int64_t* rule_stats, int64_t* per_iter);
 /* filter_mode: 0 "none", 1 "vanilla" (apply on a checkpoint + cycle check per combo,
  * cycles.py:248-254), 2 "efficient" (descendants pre-filter, cycles.py:151-169) */
 

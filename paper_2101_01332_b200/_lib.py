@@ -62,6 +62,8 @@ _SIGS = {
     "tsat_get_filter": ([C.c_void_p, u32p, C.c_int64, i64p], C.c_int),
     "tsat_load_rules": ([C.c_void_p, C.c_int64, i64p], C.c_int),
     "tsat_saturate": ([C.c_void_p, C.POINTER(Limits), C.c_int32, C.c_int32, C.POINTER(Report), i64p, i64p], C.c_int),
+    "tsat_iterate": ([C.c_void_p, C.POINTER(Limits), C.c_int32, C.c_int32, C.c_int64, C.POINTER(Report), i64p, i64p],
+                     C.c_int),
     "tsat_ilp_build": ([C.c_void_p, u32p], C.c_int),
     "tsat_ilp_download": ([C.c_void_p, u32p, u32p, u32p, u32p, u32p, u32p], C.c_int),
     "tsat_set_record_rejects": ([C.c_void_p, C.c_int32], C.c_int),

@@ -245,8 +245,8 @@ int tsat_rejects(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n) {
 
 int tsat_load_rules(tsat_engine* h, int64_t n, const int64_t* blob) { GUARD(h, h->e->load_rules((int)n, blob)); }
 
-int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self, tsat_report* rep,
-                  int64_t* rule_stats, int64_t* per_iter) {
+static int saturate_impl(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self,
+                         tsat_report* rep, int64_t* rule_stats, int64_t* per_iter) {
   GUARD(h, {
     Engine& e = *h->e;
     if (lim->n_max < 0 || lim->k_max < 0 || lim->k_multi < 0)
@@ -282,6 +282,20 @@ int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, i
       per_iter[3 * i + 2] = e.eclasses_per_iter[i];
     }
   });
+}
+
+int tsat_saturate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self, tsat_report* rep,
+                  int64_t* rule_stats, int64_t* per_iter) {
+  return saturate_impl(h, lim, filter_mode, allow_self, rep, rule_stats, per_iter);
+}
+
+int tsat_iterate(tsat_engine* h, const tsat_limits* lim, int32_t filter_mode, int32_t allow_self, int64_t iter_idx,
+                 tsat_report* rep, int64_t* rule_stats, int64_t* per_iter) {
+  if (!lim || iter_idx < 0) return TSAT_ERR_VALUE;
+  tsat_limits one = *lim;
+  one.k_max = 1;
+  one.k_multi = iter_idx < lim->k_multi ? 1 : 0;  // explorer.py:341
+  return saturate_impl(h, &one, filter_mode, allow_self, rep, rule_stats, per_iter);
 }
 
 int tsat_ematch(tsat_engine* h, int32_t pattern, uint32_t* out_cls, uint32_t* out_bind, int64_t cap, int64_t* n,

@@ -96,6 +96,22 @@ class ExploreReport:
         return out
 
 
+def iterate(
+    eg: EGraph,
+    rules: Sequence,
+    iteration: int,
+    limits: Optional[ExploreLimits] = None,
+    filter_mode: str = "efficient",
+    filt: Optional[set] = None,
+    on_reject: Optional[Callable] = None,
+    allow_self_pairs: bool = False,
+):
+    """One iteration of ``saturate`` as iteration number ``iteration`` of the
+    caller's loop (multi-pattern rules active iff ``iteration < limits.k_multi``,
+    explorer.py:338-352); ``tsat_iterate``.  Returns (filter list, ExploreReport)."""
+    return saturate(eg, rules, limits, filter_mode, filt, on_reject, allow_self_pairs, _iteration=int(iteration))
+
+
 def saturate(
     eg: EGraph,
     rules: Sequence,
@@ -104,6 +120,7 @@ def saturate(
     filt: Optional[set] = None,
     on_reject: Optional[Callable] = None,
     allow_self_pairs: bool = False,
+    _iteration: Optional[int] = None,
 ):
     """Iterate rules on ``eg`` (mutated in place) until saturation or a limit.
     Returns (filter list, ExploreReport); ``filt`` is updated in place.
@@ -130,12 +147,18 @@ def saturate(
     rep = _lib.Report()
     rs = np.zeros(max(len(rules), 1) * 7, np.int64)
     per = np.zeros(max(limits.k_max, 1) * 3, np.int64)
+    if _iteration is not None and _iteration < 0:
+        raise ValueError("iteration must be non-negative")
     if on_reject is not None:
         _lib.check(eg._h, lib.tsat_set_record_rejects(eg._h, 1))
     try:
-        _lib.check(eg._h, lib.tsat_saturate(eg._h, C.byref(lim), _MODE_CODE[filter_mode],
-                                            1 if allow_self_pairs else 0, C.byref(rep),
-                                            _lib.ptr(rs, C.c_int64), _lib.ptr(per, C.c_int64)))
+        if _iteration is None:
+            st = lib.tsat_saturate(eg._h, C.byref(lim), _MODE_CODE[filter_mode], 1 if allow_self_pairs else 0,
+                                   C.byref(rep), _lib.ptr(rs, C.c_int64), _lib.ptr(per, C.c_int64))
+        else:
+            st = lib.tsat_iterate(eg._h, C.byref(lim), _MODE_CODE[filter_mode], 1 if allow_self_pairs else 0,
+                                  _iteration, C.byref(rep), _lib.ptr(rs, C.c_int64), _lib.ptr(per, C.c_int64))
+        _lib.check(eg._h, st)
     finally:
         eg._touch()
         if on_reject is not None:

@@ -186,3 +186,23 @@ def test_vanilla_against_oracle_and_slower_than_efficient():
         out[mode] = rep
     assert out["efficient"].rules["matmul-merge-shared-lhs"].found >= 1000
     assert out["efficient"].time_s < out["vanilla"].time_s
+
+
+@pytest.mark.parametrize("case", EXPLORE[::3], ids=[c["id"] for c in EXPLORE[::3]])
+def test_tsat_iterate_matches_reference_per_iteration(case):
+    """The per-iteration C entry point (tsat_iterate through explorer.iterate):
+    iteration i of the caller's loop gates the multi-pattern rules itself."""
+    from paper_2101_01332_b200.explorer import iterate
+
+    g = cases.build_graph(bench_graphs, tensor_lang, case["graph"])
+    rules = cases.select_rules(default_rules(), case["rules"])
+    lim = ExploreLimits(**case["limits"])
+    eg, _ = build_egraph(g)
+    filt = set()
+    for i, snap in enumerate(case["iterations"]):
+        filt, rep = iterate(eg, rules, i, lim, case["filter_mode"], filt=filt,
+                            allow_self_pairs=case["allow_self_pairs"])
+        assert eg.dump() == snap["dump"], f"iteration {i}"
+        assert sorted(filt) == snap["filt"], f"iteration {i}"
+        if rep.stop_reason != "iter-limit":
+            break
