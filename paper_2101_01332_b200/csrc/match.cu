@@ -510,7 +510,7 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
           if (B.rbase[b + 1] - B.rbase[b] > SMALL_GROUP) wmax = std::max(wmax, (int)B.pat[b].nb);
         for (int w = std::min(wmax, stride) - 1; w >= -1; w--) {
           k_em_big_key<<<nblk(nbigrows), 256, 0, s>>>(nbigrows, L.p, perm.p, rb.p, stride, w, bh.p, gex.p, key.p);
-          dev_sort_pairs_u32(*this, key.p, key2.p, perm.p, perm2.p, nbigrows, w >= 0 ? eb : (int)bits_for(nbigrows));
+          dev_sort_pairs_u32(*this, key.p, key2.p, perm.p, perm2.p, nbigrows, w >= 0 ? eb : (int)bits_for(nbigrows / (SMALL_GROUP + 1)));  // every big group has > SMALL_GROUP rows
           perm.swap(perm2);
         }
         k_em_big_scatter<<<nblk(nbigrows), 256, 0, s>>>(nbigrows, L.p, perm.p, rc.p, rb.p, stride, scl.p, sbd.p);
