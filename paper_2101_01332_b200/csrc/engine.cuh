@@ -361,6 +361,8 @@ struct Engine {
 
   // exploration
   bool seq_changed = false, seq_stop = false;
+  bool seq_timeout = false;      // vanilla: deadline passed between combos
+  double apply_deadline = -1.0;  // saturate's deadline (now_s clock), < 0: none
   bool force_seq = false;  // debug: exact sequential path only
   std::vector<std::string> rule_names;
   void apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P);

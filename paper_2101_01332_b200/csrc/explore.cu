@@ -426,6 +426,12 @@ void Engine::run_rule_vanilla(int ri, int allow_self, i64 n_max, unsigned long l
   };
   unsigned long long p = 0;
   while (p < P) {
+    // the reference checks its deadline before every combo (explorer.py:198-201);
+    // the host loop here sees every combo that reaches the cycle check
+    if (apply_deadline >= 0 && now_s() > apply_deadline) {
+      seq_timeout = true;
+      return;
+    }
     DevStats d;
     launch(R, p, P, d);
     accumulate(*this, ri, d);
@@ -538,6 +544,8 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
     tick(2, tp);
     seq_changed = false;
     seq_stop = false;
+    seq_timeout = false;
+    apply_deadline = deadline;
     int stop_flag = 0;
     for (int ri : active) {
       const HRule& hr = rules[ri];
@@ -551,6 +559,10 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
       apply_rule(ri, filter_mode, allow_self, lim.n_max, P);
       if (seq_stop) {
         stop_flag = 2;
+        break;
+      }
+      if (seq_timeout) {
+        stop_flag = 3;
         break;
       }
     }
