@@ -127,15 +127,18 @@ def saturate(
 
     ``filter_mode="vanilla"`` checks each combo by applying it on a device
     checkpoint and running the cycle check from the root (cycles.py:248-254).
-    ``on_reject(eg, filt, rule, matches)`` is the post-saturation variant of
+    ``on_reject(eg, filt, rule, matches)`` is the post-iteration variant of
     the reference hook (explorer.py:223-224): the device records every
     cycle-rejected combo (rule + snapshot Match per source, in rejection
-    order) and the callbacks run after the search, with the final e-graph;
-    the live mid-iteration e-graph never leaves the GPU.  Recording routes
+    order) and the callbacks run after each iteration (the search is driven
+    one iteration at a time), with the e-graph as that iteration left it; the
+    live mid-iteration e-graph never leaves the GPU.  Recording routes
     efficient-mode rules through the exact sequential path."""
     limits = limits or ExploreLimits()
     if filter_mode not in FILTER_MODES:
         raise ValueError(f"filter_mode must be one of {FILTER_MODES}")
+    if on_reject is not None and _iteration is None:
+        return _saturate_per_iteration(eg, rules, limits, filter_mode, filt, on_reject, allow_self_pairs)
     filt = set() if filt is None else filt
     rules = list(rules)
     eg.set_filter(filt)
@@ -189,6 +192,44 @@ def saturate(
     for rule, matches in rejected:
         on_reject(eg, filt, rule, matches)
     return filt, report
+
+
+def _saturate_per_iteration(eg, rules, limits, filter_mode, filt, on_reject, allow_self_pairs):
+    """saturate() driven one iteration at a time (tsat_iterate), so on_reject
+    sees each iteration's rejected combos right after that iteration, with the
+    e-graph as the iteration left it (explorer.py:311-365 loop structure)."""
+    import dataclasses
+    import time
+
+    t0 = time.perf_counter()
+    filt = set() if filt is None else filt
+    rules = list(rules)
+    total = ExploreReport(stop_reason="iter-limit")
+    for r in rules:
+        total.rules.setdefault(r.name, RuleStats())
+    for i in range(limits.k_max):
+        lim = limits
+        if limits.time_limit_s is not None:
+            lim = dataclasses.replace(limits, time_limit_s=max(0.0, limits.time_limit_s - (time.perf_counter() - t0)))
+        filt, rep = saturate(eg, rules, lim, filter_mode, filt, on_reject, allow_self_pairs, _iteration=i)
+        total.iterations += rep.iterations
+        total.enodes_per_iter += rep.enodes_per_iter
+        total.alloc_per_iter += rep.alloc_per_iter
+        total.eclasses_per_iter += rep.eclasses_per_iter
+        for name, st in rep.rules.items():
+            acc = total.rules.setdefault(name, RuleStats())
+            for f in _RULE_FIELDS:
+                setattr(acc, f, getattr(acc, f) + getattr(st, f))
+        total.prefilter_checks += rep.prefilter_checks
+        total.prefilter_rejects += rep.prefilter_rejects
+        total.postprocess_filtered += rep.postprocess_filtered
+        total.node_limit_overshoot = rep.node_limit_overshoot
+        if rep.stop_reason != "iter-limit":
+            total.stop_reason = rep.stop_reason
+            break
+    total.filter_size = len(filt)
+    total.time_s = time.perf_counter() - t0
+    return filt, total
 
 
 def _rejected_combos(eg: EGraph, rules) -> list:

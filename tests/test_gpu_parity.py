@@ -151,7 +151,7 @@ _FILTERED = [c for c in EXPLORE if c["filter_mode"] != "none"]
 
 @pytest.mark.parametrize("case", _FILTERED, ids=[c["id"] for c in _FILTERED])
 def test_on_reject_matches_reference(case):
-    """on_reject (post-saturation variant) sees the reference's rejected combos
+    """on_reject (post-iteration variant) sees the reference's rejected combos
     in the reference's order; recording (efficient: exact sequential path)
     leaves the result unchanged."""
     g = cases.build_graph(bench_graphs, tensor_lang, case["graph"])
