@@ -202,6 +202,7 @@ struct KTimer {  // records CUDA events on the engine stream around a kernel gro
 // persistent scratch buffers (grown on demand, never freed inside a run)
 struct Scratch {
   // e-matching
+  DevBuf<u32> m_heavy;
   DevBuf<u32> m_rc, m_rb, m_cnt, m_perm, m_perm2, m_key, m_key2, m_fl, m_pos;
   DevBuf<u32> m_bnd, m_big, m_head, m_bpos, m_L, m_bh, m_gex, m_bperm, m_bperm2, m_bkey, m_bkey2;
   // sharding (shard.cu)

@@ -202,25 +202,184 @@ __device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const P
   return count;
 }
 
+#define EM_HEAVY 0xFFFFFFFFu
+#define EM_HEAVY_L1 16u
+
+// match_root restricted to part of the level-1 members: the members at
+// positions l1_first, l1_first + l1_stride, ... of apps[1]'s class, at most
+// l1_lim of them (DFS order within the part unchanged).  *l1_size receives
+// the class size (1 for single-app patterns, whose only part is part 0).
+template <int MV, int MA, class F>
+__device__ __forceinline__ u32 match_root_part(const G& g, const SnapDev& sd, const PatDev& p, u32 r, u32 l1_first,
+                                               u32 l1_stride, u32 l1_lim, u32* l1_size, F emit,
+                                               u32 heavy_cut = 0xFFFFFFFFu) {
+  *l1_size = 0;
+  if (!node_ok(g, r, p.apps[0])) return 0;
+  u32 env[MV];
+  int8_t bound_at[MV];
+  u32 cls_app[MA];
+  u32 pos[MA], end[MA];
+  for (int v = 0; v < MV; v++) {
+    env[v] = TSAT_NONE;
+    bound_at[v] = -1;
+  }
+  if (!bind_node(g, p.apps[0], r, 0, env, bound_at, cls_app)) return 0;
+  u32 rc = uf_find_ro(g.parent, r);
+  if (p.napps == 1) {
+    *l1_size = 1;
+    if (l1_first != 0) return 0;
+    emit(0u, rc, env);
+    return 1;
+  }
+  u32 count = 0, taken1 = 0;
+  int level = 1;
+  bool init = true;
+  while (true) {
+    if (level == p.napps) {
+      emit(count, rc, env);
+      count++;
+      level--;
+      unbind<MV>(level, env, bound_at);
+      init = false;
+      continue;
+    }
+    if (init) {
+      u32 c = cls_app[level];
+      u32 d = c < sd.n_alloc ? sd.cls_index[c] : TSAT_NONE;
+      if (d == TSAT_NONE) {
+        pos[level] = end[level] = 0;
+      } else {
+        pos[level] = sd.cls_off[d];
+        end[level] = sd.cls_off[d + 1];
+      }
+      if (level == 1) {
+        *l1_size = end[1] - pos[1];
+        if (*l1_size > heavy_cut) return EM_HEAVY;  // before any emit: the caller hands it to a warp
+        pos[1] += l1_first;
+      }
+    }
+    bool found = false;
+    const PatApp& a = p.apps[level];
+    while (pos[level] < end[level]) {
+      u32 m;
+      if (level == 1) {
+        if (taken1 >= l1_lim) {
+          pos[1] = end[1];
+          break;
+        }
+        m = sd.cls_nodes[pos[1]];
+        pos[1] += l1_stride;
+        taken1++;
+      } else {
+        m = sd.cls_nodes[pos[level]++];
+      }
+      if (!node_ok(g, m, a)) continue;
+      if (bind_node(g, a, m, level, env, bound_at, cls_app)) {
+        found = true;
+        break;
+      }
+      unbind<MV>(level, env, bound_at);
+    }
+    if (found) {
+      level++;
+      init = true;
+    } else {
+      level--;
+      if (level == 0) break;
+      unbind<MV>(level, env, bound_at);
+      init = false;
+    }
+  }
+  return count;
+}
+
+// Nested patterns, one warp per root candidate: the lanes split the members
+// of apps[1]'s class (large classes of commuted / reassociated forms made one
+// thread's DFS hold its whole warp).  Fast (single-app) patterns stay on the
+// thread-per-candidate kernels.
+template <int MV, int MA>
+__global__ void k_em_count_w(G g, SnapDev sd, Batch B, const u32* heavy, const u32* nheavy, u32* cnt) {
+  const u32 lane = threadIdx.x & 31;
+  const u64 w0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  const u32 nh = *nheavy;
+  for (u64 i = w0; i < nh; i += nw) {
+    const u32 t = heavy[i];
+    int p = seg_of(B.cbase, B.npat, t);
+    const PatDev& pd = B.pat[p];
+    u32 r = sd.op_nodes[B.obase[p] + (t - B.cbase[p])];
+    u32 sz;
+    u32 c = match_root_part<MV, MA>(g, sd, pd, r, lane, 32u, 0xFFFFFFFFu, &sz, [](u32, u32, const u32*) {});
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[t] = c;
+  }
+}
+
+template <int MV, int MA>
+__global__ void k_em_emit_w(G g, SnapDev sd, Batch B, const u32* heavy, const u32* nheavy, const u32* off, u32* rc,
+                            u32* rb) {
+  const u32 lane = threadIdx.x & 31;
+  const u64 w0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  const int S = B.stride;
+  const u32 nh = *nheavy;
+  for (u64 i = w0; i < nh; i += nw) {
+    const u32 t = heavy[i];
+    int p = seg_of(B.cbase, B.npat, t);
+    const PatDev& pd = B.pat[p];
+    u32 r = sd.op_nodes[B.obase[p] + (t - B.cbase[p])];
+    u32 o = off[t];
+    u32 sz = 0;
+    match_root_part<MV, MA>(g, sd, pd, r, 0xFFFFFFFFu, 1u, 0u, &sz, [](u32, u32, const u32*) {});
+    // sz: apps[1]'s class size (or 1); members in chunks of 32, one per lane
+    for (u32 c0 = 0; c0 < sz; c0 += 32) {
+      u32 mine = 0, dummy;
+      if (c0 + lane < sz)
+        mine = match_root_part<MV, MA>(g, sd, pd, r, c0 + lane, 1u, 1u, &dummy, [](u32, u32, const u32*) {});
+      u32 inc = mine;
+      for (int d = 1; d < 32; d <<= 1) {
+        u32 y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= (u32)d) inc += y;
+      }
+      u32 tot = __shfl_sync(0xffffffffu, inc, 31);
+      u32 base = o + inc - mine;
+      if (mine)
+        match_root_part<MV, MA>(g, sd, pd, r, c0 + lane, 1u, 1u, &dummy, [&](u32 k, u32 cls, const u32* env) {
+          rc[base + k] = cls;
+          for (int j = 0; j < S; j++) rb[(u64)(base + k) * S + j] = j < pd.nb ? env[pd.order[j]] : 0u;
+        });
+      o += tot;
+    }
+  }
+}
+
 // MV / MA: DFS state sizes (small instantiation keeps the state in few
 // registers + little local memory; the large one covers any loadable pattern)
 template <int MV, int MA>
-__global__ void k_em_count(G g, SnapDev sd, Batch B, u32 ntot, u32* cnt) {
+__global__ void k_em_count(G g, SnapDev sd, Batch B, u32 ntot, u32* cnt, u32* heavy, u32* nheavy) {
   GRID_STRIDE(t, ntot) {
     int p = seg_of(B.cbase, B.npat, (u32)t);
     u32 r = sd.op_nodes[B.obase[p] + ((u32)t - B.cbase[p])];
     const PatDev& pd = B.pat[p];
+    if (!pd.fast && heavy) {
+      // nested pattern: a candidate whose apps[1] class is large goes to a warp (k_em_count_w)
+      u32 sz;
+      u32 c = match_root_part<MV, MA>(g, sd, pd, r, 0u, 1u, 0xFFFFFFFFu, &sz, [](u32, u32, const u32*) {},
+                                      EM_HEAVY_L1);
+      if (c == EM_HEAVY) heavy[atomicAdd(nheavy, 1u)] = (u32)t;
+      else cnt[t] = c;
+      continue;
+    }
     cnt[t] = pd.fast ? match_root1<false>(g, pd, r, [](u32, const u32*) {})
                            : match_root<MV, MA>(g, sd, pd, r, [](u32, u32, const u32*) {});
   }
 }
 
 template <int MV, int MA>
-__global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u32* rc, u32* rb) {
+__global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u32* rc, u32* rb, int split) {
   GRID_STRIDE(t, ntot) {
     int p = seg_of(B.cbase, B.npat, (u32)t);
     const PatDev& pd = B.pat[p];
     u32 r = sd.op_nodes[B.obase[p] + ((u32)t - B.cbase[p])];
+
     u32 o = off[t];
     const int S = B.stride;
     if (pd.fast) {
@@ -230,10 +389,16 @@ __global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u3
       });
       continue;
     }
-    match_root<MV, MA>(g, sd, pd, r, [&](u32 k, u32 cls, const u32* env) {
+    auto put = [&](u32 k, u32 cls, const u32* env) {
       rc[o + k] = cls;
       for (int j = 0; j < S; j++) rb[(u64)(o + k) * S + j] = j < pd.nb ? env[pd.order[j]] : 0u;
-    });
+    };
+    if (split) {
+      u32 sz;  // heavy candidates (large apps[1] class) are emitted by k_em_emit_w
+      match_root_part<MV, MA>(g, sd, pd, r, 0u, 1u, 0xFFFFFFFFu, &sz, put, EM_HEAVY_L1);
+    } else {
+      match_root<MV, MA>(g, sd, pd, r, put);
+    }
   }
 }
 
@@ -428,8 +593,24 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
     bnd.ensure(2 * (MAX_BATCH + 1));
     bool small = maxapps <= 4 && stride <= 8;
     for (int b = 0; b < np; b++) small &= B.pat[b].nb <= 8;
-    if (small) k_em_count<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p);
-    else k_em_count<MAX_VARS, MAX_PAT_APPS><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p);
+    static const bool em_warp = getenv("TSAT_EM_THREAD") == nullptr;  // debug: thread-per-candidate DFS only
+    bool nested = false;
+    for (int b = 0; b < np; b++) nested |= !B.pat[b].fast;
+    const int split = (em_warp && nested) ? 1 : 0;
+    DevBuf<u32>& heavy = sc.m_heavy;
+    if (split) {
+      heavy.ensure((u64)ntot + 2);
+      CUDA_OK(cudaMemsetAsync(heavy.p + ntot, 0, sizeof(u32), s));
+    }
+    u32* nheavy = split ? heavy.p + ntot : nullptr;
+    const unsigned wblk = 148u * 8u;
+    if (small) k_em_count<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p, split ? heavy.p : nullptr, nheavy);
+    else k_em_count<MAX_VARS, MAX_PAT_APPS><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p,
+                                                                             split ? heavy.p : nullptr, nheavy);
+    if (split) {
+      if (small) k_em_count_w<8, 4><<<wblk, 256, 0, s>>>(view(), sd, B, heavy.p, nheavy, cnt.p);
+      else k_em_count_w<MAX_VARS, MAX_PAT_APPS><<<wblk, 256, 0, s>>>(view(), sd, B, heavy.p, nheavy, cnt.p);
+    }
     CUDA_OK(cudaMemsetAsync(cnt.p + ntot, 0, sizeof(u32), s));
     dev_exclusive_scan_u32(*this, cnt.p, off.p, ntot + 1);
     k_em_bounds<<<1, 32, 0, s>>>(off.p, B, bnd.p);
@@ -473,8 +654,14 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
       bpos.ensure(nrows + 1);
       big.ensure(nrows + 1);
       head.ensure(nrows + 1);
-      if (small) k_em_emit<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p);
-      else k_em_emit<MAX_VARS, MAX_PAT_APPS><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p);
+      if (small) k_em_emit<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p, split);
+      else k_em_emit<MAX_VARS, MAX_PAT_APPS><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p,
+                                                                            split);
+      if (split) {
+        if (small) k_em_emit_w<8, 4><<<wblk, 256, 0, s>>>(view(), sd, B, heavy.p, nheavy, off.p, rc.p, rb.p);
+        else k_em_emit_w<MAX_VARS, MAX_PAT_APPS><<<wblk, 256, 0, s>>>(view(), sd, B, heavy.p, nheavy, off.p, rc.p,
+                                                                      rb.p);
+      }
       k_em_rank<<<nblk(nrows), 256, 0, s>>>(B, nrows, rc.p, rb.p, scl.p, sbd.p, big.p, head.p);
       // large groups: stable LSD radix sort of their rows by (group, bindings)
       CUDA_OK(cudaMemsetAsync(big.p + nrows, 0, sizeof(u32), s));
