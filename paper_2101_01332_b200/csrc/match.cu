@@ -203,7 +203,7 @@ __device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const P
 }
 
 #define EM_HEAVY 0xFFFFFFFFu
-#define EM_HEAVY_L1 16u
+#define EM_HEAVY_L1 8u  // measured flat between 4 and 16 on BERT (TSAT_EM_CUT)
 
 // match_root restricted to part of the level-1 members: the members at
 // positions l1_first, l1_first + l1_stride, ... of apps[1]'s class, at most
@@ -354,7 +354,7 @@ __global__ void k_em_emit_w(G g, SnapDev sd, Batch B, const u32* heavy, const u3
 // MV / MA: DFS state sizes (small instantiation keeps the state in few
 // registers + little local memory; the large one covers any loadable pattern)
 template <int MV, int MA>
-__global__ void k_em_count(G g, SnapDev sd, Batch B, u32 ntot, u32* cnt, u32* heavy, u32* nheavy) {
+__global__ void k_em_count(G g, SnapDev sd, Batch B, u32 ntot, u32* cnt, u32* heavy, u32* nheavy, u32 cut) {
   GRID_STRIDE(t, ntot) {
     int p = seg_of(B.cbase, B.npat, (u32)t);
     u32 r = sd.op_nodes[B.obase[p] + ((u32)t - B.cbase[p])];
@@ -362,8 +362,7 @@ __global__ void k_em_count(G g, SnapDev sd, Batch B, u32 ntot, u32* cnt, u32* he
     if (!pd.fast && heavy) {
       // nested pattern: a candidate whose apps[1] class is large goes to a warp (k_em_count_w)
       u32 sz;
-      u32 c = match_root_part<MV, MA>(g, sd, pd, r, 0u, 1u, 0xFFFFFFFFu, &sz, [](u32, u32, const u32*) {},
-                                      EM_HEAVY_L1);
+      u32 c = match_root_part<MV, MA>(g, sd, pd, r, 0u, 1u, 0xFFFFFFFFu, &sz, [](u32, u32, const u32*) {}, cut);
       if (c == EM_HEAVY) heavy[atomicAdd(nheavy, 1u)] = (u32)t;
       else cnt[t] = c;
       continue;
@@ -374,7 +373,7 @@ __global__ void k_em_count(G g, SnapDev sd, Batch B, u32 ntot, u32* cnt, u32* he
 }
 
 template <int MV, int MA>
-__global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u32* rc, u32* rb, int split) {
+__global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u32* rc, u32* rb, int split, u32 cut) {
   GRID_STRIDE(t, ntot) {
     int p = seg_of(B.cbase, B.npat, (u32)t);
     const PatDev& pd = B.pat[p];
@@ -395,7 +394,7 @@ __global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u3
     };
     if (split) {
       u32 sz;  // heavy candidates (large apps[1] class) are emitted by k_em_emit_w
-      match_root_part<MV, MA>(g, sd, pd, r, 0u, 1u, 0xFFFFFFFFu, &sz, put, EM_HEAVY_L1);
+      match_root_part<MV, MA>(g, sd, pd, r, 0u, 1u, 0xFFFFFFFFu, &sz, put, cut);
     } else {
       match_root<MV, MA>(g, sd, pd, r, put);
     }
@@ -604,9 +603,10 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
     }
     u32* nheavy = split ? heavy.p + ntot : nullptr;
     const unsigned wblk = 148u * 8u;
-    if (small) k_em_count<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p, split ? heavy.p : nullptr, nheavy);
+    static const u32 cut = getenv("TSAT_EM_CUT") ? (u32)atoi(getenv("TSAT_EM_CUT")) : EM_HEAVY_L1;
+    if (small) k_em_count<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p, split ? heavy.p : nullptr, nheavy, cut);
     else k_em_count<MAX_VARS, MAX_PAT_APPS><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, cnt.p,
-                                                                             split ? heavy.p : nullptr, nheavy);
+                                                                             split ? heavy.p : nullptr, nheavy, cut);
     if (split) {
       if (small) k_em_count_w<8, 4><<<wblk, 256, 0, s>>>(view(), sd, B, heavy.p, nheavy, cnt.p);
       else k_em_count_w<MAX_VARS, MAX_PAT_APPS><<<wblk, 256, 0, s>>>(view(), sd, B, heavy.p, nheavy, cnt.p);
@@ -654,9 +654,9 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
       bpos.ensure(nrows + 1);
       big.ensure(nrows + 1);
       head.ensure(nrows + 1);
-      if (small) k_em_emit<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p, split);
+      if (small) k_em_emit<8, 4><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p, split, cut);
       else k_em_emit<MAX_VARS, MAX_PAT_APPS><<<nblk(ntot, 128), 128, 0, s>>>(view(), sd, B, ntot, off.p, rc.p, rb.p,
-                                                                            split);
+                                                                            split, cut);
       if (split) {
         if (small) k_em_emit_w<8, 4><<<wblk, 256, 0, s>>>(view(), sd, B, heavy.p, nheavy, off.p, rc.p, rb.p);
         else k_em_emit_w<MAX_VARS, MAX_PAT_APPS><<<wblk, 256, 0, s>>>(view(), sd, B, heavy.p, nheavy, off.p, rc.p,
