@@ -21,6 +21,8 @@
 
 #include <cub/cub.cuh>
 
+#include <chrono>
+
 #include "engine.cuh"
 
 namespace cg = cooperative_groups;
@@ -366,8 +368,24 @@ u32 bfs_classes(Engine& e, u32 root, u32* mark, u32* queue);
 void Engine::ensure_levels() {
   if (!snap.valid) build_snapshot();
   if (lv_snap == snap_id && lv_filter == filter_id) return;
+  static const bool dbg = getenv("TSAT_DEBUG_LEVELS") != nullptr;
+  double t0 = 0, t1 = 0;
+  if (dbg) {
+    sync();
+    t0 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
   build_class_graph(*this);
+  if (dbg) {
+    sync();
+    t1 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
   lv_n = trim_levels(*this, nullptr, lv_off, lv_trimmed);
+  if (dbg) {
+    sync();
+    double t2 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    fprintf(stderr, "levels: classes %u edges %u class graph %.3f ms peel %.3f ms (%u levels)\n", cg_n, cg_ne, t1 - t0,
+            t2 - t1, lv_n);
+  }
   lv_snap = snap_id;
   lv_filter = filter_id;
 }
