@@ -124,54 +124,92 @@ def build_workload(name, sample=False):
     return models.MODELS[w["model"]](), list(default_rules()), w
 
 
-def run_oracle_once(name):
+def _ref_modules():
+    """The reference's own package (oracle/_ref/tensorsat, installed there by
+    __graft_entry__.build() from /root/reference; test infrastructure that
+    travels to the GPU box) when present, else the golden-pinned CPU port."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "tensorsat")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import tensorsat.cost as rc
+        import tensorsat.explorer as rx
+        import tensorsat.extract as re_
+        import tensorsat.rules as rr
+        import tensorsat.tensor_lang as rt
+
+        return "reference", (rx, rc, re_, rr, rt)
+    return "port", None
+
+
+def run_cpu_once(name, sample=True):
+    """One explore + egraph_costs + greedy_extract on one host core: the
+    reference package itself when installed (kind "reference"), else the port
+    (kind "port").  The graph is handed over as tensorgraph v1 text."""
+    from paper_2101_01332_b200.tensor_lang import emit_graph
+
+    g, rules, w = build_workload(name, sample=sample)
+    kind, mods = _ref_modules()
+    if kind == "reference":
+        rx, rc, re_, rr, rt = mods
+        rg = rt.make_single_rooted(rt.parse_graph(emit_graph(g)))
+        names = {r.name for r in rules}
+        rrules = [r for r in rr.default_rules() if r.name in names]
+        t0 = time.perf_counter()
+        eg, filt, rep = rx.explore(rg, rrules, rx.ExploreLimits(n_max=w["n_max"], k_max=w["k_max"],
+                                                                k_multi=w["k_multi"]), "efficient")
+        costs = rc.egraph_costs(eg, rc.CostModel())
+        res = re_.greedy_extract(eg, costs, filt)
+        return time.perf_counter() - t0, eg.num_nodes, res.total_cost, kind
     from oracle import tsat_oracle as O
     from paper_2101_01332_b200.cost import CostModel
 
-    g, rules, w = build_workload(name, sample=True)
     t0 = time.perf_counter()
     eg, filt, rep = O.oracle_explore(g, rules, n_max=w["n_max"], k_max=w["k_max"], k_multi=w["k_multi"])
     costs = O.oracle_costs(eg, CostModel())
     sel, total, _ = O.oracle_greedy(eg, costs, filt)
-    return time.perf_counter() - t0, eg.num_nodes, total
+    return time.perf_counter() - t0, eg.num_nodes, total, kind
 
 
-def _oracle_worker(name):
-    return run_oracle_once(name)
+def _scale_10m(w):
+    n = w["sample_n"]
+    return (5 * 1415 * 1415 - 1415 + 3) / (5 * n * n - n + 3)
 
 
 def reference_arm(args):
+    """The reference's CPU implementation on the same workload, metric and
+    config as the B200 arm: one graph per step (the metric is search time per
+    graph; the pure-Python reference is single-threaded by construction, so
+    one graph uses one core)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import multiprocessing as mp
-
-    cores = os.cpu_count() or 1
-    g, rules, w = build_workload(args.workload)
+    _, _, w = build_workload(args.workload, sample=True)
     times = []
-    with mp.get_context("fork").Pool(cores) as pool:
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            res = pool.map(_oracle_worker, [args.workload] * cores)
-            dt = time.perf_counter() - t0
-            if i >= args.warmup:
-                times.append(dt)
-    per_graph = statistics.mean(times) / cores
+    nodes = total = kind = None
+    warm = min(args.warmup, 1)  # CPython has nothing to warm beyond imports; bounds the run
+    for i in range(warm + args.steps):
+        dt, nodes, total, kind = run_cpu_once(args.workload)
+        if i >= warm:
+            times.append(dt)
+    per_graph = statistics.mean(times)
     sample = "the full graph"
     if "sample_n" in w:
-        # bounded sample (matmul_chain(sample_n)); scale by e-node count to the full config
-        n = w["sample_n"]
-        per_graph *= (5 * 1415 * 1415 - 1415 + 3) / (5 * n * n - n + 3)
-        sample = f"matmul_chain({n}) per core, scaled by e-node count to matmul_chain(1415)"
+        per_graph *= _scale_10m(w)
+        sample = (f"matmul_chain({w['sample_n']}) ({nodes} e-nodes), scaled by e-node count to "
+                  f"matmul_chain(1415)")
+    src = ("tensorsat (the reference package, oracle/_ref)" if kind == "reference"
+           else "the golden-pinned CPU port (oracle/tsat_oracle.py)")
     line = {
         "impl": "reference", "metric": "explore+extract search time (s) per graph", "value": per_graph,
-        "unit": "s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": statistics.mean(times) * 1e3, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32+f64", "data": "synthetic (authored model graph)",
-        "config": {"workload": w["desc"], "graphs_per_step": cores},
-        "cpu_baseline": {"value": per_graph, "unit": "s", "cores": cores, "kind": "port",
-                         "sample": f"{cores} concurrent explore+costs+greedy runs per step on {sample} "
-                                   f"(oracle/tsat_oracle.py)"},
+        "unit": "s", "n_gpus": args.gpus, "steps": args.steps, "warmup": warm, "ms_per_step": per_graph * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64",
+        "data": "synthetic (authored model graph, random-free)",
+        "config": {"workload": w["desc"], "graphs_per_step": 1},
+        "result": {"final_enodes": nodes, "total_cost": total},
+        "cpu_baseline": {"value": per_graph, "unit": "s", "cores": 1, "kind": kind,
+                         "sample": f"one explore+egraph_costs+greedy_extract per step on {sample}, {src}, "
+                                   f"1 core of {os.cpu_count()}"},
         "e2e": {"value": per_graph, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -325,8 +363,8 @@ def main():
         "dtype": "int32+f64",
         "data": "synthetic (authored model graph, random-free; L2 flushed between steps)",
         "config": {"workload": w["desc"], "graphs_per_step": 1 if shard_mode else world,
-                   "l2": "flushed (256 MiB write) between steps",
-                   "final_enodes": nodes, "stop_reason": rep.stop_reason, "total_cost": res.total_cost,
+                   "l2": "flushed (256 MiB write) between steps"},
+        "result": {"final_enodes": nodes, "stop_reason": rep.stop_reason, "total_cost": res.total_cost,
                    "parallelism": f"ematch-shard x{world}" if shard_mode else f"replicas x{world}"},
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "enodes_matched_per_s": None, "kernel_groups_ms_per_step": groups_ms,
@@ -370,17 +408,17 @@ def main():
                                                 "peak_GBps": sw["peak_GBps"],
                                                 "enodes_matched_per_s": sw["enodes_matched_per_s"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t_cpu, n_cpu, total_cpu = run_oracle_once(args.workload)
+        t_cpu, n_cpu, total_cpu, kind = run_cpu_once(args.workload)
+        src = "tensorsat, oracle/_ref" if kind == "reference" else "oracle/tsat_oracle.py"
         if "sample_n" in w:
-            n = w["sample_n"]
-            scale = (5 * 1415 * 1415 - 1415 + 3) / (5 * n * n - n + 3)
-            line["cpu_baseline"] = {"value": t_cpu * scale, "unit": "s", "cores": 1, "kind": "port",
-                                    "sample": f"matmul_chain({n}) ({n_cpu} e-nodes, {t_cpu:.2f} s on 1 core, "
-                                              f"oracle/tsat_oracle.py) scaled x{scale:.1f} by e-node count"}
+            scale = _scale_10m(w)
+            line["cpu_baseline"] = {"value": t_cpu * scale, "unit": "s", "cores": 1, "kind": kind,
+                                    "sample": f"matmul_chain({w['sample_n']}) ({n_cpu} e-nodes, {t_cpu:.2f} s on "
+                                              f"1 core, {src}) scaled x{scale:.1f} by e-node count"}
         else:
-            line["cpu_baseline"] = {"value": t_cpu, "unit": "s", "cores": 1, "kind": "port",
+            line["cpu_baseline"] = {"value": t_cpu, "unit": "s", "cores": 1, "kind": kind,
                                     "sample": f"one full explore+costs+greedy of the same graph on 1 core "
-                                              f"(oracle/tsat_oracle.py), {n_cpu} e-nodes, cost {total_cpu:.6f}"}
+                                              f"({src}), {n_cpu} e-nodes, cost {total_cpu:.6f}"}
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:

@@ -84,3 +84,32 @@ def test_oracle_toy_saturation_matches_reference():
     assert eg.dump() == want["dump"]
     assert sorted(filt) == want["filt"]
     assert {k: v for k, v in rep.to_stats().items() if "time" not in k} == want["stats"]
+
+
+MODELS = json.load(open(os.path.join(HERE, "model_golden.json")))
+
+
+@pytest.mark.parametrize("case", [c for c in MODELS if c["model"] != "bert"], ids=lambda c: c["id"])
+def test_oracle_model_graph_matches_reference(case):
+    """The port against the reference's per-iteration hashes on the authored
+    model graphs (tests/golden/make_model_golden.py); BERT (~20 s in the port)
+    is left to the GPU suite, which checks the device against the same hashes."""
+    import make_model_golden as MG
+    from paper_2101_01332_b200 import models
+    from paper_2101_01332_b200.tensor_lang import emit_graph, make_single_rooted, parse_graph
+
+    g = make_single_rooted(parse_graph(emit_graph(models.MODELS[case["model"]]())))
+    snaps = []
+
+    def on_it(eg, filt, rep):
+        snaps.append((MG.sha(eg.dump()), MG.sha(MG.filt_text(filt)), eg.num_nodes))
+
+    eg, filt, rep = O.oracle_explore(g, list(default_rules()), n_max=case["n_max"], k_max=case["k_max"],
+                                     k_multi=case["k_multi"], on_iteration=on_it)
+    assert snaps == [(s["dump_sha"], s["filt_sha"], s["nodes"]) for s in case["iterations"]]
+    assert {k: v for k, v in rep.to_stats().items() if "time" not in k} == case["stats"]
+    costs = O.oracle_costs(eg, CostModel())
+    assert MG.sha(MG.costs_text(costs)) == case["costs_sha"]
+    sel, total, _ = O.oracle_greedy(eg, costs, filt)
+    assert MG.sha(MG.selection_text(sel)) == case["selection_sha"]
+    assert total == pytest.approx(case["total"], rel=1e-12)
