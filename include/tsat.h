@@ -129,6 +129,16 @@ int tsat_ilp_download(tsat_engine* h, uint32_t* classes, uint32_t* nodes, uint32
                       uint32_t* pick_off, uint32_t* pick_child);
 
 int tsat_set_record_rejects(tsat_engine* h, int32_t on);
+
+/* Memory budget (bytes) of the efficient pre-filter's descendants bitset
+ * (cycles.get_descendants, cycles.py:70-148; the reference's big-int closure).
+ * Snapshots whose C x C bitset exceeds it answer will_create_cycle's reaches()
+ * (cycles.py:52-57, 151-169) from the peel levels plus a pruned search instead
+ * (same answers, O(C + E) memory).  0 forces that mode.  Default 16 GiB, or the
+ * TSAT_REACH_BUDGET environment variable; reset when the engine is reused. */
+int tsat_set_reach_budget(tsat_engine* h, uint64_t bytes);
+/* mode of the last efficient iteration's pre-filter: 0 bitset, 1 levels + search */
+int tsat_reach_mode(tsat_engine* h, int32_t* mode);
 int tsat_rejects(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n);
 
 /* EGraph.ematch of a loaded canonical pattern (egraph.py:248-262) */
@@ -176,7 +186,8 @@ int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launch
 
 /* diagnostics: level count, peeled classes, classes, class edges, snapshot /
  * filter versions, allocated and live e-nodes, device blocks allocated by the
- * block cache (count, bytes), engines constructed */
+ * block cache (count, bytes), engines constructed, host stream waits and kernels
+ * launched by this engine */
 int tsat_debug_info(tsat_engine* h, int64_t* out, int32_t n);
 
 /* per-phase device timings of the last saturate / greedy (ms) */

@@ -67,6 +67,8 @@ _SIGS = {
     "tsat_ilp_build": ([C.c_void_p, u32p], C.c_int),
     "tsat_ilp_download": ([C.c_void_p, u32p, u32p, u32p, u32p, u32p, u32p], C.c_int),
     "tsat_set_record_rejects": ([C.c_void_p, C.c_int32], C.c_int),
+    "tsat_set_reach_budget": ([C.c_void_p, C.c_uint64], C.c_int),
+    "tsat_reach_mode": ([C.c_void_p, C.POINTER(C.c_int32)], C.c_int),
     "tsat_rejects": ([C.c_void_p, u32p, C.c_int64, i64p], C.c_int),
     "tsat_ematch": ([C.c_void_p, C.c_int32, u32p, u32p, C.c_int64, i64p, i32p], C.c_int),
     "tsat_ematch_batch": ([C.c_void_p, C.c_int32, i32p, i64p], C.c_int),

@@ -232,6 +232,13 @@ int tsat_ilp_download(tsat_engine* h, uint32_t* classes, uint32_t* nodes, uint32
 
 int tsat_set_record_rejects(tsat_engine* h, int32_t on) { GUARD(h, h->e->record_rejects = on != 0); }
 
+int tsat_set_reach_budget(tsat_engine* h, uint64_t bytes) { GUARD(h, h->e->reach.budget = bytes); }
+
+int tsat_reach_mode(tsat_engine* h, int32_t* mode) {
+  if (!mode) return TSAT_ERR_ARG;
+  GUARD(h, *mode = h->e->reach.mode);
+}
+
 int tsat_rejects(tsat_engine* h, uint32_t* out, int64_t cap, int64_t* n) {
   GUARD(h, {
     const std::vector<u32>& r = h->e->rejects;
@@ -397,6 +404,7 @@ int tsat_shard_range(uint64_t n_alloc, int32_t rank, int32_t world, uint32_t* lo
 int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launches, int32_t n, int32_t reset) {
   GUARD(h, {
     Engine& e = *h->e;
+    e.kt_resolve(true);
     for (int i = 0; i < n && i < KG_COUNT; i++) {
       ms[i] = e.kstat[i].ms;
       bytes[i] = e.kstat[i].bytes;
@@ -410,10 +418,10 @@ int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launch
 int tsat_debug_info(tsat_engine* h, int64_t* out, int32_t n) {
   GUARD(h, {
     Engine& e = *h->e;
-    int64_t v[11] = {e.lv_n, e.lv_trimmed, e.snap.ncls, e.cg_ne, (int64_t)e.snap_id, (int64_t)e.filter_id,
+    int64_t v[13] = {e.lv_n, e.lv_trimmed, e.snap.ncls, e.cg_ne, (int64_t)e.snap_id, (int64_t)e.filter_id,
                      (int64_t)e.h.next_id, (int64_t)e.h.live, (int64_t)g_dev_allocs, (int64_t)g_dev_alloc_bytes,
-                     (int64_t)g_engines};
-    for (int i = 0; i < n && i < 11; i++) out[i] = v[i];
+                     (int64_t)g_engines, (int64_t)e.nsync, (int64_t)e.nlaunch};
+    for (int i = 0; i < n && i < 13; i++) out[i] = v[i];
   });
 }
 

@@ -48,8 +48,6 @@ Engine::Engine(int dev) : device(dev) {
   CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   tl_stream = s;
   g_engines++;
-  CUDA_OK(cudaEventCreate(&ev_pool[0]));
-  CUDA_OK(cudaEventCreate(&ev_pool[1]));
   cnt.alloc(1);
   err.alloc(1);
   dstats.alloc(1);
@@ -64,25 +62,63 @@ Engine::Engine(int dev) : device(dev) {
   CUDA_OK(cudaMemsetAsync(tree_hc.p, 0xFF, tree_hc_cap * sizeof(u32), s));
   CUDA_OK(cudaMemsetAsync(tree_count.p, 0, sizeof(u32), s));
   ensure_nodes(1024, 4096);
+  reach.budget = default_reach_budget();
   sync();
+}
+
+u64 default_reach_budget() {
+  const char* v = getenv("TSAT_REACH_BUDGET");
+  return v ? strtoull(v, nullptr, 10) : (16ull << 30);
 }
 
 KTimer::KTimer(Engine& e_, int g_, double bytes_, unsigned long long launches_)
     : e(e_), g(g_), bytes(bytes_), launches(launches_) {
-  a = e.ev_pool[0];
-  b = e.ev_pool[1];
+  a = e.ev_get();
+  b = nullptr;
   CUDA_OK(cudaEventRecord(a, e.s));
 }
 
+// The closing event is recorded and queued; its elapsed time is read when the
+// stats are queried (tsat_kernel_stats) or when the queue grows, so timing a
+// group never makes the host wait for the device.
 KTimer::~KTimer() {
+  b = e.ev_get();
   cudaEventRecord(b, e.s);
-  cudaEventSynchronize(b);
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, a, b);
-  e.kstat[g].ms += ms;
+  e.kt_pending.push_back({a, b, g});
   e.kstat[g].bytes += bytes;
   e.kstat[g].launches += launches;
   e.nlaunch += launches;
+  if (e.kt_pending.size() >= 256) e.kt_resolve(false);
+}
+
+cudaEvent_t Engine::ev_get() {
+  if (ev_free.empty()) {
+    cudaEvent_t ev;
+    CUDA_OK(cudaEventCreate(&ev));
+    return ev;
+  }
+  cudaEvent_t ev = ev_free.back();
+  ev_free.pop_back();
+  return ev;
+}
+
+void Engine::kt_resolve(bool block) {
+  size_t k = 0;
+  for (; k < kt_pending.size(); k++) {
+    PendingTimer& t = kt_pending[k];
+    if (block) {
+      CUDA_OK(cudaEventSynchronize(t.b));
+    } else if (cudaEventQuery(t.b) != cudaSuccess) {
+      cudaGetLastError();  // cudaErrorNotReady is not an error
+      break;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    kstat[t.g].ms += ms;
+    ev_free.push_back(t.a);
+    ev_free.push_back(t.b);
+  }
+  kt_pending.erase(kt_pending.begin(), kt_pending.begin() + k);
 }
 
 void free_wave_bufs(WaveBufs* b);
@@ -108,8 +144,11 @@ void Engine::reset(bool analysis_) {
   for (auto& m : matches) m.n = 0;  // keep the device buffers for the next graph
   snap.valid = false;
   reach.valid = false;
+  reach.mode = 0;
+  reach.budget = default_reach_budget();
   lv_snap = lv_filter = ~0ull;
   costs_valid_for = TSAT_NONE;
+  kt_resolve(true);
   for (int i = 0; i < KG_COUNT; i++) kstat[i] = KStat();
   nlaunch = 0;
   last_error.clear();
@@ -122,6 +161,11 @@ Engine::~Engine() {
   } catch (...) {
   }
   if (s) cudaStreamSynchronize(s);
+  for (auto& t : kt_pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto ev : ev_free) cudaEventDestroy(ev);
   // everything this engine released is idle now; members released below too
   tl_stream = nullptr;
   if (wave) free_wave_bufs(wave);
@@ -234,7 +278,10 @@ void dev_cache_forget_stream(cudaStream_t s) {
       if (blk.s == s) blk.s = nullptr;
 }
 
-void Engine::sync() { CUDA_OK(cudaStreamSynchronize(s)); }
+void Engine::sync() {
+  nsync++;
+  CUDA_OK(cudaStreamSynchronize(s));
+}
 
 void Engine::pull_counters() {
   CUDA_OK(cudaMemcpyAsync(&h, cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, s));

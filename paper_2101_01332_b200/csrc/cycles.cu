@@ -397,7 +397,23 @@ void Engine::build_reach() {
   u32 n = cg_n;
   u32 words = (n + 31) / 32;
   u64 bytes = (u64)n * words * 4;
-  if (bytes > (u64)48 << 30) throw TsatException(TSAT_ERR_UNSUPPORTED, "descendants bitset would exceed 48 GiB");
+  if (bytes > reach.budget) {
+    // mode 1: the peel levels ensure_levels just computed + the class graph
+    // answer the queries (rulesdev.cuh reach_query); nothing O(C^2) is built
+    reach.visit.ensure((u64)n + 1);
+    reach.stack.ensure((u64)n + cg_ne + 1);
+    reach.epoch.ensure(1);
+    CUDA_OK(cudaMemsetAsync(reach.visit.p, 0, ((u64)n + 1) * sizeof(u32), s));
+    CUDA_OK(cudaMemsetAsync(reach.epoch.p, 0, sizeof(u32), s));
+    reach.n = n;
+    reach.words = 0;
+    reach.mode = 1;
+    reach.valid = true;
+    kt.bytes = 8.0 * n;
+    kt.launches = 0;
+    return;
+  }
+  reach.mode = 0;
   reach.bits.ensure((u64)n * words + 1);
   u32 nl = lv_n, ntr = lv_trimmed;
   if (getenv("TSAT_SEL_DEBUG")) {

@@ -162,10 +162,15 @@ struct Snapshot {
   bool valid = false;
 };
 
-struct Reach {  // descendants bitset over a snapshot
+u64 default_reach_budget();
+
+struct Reach {  // efficient pre-filter over a snapshot (rulesdev.cuh ReachDev)
   u32 n = 0, words = 0;
+  int mode = 0;            // 0 descendants bitset, 1 peel levels + pruned search
   DevBuf<u32> bits;
+  DevBuf<u32> visit, stack, epoch;
   bool valid = false;
+  u64 budget = 16ull << 30;  // bitset bytes allowed before mode 1 (tsat_set_reach_budget)
 };
 
 struct ExploreLimitsC {
@@ -216,7 +221,8 @@ struct Scratch {
   DevBuf<unsigned char> c_stack;
   // greedy / costs
   DevBuf<double> g_c0, g_c1, g_upl, k_dv, g_rinfo;
-  DevBuf<u32> g_n0, g_n1, g_flag, g_mark, g_fa, g_fb, g_oc, g_on, k_slots, g_eoff, g_edst, g_cnt;
+  DevBuf<u32> g_n0, g_n1, g_flag, g_mark, g_fa, g_fb, g_oc, g_on, k_slots, g_eoff, g_edst, g_cnt, k_miss;
+  DevBuf<char> k_keyout;
   DevBuf<char> k_keys;
   DevBuf<u32> gq_batch;
   DevBuf<u32> gq_lvm, gq_cnt, gq_k, gq_node, gq_deg, gq_eoff, gq_edst, gq_lb, gq_head, gq_slot, gq_big;
@@ -304,8 +310,17 @@ struct Engine {
   ExploreReportC report{};
   std::vector<double> phase_ms = std::vector<double>(32, 0.0);
   unsigned long long nlaunch = 0;  // kernels of ours launched (not CUB)
+  unsigned long long nsync = 0;    // host waits on the stream (Engine::sync)
   KStat kstat[KG_COUNT];
-  cudaEvent_t ev_pool[2] = {nullptr, nullptr};
+  // kernel-group timers: event pairs resolved lazily (no host sync per group)
+  struct PendingTimer {
+    cudaEvent_t a, b;
+    int g;
+  };
+  std::vector<cudaEvent_t> ev_free;
+  std::vector<PendingTimer> kt_pending;
+  cudaEvent_t ev_get();
+  void kt_resolve(bool block);
 
   Engine(int dev);
   ~Engine();

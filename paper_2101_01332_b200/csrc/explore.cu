@@ -158,6 +158,17 @@ ReachDev make_reach_dev(Engine& e) {
   r.cls_index = e.snap.cls_index.p;
   r.n_alloc = e.snap.n_alloc;
   r.valid = e.reach.valid ? 1 : 0;
+  r.mode = e.reach.mode;
+  r.level = e.sc.cg_level.p;
+  r.eoff = e.sc.cg_eoff.p;
+  r.edst = e.sc.cg_edst.p;
+  r.visit = e.reach.visit.p;
+  r.stack = e.reach.stack.p;
+  r.epoch = e.reach.epoch.p;
+  // TSAT_REACH_STEPS (tests): budget of the private searches; 0 sends every
+  // query the level filter cannot decide to the exact path
+  static const char* st = getenv("TSAT_REACH_STEPS");
+  r.steps = st ? atoi(st) : 96;
   return r;
 }
 
@@ -237,7 +248,7 @@ __global__ void k_seq_rule(G g, RuleDev R, ReachDev RD, DevStats* st, unsigned l
         u32 out = uf_find(g.parent, R.mcls[t][idx[t]]);
         for (int l = 0; l < R.leaf_len[t]; l++) {
           u32 leaf = uf_find(g.parent, env[R.leaf[R.leaf_off[t] + l]]);
-          if (leaf == out || reach_query(RD, leaf, out)) {
+          if (leaf == out || reach_query(RD, leaf, out, true) == REACH_YES) {
             hit = true;
             break;
           }

@@ -43,6 +43,9 @@ struct CostTab {
   int strict;
   const char* names;
   const u32* name_off;
+  u32* miss;       // strict: smallest node id whose signature has no entry (iter_nodes order, egraph.py:155-157)
+  u32 dump_node;   // != TSAT_NONE: render that node's key into key_out only
+  char* key_out;
 };
 
 __device__ __forceinline__ u64 fnv1a(const char* p, int n) {
@@ -148,7 +151,7 @@ __device__ __forceinline__ double base_cost(int op) {
 __global__ void k_node_costs(G g, CostTab ct, u32 n, double* out) {
   const double RATE_MOVE = 0.05 * 1e-7;
   GRID_STRIDE(i0, n) {
-    u32 i = (u32)i0;
+    u32 i = ct.dump_node != TSAT_NONE ? ct.dump_node : (u32)i0;
     if (!(g.flags[i] & NF_ALIVE)) {
       out[i] = 0.0;
       continue;
@@ -244,9 +247,14 @@ __global__ void k_node_costs(G g, CostTab ct, u32 n, double* out) {
           slot = (slot + 1) & ct.mask;
         }
       }
+      if (ct.dump_node != TSAT_NONE) {
+        for (int q = 0; q < s.n; q++) ct.key_out[q] = s.b[q];
+        ct.key_out[s.n] = 0;
+        continue;
+      }
       if (hit) continue;
       if (ct.strict) {
-        dev_set_error(g.err, TSAT_ERR_UNKNOWN_SIG, 21, i, g.op[i]);
+        atomicMin(ct.miss, i);
         out[i] = 0.0;
         continue;
       }
@@ -397,14 +405,36 @@ void Engine::costs(int mode, int strict, int ntab, const char* keys, const i64* 
     ct.mask = cap - 1;
   }
   d_costs.ensure(n + 1);
+  ct.dump_node = TSAT_NONE;
+  DevBuf<u32>& dmiss = sc.k_miss;
+  if (strict) {
+    dmiss.ensure(1);
+    CUDA_OK(cudaMemsetAsync(dmiss.p, 0xFF, sizeof(u32), s));
+    ct.miss = dmiss.p;
+  }
   {
     // node: op 4 + koff 8 + flag 1 + cost 8; child: id 4 + parent 4 + analysis fields 48
     KTimer kt(*this, KG_COSTS, 21.0 * h.live + 56.0 * h.nkids, 1);
     k_node_costs<<<nblk(n, 128), 128, 0, s>>>(view(), ct, n, d_costs.p);
   }
   if (out) CUDA_OK(cudaMemcpyAsync(out, d_costs.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  u32 miss = TSAT_NONE;
+  if (strict) CUDA_OK(cudaMemcpyAsync(&miss, dmiss.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
   sync();
   check_error();
+  if (miss != TSAT_NONE) {  // UnknownSignature for the first node in id order, with its rendered key (cost.py:170-172)
+    DevBuf<char>& kb = sc.k_keyout;
+    kb.ensure(512);
+    ct.dump_node = miss;
+    ct.key_out = kb.p;
+    k_node_costs<<<1, 1, 0, s>>>(view(), ct, 1, d_costs.p);
+    char key[512];
+    CUDA_OK(cudaMemcpyAsync(key, kb.p, sizeof(key), cudaMemcpyDeviceToHost, s));
+    sync();
+    key[511] = 0;
+    costs_valid_for = 0;
+    throw TsatException(TSAT_ERR_UNKNOWN_SIG, std::string("no cost for ") + key);
+  }
   costs_valid_for = n;
 }
 

@@ -207,16 +207,19 @@ __device__ __forceinline__ void d_gates(u64 tid, u64 nth, const G& g, const Rule
       }
     }
     if (st == 0 && !hz && R.efficient) {
-      bool hit = false;
-      for (int t = 0; t < R.nsrc && !hit; t++)
+      int hit = REACH_NO;
+      for (int t = 0; t < R.nsrc && hit != REACH_YES; t++)
         for (int l = 0; l < R.leaf_len[t]; l++) {
           u32 leaf = env[R.leaf[R.leaf_off[t] + l]];
-          if (leaf == olds[t] || reach_query(RD, leaf, olds[t])) {
-            hit = true;
+          int q = leaf == olds[t] ? REACH_YES : reach_query(RD, leaf, olds[t]);
+          if (q == REACH_YES) {
+            hit = REACH_YES;
             break;
           }
+          if (q == REACH_UNKNOWN) hit = REACH_UNKNOWN;  // a later leaf may still say yes
         }
-      if (hit) st = 2;
+      if (hit == REACH_YES) st = 2;
+      else if (hit == REACH_UNKNOWN) hz = 1;  // undecided within the budget: exact path
     }
     status[c] = st;
     hazard[c] = hz;
@@ -544,13 +547,17 @@ __device__ __forceinline__ u32 soft_find(u32 id, u32 c, u32 ep, const WaveRule& 
   return TSAT_NONE;
 }
 
-__device__ __forceinline__ bool cycle_hit(const RuleDev& R, const ReachDev& RD, const u32* env, const u32* outs) {
+// REACH_YES / REACH_NO, or REACH_UNKNOWN when a bounded search gave up
+__device__ __forceinline__ int cycle_hit(const RuleDev& R, const ReachDev& RD, const u32* env, const u32* outs) {
+  int res = REACH_NO;
   for (int t = 0; t < R.nsrc; t++)
     for (int l = 0; l < R.leaf_len[t]; l++) {
       u32 leaf = env[R.leaf[R.leaf_off[t] + l]];
-      if (leaf == outs[t] || reach_query(RD, leaf, outs[t])) return true;
+      int q = leaf == outs[t] ? REACH_YES : reach_query(RD, leaf, outs[t]);
+      if (q == REACH_YES) return REACH_YES;
+      if (q == REACH_UNKNOWN) res = REACH_UNKNOWN;
     }
-  return false;
+  return res;
 }
 
 // candidate validity against earlier writes in the wave (all candidates:
@@ -608,7 +615,10 @@ __device__ __forceinline__ void d_validity(u64 tid, u64 nth, const WaveRule& W, 
         outs[t] = soft_find(olds[(u64)c * MAX_SRC + t], c, ep, W, fw_cls, accpre, olds, ukind, uother, &gr);
         bad = outs[t] == TSAT_NONE;
       }
-      if (!bad) bad = cycle_hit(R, RD, env + (u64)c * MAX_VARS, outs) != (st == 2);
+      if (!bad) {
+        int ch = cycle_hit(R, RD, env + (u64)c * MAX_VARS, outs);
+        bad = ch == REACH_UNKNOWN || (ch == REACH_YES) != (st == 2);
+      }
       WDBG_CAT(5);
     }
     if (!bad && st == 0) {
@@ -681,7 +691,7 @@ __device__ bool d_resolve_soft(const G& g, const WaveRule& W, const WaveTab& T, 
     uother[ia] = x;
     grow[ia] = ng;
   }
-  if (R.efficient && cycle_hit(R, RD, env + (u64)c * MAX_VARS, outs)) return false;
+  if (R.efficient && cycle_hit(R, RD, env + (u64)c * MAX_VARS, outs) != REACH_NO) return false;
   return true;
 }
 

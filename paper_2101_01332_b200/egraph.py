@@ -187,6 +187,23 @@ class EGraph:
         self._view: Optional[_View] = None
         self._filt_dev: Optional[frozenset] = frozenset()  # filter list known to be on the device
 
+    @property
+    def reach_budget(self) -> None:
+        raise AttributeError("write-only")
+
+    @reach_budget.setter
+    def reach_budget(self, nbytes: int) -> None:
+        """Bytes the efficient pre-filter may spend on the C x C descendants
+        bitset (reference cycles.py:70-148) before it answers reaches() from
+        the peel levels + a pruned search; 0 forces the latter."""
+        _lib.check(self._h, _lib.load().tsat_set_reach_budget(self._h, int(nbytes)))
+
+    @property
+    def reach_mode(self) -> int:
+        out = C.c_int32()
+        _lib.check(self._h, _lib.load().tsat_reach_mode(self._h, C.byref(out)))
+        return out.value
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and _lib._lib is not None:

@@ -31,13 +31,13 @@ for i in range(int(__import__("os").environ.get("REPS", "4"))):
     t1 = time.perf_counter()
     ph = np.zeros(32)
     lib.tsat_phase_times(eg._h, ph.ctypes.data_as(C.POINTER(C.c_double)), 32)
-    dbg = np.zeros(11, np.int64)
-    lib.tsat_debug_info(eg._h, dbg.ctypes.data_as(C.POINTER(C.c_int64)), 11)
+    dbg = np.zeros(13, np.int64)
+    lib.tsat_debug_info(eg._h, dbg.ctypes.data_as(C.POINTER(C.c_int64)), 13)
     costs = egraph_costs(eg, CostModel()); t2 = time.perf_counter()
     res = greedy_extract(eg, costs, filt); t3 = time.perf_counter()
     f(0)
     print(f"[{i}] saturate {1e3*(t1-t0):.1f} costs {1e3*(t2-t1):.1f} greedy {1e3*(t3-t2):.1f} total {1e3*(t3-t0):.1f} ms nodes {rep.enodes_per_iter} iters {rep.iterations}")
-    print("   levels %d peeled %d classes %d class-edges %d alloc %d live %d | cudaMallocs so far %d (%.1f MB) engines %d" % (dbg[0], dbg[1], dbg[2], dbg[3], dbg[6], dbg[7], dbg[8], dbg[9] / 1e6, dbg[10]))
+    print("   levels %d peeled %d classes %d class-edges %d alloc %d live %d | cudaMallocs so far %d (%.1f MB) engines %d | host syncs %d launches %d" % (dbg[0], dbg[1], dbg[2], dbg[3], dbg[6], dbg[7], dbg[8], dbg[9] / 1e6, dbg[10], dbg[11], dbg[12]))
     print("   phases(ms) snap %.2f reach %.2f ematch %.2f apply %.2f rebuild %.2f cycles %.2f | waves %d hazards %d why %s resolved %d+%d" % (
         ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[8], ph[9], ph[10:16].astype(int).tolist(), ph[28], ph[29]))
     names = ["gates", "accept", "resolve", "candchk", "conflicts", "stops", "boundary", "commit", "unions", "insert", "bookkeep", "top"]
