@@ -13,8 +13,10 @@ Arms:
     greedy_extract), host<->device copies inside the timed region.
   * --impl reference: the CPU port of the reference (oracle/, the reference
     itself is pure Python and cannot travel to the GPU box) on all host cores.
-N>1: one process per GPU, each explores its own graph (weak scaling, no
-collective on the data path); value = step time / graphs per step.
+N>1: one process per GPU; by default the ranks search ONE graph together
+(e-matching sharded by e-class range, match lists and greedy wide-level
+records all-gathered over NCCL; strong scaling); --replicas runs one
+independent graph per GPU instead (weak scaling, no collective).
 """
 
 from __future__ import annotations
@@ -224,9 +226,9 @@ def main():
     ap.add_argument("--workload", default="bert", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] 10M-node kernel sweep")
-    ap.add_argument("--shard", action="store_true",
-                    help="N>1: the ranks explore ONE graph together, e-matching split by e-class range "
-                         "with an NCCL all-gather of the match lists (SURVEY 8(e)); default: one graph per GPU")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: one independent graph per GPU (weak scaling, no collective) instead of the "
+                         "default sharded search")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
@@ -240,7 +242,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    shard_mode = args.shard and world > 1
+    # N>1 default: the ranks explore ONE graph together -- e-matching split by
+    # e-class range with an NCCL all-gather of the match lists, greedy's wide
+    # levels split with an all-gather of {cost, node}
+    shard_mode = world > 1 and not args.replicas
     if world > 1:
         import torch.distributed as dist
 

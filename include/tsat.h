@@ -134,8 +134,10 @@ int tsat_set_record_rejects(tsat_engine* h, int32_t on);
  * (cycles.get_descendants, cycles.py:70-148; the reference's big-int closure).
  * Snapshots whose C x C bitset exceeds it answer will_create_cycle's reaches()
  * (cycles.py:52-57, 151-169) from the peel levels plus a pruned search instead
- * (same answers, O(C + E) memory).  0 forces that mode.  Default 16 GiB, or the
- * TSAT_REACH_BUDGET environment variable; reset when the engine is reused. */
+ * (same answers, O(C + E) memory, no O(C^2/32) closure pass: a match's leaves lie
+ * below its class, so the level test alone decides all but multi-pattern cross
+ * queries).  Default 0 (levels always), or the TSAT_REACH_BUDGET environment
+ * variable; reset when the engine is reused. */
 int tsat_set_reach_budget(tsat_engine* h, uint64_t bytes);
 /* mode of the last efficient iteration's pre-filter: 0 bitset, 1 levels + search */
 int tsat_reach_mode(tsat_engine* h, int32_t* mode);
@@ -176,6 +178,12 @@ int tsat_greedy(tsat_engine* h, const double* cost_by_node, uint32_t* sel_cls, u
  * world == 1 disables sharding; nccl_id == NULL with world > 1 computes this
  * rank's part only, without the exchange (diagnostics / single-GPU tests). */
 int tsat_shard_setup(tsat_engine* h, int32_t rank, int32_t world, const void* nccl_id, int32_t id_bytes);
+/* Same shard group over a caller-supplied transport instead of NCCL: fn must
+ * all-gather ``bytes`` from every rank's ``send`` into ``recv`` (world * bytes,
+ * rank order; host memory) and return 0.  Used to run the exchange over
+ * torch.distributed / gloo (tests with several ranks on one GPU). */
+typedef int32_t (*tsat_allgather_fn)(void* ctx, const void* send, void* recv, uint64_t bytes);
+int tsat_shard_setup_host(tsat_engine* h, int32_t rank, int32_t world, tsat_allgather_fn fn, void* ctx);
 int tsat_nccl_unique_id(void* out, int32_t cap, int32_t* len);
 int tsat_shard_range(uint64_t n_alloc, int32_t rank, int32_t world, uint32_t* lo, uint32_t* hi);
 

@@ -36,6 +36,9 @@ class Report(C.Structure):
                 ("filter_size", C.c_int64), ("time_s", C.c_double)]
 
 
+# tsat_allgather_fn: (ctx, send, recv, bytes) -> 0 on success
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+
 _SIGS = {
     "tsat_create": ([C.c_int, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "tsat_destroy": ([C.c_void_p], None),
@@ -81,6 +84,7 @@ _SIGS = {
     "tsat_debug_info": ([C.c_void_p, i64p, C.c_int32], C.c_int),
     "tsat_kernel_stats": ([C.c_void_p, f64p, f64p, i64p, C.c_int32, C.c_int32], C.c_int),
     "tsat_shard_setup": ([C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_int32], C.c_int),
+    "tsat_shard_setup_host": ([C.c_void_p, C.c_int32, C.c_int32, ALLGATHER_FN, C.c_void_p], C.c_int),
     "tsat_nccl_unique_id": ([C.c_char_p, C.c_int32, i32p], C.c_int),
     "tsat_shard_range": ([C.c_uint64, C.c_int32, C.c_int32, u32p, u32p], C.c_int),
 }

@@ -384,6 +384,15 @@ int tsat_shard_setup(tsat_engine* h, int32_t rank, int32_t world, const void* nc
   });
 }
 
+int tsat_shard_setup_host(tsat_engine* h, int32_t rank, int32_t world, tsat_allgather_fn fn, void* ctx) {
+  GUARD(h, {
+    if (world > 1 && !fn) throw TsatException(TSAT_ERR_ARG, "need an all-gather function");
+    h->e->shard_setup(rank, world, nullptr);
+    h->e->host_ag = world > 1 ? fn : nullptr;
+    h->e->host_ctx = ctx;
+  });
+}
+
 int tsat_nccl_unique_id(void* out, int32_t cap, int32_t* len) {
   if (!out || !len || cap < 128) return TSAT_ERR_ARG;
   try {

@@ -68,7 +68,7 @@ Engine::Engine(int dev) : device(dev) {
 
 u64 default_reach_budget() {
   const char* v = getenv("TSAT_REACH_BUDGET");
-  return v ? strtoull(v, nullptr, 10) : (16ull << 30);
+  return v ? strtoull(v, nullptr, 10) : 0ull;
 }
 
 KTimer::KTimer(Engine& e_, int g_, double bytes_, unsigned long long launches_)

@@ -333,6 +333,13 @@ __global__ void k_untrimmed(const u32* level, u32 n, const u8* mask, u32* list, 
 
 // ---------------------------------------------------------------- host helpers
 
+__global__ void k_level_keys(const u32* level, u32 n, u32* key, u32* val) {
+  GRID_STRIDE(i, n) {
+    key[i] = level[i];
+    val[i] = (u32)i;
+  }
+}
+
 void build_class_graph(Engine& e) {
   Snapshot& S = e.snap;
   Scratch& X = e.sc;
@@ -380,6 +387,19 @@ void Engine::ensure_levels() {
     t1 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
   }
   lv_n = trim_levels(*this, nullptr, lv_off, lv_trimmed);
+  if (shard_world > 1 && cg_n) {
+    // shard ranks split wide peel levels by position (greedy), so every rank
+    // needs the same order inside a level: (level, class) ascending instead
+    // of the peel's arrival order.  Stable radix sort of the class ids by
+    // level; unpeeled classes (TSAT_NONE) sort last, outside the levels.
+    Scratch& X = sc;
+    u32 n = cg_n;
+    X.c_skey.ensure(n + 1);
+    X.c_sval.ensure(n + 1);
+    X.c_skey2.ensure(n + 1);
+    k_level_keys<<<nblk(n), 256, 0, s>>>(X.cg_level.p, n, X.c_skey.p, X.c_sval.p);
+    dev_sort_pairs_u32(*this, X.c_skey.p, X.c_skey2.p, X.c_sval.p, X.c_order.p, n, 32);
+  }
   if (dbg) {
     sync();
     double t2 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();

@@ -170,7 +170,7 @@ struct Reach {  // efficient pre-filter over a snapshot (rulesdev.cuh ReachDev)
   DevBuf<u32> bits;
   DevBuf<u32> visit, stack, epoch;
   bool valid = false;
-  u64 budget = 16ull << 30;  // bitset bytes allowed before mode 1 (tsat_set_reach_budget)
+  u64 budget = 0;  // bitset bytes allowed before mode 1 (tsat_set_reach_budget); default: always mode 1
 };
 
 struct ExploreLimitsC {
@@ -208,6 +208,7 @@ struct KTimer {  // records CUDA events on the engine stream around a kernel gro
 struct Scratch {
   // e-matching
   DevBuf<u32> m_heavy;
+  DevBuf<u32> c_skey, c_sval, c_skey2;  // deterministic level order (sharded runs)
   DevBuf<u32> m_rc, m_rb, m_cnt, m_perm, m_perm2, m_key, m_key2, m_fl, m_pos;
   DevBuf<u32> m_bnd, m_big, m_head, m_bpos, m_L, m_bh, m_gex, m_bperm, m_bperm2, m_bkey, m_bkey2;
   // sharding (shard.cu)
@@ -364,6 +365,13 @@ struct Engine {
   // multi-GPU e-matching shards (shard.cu)
   int shard_rank = 0, shard_world = 1;
   void* comm = nullptr;  // ncclComm_t
+  // host transport (tsat_shard_setup_host): all-gather of host buffers by the
+  // caller (e.g. torch.distributed / gloo); used when no NCCL communicator
+  int32_t (*host_ag)(void*, const void*, void*, uint64_t) = nullptr;
+  void* host_ctx = nullptr;
+  std::vector<unsigned char> ag_send, ag_recv;
+  bool shard_exchange() const { return comm != nullptr || host_ag != nullptr; }
+  void shard_allgather(const void* dsend, void* drecv, size_t bytes);  // device buffers, rank order
   void shard_setup(int rank, int world, const void* nccl_id);
   void shard_teardown();
   void shard_candidate_ranges(std::vector<u32>& rng);

@@ -1167,7 +1167,7 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
         X.gq_pack.ensure(2ull * chunk + 2);
         X.gq_recv.ensure(2ull * chunk * W + 2);
         for (u32 r = 0; r < W; r++) {
-          if (comm && (int)r != shard_rank) continue;
+          if (shard_exchange() && (int)r != shard_rank) continue;
           u32 ta = std::min(b, a + r * chunk), tb = std::min(b, ta + chunk);
           if (tb > ta) {
             k_gq_totals_slots<<<nblk(wm), 256, 0, s>>>(lvm[l], lvm[l + 1], ta, tb, X.gq_slot.p, X.gq_cost.p,
@@ -1175,10 +1175,10 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
             k_gq_fold_wide<<<nblk(bigf[l] ? (u64)(tb - ta) * 32 : tb - ta), 256, 0, s>>>(
                 ta, tb, ord, X.gq_lvm.p, X.gq_node.p, X.gq_tot.p, c0.p, n0.p, bigf[l]);
           }
-          double* dst = comm ? X.gq_pack.p : X.gq_recv.p + 2ull * chunk * r;
+          double* dst = shard_exchange() ? X.gq_pack.p : X.gq_recv.p + 2ull * chunk * r;
           if (tb > ta) k_gq_pack<<<nblk(tb - ta), 256, 0, s>>>(ta, tb, ord, c0.p, n0.p, dst);
         }
-        if (comm) shard_allgather_bytes(X.gq_pack.p, X.gq_recv.p, 2ull * chunk * sizeof(double));
+        if (shard_exchange()) shard_allgather_bytes(X.gq_pack.p, X.gq_recv.p, 2ull * chunk * sizeof(double));
         k_gq_unpack<<<nblk(wc), 256, 0, s>>>(a, b, ord, X.gq_recv.p, c0.p, n0.p);
         l++;
         continue;

@@ -495,6 +495,193 @@ static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& tot
   total = h[0];
 }
 
+// Barrier-free Kahn peel for class graphs that fit one CTA's shared memory
+// (out-degree counters, levels, the work queue and the reverse CSR offsets).
+// A level-synchronous peel pays a CTA barrier plus dependent L2 round trips
+// per level, and these graphs are hundreds of levels deep and a few classes
+// wide; here a class is processed as soon as its last child is: every class
+// raises its parents' level (atomicMax of level + 1) and decrements their
+// counters, and the thread that brings a counter to zero queues the parent.
+// Warps take queue tickets; a class with more than 32 parent edges is swept
+// by its whole warp.  ``pending`` (queued, not yet finished) reaching zero
+// ends the walk.  The queue is then counting-sorted by level into the peel
+// order + level offsets the level-synchronous consumers read.
+#define PA_WIDE 32u
+__global__ void __launch_bounds__(1024) k_peel_async(const u32* eoff, const u32* groff, const u32* grsrc, const u8* mask,
+                                                     u32 n, u32 ne, u32* level_out, u32* order_out,
+                                                     u32* lvl_off_out, u32* outdeg_out, u32* ctl) {
+  extern __shared__ u32 sm[];
+  u32* deg = sm;
+  u32* lev = sm + n;
+  u32* q = sm + 2 * (u64)n;
+  u32* roff = sm + 3 * (u64)n;
+  u32* rsrc = roff + n + 1;
+  __shared__ u32 s_head, s_tail, s_pending, s_nl;
+  const u32 FULL = 0xffffffffu, MASKED = 0x7fffffffu;
+  unsigned long long t_a, t_b, t_c;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_a));
+  if (threadIdx.x == 0) {
+    s_head = 0;
+    s_tail = 0;
+    s_nl = 0;
+  }
+  for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+    lev[i] = 0;
+    q[i] = TSAT_NONE;
+    roff[i] = groff[i];
+  }
+  if (threadIdx.x == 0) roff[n] = groff[n];
+  for (u32 e = threadIdx.x; e < ne; e += blockDim.x) rsrc[e] = grsrc[e];
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+    if (mask && !mask[i]) {
+      deg[i] = MASKED;
+      continue;
+    }
+    u32 d = eoff[i + 1] - eoff[i];
+    deg[i] = d;
+    if (d == 0) q[atomicAdd(&s_tail, 1u)] = i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s_pending = s_tail;
+  __syncthreads();
+  const u32 lane = threadIdx.x & 31;
+  auto raise = [&](u32 e, u32 lv) {
+    u32 p = rsrc[e];
+    if (!mask || mask[p]) atomicMax(&lev[p], lv + 1);
+  };
+  // a ready parent becomes the finder's next class when it has none (no
+  // queue round trip on a chain), else it is queued
+  auto push = [&](u32 p) {
+    atomicAdd(&s_pending, 1u);
+    u32 pos = atomicAdd(&s_tail, 1u);
+    __threadfence_block();
+    ((volatile u32*)q)[pos] = p;
+  };
+  u32 h = TSAT_NONE, cur = TSAT_NONE;
+  bool done = false;
+  while (true) {
+    if (cur == TSAT_NONE && !done) {
+      if (h == TSAT_NONE) {
+        h = atomicAdd(&s_head, 1u);
+        if (h >= n) done = true;
+      }
+      if (!done) {
+        u32 x = ((volatile u32*)q)[h];
+        if (x != TSAT_NONE) {
+          cur = x;
+          h = TSAT_NONE;
+          __threadfence_block();
+        } else if (((volatile u32*)&s_pending)[0] == 0) {
+          done = true;
+        }
+      }
+    }
+    if (__all_sync(FULL, done)) break;
+    const u32 v = cur;
+    u32 a = 0, b = 0, lv = 0;
+    if (v != TSAT_NONE) {
+      a = roff[v];
+      b = roff[v + 1];
+      lv = ((volatile u32*)lev)[v];
+    }
+    unsigned wide = __ballot_sync(FULL, v != TSAT_NONE && b - a > PA_WIDE);
+    while (wide) {
+      int src = __ffs(wide) - 1;
+      wide &= wide - 1;
+      u32 wa = __shfl_sync(FULL, a, src), wb = __shfl_sync(FULL, b, src), wl = __shfl_sync(FULL, lv, src);
+      for (u32 e0 = wa; e0 < wb; e0 += 32)
+        if (e0 + lane < wb) raise(e0 + lane, wl);
+      __threadfence_block();
+      __syncwarp();
+      for (u32 e0 = wa; e0 < wb; e0 += 32)
+        if (e0 + lane < wb) {
+          u32 p = rsrc[e0 + lane];
+          if ((!mask || mask[p]) && atomicSub(&deg[p], 1u) == 1u) push(p);
+        }
+      __syncwarp();
+    }
+    if (v != TSAT_NONE) {
+      u32 nxt = TSAT_NONE;
+      if (b - a <= PA_WIDE) {
+        for (u32 e = a; e < b; e++) raise(e, lv);
+        __threadfence_block();
+        for (u32 e = a; e < b; e++) {
+          u32 p = rsrc[e];
+          if ((!mask || mask[p]) && atomicSub(&deg[p], 1u) == 1u) {
+            if (nxt == TSAT_NONE) nxt = p;
+            else push(p);
+          }
+        }
+      }
+      if (nxt != TSAT_NONE) {
+        cur = nxt;  // one class finished, one started: pending unchanged
+        __threadfence_block();
+      } else {
+        __threadfence_block();
+        atomicSub(&s_pending, 1u);
+        cur = TSAT_NONE;
+      }
+    }
+  }
+  __syncthreads();
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_b));
+  // level histogram -> offsets -> peel order (the counters are reused)
+  // (the queue holds only the classes that were handed over; q is reused as
+  // the per-class level, TSAT_NONE = not peeled)
+  if (threadIdx.x == 0) s_tail = 0;
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+    u32 d = deg[i];
+    u32 l = d == 0 ? lev[i] : TSAT_NONE;
+    level_out[i] = l;
+    q[i] = l;
+    outdeg_out[i] = d == MASKED ? 0u : d;
+    if (l != TSAT_NONE) {
+      atomicMax(&s_nl, l + 1);
+      atomicAdd(&s_tail, 1u);
+    }
+  }
+  __syncthreads();
+  const u32 nl = s_nl, total = s_tail;
+  u32* cnt = deg;  // nl <= n
+  for (u32 i = threadIdx.x; i <= nl; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < n; i += blockDim.x)
+    if (q[i] != TSAT_NONE) atomicAdd(&cnt[q[i]], 1u);
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of nl counts by one warp
+    u32 carry = 0;
+    for (u32 base = 0; base < nl; base += 32) {
+      u32 i = base + lane;
+      u32 x = i < nl ? cnt[i] : 0u, y = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        u32 t = __shfl_up_sync(FULL, y, o);
+        if (lane >= (u32)o) y += t;
+      }
+      if (i < nl) {
+        cnt[i] = carry + y - x;
+        lvl_off_out[i] = carry + y - x;
+      }
+      carry += __shfl_sync(FULL, y, 31);
+    }
+    if (lane == 0) lvl_off_out[nl] = carry;
+  }
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < n; i += blockDim.x)
+    if (q[i] != TSAT_NONE) order_out[atomicAdd(&cnt[q[i]], 1u)] = i;
+  __syncthreads();
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_c));
+  if (threadIdx.x == 0) {
+    ctl[0] = total;
+    ctl[1] = nl;
+    ctl[2] = (u32)(t_b - t_a);  // ns: walk, then level sort (TSAT_DEBUG_LEVELS)
+    ctl[3] = (u32)(t_c - t_b);
+  }
+}
+
+#define PA_SMEM (200u << 10)
+
 u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrimmed) {
   Scratch& X = e.sc;
   u32 n = e.cg_n;
@@ -503,7 +690,33 @@ u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrim
   Frontier F{X.cg_eoff.p, X.cg_edst.p, X.cg_roff.p, X.cg_rsrc.p, mask, X.cg_outdeg.p, X.cg_level.p,
              X.c_order.p, X.c_lvloff.p, nullptr, n, 0};
   u32 nl = 0, tot = 0;
-  run_frontier(e, F, 0, nl, tot, e.cg_ne);  // class graph: reverse edges = forward edges
+  static const bool no_async = getenv("TSAT_PEEL_SYNC") != nullptr;
+  // the barrier-free walk only when the whole reverse graph sits in shared
+  // memory: with edges in L2 every class pays a dependent round trip and the
+  // level-synchronous walk (edges flattened over the CTA) is faster
+  if (!no_async && n > 0 && 16ull * n + 4ull * e.cg_ne + 16 <= PA_SMEM) {
+    static int smem_set = 0;
+    if (!smem_set) {
+      CUDA_OK(cudaFuncSetAttribute(k_peel_async, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PA_SMEM));
+      smem_set = 1;
+    }
+    size_t bytes = (size_t)(4ull * n + 1 + e.cg_ne) * 4;
+    DevBuf<u32>& ctl = X.c_res;
+    ctl.ensure(16);
+    static const int pa_threads = getenv("TSAT_PEEL_THREADS") ? atoi(getenv("TSAT_PEEL_THREADS")) : 1024;
+    k_peel_async<<<1, pa_threads, bytes, e.s>>>(X.cg_eoff.p, X.cg_roff.p, X.cg_rsrc.p, mask, n, e.cg_ne, X.cg_level.p,
+                                          X.c_order.p, X.c_lvloff.p, X.cg_outdeg.p, ctl.p);
+    CUDA_OK(cudaGetLastError());
+    u32 hc[4];
+    CUDA_OK(cudaMemcpyAsync(hc, ctl.p, 4 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+    e.sync();
+    static const bool dbg = getenv("TSAT_DEBUG_LEVELS") != nullptr;
+    if (dbg) fprintf(stderr, "peel_async: n %u ne %u walk %.1f us sort %.1f us\n", n, e.cg_ne, hc[2] * 1e-3, hc[3] * 1e-3);
+    tot = hc[0];
+    nl = hc[1];
+  } else {
+    run_frontier(e, F, 0, nl, tot, e.cg_ne);  // class graph: reverse edges = forward edges
+  }
   ntrimmed = tot;
   lvl_off.resize(nl + 1);
   CUDA_OK(cudaMemcpyAsync(lvl_off.data(), X.c_lvloff.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, e.s));

@@ -104,6 +104,8 @@ void Engine::shard_setup(int rank_, int world_, const void* id) {
 }
 
 void Engine::shard_teardown() {
+  host_ag = nullptr;
+  host_ctx = nullptr;
   if (comm) {
     sync();
     auto& cc = comm_cache();
@@ -183,16 +185,15 @@ static void copy_segs(Engine& e, const std::vector<CopySeg>& segs) {
 // order on every rank) and rebuild each MatchSet as the rank-order
 // concatenation.
 void Engine::shard_gather_matches(const std::vector<int>& pids) {
-  if (shard_world <= 1 || pids.empty() || !comm) return;
+  if (shard_world <= 1 || pids.empty() || !shard_exchange()) return;
   const int W = shard_world, np = (int)pids.size();
-  ncclComm_t c = (ncclComm_t)comm;
   // 1. per-pattern counts of every rank
   std::vector<u32> mine(np), all((size_t)W * np);
   for (int i = 0; i < np; i++) mine[i] = matches[pids[i]].n;
   DevBuf<u32>& dc = sc.sh_cnt;
   dc.ensure((size_t)(W + 1) * np + 1);
   CUDA_OK(cudaMemcpyAsync(dc.p, mine.data(), np * sizeof(u32), cudaMemcpyHostToDevice, s));
-  NCCL_OK(nccl().AllGather(dc.p, dc.p + np, np, ncclUint32, c, s));
+  shard_allgather(dc.p, dc.p + np, np * sizeof(u32));
   CUDA_OK(cudaMemcpyAsync(all.data(), dc.p + np, (size_t)W * np * sizeof(u32), cudaMemcpyDeviceToHost, s));
   sync();
   // 2. pack this rank's lists: per pattern [classes | bindings]
@@ -216,7 +217,7 @@ void Engine::shard_gather_matches(const std::vector<int>& pids) {
   }
   copy_segs(*this, segs);
   // 3. one all-gather of the packed lists (padded to the largest rank)
-  NCCL_OK(nccl().AllGather(pk.p, rv.p, smax, ncclUint32, c, s));
+  shard_allgather(pk.p, rv.p, smax * sizeof(u32));
   // 4. unpack in rank order
   segs.clear();
   std::vector<u64> roff(W, 0);
@@ -243,6 +244,25 @@ void Engine::shard_gather_matches(const std::vector<int>& pids) {
 
 // plain all-gather of ``bytes`` from every rank into recv (rank order)
 void Engine::shard_allgather_bytes(const void* send, void* recv, size_t bytes) {
-  if (shard_world <= 1 || !comm) throw TsatException(TSAT_ERR_STATE, "no shard communicator");
-  NCCL_OK(nccl().AllGather(send, recv, bytes, ncclUint8, (ncclComm_t)comm, s));
+  if (shard_world <= 1 || !shard_exchange()) throw TsatException(TSAT_ERR_STATE, "no shard communicator");
+  shard_allgather(send, recv, bytes);
+}
+
+// The one exchange primitive: NCCL over NVLink when a communicator exists,
+// else the caller's host all-gather (device -> host, callback, host -> device
+// on the engine stream).  Both deliver rank r's bytes at recv + r * bytes.
+void Engine::shard_allgather(const void* dsend, void* drecv, size_t bytes) {
+  if (comm) {
+    NCCL_OK(nccl().AllGather(dsend, drecv, bytes, ncclUint8, (ncclComm_t)comm, s));
+    return;
+  }
+  if (!host_ag) throw TsatException(TSAT_ERR_STATE, "no shard transport");
+  ag_send.resize(bytes + 1);
+  ag_recv.resize(bytes * (size_t)shard_world + 1);
+  if (bytes) CUDA_OK(cudaMemcpyAsync(ag_send.data(), dsend, bytes, cudaMemcpyDeviceToHost, s));
+  sync();
+  if (host_ag(host_ctx, ag_send.data(), ag_recv.data(), (uint64_t)bytes) != 0)
+    throw TsatException(TSAT_ERR_STATE, "host all-gather transport failed");
+  if (bytes) CUDA_OK(cudaMemcpyAsync(drecv, ag_recv.data(), bytes * (size_t)shard_world, cudaMemcpyHostToDevice, s));
+  sync();
 }

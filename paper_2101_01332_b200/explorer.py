@@ -277,9 +277,14 @@ def explore(
         raise TensorSatError("graph must be single-rooted (run make_single_rooted)")
     eg, _ = build_egraph(g, device=device)
     if shard_group is not None:
-        from .shard import attach_group
+        import torch.distributed as dist
 
-        attach_group(eg, None if shard_group is True else shard_group)
+        from .shard import attach_group, attach_host
+
+        grp = None if shard_group is True else shard_group
+        # NCCL over NVLink for an nccl group; a host (gloo) group exchanges
+        # through host memory (several ranks may then share a GPU)
+        (attach_host if dist.get_backend(grp) == "gloo" else attach_group)(eg, grp)
     filt, report = saturate(eg, rules, limits, filter_mode, on_reject=on_reject,
                             allow_self_pairs=allow_self_pairs)
     return eg, filt, report

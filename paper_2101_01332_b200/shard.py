@@ -95,6 +95,39 @@ def attach_group(eg, group=None) -> None:
     attach(eg, dist.get_rank(group), dist.get_world_size(group), group_uid(group))
 
 
+def attach_host(eg, group=None) -> None:
+    """Shard ``eg`` over a torch.distributed group whose backend moves HOST
+    tensors (gloo): the engine's exchanges (per-pattern match counts, packed
+    match lists, greedy wide-level {cost, node} records) go device -> host ->
+    ``all_gather`` -> host -> device instead of NCCL.  Several ranks can then
+    share one GPU, which is how the exchange is tested on a one-GPU box."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+
+    def _allgather(_ctx, send, recv, nbytes):
+        try:
+            n = int(nbytes)
+            src = torch.empty(n, dtype=torch.uint8)
+            if n:
+                C.memmove(src.data_ptr(), send, n)
+            parts = [torch.empty(n, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, src, group=group)
+            for r, t in enumerate(parts):
+                if n:
+                    C.memmove(recv + r * n, t.data_ptr(), n)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the engine as a failed transport
+            return 1
+
+    cb = _lib.ALLGATHER_FN(_allgather)
+    eg._shard_cb = cb  # keep the trampoline alive as long as the engine
+    lib = _lib.load()
+    _lib.check(eg._h, lib.tsat_shard_setup_host(eg._h, rank, world, cb, None))
+
+
 def lib_class_range(n_alloc: int, rank: int, world: int) -> Tuple[int, int]:
     """tsat_shard_range through the C-ABI (pure host function, no device)."""
     lib = _lib.load()

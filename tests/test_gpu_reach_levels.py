@@ -5,7 +5,8 @@ Forced on (reach budget 0), every efficient-mode golden case must still give
 the reference's per-iteration dumps, filter lists and stats; with the private
 search budget at 0 (TSAT_REACH_STEPS=0, read once per process, so those runs
 go through a subprocess) every query the levels cannot decide takes the exact
-one-thread path.  The bitset is kept as the default below the memory budget."""
+one-thread path.  The level mode is the default (budget 0); the bitset mode
+is kept for budgets that fit it and tested here too."""
 
 import json
 import os
@@ -35,23 +36,23 @@ def _stats(rep):
     return {k: v for k, v in rep.to_stats().items() if "time" not in k}
 
 
-def run_case_levels(case):
+def run_case_levels(case, budget=0):
     g = cases.build_graph(bench_graphs, tensor_lang, case["graph"])
     rules = cases.select_rules(default_rules(), case["rules"])
     L = case["limits"]
     eg, _ = build_egraph(g)
-    eg.reach_budget = 0
+    eg.reach_budget = budget
     filt = set()
     for i, snap in enumerate(case["iterations"]):
         lim = ExploreLimits(n_max=L["n_max"], k_max=1, k_multi=1 if i < L["k_multi"] else 0)
         filt, rep = saturate(eg, rules, lim, "efficient", filt=filt, allow_self_pairs=case["allow_self_pairs"])
-        assert eg.reach_mode == 1
+        assert eg.reach_mode == (1 if budget == 0 else 0)
         assert eg.dump() == snap["dump"], f"iteration {i}"
         assert sorted(filt) == snap["filt"], f"iteration {i}"
         if rep.stop_reason != "iter-limit":
             break
     eg2, _ = build_egraph(g)
-    eg2.reach_budget = 0
+    eg2.reach_budget = budget
     filt2, rep2 = saturate(eg2, rules, ExploreLimits(**L), "efficient", filt=set(),
                            allow_self_pairs=case["allow_self_pairs"])
     assert eg2.dump() == case["final_dump"]
@@ -62,6 +63,12 @@ def run_case_levels(case):
 @pytest.mark.parametrize("case", EXPLORE, ids=[c["id"] for c in EXPLORE])
 def test_levels_prefilter_matches_reference(case):
     run_case_levels(case)
+
+
+@pytest.mark.parametrize("case", EXPLORE, ids=[c["id"] for c in EXPLORE])
+def test_bitset_prefilter_matches_reference(case):
+    """The descendants-bitset mode (a budget that fits) on the same cases."""
+    run_case_levels(case, budget=1 << 40)
 
 
 def test_levels_prefilter_exact_path_matches_reference():
