@@ -240,6 +240,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # fewer GPUs than ranks (a one-GPU box exercising the N>1 path): ranks
+    # share devices and exchange over gloo through the engine's host transport
+    shared_gpus = world > torch.cuda.device_count()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     # N>1 default: the ranks explore ONE graph together -- e-matching split by
@@ -249,7 +253,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpus:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         torch.cuda.synchronize()
@@ -259,7 +266,7 @@ def main():
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared_gpus else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -283,9 +290,9 @@ def main():
         for i in range(args.warmup + args.steps):
             eg = build_egraph(g, device=local)[0]
             if shard_mode:
-                from paper_2101_01332_b200.shard import attach_group
+                from paper_2101_01332_b200.shard import attach_group, attach_host
 
-                attach_group(eg)
+                (attach_host if shared_gpus else attach_group)(eg)
             flush.zero_()
             barrier()
             ms = np.zeros(9)

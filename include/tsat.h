@@ -201,6 +201,29 @@ int tsat_debug_info(tsat_engine* h, int64_t* out, int32_t n);
 /* per-phase device timings of the last saturate / greedy (ms) */
 int tsat_phase_times(tsat_engine* h, double* out, int32_t n);
 
+/* ---- reference API pieces outside the explore loop ---------------------- */
+
+/* EGraph.clone (egraph.py:351-364): copy src's e-graph state into dst (same
+ * device; dst's atom table must already hold src's atoms in the same order). */
+int tsat_copy_state(tsat_engine* dst, tsat_engine* src);
+/* rules.eval_pattern (rules.py:126-138): shape-infer nterm post-order programs
+ * (the tsat_add_terms format) under env[env_off[t] ...] on the device analysis,
+ * without inserting anything.  out_vals: nterm device Value records (the
+ * tsat_download_values layout); out_status: 0 ok, 1 ShapeMismatch,
+ * 2 MissingSplitOrigin, other = capacity. */
+int tsat_eval_terms(tsat_engine* h, int32_t ninstr, const int32_t* instr, int32_t nterm, const int32_t* term_len,
+                    int32_t nenv, const uint32_t* env, const uint32_t* env_off, void* out_vals, int32_t* out_status);
+/* cycles.live_adjacency (cycles.py:29-39) over the current filter list: classes
+ * (ascending id), CSR offsets and child positions (one per child of every live,
+ * unfiltered member).  sizes = {classes, edges}; outputs may be NULL. */
+int tsat_class_graph(tsat_engine* h, uint32_t* cls, uint32_t* eoff, uint32_t* edst, uint32_t* sizes);
+/* cycles.get_descendants (cycles.py:70-148): the transitive closure of the
+ * live child relation as a word-major bitset (bits[w * n + i] = word w of
+ * class i's descendants; a class is its own descendant iff it lies on a
+ * cycle).  sizes = {classes, words}; bits NULL or cap_words < classes * words:
+ * sizes only. */
+int tsat_descendants(tsat_engine* h, uint32_t* cls, uint32_t* bits, uint64_t cap_words, uint32_t* sizes);
+
 #ifdef __cplusplus
 }
 #endif

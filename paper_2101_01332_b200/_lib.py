@@ -71,6 +71,11 @@ _SIGS = {
     "tsat_ilp_download": ([C.c_void_p, u32p, u32p, u32p, u32p, u32p, u32p], C.c_int),
     "tsat_set_record_rejects": ([C.c_void_p, C.c_int32], C.c_int),
     "tsat_set_reach_budget": ([C.c_void_p, C.c_uint64], C.c_int),
+    "tsat_copy_state": ([C.c_void_p, C.c_void_p], C.c_int),
+    "tsat_eval_terms": ([C.c_void_p, C.c_int32, i32p, C.c_int32, i32p, C.c_int32, u32p, u32p, C.c_void_p, i32p],
+                        C.c_int),
+    "tsat_class_graph": ([C.c_void_p, u32p, u32p, u32p, u32p], C.c_int),
+    "tsat_descendants": ([C.c_void_p, u32p, u32p, C.c_uint64, u32p], C.c_int),
     "tsat_reach_mode": ([C.c_void_p, C.POINTER(C.c_int32)], C.c_int),
     "tsat_rejects": ([C.c_void_p, u32p, C.c_int64, i64p], C.c_int),
     "tsat_ematch": ([C.c_void_p, C.c_int32, u32p, u32p, C.c_int64, i64p, i32p], C.c_int),

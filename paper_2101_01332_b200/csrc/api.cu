@@ -441,3 +441,34 @@ int tsat_phase_times(tsat_engine* h, double* out, int32_t n) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- drop-in API helpers
+
+int tsat_copy_state(tsat_engine* dst, tsat_engine* src) {
+  if (!src) return TSAT_ERR_ARG;
+  GUARD(dst, dst->e->copy_state_from(*src->e));
+}
+
+int tsat_eval_terms(tsat_engine* h, int32_t ninstr, const int32_t* instr, int32_t nterm, const int32_t* term_len,
+                    int32_t nenv, const uint32_t* env, const uint32_t* env_off, void* out_vals, int32_t* out_status) {
+  GUARD(h, {
+    std::vector<Instr> prog(ninstr);
+    for (int i = 0; i < ninstr; i++) {
+      prog[i].kind = instr[4 * i];
+      prog[i].arg = instr[4 * i + 1];
+      prog[i].atom = (u32)instr[4 * i + 2];
+      prog[i].depth = instr[4 * i + 3];
+    }
+    h->e->eval_terms(ninstr, prog.data(), nterm, term_len, nenv, env, env_off, out_vals, out_status);
+  });
+}
+
+int tsat_class_graph(tsat_engine* h, uint32_t* cls, uint32_t* eoff, uint32_t* edst, uint32_t* sizes) {
+  if (!sizes) return TSAT_ERR_ARG;
+  GUARD(h, h->e->class_graph_download(cls, eoff, edst, sizes));
+}
+
+int tsat_descendants(tsat_engine* h, uint32_t* cls, uint32_t* bits, uint64_t cap_words, uint32_t* sizes) {
+  if (!sizes) return TSAT_ERR_ARG;
+  GUARD(h, h->e->descendants_download(cls, bits, cap_words, sizes));
+}

@@ -9,6 +9,7 @@
 #include <mutex>
 
 #include "engine.cuh"
+#include "rulesdev.cuh"
 
 static inline unsigned nblk(u64 n, unsigned t = 256) {
   u64 b = (n + t - 1) / t;
@@ -1136,4 +1137,99 @@ std::string Engine::dump_text() {
     os << "\n";
   }
   return os.str();
+}
+
+// ---------------------------------------------------------------- API helpers
+// (drop-in pieces of the reference API the explore loop does not use itself)
+
+// EGraph.clone (egraph.py:351-364): device-to-device copy of the e-graph state
+// of ``o`` (same device).  Atoms are re-sent by the caller in the same order,
+// so atom ids, analyses and interned cut trees stay valid as copied.
+void Engine::copy_state_from(Engine& o) {
+  if (o.device != device) throw TsatException(TSAT_ERR_ARG, "clone across devices");
+  o.sync();
+  sync();
+  analysis = o.analysis;
+  h = o.h;
+  h.nkids = o.h.nkids;
+  u64 n = o.h.next_id, nk = o.h.nkids;
+  if (cap_nodes < n + 1 || cap_kids < nk + 1) {
+    Counters keep = h;
+    memset(&h, 0, sizeof(h));  // nothing of the old content needs preserving
+    ensure_nodes(n + 1, nk + 1);
+    h = keep;
+  }
+  if (hc_cap != o.hc_cap) {
+    hc.alloc(o.hc_cap);
+    hc_cap = o.hc_cap;
+  }
+  hc_epoch = o.hc_epoch;
+  if (n) {
+    CUDA_OK(cudaMemcpyAsync(op.p, o.op.p, n * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(parent.p, o.parent.p, n * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(flags.p, o.flags.p, n * sizeof(u8), cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(val.p, o.val.p, n * sizeof(Val), cudaMemcpyDeviceToDevice, s));
+  }
+  CUDA_OK(cudaMemcpyAsync(koff.p, o.koff.p, (n + 1) * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+  if (nk) CUDA_OK(cudaMemcpyAsync(kids.p, o.kids.p, nk * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+  if (hc_cap)
+    CUDA_OK(cudaMemcpyAsync(hc.p, o.hc.p, (size_t)hc_cap * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+  if (tree_cap != o.tree_cap) {
+    trees.alloc(o.tree_cap);
+    tree_cap = o.tree_cap;
+  }
+  if (tree_hc_cap != o.tree_hc_cap) {
+    tree_hc.alloc(o.tree_hc_cap);
+    tree_hc_cap = o.tree_hc_cap;
+  }
+  CUDA_OK(cudaMemcpyAsync(trees.p, o.trees.p, (size_t)tree_cap * sizeof(Tree), cudaMemcpyDeviceToDevice, s));
+  CUDA_OK(cudaMemcpyAsync(tree_hc.p, o.tree_hc.p, (size_t)tree_hc_cap * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+  CUDA_OK(cudaMemcpyAsync(tree_count.p, o.tree_count.p, sizeof(u32), cudaMemcpyDeviceToDevice, s));
+  root = o.root;
+  push_counters();
+  snap.valid = false;
+  reach.valid = false;
+  filter_id++;
+  costs_valid_for = TSAT_NONE;
+  sync();
+}
+
+// eval_pattern (rules.py:126-138) of each term under its environment slice,
+// on the device analysis; status = ana status (0 ok)
+__global__ void k_eval_terms(G g, const Instr* prog, const int32_t* len, int nterm, const u32* env, const u32* env_off,
+                             Val* out, int32_t* status) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nterm) return;
+  u32 off = 0;
+  for (int k = 0; k < t; k++) off += (u32)len[k];
+  Val scratch[MAX_STACK];
+  const Val* res = nullptr;
+  int st = eval_target(g, prog + off, len[t], env + env_off[t], scratch, res);
+  status[t] = st;
+  if (st == AS_OK) out[t] = *res;
+}
+
+void Engine::eval_terms(int ninstr, const Instr* prog, int nterm, const int32_t* term_len, int nenv, const u32* env,
+                        const u32* env_off, void* out_vals, int32_t* status) {
+  if (!analysis) throw TsatException(TSAT_ERR_STATE, "eval_pattern needs the tensor analysis");
+  for (int i = 0; i < ninstr; i++)
+    if (prog[i].kind == I_APP && prog[i].arg > 8) throw TsatException(TSAT_ERR_ARG, "arity > 8 not supported");
+  DevBuf<Instr>& dp = sc.a_prog;
+  dp.ensure(ninstr + 1);
+  DevBuf<int32_t>& dl = sc.a_len;
+  dl.ensure(2 * (u64)nterm + 1);
+  DevBuf<u32>& de = sc.a_env;
+  de.ensure(nenv + (u64)nterm + 1);
+  DevBuf<Val>& dv = sc.a_val;
+  dv.ensure(nterm + 1);
+  CUDA_OK(cudaMemcpyAsync(dp.p, prog, ninstr * sizeof(Instr), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpyAsync(dl.p, term_len, nterm * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (nenv) CUDA_OK(cudaMemcpyAsync(de.p, env, nenv * sizeof(u32), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpyAsync(de.p + nenv, env_off, nterm * sizeof(u32), cudaMemcpyHostToDevice, s));
+  int32_t* dst = dl.p + nterm;
+  k_eval_terms<<<(nterm + 127) / 128, 128, 0, s>>>(view(), dp.p, dl.p, nterm, de.p, de.p + nenv, dv.p, dst);
+  CUDA_OK(cudaMemcpyAsync(out_vals, dv.p, nterm * sizeof(Val), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaMemcpyAsync(status, dst, nterm * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  sync();
+  check_error();
 }

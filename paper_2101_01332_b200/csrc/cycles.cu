@@ -668,3 +668,43 @@ i64 Engine::break_all_cycles(bool precheck_only, std::vector<std::vector<u32>>* 
     if (hres[3]) filter_id++;
   }
 }
+
+// ---------------------------------------------------------------- API helpers
+
+// live_adjacency (cycles.py:29-39) over the current filter: the snapshot class
+// graph (dense indices, one edge per child of every live unfiltered member).
+// sizes = {classes, edges}; any output pointer may be NULL.
+void Engine::class_graph_download(u32* cls, u32* eoff, u32* edst, u32* sizes) {
+  ensure_levels();
+  sizes[0] = cg_n;
+  sizes[1] = cg_ne;
+  if (cls && cg_n) CUDA_OK(cudaMemcpyAsync(cls, snap.cls_ids.p, cg_n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  if (eoff) CUDA_OK(cudaMemcpyAsync(eoff, sc.cg_eoff.p, (cg_n + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  if (edst && cg_ne) CUDA_OK(cudaMemcpyAsync(edst, sc.cg_edst.p, cg_ne * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
+}
+
+// get_descendants (cycles.py:70-148): the closure as the device bitset
+// (word-major: bits[w * n + i] = word w of class i's descendant set), built
+// regardless of the pre-filter budget.  sizes = {classes, words}; bits NULL
+// or too small: sizes only.
+void Engine::descendants_download(u32* cls, u32* bits, u64 cap_words, u32* sizes) {
+  if (!snap.valid) build_snapshot();
+  u64 keep = reach.budget;
+  reach.budget = ~0ull;
+  try {
+    build_reach();
+  } catch (...) {
+    reach.budget = keep;
+    throw;
+  }
+  reach.budget = keep;
+  sizes[0] = reach.n;
+  sizes[1] = reach.words;
+  u64 need = (u64)reach.n * reach.words;
+  if (cls && reach.n) CUDA_OK(cudaMemcpyAsync(cls, snap.cls_ids.p, reach.n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  if (bits && cap_words >= need && need)
+    CUDA_OK(cudaMemcpyAsync(bits, reach.bits.p, need * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  sync();
+  reach.valid = false;  // the pre-filter of the next iteration rebuilds its own
+}

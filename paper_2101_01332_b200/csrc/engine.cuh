@@ -241,6 +241,7 @@ struct Scratch {
   DevBuf<Instr> a_prog;
   DevBuf<int32_t> a_len;
   DevBuf<u32> a_env, a_out, a_ids;
+  DevBuf<Val> a_val;
 };
 
 struct WaveBufs;
@@ -373,6 +374,12 @@ struct Engine {
   bool shard_exchange() const { return comm != nullptr || host_ag != nullptr; }
   void shard_allgather(const void* dsend, void* drecv, size_t bytes);  // device buffers, rank order
   void shard_setup(int rank, int world, const void* nccl_id);
+  // API helpers (core.cu / cycles.cu)
+  void copy_state_from(Engine& o);
+  void eval_terms(int ninstr, const Instr* prog, int nterm, const int32_t* term_len, int nenv, const u32* env,
+                  const u32* env_off, void* out_vals, int32_t* status);
+  void class_graph_download(u32* cls, u32* eoff, u32* edst, u32* sizes);
+  void descendants_download(u32* cls, u32* bits, u64 cap_words, u32* sizes);
   void shard_teardown();
   void shard_candidate_ranges(std::vector<u32>& rng);
   void shard_gather_matches(const std::vector<int>& pids);

@@ -14,7 +14,7 @@ import functools
 
 import ctypes as C
 from dataclasses import dataclass
-from typing import Any, Iterable, Iterator, Mapping, Optional
+from typing import Any, Iterable, Iterator, Mapping, Optional, Protocol
 
 import numpy as np
 
@@ -169,6 +169,51 @@ class _View:
         return None
 
 
+class Analysis(Protocol):
+    """Language client of the e-graph (reference egraph.py:28-39).  The device
+    engine implements the tensor analysis natively (``TensorAnalysis``) or
+    none; the protocol is kept for type annotations of client code."""
+
+    def make(self, op: Atom, child_values: list) -> Any: ...
+
+    def merge(self, a: Any, b: Any) -> Any: ...
+
+
+class UnionFind:
+    """Host union-find with the reference's contract (egraph.py:42-71): the
+    representative is the SMALLEST id.  The engine's own union-find lives on
+    the device (csrc/common.cuh uf_find / uf_union_min); this class serves
+    client code and tests that use the reference type directly."""
+
+    __slots__ = ("_parent",)
+
+    def __init__(self) -> None:
+        self._parent: dict = {}
+
+    def make(self, x: int) -> None:
+        self._parent[x] = x
+
+    def find(self, x: int) -> int:
+        p = self._parent
+        while p[x] != x:  # path halving
+            p[x] = p[p[x]]
+            x = p[x]
+        return x
+
+    def union(self, a: int, b: int) -> int:
+        ra, rb = self.find(a), self.find(b)
+        if ra != rb:
+            lo, hi = min(ra, rb), max(ra, rb)
+            self._parent[hi] = lo
+            return lo
+        return ra
+
+    def copy(self) -> "UnionFind":
+        out = UnionFind()
+        out._parent = self._parent.copy()
+        return out
+
+
 class EGraph:
     """Device-backed e-graph with the reference's public interface."""
 
@@ -186,6 +231,66 @@ class EGraph:
         self._sent = 0
         self._view: Optional[_View] = None
         self._filt_dev: Optional[frozenset] = frozenset()  # filter list known to be on the device
+
+    def clone(self) -> "EGraph":
+        """Independent copy (reference egraph.py:351-364): a second engine on
+        the same device, filled by a device-to-device copy of the node table,
+        union-find, analyses, cut trees and hashcons (tsat_copy_state)."""
+        self._flush_atoms()
+        other = EGraph(self.analysis, self.device)
+        other._atoms = dict(self._atoms)
+        other._atom_list = list(self._atom_list)
+        other._sent = 0
+        other._flush_atoms()
+        _lib.check(other._h, _lib.load().tsat_copy_state(other._h, self._h))
+        other._filt_dev = self._filt_dev
+        return other
+
+    def eval_patterns(self, terms, substs) -> list:
+        """Device shape inference of each term under its substitution
+        (rules.eval_pattern, reference rules.py:126-138): one program per term
+        in the add_term format, evaluated by k_eval_terms without inserting."""
+        from .errors import MissingSplitOrigin
+
+        progs, env, env_off = [], [], []
+        for term, sub in zip(terms, substs):
+            slots: dict = {}
+            env_off.append(len(env))
+
+            def slot_of(name, slots=slots, sub=sub):
+                if name not in slots:
+                    slots[name] = len(slots)
+                    env.append(int(sub[name]))
+                return slots[name]
+
+            progs.append(compile_term(term, self._atom, slot_of))
+        self._flush_atoms()
+        instr = np.array([x for prog in progs for ins in prog for x in ins] or [0], np.int32)
+        lens = np.array([len(p) for p in progs], np.int32)
+        envv = np.array(env or [0], np.uint32)
+        offs = np.array(env_off or [0], np.uint32)
+        vals = np.zeros(max(len(progs), 1), VAL_DTYPE)
+        status = np.zeros(max(len(progs), 1), np.int32)
+        lib = _lib.load()
+        _lib.check(self._h, lib.tsat_eval_terms(
+            self._h, int(lens.sum()), _lib.ptr(instr, C.c_int32), len(progs), _lib.ptr(lens, C.c_int32), len(env),
+            _lib.ptr(envv, C.c_uint32), _lib.ptr(offs, C.c_uint32), vals.ctypes.data_as(C.c_void_p),
+            _lib.ptr(status, C.c_int32)))
+        for i, st in enumerate(status[: len(progs)]):
+            if st == 2:
+                raise MissingSplitOrigin(f"split of {terms[i]} has no recorded origin on its axis")
+            if st != 0:
+                raise ShapeMismatch(f"pattern {terms[i]} does not shape-check")
+        nt = C.c_uint32()
+        _lib.check(self._h, lib.tsat_download_values(self._h, None, 0, None, 0, C.byref(nt)))
+        view = _View.__new__(_View)
+        view.values = vals
+        view.trees = np.zeros(max(nt.value, 1), TREE_DTYPE)
+        _lib.check(self._h, lib.tsat_download_values(self._h, None, 0, view.trees.ctypes.data_as(C.c_void_p),
+                                                       view.trees.nbytes, C.byref(nt)))
+        view.atoms = self._atom_list
+        view._tree_cache = {}
+        return [view.value(i) for i in range(len(progs))]
 
     @property
     def reach_budget(self) -> None:

@@ -16,8 +16,8 @@ import numpy as np
 
 from . import _lib
 from .egraph import EGraph, compile_ruleset
-from .errors import TensorSatError
-from .rules import Match
+from .errors import AnalysisMergeError, TensorSatError
+from .rules import Match, combined_subst
 from .tensor_lang import TensorGraph, build_egraph
 
 FILTER_MODES = ("none", "vanilla", "efficient")
@@ -257,6 +257,27 @@ def _rejected_combos(eg: EGraph, rules) -> list:
             matches.append(Match(cls, tuple(sorted((back[names[k]], int(b[k])) for k in range(nb)))))
         out.append((rule, matches))
     return out
+
+
+def _apply_combo(eg, rule, matches: Sequence[Match]) -> bool:
+    """Instantiate each target under the combined substitution and union it
+    with its matched class (reference explorer.py:146-163), through the
+    device add_term / union; True iff nodes were allocated or a real merge
+    happened.  The engine's own apply is the batched wave path (csrc/wave.cu);
+    this is the single-combo form the reference API and vanilla_check use."""
+    before = eg.allocated_nodes
+    changed = False
+    subst = combined_subst([m.subst for m in matches], eg)
+    try:
+        for tgt, m in zip(rule.targets, matches):
+            new_cid = eg.add_term(tgt, subst)
+            old_cid = eg.find(m.eclass)
+            if eg.find(new_cid) != old_cid:
+                eg.union(old_cid, new_cid)
+                changed = True
+    except AnalysisMergeError as e:
+        raise AnalysisMergeError(f"unsound rule {rule.name!r}: {e}") from e
+    return changed or eg.allocated_nodes > before
 
 
 def explore(

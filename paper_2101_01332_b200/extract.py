@@ -420,6 +420,8 @@ def solve_ilp(model: ILPModel, eg: EGraph, time_limit_s: float = 60.0) -> Extrac
     from .errors import InfeasibleModel, SolveTimeout
 
     t0 = time.perf_counter()
+    if time_limit_s <= 0:  # no budget: the reference's search loop never starts (extract.py:464, 516)
+        raise SolveTimeout(f"no feasible incumbent within {time_limit_s}s")
     c, a_ub, b_ub, a_eq, b_eq = _lp_arrays(model)
     integ = np.zeros(model.num_vars)
     integ[model.binary_idx] = 1
