@@ -206,18 +206,21 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier Fg, u32* c
   }
   __syncthreads();
   while (true) {
-    u32 start = s_start, end = s_end, lvl = s_lvl;
+    u32 start = s_start, end = s_end, lvl = s_lvl, edges = s_edges;
+    // every thread has read the level state before anyone (warp 0 in the
+    // thin-level walk, thread 0 at the end of a level) overwrites it
+    __syncthreads();
     if (start >= end) {
       if (threadIdx.x == 0) ctl[4] = 1;
       break;
     }
-    if (end - start > LV_WIDE || s_edges > LV_EDGES) break;
-    if (end - start <= 32 && s_edges <= 64) {
+    if (end - start > LV_WIDE || edges > LV_EDGES) break;
+    if (end - start <= 32 && edges <= 64) {
       // Very thin levels (deep chains): warp 0 alone walks level after level
       // with __syncwarp() only; the queue tail lives in a register.
       if (threadIdx.x < 32) {
         const u32 lane = threadIdx.x;
-        u32 st = start, en = end, lv = lvl, ed = s_edges, tl = *(volatile u32*)tail;
+        u32 st = start, en = end, lv = lvl, ed = edges, tl = *(volatile u32*)tail;
         // the frontier stays in registers: lane q holds vertex st + q and its
         // edge range, handed over by shuffles from the lane that queued it
         u32 a = 0, b = 0;
@@ -290,6 +293,7 @@ __global__ void __launch_bounds__(LV_BLOCK) k_frontier_block(Frontier Fg, u32* c
           b = nb;
           __syncwarp();
         }
+        __syncwarp();  // every lane read *tail before lane 0 rewrites it
         if (lane == 0) {
           s_start = st;
           s_end = en;
@@ -556,7 +560,7 @@ __global__ void __launch_bounds__(1024) k_peel_async(const u32* eoff, const u32*
     atomicAdd(&s_pending, 1u);
     u32 pos = atomicAdd(&s_tail, 1u);
     __threadfence_block();
-    ((volatile u32*)q)[pos] = p;
+    atomicExch(&q[pos], p);  // slot publish (atomic: the consumer spins on it)
   };
   u32 h = TSAT_NONE, cur = TSAT_NONE;
   bool done = false;
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(1024) k_peel_async(const u32* eoff, const u32*
         if (h >= n) done = true;
       }
       if (!done) {
-        u32 x = ((volatile u32*)q)[h];
+        u32 x = atomicAdd(&q[h], 0u);
         if (x != TSAT_NONE) {
           cur = x;
           h = TSAT_NONE;
