@@ -147,6 +147,7 @@ void Engine::reset(bool analysis_) {
   reach.valid = false;
   reach.mode = 0;
   reach.budget = default_reach_budget();
+  uf_changed = false;
   lv_snap = lv_filter = ~0ull;
   costs_valid_for = TSAT_NONE;
   kt_resolve(true);
@@ -622,6 +623,7 @@ u32 Engine::union_pair(u32 a, u32 b) {
   DevBuf<u32>& o = scratch_u32[7];
   o.ensure(1);
   snap.valid = false;
+  uf_changed = true;
   k_seq_union<<<1, 1, 0, s>>>(view(), a, b, o.p);
   u32 r;
   CUDA_OK(cudaMemcpyAsync(&r, o.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -845,6 +847,7 @@ void Engine::rebuild() {
     if (m == 0) break;
   }
   h.dirty = 0;
+  uf_changed = false;
   push_counters();
   check_error();  // syncs the stream
   snap.valid = false;
@@ -1186,6 +1189,7 @@ void Engine::copy_state_from(Engine& o) {
   CUDA_OK(cudaMemcpyAsync(tree_hc.p, o.tree_hc.p, (size_t)tree_hc_cap * sizeof(u32), cudaMemcpyDeviceToDevice, s));
   CUDA_OK(cudaMemcpyAsync(tree_count.p, o.tree_count.p, sizeof(u32), cudaMemcpyDeviceToDevice, s));
   root = o.root;
+  uf_changed = o.uf_changed;
   push_counters();
   snap.valid = false;
   reach.valid = false;

@@ -283,6 +283,9 @@ struct Engine {
   Counters h{};
   DevBuf<DevError> err;
   u32 root = TSAT_NONE;
+  // a union may have happened since the last rebuild (host-side, conservative;
+  // false = every stored child id is a class id: e-matching skips finds)
+  bool uf_changed = false;
 
   // rules
   std::vector<HPattern> patterns;
@@ -361,6 +364,7 @@ struct Engine {
 
   // snapshot + matching
   void build_snapshot();
+  DevBuf<u32> em_pool;  // e-matching semi-join bitmaps (match.cu)
   void ematch_batch(const std::vector<int>& pids);
 
   // multi-GPU e-matching shards (shard.cu)

@@ -622,6 +622,7 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
 void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P);
 
 void Engine::apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P) {
+  uf_changed = true;
   const HRule& hr = rules[ri];
   int R = 0;
   for (auto& t : hr.targets)

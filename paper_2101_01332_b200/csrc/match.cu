@@ -20,6 +20,7 @@
 // Two host synchronisations per batch (row counts, unique counts).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 
@@ -35,6 +36,10 @@ static inline unsigned nblk(u64 n, unsigned t = 256) {
 
 struct PatDev {
   PatApp apps[MAX_PAT_APPS];
+  // semi-join filter per nested app (i >= 1): bit c set iff class c holds a
+  // live, unfiltered node with apps[i]'s operator (bitmap over class ids,
+  // L2-resident: n_alloc / 8 bytes per operator); null = no filter
+  const u32* bm[MAX_PAT_APPS];
   int napps;
   int nb;
   int order[MAX_VARS];
@@ -52,7 +57,14 @@ struct SnapDev {
   const u32* cls_nodes;
   const u32* op_nodes;
   u32 n_alloc;
+  int clean;  // no union since the last rebuild: stored children are canonical, no find needed
 };
+
+__device__ __forceinline__ u32 kid_cls(const G& g, const SnapDev& sd, u32 k) {
+  return sd.clean ? k : uf_find_ro(g.parent, k);
+}
+
+__device__ __forceinline__ bool bm_has(const u32* bm, u32 c) { return !bm || ((bm[c >> 5] >> (c & 31)) & 1u); }
 
 #define MAX_BATCH 24
 #define SMALL_GROUP 32u
@@ -66,6 +78,12 @@ struct Batch {
   u32 rbase[MAX_BATCH + 1];   // raw row ranges (after the count scan)
   u32* out_cls[MAX_BATCH];
   u32* out_bind[MAX_BATCH];
+  // root-operator groups: patterns [gp[g], gp[g+1]) share a root atom (and
+  // so a candidate range); the count pass reads each candidate node once for
+  // the whole group.  gbase: flat ranges of group candidates.
+  int ngrp;
+  int gp[MAX_BATCH + 1];
+  u32 gbase[MAX_BATCH + 1];
 };
 
 __device__ __forceinline__ int seg_of(const u32* base, int n, u32 t) {
@@ -84,14 +102,17 @@ __device__ __forceinline__ bool node_ok(const G& g, u32 nid, const PatApp& a) {
   return (int)(g.koff[nid + 1] - g.koff[nid]) == a.nargs;
 }
 
-// bind the variable children of app t for node nid; set classes of app children
-__device__ __forceinline__ bool bind_node(const G& g, const PatApp& a, u32 nid, int t, u32* env,
-                                          int8_t* bound_at, u32* cls_app) {
+// bind the variable children of app t for node nid; set classes of app
+// children (rejecting the node when such a class has no node of the child
+// app's operator: the semi-join filter)
+__device__ __forceinline__ bool bind_node(const G& g, const SnapDev& sd, const PatDev& p, const PatApp& a, u32 nid,
+                                          int t, u32* env, int8_t* bound_at, u32* cls_app) {
   u32 base = g.koff[nid];
   for (int j = 0; j < a.nargs; j++) {
-    u32 ch = uf_find_ro(g.parent, g.kids[base + j]);
+    u32 ch = kid_cls(g, sd, g.kids[base + j]);
     int c = a.child[j];
     if (c >= 0) {
+      if (!bm_has(p.bm[c], ch)) return false;
       cls_app[c] = ch;
     } else {
       int v = -c - 1;
@@ -127,24 +148,39 @@ __device__ __forceinline__ u32 sel8(const u32* kc, int i) {
 // Counting (EMIT = false) of a pattern without repeated variables only needs
 // the root's op / arity / filter flag.
 template <bool EMIT, class F>
-__device__ __forceinline__ u32 match_root1(const G& g, const PatDev& p, u32 r, F emit) {
+__device__ __forceinline__ u32 match_root1(const G& g, const SnapDev& sd, const PatDev& p, u32 r, F emit) {
   const PatApp& a = p.apps[0];
   if (!node_ok(g, r, a)) return 0;
   if (!EMIT && p.neq == 0) return 1;
   u32 base = g.koff[r];
   u32 kc[8];
 #pragma unroll
-  for (int j = 0; j < 8; j++) kc[j] = j < a.nargs ? uf_find_ro(g.parent, g.kids[base + j]) : 0u;
+  for (int j = 0; j < 8; j++) kc[j] = j < a.nargs ? kid_cls(g, sd, g.kids[base + j]) : 0u;
   for (int i = 0; i < p.neq; i++)
     if (sel8(kc, p.eq[i][0]) != sel8(kc, p.eq[i][1])) return 0;
   if (EMIT) emit(uf_find_ro(g.parent, r), kc);
   return 1;
 }
 
+// semi-join pre-check of a root candidate, in registers: every app child of
+// the root must be a class holding its operator.  Most candidates of nested
+// patterns fail here, before any DFS state (local memory) is touched.
+__device__ __forceinline__ bool root_semijoin(const G& g, const SnapDev& sd, const PatDev& p, u32 r) {
+  const PatApp& a = p.apps[0];
+  u32 base = g.koff[r];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    if (j >= a.nargs) break;
+    int c = a.child[j];
+    if (c >= 0 && p.bm[c] && !bm_has(p.bm[c], kid_cls(g, sd, g.kids[base + j]))) return false;
+  }
+  return true;
+}
+
 // DFS over the pattern's join for root node r; emit(k, rc, env) per match.
 template <int MV, int MA, class F>
 __device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const PatDev& p, u32 r, F emit) {
-  if (!node_ok(g, r, p.apps[0])) return 0;
+  if (!node_ok(g, r, p.apps[0]) || !root_semijoin(g, sd, p, r)) return 0;
   u32 env[MV];
   int8_t bound_at[MV];
   u32 cls_app[MA];
@@ -153,7 +189,7 @@ __device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const P
     env[v] = TSAT_NONE;
     bound_at[v] = -1;
   }
-  if (!bind_node(g, p.apps[0], r, 0, env, bound_at, cls_app)) return 0;
+  if (!bind_node(g, sd, p, p.apps[0], r, 0, env, bound_at, cls_app)) return 0;
   u32 rc = uf_find_ro(g.parent, r);
   u32 count = 0;
   int level = 1;
@@ -183,7 +219,7 @@ __device__ __forceinline__ u32 match_root(const G& g, const SnapDev& sd, const P
     while (pos[level] < end[level]) {
       u32 m = sd.cls_nodes[pos[level]++];
       if (!node_ok(g, m, a)) continue;
-      if (bind_node(g, a, m, level, env, bound_at, cls_app)) {
+      if (bind_node(g, sd, p, a, m, level, env, bound_at, cls_app)) {
         found = true;
         break;
       }
@@ -214,7 +250,7 @@ __device__ __forceinline__ u32 match_root_part(const G& g, const SnapDev& sd, co
                                                u32 l1_stride, u32 l1_lim, u32* l1_size, F emit,
                                                u32 heavy_cut = 0xFFFFFFFFu) {
   *l1_size = 0;
-  if (!node_ok(g, r, p.apps[0])) return 0;
+  if (!node_ok(g, r, p.apps[0]) || !root_semijoin(g, sd, p, r)) return 0;
   u32 env[MV];
   int8_t bound_at[MV];
   u32 cls_app[MA];
@@ -223,7 +259,7 @@ __device__ __forceinline__ u32 match_root_part(const G& g, const SnapDev& sd, co
     env[v] = TSAT_NONE;
     bound_at[v] = -1;
   }
-  if (!bind_node(g, p.apps[0], r, 0, env, bound_at, cls_app)) return 0;
+  if (!bind_node(g, sd, p, p.apps[0], r, 0, env, bound_at, cls_app)) return 0;
   u32 rc = uf_find_ro(g.parent, r);
   if (p.napps == 1) {
     *l1_size = 1;
@@ -274,7 +310,7 @@ __device__ __forceinline__ u32 match_root_part(const G& g, const SnapDev& sd, co
         m = sd.cls_nodes[pos[level]++];
       }
       if (!node_ok(g, m, a)) continue;
-      if (bind_node(g, a, m, level, env, bound_at, cls_app)) {
+      if (bind_node(g, sd, p, a, m, level, env, bound_at, cls_app)) {
         found = true;
         break;
       }
@@ -355,20 +391,26 @@ __global__ void k_em_emit_w(G g, SnapDev sd, Batch B, const u32* heavy, const u3
 // registers + little local memory; the large one covers any loadable pattern)
 template <int MV, int MA>
 __global__ void k_em_count(G g, SnapDev sd, Batch B, u32 ntot, u32* cnt, u32* heavy, u32* nheavy, u32 cut) {
-  GRID_STRIDE(t, ntot) {
-    int p = seg_of(B.cbase, B.npat, (u32)t);
-    u32 r = sd.op_nodes[B.obase[p] + ((u32)t - B.cbase[p])];
-    const PatDev& pd = B.pat[p];
-    if (!pd.fast && heavy) {
-      // nested pattern: a candidate whose apps[1] class is large goes to a warp (k_em_count_w)
-      u32 sz;
-      u32 c = match_root_part<MV, MA>(g, sd, pd, r, 0u, 1u, 0xFFFFFFFFu, &sz, [](u32, u32, const u32*) {}, cut);
-      if (c == EM_HEAVY) heavy[atomicAdd(nheavy, 1u)] = (u32)t;
-      else cnt[t] = c;
-      continue;
+  GRID_STRIDE(t0, (u64)B.gbase[B.ngrp]) {
+    int gi = seg_of(B.gbase, B.ngrp, (u32)t0);
+    u32 k = (u32)t0 - B.gbase[gi];
+    u32 r = sd.op_nodes[B.obase[B.gp[gi]] + k];
+    // one candidate node, every pattern rooted at its operator (the node's
+    // record is read from DRAM once, then from L1)
+    for (int p = B.gp[gi]; p < B.gp[gi + 1]; p++) {
+      const u32 t = B.cbase[p] + k;
+      const PatDev& pd = B.pat[p];
+      if (!pd.fast && heavy) {
+        // nested pattern: a candidate whose apps[1] class is large goes to a warp (k_em_count_w)
+        u32 sz;
+        u32 c = match_root_part<MV, MA>(g, sd, pd, r, 0u, 1u, 0xFFFFFFFFu, &sz, [](u32, u32, const u32*) {}, cut);
+        if (c == EM_HEAVY) heavy[atomicAdd(nheavy, 1u)] = t;
+        else cnt[t] = c;
+        continue;
+      }
+      cnt[t] = pd.fast ? match_root1<false>(g, sd, pd, r, [](u32, const u32*) {})
+                       : match_root<MV, MA>(g, sd, pd, r, [](u32, u32, const u32*) {});
     }
-    cnt[t] = pd.fast ? match_root1<false>(g, pd, r, [](u32, const u32*) {})
-                           : match_root<MV, MA>(g, sd, pd, r, [](u32, u32, const u32*) {});
   }
 }
 
@@ -380,9 +422,10 @@ __global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u3
     u32 r = sd.op_nodes[B.obase[p] + ((u32)t - B.cbase[p])];
 
     u32 o = off[t];
+    if (off[t + 1] == o) continue;  // no match (the count pass decided)
     const int S = B.stride;
     if (pd.fast) {
-      match_root1<true>(g, pd, r, [&](u32 cls, const u32* kc) {
+      match_root1<true>(g, sd, pd, r, [&](u32 cls, const u32* kc) {
         rc[o] = cls;
         for (int j = 0; j < S; j++) rb[(u64)o * S + j] = j < pd.nb ? sel8(kc, pd.src[j]) : 0u;
       });
@@ -398,6 +441,48 @@ __global__ void k_em_emit(G g, SnapDev sd, Batch B, u32 ntot, const u32* off, u3
     } else {
       match_root<MV, MA>(g, sd, pd, r, put);
     }
+  }
+}
+
+// Semi-join reduction of the pattern trees (bottom-up, one launch per app
+// height): bitmap (p, i) over class ids marks the classes holding a live,
+// unfiltered node that matches pattern p's sub-pattern at app i ignoring
+// repeated-variable equalities -- operator, arity, and every app child's
+// class marked in that child's bitmap.  A root candidate then survives only
+// if each app child's class is marked: the join runs on L2-resident bitmaps
+// instead of chasing class members (a necessary condition, so the DFS that
+// follows stays the exact matcher).
+struct SemiJob {
+  u32 lo, hi;      // op-table range of the app's operator
+  u32 out;         // bitmap index
+  int nargs;
+  int child[8];    // bitmap index of an app child, -1 for a variable
+};
+#define SEMI_MAX 64
+struct SemiJobs {
+  int n;
+  u32 base[SEMI_MAX + 1];
+  SemiJob job[SEMI_MAX];
+};
+
+__global__ void k_em_semijoin(G g, SnapDev sd, SemiJobs J, u32* pool, u64 words) {
+  GRID_STRIDE(t, (u64)J.base[J.n]) {
+    int q = seg_of(J.base, J.n, (u32)t);
+    const SemiJob& jb = J.job[q];
+    u32 x = sd.op_nodes[jb.lo + ((u32)t - J.base[q])];
+    if (g.flags[x] & NF_FILT) continue;
+    u32 a = g.koff[x];
+    if ((int)(g.koff[x + 1] - a) != jb.nargs) continue;
+    bool ok = true;
+    for (int j = 0; j < jb.nargs && ok; j++) {
+      int c = jb.child[j];
+      if (c < 0) continue;
+      u32 k = kid_cls(g, sd, g.kids[a + j]);
+      ok = (pool[(u64)c * words + (k >> 5)] >> (k & 31)) & 1u;
+    }
+    if (!ok) continue;
+    u32 cls = uf_find_ro(g.parent, x);
+    atomicOr(&pool[(u64)jb.out * words + (cls >> 5)], 1u << (cls & 31));
   }
 }
 
@@ -582,8 +667,107 @@ void Engine::ematch_batch(const std::vector<int>& pids_all) {
     B.npat = np;
     B.cbase[np] = ntot;
     B.stride = stride;
+    // root-operator groups (patterns with one root atom are adjacent: the
+    // patterns were laid out in pids order, so regroup by a stable sort)
+    {
+      std::vector<int> idx(np);
+      for (int b = 0; b < np; b++) idx[b] = b;
+      std::stable_sort(idx.begin(), idx.end(),
+                       [&](int x, int y) { return B.pat[x].apps[0].atom < B.pat[y].apps[0].atom; });
+      Batch B2 = B;
+      std::vector<int> live2(np);
+      u32 cb = 0;
+      for (int b = 0; b < np; b++) {
+        int o = idx[b];
+        B2.pat[b] = B.pat[o];
+        B2.obase[b] = B.obase[o];
+        u32 sz = B.cbase[o + 1] - B.cbase[o];
+        B2.cbase[b] = cb;
+        cb += sz;
+        live2[b] = live[o];
+      }
+      B2.cbase[np] = cb;
+      B2.ngrp = 0;
+      u32 gb = 0;
+      for (int b = 0; b < np; b++) {
+        if (b == 0 || B2.pat[b].apps[0].atom != B2.pat[b - 1].apps[0].atom || B2.obase[b] != B2.obase[b - 1]) {
+          B2.gp[B2.ngrp] = b;
+          B2.gbase[B2.ngrp] = gb;
+          gb += B2.cbase[b + 1] - B2.cbase[b];
+          B2.ngrp++;
+        }
+      }
+      B2.gp[B2.ngrp] = np;
+      B2.gbase[B2.ngrp] = gb;
+      B = B2;
+      live = live2;
+    }
     KTimer kt(*this, KG_EMATCH, 0.0, 0);
-    SnapDev sd{snap.cls_index.p, snap.cls_off.p, snap.cls_nodes.p, snap.op_nodes.p, snap.n_alloc};
+    SnapDev sd{snap.cls_index.p, snap.cls_off.p, snap.cls_nodes.p, snap.op_nodes.p, snap.n_alloc,
+                (h.dirty || uf_changed) ? 0 : 1};
+    // semi-join reduction: bitmaps of every nested app of every live pattern
+    {
+      const u64 words = ((u64)snap.n_alloc + 31) / 32 + 1;
+      int nbm = 0;
+      int bmidx[MAX_BATCH][MAX_PAT_APPS];
+      int height[MAX_BATCH][MAX_PAT_APPS];
+      int hmax = -1;
+      for (int b = 0; b < np; b++) {
+        PatDev& p = B.pat[b];
+        for (int i = p.napps - 1; i >= 0; i--) {  // pre-order: children after their parent
+          int hgt = 0;
+          for (int j = 0; j < p.apps[i].nargs; j++)
+            if (p.apps[i].child[j] >= 0) hgt = std::max(hgt, height[b][p.apps[i].child[j]] + 1);
+          height[b][i] = hgt;
+          bmidx[b][i] = -1;
+          p.bm[i] = nullptr;
+          if (i >= 1 && nbm < SEMI_MAX) {
+            bmidx[b][i] = nbm++;
+            hmax = std::max(hmax, hgt);
+          }
+        }
+      }
+      if (nbm) {
+        em_pool.ensure((u64)nbm * words);
+        CUDA_OK(cudaMemsetAsync(em_pool.p, 0, (u64)nbm * words * sizeof(u32), s));
+        for (int hgt = 0; hgt <= hmax; hgt++) {
+          SemiJobs J;
+          memset(&J, 0, sizeof(J));
+          u32 tot = 0;
+          for (int b = 0; b < np; b++) {
+            const PatDev& p = B.pat[b];
+            for (int i = 1; i < p.napps; i++) {
+              if (bmidx[b][i] < 0 || height[b][i] != hgt) continue;
+              SemiJob& jb = J.job[J.n];
+              u32 atom = p.apps[i].atom;
+              jb.lo = atom + 1 < snap.op_off_h.size() ? snap.op_off_h[atom] : 0;
+              jb.hi = atom + 1 < snap.op_off_h.size() ? snap.op_off_h[atom + 1] : 0;
+              jb.out = (u32)bmidx[b][i];
+              jb.nargs = p.apps[i].nargs;
+              bool usable = true;
+              for (int j = 0; j < 8; j++) {
+                int c = j < jb.nargs ? p.apps[i].child[j] : -1;
+                jb.child[j] = c >= 0 ? bmidx[b][c] : -1;
+                if (c >= 0 && bmidx[b][c] < 0) usable = false;
+              }
+              if (!usable) {  // a child without a bitmap: this app cannot be pre-filtered
+                bmidx[b][i] = -1;
+                continue;
+              }
+              J.base[J.n] = tot;
+              tot += jb.hi - jb.lo;
+              cand_bytes += 13.0 * (jb.hi - jb.lo) + 8.0 * jb.nargs * (jb.hi - jb.lo);
+              J.n++;
+            }
+          }
+          J.base[J.n] = tot;
+          if (tot) k_em_semijoin<<<nblk(tot), 256, 0, s>>>(view(), sd, J, em_pool.p, words);
+        }
+        for (int b = 0; b < np; b++)
+          for (int i = 1; i < B.pat[b].napps; i++)
+            B.pat[b].bm[i] = bmidx[b][i] >= 0 ? em_pool.p + (u64)bmidx[b][i] * words : nullptr;
+      }
+    }
     DevBuf<u32>& cnt = sc.m_cnt;
     DevBuf<u32>& off = sc.m_pos;
     DevBuf<u32>& bnd = sc.m_bnd;
