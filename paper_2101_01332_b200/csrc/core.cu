@@ -1,5 +1,6 @@
 // libtsat core: buffers, loading, sequential (exact) mutation kernels,
 // parallel congruence rebuild, snapshot CSR construction, download + dump.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -10,6 +11,8 @@
 
 #include "engine.cuh"
 #include "rulesdev.cuh"
+
+namespace cg = cooperative_groups;
 
 static inline unsigned nblk(u64 n, unsigned t = 256) {
   u64 b = (n + t - 1) / t;
@@ -773,18 +776,28 @@ __global__ void k_rebuild_round(G g, u32 lo, u32 n, u32* linked, u32* nlinked, u
     }
     if (loser == TSAT_NONE) continue;
     g.flags[loser] &= ~NF_ALIVE;
-    atomicAdd(dropped, 1u);
-    u32 x = winner, y = loser;
+    u32 x = winner, y = loser, link = TSAT_NONE;
     while (true) {
       x = uf_find_ro(g.parent, x);
       y = uf_find_ro(g.parent, y);
       if (x == y) break;
       u32 lo = x < y ? x : y, hi = x < y ? y : x;
       if (atomicCAS(&g.parent[hi], hi, lo) == hi) {
-        linked[atomicAdd(nlinked, 1u)] = hi;
+        link = hi;
         break;
       }
     }
+    // counters bumped once per group of converged threads: a cascade round
+    // drops ~10^6 nodes, and per-thread atomics on one address serialise
+    cg::coalesced_group grp = cg::coalesced_threads();
+    u32 nl = grp.ballot(link != TSAT_NONE);
+    u32 base = 0;
+    if (grp.thread_rank() == 0) {
+      atomicAdd(dropped, grp.size());
+      if (nl) base = atomicAdd(nlinked, (u32)__popc(nl));
+    }
+    base = grp.shfl(base, 0);
+    if (link != TSAT_NONE) linked[base + __popc(nl & ((1u << grp.thread_rank()) - 1))] = link;
   }
 }
 
