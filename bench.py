@@ -62,6 +62,40 @@ KERNEL_OF = {"rebuild": "rebuild round (k_canon_kids+k_dedup_insert+k_dedup_drop
              "costs": "k_node_costs", "cycles": "cycle check (peel/BFS/DFS)", "snapshot": "snapshot CSR"}
 
 
+# source files whose kernels each ncu region describes: a capture whose stored
+# sha256 of any of them differs from the tree being benchmarked is stale
+NCU_SOURCES = {"ematch_13": ["match.cu", "egraph.cuh", "common.cuh"],
+               "rebuild_forced": ["core.cu", "egraph.cuh", "common.cuh", "analysis.cuh"],
+               "rebuild_cascade": ["core.cu", "egraph.cuh", "common.cuh", "analysis.cuh"],
+               "costs": ["extract.cu", "analysis.cuh"], "greedy": ["extract.cu", "levels.cu"],
+               "apply_wave": ["wave.cu", "analysis.cuh", "rulesdev.cuh", "egraph.cuh"]}
+
+
+def load_ncu():
+    """The newest profiles/*_ncu_traffic.json (scripts/ncu_summary.py), each
+    region marked stale when its kernel sources changed since the capture."""
+    import glob
+    import hashlib
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
+    if not files:
+        return {}, None
+    d = json.load(open(files[-1]))
+    srcs = d.get("_sources_sha256", {})
+    csrc = os.path.join(ROOT, "paper_2101_01332_b200", "csrc")
+    for k, deps in NCU_SOURCES.items():
+        if k not in d:
+            continue
+        for f in deps:
+            try:
+                cur = hashlib.sha256(open(os.path.join(csrc, f), "rb").read()).hexdigest()
+            except OSError:
+                cur = None
+            if srcs.get(f) != cur:
+                d[k]["stale"] = True
+    return d, os.path.relpath(files[-1], ROOT)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -356,16 +390,15 @@ def main():
     dom = dom_all if per_step[1][dom_all] > 0 else (max(with_bytes, key=lambda i: per_step[0][i]) if with_bytes else 0)
     achieved = per_step[1][dom] / (per_step[0][dom] / 1e3) / 1e9 if per_step[0][dom] > 0 else 0.0
     traffic = None
-    try:  # ncu DRAM bytes per launch of the same kernel group (committed capture)
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
-        if w["model"] == "bert" and KGROUPS[dom] in tr:
-            traffic = tr[KGROUPS[dom]]["dram_GB"] * 1e9
-    except Exception:
-        pass
+    ncu, ncu_file = load_ncu()
+    if w["model"] == "bert" and KGROUPS[dom] in ncu and not ncu[KGROUPS[dom]].get("stale"):
+        traffic = ncu[KGROUPS[dom]]["dram_GB"] * 1e9  # per launch, like `achieved`'s launch average
     roofline = {"bound": "hbm", "kernel": KERNEL_OF[KGROUPS[dom]], "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                 "launches_per_step": per_step[2][dom], "ms_per_step": per_step[0][dom],
-                "algorithmic_bytes_per_step": per_step[1][dom]}
+                "algorithmic_bytes_per_step": per_step[1][dom],
+                "algorithmic_bytes_per_launch": per_step[1][dom] / max(per_step[2][dom], 1),
+                "traffic_source": ncu_file if traffic is not None else None}
     groups_ms = {KGROUPS[i]: round(per_step[0][i], 3) for i in range(9)}
 
     line = {
@@ -405,17 +438,21 @@ def main():
         if w["model"] == "synth10m":
             line["sweep"] = sw
         else:
-            ncu = {}
-            try:
-                ncu = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
-            except Exception:
-                pass
+            def ncu_of(k):
+                c = ncu.get(k, {})
+                if not c or c.get("stale"):
+                    return {"ncu_dram_GB": None, "ncu_dram_GBps": None, "ncu_stale": bool(c)}
+                return {"ncu_dram_GB": c.get("dram_GB"), "ncu_dram_GBps": c.get("dram_GBps"),
+                        "ncu_kernel_ms": c.get("kernel_ms"), "ncu_dram_over_algorithmic":
+                        round(c["dram_GB"] / (sw[k]["bytes"] / 1e9), 3) if sw[k]["bytes"] and "dram_GB" in c
+                        and k != "apply_wave" else None}
+
             line["config5_kernels"] = {
-                k: {"ms": round(sw[k]["ms"], 4), "algorithmic_GB": round(sw[k]["bytes"] / 1e9, 4),
-                    "achieved_GBps": round(sw[k]["GBps"], 1), "frac": round(sw[k]["frac"], 4),
-                    "ncu_dram_GB_per_launch": ncu.get(k, {}).get("dram_GB"),
-                    "ncu_dram_GBps": ncu.get(k, {}).get("dram_GBps")}
+                k: dict({"ms": round(sw[k]["ms"], 4), "algorithmic_GB": round(sw[k]["bytes"] / 1e9, 4),
+                         "achieved_GBps": round(sw[k]["GBps"], 1), "frac": round(sw[k]["frac"], 4)},
+                        **(ncu_of(k) if k != "apply_wave" else {}))
                 for k in ("ematch_13", "rebuild_forced", "rebuild_cascade", "costs", "greedy", "apply_wave") if k in sw}
+            line["config5_kernels"]["ncu_capture"] = ncu_file
             line["config5_kernels"]["graph"] = {"nodes": sw["nodes"], "classes": sw["classes"],
                                                 "peak_GBps": sw["peak_GBps"],
                                                 "enodes_matched_per_s": sw["enodes_matched_per_s"]}

@@ -119,7 +119,7 @@ int tsat_force_rebuild(tsat_engine* h) {
     Engine& e = *h->e;
     e.h.dirty = 1;
     e.push_counters();
-    e.rebuild();
+    e.rebuild(true);
   });
 }
 

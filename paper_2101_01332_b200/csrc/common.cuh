@@ -14,6 +14,7 @@ typedef uint8_t u8;
 // node flag bits
 #define NF_ALIVE 1u
 #define NF_FILT 2u
+#define NF_LOCK 0x80u  // transient: analysis merge lock of a root (rebuild)
 
 // status / error codes shared with the Python boundary (_lib.py)
 #include "../../include/tsat.h"

@@ -139,6 +139,7 @@ void Engine::reset(bool analysis_) {
   CUDA_OK(cudaMemsetAsync(tree_count.p, 0, sizeof(u32), s));
   if (hc_cap) CUDA_OK(cudaMemsetAsync(hc.p, 0, (size_t)hc_cap * sizeof(unsigned long long), s));
   hc_epoch = 1;
+  hc_tombs = 0;
   root = TSAT_NONE;
   h_atoms.clear();
   atom_names.clear();
@@ -283,14 +284,19 @@ void dev_cache_forget_stream(cudaStream_t s) {
       if (blk.s == s) blk.s = nullptr;
 }
 
-void Engine::sync() {
+void Engine::sync(const char* sf, int sl) {
   nsync++;
+  static const bool dbg = getenv("TSAT_DEBUG_SYNCS") != nullptr;
+  if (dbg) {
+    const char* b = strrchr(sf, '/');
+    sync_sites[std::string(b ? b + 1 : sf) + ":" + std::to_string(sl)]++;
+  }
   CUDA_OK(cudaStreamSynchronize(s));
 }
 
-void Engine::pull_counters() {
+void Engine::pull_counters(const char* sf, int sl) {
   CUDA_OK(cudaMemcpyAsync(&h, cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-  sync();
+  sync(sf, sl);
 }
 
 void Engine::push_counters() {
@@ -307,10 +313,10 @@ static const char* status_name(int c) {
   }
 }
 
-void Engine::check_error() {
+void Engine::check_error(const char* sf, int sl) {
   DevError he;
   CUDA_OK(cudaMemcpyAsync(&he, err.p, sizeof(he), cudaMemcpyDeviceToHost, s));
-  sync();
+  sync(sf, sl);
   if (he.code != 0) {
     CUDA_OK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
     std::ostringstream os;
@@ -337,6 +343,7 @@ __global__ void k_hc_insert_alive(G g, u32 n) {
 
 // the next hashcons epoch: an empty table without a clear (a clear every 255)
 void Engine::hc_new_epoch() {
+  hc_tombs = 0;
   if (++hc_epoch > 255) {
     CUDA_OK(cudaMemsetAsync(hc.p, 0, (size_t)hc_cap * sizeof(unsigned long long), s));
     hc_epoch = 1;
@@ -347,6 +354,7 @@ void Engine::rehash(u32 new_cap) {
   hc.alloc(new_cap);
   hc_cap = new_cap;
   hc_epoch = 1;
+  hc_tombs = 0;
   CUDA_OK(cudaMemsetAsync(hc.p, 0, (size_t)new_cap * sizeof(unsigned long long), s));
   if (h.next_id) k_hc_insert_alive<<<nblk(h.next_id), 256, 0, s>>>(view(), h.next_id);
 }
@@ -743,40 +751,53 @@ __device__ __forceinline__ bool key_eq_canon(const G& g, u32 other, u32 op, u32 
   return true;
 }
 
-__global__ void k_rebuild_round(G g, u32 lo, u32 n, u32* linked, u32* nlinked, u32* dropped) {
-  GRID_STRIDE(i0, n) {
-    u32 i = lo + (u32)i0;
-    if (!(g.flags[i] & NF_ALIVE)) continue;
-    u32 a = g.koff[i], b = g.koff[i + 1];
-    u32 op = g.op[i];
-    u64 h = hash_mix(0x2545f4914f6cdd1dULL ^ ((u64)(b - a) << 32), op);
-    for (u32 j = a; j < b; j++) {
-      u32 k = g.kids[j], c = uf_find(g.parent, k);
-      if (c != k) g.kids[j] = c;
-      h = hash_mix(h, c);
+static_assert(sizeof(Val) % 16 == 0, "Val is copied in 16-byte words");
+struct RbCtl {
+  u32 ndirty[2];  // dirty-list length by round parity
+  u32 nlinked;    // links so far (merge list length)
+  u32 dropped;
+  u32 rounds;
+  u32 dirty_total;
+  u32 tombs;
+  u32 lost;       // dirty nodes whose slot was not found (invariant check)
+  unsigned long long t[4];  // %globaltimer: start, rounds done, merges done (TSAT_DEBUG_REBUILD)
+};
+
+// canonicalise node i's children (written back), then claim its slot under
+// the canonical key; a congruent node met there makes the larger id the loser:
+// dropped and its class linked on the spot (one drop per non-minimum).
+__device__ __forceinline__ u32 rb_process(const G& g, u32 i, u32* linkbits) {
+  u32 a = g.koff[i], b = g.koff[i + 1];
+  u32 op = g.op[i];
+  u64 h = hash_mix(0x2545f4914f6cdd1dULL ^ ((u64)(b - a) << 32), op);
+  for (u32 j = a; j < b; j++) {
+    u32 k = g.kids[j], c = uf_find(g.parent, k);
+    if (c != k) g.kids[j] = c;
+    h = hash_mix(h, c);
+  }
+  u32 slot = (u32)h & g.hc_mask;
+  u32 tag = hc_tag(g.hc_epoch, h);
+  unsigned long long mine = ((unsigned long long)tag << 32) | i;
+  u32 loser = TSAT_NONE, winner = TSAT_NONE;
+  while (true) {
+    unsigned long long e = ((volatile unsigned long long*)g.hc)[slot];
+    if (!hc_live(g, e)) {
+      if (atomicCAS(&g.hc[slot], e, mine) == e) break;
+      continue;
     }
-    u32 slot = (u32)h & g.hc_mask;
-    u32 tag = hc_tag(g.hc_epoch, h);
-    unsigned long long mine = ((unsigned long long)tag << 32) | i;
-    u32 loser = TSAT_NONE, winner = TSAT_NONE;
-    while (true) {
-      unsigned long long e = ((volatile unsigned long long*)g.hc)[slot];
-      if (!hc_live(g, e)) {
-        if (atomicCAS(&g.hc[slot], e, mine) == e) break;
-        continue;
-      }
-      if ((u32)(e >> 32) == tag && key_eq_canon(g, (u32)e, op, a, b - a)) {
-        unsigned long long old = atomicMin(&g.hc[slot], mine);
-        u32 o = (u32)old;
-        loser = o > i ? o : i;
-        winner = o > i ? i : o;
-        break;
-      }
-      slot = (slot + 1) & g.hc_mask;
+    if ((u32)(e >> 32) == tag && key_eq_canon(g, (u32)e, op, a, b - a)) {
+      unsigned long long old = atomicMin(&g.hc[slot], mine);
+      u32 o = (u32)old;
+      loser = o > i ? o : i;
+      winner = o > i ? i : o;
+      break;
     }
-    if (loser == TSAT_NONE) continue;
+    slot = (slot + 1) & g.hc_mask;
+  }
+  u32 link = TSAT_NONE;
+  if (loser != TSAT_NONE) {
     g.flags[loser] &= ~NF_ALIVE;
-    u32 x = winner, y = loser, link = TSAT_NONE;
+    u32 x = winner, y = loser;
     while (true) {
       x = uf_find_ro(g.parent, x);
       y = uf_find_ro(g.parent, y);
@@ -787,17 +808,229 @@ __global__ void k_rebuild_round(G g, u32 lo, u32 n, u32* linked, u32* nlinked, u
         break;
       }
     }
-    // counters bumped once per group of converged threads: a cascade round
-    // drops ~10^6 nodes, and per-thread atomics on one address serialise
-    cg::coalesced_group grp = cg::coalesced_threads();
-    u32 nl = grp.ballot(link != TSAT_NONE);
-    u32 base = 0;
-    if (grp.thread_rank() == 0) {
-      atomicAdd(dropped, grp.size());
-      if (nl) base = atomicAdd(nlinked, (u32)__popc(nl));
+  }
+  if (link != TSAT_NONE) atomicOr(&linkbits[link >> 5], 1u << (link & 31));
+  return (loser != TSAT_NONE ? 1u : 0u) | (link != TSAT_NONE ? 2u : 0u);
+}
+
+// per-warp counter flush (one atomic per warp instead of one per event: a
+// cascade round drops ~10^6 nodes, and atomics on one address serialise)
+__device__ __forceinline__ void rb_flush(u32 drops, u32 links, RbCtl* ctl) {
+  drops = __reduce_add_sync(0xffffffffu, drops);
+  links = __reduce_add_sync(0xffffffffu, links);
+  if ((threadIdx.x & 31) == 0) {
+    if (drops) atomicAdd(&ctl->dropped, drops);
+    if (links) atomicAdd(&ctl->nlinked, links);
+  }
+}
+
+__global__ void k_rebuild_round(G g, u32 n, u32* linkbits, RbCtl* ctl) {
+  u32 drops = 0, links = 0;
+  GRID_STRIDE(i, n) {
+    if (g.flags[i] & NF_ALIVE) {
+      u32 r = rb_process(g, (u32)i, linkbits);
+      drops += r & 1u;
+      links += r >> 1;
     }
-    base = grp.shfl(base, 0);
-    if (link != TSAT_NONE) linked[base + __popc(nl & ((1u << grp.thread_rank()) - 1))] = link;
+  }
+  rb_flush(drops, links, ctl);
+}
+
+// Rebuild to fixpoint in one cooperative launch (no host round trip per
+// round).  Every live node sits in the hashcons exactly once, under its
+// stored children; a node needs work in a round only when one of its stored
+// children is no longer a root (its class was linked since the node was last
+// keyed).  So after an optional full first round (fresh epoch: forced
+// rebuilds / table cleanup), each round (1) lists the live nodes with a
+// non-root stored child, (2) replaces their old slots with tombstones (found
+// by the stale key they were inserted under), (3) re-keys and re-inserts them
+// exactly like a full round.  Nodes without a stale child keep their entries,
+// which are current; a round that links nothing is the fixpoint.  The result
+// equals a sequence of full rounds: same survivors (min id per final key),
+// same partition, and the table holds exactly the live nodes under their
+// canonical keys (plus tombstones, cleared by the next new epoch).
+
+__device__ __forceinline__ void rb_tombstone(const G& g, u32 i, RbCtl* ctl) {
+  u64 h = node_hash(g, i);  // the stored (stale) key the node was inserted under
+  u32 slot = (u32)h & g.hc_mask, tag = hc_tag(g.hc_epoch, h);
+  unsigned long long mine = ((unsigned long long)tag << 32) | i;
+  while (true) {
+    unsigned long long e = g.hc[slot];
+    if (!hc_live(g, e)) {
+      atomicAdd(&ctl->lost, 1u);
+      return;
+    }
+    if (e == mine) {
+      g.hc[slot] = hc_tomb(g.hc_epoch);
+      return;
+    }
+    slot = (slot + 1) & g.hc_mask;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_rebuild_fix(G g, u32 n, int full, u32* dl, u32* linkbits, RbCtl* ctl) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ u32 sm_ko[8 * 129];
+  __shared__ u8 sm_df[8 * 128];
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x, nth = (u64)gridDim.x * blockDim.x;
+  if (tid == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ctl->t[0]));
+  // a full first round (k_rebuild_round, launched before) left its links here
+  u32 l0 = ((volatile RbCtl*)ctl)->nlinked;
+  u32 r = full ? 1 : 0;
+  if (full && l0 == 0) {
+    if (tid == 0) ctl->rounds = 1;
+    return;
+  }
+  for (;; r++) {
+    u32* cnt = &ctl->ndirty[r & 1];
+    if (tid == 0) ctl->ndirty[(r + 1) & 1] = 0;  // the previous round's list (next used by round r + 1)
+    // (1) live nodes with a non-root stored child.  A warp takes 128
+    // consecutive nodes: their child offsets go to shared memory (4
+    // coalesced loads), the combined child range is swept 128 slots per step
+    // (4 independent coalesced loads + 4 independent parent gathers per
+    // lane), and a stale slot flags its owner (binary search of the offsets)
+    {
+      const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+      u32* ko = sm_ko + wib * 129;
+      u8* df = sm_df + wib * 128;
+      const u64 wid = tid >> 5, nw = nth >> 5;
+      for (u64 base = wid * 128; base < n; base += nw * 128) {
+        const u32 cntn = (u32)((n - base) < 128 ? (n - base) : 128);
+        u32 am = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const u32 li = q * 32 + lane, i = (u32)base + li;
+          ko[li] = li < cntn ? g.koff[i] : 0u;
+          if (li < cntn && (g.flags[i] & NF_ALIVE)) am |= 1u << q;
+          df[li] = 0;
+        }
+        if (lane == 0) ko[128] = g.koff[base + cntn];
+        __syncwarp();
+        for (u32 li = cntn + lane; li < 128; li += 32) ko[li] = ko[128];
+        __syncwarp();
+        const u32 lo = ko[0], hi = ko[128];
+        for (u32 c = lo; c < hi; c += 128) {
+          u32 k[4], pp[4];
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const u32 j = c + q * 32 + lane;
+            k[q] = j < hi ? g.kids[j] : TSAT_NONE;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; q++) pp[q] = k[q] != TSAT_NONE ? g.parent[k[q]] : TSAT_NONE;
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            if (pp[q] != k[q]) {
+              const u32 j = c + q * 32 + lane;
+              u32 l = 0, h2 = 128;  // last li with ko[li] <= j
+              while (h2 - l > 1) {
+                u32 mid = (l + h2) >> 1;
+                if (ko[mid] <= j) l = mid;
+                else h2 = mid;
+              }
+              df[l] = 1;
+            }
+        }
+        __syncwarp();
+        u32 dm[4], tot = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          dm[q] = __ballot_sync(0xffffffffu, ((am >> q) & 1u) && df[q * 32 + lane]);
+          tot += __popc(dm[q]);
+        }
+        if (tot) {
+          u32 wb = 0;
+          if (lane == 0) wb = atomicAdd(cnt, tot);
+          wb = __shfl_sync(0xffffffffu, wb, 0);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            if ((dm[q] >> lane) & 1u) dl[wb + __popc(dm[q] & ((1u << lane) - 1))] = (u32)base + q * 32 + lane;
+            wb += __popc(dm[q]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    grid.sync();
+    const u32 nd = ((volatile u32*)cnt)[0];
+    if (nd == 0) break;
+    // (2) tombstones for their stale entries
+    for (u64 k = tid; k < nd; k += nth) rb_tombstone(g, dl[k], ctl);
+    grid.sync();
+    // (3) re-key + re-insert (drops / links like a full round)
+    {
+      u32 drops = 0, links = 0;
+      for (u64 k = tid; k < nd; k += nth) {
+        u32 rr = rb_process(g, dl[k], linkbits);
+        drops += rr & 1u;
+        links += rr >> 1;
+      }
+      rb_flush(drops, links, ctl);
+    }
+    if (tid == 0) {
+      ctl->dirty_total += nd;
+      ctl->tombs += nd;
+    }
+    grid.sync();
+    const u32 l1 = ((volatile RbCtl*)ctl)->nlinked;
+    if (l1 == l0) {
+      r++;
+      break;
+    }
+    l0 = l1;
+  }
+  if (tid == 0) {
+    ctl->rounds = r;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ctl->t[1]));
+  }
+  // every linked root's own analysis folds into its final root (set unions:
+  // order free) under a per-root lock bit in its flags word; sources are
+  // non-roots, so nobody writes them meanwhile
+  const u32 nwords = (n + 31) >> 5;
+  for (u64 w = tid; w < nwords; w += nth) {
+    u32 bits = linkbits[w];
+    if (!bits) continue;
+    linkbits[w] = 0;  // left clear for the next rebuild
+    if (!g.analysis) continue;
+   while (bits) {
+    const u32 src = (u32)w * 32 + (__ffs(bits) - 1);
+    bits &= bits - 1;
+    const u32 t = uf_find_ro(g.parent, src);    u32* word = (u32*)(g.flags + (t & ~3u));
+    const u32 bit = NF_LOCK << (8 * (t & 3u));
+    bool done = false;
+    {
+      // lock-free when the source adds nothing: a root's origin sets only
+      // grow, so a source already contained stays contained
+      Val cur;
+      const int4* sp = (const int4*)(g.val + t);
+      int4* dp = (int4*)&cur;
+      for (int q = 0; q < (int)(sizeof(Val) / 16); q++) dp[q] = __ldcg(sp + q);
+      const Val& o = g.val[src];
+      done = val_same_data(cur, o) && !val_merge_grows(cur, o);
+    }
+    while (!done) {
+      if (!(atomicOr(word, bit) & bit)) {
+        __threadfence();
+        Val acc;
+        {  // L2 copy: another SM may have merged into t since this SM last saw it
+          const int4* sp = (const int4*)(g.val + t);
+          int4* dp = (int4*)&acc;
+          for (int q = 0; q < (int)(sizeof(Val) / 16); q++) dp[q] = __ldcg(sp + q);
+        }
+        const Val& o = g.val[src];
+        if (!val_same_data(acc, o)) dev_set_error(g.err, TSAT_ERR_MERGE, 4, t, src);
+        else if (val_merge_into(acc, o) != AS_OK) dev_set_error(g.err, TSAT_ERR_CAPACITY, 5, t, src);
+        else g.val[t] = acc;
+        __threadfence();
+        atomicAnd(word, ~bit);
+        done = true;
+      }
+    }
+   }
+  }
+  if (ctl->t[3]) {  // debug: time the merge phase
+    grid.sync();
+    if (tid == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ctl->t[2]));
   }
 }
 
@@ -826,39 +1059,72 @@ __global__ void k_merge_groups(G g, const u32* tgt, const u32* src, u32 m) {
   }
 }
 
-void Engine::rebuild() {
+void Engine::rebuild(bool full) {
   if (!h.dirty) return;
   u32 n = h.next_id;
-  DevBuf<u32>& linked = scratch_u32[1];
-  DevBuf<u32>& tgt = scratch_u32[2];
-  DevBuf<u32>& srt_t = scratch_u32[3];
-  DevBuf<u32>& srt_s = scratch_u32[4];
   DevBuf<u32>& small = scratch_u32[5];
-  linked.ensure(n + 1);
-  tgt.ensure(n + 1);
-  srt_t.ensure(n + 1);
-  srt_s.ensure(n + 1);
-  small.ensure(4);
-  while (true) {
-    {
-      // algorithmic bytes of one dirty round: 60 N + 12 A
-      KTimer kt(*this, KG_REBUILD, 60.0 * h.live + 12.0 * h.nkids, 1);
-      hc_new_epoch();
-      CUDA_OK(cudaMemsetAsync(small.p, 0, 2 * sizeof(u32), s));
-      k_rebuild_round<<<nblk(n), 256, 0, s>>>(view(), 0, n, linked.p, small.p, small.p + 1);
-    }
-    u32 hm[2];
-    CUDA_OK(cudaMemcpyAsync(hm, small.p, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
-    sync();
-    u32 m = hm[0];
-    h.live -= hm[1];
-    if (m && analysis) {
-      k_link_targets<<<nblk(m), 256, 0, s>>>(view(), linked.p, m, tgt.p);
-      dev_sort_pairs_u32(*this, tgt.p, srt_t.p, linked.p, srt_s.p, m, bits_for(n));
-      k_merge_groups<<<nblk(m), 256, 0, s>>>(view(), srt_t.p, srt_s.p, m);
-    }
-    if (m == 0) break;
+  DevBuf<u32>& dl = scratch_u32[6];
+  // link bitmap (one bit per node id), kept clear between rebuilds by the
+  // merge pass that consumes it
+  if (rb_linkbits.cap < (u64)(n + 31) / 32 + 1) {
+    rb_linkbits.ensure((u64)(n + 31) / 32 + 1);
+    CUDA_OK(cudaMemsetAsync(rb_linkbits.p, 0, rb_linkbits.cap * sizeof(u32), s));
   }
+  DevBuf<u32>& linked = rb_linkbits;
+  dl.ensure(n + 1);
+  small.ensure(sizeof(RbCtl) / 4 + 1);
+  // tombstones accumulate until the next epoch: a full round (fresh epoch)
+  // once live entries + tombstones could pass half the table
+  static const bool always_full = getenv("TSAT_REBUILD_FULL") != nullptr;
+  if (always_full || hc_tombs + 2ull * h.live > hc_cap / 2 + (u64)h.live) full = true;
+  if (full) hc_new_epoch();
+  static int coop = 0;
+  if (!coop) {
+    int per_sm = 0, nsm = 0, dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rebuild_fix, 256, 0));
+    coop = std::max(1, per_sm) * nsm;
+  }
+  RbCtl hc_;
+  {
+    KTimer kt(*this, KG_REBUILD, 0.0, 1);
+    CUDA_OK(cudaMemsetAsync(small.p, 0, sizeof(RbCtl), s));
+    static const bool dbg_t = getenv("TSAT_DEBUG_REBUILD") != nullptr;
+    if (dbg_t) CUDA_OK(cudaMemsetAsync((char*)small.p + offsetof(RbCtl, t) + 24, 1, 1, s));
+    G gv = view();
+    int fl = full ? 1 : 0;
+    RbCtl* cp0 = (RbCtl*)small.p;
+    // the full round streams every node: a plain (oversubscribed) grid keeps
+    // more loads in flight than the co-resident cooperative grid
+    if (full) k_rebuild_round<<<nblk(n), 256, 0, s>>>(gv, n, linked.p, cp0);
+    RbCtl* cp = (RbCtl*)small.p;
+    void* args[] = {&gv, &n, &fl, &dl.p, &linked.p, &cp};
+    unsigned nb = (unsigned)std::min<u64>((u64)coop, std::max<u64>(1, ((u64)n + 255) / 256));
+    CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_rebuild_fix, nb, 256, args, 0, s));
+  }
+  CUDA_OK(cudaMemcpyAsync(&hc_, small.p, sizeof(RbCtl), cudaMemcpyDeviceToHost, s));
+  sync();
+  {
+    // algorithmic bytes: a full round 60 N + 12 A; an
+    // incremental round scans flags / offsets / stored children + their
+    // parents (13 N + 8 A) and re-keys its dirty nodes (~60 + 12 arity + 16
+    // for the tombstone probe each)
+    const double avg_a = h.next_id ? (double)h.nkids / h.next_id : 0.0;
+    const u32 inc_rounds = hc_.rounds - (full ? 1 : 0);
+    kstat[KG_REBUILD].bytes += (full ? 60.0 * h.live + 12.0 * h.nkids : 0.0) +
+                               inc_rounds * (13.0 * n + 8.0 * h.nkids) + hc_.dirty_total * (76.0 + 12.0 * avg_a);
+    static const bool dbg = getenv("TSAT_DEBUG_REBUILD") != nullptr;
+    if (dbg)
+      fprintf(stderr, "rebuild: full %d rounds %u dirty %u dropped %u linked %u tombs %llu/%u live %u | rounds %.1f us merges %.1f us\n", (int)full,
+              hc_.rounds, hc_.dirty_total, hc_.dropped, hc_.nlinked, (unsigned long long)(hc_tombs + hc_.tombs),
+              hc_cap, h.live, (hc_.t[1] - hc_.t[0]) * 1e-3, hc_.t[2] ? (hc_.t[2] - hc_.t[1]) * 1e-3 : 0.0);
+  }
+  if (hc_.lost) throw TsatException(TSAT_ERR_STATE, "rebuild: hashcons entry of a live node not found");
+  hc_tombs += hc_.tombs;
+  rb_rounds_last = hc_.rounds;
+  rb_dirty_last = hc_.dirty_total;
+  h.live -= hc_.dropped;
   h.dirty = 0;
   uf_changed = false;
   push_counters();
@@ -1180,6 +1446,7 @@ void Engine::copy_state_from(Engine& o) {
     hc_cap = o.hc_cap;
   }
   hc_epoch = o.hc_epoch;
+  hc_tombs = o.hc_tombs;
   if (n) {
     CUDA_OK(cudaMemcpyAsync(op.p, o.op.p, n * sizeof(u32), cudaMemcpyDeviceToDevice, s));
     CUDA_OK(cudaMemcpyAsync(parent.p, o.parent.p, n * sizeof(u32), cudaMemcpyDeviceToDevice, s));

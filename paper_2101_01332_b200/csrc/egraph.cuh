@@ -76,7 +76,15 @@ __device__ __forceinline__ bool node_eq_node(const G& g, u32 x, u32 y) {
   return true;
 }
 
-__device__ __forceinline__ u32 hc_tag(u32 epoch, u64 h) { return (epoch << 24) | (u32)(h >> 40); }
+// fingerprint 0 is reserved for tombstones (incremental rebuild rounds), so
+// a tombstone is an occupied slot no probe's tag ever matches
+__device__ __forceinline__ u32 hc_tag(u32 epoch, u64 h) {
+  u32 fp = (u32)(h >> 40);
+  return (epoch << 24) | (fp ? fp : 1u);
+}
+__device__ __forceinline__ unsigned long long hc_tomb(u32 epoch) {
+  return ((unsigned long long)(epoch << 24) << 32) | 0xFFFFFFFFull;
+}
 __device__ __forceinline__ bool hc_live(const G& g, unsigned long long e) { return (u32)(e >> 56) == g.hc_epoch; }
 
 // hashcons lookup of a (canonical) key; TSAT_NONE on miss

@@ -1,5 +1,7 @@
 // Host-side engine object behind one C-ABI handle (include/tsat.h).
 #pragma once
+#include <cstring>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -270,6 +272,9 @@ struct Engine {
   u32 cap_nodes = 0, cap_kids = 0;
   DevBuf<unsigned long long> hc;
   u32 hc_cap = 0;
+  u64 hc_tombs = 0;
+  u32 rb_rounds_last = 0, rb_dirty_last = 0;
+  DevBuf<u32> rb_linkbits;  // rebuild: roots linked by the current rebuild (bitmap, zero between rebuilds)  // last rebuild: rounds, nodes re-keyed by incremental rounds  // tombstones left in the current epoch by incremental rebuild rounds
   u32 hc_epoch = 1;
   void hc_new_epoch();
 
@@ -331,10 +336,11 @@ struct Engine {
   ~Engine();
 
   G view();
-  void pull_counters();
+  void pull_counters(const char* sf = __builtin_FILE(), int sl = __builtin_LINE());
   void push_counters();
-  void check_error();
-  void sync();
+  void check_error(const char* sf = __builtin_FILE(), int sl = __builtin_LINE());
+  void sync(const char* sf = __builtin_FILE(), int sl = __builtin_LINE());
+  std::map<std::string, long> sync_sites;  // TSAT_DEBUG_SYNCS: host syncs per call site
   void ensure_nodes(u64 extra_nodes, u64 extra_kids);
   void rehash(u32 new_cap);
 
@@ -346,7 +352,7 @@ struct Engine {
   void add_terms(int ninstr, const Instr* prog, int nterm, const int32_t* term_len, int nenv,
                  const u32* env, u32* out_cls);
   u32 union_pair(u32 a, u32 b);
-  void rebuild();
+  void rebuild(bool full = false);
   void set_filter(int n, const u32* ids, int on);
   std::vector<u32> get_filter();
   u32 find(u32 x);

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Exploration driver (reference: pkg/src/tensorsat/explorer.py:136-365).
 //
 // Per iteration: snapshot CSR -> (efficient) descendants bitset -> e-match
@@ -617,6 +618,13 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
   report.stop_reason = stop;
   report.filter_size = (i64)get_filter().size();
   report.time_s = now_s() - t0;
+  if (getenv("TSAT_DEBUG_SYNCS")) {
+    std::vector<std::pair<long, std::string>> v;
+    for (auto& kv : sync_sites) v.push_back({kv.second, kv.first});
+    std::sort(v.rbegin(), v.rend());
+    for (auto& x : v) fprintf(stderr, "sync %6ld  %s\n", x.first, x.second.c_str());
+    sync_sites.clear();
+  }
 }
 
 void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P);

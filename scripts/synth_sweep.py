@@ -20,6 +20,30 @@ from paper_2101_01332_b200.extract import greedy_extract  # noqa: E402
 from paper_2101_01332_b200.rules import default_rules  # noqa: E402
 from paper_2101_01332_b200.tensor_lang import build_egraph  # noqa: E402
 
+PROF = os.environ.get("TSAT_PROF_REGION", "")  # ncu --profile-from-start off: capture one region
+
+
+class region:
+    """cudaProfilerStart/Stop around one named region on the last repetition
+    (TSAT_PROF_REGION=ematch|rebuild_forced|rebuild_cascade|costs|greedy|search)."""
+    last = False
+
+    def __init__(self, name):
+        self.on = PROF == name and region.last
+
+    def __enter__(self):
+        if self.on:
+            import torch
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
+
+    def __exit__(self, *a):
+        if self.on:
+            import torch
+            torch.cuda.synchronize()
+            torch.cuda.profiler.stop()
+
+
 GROUPS = ["rebuild", "ematch", "apply_seq", "apply_wave", "reach", "cycles", "costs", "greedy", "snapshot"]
 
 
@@ -39,11 +63,15 @@ def run(n=1415, reps=3):
     out = {"n": n}
     best = {}
     for rep in range(reps):
+        region.last = rep == reps - 1
         eg, classes = build_egraph(g)
         t0 = time.perf_counter()
-        filt, report = saturate(eg, merge, ExploreLimits(n_max=10**9, k_max=1, k_multi=1))
-        costs = egraph_costs(eg, CostModel())
-        res = greedy_extract(eg, costs, filt)
+        with region("search"):
+            filt, report = saturate(eg, merge, ExploreLimits(n_max=10**9, k_max=1, k_multi=1))
+        with region("costs"):
+            costs = egraph_costs(eg, CostModel())
+        with region("greedy"):
+            res = greedy_extract(eg, costs, filt)
         t1 = time.perf_counter()
         step = kstats(lib, eg)
         out["nodes"] = report.enodes_per_iter[-1]
@@ -55,19 +83,22 @@ def run(n=1415, reps=3):
         kstats(lib, eg)
         pids = np.arange(len(pidx), dtype=np.int32)
         counts = np.zeros(len(pidx), np.int64)
-        _lib.check(eg._h, lib.tsat_ematch_batch(eg._h, len(pids), pids.ctypes.data_as(C.POINTER(C.c_int32)),
-                                                counts.ctypes.data_as(C.POINTER(C.c_int64))))
+        with region("ematch"):
+            _lib.check(eg._h, lib.tsat_ematch_batch(eg._h, len(pids), pids.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                    counts.ctypes.data_as(C.POINTER(C.c_int64))))
         matched = int(counts.sum())
         em = kstats(lib, eg)["ematch"]
         # (ii) forced full rebuild, then a congruence cascade: w_{2k} ~ w_{2k+1}
-        _lib.check(eg._h, lib.tsat_force_rebuild(eg._h))
+        with region("rebuild_forced"):
+            _lib.check(eg._h, lib.tsat_force_rebuild(eg._h))
         rb = kstats(lib, eg)["rebuild"]
         a = np.array([classes[f"w{2 * k}"] for k in range(n // 2)], np.uint32)
         b = np.array([classes[f"w{2 * k + 1}"] for k in range(n // 2)], np.uint32)
         _lib.check(eg._h, lib.tsat_union_batch(eg._h, len(a), a.ctypes.data_as(C.POINTER(C.c_uint32)),
                                                b.ctypes.data_as(C.POINTER(C.c_uint32))))
         kstats(lib, eg)
-        _lib.check(eg._h, lib.tsat_rebuild(eg._h))
+        with region("rebuild_cascade"):
+            _lib.check(eg._h, lib.tsat_rebuild(eg._h))
         cas = kstats(lib, eg)["rebuild"]
         nodes_after = eg.num_nodes
         cur = {"ematch_13": em, "ematch_matches": matched, "rebuild_forced": rb, "rebuild_cascade": cas,
@@ -91,4 +122,4 @@ def run(n=1415, reps=3):
 
 if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1415
-    print(json.dumps(run(n), indent=1))
+    print(json.dumps(run(n, reps=int(os.environ.get("REPS", "3"))), indent=1))
