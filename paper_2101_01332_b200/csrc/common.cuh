@@ -26,8 +26,12 @@ struct DevError {
   i64 a, b;      // context (node id, combo position, ...)
 };
 
+// TSAT_DEBUG_SYNCS: count memcpy / memset calls per source line (host debug)
+extern bool g_dbg_sites;
+void tsat_count_site(const char* what, const char* file, int line);
 #define CUDA_OK(x)                                                                  \
   do {                                                                              \
+    if (g_dbg_sites) tsat_count_site(#x, __FILE__, __LINE__);                       \
     cudaError_t _e = (x);                                                           \
     if (_e != cudaSuccess) {                                                        \
       throw TsatException(TSAT_ERR_CUDA, std::string("CUDA: ") + cudaGetErrorString(_e) + \

@@ -284,6 +284,17 @@ void dev_cache_forget_stream(cudaStream_t s) {
       if (blk.s == s) blk.s = nullptr;
 }
 
+bool g_dbg_sites = getenv("TSAT_DEBUG_SYNCS") != nullptr;
+std::map<std::string, long> g_site_counts;
+void tsat_count_site(const char* what, const char* file, int line) {
+  const char* kind = strncmp(what, "cudaMemcpyAsync", 15) == 0   ? "memcpy"
+                     : strncmp(what, "cudaMemsetAsync", 15) == 0 ? "memset"
+                                                                 : nullptr;
+  if (!kind) return;
+  const char* b = strrchr(file, '/');
+  g_site_counts[std::string(kind) + " " + (b ? b + 1 : file) + ":" + std::to_string(line)]++;
+}
+
 void Engine::sync(const char* sf, int sl) {
   nsync++;
   static const bool dbg = getenv("TSAT_DEBUG_SYNCS") != nullptr;

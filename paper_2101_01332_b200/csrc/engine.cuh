@@ -406,6 +406,7 @@ struct Engine {
   double apply_deadline = -1.0;  // saturate's deadline (now_s clock), < 0: none
   bool force_seq = false;  // debug: exact sequential path only
   std::vector<std::string> rule_names;
+  bool wave_path(int ri, int filter_mode) const;
   void apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P);
   void saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self, const int* active_rule_mask,
                 int n_active);

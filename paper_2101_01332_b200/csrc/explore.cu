@@ -14,6 +14,12 @@
 
 #include "rulesdev.cuh"
 
+struct CtaCtl;
+void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P,
+                   const CtaCtl* resume, const DevStats* resume_stats);
+void run_rules_chain(Engine& e, const std::vector<int>& rules, const std::vector<unsigned long long>& Ps,
+                     int filter_mode, int allow_self, i64 n_max);
+
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -559,24 +565,44 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
     seq_timeout = false;
     apply_deadline = deadline;
     int stop_flag = 0;
+    // consecutive single-source rules on the wave path run as one chain of
+    // single-CTA launches (run_rules_chain); without a time limit only, since
+    // the deadline is checked between rules on the host
+    std::vector<int> chain;
+    std::vector<unsigned long long> chainP;
+    static const bool no_chain = getenv("TSAT_NO_CHAIN") != nullptr;
+    auto flush = [&]() {
+      if (chain.empty()) return;
+      uf_changed = true;
+      run_rules_chain(*this, chain, chainP, filter_mode, allow_self, lim.n_max);
+      chain.clear();
+      chainP.clear();
+    };
     for (int ri : active) {
       const HRule& hr = rules[ri];
       unsigned long long P = 1;
       for (int t = 0; t < hr.nsrc; t++) P *= matches[hr.src_pat[t]].n;
       if (P == 0) continue;
+      // (rules of <= 2048 positions: what the per-rule loop would run as one
+      // single-CTA launch too; larger ones start on grid waves)
+      if (!no_chain && deadline < 0 && hr.nsrc == 1 && P <= 2048 && wave_path(ri, filter_mode)) {
+        chain.push_back(ri);
+        chainP.push_back(P);
+        continue;
+      }
+      flush();
+      if (seq_stop) break;
       if (deadline >= 0 && now_s() > deadline) {
         stop_flag = 3;
         break;
       }
       apply_rule(ri, filter_mode, allow_self, lim.n_max, P);
-      if (seq_stop) {
-        stop_flag = 2;
-        break;
-      }
-      if (seq_timeout) {
-        stop_flag = 3;
-        break;
-      }
+      if (seq_stop || seq_timeout) break;
+    }
+    if (!seq_stop && !seq_timeout) flush();
+    if (!stop_flag) {
+      if (seq_stop) stop_flag = 2;
+      else if (seq_timeout) stop_flag = 3;
     }
     snap.valid = false;
     tick(3, tp);
@@ -621,22 +647,27 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
   if (getenv("TSAT_DEBUG_SYNCS")) {
     std::vector<std::pair<long, std::string>> v;
     for (auto& kv : sync_sites) v.push_back({kv.second, kv.first});
+    extern std::map<std::string, long> g_site_counts;
+    for (auto& kv : g_site_counts) v.push_back({kv.second, kv.first});
+    g_site_counts.clear();
     std::sort(v.rbegin(), v.rend());
     for (auto& x : v) fprintf(stderr, "sync %6ld  %s\n", x.first, x.second.c_str());
     sync_sites.clear();
   }
 }
 
-void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P);
 
-void Engine::apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P) {
-  uf_changed = true;
+bool Engine::wave_path(int ri, int filter_mode) const {
   const HRule& hr = rules[ri];
   int R = 0;
   for (auto& t : hr.targets)
     for (auto& in : t) R += in.kind == I_APP;
+  return filter_mode != 1 && hr.nsrc <= 2 && R <= 32 && !force_seq && !(record_rejects && filter_mode == 2);
+}
+
+void Engine::apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P) {
+  uf_changed = true;
   if (filter_mode == 1) run_rule_vanilla(ri, allow_self, n_max, P);
-  else if (hr.nsrc <= 2 && R <= 32 && !force_seq && !(record_rejects && filter_mode == 2))
-    run_rule_wave(*this, ri, filter_mode, allow_self, n_max, P);
+  else if (wave_path(ri, filter_mode)) run_rule_wave(*this, ri, filter_mode, allow_self, n_max, P, nullptr, nullptr);
   else run_rule_seq(ri, filter_mode, allow_self, n_max, 0, P);
 }

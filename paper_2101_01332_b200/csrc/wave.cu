@@ -1169,6 +1169,7 @@ struct WaveIO {
 #define CR_CAPACITY 4 // grow node / kid / hashcons capacity, then resume
 #define CR_WIDE 5     // clean full windows: continue on the grid path
 #define CR_ERROR 6    // analysis/table capacity error (exact path reports it)
+#define CR_NOTRUN 7   // chained launch skipped: an earlier rule of the chain returned to the host
 
 struct CtaCtl {
   unsigned long long p, P;
@@ -1268,7 +1269,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   }
 
 __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev RD, WaveRule W, WaveTab T, WaveIO io,
-                                                       CtaArgs A, CtaCtl* ctl) {
+                                                       CtaArgs A, CtaCtl* ctl, const CtaCtl* prev) {
   extern __shared__ __align__(16) unsigned char wsm[];
   // per-candidate arrays in shared memory: each phase reads what the previous
   // one wrote, so this removes an L2 round trip from most phase chains
@@ -1279,12 +1280,26 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
   __shared__ u32 s_wres;  // soft writers resolved in the current wave
   const u64 tid = threadIdx.x, nth = CTA_T;
   unsigned long long t_last = tid == 0 ? gtimer() : 0;
+  __shared__ int s_abort;
   if (tid == 0) {
     s_p = ctl->p;
     s_jcur = ctl->jcursor;
     s_epoch = ctl->epoch;
+    s_abort = 0;
+    // chained launch (run_rules_chain): runs only when the previous rule of
+    // the chain finished (CR_DONE), continuing its wave epoch
+    if (prev) {
+      if (prev->reason != CR_DONE) {
+        s_abort = 1;
+        ctl->reason = CR_NOTRUN;
+        ctl->epoch = prev->epoch;
+      } else {
+        s_epoch = prev->epoch;
+      }
+    }
   }
   __syncthreads();
+  if (s_abort) return;
   while (true) {
     if (tid == 0) {
       s_exit = 0xFFFFFFFFu;
@@ -1550,7 +1565,13 @@ struct WaveBufs {
   DevBuf<int> lvl_all;
   CtaCtl* hctl = nullptr;       // pinned
   Counters* hcnt = nullptr;     // pinned
+  // chained single-CTA launches (run_rules_chain)
+  DevBuf<CtaCtl> chain_ctl;
+  DevBuf<DevStats> chain_stats;
+  CtaCtl* hchain = nullptr;     // pinned: K control blocks, then K DevStats
+  size_t chain_cap = 0;
   ~WaveBufs() {
+    if (hchain) cudaFreeHost(hchain);
     if (hctl) cudaFreeHost(hctl);
     if (hcnt) cudaFreeHost(hcnt);
   }
@@ -1745,13 +1766,8 @@ static double wave_bytes(const Engine& e, const RuleDev& Rd, double ncand, doubl
   return per_cand * ncand + per_req * nreq + per_node * nwin + 4.0 * nk;
 }
 
-// one rule, positions [0, P): waves + exact fallback at hazards.  Windows of
-// up to CTA_WIN candidates run inside k_wave_cta (one launch for a whole run
-// of waves); larger windows run as grid waves.
-void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P) {
-  const HRule& hr = e.rules[ri];
-  if (!e.wave) e.wave = new WaveBufs();
-  WaveBufs& B = *e.wave;
+// templates of every rule of the loaded set, uploaded once per rule set
+static void ensure_wave_templates(Engine& e, WaveBufs& B) {
   if (!B.hctl) {
     CUDA_OK(cudaMallocHost((void**)&B.hctl, sizeof(CtaCtl)));
     CUDA_OK(cudaMallocHost((void**)&B.hcnt, sizeof(Counters)));
@@ -1783,6 +1799,117 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       CUDA_OK(cudaMemcpyAsync(B.lvl_all.p, lall.data(), lall.size() * sizeof(int), cudaMemcpyHostToDevice, e.s));
     B.rw_gen = e.rules_gen;
   }
+}
+
+// window of a single-CTA run: the per-candidate arrays go to shared memory
+// when they fit (a small window keeps most of the SM's L1 for the node table)
+#define CTA_WSMEM (160u << 10)
+static u32 cta_smem_win(int R) {
+  return wave_smem_layout(CTA_T, R, nullptr, nullptr) <= CTA_WSMEM ? CTA_T : 512u;
+}
+static void cta_fit_window(CtaCtl& c, int R) {
+  u32 SWIN = cta_smem_win(R);
+  if (wave_smem_layout(SWIN, R, nullptr, nullptr) <= CTA_WSMEM && c.win > SWIN) c.win = SWIN;
+}
+
+// launch k_wave_cta for rule ri on the engine stream (control block dctl,
+// statistics wstats; prev = the previous launch of a chain or null)
+static void cta_launch(Engine& e, WaveBufs& B, int ri, const RuleDev& Rd, const ReachDev& RD, int skip_self,
+                       bool multi, i64 n_max, CtaCtl* dctl, const CtaCtl* prev, DevStats* wstats) {
+  WaveBufs::RuleWave& RWc = B.rw[ri];
+  WaveRule W = RWc.W;
+  const std::vector<std::vector<int>>& lv = RWc.lv;
+  const int R = RWc.R;
+  W.tmpl = B.tmpl_all.p + RWc.tmpl_base;
+  const std::vector<int>& lvl_off = RWc.lvl_off;
+  int* lvl_dev = B.lvl_all.p + RWc.lvl_base;
+  WaveTab T{B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0, B.wtag.p, B.wown.p};
+  WaveIO io{B.status.p, B.hazard.p, B.ukind.p, B.grow.p, B.sa.p, B.env.p, B.olds.p, B.pre.p, B.acc.p,
+            B.ident.p, B.alloc.p, B.apre.p, B.wf.p, B.wpre.p, B.ka.p, B.kpre.p, B.uother.p, B.stops.p,
+            B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, wstats, lvl_dev};
+  CtaArgs A;
+  memset(&A, 0, sizeof(A));
+  A.nlv = (int)lv.size();
+  for (size_t d = 0; d < lv.size(); d++) {
+    A.lvl_off[d] = lvl_off[d];
+    A.nlvl[d] = (int)lv[d].size();
+  }
+  A.skip_self = skip_self;
+  A.multi = multi ? 1 : 0;
+  A.Kmax = RWc.Kmax;
+  A.nA = Rd.nmatch[0];
+  A.nB = multi ? Rd.nmatch[1] : 1;
+  A.n_max = n_max;
+  A.cta_win = CTA_WIN;
+  {
+    static const char* wa = getenv("TSAT_WIDE_AFTER");
+    A.wide_after = wa ? (u32)atoi(wa) : 8u;
+  }
+  A.pos = B.pos.p;
+  size_t smem_bytes = 0;
+  {
+    u32 SWIN = cta_smem_win(R);
+    size_t need = wave_smem_layout(SWIN, R, nullptr, nullptr);
+    if (need <= CTA_WSMEM) {
+      static int smem_set = 0;
+      if (!smem_set) {
+        CUDA_OK(cudaFuncSetAttribute(k_wave_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTA_WSMEM));
+        smem_set = 1;
+      }
+      A.smem = 1;
+      A.cta_win = SWIN;
+      smem_bytes = need;
+    }
+  }
+  k_wave_cta<<<1, CTA_T, smem_bytes, e.s>>>(e.view(), Rd, RD, W, T, io, A, dctl, prev);
+  CUDA_OK(cudaGetLastError());
+}
+
+// host side of a single-CTA run's return (its control block c): statistics,
+// resume position, and the reason's follow-up.  Returns true when the rule's
+// loop must stop (node limit / stop inside the exact path).
+static bool cta_exit(Engine& e, WaveBufs& B, int ri, const CtaCtl& c, unsigned long long& p, u32& jcursor, u32& win,
+                     bool& jvalid, bool multi, int filter_mode, int allow_self, i64 n_max) {
+  RuleStatsH& rs = e.rstats[ri];
+  B.epoch = c.epoch;
+  rs.found += c.found;
+  rs.skipped_self += c.self;
+  rs.skipped_compat += c.compat;
+  e.phase_ms[8] += c.waves;
+  for (int k = 0; k < 6; k++) e.phase_ms[10 + k] += c.cuts[k];
+  for (int k = 0; k < 12; k++) e.phase_ms[16 + k] += c.prof[k] * 1e-6;
+  e.phase_ms[28] += c.resolved;
+  p = c.p;
+  jcursor = c.jcursor;
+  win = c.win;
+  if (c.reason == CR_STOP) {
+    e.seq_stop = true;
+    e.report.node_limit_overshoot = c.overshoot;
+    return true;
+  } else if (c.reason == CR_HAZARD) {
+    e.phase_ms[9] += 1;
+    if (multi) jvalid = false;
+    e.ensure_nodes(4096, 4096);
+    e.run_rule_seq(ri, filter_mode, allow_self, n_max, p, p + 1);
+    if (e.seq_stop) return true;
+    p = p + 1;
+  } else if (c.reason == CR_REJOIN) {
+    jvalid = false;
+  } else if (c.reason == CR_WIDE) {
+    win = 4 * CTA_WIN;
+  }
+  return false;
+}
+
+// one rule, positions [0, P): waves + exact fallback at hazards.  Windows of
+// up to CTA_WIN candidates run inside k_wave_cta (one launch for a whole run
+// of waves); larger windows run as grid waves.
+void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P,
+                   const CtaCtl* resume, const DevStats* resume_stats) {
+  const HRule& hr = e.rules[ri];
+  if (!e.wave) e.wave = new WaveBufs();
+  WaveBufs& B = *e.wave;
+  ensure_wave_templates(e, B);
   WaveBufs::RuleWave& RWc = B.rw[ri];
   WaveRule W = RWc.W;
   const std::vector<std::vector<int>>& lv = RWc.lv;
@@ -1803,7 +1930,8 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     dbg_t0 = std::chrono::steady_clock::now();
   }
   B.wstats.ensure(1);
-  CUDA_OK(cudaMemsetAsync(B.wstats.p, 0, sizeof(DevStats), e.s));
+  if (resume_stats) CUDA_OK(cudaMemcpyAsync(B.wstats.p, resume_stats, sizeof(DevStats), cudaMemcpyHostToDevice, e.s));
+  else CUDA_OK(cudaMemsetAsync(B.wstats.p, 0, sizeof(DevStats), e.s));
   B.stops.ensure(6);
   CUDA_OK(cudaMemsetAsync(B.stops.p + 4, 0, sizeof(u32), e.s));  // grid-wave soft writers resolved
   // multi-pattern join cache: compatible positions stay valid until a union of
@@ -1814,7 +1942,11 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
   unsigned long long p = 0;
   static const u32 win0 = getenv("TSAT_WIN0") ? (u32)atoi(getenv("TSAT_WIN0")) : (1u << 12);
   u32 win = win0;  // adaptive candidate window (grows on clean waves, shrinks on dependencies)
-  while (p < P) {
+  bool stopped = false;
+  if (resume) {  // a chained single-CTA launch returned here (run_rules_chain)
+    stopped = cta_exit(e, B, ri, *resume, p, jcursor, win, jvalid, multi, filter_mode, allow_self, n_max);
+  }
+  while (!stopped && p < P) {
     // budget check at the segment's first position (explorer.py:198-206)
     if ((i64)e.h.live >= n_max) {
       e.seq_stop = true;
@@ -1875,57 +2007,12 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       c.jtotal = jtotal;
       c.jcomplete = jcomplete ? 1 : 0;
       c.reason = CR_DONE;
+      cta_fit_window(c, R);
       *B.hctl = c;
       CUDA_OK(cudaMemcpyAsync(B.ctl.p, B.hctl, sizeof(c), cudaMemcpyHostToDevice, e.s));
-      WaveTab T{B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0, B.wtag.p, B.wown.p};
-      WaveIO io{B.status.p, B.hazard.p, B.ukind.p, B.grow.p, B.sa.p, B.env.p, B.olds.p, B.pre.p, B.acc.p,
-                B.ident.p, B.alloc.p, B.apre.p, B.wf.p, B.wpre.p, B.ka.p, B.kpre.p, B.uother.p, B.stops.p,
-                B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, lvl_dev};
-      CtaArgs A;
-      memset(&A, 0, sizeof(A));
-      A.nlv = (int)lv.size();
-      for (size_t d = 0; d < lv.size(); d++) {
-        A.lvl_off[d] = lvl_off[d];
-        A.nlvl[d] = (int)lv[d].size();
-      }
-      A.skip_self = skip_self;
-      A.multi = multi ? 1 : 0;
-      A.Kmax = Kmax;
-      A.nA = Rd.nmatch[0];
-      A.nB = multi ? Rd.nmatch[1] : 1;
-      A.n_max = n_max;
-      A.cta_win = CTA_WIN;
-      {
-        static const char* wa = getenv("TSAT_WIDE_AFTER");
-        A.wide_after = wa ? (u32)atoi(wa) : 8u;
-      }
-      A.pos = B.pos.p;
-      size_t smem_bytes = 0;
-      {
-        // a small window keeps most of the SM's L1 for the node table / analyses
-        const size_t WSMEM = 160u << 10;
-        u32 SWIN = wave_smem_layout(CTA_T, R, nullptr, nullptr) <= WSMEM ? CTA_T : 512u;
-        size_t need = wave_smem_layout(SWIN, R, nullptr, nullptr);
-        if (need <= WSMEM) {
-          static int smem_set = 0;
-          if (!smem_set) {
-            CUDA_OK(cudaFuncSetAttribute(k_wave_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSMEM));
-            smem_set = 1;
-          }
-          A.smem = 1;
-          A.cta_win = SWIN;
-          smem_bytes = need;
-          if (c.win > SWIN) {
-            c.win = SWIN;
-            *B.hctl = c;
-            CUDA_OK(cudaMemcpyAsync(B.ctl.p, B.hctl, sizeof(c), cudaMemcpyHostToDevice, e.s));
-          }
-        }
-      }
       {
         KTimer kt(e, KG_APPLY_WAVE, 0.0, 1);
-        k_wave_cta<<<1, CTA_T, smem_bytes, e.s>>>(e.view(), Rd, RD, W, T, io, A, B.ctl.p);
-        CUDA_OK(cudaGetLastError());
+        cta_launch(e, B, ri, Rd, RD, skip_self, multi, n_max, B.ctl.p, nullptr, B.wstats.p);
         CUDA_OK(cudaMemcpyAsync(B.hctl, B.ctl.p, sizeof(c), cudaMemcpyDeviceToHost, e.s));
         CUDA_OK(cudaMemcpyAsync(B.hcnt, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
         e.sync();
@@ -1937,33 +2024,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         fprintf(stderr, "   cta: reason %u waves %u cand %llu resolved %u p %llu/%llu prof %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f | %.3f ms\n", c.reason, c.waves,
                 c.s_cand, c.resolved, c.p, P, c.prof[0]*1e-6, c.prof[1]*1e-6, c.prof[2]*1e-6, c.prof[3]*1e-6, c.prof[4]*1e-6, c.prof[5]*1e-6, c.prof[6]*1e-6, c.prof[7]*1e-6, c.prof[8]*1e-6, c.prof[9]*1e-6, c.prof[10]*1e-6, c.prof[11]*1e-6,
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0).count());
-      B.epoch = c.epoch;
-      rs.found += c.found;
-      rs.skipped_self += c.self;
-      rs.skipped_compat += c.compat;
-      e.phase_ms[8] += c.waves;
-      for (int k = 0; k < 6; k++) e.phase_ms[10 + k] += c.cuts[k];
-      for (int k = 0; k < 12; k++) e.phase_ms[16 + k] += c.prof[k] * 1e-6;
-      e.phase_ms[28] += c.resolved;
-      p = c.p;
-      jcursor = c.jcursor;
-      win = c.win;
-      if (c.reason == CR_STOP) {
-        e.seq_stop = true;
-        e.report.node_limit_overshoot = c.overshoot;
-        break;
-      } else if (c.reason == CR_HAZARD) {
-        e.phase_ms[9] += 1;
-        if (multi) jvalid = false;
-        e.ensure_nodes(4096, 4096);
-        e.run_rule_seq(ri, filter_mode, allow_self, n_max, p, p + 1);
-        if (e.seq_stop) break;
-        p = p + 1;
-      } else if (c.reason == CR_REJOIN) {
-        jvalid = false;
-      } else if (c.reason == CR_WIDE) {
-        win = 4 * CTA_WIN;
-      }
+      if (cta_exit(e, B, ri, c, p, jcursor, win, jvalid, multi, filter_mode, allow_self, n_max)) break;
       continue;
     }
     e.phase_ms[8] += 1;  // waves
@@ -2167,4 +2228,104 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     fprintf(stderr, "\n");
   }
 #endif
+}
+
+// A run of consecutive single-source rules, each launched as one single-CTA
+// run of waves without a host round trip in between: the launches are queued
+// back to back, each continuing the previous one's wave epoch, and a launch
+// whose predecessor did not finish its rule (hazard, node limit, capacity,
+// wide windows) does nothing (CR_NOTRUN).  One read-back after the run: the
+// finished rules are accounted exactly like their own loop would; the first
+// unfinished one resumes in run_rule_wave from its control block, and the
+// rest of the run is chained again.  Same sequence of device work as the
+// per-rule loop, minus ~10 host <-> device operations and 2 syncs per rule.
+void run_rules_chain(Engine& e, const std::vector<int>& rules, const std::vector<unsigned long long>& Ps,
+                     int filter_mode, int allow_self, i64 n_max) {
+  const size_t K = rules.size();
+  if (!K) return;
+  if ((i64)e.h.live >= n_max) {
+    e.seq_stop = true;
+    e.report.node_limit_overshoot = (i64)e.h.live - n_max;
+    return;
+  }
+  if (!e.wave) e.wave = new WaveBufs();
+  WaveBufs& B = *e.wave;
+  ensure_wave_templates(e, B);
+  if (B.chain_cap < K) {
+    if (B.hchain) cudaFreeHost(B.hchain);
+    CUDA_OK(cudaMallocHost((void**)&B.hchain, K * (sizeof(CtaCtl) + sizeof(DevStats))));
+    B.chain_ctl.alloc(K);
+    B.chain_stats.alloc(K);
+    B.chain_cap = K;
+  }
+  CtaCtl* hc = B.hchain;
+  DevStats* hs = (DevStats*)(B.hchain + K);
+  int maxR = 0, maxK = 0;
+  for (int ri : rules) {
+    if (B.rw[ri].lv.size() > 12)
+      throw TsatException(TSAT_ERR_UNSUPPORTED, "target deeper than the wave engine supports");
+    maxR = std::max(maxR, B.rw[ri].R);
+    maxK = std::max(maxK, B.rw[ri].Kmax);
+  }
+  e.ensure_nodes((u64)CTA_WIN * maxR + 2, (u64)CTA_WIN * maxK + 2);
+  ensure_cand_bufs(e, B, CTA_WIN, maxR);
+  static const u32 win0 = getenv("TSAT_WIN0") ? (u32)atoi(getenv("TSAT_WIN0")) : (1u << 12);
+  for (size_t k = 0; k < K; k++) {
+    CtaCtl& c = hc[k];
+    memset(&c, 0, sizeof(c));
+    c.P = Ps[k];
+    c.win = std::min<u32>(win0, CTA_WIN);
+    c.epoch = B.epoch;
+    c.jcomplete = 1;
+    c.reason = CR_DONE;
+    cta_fit_window(c, B.rw[rules[k]].R);
+  }
+  CUDA_OK(cudaMemcpyAsync(B.chain_ctl.p, hc, K * sizeof(CtaCtl), cudaMemcpyHostToDevice, e.s));
+  CUDA_OK(cudaMemsetAsync(B.chain_stats.p, 0, K * sizeof(DevStats), e.s));
+  {
+    KTimer kt(e, KG_APPLY_WAVE, 0.0, K);
+    for (size_t k = 0; k < K; k++) {
+      const int ri = rules[k];
+      RuleDev Rd = make_rule_dev(e, ri, filter_mode, allow_self);
+      ReachDev RD = make_reach_dev(e);
+      cta_launch(e, B, ri, Rd, RD, 0, false, n_max, B.chain_ctl.p + k, k ? B.chain_ctl.p + k - 1 : nullptr,
+                 B.chain_stats.p + k);
+    }
+  }
+  CUDA_OK(cudaMemcpyAsync(hc, B.chain_ctl.p, K * sizeof(CtaCtl), cudaMemcpyDeviceToHost, e.s));
+  CUDA_OK(cudaMemcpyAsync(hs, B.chain_stats.p, K * sizeof(DevStats), cudaMemcpyDeviceToHost, e.s));
+  CUDA_OK(cudaMemcpyAsync(&e.h, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
+  e.sync();
+  for (size_t k = 0; k < K; k++) {
+    const int ri = rules[k];
+    const CtaCtl c = hc[k];
+    if (c.reason == CR_NOTRUN) {
+      // an earlier rule returned to the host and was finished there: chain the rest again
+      std::vector<int> rest(rules.begin() + k, rules.end());
+      std::vector<unsigned long long> restP(Ps.begin() + k, Ps.end());
+      run_rules_chain(e, rest, restP, filter_mode, allow_self, n_max);
+      return;
+    }
+    {
+      RuleDev Rd = make_rule_dev(e, ri, filter_mode, allow_self);
+      e.kstat[KG_APPLY_WAVE].bytes +=
+          wave_bytes(e, Rd, (double)c.s_cand, (double)c.s_req, (double)c.s_win, (double)c.s_nk);
+    }
+    if (c.reason == CR_DONE && c.p >= c.P) {
+      unsigned long long p = 0;
+      u32 jc = 0, win = 0;
+      bool jv = false;
+      cta_exit(e, B, ri, c, p, jc, win, jv, false, filter_mode, allow_self, n_max);
+      accumulate_seg(e, ri, hs[k]);
+      continue;
+    }
+    e.uf_changed = true;
+    run_rule_wave(e, ri, filter_mode, allow_self, n_max, c.P, &c, &hs[k]);
+    if (e.seq_stop || e.seq_timeout) return;
+    // the launches after k were skipped (CR_NOTRUN): continue with k + 1
+    std::vector<int> rest(rules.begin() + k + 1, rules.end());
+    std::vector<unsigned long long> restP(Ps.begin() + k + 1, Ps.end());
+    run_rules_chain(e, rest, restP, filter_mode, allow_self, n_max);
+    return;
+  }
 }
