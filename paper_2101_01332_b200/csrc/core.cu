@@ -175,10 +175,43 @@ Engine::~Engine() {
   // everything this engine released is idle now; members released below too
   tl_stream = nullptr;
   if (wave) free_wave_bufs(wave);
+  if (s2) {
+    cudaStreamSynchronize(s2);
+    dev_cache_forget_stream(s2);
+    cudaStreamDestroy(s2);
+  }
+  if (ev_ov) cudaEventDestroy(ev_ov);
   if (s) {
     dev_cache_forget_stream(s);
     cudaStreamDestroy(s);
   }
+}
+
+// Run the pending overlap work (if any) on the overlap stream: the engine's
+// stream, CUB scratch and allocator stream are swapped for its duration, so
+// every launch / sync inside goes to s2; it waits only for ev_ov (recorded
+// before the work it overlaps), and the main stream waits for it afterwards.
+void Engine::run_overlap_hook() {
+  if (!overlap_hook) return;
+  std::function<void()> f = std::move(overlap_hook);
+  overlap_hook = nullptr;
+  CUDA_OK(cudaStreamWaitEvent(s2, ev_ov, 0));
+  std::swap(s, s2);
+  temp.swap(temp2);
+  tl_stream = s;
+  try {
+    f();
+  } catch (...) {
+    std::swap(s, s2);
+    temp.swap(temp2);
+    tl_stream = s;
+    throw;
+  }
+  CUDA_OK(cudaEventRecord(ev_ov, s));
+  std::swap(s, s2);
+  temp.swap(temp2);
+  tl_stream = s;
+  CUDA_OK(cudaStreamWaitEvent(s, ev_ov, 0));
 }
 
 G Engine::view() {

@@ -1,6 +1,7 @@
 // Host-side engine object behind one C-ABI handle (include/tsat.h).
 #pragma once
 #include <cstring>
+#include <functional>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -311,6 +312,14 @@ struct Engine {
   void reset(bool analysis_);
   Reach reach;
   DevBuf<u8> temp;  // cub scratch
+  // overlap stream: the next iteration's e-matching runs speculatively next to
+  // the (single-CTA, latency-bound) level peel of the cycle check
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_ov = nullptr;  // main-stream point (post-iteration snapshot) the overlap work waits for
+  DevBuf<u8> temp2;
+  std::function<void()> overlap_hook;  // run once by the level peel right after its launch
+  bool spec_ematch = false;            // the next iteration's e-matching is already done
+  void run_overlap_hook();
   DevBuf<u32> scratch_u32[8];
   DevBuf<DevStats> dstats;
 

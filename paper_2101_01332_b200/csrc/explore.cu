@@ -524,6 +524,9 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
   std::vector<int> multi, single;
   for (size_t i = 0; i < rules.size(); i++) (rules[i].nsrc > 1 ? multi : single).push_back((int)i);
   int stop = 0;  // iter-limit
+  spec_ematch = false;
+  static const bool no_overlap = getenv("TSAT_NO_OVERLAP") != nullptr;
+  const bool overlap_ok = !no_overlap && shard_world <= 1 && !getenv("TSAT_PHASE_SYNC") && !getenv("TSAT_DEBUG_ITERS");
   for (int q = 0; q < 32; q++) phase_ms[q] = 0.0;
   // host-side phase clocks (tsat_phase_times) need a stream sync per phase:
   // only when asked for (TSAT_PHASE_SYNC / TSAT_DEBUG_ITERS); the kernel-group
@@ -558,7 +561,8 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
     std::vector<int> todo;
     for (size_t p = 0; p < patterns.size(); p++)
       if (need[p]) todo.push_back((int)p);
-    ematch_batch(todo);
+    if (spec_ematch) spec_ematch = false;  // done next to the previous iteration's peel
+    else ematch_batch(todo);
     tick(2, tp);
     seq_changed = false;
     seq_stop = false;
@@ -610,7 +614,37 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
     tick(4, tp);
     build_snapshot();
     tick(0, tp);
-    if (filter_mode != 0) report.postprocess_filtered += break_all_cycles(false, nullptr);
+    if (filter_mode != 0) {
+      // when another iteration follows, its e-matching runs on the overlap
+      // stream right after the cycle check's level peel is launched (the peel
+      // is one latency-bound CTA); kept only if the check filters nothing
+      const bool next = !stop_flag && seq_changed && it + 1 < lim.k_max && !(deadline >= 0 && now_s() > deadline);
+      bool ran = false;
+      if (next && overlap_ok) {
+        std::vector<int> act2;
+        if (it + 1 < lim.k_multi) act2 = multi;
+        act2.insert(act2.end(), single.begin(), single.end());
+        std::vector<char> need2(patterns.size(), 0);
+        for (int ri : act2)
+          for (int t = 0; t < rules[ri].nsrc; t++) need2[rules[ri].src_pat[t]] = 1;
+        std::vector<int> todo2;
+        for (size_t p = 0; p < patterns.size(); p++)
+          if (need2[p]) todo2.push_back((int)p);
+        if (!s2) {
+          CUDA_OK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+          CUDA_OK(cudaEventCreateWithFlags(&ev_ov, cudaEventDisableTiming));
+        }
+        CUDA_OK(cudaEventRecord(ev_ov, s));
+        overlap_hook = [this, todo2, &ran]() {
+          ematch_batch(todo2);
+          ran = true;
+        };
+      }
+      const i64 added = break_all_cycles(false, nullptr);
+      overlap_hook = nullptr;
+      report.postprocess_filtered += added;
+      spec_ematch = ran && added == 0 && snap.valid;
+    }
     tick(5, tp);
     report.iterations = it + 1;
     {

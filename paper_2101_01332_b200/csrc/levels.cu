@@ -484,6 +484,7 @@ static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& tot
   }
   while (true) {
     k_frontier_block<<<1, LV_BLOCK, smem_bytes, e.s>>>(F, ctl.p, use_smem);
+    if (!F.bfs) e.run_overlap_hook();  // overlap work runs while the peel does
     CUDA_OK(cudaMemcpyAsync(h, ctl.p, 5 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
     e.sync();
     if (h[4]) break;
@@ -711,6 +712,7 @@ u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrim
     k_peel_async<<<1, pa_threads, bytes, e.s>>>(X.cg_eoff.p, X.cg_roff.p, X.cg_rsrc.p, mask, n, e.cg_ne, X.cg_level.p,
                                           X.c_order.p, X.c_lvloff.p, X.cg_outdeg.p, ctl.p);
     CUDA_OK(cudaGetLastError());
+    e.run_overlap_hook();  // work queued for the overlap stream runs while the peel does
     u32 hc[4];
     CUDA_OK(cudaMemcpyAsync(hc, ctl.p, 4 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
     e.sync();
