@@ -320,7 +320,8 @@ void dev_cache_forget_stream(cudaStream_t s) {
 bool g_dbg_sites = getenv("TSAT_DEBUG_SYNCS") != nullptr;
 std::map<std::string, long> g_site_counts;
 void tsat_count_site(const char* what, const char* file, int line) {
-  const char* kind = strncmp(what, "cudaMemcpyAsync", 15) == 0   ? "memcpy"
+  const char* kind = strncmp(what, "cudaMemcpyAsync", 15) == 0
+                         ? (strstr(what, "HostToDevice") ? "H2D" : strstr(what, "DeviceToHost") ? "D2H" : "D2D")
                      : strncmp(what, "cudaMemsetAsync", 15) == 0 ? "memset"
                                                                  : nullptr;
   if (!kind) return;
@@ -361,6 +362,11 @@ void Engine::check_error(const char* sf, int sl) {
   DevError he;
   CUDA_OK(cudaMemcpyAsync(&he, err.p, sizeof(he), cudaMemcpyDeviceToHost, s));
   sync(sf, sl);
+  raise_error(he);
+}
+
+// throw the device error ``he`` (read back by the caller) if one is set
+void Engine::raise_error(const DevError& he) {
   if (he.code != 0) {
     CUDA_OK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
     std::ostringstream os;
@@ -922,7 +928,11 @@ __global__ void __launch_bounds__(256) k_rebuild_fix(G g, u32 n, int full, u32* 
   u32 l0 = ((volatile RbCtl*)ctl)->nlinked;
   u32 r = full ? 1 : 0;
   if (full && l0 == 0) {
-    if (tid == 0) ctl->rounds = 1;
+    if (tid == 0) {
+      ctl->rounds = 1;
+      g.cnt->live -= ctl->dropped;  // congruent members of one class: dropped, nothing linked
+      g.cnt->dirty = 0;
+    }
     return;
   }
   for (;; r++) {
@@ -1026,6 +1036,10 @@ __global__ void __launch_bounds__(256) k_rebuild_fix(G g, u32 n, int full, u32* 
   if (tid == 0) {
     ctl->rounds = r;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ctl->t[1]));
+    // counters updated here, so the host reads them back with the control
+    // block (one sync per rebuild)
+    g.cnt->live -= ctl->dropped;
+    g.cnt->dirty = 0;
   }
   // every linked root's own analysis folds into its final root (set unions:
   // order free) under a per-root lock bit in its flags word; sources are
@@ -1148,6 +1162,9 @@ void Engine::rebuild(bool full) {
     CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_rebuild_fix, nb, 256, args, 0, s));
   }
   CUDA_OK(cudaMemcpyAsync(&hc_, small.p, sizeof(RbCtl), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaMemcpyAsync(&h, cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  DevError he;
+  CUDA_OK(cudaMemcpyAsync(&he, err.p, sizeof(he), cudaMemcpyDeviceToHost, s));
   sync();
   {
     // algorithmic bytes: a full round 60 N + 12 A; an
@@ -1168,12 +1185,9 @@ void Engine::rebuild(bool full) {
   hc_tombs += hc_.tombs;
   rb_rounds_last = hc_.rounds;
   rb_dirty_last = hc_.dirty_total;
-  h.live -= hc_.dropped;
-  h.dirty = 0;
   uf_changed = false;
-  push_counters();
-  check_error();  // syncs the stream
   snap.valid = false;
+  raise_error(he);
 }
 
 // ---------------------------------------------------------------- snapshot CSR

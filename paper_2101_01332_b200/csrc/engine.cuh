@@ -348,6 +348,7 @@ struct Engine {
   void pull_counters(const char* sf = __builtin_FILE(), int sl = __builtin_LINE());
   void push_counters();
   void check_error(const char* sf = __builtin_FILE(), int sl = __builtin_LINE());
+  void raise_error(const DevError& he);
   void sync(const char* sf = __builtin_FILE(), int sl = __builtin_LINE());
   std::map<std::string, long> sync_sites;  // TSAT_DEBUG_SYNCS: host syncs per call site
   void ensure_nodes(u64 extra_nodes, u64 extra_kids);
