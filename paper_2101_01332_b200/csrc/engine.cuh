@@ -319,6 +319,7 @@ struct Engine {
   DevBuf<u8> temp2;
   std::function<void()> overlap_hook;  // run once by the level peel right after its launch
   bool spec_ematch = false;            // the next iteration's e-matching is already done
+  bool levels_cached() const { return snap.valid && lv_snap == snap_id && lv_filter == filter_id; }
   void run_overlap_hook();
   DevBuf<u32> scratch_u32[8];
   DevBuf<DevStats> dstats;

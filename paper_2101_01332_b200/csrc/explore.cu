@@ -549,9 +549,6 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
   for (i64 it = 0; it < lim.k_max; it++) {
     if (!snap.valid) build_snapshot();
     tick(0, tp);
-    if (filter_mode == 2) build_reach();
-    else reach.valid = false;
-    tick(1, tp);
     std::vector<int> active;
     if (it < lim.k_multi) active = multi;
     active.insert(active.end(), single.begin(), single.end());
@@ -561,7 +558,27 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
     std::vector<int> todo;
     for (size_t p = 0; p < patterns.size(); p++)
       if (need[p]) todo.push_back((int)p);
-    if (spec_ematch) spec_ematch = false;  // done next to the previous iteration's peel
+    if (filter_mode == 2) {
+      // a pre-filter that needs a fresh peel (first iteration): this
+      // iteration's e-matching overlaps it (nothing here changes the filter)
+      if (!spec_ematch && overlap_ok && !levels_cached()) {
+        if (!s2) {
+          CUDA_OK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+          CUDA_OK(cudaEventCreateWithFlags(&ev_ov, cudaEventDisableTiming));
+        }
+        CUDA_OK(cudaEventRecord(ev_ov, s));
+        overlap_hook = [this, todo]() {
+          ematch_batch(todo);
+          spec_ematch = true;
+        };
+      }
+      build_reach();
+      overlap_hook = nullptr;
+    } else {
+      reach.valid = false;
+    }
+    tick(1, tp);
+    if (spec_ematch) spec_ematch = false;  // done next to a level peel
     else ematch_batch(todo);
     tick(2, tp);
     seq_changed = false;
