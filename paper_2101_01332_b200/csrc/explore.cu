@@ -19,6 +19,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
                    const CtaCtl* resume, const DevStats* resume_stats);
 void run_rules_chain(Engine& e, const std::vector<int>& rules, const std::vector<unsigned long long>& Ps,
                      int filter_mode, int allow_self, i64 n_max);
+u32 wave_cta_cap();
 
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -606,7 +607,7 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
       if (P == 0) continue;
       // (rules of <= 2048 positions: what the per-rule loop would run as one
       // single-CTA launch too; larger ones start on grid waves)
-      if (!no_chain && deadline < 0 && hr.nsrc == 1 && P <= 2048 && wave_path(ri, filter_mode)) {
+      if (!no_chain && deadline < 0 && hr.nsrc == 1 && P <= wave_cta_cap() && wave_path(ri, filter_mode)) {
         chain.push_back(ri);
         chainP.push_back(P);
         continue;

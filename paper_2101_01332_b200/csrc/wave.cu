@@ -26,6 +26,7 @@
 //                inserts.  The hazard combo itself runs on the exact
 //                sequential path (k_seq_rule) and the next wave starts after it.
 #include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -1268,50 +1269,179 @@ __device__ __forceinline__ unsigned long long gtimer() {
     t_last = t_;                          \
   }
 
+// control words of a wave loop (k_wave_cta): written by thread 0 of rank 0,
+// read by every thread after the next barrier
+struct WaveSh {
+  unsigned long long p, seg_end;
+  u32 ncand, jcur, exit, epoch, nacc, ncacc, base, kbase;
+  int rejoin_after;
+  u32 wres;  // soft writers resolved in the current wave
+  int abort;
+};
+
+template <int NC>
+__device__ __forceinline__ void wsync() {
+  if constexpr (NC > 1) cg::this_cluster().sync();
+  else __syncthreads();
+}
+
+// exclusive scan of f(i) over n elements, total at out[n]; NC > 1: each CTA
+// of the cluster scans one contiguous chunk, then adds the totals of the
+// chunks before it (read from the other CTAs' shared memory)
+template <int BT, class V, class F>
+__device__ __forceinline__ V chunk_scan(u32 lo, u32 hi, F f, V* carry_out) {
+  typedef cub::BlockScan<V, BT> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ V carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u32 base = lo; base < hi; base += BT) {
+    u32 i = base + threadIdx.x;
+    V v = i < hi ? f(i, (V)0, false) : (V)0, x, tot;
+    BS(tmp).ExclusiveSum(v, x, tot);
+    if (i < hi) f(i, carry + x, true);
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  V total = carry;
+  __syncthreads();
+  (void)carry_out;
+  return total;
+}
+
+template <int NC, class F>
+__device__ __forceinline__ u32 wscan(u32 n, u32* out, F f) {
+  if constexpr (NC == 1) {
+    return block_scan<CTA_T>(n, out, f);
+  } else {
+    cg::cluster_group cl = cg::this_cluster();
+    const u32 r = cl.block_rank(), chunk = (n + NC - 1) / NC;
+    const u32 lo = min(n, r * chunk), hi = min(n, lo + chunk);
+    __shared__ u32 s_ctot;
+    u32 t = chunk_scan<CTA_T, u32>(lo, hi, [&](u32 i, u32 x, bool wr) -> u32 {
+      if (wr) {
+        out[i] = x;
+        return 0u;
+      }
+      return f(i);
+    }, (u32*)nullptr);
+    if (threadIdx.x == 0) s_ctot = t;
+    cl.sync();
+    u32 off = 0, total = 0;
+    for (u32 q = 0; q < (u32)NC; q++) {
+      const u32 v = *cl.map_shared_rank(&s_ctot, q);
+      if (q < r) off += v;
+      total += v;
+    }
+    if (off)
+      for (u32 i = lo + threadIdx.x; i < hi; i += CTA_T) out[i] += off;
+    if (r == NC - 1 && threadIdx.x == 0) out[n] = total;
+    cl.sync();
+    return total;
+  }
+}
+
+template <int NC, class F>
+__device__ __forceinline__ void wscan2(u32 n, u32* out_a, u32* out_b, F f) {
+  if constexpr (NC == 1) {
+    block_scan2<CTA_T>(n, out_a, out_b, f);
+  } else {
+    cg::cluster_group cl = cg::this_cluster();
+    const u32 r = cl.block_rank(), chunk = (n + NC - 1) / NC;
+    const u32 lo = min(n, r * chunk), hi = min(n, lo + chunk);
+    __shared__ unsigned long long s_ctot2;
+    unsigned long long t = chunk_scan<CTA_T, unsigned long long>(
+        lo, hi, [&](u32 i, unsigned long long x, bool wr) -> unsigned long long {
+          if (wr) {
+            out_a[i] = (u32)(x >> 32);
+            out_b[i] = (u32)x;
+            return 0ull;
+          }
+          return f(i);
+        }, (unsigned long long*)nullptr);
+    if (threadIdx.x == 0) s_ctot2 = t;
+    cl.sync();
+    unsigned long long off = 0, total = 0;
+    for (u32 q = 0; q < (u32)NC; q++) {
+      const unsigned long long v = *cl.map_shared_rank(&s_ctot2, q);
+      if (q < r) off += v;
+      total += v;
+    }
+    if (off)
+      for (u32 i = lo + threadIdx.x; i < hi; i += CTA_T) {
+        const unsigned long long x = (((unsigned long long)out_a[i] << 32) | out_b[i]) + off;
+        out_a[i] = (u32)(x >> 32);
+        out_b[i] = (u32)x;
+      }
+    if (r == NC - 1 && threadIdx.x == 0) {
+      out_a[n] = (u32)(total >> 32);
+      out_b[n] = (u32)total;
+    }
+    cl.sync();
+  }
+}
+
+// NC = 1: one CTA, per-candidate arrays in shared memory when they fit.
+// NC > 1: a thread-block cluster of NC CTAs runs the same loop over NC x
+// larger windows: tid / nth span the cluster, phases end with cluster-wide
+// barriers (release / acquire: global writes of one phase are visible to the
+// next), the wave's control words live in rank 0's shared memory (read by
+// every CTA through distributed shared memory), the per-candidate arrays in
+// global memory (L2), and the accepted / allocation prefix sums are cluster
+// scans (per-CTA chunk scans + DSMEM totals).
+template <int NC>
 __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev RD, WaveRule W, WaveTab T, WaveIO io,
                                                        CtaArgs A, CtaCtl* ctl, const CtaCtl* prev) {
   extern __shared__ __align__(16) unsigned char wsm[];
   // per-candidate arrays in shared memory: each phase reads what the previous
   // one wrote, so this removes an L2 round trip from most phase chains
-  if (A.smem) wave_smem_layout(A.cta_win, W.R, wsm, &io);
-  __shared__ unsigned long long s_p, s_seg_end;
-  __shared__ u32 s_ncand, s_jcur, s_exit, s_epoch, s_nacc, s_ncacc, s_base, s_kbase;
-  __shared__ int s_rejoin_after;
-  __shared__ u32 s_wres;  // soft writers resolved in the current wave
-  const u64 tid = threadIdx.x, nth = CTA_T;
+  if (NC == 1 && A.smem) wave_smem_layout(A.cta_win, W.R, wsm, &io);
+  __shared__ WaveSh sh;
+  WaveSh* S = &sh;
+  u32 rank = 0;
+  if constexpr (NC > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    rank = cl.block_rank();
+    S = cl.map_shared_rank(&sh, 0);
+  }
+  const u64 tid = (u64)rank * CTA_T + threadIdx.x, nth = (u64)CTA_T * NC;
   unsigned long long t_last = tid == 0 ? gtimer() : 0;
-  __shared__ int s_abort;
   if (tid == 0) {
-    s_p = ctl->p;
-    s_jcur = ctl->jcursor;
-    s_epoch = ctl->epoch;
-    s_abort = 0;
+    S->p = ctl->p;
+    S->jcur = ctl->jcursor;
+    S->epoch = ctl->epoch;
+    S->abort = 0;
     // chained launch (run_rules_chain): runs only when the previous rule of
     // the chain finished (CR_DONE), continuing its wave epoch
     if (prev) {
       if (prev->reason != CR_DONE) {
-        s_abort = 1;
+        S->abort = 1;
         ctl->reason = CR_NOTRUN;
         ctl->epoch = prev->epoch;
       } else {
-        s_epoch = prev->epoch;
+        S->epoch = prev->epoch;
       }
     }
   }
-  __syncthreads();
-  if (s_abort) return;
+  wsync<NC>();
+  {
+    const int ab = S->abort;
+    wsync<NC>();  // rank 0 stays until every CTA has read its shared memory
+    if (ab) return;
+  }
   while (true) {
     if (tid == 0) {
-      s_exit = 0xFFFFFFFFu;
-      s_rejoin_after = 0;
-      unsigned long long p = s_p, P = ctl->P;
+      S->exit = 0xFFFFFFFFu;
+      S->rejoin_after = 0;
+      unsigned long long p = S->p, P = ctl->P;
       Counters* cn = g.cnt;
       if (p >= P) {
-        s_exit = CR_DONE;
+        S->exit = CR_DONE;
       } else if ((i64)cn->live >= A.n_max) {
         ctl->seq_stop = 1;
         ctl->overshoot = (i64)cn->live - A.n_max;
-        s_exit = CR_STOP;
+        S->exit = CR_STOP;
       } else {
         u32 win = ctl->win;
         u32 ncand;
@@ -1321,12 +1451,12 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
           ncand = (u32)n;
           seg_end = p + n;
         } else {
-          u32 remain = ctl->jtotal - s_jcur;
+          u32 remain = ctl->jtotal - S->jcur;
           ncand = remain < win ? remain : win;
-          if (ncand < remain) seg_end = A.pos[s_jcur + ncand];
+          if (ncand < remain) seg_end = A.pos[S->jcur + ncand];
           else if (!ctl->jcomplete) {
             seg_end = A.pos[ctl->jtotal - 1] + 1;
-            s_rejoin_after = 1;
+            S->rejoin_after = 1;
           }
         }
         if (ncand == 0) {
@@ -1334,82 +1464,82 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
           ctl->found += cover;
           ctl->self += self;
           ctl->compat += cover - self;
-          s_p = seg_end;
-          s_exit = s_rejoin_after ? CR_REJOIN : 0xFFFFFFFEu;  // continue
+          S->p = seg_end;
+          S->exit = S->rejoin_after ? CR_REJOIN : 0xFFFFFFFEu;  // continue
         } else {
           u64 need_n = (u64)cn->next_id + (u64)ncand * W.R + 2;
           u64 need_k = (u64)cn->nkids + (u64)ncand * A.Kmax + 2;
           if (need_n + 1 > g.cap_nodes || need_k + 1 > g.cap_kids || 2 * need_n > (u64)g.hc_mask + 1) {
-            s_exit = CR_CAPACITY;
+            S->exit = CR_CAPACITY;
           } else {
-            s_ncand = ncand;
-            s_seg_end = seg_end;
-            s_epoch += 1;
-            s_wres = 0;
+            S->ncand = ncand;
+            S->seg_end = seg_end;
+            S->epoch += 1;
+            S->wres = 0;
             ctl->waves += 1;
             io.stops[0] = io.stops[1] = io.stops[2] = io.stops[3] = TSAT_NONE;
           }
         }
       }
     }
-    __syncthreads();
+    wsync<NC>();
     {
-      u32 ex = s_exit;
-      __syncthreads();
+      u32 ex = S->exit;
+      wsync<NC>();
       if (ex == 0xFFFFFFFEu) continue;
       if (ex != 0xFFFFFFFFu) break;
     }
-    const u32 ncand = s_ncand;
+    const u32 ncand = S->ncand;
     WPROF(11);
-    const unsigned long long p = s_p;
-    const unsigned long long* posp = A.multi ? A.pos + s_jcur : nullptr;
+    const unsigned long long p = S->p;
+    const unsigned long long* posp = A.multi ? A.pos + S->jcur : nullptr;
     WaveTab Tw = T;
-    Tw.epoch = s_epoch;
+    Tw.epoch = S->epoch;
     // ---- gates + accepted list
     d_gates(tid, nth, g, R, RD, posp, ncand, p, io.status, io.env, io.olds, io.hazard);
-    __syncthreads();
+    wsync<NC>();
     WPROF(0);
     {
-      u32 tot = block_scan<CTA_T>(ncand, io.pre,
+      u32 tot = wscan<NC>(ncand, io.pre,
                                   [&](u32 c) { return (io.status[c] == 0 || io.hazard[c]) ? 1u : 0u; });
-      for (u32 c = tid; c < ncand; c += CTA_T)
+      for (u32 c = tid; c < ncand; c += nth)
         if (io.status[c] == 0 || io.hazard[c]) io.acc[io.pre[c]] = c;
-      if (tid == 0) s_nacc = tot;
-      __syncthreads();
+      if (tid == 0) S->nacc = tot;
+      wsync<NC>();
     }
     WPROF(1);
-    const u32 nacc = s_nacc;
+    const u32 nacc = S->nacc;
     // ---- resolve requests level by level
     if (W.R > 0) {
       for (int d = 1; d < A.nlv; d++) {
         if (!A.nlvl[d]) continue;
         d_resolve_claim(tid, nth, g, W, Tw, io.acc, nacc, io.lvl + A.lvl_off[d], A.nlvl[d], io.env, io.ident,
                         io.hazard);
-        __syncthreads();
+        wsync<NC>();
         d_resolve_verify(tid, nth, g, W, Tw, io.acc, nacc, io.lvl + A.lvl_off[d], A.nlvl[d], io.env, io.ident,
                          io.hazard);
-        __syncthreads();
+        wsync<NC>();
       }
       d_mark_roots(tid, nth, W, Tw, io.acc, nacc, io.ident, io.hazard, io.olds);
-      __syncthreads();
+      wsync<NC>();
     }
     WPROF(2);
     d_cand_check(tid, nth, g, W, Tw, io.acc, nacc, ncand, io.ident, io.env, io.olds, A.multi, io.hazard, io.alloc,
                  io.ukind, io.uother, io.grow, io.sa, io.akid);
-    __syncthreads();
+    wsync<NC>();
     WPROF(3);
     // ---- conflicts (re-run while the first one is a soft writer that
     // resolves), stop-after, node-limit cutoff, boundary
     for (int it = 0;; it++) {
-      const u32 fwep = s_epoch;
+      const u32 fwep = S->epoch;
       d_first_writer(tid, nth, W, fwep, io.acc, nacc, io.hazard, io.olds, io.ukind, io.uother, io.grow, io.fw_cls,
                      io.fw_fresh);
-      __syncthreads();
+      wsync<NC>();
       d_validity(tid, nth, W, Tw, fwep, R, RD, ncand, io.hazard, io.env, io.olds, io.pre, io.status, io.ident,
                  io.ukind, io.grow, io.uother, io.fw_cls, io.fw_fresh, io.stops + 2, io.stops + 3);
-      __syncthreads();
+      wsync<NC>();
       const u32 fb = io.stops[2], sw = io.stops[3];
-      __syncthreads();
+      wsync<NC>();
       if (sw == TSAT_NONE || sw >= fb) break;
       if (tid == 0) {
         if (it >= 64 || !d_resolve_soft(g, W, Tw, fwep, R, RD, sw, io.env, io.olds, io.pre, io.ukind, io.uother,
@@ -1417,48 +1547,48 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
           io.status[sw] = 3;  // ends the prefix
         else {
           ctl->resolved += 1;
-          s_wres += 1;
+          S->wres += 1;
         }
         io.stops[2] = io.stops[3] = TSAT_NONE;
-        s_epoch += 1;  // fresh first-writer tags
+        S->epoch += 1;  // fresh first-writer tags
       }
-      __syncthreads();
+      wsync<NC>();
     }
     WPROF(4);
-    block_scan2<CTA_T>(ncand, io.apre, io.ckpre,
+    wscan2<NC>(ncand, io.apre, io.ckpre,
                        [&](u32 c) { return ((unsigned long long)io.alloc[c] << 32) | io.akid[c]; });
     d_find_stops(tid, nth, io.acc, nacc, io.sa, io.apre, io.alloc, (i64)g.cnt->live, A.n_max, io.stops);
-    __syncthreads();
+    wsync<NC>();
     WPROF(5);
     if (tid == 0) {
-      d_boundary(io.ws, io.stops, ncand, posp, p, s_seg_end, io.pre, io.hazard);
+      d_boundary(io.ws, io.stops, ncand, posp, p, S->seg_end, io.pre, io.hazard);
 #ifdef WAVE_DBG
       if (io.stops[2] != TSAT_NONE && io.ws->ncommit_cand == io.stops[2] && (g_wdbg_first >> 8) == io.stops[2])
         g_wdbg_cnt[g_wdbg_first & 31] += 1;
       g_wdbg_first = ~0ull;
 #endif
-      s_ncacc = io.ws->ncommit_acc;
-      s_base = g.cnt->next_id;
-      s_kbase = g.cnt->nkids;
+      S->ncacc = io.ws->ncommit_acc;
+      S->base = g.cnt->next_id;
+      S->kbase = g.cnt->nkids;
     }
-    __syncthreads();
+    wsync<NC>();
     WPROF(6);
-    const u32 ncacc = s_ncacc;
+    const u32 ncacc = S->ncacc;
     d_seg_stats(tid, nth, io.status, io.ws, io.ws->ncommit_cand, io.pre, io.alloc, io.ukind, R.efficient, io.wstats);
     // ---- commit (requests of committed combos only)
     const u32 nwin = io.apre[ncacc], nk = io.ckpre[ncacc];
     if (nwin) {
-      d_assign_combos(tid, nth, W, Tw, ncacc, io.ident, io.apre, s_base);
-      __syncthreads();
-      d_write_combos(tid, nth, g, W, Tw, io.acc, ncacc, io.ident, io.apre, io.ckpre, s_base, s_kbase, io.env, io.olds);
-      __syncthreads();  // unions overwrite parent[] of fresh non-root nodes
+      d_assign_combos(tid, nth, W, Tw, ncacc, io.ident, io.apre, S->base);
+      wsync<NC>();
+      d_write_combos(tid, nth, g, W, Tw, io.acc, ncacc, io.ident, io.apre, io.ckpre, S->base, S->kbase, io.env, io.olds);
+      wsync<NC>();  // unions overwrite parent[] of fresh non-root nodes
     }
     WPROF(7);
     d_commit_unions(tid, nth, g, W, Tw, io.acc, ncacc, io.olds, io.ukind, io.uother, io.grow);
-    __syncthreads();
+    wsync<NC>();
     WPROF(8);
-    for (u32 i = tid; i < nwin; i += CTA_T) hc_insert(g, s_base + i);
-    __syncthreads();
+    for (u32 i = tid; i < nwin; i += nth) hc_insert(g, S->base + i);
+    wsync<NC>();
     WPROF(9);
     // ---- bookkeeping (thread 0)
     if (tid == 0) {
@@ -1480,8 +1610,8 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
       ctl->found += cover;
       ctl->self += self;
       ctl->compat += cover - self - ncommit;
-      if (A.multi) s_jcur += ncommit;
-      s_p = p_end;
+      if (A.multi) S->jcur += ncommit;
+      S->p = p_end;
       u32 exitr = 0xFFFFFFFFu;
       if (stop) {
         if (p_end < ctl->P) {
@@ -1499,31 +1629,31 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
           win = win * 4u;
           // a wave that needed soft-writer resolutions would be cut on the
           // grid path (which resolves only a few): stay here
-          if (s_wres) ctl->clean_full = 0;
+          if (S->wres) ctl->clean_full = 0;
           else if (ncand >= A.cta_win) ctl->clean_full += 1;
         }
         if (win > A.cta_win) win = A.cta_win;
         ctl->win = win;
         if (hazard) exitr = CR_HAZARD;
         else if (A.multi && ws->sa_hit) exitr = CR_REJOIN;
-        else if (s_rejoin_after) exitr = CR_REJOIN;
+        else if (S->rejoin_after) exitr = CR_REJOIN;
         else if (ctl->clean_full >= A.wide_after) exitr = CR_WIDE;
       }
-      s_exit = exitr;
+      S->exit = exitr;
     }
-    __syncthreads();
+    wsync<NC>();
     WPROF(10);
     {
-      u32 ex = s_exit;
-      __syncthreads();
+      u32 ex = S->exit;
+      wsync<NC>();
       if (ex != 0xFFFFFFFFu) break;
     }
   }
   if (tid == 0) {
-    ctl->p = s_p;
-    ctl->jcursor = s_jcur;
-    ctl->epoch = s_epoch;
-    ctl->reason = s_exit;
+    ctl->p = S->p;
+    ctl->jcursor = S->jcur;
+    ctl->epoch = S->epoch;
+    ctl->reason = S->exit;
   }
 }
 
@@ -1690,7 +1820,25 @@ static void accumulate_seg(Engine& e, int ri, const DevStats& d) {
 }
 
 
-#define CTA_WIN 2048u
+#define CTA_WIN_1 2048u
+// thread-block cluster size of the wave loop (TSAT_WAVE_CLUSTER: 1, 2, 4, 8
+// or 16) and the largest window it runs (one candidate per thread).  Default
+// 1: measured on BERT (scripts/cluster_sweep.sh), larger windows do not cut
+// the wave count -- waves end at the sequential-order conflicts (~1 per 2k
+// combos), and a bigger window only adds soft writers to the serial
+// resolution and L2 round trips (arrays leave shared memory): saturate
+// 10.5 ms at 1, 11.5 at 4, 12.4 at 8, 12.0 at 16.
+static int wave_nc() {
+  static int nc = -1;
+  if (nc < 0) {
+    const char* v = getenv("TSAT_WAVE_CLUSTER");
+    nc = v ? atoi(v) : 1;
+    if (nc != 1 && nc != 2 && nc != 4 && nc != 8 && nc != 16) nc = 1;
+  }
+  return nc;
+}
+u32 wave_cta_cap() { return wave_nc() > 1 ? (u32)wave_nc() * CTA_T : CTA_WIN_1; }
+#define CTA_WIN (wave_cta_cap())
 
 // per-candidate buffers, wave table and first-writer arrays for windows of up
 // to ncand candidates (grown only; fresh tag arrays are set to "no epoch")
@@ -1805,9 +1953,10 @@ static void ensure_wave_templates(Engine& e, WaveBufs& B) {
 // when they fit (a small window keeps most of the SM's L1 for the node table)
 #define CTA_WSMEM (160u << 10)
 static u32 cta_smem_win(int R) {
-  return wave_smem_layout(CTA_T, R, nullptr, nullptr) <= CTA_WSMEM ? CTA_T : 512u;
+  return wave_smem_layout(CTA_T, R, nullptr, nullptr) <= CTA_WSMEM ? (u32)CTA_T : 512u;
 }
 static void cta_fit_window(CtaCtl& c, int R) {
+  if (wave_nc() > 1) return;  // cluster windows: arrays in global memory
   u32 SWIN = cta_smem_win(R);
   if (wave_smem_layout(SWIN, R, nullptr, nullptr) <= CTA_WSMEM && c.win > SWIN) c.win = SWIN;
 }
@@ -1846,6 +1995,39 @@ static void cta_launch(Engine& e, WaveBufs& B, int ri, const RuleDev& Rd, const 
     A.wide_after = wa ? (u32)atoi(wa) : 8u;
   }
   A.pos = B.pos.p;
+  const int nc = wave_nc();
+  if (nc > 1) {
+    G gv = e.view();
+    A.smem = 0;
+    A.cta_win = (u32)nc * CTA_T;
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(nc, 1, 1);
+    cfg.blockDim = dim3(CTA_T, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = e.s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = nc;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    switch (nc) {
+      case 2: CUDA_OK(cudaLaunchKernelEx(&cfg, k_wave_cta<2>, gv, Rd, RD, W, T, io, A, dctl, prev)); break;
+      case 4: CUDA_OK(cudaLaunchKernelEx(&cfg, k_wave_cta<4>, gv, Rd, RD, W, T, io, A, dctl, prev)); break;
+      case 8: CUDA_OK(cudaLaunchKernelEx(&cfg, k_wave_cta<8>, gv, Rd, RD, W, T, io, A, dctl, prev)); break;
+      default: {
+        static int np_set = 0;
+        if (!np_set) {
+          CUDA_OK(cudaFuncSetAttribute(k_wave_cta<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+          np_set = 1;
+        }
+        CUDA_OK(cudaLaunchKernelEx(&cfg, k_wave_cta<16>, gv, Rd, RD, W, T, io, A, dctl, prev));
+      }
+    }
+    return;
+  }
   size_t smem_bytes = 0;
   {
     u32 SWIN = cta_smem_win(R);
@@ -1853,7 +2035,7 @@ static void cta_launch(Engine& e, WaveBufs& B, int ri, const RuleDev& Rd, const 
     if (need <= CTA_WSMEM) {
       static int smem_set = 0;
       if (!smem_set) {
-        CUDA_OK(cudaFuncSetAttribute(k_wave_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTA_WSMEM));
+        CUDA_OK(cudaFuncSetAttribute(k_wave_cta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTA_WSMEM));
         smem_set = 1;
       }
       A.smem = 1;
@@ -1861,7 +2043,7 @@ static void cta_launch(Engine& e, WaveBufs& B, int ri, const RuleDev& Rd, const 
       smem_bytes = need;
     }
   }
-  k_wave_cta<<<1, CTA_T, smem_bytes, e.s>>>(e.view(), Rd, RD, W, T, io, A, dctl, prev);
+  k_wave_cta<1><<<1, CTA_T, smem_bytes, e.s>>>(e.view(), Rd, RD, W, T, io, A, dctl, prev);
   CUDA_OK(cudaGetLastError());
 }
 
