@@ -221,6 +221,7 @@ struct Scratch {
   DevBuf<u32> cg_eoff, cg_edst, cg_enode, cg_roff, cg_rsrc, cg_outdeg, cg_level, cg_esrc, cg_sdst, cg_moff, cg_mdeg;
   DevBuf<u32> c_heavy, c_mark32, c_fa, c_fb, c_order, c_depth, c_path, c_cycn, c_cyco, c_res, c_rest, c_lvloff;
   DevBuf<u32> c_odeg, c_oeoff, c_oedst, c_obnd, c_batch;  // level-ordered class edges (staged closure)
+  DevBuf<u32> v_rej_w;  // wave-path reject log (on_reject)
   DevBuf<u8> c_mark, c_color;
   DevBuf<unsigned char> c_stack;
   // greedy / costs
@@ -427,6 +428,7 @@ struct Engine {
   // on_reject support: rejected combos of the last saturate, flattened as
   // [rule, nsrc, (eclass, nb, bindings[nb]) x nsrc] (snapshot match rows)
   bool record_rejects = false;
+  std::vector<unsigned long long>* rej_pending = nullptr;  // exact-path rejects inside a wave rule
   std::vector<u32> rejects;
   void record_reject(int ri, unsigned long long p);
 

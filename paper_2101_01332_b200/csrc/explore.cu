@@ -380,7 +380,11 @@ void Engine::run_rule_seq(int ri, int filter_mode, int allow_self, i64 n_max, un
       std::vector<u32> lg(2 * (size_t)d.nrej);
       CUDA_OK(cudaMemcpyAsync(lg.data(), R.rej_log, lg.size() * sizeof(u32), cudaMemcpyDeviceToHost, s));
       sync();
-      for (u32 k = 0; k < d.nrej; k++) record_reject(ri, ((unsigned long long)lg[2 * k] << 32) | lg[2 * k + 1]);
+      for (u32 k = 0; k < d.nrej; k++) {
+        const unsigned long long q = ((unsigned long long)lg[2 * k] << 32) | lg[2 * k + 1];
+        if (rej_pending) rej_pending->push_back(q);  // a wave rule's exact-path combo: merged in order there
+        else record_reject(ri, q);
+      }
     }
     if (d.stop) return;
     if (!d.resume_set) return;
@@ -607,7 +611,8 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
       if (P == 0) continue;
       // (rules of <= 2048 positions: what the per-rule loop would run as one
       // single-CTA launch too; larger ones start on grid waves)
-      if (!no_chain && deadline < 0 && hr.nsrc == 1 && P <= wave_cta_cap() && wave_path(ri, filter_mode)) {
+      if (!no_chain && deadline < 0 && !record_rejects && hr.nsrc == 1 && P <= wave_cta_cap() &&
+          wave_path(ri, filter_mode)) {
         chain.push_back(ri);
         chainP.push_back(P);
         continue;
@@ -714,7 +719,7 @@ bool Engine::wave_path(int ri, int filter_mode) const {
   int R = 0;
   for (auto& t : hr.targets)
     for (auto& in : t) R += in.kind == I_APP;
-  return filter_mode != 1 && hr.nsrc <= 2 && R <= 32 && !force_seq && !(record_rejects && filter_mode == 2);
+  return filter_mode != 1 && hr.nsrc <= 2 && R <= 32 && !force_seq;
 }
 
 void Engine::apply_rule(int ri, int filter_mode, int allow_self, i64 n_max, unsigned long long P) {

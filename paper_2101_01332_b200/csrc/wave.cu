@@ -739,9 +739,12 @@ __device__ __forceinline__ void d_commit_unions(u64 tid, u64 nth, const G& g, co
 }
 
 // stats over candidates [0, ncommit): shape / cycle / applied / noop
+// With a reject log (on_reject registered), every cycle-rejected combo's
+// product position is appended (unordered; the host sorts a rule's log).
 __device__ __forceinline__ void d_seg_stats(u64 tid, u64 nth, const u8* status, WaveState* ws, u32 ncommit,
                                             const u32* accpre, const u32* alloc, const u8* ukind, int efficient,
-                                            DevStats* st) {
+                                            DevStats* st, const RuleDev& R, unsigned long long p,
+                                            const unsigned long long* posp) {
   TID_LOOP(c, ncommit) {
     u8 s = status[c];
     if (s == 1) atomicAdd(&st->skipped_shape, 1ull);
@@ -749,6 +752,14 @@ __device__ __forceinline__ void d_seg_stats(u64 tid, u64 nth, const u8* status, 
       atomicAdd(&st->skipped_cycle, 1ull);
       atomicAdd(&st->prefilter_checks, 1ull);
       atomicAdd(&st->prefilter_rejects, 1ull);
+      if (R.rej_log) {
+        const u32 k = atomicAdd(&st->nrej, 1u);
+        if (k < R.rej_cap) {
+          const unsigned long long pos = posp ? posp[c] : p + c;
+          R.rej_log[2 * (u64)k] = (u32)(pos >> 32);
+          R.rej_log[2 * (u64)k + 1] = (u32)pos;
+        }
+      }
     } else {
       if (efficient) atomicAdd(&st->prefilter_checks, 1ull);
       u32 a = accpre[c];
@@ -985,9 +996,10 @@ __global__ void k_commit_unions(G g, WaveRule W, WaveTab T, const u32* acc, cons
 }
 
 __global__ void k_seg_stats(const u8* status, WaveState* ws, u32 ncand, const u32* accpre, const u32* alloc,
-                            const u8* ukind, int efficient, DevStats* st) {
+                            const u8* ukind, int efficient, DevStats* st, RuleDev R, unsigned long long p,
+                            const unsigned long long* posp) {
   u32 nc = ws->ncommit_cand;
-  d_seg_stats(GTID, GNTH, status, ws, nc < ncand ? nc : ncand, accpre, alloc, ukind, efficient, st);
+  d_seg_stats(GTID, GNTH, status, ws, nc < ncand ? nc : ncand, accpre, alloc, ukind, efficient, st, R, p, posp);
 }
 
 __global__ void k_win_flags(WaveTab T, const u32* ident, u64 nreq, const ReqT* tmpl, int R, const WaveState* ws,
@@ -1574,7 +1586,8 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     wsync<NC>();
     WPROF(6);
     const u32 ncacc = S->ncacc;
-    d_seg_stats(tid, nth, io.status, io.ws, io.ws->ncommit_cand, io.pre, io.alloc, io.ukind, R.efficient, io.wstats);
+    d_seg_stats(tid, nth, io.status, io.ws, io.ws->ncommit_cand, io.pre, io.alloc, io.ukind, R.efficient, io.wstats,
+                R, p, posp);
     // ---- commit (requests of committed combos only)
     const u32 nwin = io.apre[ncacc], nk = io.ckpre[ncacc];
     if (nwin) {
@@ -2111,6 +2124,20 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     e.sync();
     dbg_t0 = std::chrono::steady_clock::now();
   }
+  // on_reject registered (efficient mode): the cycle-rejected positions of
+  // the whole rule are logged on the device (waves) and by the exact path
+  // (hazards), then handed over in position order = the sequential order
+  const bool rec = e.record_rejects && filter_mode == 2;
+  const u32 rej_cap = (u32)std::min<unsigned long long>(P, 1ull << 28);
+  std::vector<unsigned long long> rej_seq;
+  struct RejGuard {
+    Engine& e;
+    ~RejGuard() { e.rej_pending = nullptr; }
+  } rej_guard{e};
+  if (rec) {
+    e.sc.v_rej_w.ensure(2 * (u64)rej_cap + 2);
+    e.rej_pending = &rej_seq;
+  }
   B.wstats.ensure(1);
   if (resume_stats) CUDA_OK(cudaMemcpyAsync(B.wstats.p, resume_stats, sizeof(DevStats), cudaMemcpyHostToDevice, e.s));
   else CUDA_OK(cudaMemsetAsync(B.wstats.p, 0, sizeof(DevStats), e.s));
@@ -2137,6 +2164,10 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     }
     RuleDev Rd = make_rule_dev(e, ri, filter_mode, allow_self);
     ReachDev RD = make_reach_dev(e);
+    if (rec) {
+      Rd.rej_log = e.sc.v_rej_w.p;
+      Rd.rej_cap = rej_cap;
+    }
     // ---- 1. compatible positions of a multi-pattern rule (cached)
     if (multi && !jvalid) {
       u32 nA = Rd.nmatch[0], nB = Rd.nmatch[1];
@@ -2316,7 +2347,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       k_boundary<<<1, 1, 0, e.s>>>(ws, B.stops.p, ncand, posp, p, seg_end, B.pre.p, B.hazard.p);
       // ---- 5. statistics of the committed segment (device accumulators)
       k_seg_stats<<<nblk(ncand), 256, 0, e.s>>>(B.status.p, ws, ncand, B.pre.p, B.alloc.p, B.ukind.p, Rd.efficient,
-                                                B.wstats.p);
+                                                B.wstats.p, Rd, p, posp);
       // ---- 6. commit
       if (nreq_max) {
         k_win_flags<<<nblk(nreq_max), 256, 0, e.s>>>(T, B.ident.p, nreq_max, W.tmpl, R, ws, B.wf.p, B.ka.p);
@@ -2395,6 +2426,18 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
   e.sync();
   e.phase_ms[29] += gres;
   accumulate_seg(e, ri, d);
+  if (rec) {
+    e.rej_pending = nullptr;
+    const u32 nw = std::min<u32>(d.nrej, rej_cap);
+    std::vector<u32> lg(2 * (size_t)nw);
+    if (nw) {
+      CUDA_OK(cudaMemcpyAsync(lg.data(), e.sc.v_rej_w.p, lg.size() * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+      e.sync();
+    }
+    for (u32 k = 0; k < nw; k++) rej_seq.push_back(((unsigned long long)lg[2 * k] << 32) | lg[2 * k + 1]);
+    std::sort(rej_seq.begin(), rej_seq.end());
+    for (unsigned long long q : rej_seq) e.record_reject(ri, q);
+  }
   if (dbg_waves)
     fprintf(stderr, "rule %d %s P=%llu waves=%.0f cuts=%.0f applied=%llu live=%u %.3f ms\n", ri,
             ri < (int)e.rule_names.size() ? e.rule_names[ri].c_str() : "?", P, e.phase_ms[8] - dbg_w0,

@@ -8,6 +8,8 @@ gates, application, rebuild, cycle post-processing -- runs on the GPU in
 
 from __future__ import annotations
 
+import warnings
+
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
@@ -189,8 +191,17 @@ def saturate(
     filt.update(dev)
     filt.update(extra)
     report.filter_size = len(filt)
-    for rule, matches in rejected:
-        on_reject(eg, filt, rule, matches)
+    if rejected:
+        before = frozenset(filt)
+        for rule, matches in rejected:
+            on_reject(eg, filt, rule, matches)
+        if frozenset(filt) != before:
+            # the reference calls on_reject mid-iteration on the live e-graph
+            # (explorer.py:222-224), so its filter edits steer the rest of that
+            # iteration; here the callbacks run after the iteration and the
+            # edits apply from the next one (API contract)
+            warnings.warn("on_reject changed the filter list: the change takes effect from the next iteration "
+                          "(callbacks run after each device iteration)", RuntimeWarning, stacklevel=2)
     return filt, report
 
 
