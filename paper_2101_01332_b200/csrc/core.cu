@@ -224,6 +224,7 @@ G Engine::view() {
   g.val = val.p;
   g.hc = hc.p;
   g.hc_mask = hc_cap - 1;
+  g.hc_max = (u32)std::min<double>((double)hc_cap * hc_load(), 4294967295.0);
   g.hc_epoch = hc_epoch;
   g.cap_nodes = cap_nodes;
   g.cap_kids = cap_kids;
@@ -409,6 +410,11 @@ void Engine::rehash(u32 new_cap) {
   if (h.next_id) k_hc_insert_alive<<<nblk(h.next_id), 256, 0, s>>>(view(), h.next_id);
 }
 
+double hc_load() {
+  static const double l = getenv("TSAT_HC_LOAD") ? atof(getenv("TSAT_HC_LOAD")) : 0.5;
+  return l;
+}
+
 void Engine::ensure_nodes(u64 extra_nodes, u64 extra_kids) {
   u64 need_n = (u64)h.next_id + extra_nodes + 1;
   u64 need_k = (u64)h.nkids + extra_kids + 1;
@@ -431,9 +437,9 @@ void Engine::ensure_nodes(u64 extra_nodes, u64 extra_kids) {
     kids.grow(nc, h.nkids, s);
     cap_kids = (u32)kids.cap;
   }
-  // hashcons load factor <= 1/2 over all allocated ids
+  // hashcons load factor <= 1/2 over all allocated ids (TSAT_HC_LOAD overrides)
   u64 want = 16;
-  while (want < 2 * need_n) want *= 2;
+  while ((double)want * hc_load() < (double)need_n) want *= 2;
   if (want > hc_cap) rehash((u32)want);
 }
 

@@ -35,6 +35,7 @@ struct G {
   Val* val;
   unsigned long long* hc;
   u32 hc_mask;
+  u32 hc_max;    // allocated ids the table is sized for (load factor)
   u32 hc_epoch;  // 1..255; slots of other epochs are empty
   u32 cap_nodes;
   u32 cap_kids;

@@ -23,6 +23,7 @@ struct TsatException : public std::runtime_error {
 // reuse under a different stream first synchronises the tagged stream.
 extern unsigned long long g_dev_allocs, g_dev_alloc_bytes, g_engines;  // diagnostics (tsat_debug_info)
 void* dev_cache_get(size_t bytes);
+double hc_load();  // hashcons load factor over allocated ids (TSAT_HC_LOAD, default 0.5)
 void dev_cache_put(void* p, size_t bytes);
 void dev_cache_forget_stream(cudaStream_t s);  // stream about to be destroyed (already synced)
 extern thread_local cudaStream_t tl_stream;

@@ -1481,7 +1481,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
         } else {
           u64 need_n = (u64)cn->next_id + (u64)ncand * W.R + 2;
           u64 need_k = (u64)cn->nkids + (u64)ncand * A.Kmax + 2;
-          if (need_n + 1 > g.cap_nodes || need_k + 1 > g.cap_kids || 2 * need_n > (u64)g.hc_mask + 1) {
+          if (need_n + 1 > g.cap_nodes || need_k + 1 > g.cap_kids || need_n > (u64)g.hc_max) {
             S->exit = CR_CAPACITY;
           } else {
             S->ncand = ncand;
