@@ -1183,6 +1183,7 @@ struct WaveIO {
 #define CR_WIDE 5     // clean full windows: continue on the grid path
 #define CR_ERROR 6    // analysis/table capacity error (exact path reports it)
 #define CR_NOTRUN 7   // chained launch skipped: an earlier rule of the chain returned to the host
+#define CR_NARROW 8   // grid-mode loop: windows shrank to single-CTA size
 
 struct CtaCtl {
   unsigned long long p, P;
@@ -1211,6 +1212,10 @@ struct CtaArgs {
   const unsigned long long* pos;  // cached join list (multi)
   int smem;  // per-candidate wave arrays in shared memory (window <= cta_win)
   u32 wide_after;  // clean full windows before handing over to the grid path
+  // grid mode (NC == 0): control words and per-block scan totals in global memory
+  void* gsh;
+  unsigned long long* gtot;
+  u32 narrow_win;  // grid mode: a window this small goes back to the single-CTA loop
 };
 
 // shared-memory carve-out of the per-candidate wave arrays (window of `win`
@@ -1294,8 +1299,11 @@ struct WaveSh {
 template <int NC>
 __device__ __forceinline__ void wsync() {
   if constexpr (NC > 1) cg::this_cluster().sync();
+  else if constexpr (NC == 0) cg::this_grid().sync();
   else __syncthreads();
 }
+
+
 
 // exclusive scan of f(i) over n elements, total at out[n]; NC > 1: each CTA
 // of the cluster scans one contiguous chunk, then adds the totals of the
@@ -1322,10 +1330,52 @@ __device__ __forceinline__ V chunk_scan(u32 lo, u32 hi, F f, V* carry_out) {
   return total;
 }
 
+// grid mode (NC == 0): one chunk per block; block totals meet in global
+// memory.  Returns the exclusive offset of this block's chunk [lo, hi) and
+// the total; the caller adds the offset, then syncs the grid.
+template <class V, class F, class W>
+__device__ __forceinline__ V grid_chunk_scan(u32 n, F f, W wr, unsigned long long* gtot, u32& lo, u32& hi, V& off) {
+  cg::grid_group gg = cg::this_grid();
+  const u32 nb = gridDim.x, r = blockIdx.x, chunk = (n + nb - 1) / nb;
+  lo = min(n, r * chunk);
+  hi = min(n, lo + chunk);
+  V t = chunk_scan<CTA_T, V>(lo, hi, [&](u32 i, V x, bool w) -> V {
+    if (w) {
+      wr(i, x);
+      return (V)0;
+    }
+    return f(i);
+  }, (V*)nullptr);
+  if (threadIdx.x == 0) gtot[r] = (unsigned long long)t;
+  gg.sync();
+  __shared__ unsigned long long s_off, s_total;
+  if (threadIdx.x == 0) {
+    unsigned long long o = 0, total = 0;
+    for (u32 q = 0; q < nb; q++) {
+      const unsigned long long v = ((volatile unsigned long long*)gtot)[q];
+      if (q < r) o += v;
+      total += v;
+    }
+    s_off = o;
+    s_total = total;
+  }
+  __syncthreads();
+  off = (V)s_off;
+  return (V)s_total;
+}
+
 template <int NC, class F>
-__device__ __forceinline__ u32 wscan(u32 n, u32* out, F f) {
+__device__ __forceinline__ u32 wscan(u32 n, u32* out, F f, unsigned long long* gtot = nullptr) {
   if constexpr (NC == 1) {
     return block_scan<CTA_T>(n, out, f);
+  } else if constexpr (NC == 0) {
+    u32 lo, hi, off;
+    const u32 total = grid_chunk_scan<u32>(n, f, [&](u32 i, u32 x) { out[i] = x; }, gtot, lo, hi, off);
+    if (off)
+      for (u32 i = lo + threadIdx.x; i < hi; i += CTA_T) out[i] += off;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = total;
+    cg::this_grid().sync();
+    return total;
   } else {
     cg::cluster_group cl = cg::this_cluster();
     const u32 r = cl.block_rank(), chunk = (n + NC - 1) / NC;
@@ -1355,9 +1405,30 @@ __device__ __forceinline__ u32 wscan(u32 n, u32* out, F f) {
 }
 
 template <int NC, class F>
-__device__ __forceinline__ void wscan2(u32 n, u32* out_a, u32* out_b, F f) {
+__device__ __forceinline__ void wscan2(u32 n, u32* out_a, u32* out_b, F f, unsigned long long* gtot = nullptr) {
   if constexpr (NC == 1) {
     block_scan2<CTA_T>(n, out_a, out_b, f);
+  } else if constexpr (NC == 0) {
+    u32 lo, hi;
+    unsigned long long off;
+    const unsigned long long total = grid_chunk_scan<unsigned long long>(
+        n, f,
+        [&](u32 i, unsigned long long x) {
+          out_a[i] = (u32)(x >> 32);
+          out_b[i] = (u32)x;
+        },
+        gtot, lo, hi, off);
+    if (off)
+      for (u32 i = lo + threadIdx.x; i < hi; i += CTA_T) {
+        const unsigned long long x = (((unsigned long long)out_a[i] << 32) | out_b[i]) + off;
+        out_a[i] = (u32)(x >> 32);
+        out_b[i] = (u32)x;
+      }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+      out_a[n] = (u32)(total >> 32);
+      out_b[n] = (u32)total;
+    }
+    cg::this_grid().sync();
   } else {
     cg::cluster_group cl = cg::this_cluster();
     const u32 r = cl.block_rank(), chunk = (n + NC - 1) / NC;
@@ -1416,8 +1487,11 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     cg::cluster_group cl = cg::this_cluster();
     rank = cl.block_rank();
     S = cl.map_shared_rank(&sh, 0);
+  } else if constexpr (NC == 0) {  // cooperative grid: control words in global memory
+    rank = blockIdx.x;
+    S = (WaveSh*)A.gsh;
   }
-  const u64 tid = (u64)rank * CTA_T + threadIdx.x, nth = (u64)CTA_T * NC;
+  const u64 tid = (u64)rank * CTA_T + threadIdx.x, nth = (u64)CTA_T * (NC == 0 ? gridDim.x : NC);
   unsigned long long t_last = tid == 0 ? gtimer() : 0;
   if (tid == 0) {
     S->p = ctl->p;
@@ -1513,7 +1587,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     WPROF(0);
     {
       u32 tot = wscan<NC>(ncand, io.pre,
-                                  [&](u32 c) { return (io.status[c] == 0 || io.hazard[c]) ? 1u : 0u; });
+                          [&](u32 c) { return (io.status[c] == 0 || io.hazard[c]) ? 1u : 0u; }, A.gtot);
       for (u32 c = tid; c < ncand; c += nth)
         if (io.status[c] == 0 || io.hazard[c]) io.acc[io.pre[c]] = c;
       if (tid == 0) S->nacc = tot;
@@ -1554,7 +1628,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
       wsync<NC>();
       if (sw == TSAT_NONE || sw >= fb) break;
       if (tid == 0) {
-        if (it >= 64 || !d_resolve_soft(g, W, Tw, fwep, R, RD, sw, io.env, io.olds, io.pre, io.ukind, io.uother,
+        if (it >= (NC == 0 ? 4 : 64) || !d_resolve_soft(g, W, Tw, fwep, R, RD, sw, io.env, io.olds, io.pre, io.ukind, io.uother,
                                          io.grow, io.fw_cls, io.fw_fresh))
           io.status[sw] = 3;  // ends the prefix
         else {
@@ -1568,7 +1642,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
     }
     WPROF(4);
     wscan2<NC>(ncand, io.apre, io.ckpre,
-                       [&](u32 c) { return ((unsigned long long)io.alloc[c] << 32) | io.akid[c]; });
+               [&](u32 c) { return ((unsigned long long)io.alloc[c] << 32) | io.akid[c]; }, A.gtot);
     d_find_stops(tid, nth, io.acc, nacc, io.sa, io.apre, io.alloc, (i64)g.cnt->live, A.n_max, io.stops);
     wsync<NC>();
     WPROF(5);
@@ -1651,6 +1725,7 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
         else if (A.multi && ws->sa_hit) exitr = CR_REJOIN;
         else if (S->rejoin_after) exitr = CR_REJOIN;
         else if (ctl->clean_full >= A.wide_after) exitr = CR_WIDE;
+        else if (NC == 0 && win <= A.narrow_win) exitr = CR_NARROW;
       }
       S->exit = exitr;
     }
@@ -1708,6 +1783,7 @@ struct WaveBufs {
   DevBuf<int> lvl_all;
   CtaCtl* hctl = nullptr;       // pinned
   Counters* hcnt = nullptr;     // pinned
+  DevBuf<unsigned long long> gsh, gtot;  // grid-mode control words / block totals
   // chained single-CTA launches (run_rules_chain)
   DevBuf<CtaCtl> chain_ctl;
   DevBuf<DevStats> chain_stats;
@@ -2060,6 +2136,70 @@ static void cta_launch(Engine& e, WaveBufs& B, int ri, const RuleDev& Rd, const 
   CUDA_OK(cudaGetLastError());
 }
 
+// grid mode: the same wave loop as one cooperative launch over all SMs (one
+// 1024-thread CTA per SM, windows up to 148 x 1024 candidates), replacing the
+// host-driven grid waves (about 20 launches and a host round trip per wave)
+static int grid_blocks() {
+  static int nb = 0;
+  if (!nb) {
+    int per_sm = 0, nsm = 0, dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wave_cta<0>, CTA_T, 0));
+    nb = std::max(1, per_sm) * nsm;
+  }
+  return nb;
+}
+// Opt-in (TSAT_WAVE_GRID=1): measured no faster than the host-driven grid
+// waves -- ~20 grid-wide barriers per wave cost about what the launches did
+// (BERT saturate 10.6 vs 10.4 ms, configs[4] apply 11.5 vs 11.7 ms).
+static bool grid_mode_on() {
+  static const int on = getenv("TSAT_WAVE_GRID") ? atoi(getenv("TSAT_WAVE_GRID")) : 0;
+  return on != 0;
+}
+u32 wave_grid_cap() { return (u32)grid_blocks() * CTA_T; }
+
+static void grid_launch(Engine& e, WaveBufs& B, int ri, const RuleDev& Rd, const ReachDev& RD, int skip_self,
+                        bool multi, i64 n_max, CtaCtl* dctl) {
+  WaveBufs::RuleWave& RWc = B.rw[ri];
+  WaveRule W = RWc.W;
+  const std::vector<std::vector<int>>& lv = RWc.lv;
+  W.tmpl = B.tmpl_all.p + RWc.tmpl_base;
+  WaveTab T{B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0, B.wtag.p, B.wown.p};
+  WaveIO io{B.status.p, B.hazard.p, B.ukind.p, B.grow.p, B.sa.p, B.env.p, B.olds.p, B.pre.p, B.acc.p,
+            B.ident.p, B.alloc.p, B.apre.p, B.wf.p, B.wpre.p, B.ka.p, B.kpre.p, B.uother.p, B.stops.p,
+            B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, B.lvl_all.p + RWc.lvl_base};
+  CtaArgs A;
+  memset(&A, 0, sizeof(A));
+  A.nlv = (int)lv.size();
+  for (size_t d = 0; d < lv.size(); d++) {
+    A.lvl_off[d] = RWc.lvl_off[d];
+    A.nlvl[d] = (int)lv[d].size();
+  }
+  A.skip_self = skip_self;
+  A.multi = multi ? 1 : 0;
+  A.Kmax = RWc.Kmax;
+  A.nA = Rd.nmatch[0];
+  A.nB = multi ? Rd.nmatch[1] : 1;
+  A.n_max = n_max;
+  const int nb = grid_blocks();
+  A.cta_win = (u32)nb * CTA_T;
+  A.wide_after = 0xffffffffu;
+  A.narrow_win = CTA_WIN_1;
+  A.pos = B.pos.p;
+  A.smem = 0;
+  B.gsh.ensure(sizeof(WaveSh) / 8 + 2);
+  B.gtot.ensure((u64)nb + 2);
+  A.gsh = B.gsh.p;
+  A.gtot = B.gtot.p;
+  G gv = e.view();
+  RuleDev R = Rd;
+  ReachDev RDv = RD;
+  const CtaCtl* prev = nullptr;
+  void* args[] = {&gv, &R, &RDv, &W, &T, &io, &A, &dctl, &prev};
+  CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_wave_cta<0>, nb, CTA_T, args, 0, e.s));
+}
+
 // host side of a single-CTA run's return (its control block c): statistics,
 // resume position, and the reason's follow-up.  Returns true when the rule's
 // loop must stop (node limit / stop inside the exact path).
@@ -2236,6 +2376,43 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       if (dbg_waves)
         fprintf(stderr, "   cta: reason %u waves %u cand %llu resolved %u p %llu/%llu prof %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f %.3f | %.3f ms\n", c.reason, c.waves,
                 c.s_cand, c.resolved, c.p, P, c.prof[0]*1e-6, c.prof[1]*1e-6, c.prof[2]*1e-6, c.prof[3]*1e-6, c.prof[4]*1e-6, c.prof[5]*1e-6, c.prof[6]*1e-6, c.prof[7]*1e-6, c.prof[8]*1e-6, c.prof[9]*1e-6, c.prof[10]*1e-6, c.prof[11]*1e-6,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0).count());
+      if (cta_exit(e, B, ri, c, p, jcursor, win, jvalid, multi, filter_mode, allow_self, n_max)) break;
+      continue;
+    }
+    if (grid_mode_on()) {
+      // ---- cooperative grid-wide run of waves (one launch, no host round
+      // trip per wave); back here on hazards, capacity, stops, or when the
+      // window shrinks to single-CTA size
+      const u32 gcap = wave_grid_cap();
+      const u64 wmax = std::min<u64>(std::min<u64>(remain, (u64)win * 4), gcap);
+      e.ensure_nodes(wmax * R + 2, wmax * Kmax + 2);
+      ensure_cand_bufs(e, B, gcap, R);
+      CtaCtl c;
+      memset(&c, 0, sizeof(c));
+      c.p = p;
+      c.P = P;
+      c.win = std::min<u32>(win, gcap);
+      c.epoch = B.epoch;
+      c.jcursor = jcursor;
+      c.jtotal = jtotal;
+      c.jcomplete = jcomplete ? 1 : 0;
+      c.reason = CR_DONE;
+      *B.hctl = c;
+      CUDA_OK(cudaMemcpyAsync(B.ctl.p, B.hctl, sizeof(c), cudaMemcpyHostToDevice, e.s));
+      {
+        KTimer kt(e, KG_APPLY_WAVE, 0.0, 1);
+        grid_launch(e, B, ri, Rd, RD, skip_self, multi, n_max, B.ctl.p);
+        CUDA_OK(cudaMemcpyAsync(B.hctl, B.ctl.p, sizeof(c), cudaMemcpyDeviceToHost, e.s));
+        CUDA_OK(cudaMemcpyAsync(B.hcnt, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
+        e.sync();
+        c = *B.hctl;
+        e.h = *B.hcnt;
+        kt.bytes = wave_bytes(e, Rd, (double)c.s_cand, (double)c.s_req, (double)c.s_win, (double)c.s_nk);
+      }
+      if (dbg_waves)
+        fprintf(stderr, "   gridloop: reason %u waves %u cand %llu resolved %u p %llu/%llu win %u | %.3f ms\n", c.reason,
+                c.waves, c.s_cand, c.resolved, c.p, P, c.win,
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0).count());
       if (cta_exit(e, B, ri, c, p, jcursor, win, jvalid, multi, filter_mode, allow_self, n_max)) break;
       continue;
