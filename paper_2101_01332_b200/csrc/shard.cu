@@ -108,11 +108,14 @@ void Engine::shard_teardown() {
   host_ctx = nullptr;
   if (comm) {
     sync();
+    // the communicator stays cached for the process: the next e-graph of the
+    // same group (bench steps, repeated explores) reuses it -- an NCCL unique
+    // id must not be used for a second ncclCommInitRank once its bootstrap
+    // has completed, so destroying here would make that re-init hang
     auto& cc = comm_cache();
     for (size_t i = 0; i < cc.size(); i++)
-      if ((void*)cc[i].comm == comm && --cc[i].refs == 0) {
-        nccl().CommDestroy(cc[i].comm);
-        cc.erase(cc.begin() + i);
+      if ((void*)cc[i].comm == comm) {
+        if (cc[i].refs > 0) cc[i].refs--;
         break;
       }
     comm = nullptr;
