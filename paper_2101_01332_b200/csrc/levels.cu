@@ -454,7 +454,10 @@ static int coop_blocks(Engine& e, const void* fn, int threads) {
 }
 
 // runs the frontier to completion; returns (levels, total processed)
-static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& total, u32 ne_known = TSAT_NONE) {
+// lvl_host (optional, >= F.n + 2 entries): the level offsets come back with
+// the final control read (one host sync instead of two)
+static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& total, u32 ne_known = TSAT_NONE,
+                         u32* lvl_host = nullptr) {
   DevBuf<u32>& ctl = e.sc.c_res;
   ctl.ensure(16);
   CUDA_OK(cudaMemsetAsync(ctl.p, 0, 16 * sizeof(u32), e.s));
@@ -482,18 +485,22 @@ static void run_frontier(Engine& e, Frontier F, u32 root, u32& nlevels, u32& tot
     CUDA_OK(cudaFuncSetAttribute(k_frontier_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FR_SMEM));
     smem_set = 1;
   }
+  auto read_ctl = [&]() {
+    CUDA_OK(cudaMemcpyAsync(h, ctl.p, 5 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+    if (lvl_host && F.lvl_off)
+      CUDA_OK(cudaMemcpyAsync(lvl_host, F.lvl_off, ((u64)F.n + 2) * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+    e.sync();
+  };
   while (true) {
     k_frontier_block<<<1, LV_BLOCK, smem_bytes, e.s>>>(F, ctl.p, use_smem);
     if (!F.bfs) e.run_overlap_hook();  // overlap work runs while the peel does
-    CUDA_OK(cudaMemcpyAsync(h, ctl.p, 5 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-    e.sync();
+    read_ctl();
     if (h[4]) break;
     u32* c = ctl.p;
     u32* hv = heavy.p;
     void* args[] = {&F, &c, &hv};
     CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_frontier_grid, gblocks, 256, args, 0, e.s));
-    CUDA_OK(cudaMemcpyAsync(h, ctl.p, 5 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-    e.sync();
+    read_ctl();
     if (h[4]) break;
   }
   nlevels = h[1];
@@ -715,18 +722,19 @@ u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrim
     e.run_overlap_hook();  // work queued for the overlap stream runs while the peel does
     u32 hc[4];
     CUDA_OK(cudaMemcpyAsync(hc, ctl.p, 4 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+    lvl_off.resize((size_t)n + 2);
+    CUDA_OK(cudaMemcpyAsync(lvl_off.data(), X.c_lvloff.p, ((u64)n + 2) * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
     e.sync();
     static const bool dbg = getenv("TSAT_DEBUG_LEVELS") != nullptr;
     if (dbg) fprintf(stderr, "peel_async: n %u ne %u walk %.1f us sort %.1f us\n", n, e.cg_ne, hc[2] * 1e-3, hc[3] * 1e-3);
     tot = hc[0];
     nl = hc[1];
   } else {
-    run_frontier(e, F, 0, nl, tot, e.cg_ne);  // class graph: reverse edges = forward edges
+    lvl_off.resize((size_t)n + 2);
+    run_frontier(e, F, 0, nl, tot, e.cg_ne, lvl_off.data());  // class graph: reverse edges = forward edges
   }
   ntrimmed = tot;
-  lvl_off.resize(nl + 1);
-  CUDA_OK(cudaMemcpyAsync(lvl_off.data(), X.c_lvloff.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-  e.sync();
+  lvl_off.resize(nl + 1);  // offsets [0, nl] came back with the final control read
   return nl;
 }
 
