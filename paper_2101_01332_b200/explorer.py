@@ -134,8 +134,8 @@ def saturate(
     cycle-rejected combo (rule + snapshot Match per source, in rejection
     order) and the callbacks run after each iteration (the search is driven
     one iteration at a time), with the e-graph as that iteration left it; the
-    live mid-iteration e-graph never leaves the GPU.  Recording routes
-    efficient-mode rules through the exact sequential path."""
+    live mid-iteration e-graph never leaves the GPU.  Recording keeps the
+    wave path (rejected positions are logged on the device)."""
     limits = limits or ExploreLimits()
     if filter_mode not in FILTER_MODES:
         raise ValueError(f"filter_mode must be one of {FILTER_MODES}")

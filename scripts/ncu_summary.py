@@ -15,8 +15,14 @@ from launch_table import load  # noqa: E402
 T, B_R, B_W, HIT = "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct"
 
 
-def region(path):
+def region(path, start_at=None):
+    """Summed time / DRAM bytes of the launches in a region CSV; start_at = the
+    first kernel name prefix that belongs to the group (earlier launches, e.g.
+    the snapshot rebuilt after a rule load, are left out)."""
     L = load(path)
+    if start_at:
+        first = next((i for i, x in enumerate(L) if x["name"].startswith(start_at)), 0)
+        L = L[first:]
     t = sum(x.get(T, 0) for x in L) / 1e9
     by = sum(x.get(B_R, 0) + x.get(B_W, 0) for x in L)
     per = collections.OrderedDict()
@@ -44,7 +50,7 @@ def main(d, out):
     for r in ("ematch", "rebuild_forced", "rebuild_cascade", "costs", "greedy"):
         p = os.path.join(d, f"launches_10m_{r}.csv")
         if os.path.exists(p):
-            res["ematch_13" if r == "ematch" else r] = region(p)
+            res["ematch_13" if r == "ematch" else r] = region(p, "k_em_" if r == "ematch" else None)
     p = os.path.join(d, "launches_bert.csv")
     if os.path.exists(p):
         b = region(p)

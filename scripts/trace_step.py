@@ -69,3 +69,17 @@ for d, n in gaps:
 print("idle before (top):")
 for k, d in gh.most_common(15):
     print(f"  {k:50s} {d / 1e3:8.3f} ms")
+# the biggest single gaps with the operations around them
+print("largest gaps:")
+last_end, prev = ks[0][0], ""
+gl = []
+for a, b, n in ks:
+    if a > last_end:
+        gl.append((a - last_end, prev, n))
+    if b > last_end:
+        last_end, prev = b, n
+for d, p0, n in sorted(gl, reverse=True)[:25]:
+    print(f"  {d:8.1f} us  after {p0.split('(')[0][:40]:40s} before {n.split('(')[0][:40]}")
+print("gap histogram (us): ", {k: sum(1 for d, _, _ in gl if lo <= d < hi) for k, (lo, hi) in
+      {"<5": (0, 5), "5-10": (5, 10), "10-20": (10, 20), "20-50": (20, 50), ">50": (50, 1e9)}.items()},
+      "total", round(sum(d for d, _, _ in gl) / 1e3, 3), "ms")
