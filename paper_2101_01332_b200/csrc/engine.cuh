@@ -1,5 +1,6 @@
 // Host-side engine object behind one C-ABI handle (include/tsat.h).
 #pragma once
+#include <chrono>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -23,7 +24,11 @@ struct TsatException : public std::runtime_error {
 // reuse under a different stream first synchronises the tagged stream.
 extern unsigned long long g_dev_allocs, g_dev_alloc_bytes, g_engines;  // diagnostics (tsat_debug_info)
 void* dev_cache_get(size_t bytes);
-double hc_load();  // hashcons load factor over allocated ids (TSAT_HC_LOAD, default 0.5)
+double hc_load();
+inline double now_s() {  // host monotonic clock (s): time limits
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+  // hashcons load factor over allocated ids (TSAT_HC_LOAD, default 0.5)
 void dev_cache_put(void* p, size_t bytes);
 void dev_cache_forget_stream(cudaStream_t s);  // stream about to be destroyed (already synced)
 extern thread_local cudaStream_t tl_stream;
@@ -148,6 +153,7 @@ struct DevStats {
   unsigned long long resume_pos;
   u32 vpend;       // vanilla: combo at resume_pos awaits its apply-on-checkpoint check
   u32 nrej;        // entries written to RuleDev::rej_log
+  u32 timeout;     // the device deadline passed before the next combo
 };
 
 struct Snapshot {
@@ -417,6 +423,8 @@ struct Engine {
   bool seq_changed = false, seq_stop = false;
   bool seq_timeout = false;      // vanilla: deadline passed between combos
   double apply_deadline = -1.0;  // saturate's deadline (now_s clock), < 0: none
+  unsigned long long dev_deadline_ns = 0;  // the same deadline on the device clock (%globaltimer)
+  void set_device_deadline(double deadline_s);
   bool force_seq = false;  // debug: exact sequential path only
   std::vector<std::string> rule_names;
   bool wave_path(int ri, int filter_mode) const;

@@ -21,9 +21,6 @@ void run_rules_chain(Engine& e, const std::vector<int>& rules, const std::vector
                      int filter_mode, int allow_self, i64 n_max);
 u32 wave_cta_cap();
 
-static double now_s() {
-  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
 
 // ---------------------------------------------------------------- rule loading
 
@@ -155,7 +152,25 @@ RuleDev make_rule_dev(Engine& e, int ri, int filter_mode, int allow_self) {
   R.max_kids = mk;
   R.instr = e.d_instr.p;
   R.leaf = e.d_leaf.p;
+  R.deadline_ns = e.apply_deadline >= 0 ? e.dev_deadline_ns : 0ull;
   return R;
+}
+
+__global__ void k_dev_now(unsigned long long* out) { *out = dev_now_ns(); }
+
+// the saturate deadline on the device clock: one clock read-back to map the
+// host's now_s() onto %globaltimer
+void Engine::set_device_deadline(double deadline_s) {
+  dev_deadline_ns = 0;
+  if (deadline_s < 0) return;
+  DevBuf<unsigned long long> t;
+  t.alloc(1);
+  unsigned long long hd = 0;
+  k_dev_now<<<1, 1, 0, s>>>(t.p);
+  CUDA_OK(cudaMemcpyAsync(&hd, t.p, sizeof(hd), cudaMemcpyDeviceToHost, s));
+  sync();
+  const double left = deadline_s - now_s();
+  dev_deadline_ns = left <= 0 ? 1ull : hd + (unsigned long long)(left * 1e9);
 }
 
 ReachDev make_reach_dev(Engine& e) {
@@ -192,9 +207,15 @@ __global__ void k_seq_rule(G g, RuleDev R, ReachDev RD, DevStats* st, unsigned l
   u32 env[MAX_VARS];
   for (unsigned long long p = p0; p < p1; p++) {
     if ((u64)c->next_id + R.max_req + 2 > g.cap_nodes || (u64)c->nkids + R.max_kids + 2 > g.cap_kids ||
-        2ull * ((u64)c->next_id + R.max_req + 2) > (u64)g.hc_mask + 1) {
+        (u64)c->next_id + R.max_req + 2 > (u64)g.hc_max) {
       st->resume_set = 1;
       st->resume_pos = p;
+      return;
+    }
+    // the time limit, checked before every combo like the reference
+    // (explorer.py:198-201) through the device clock
+    if (R.deadline_ns && dev_now_ns() > R.deadline_ns) {
+      st->timeout = 1;
       return;
     }
     if ((i64)c->live >= n_max) {
@@ -369,6 +390,7 @@ void Engine::run_rule_seq(int ri, int filter_mode, int allow_self, i64 n_max, un
       seq_stop = true;
       report.node_limit_overshoot = d.overshoot;
     }
+    if (d.timeout) seq_timeout = true;
     try {
       check_error();
     } catch (TsatException& ex) {
@@ -386,7 +408,7 @@ void Engine::run_rule_seq(int ri, int filter_mode, int allow_self, i64 n_max, un
         else record_reject(ri, q);
       }
     }
-    if (d.stop) return;
+    if (d.stop || d.timeout) return;
     if (!d.resume_set) return;
     p = d.resume_pos;
     ensure_nodes(4096 + (u64)R.max_req * 64, 4096 + (u64)R.max_kids * 64);
@@ -463,6 +485,10 @@ void Engine::run_rule_vanilla(int ri, int allow_self, i64 n_max, unsigned long l
       report.node_limit_overshoot = d.overshoot;
       return;
     }
+    if (d.timeout) {
+      seq_timeout = true;
+      return;
+    }
     if (d.resume_set) {  // capacity
       p = d.resume_pos;
       ensure_nodes(4096 + (u64)R.max_req * 64, 4096 + (u64)R.max_kids * 64);
@@ -521,6 +547,7 @@ void Engine::run_rule_vanilla(int ri, int allow_self, i64 n_max, unsigned long l
 void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self, const int*, int) {
   double t0 = now_s();
   double deadline = lim.time_limit_s < 0 ? -1.0 : t0 + lim.time_limit_s;
+  set_device_deadline(deadline);
   memset(&report, 0, sizeof(report));
   rstats.assign(rules.size(), RuleStatsH());
   enodes_per_iter.clear();

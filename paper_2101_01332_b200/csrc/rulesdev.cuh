@@ -17,7 +17,14 @@ struct RuleDev {
   unsigned long long vanilla_go;   // ... except at this position (apply it)
   u32* rej_log;                    // efficient-mode reject positions (on_reject), or null
   u32 rej_cap;
+  unsigned long long deadline_ns;  // time limit on the device clock (%globaltimer), 0 = none
 };
+
+__device__ __forceinline__ unsigned long long dev_now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Efficient-mode pre-filter: reaches(a, b) over the iteration-start snapshot
 // (reference cycles.py:52-57, 151-169), dense class indices via cls_index.

@@ -1184,6 +1184,7 @@ struct WaveIO {
 #define CR_ERROR 6    // analysis/table capacity error (exact path reports it)
 #define CR_NOTRUN 7   // chained launch skipped: an earlier rule of the chain returned to the host
 #define CR_NARROW 8   // grid-mode loop: windows shrank to single-CTA size
+#define CR_TIMEOUT 9  // the time limit passed before the next wave (device clock)
 
 struct CtaCtl {
   unsigned long long p, P;
@@ -1528,6 +1529,8 @@ __global__ void __launch_bounds__(CTA_T, 1) k_wave_cta(G g, RuleDev R, ReachDev 
         ctl->seq_stop = 1;
         ctl->overshoot = (i64)cn->live - A.n_max;
         S->exit = CR_STOP;
+      } else if (R.deadline_ns && dev_now_ns() > R.deadline_ns) {
+        S->exit = CR_TIMEOUT;  // the next wave's combos are not reached (explorer.py:198-201)
       } else {
         u32 win = ctl->win;
         u32 ncand;
@@ -2221,6 +2224,9 @@ static bool cta_exit(Engine& e, WaveBufs& B, int ri, const CtaCtl& c, unsigned l
     e.seq_stop = true;
     e.report.node_limit_overshoot = c.overshoot;
     return true;
+  } else if (c.reason == CR_TIMEOUT) {
+    e.seq_timeout = true;
+    return true;
   } else if (c.reason == CR_HAZARD) {
     e.phase_ms[9] += 1;
     if (multi) jvalid = false;
@@ -2300,6 +2306,10 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     if ((i64)e.h.live >= n_max) {
       e.seq_stop = true;
       e.report.node_limit_overshoot = (i64)e.h.live - n_max;
+      break;
+    }
+    if (e.apply_deadline >= 0 && now_s() > e.apply_deadline) {
+      e.seq_timeout = true;
       break;
     }
     RuleDev Rd = make_rule_dev(e, ri, filter_mode, allow_self);
