@@ -168,7 +168,8 @@ static __device__ u32 tree_intern(const TreeTab& tt, int npos, const i64* pos, c
       if (prev == TSAT_NONE) return mine;
       cur = prev;
     }
-    __threadfence();
+    // no fence here: the inserter fenced its tree before publishing the id,
+    // and tree_eq's volatile (L2) loads are address-dependent on that id
     if (tree_eq(&tt.trees[cur], npos, pos, kid)) return cur;
     slot = (slot + 1) & tt.hc_mask;
   }

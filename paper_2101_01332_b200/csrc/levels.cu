@@ -724,17 +724,25 @@ u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrim
     CUDA_OK(cudaMemcpyAsync(hc, ctl.p, 4 * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
     lvl_off.resize((size_t)n + 2);
     CUDA_OK(cudaMemcpyAsync(lvl_off.data(), X.c_lvloff.p, ((u64)n + 2) * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-    e.sync();
+    e.sync();  // (async path: n is small here, the whole offset array is a few KB)
     static const bool dbg = getenv("TSAT_DEBUG_LEVELS") != nullptr;
     if (dbg) fprintf(stderr, "peel_async: n %u ne %u walk %.1f us sort %.1f us\n", n, e.cg_ne, hc[2] * 1e-3, hc[3] * 1e-3);
     tot = hc[0];
     nl = hc[1];
   } else {
-    lvl_off.resize((size_t)n + 2);
-    run_frontier(e, F, 0, nl, tot, e.cg_ne, lvl_off.data());  // class graph: reverse edges = forward edges
+    // small graphs: the level offsets come back with the final control read
+    // (one sync); large ones (10^6 classes) copy only the [0, nl] used
+    const bool fold = n <= (1u << 16);
+    lvl_off.resize(fold ? (size_t)n + 2 : 0);
+    run_frontier(e, F, 0, nl, tot, e.cg_ne, fold ? lvl_off.data() : nullptr);
+    if (!fold) {
+      lvl_off.resize(nl + 1);
+      CUDA_OK(cudaMemcpyAsync(lvl_off.data(), X.c_lvloff.p, (nl + 1) * sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+      e.sync();
+    }
   }
   ntrimmed = tot;
-  lvl_off.resize(nl + 1);  // offsets [0, nl] came back with the final control read
+  lvl_off.resize(nl + 1);
   return nl;
 }
 
