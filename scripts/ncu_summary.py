@@ -59,7 +59,7 @@ def main(d, out):
             a["share"] = round(a["us"] / tot, 4) if tot else 0
         b["kernels"] = dict(sorted(b["kernels"].items(), key=lambda kv: -kv[1]["us"]))
         res["bert_step"] = b
-        wave = [k for k in b["kernels"] if k.startswith("k_wave_cta")]
+        wave = [k for k in b["kernels"] if "k_wave_cta" in k]
         if wave:
             a = b["kernels"][wave[0]]
             res["apply_wave"] = {"kernel": "k_wave_cta (BERT step)", "launches": a["launches"],
