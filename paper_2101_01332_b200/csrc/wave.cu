@@ -1913,8 +1913,8 @@ static void accumulate_seg(Engine& e, int ri, const DevStats& d) {
 
 
 #define CTA_WIN_1 2048u
-// thread-block cluster size of the wave loop (TSAT_WAVE_CLUSTER: 1, 2, 4, 8
-// or 16) and the largest window it runs (one candidate per thread).  Default
+// thread-block cluster size of the wave loop (TSAT_WAVE_CLUSTER: 1 or 8; 2, 4
+// and 16 were measured too) and the largest window it runs (one candidate per thread).  Default
 // 1: measured on BERT (scripts/cluster_sweep.sh), larger windows do not cut
 // the wave count -- waves end at the sequential-order conflicts (~1 per 2k
 // combos), and a bigger window only adds soft writers to the serial
@@ -1925,7 +1925,7 @@ static int wave_nc() {
   if (nc < 0) {
     const char* v = getenv("TSAT_WAVE_CLUSTER");
     nc = v ? atoi(v) : 1;
-    if (nc != 1 && nc != 2 && nc != 4 && nc != 8 && nc != 16) nc = 1;
+    if (nc != 1 && nc != 8) nc = 1;
   }
   return nc;
 }
@@ -2105,19 +2105,8 @@ static void cta_launch(Engine& e, WaveBufs& B, int ri, const RuleDev& Rd, const 
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    switch (nc) {
-      case 2: CUDA_OK(cudaLaunchKernelEx(&cfg, k_wave_cta<2>, gv, Rd, RD, W, T, io, A, dctl, prev)); break;
-      case 4: CUDA_OK(cudaLaunchKernelEx(&cfg, k_wave_cta<4>, gv, Rd, RD, W, T, io, A, dctl, prev)); break;
-      case 8: CUDA_OK(cudaLaunchKernelEx(&cfg, k_wave_cta<8>, gv, Rd, RD, W, T, io, A, dctl, prev)); break;
-      default: {
-        static int np_set = 0;
-        if (!np_set) {
-          CUDA_OK(cudaFuncSetAttribute(k_wave_cta<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-          np_set = 1;
-        }
-        CUDA_OK(cudaLaunchKernelEx(&cfg, k_wave_cta<16>, gv, Rd, RD, W, T, io, A, dctl, prev));
-      }
-    }
+    // one instantiation (compile time); the 2 / 4 / 16 variants measured no better
+    CUDA_OK(cudaLaunchKernelEx(&cfg, k_wave_cta<8>, gv, Rd, RD, W, T, io, A, dctl, prev));
     return;
   }
   size_t smem_bytes = 0;
