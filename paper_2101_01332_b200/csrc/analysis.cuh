@@ -49,12 +49,18 @@ struct Val {
   u32 o1[MAXO];
 };
 
-struct Tree {
+// One tree per 128-byte line: a published tree is immutable and no other
+// tree shares its line, so readers may cache it in L1 (a popular tree --
+// every combo of a merge rule builds the same concat -- otherwise turns into
+// one hot L2 line read by every thread of the wave)
+struct __align__(128) Tree {
   int32_t npos;
   int32_t pad;
   i64 pos[TREE_MAXPOS];
   u32 kid[TREE_MAXPOS + 1];  // TREE_NONE = no subtree
+  u32 pad2[14];
 };
+static_assert(sizeof(Tree) == 128, "one tree per 128-byte line");
 
 struct TreeTab {
   Tree* trees;
@@ -136,13 +142,14 @@ __device__ __forceinline__ u64 tree_hash(int npos, const i64* pos, const u32* ki
   return h;
 }
 
+// cached loads: t was published (its id read from the table) after the
+// inserter fenced its contents, and its line holds no other tree
 __device__ __forceinline__ bool tree_eq(const Tree* t, int npos, const i64* pos, const u32* kid) {
-  const volatile Tree* vt = (const volatile Tree*)t;
-  if (vt->npos != npos) return false;
+  if (t->npos != npos) return false;
   for (int i = 0; i < npos; i++)
-    if (vt->pos[i] != pos[i]) return false;
+    if (t->pos[i] != pos[i]) return false;
   for (int i = 0; i <= npos; i++)
-    if (vt->kid[i] != kid[i]) return false;
+    if (t->kid[i] != kid[i]) return false;
   return true;
 }
 
@@ -152,7 +159,9 @@ static __device__ u32 tree_intern(const TreeTab& tt, int npos, const i64* pos, c
   u32 slot = (u32)h & tt.hc_mask;
   u32 mine = TSAT_NONE;
   for (u32 probe = 0; probe <= tt.hc_mask; probe++) {
-    u32 cur = ((volatile u32*)tt.hc)[slot];
+    // a slot goes NONE -> id once per engine lifetime: a stale NONE only
+    // sends this thread to the CAS below, which returns the published id
+    u32 cur = tt.hc[slot];
     if (cur == TSAT_NONE) {
       if (mine == TSAT_NONE) {
         mine = atomicAdd(tt.count, 1u);
@@ -177,7 +186,7 @@ static __device__ u32 tree_intern(const TreeTab& tt, int npos, const i64* pos, c
 }
 
 __device__ __forceinline__ void tree_read(const TreeTab& tt, u32 id, int& npos, i64* pos, u32* kid) {
-  const volatile Tree* t = (const volatile Tree*)&tt.trees[id];
+  const Tree* t = &tt.trees[id];  // published, immutable, alone in its line
   npos = t->npos;
   for (int i = 0; i < TREE_MAXPOS; i++) pos[i] = t->pos[i];
   for (int i = 0; i <= TREE_MAXPOS; i++) kid[i] = t->kid[i];

@@ -29,8 +29,8 @@ VAL_DTYPE = np.dtype(
     [("kind", "i1"), ("r0", "i1"), ("r1", "i1"), ("n0", "i1"), ("n1", "i1"), ("pad", "i1", 3),
      ("iv", "<i8"), ("d0", "<i8", 4), ("d1", "<i8", 4), ("o0", "<u4", 6), ("o1", "<u4", 6)]
 )
-TREE_DTYPE = np.dtype([("npos", "<i4"), ("pad", "<i4"), ("pos", "<i8", 5), ("kid", "<u4", 6)])
-assert VAL_DTYPE.itemsize == 128 and TREE_DTYPE.itemsize == 72
+TREE_DTYPE = np.dtype([("npos", "<i4"), ("pad", "<i4"), ("pos", "<i8", 5), ("kid", "<u4", 6), ("pad2", "<u4", 14)])
+assert VAL_DTYPE.itemsize == 128 and TREE_DTYPE.itemsize == 128
 
 
 @dataclass
