@@ -13,6 +13,7 @@ from __future__ import annotations
 import functools
 
 import ctypes as C
+import itertools
 from dataclasses import dataclass
 from typing import Any, Iterable, Iterator, Mapping, Optional, Protocol
 
@@ -29,6 +30,7 @@ VAL_DTYPE = np.dtype(
     [("kind", "i1"), ("r0", "i1"), ("r1", "i1"), ("n0", "i1"), ("n1", "i1"), ("pad", "i1", 3),
      ("iv", "<i8"), ("d0", "<i8", 4), ("d1", "<i8", 4), ("o0", "<u4", 6), ("o1", "<u4", 6)]
 )
+_ATOM_ROWS: dict = {}  # encoded atom tables by atom sequence (_flush_atoms)
 TREE_DTYPE = np.dtype([("npos", "<i4"), ("pad", "<i4"), ("pos", "<i8", 5), ("kid", "<u4", 6), ("pad2", "<u4", 14)])
 assert VAL_DTYPE.itemsize == 128 and TREE_DTYPE.itemsize == 128
 
@@ -329,18 +331,21 @@ class EGraph:
         n = len(self._atom_list)
         if n == self._sent:
             return
-        info = [_atom_info(a) for a in self._atom_list]
-        kind = np.array([x[0] for x in info], np.int32)
-        ival = np.array([x[1] for x in info], np.int64)
-        opc = np.array([x[2] for x in info], np.int32)
-        nd = np.array([x[3] for x in info], np.int32)
-        dims = np.array([x[4] for x in info], np.int64).reshape(-1)
-        ni = np.array([x[5] for x in info], np.int32)
-        idims = np.array([x[6] for x in info], np.int64).reshape(-1)
-        names = [str(a).encode() for a in self._atom_list]
-        off = np.zeros(n + 1, np.int64)
-        off[1:] = np.cumsum([len(b) for b in names])
-        blob = b"".join(names) + b"\0"
+        key = tuple((type(a) is int, a) for a in self._atom_list)
+        rows = _ATOM_ROWS.get(key)
+        if rows is None:  # the same atom sequence (same graph / rules) reuses its encoded table
+            info = [_atom_info(a) for a in self._atom_list]
+            names = [str(a).encode() for a in self._atom_list]
+            off = np.zeros(n + 1, np.int64)
+            off[1:] = np.cumsum([len(b) for b in names])
+            rows = (np.array([x[0] for x in info], np.int32), np.array([x[1] for x in info], np.int64),
+                    np.array([x[2] for x in info], np.int32), np.array([x[3] for x in info], np.int32),
+                    np.array([x[4] for x in info], np.int64).reshape(-1), np.array([x[5] for x in info], np.int32),
+                    np.array([x[6] for x in info], np.int64).reshape(-1), b"".join(names) + b"\0", off)
+            if len(_ATOM_ROWS) > 64:
+                _ATOM_ROWS.clear()
+            _ATOM_ROWS[key] = rows
+        kind, ival, opc, nd, dims, ni, idims, blob, off = rows
         lib = _lib.load()
         _lib.check(self._h, lib.tsat_set_atoms(
             self._h, n, _lib.ptr(kind, C.c_int32), _lib.ptr(ival, C.c_int64), _lib.ptr(opc, C.c_int32),
@@ -402,11 +407,13 @@ class EGraph:
 
     # ---------------------------------------------------------------- construction
     def _load_initial(self, ops, kids, root) -> None:
-        op_ids = np.array([self._atom(o) for o in ops], np.uint32)
+        atom = self._atom
+        op_ids = np.fromiter((atom(o) for o in ops), np.uint32, len(ops))
         self._flush_atoms()
         koff = np.zeros(len(ops) + 1, np.uint32)
-        koff[1:] = np.cumsum([len(k) for k in kids])
-        flat = np.array([c for k in kids for c in k] or [0], np.uint32)
+        koff[1:] = np.cumsum(np.fromiter(map(len, kids), np.uint32, len(kids)))
+        flat = np.fromiter(itertools.chain.from_iterable(kids), np.uint32, int(koff[-1])) if koff[-1] else \
+            np.zeros(1, np.uint32)
         _lib.check(self._h, _lib.load().tsat_load_egraph(
             self._h, len(ops), _lib.ptr(op_ids, C.c_uint32), _lib.ptr(koff, C.c_uint32),
             _lib.ptr(flat, C.c_uint32), root))
