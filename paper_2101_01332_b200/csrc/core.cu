@@ -615,11 +615,10 @@ void Engine::load_initial(u32 n, const u32* hop, const u32* hkoff, const u32* hk
       k_make_levels<<<1, 256, 0, s>>>(view(), ids.p, doff.p, (u32)l, (u32)l1);
       l = l1;
     }
-    sync();
   }
   root = r;
   root_ver = ~0ull;
-  check_error();
+  check_error();  // the one sync (the level vectors above outlive it)
 }
 
 // ---------------------------------------------------------------- sequential ops

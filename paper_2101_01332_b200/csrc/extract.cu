@@ -420,8 +420,7 @@ void Engine::costs(int mode, int strict, int ntab, const char* keys, const i64* 
   if (out) CUDA_OK(cudaMemcpyAsync(out, d_costs.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   u32 miss = TSAT_NONE;
   if (strict) CUDA_OK(cudaMemcpyAsync(&miss, dmiss.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  sync();
-  check_error();
+  check_error();  // syncs the stream (the two reads above land first)
   if (miss != TSAT_NONE) {  // UnknownSignature for the first node in id order, with its rendered key (cost.py:170-172)
     DevBuf<char>& kb = sc.k_keyout;
     kb.ensure(512);
@@ -1242,10 +1241,9 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
     sc.g_eoff.ensure(C + 1);
     k_sel_count<<<nblk(C), 256, 0, s>>>(gv, n0.p, C, cnt.p);
     dev_exclusive_scan_u32(*this, cnt.p, sc.g_eoff.p, C + 1);
-    u32 ne;
-    CUDA_OK(cudaMemcpyAsync(&ne, sc.g_eoff.p + C, sizeof(u32), cudaMemcpyDeviceToHost, s));
-    sync();
-    sc.g_edst.ensure(ne + 1);
+    // one chosen node per class: its children are at most all stored children
+    // (no read-back of the exact count)
+    sc.g_edst.ensure((u64)h.nkids + 1);
     k_sel_fill<<<nblk(C), 256, 0, s>>>(gv, n0.p, ci, C, sc.g_eoff.p, sc.g_edst.p);
   }
   DevBuf<u32>& oc = sc.g_oc;
@@ -1293,15 +1291,14 @@ double Engine::greedy(const double* cost_by_node, u32* sel_cls, u32* sel_node, u
     k = bfs_graph(*this, sc.g_eoff.p, sc.g_edst.p, C, rd, mark.p, q.p);
     CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(u32), s));
     k_sel_missing<<<nblk(k), 256, 0, s>>>(q.p, k, n0.p, flag.p);
-    u32 miss;
-    CUDA_OK(cudaMemcpyAsync(&miss, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
-    sync();
-    if (miss) throw TsatException(TSAT_ERR_STATE, "no selected node covers a reached e-class");
     k_sel_collect<<<nblk(k), 256, 0, s>>>(q.p, k, snap.cls_ids.p, n0.p, oc.p, on.p);
   }
+  u32 miss = 0;
+  if (!sweep) CUDA_OK(cudaMemcpyAsync(&miss, flag.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaMemcpyAsync(sel_cls, oc.p, k * sizeof(u32), cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaMemcpyAsync(sel_node, on.p, k * sizeof(u32), cudaMemcpyDeviceToHost, s));
-  sync();
+  sync();  // one read-back: the coverage flag with the selection
+  if (miss) throw TsatException(TSAT_ERR_STATE, "no selected node covers a reached e-class");
   *nsel = k;
   return rcost;
 }
