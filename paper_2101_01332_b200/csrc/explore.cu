@@ -20,6 +20,8 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
 void run_rules_chain(Engine& e, const std::vector<int>& rules, const std::vector<unsigned long long>& Ps,
                      int filter_mode, int allow_self, i64 n_max);
 u32 wave_cta_cap();
+void begin_wave_stats(Engine& e);
+void flush_wave_stats(Engine& e);
 
 
 // ---------------------------------------------------------------- rule loading
@@ -631,6 +633,7 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
       chain.clear();
       chainP.clear();
     };
+    begin_wave_stats(*this);
     for (int ri : active) {
       const HRule& hr = rules[ri];
       unsigned long long P = 1;
@@ -654,6 +657,7 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
       if (seq_stop || seq_timeout) break;
     }
     if (!seq_stop && !seq_timeout) flush();
+    flush_wave_stats(*this);
     if (!stop_flag) {
       if (seq_stop) stop_flag = 2;
       else if (seq_timeout) stop_flag = 3;

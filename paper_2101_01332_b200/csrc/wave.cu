@@ -1761,6 +1761,10 @@ struct WaveBufs {
   DevBuf<u8> ukind, grow, sa;
   DevBuf<WaveState> ws;
   DevBuf<DevStats> wstats;
+  // deferred per-rule statistics (saturate reads an iteration's slots once)
+  DevBuf<DevStats> wstats_def;
+  std::vector<int> def_ri;
+  DevStats* ws_cur = nullptr;  // the rule's statistics slot in use
   DevBuf<int> lvl;
   DevBuf<ReqT> tmpl;
   // wave table
@@ -2160,7 +2164,7 @@ static void grid_launch(Engine& e, WaveBufs& B, int ri, const RuleDev& Rd, const
   WaveTab T{B.wminpos.p, B.wid.p, B.wroot.p, B.wval.p, B.wcap - 1, B.wold.p, 0, B.wtag.p, B.wown.p};
   WaveIO io{B.status.p, B.hazard.p, B.ukind.p, B.grow.p, B.sa.p, B.env.p, B.olds.p, B.pre.p, B.acc.p,
             B.ident.p, B.alloc.p, B.apre.p, B.wf.p, B.wpre.p, B.ka.p, B.kpre.p, B.uother.p, B.stops.p,
-            B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.wstats.p, B.lvl_all.p + RWc.lvl_base};
+            B.akid.p, B.ckpre.p, B.fw_cls.p, B.fw_fresh.p, B.ws.p, B.ws_cur, B.lvl_all.p + RWc.lvl_base};
   CtaArgs A;
   memset(&A, 0, sizeof(A));
   A.nlv = (int)lv.size();
@@ -2274,10 +2278,15 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     e.rej_pending = &rej_seq;
   }
   B.wstats.ensure(1);
-  if (resume_stats) CUDA_OK(cudaMemcpyAsync(B.wstats.p, resume_stats, sizeof(DevStats), cudaMemcpyHostToDevice, e.s));
-  else CUDA_OK(cudaMemsetAsync(B.wstats.p, 0, sizeof(DevStats), e.s));
+  // statistics slot: deferred (saturate reads all of an iteration's rules in
+  // one read-back) unless this rule's rejects must be handed over now
+  const bool defer = e.defer_wave_stats && !rec && B.def_ri.size() < B.wstats_def.cap;
+  B.ws_cur = defer ? B.wstats_def.p + B.def_ri.size() : B.wstats.p;
+  if (defer) B.def_ri.push_back(ri);
+  if (resume_stats) CUDA_OK(cudaMemcpyAsync(B.ws_cur, resume_stats, sizeof(DevStats), cudaMemcpyHostToDevice, e.s));
+  else CUDA_OK(cudaMemsetAsync(B.ws_cur, 0, sizeof(DevStats), e.s));
   B.stops.ensure(6);
-  CUDA_OK(cudaMemsetAsync(B.stops.p + 4, 0, sizeof(u32), e.s));  // grid-wave soft writers resolved
+  if (!defer) CUDA_OK(cudaMemsetAsync(B.stops.p + 4, 0, sizeof(u32), e.s));  // grid-wave soft writers resolved
   // multi-pattern join cache: compatible positions stay valid until a union of
   // existing classes changes find() (stop-after waves / exact-path combos)
   bool jvalid = false, jcomplete = true;
@@ -2364,7 +2373,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       CUDA_OK(cudaMemcpyAsync(B.ctl.p, B.hctl, sizeof(c), cudaMemcpyHostToDevice, e.s));
       {
         KTimer kt(e, KG_APPLY_WAVE, 0.0, 1);
-        cta_launch(e, B, ri, Rd, RD, skip_self, multi, n_max, B.ctl.p, nullptr, B.wstats.p);
+        cta_launch(e, B, ri, Rd, RD, skip_self, multi, n_max, B.ctl.p, nullptr, B.ws_cur);
         CUDA_OK(cudaMemcpyAsync(B.hctl, B.ctl.p, sizeof(c), cudaMemcpyDeviceToHost, e.s));
         CUDA_OK(cudaMemcpyAsync(B.hcnt, e.cnt.p, sizeof(Counters), cudaMemcpyDeviceToHost, e.s));
         e.sync();
@@ -2523,7 +2532,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       k_boundary<<<1, 1, 0, e.s>>>(ws, B.stops.p, ncand, posp, p, seg_end, B.pre.p, B.hazard.p);
       // ---- 5. statistics of the committed segment (device accumulators)
       k_seg_stats<<<nblk(ncand), 256, 0, e.s>>>(B.status.p, ws, ncand, B.pre.p, B.alloc.p, B.ukind.p, Rd.efficient,
-                                                B.wstats.p, Rd, p, posp);
+                                                B.ws_cur, Rd, p, posp);
       // ---- 6. commit
       if (nreq_max) {
         k_win_flags<<<nblk(nreq_max), 256, 0, e.s>>>(T, B.ident.p, nreq_max, W.tmpl, R, ws, B.wf.p, B.ka.p);
@@ -2595,9 +2604,10 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
     }
     p = p_end;
   }
+  if (defer) return;  // read with the iteration's other rules (flush_wave_stats)
   DevStats d;
   u32 gres = 0;
-  CUDA_OK(cudaMemcpyAsync(&d, B.wstats.p, sizeof(d), cudaMemcpyDeviceToHost, e.s));
+  CUDA_OK(cudaMemcpyAsync(&d, B.ws_cur, sizeof(d), cudaMemcpyDeviceToHost, e.s));
   CUDA_OK(cudaMemcpyAsync(&gres, B.stops.p + 4, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
   e.sync();
   e.phase_ms[29] += gres;
@@ -2729,4 +2739,33 @@ void run_rules_chain(Engine& e, const std::vector<int>& rules, const std::vector
     run_rules_chain(e, rest, restP, filter_mode, allow_self, n_max);
     return;
   }
+}
+
+// saturate's rule loop defers each wave rule's statistics to one read-back
+// per iteration (begin: slots for every rule; flush: read them, accumulate in
+// rule order -- the counters are sums, so the order does not matter)
+void begin_wave_stats(Engine& e) {
+  if (!e.wave) e.wave = new WaveBufs();
+  WaveBufs& B = *e.wave;
+  B.wstats_def.ensure(2 * e.rules.size() + 2);
+  B.def_ri.clear();
+  B.stops.ensure(6);
+  CUDA_OK(cudaMemsetAsync(B.stops.p + 4, 0, sizeof(u32), e.s));
+  e.defer_wave_stats = true;
+}
+
+void flush_wave_stats(Engine& e) {
+  e.defer_wave_stats = false;
+  if (!e.wave) return;
+  WaveBufs& B = *e.wave;
+  const size_t k = B.def_ri.size();
+  if (!k) return;
+  std::vector<DevStats> d(k);
+  u32 gres = 0;
+  CUDA_OK(cudaMemcpyAsync(d.data(), B.wstats_def.p, k * sizeof(DevStats), cudaMemcpyDeviceToHost, e.s));
+  CUDA_OK(cudaMemcpyAsync(&gres, B.stops.p + 4, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+  e.sync();
+  e.phase_ms[29] += gres;
+  for (size_t i = 0; i < k; i++) accumulate_seg(e, B.def_ri[i], d[i]);
+  B.def_ri.clear();
 }
