@@ -181,6 +181,7 @@ Engine::~Engine() {
     cudaStreamDestroy(s2);
   }
   if (ev_ov) cudaEventDestroy(ev_ov);
+  if (pin_small) cudaFreeHost(pin_small);
   if (s) {
     dev_cache_forget_stream(s);
     cudaStreamDestroy(s);

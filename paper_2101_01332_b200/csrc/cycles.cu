@@ -351,20 +351,25 @@ void build_class_graph(Engine& e) {
   CUDA_OK(cudaMemsetAsync(X.cg_mdeg.p + m, 0, sizeof(u32), e.s));
   dev_exclusive_scan_u32(e, X.cg_mdeg.p, X.cg_moff.p, m + 1);
   k_class_eoff<<<nblk((u64)n + 1), 256, 0, e.s>>>(S.cls_off.p, X.cg_moff.p, n, X.cg_eoff.p);
-  u32 ne;
-  CUDA_OK(cudaMemcpyAsync(&ne, X.cg_moff.p + m, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-  e.sync();
+  // No host read of the edge count: the buffers and the sort take the bound
+  // ub = stored children of all nodes (>= the live, unfiltered member edges),
+  // the slots past the real edges hold key 0xFFFFFFFF, which sorts after every
+  // class index, so roff[n] = the real count.  The level peel that follows
+  // reads it back with its own results (trim_levels), so the class graph
+  // costs no host round trip before the peel is launched.
+  const u32 ub = e.h.nkids;
   e.cg_n = n;
-  e.cg_ne = ne;
-  X.cg_edst.ensure(ne + 1);
-  X.cg_esrc.ensure(ne + 1);
-  X.cg_sdst.ensure(ne + 1);
-  X.cg_rsrc.ensure(ne + 1);
+  e.cg_ne = ub;  // upper bound until trim_levels reads roff[n]
+  X.cg_edst.ensure((u64)ub + 1);
+  X.cg_esrc.ensure((u64)ub + 1);
+  X.cg_sdst.ensure((u64)ub + 1);
+  X.cg_rsrc.ensure((u64)ub + 1);
   X.cg_roff.ensure(n + 1);
+  if (ub) CUDA_OK(cudaMemsetAsync(X.cg_edst.p, 0xFF, (size_t)ub * sizeof(u32), e.s));
   k_member_fill<<<nblk(m), 256, 0, e.s>>>(e.view(), S.cls_nodes.p, S.cls_of.p, S.cls_index.p, m, X.cg_moff.p,
                                           X.cg_edst.p, X.cg_esrc.p);
-  if (ne) dev_sort_pairs_u32(e, X.cg_edst.p, X.cg_sdst.p, X.cg_esrc.p, X.cg_rsrc.p, ne, bits_for(n));
-  k_lower_bounds2<<<nblk((u64)n + 1), 256, 0, e.s>>>(X.cg_sdst.p, ne, n, X.cg_roff.p);
+  if (ub) dev_sort_pairs_u32(e, X.cg_edst.p, X.cg_sdst.p, X.cg_esrc.p, X.cg_rsrc.p, ub, bits_for(n));
+  k_lower_bounds2<<<nblk((u64)n + 1), 256, 0, e.s>>>(X.cg_sdst.p, ub, n, X.cg_roff.p);
   X.cg_outdeg.ensure(n + 1);
   X.cg_level.ensure(n + 1);
 }

@@ -437,7 +437,8 @@ struct Engine {
   // on_reject support: rejected combos of the last saturate, flattened as
   // [rule, nsrc, (eclass, nb, bindings[nb]) x nsrc] (snapshot match rows)
   bool record_rejects = false;
-  bool defer_wave_stats = false;  // saturate: wave rules' statistics read once per iteration
+  bool defer_wave_stats = false;
+  u32* pin_small = nullptr;  // pinned host words for asynchronous read-backs  // saturate: wave rules' statistics read once per iteration
   std::vector<unsigned long long>* rej_pending = nullptr;  // exact-path rejects inside a wave rule
   std::vector<u32> rejects;
   void record_reject(int ri, unsigned long long p);

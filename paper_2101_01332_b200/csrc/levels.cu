@@ -543,7 +543,8 @@ __global__ void __launch_bounds__(1024) k_peel_async(const u32* eoff, const u32*
     roff[i] = groff[i];
   }
   if (threadIdx.x == 0) roff[n] = groff[n];
-  for (u32 e = threadIdx.x; e < ne; e += blockDim.x) rsrc[e] = grsrc[e];
+  const u32 ne_real = min(ne, groff[n]);  // ne may be the class graph's upper bound
+  for (u32 e = threadIdx.x; e < ne_real; e += blockDim.x) rsrc[e] = grsrc[e];
   __syncthreads();
   for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
     if (mask && !mask[i]) {
@@ -702,6 +703,10 @@ u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrim
   Frontier F{X.cg_eoff.p, X.cg_edst.p, X.cg_roff.p, X.cg_rsrc.p, mask, X.cg_outdeg.p, X.cg_level.p,
              X.c_order.p, X.c_lvloff.p, nullptr, n, 0};
   u32 nl = 0, tot = 0;
+  // the real edge count comes back with the peel's results (the class graph
+  // was built on an upper bound, build_class_graph)
+  if (!e.pin_small) CUDA_OK(cudaMallocHost((void**)&e.pin_small, 16 * sizeof(u32)));
+  CUDA_OK(cudaMemcpyAsync(e.pin_small, X.cg_roff.p + n, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
   static const bool no_async = getenv("TSAT_PEEL_SYNC") != nullptr;
   // the barrier-free walk only when the whole reverse graph sits in shared
   // memory: with edges in L2 every class pays a dependent round trip and the
@@ -743,6 +748,7 @@ u32 trim_levels(Engine& e, const u8* mask, std::vector<u32>& lvl_off, u32& ntrim
   }
   ntrimmed = tot;
   lvl_off.resize(nl + 1);
+  e.cg_ne = e.pin_small[0];  // landed before the peel's read-back (same stream, pinned)
   return nl;
 }
 
