@@ -1917,6 +1917,10 @@ static void accumulate_seg(Engine& e, int ri, const DevStats& d) {
 
 
 #define CTA_WIN_1 2048u
+// grid waves: one-CTA scans up to this size (a 1024-thread CTA walks 8k
+// elements per tile step); larger ones take CUB's decoupled look-back scan
+// (two launches, ~8 us) -- a 64k one-CTA scan took ~27 us
+#define SCAN1_MAX 16384u
 // thread-block cluster size of the wave loop (TSAT_WAVE_CLUSTER: 1 or 8; 2, 4
 // and 16 were measured too) and the largest window it runs (one candidate per thread).  Default
 // 1: measured on BERT (scripts/cluster_sweep.sh), larger windows do not cut
@@ -2471,7 +2475,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       KTimer kt(e, KG_APPLY_WAVE, 0.0, 16 + lv.size());
       k_gates<<<nblk(ncand, 128), 128, 0, e.s>>>(e.view(), Rd, RD, W, posp, ncand, p, B.status.p, B.env.p, B.olds.p,
                                                  B.hazard.p);
-      if (ncand <= 65536) {
+      if (ncand <= 65536) {  // the accepted-list variant replaces 5 launches
         k_accept_scan<<<1, 1024, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.pre.p, B.acc.p, ws);
       } else {
         k_accept_flags<<<nblk(ncand), 256, 0, e.s>>>(B.status.p, B.hazard.p, ncand, B.fl.p);
@@ -2522,7 +2526,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
         unsigned nb = (unsigned)std::min<u64>((u64)coop_blocks, std::max<u64>(1, ((u64)ncand + 255) / 256));
         CUDA_OK(cudaLaunchCooperativeKernel((const void*)k_conflicts_grid, nb, 256, args, 0, e.s));
       }
-      if (ncand <= 65536) {
+      if (ncand <= SCAN1_MAX) {
         k_scan_block<<<1, 1024, 0, e.s>>>(B.alloc.p, B.apre.p, ncand);
       } else {
         CUDA_OK(cudaMemsetAsync(B.alloc.p + ncand, 0, sizeof(u32), e.s));
@@ -2536,7 +2540,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       // ---- 6. commit
       if (nreq_max) {
         k_win_flags<<<nblk(nreq_max), 256, 0, e.s>>>(T, B.ident.p, nreq_max, W.tmpl, R, ws, B.wf.p, B.ka.p);
-        if (nreq_max <= 65536) {
+        if (nreq_max <= SCAN1_MAX) {
           k_scan_block<<<1, 1024, 0, e.s>>>(B.wf.p, B.wpre.p, (u32)nreq_max);
           k_scan_block<<<1, 1024, 0, e.s>>>(B.ka.p, B.kpre.p, (u32)nreq_max);
         } else {
