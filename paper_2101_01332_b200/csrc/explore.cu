@@ -21,7 +21,8 @@ void run_rules_chain(Engine& e, const std::vector<int>& rules, const std::vector
                      int filter_mode, int allow_self, i64 n_max);
 u32 wave_cta_cap();
 void begin_wave_stats(Engine& e);
-void flush_wave_stats(Engine& e);
+void flush_wave_stats_begin(Engine& e);
+void flush_wave_stats_finish(Engine& e);
 
 
 // ---------------------------------------------------------------- rule loading
@@ -657,7 +658,7 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
       if (seq_stop || seq_timeout) break;
     }
     if (!seq_stop && !seq_timeout) flush();
-    flush_wave_stats(*this);
+    flush_wave_stats_begin(*this);  // read back with the rebuild's read-back
     if (!stop_flag) {
       if (seq_stop) stop_flag = 2;
       else if (seq_timeout) stop_flag = 3;
@@ -665,6 +666,7 @@ void Engine::saturate(const ExploreLimitsC& lim, int filter_mode, int allow_self
     snap.valid = false;
     tick(3, tp);
     rebuild();
+    flush_wave_stats_finish(*this);
     tick(4, tp);
     build_snapshot();
     tick(0, tp);

@@ -1765,6 +1765,9 @@ struct WaveBufs {
   DevBuf<DevStats> wstats_def;
   std::vector<int> def_ri;
   DevStats* ws_cur = nullptr;  // the rule's statistics slot in use
+  DevStats* hdef = nullptr;     // pinned: the deferred slots' read-back
+  size_t hdef_cap = 0;
+  bool def_pending = false;
   DevBuf<int> lvl;
   DevBuf<ReqT> tmpl;
   // wave table
@@ -1797,6 +1800,7 @@ struct WaveBufs {
   CtaCtl* hchain = nullptr;     // pinned: K control blocks, then K DevStats
   size_t chain_cap = 0;
   ~WaveBufs() {
+    if (hdef) cudaFreeHost(hdef);
     if (hchain) cudaFreeHost(hchain);
     if (hctl) cudaFreeHost(hctl);
     if (hcnt) cudaFreeHost(hcnt);
@@ -2753,23 +2757,38 @@ void begin_wave_stats(Engine& e) {
   WaveBufs& B = *e.wave;
   B.wstats_def.ensure(2 * e.rules.size() + 2);
   B.def_ri.clear();
+  B.def_pending = false;
   B.stops.ensure(6);
   CUDA_OK(cudaMemsetAsync(B.stops.p + 4, 0, sizeof(u32), e.s));
   e.defer_wave_stats = true;
 }
 
-void flush_wave_stats(Engine& e) {
+// flush in two halves: the read-back is queued (pinned host memory) and
+// lands with the rebuild's own read-back; finish accumulates it afterwards
+void flush_wave_stats_begin(Engine& e) {
   e.defer_wave_stats = false;
   if (!e.wave) return;
   WaveBufs& B = *e.wave;
   const size_t k = B.def_ri.size();
   if (!k) return;
-  std::vector<DevStats> d(k);
-  u32 gres = 0;
-  CUDA_OK(cudaMemcpyAsync(d.data(), B.wstats_def.p, k * sizeof(DevStats), cudaMemcpyDeviceToHost, e.s));
-  CUDA_OK(cudaMemcpyAsync(&gres, B.stops.p + 4, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
-  e.sync();
-  e.phase_ms[29] += gres;
-  for (size_t i = 0; i < k; i++) accumulate_seg(e, B.def_ri[i], d[i]);
+  if (B.hdef_cap < k + 1) {
+    if (B.hdef) cudaFreeHost(B.hdef);
+    CUDA_OK(cudaMallocHost((void**)&B.hdef, (k + 1) * sizeof(DevStats)));
+    B.hdef_cap = k + 1;
+  }
+  CUDA_OK(cudaMemcpyAsync(B.hdef, B.wstats_def.p, k * sizeof(DevStats), cudaMemcpyDeviceToHost, e.s));
+  CUDA_OK(cudaMemcpyAsync(&B.hdef[k].nrej, B.stops.p + 4, sizeof(u32), cudaMemcpyDeviceToHost, e.s));
+  B.def_pending = true;
+}
+
+void flush_wave_stats_finish(Engine& e) {
+  if (!e.wave) return;
+  WaveBufs& B = *e.wave;
+  if (!B.def_pending) return;
+  e.sync();  // normally already passed by the rebuild's read-back
+  const size_t k = B.def_ri.size();
+  e.phase_ms[29] += B.hdef[k].nrej;  // grid-wave soft writers resolved (carried in a spare slot)
+  for (size_t i = 0; i < k; i++) accumulate_seg(e, B.def_ri[i], B.hdef[i]);
   B.def_ri.clear();
+  B.def_pending = false;
 }
