@@ -192,6 +192,11 @@ int tsat_shard_range(uint64_t n_alloc, int32_t rank, int32_t world, uint32_t* lo
  * costs, greedy, snapshot */
 int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launches, int32_t n, int32_t reset);
 
+/* the engine's CUDA stream (cudaStream_t) -- measurement only: bench.py
+ * records its step events on it, so a step is timed on the device where its
+ * kernels run (no reference counterpart) */
+int tsat_stream(tsat_engine* h, void** stream);
+
 /* diagnostics: level count, peeled classes, classes, class edges, snapshot /
  * filter versions, allocated and live e-nodes, device blocks allocated by the
  * block cache (count, bytes), engines constructed, host stream waits and kernels

@@ -88,6 +88,7 @@ _SIGS = {
     "tsat_phase_times": ([C.c_void_p, f64p, C.c_int32], C.c_int),
     "tsat_debug_info": ([C.c_void_p, i64p, C.c_int32], C.c_int),
     "tsat_kernel_stats": ([C.c_void_p, f64p, f64p, i64p, C.c_int32, C.c_int32], C.c_int),
+    "tsat_stream": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
     "tsat_shard_setup": ([C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_int32], C.c_int),
     "tsat_shard_setup_host": ([C.c_void_p, C.c_int32, C.c_int32, ALLGATHER_FN, C.c_void_p], C.c_int),
     "tsat_nccl_unique_id": ([C.c_char_p, C.c_int32, i32p], C.c_int),

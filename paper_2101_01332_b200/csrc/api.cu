@@ -410,6 +410,8 @@ int tsat_shard_range(uint64_t n_alloc, int32_t rank, int32_t world, uint32_t* lo
   return TSAT_OK;
 }
 
+int tsat_stream(tsat_engine* h, void** stream) { GUARD(h, *stream = (void*)h->e->s); }
+
 int tsat_kernel_stats(tsat_engine* h, double* ms, double* bytes, int64_t* launches, int32_t n, int32_t reset) {
   GUARD(h, {
     Engine& e = *h->e;
