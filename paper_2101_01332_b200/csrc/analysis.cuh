@@ -37,7 +37,7 @@ struct AtomInfo {
   i64 idims[4];
 };
 
-struct Val {
+struct __align__(16) Val {
   int8_t kind;
   int8_t r0, r1;   // ranks of shape / pair halves
   int8_t n0, n1;   // origin counts
@@ -199,6 +199,17 @@ __device__ __forceinline__ bool shape_eq(const i64* a, int ra, const i64* b, int
   for (int i = 0; i < ra; i++)
     if (a[i] != b[i]) return false;
   return true;
+}
+
+// 16-byte-word copy (eight vector loads, then eight vector stores)
+__device__ __forceinline__ void val_copy(Val& d, const Val& s) {
+  const uint4* a = reinterpret_cast<const uint4*>(&s);
+  uint4* b = reinterpret_cast<uint4*>(&d);
+  uint4 w[sizeof(Val) / 16];
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Val) / 16); i++) w[i] = a[i];
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Val) / 16); i++) b[i] = w[i];
 }
 
 __device__ __forceinline__ bool val_same_data(const Val& a, const Val& b) {
@@ -466,20 +477,26 @@ static __device__ int infer_shape_dev(int op, ValRefs a, int n, Val& out, const 
     }
     case OP_SPLIT0:
     case OP_SPLIT1: {
+      // every load before the first store: out may alias a generic argument
+      // pointer as far as the compiler knows, so interleaved field copies
+      // would serialise load -> store -> load
       const Val& p = a[0];
+      const bool lo = op == OP_SPLIT0;
+      const int8_t r = lo ? p.r0 : p.r1, no = lo ? p.n0 : p.n1;
+      i64 d[4];
+      u32 o[MAXO];
+#pragma unroll
+      for (int i = 0; i < 4; i++) d[i] = lo ? p.d0[i] : p.d1[i];
+#pragma unroll
+      for (int i = 0; i < MAXO; i++) o[i] = lo ? p.o0[i] : p.o1[i];
       val_clear(out);
       out.kind = VK_T;
-      if (op == OP_SPLIT0) {
-        out.r0 = p.r0;
-        for (int i = 0; i < 4; i++) out.d0[i] = p.d0[i];
-        out.n0 = p.n0;
-        for (int i = 0; i < MAXO; i++) out.o0[i] = p.o0[i];
-      } else {
-        out.r0 = p.r1;
-        for (int i = 0; i < 4; i++) out.d0[i] = p.d1[i];
-        out.n0 = p.n1;
-        for (int i = 0; i < MAXO; i++) out.o0[i] = p.o1[i];
-      }
+      out.r0 = r;
+      out.n0 = no;
+#pragma unroll
+      for (int i = 0; i < 4; i++) out.d0[i] = d[i];
+#pragma unroll
+      for (int i = 0; i < MAXO; i++) out.o0[i] = o[i];
       return AS_OK;
     }
     case OP_MERGE: {

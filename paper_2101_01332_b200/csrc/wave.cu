@@ -337,7 +337,7 @@ __device__ __forceinline__ void d_resolve_verify(u64 tid, u64 nth, const G& g, c
       Val v;
       int st = val_make(q.atom, ValRefs{kv}, n, v, g.atoms, g.tt);
       if (st != AS_OK) hazard[c] = 2;
-      else if (own == (u32)gpos) T.val[s] = v;
+      else if (own == (u32)gpos) val_copy(T.val[s], v);
     }
   }
 }

@@ -488,7 +488,12 @@ class EGraph:
 
     def set_filter(self, filt: Iterable[int]) -> None:
         """Replace the device filter list (every call taking ``filt`` uploads it)."""
-        want = frozenset(int(x) for x in filt)
+        # the common call passes back the set saturate() returned: compare
+        # before converting element by element
+        want = filt if isinstance(filt, frozenset) else frozenset(filt)
+        if self._filt_dev is not None and want == self._filt_dev:
+            return
+        want = frozenset(int(x) for x in want)
         if self._filt_dev is not None and want == self._filt_dev:
             return
         n_alloc = self._sizes()[0]
@@ -504,9 +509,9 @@ class EGraph:
     def get_filter(self) -> list:
         lib = _lib.load()
         n = C.c_int64()
-        cap = 1024
+        cap = max(self._sizes()[0], 1)  # upper bound: one device compaction, no retry
         while True:
-            out = np.zeros(cap, np.uint32)
+            out = np.empty(cap, np.uint32)
             _lib.check(self._h, lib.tsat_get_filter(self._h, _lib.ptr(out, C.c_uint32), cap, C.byref(n)))
             if n.value <= cap:
                 return out[: n.value].tolist()

@@ -83,3 +83,10 @@ for d, p0, n in sorted(gl, reverse=True)[:25]:
 print("gap histogram (us): ", {k: sum(1 for d, _, _ in gl if lo <= d < hi) for k, (lo, hi) in
       {"<5": (0, 5), "5-10": (5, 10), "10-20": (10, 20), "20-50": (20, 50), ">50": (50, 1e9)}.items()},
       "total", round(sum(d for d, _, _ in gl) / 1e3, 3), "ms")
+if os.environ.get("TRACE_DUMP"):
+    # full timeline (start offset, duration, gap before, name) for offline reading
+    with open(os.environ["TRACE_DUMP"], "w") as f:
+        t0, last_end = ks[0][0], ks[0][0]
+        for a, b, n in ks:
+            f.write(f"{(a - t0):10.1f} {b - a:8.1f} {max(0.0, a - last_end):8.1f}  {n.split('(')[0][:70]}\n")
+            last_end = max(last_end, b)
