@@ -1941,7 +1941,18 @@ static int wave_nc() {
   }
   return nc;
 }
-u32 wave_cta_cap() { return wave_nc() > 1 ? (u32)wave_nc() * CTA_T : CTA_WIN_1; }
+// largest window of the cluster loop (TSAT_WAVE_CLUSTER_WIN, default one
+// candidate per thread of the cluster)
+static u32 wave_cluster_win() {
+  static u32 w = 0;
+  if (!w) {
+    const char* v = getenv("TSAT_WAVE_CLUSTER_WIN");
+    w = (u32)wave_nc() * CTA_T;
+    if (v && atoi(v) >= 64 && (u32)atoi(v) < w) w = (u32)atoi(v);
+  }
+  return w;
+}
+u32 wave_cta_cap() { return wave_nc() > 1 ? wave_cluster_win() : CTA_WIN_1; }
 #define CTA_WIN (wave_cta_cap())
 
 // per-candidate buffers, wave table and first-writer arrays for windows of up
@@ -2103,7 +2114,7 @@ static void cta_launch(Engine& e, WaveBufs& B, int ri, const RuleDev& Rd, const 
   if (nc > 1) {
     G gv = e.view();
     A.smem = 0;
-    A.cta_win = (u32)nc * CTA_T;
+    A.cta_win = wave_cluster_win();
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(nc, 1, 1);
