@@ -14,9 +14,15 @@ from paper_2101_01332_b200.extract import greedy_extract  # noqa: E402
 from paper_2101_01332_b200.rules import default_rules  # noqa: E402
 from paper_2101_01332_b200.tensor_lang import build_egraph, initial_enodes  # noqa: E402
 
-g = models.MODELS["bert"]()
-rules = list(default_rules())
-lim = ExploreLimits(k_multi=1)
+name = sys.argv[1] if len(sys.argv) > 1 else "bert"
+if name == "bert":
+    g = models.MODELS["bert"]()
+    rules = list(default_rules())
+    lim = ExploreLimits(k_multi=1)
+else:  # a bench.py workload (e.g. synth10m)
+    import bench
+    g, rules, w = bench.build_workload(name)
+    lim = ExploreLimits(n_max=w["n_max"], k_max=w["k_max"], k_multi=w["k_multi"])
 for rep in range(6):
     torch.cuda.synchronize()
     t = [time.perf_counter()]
@@ -31,6 +37,18 @@ for rep in range(6):
     res = greedy_extract(eg, costs, filt)
     torch.cuda.synchronize()
     t.append(time.perf_counter())
+    if name != "bert" and rep == 5:
+        import cProfile
+        import pstats
+        eg2, _ = build_egraph(g)
+        pr = cProfile.Profile()
+        pr.enable()
+        f2, _ = saturate(eg2, rules, lim, "efficient")
+        c2 = egraph_costs(eg2, CostModel())
+        greedy_extract(eg2, c2, f2)
+        torch.cuda.synchronize()
+        pr.disable()
+        pstats.Stats(pr).sort_stats("tottime").print_stats(15)
     d = [1e3 * (b - a) for a, b in zip(t, t[1:])]
     print("initial_enodes %.3f build_egraph(incl.) %.3f saturate %.3f costs %.3f greedy %.3f | total %.3f ms" %
           (d[0], d[1], d[2], d[3], d[4], sum(d[1:])))
