@@ -1952,6 +1952,29 @@ static u32 wave_cluster_win() {
   }
   return w;
 }
+// growth factor of the grid path's window after a clean full wave (TSAT_WIN_GROW;
+// 16 measured against 4 / 8 (scripts/grow_sweep.sh): configs[4] apply 8.9 -> 8.3 ms,
+// the fixed cost of a grid wave (~0.3 ms of launches and read-backs) paid on fewer
+// ramp-up waves; BERT unchanged)
+static u32 wave_grow() {
+  static u32 gf = 0;
+  if (!gf) {
+    const char* v = getenv("TSAT_WIN_GROW");
+    gf = v && atoi(v) >= 2 && atoi(v) <= 64 ? (u32)atoi(v) : 16u;
+  }
+  return gf;
+}
+// largest grid-path window (TSAT_WIN_MAX).  Grid windows start at 16k (TSAT_WIN0),
+// grow 16x per clean full wave up to 1M (scripts/grow_sweep.sh, same box: BERT
+// 10.9 -> 10.6 ms against 4k / 4x / 4M; configs[4] apply 8.9 -> 8.4 ms)
+static u32 wave_win_max() {
+  static u32 wm = 0;
+  if (!wm) {
+    const char* v = getenv("TSAT_WIN_MAX");
+    wm = v && atoi(v) >= 4096 && atoi(v) <= (1 << 22) ? (u32)atoi(v) : (1u << 20);
+  }
+  return wm;
+}
 u32 wave_cta_cap() { return wave_nc() > 1 ? wave_cluster_win() : CTA_WIN_1; }
 #define CTA_WIN (wave_cta_cap())
 
@@ -2312,7 +2335,7 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
   u32 jtotal = 0, jcursor = 0;
   const u32 JCAP = 1u << 24;
   unsigned long long p = 0;
-  static const u32 win0 = getenv("TSAT_WIN0") ? (u32)atoi(getenv("TSAT_WIN0")) : (1u << 12);
+  static const u32 win0 = getenv("TSAT_WIN0") ? (u32)atoi(getenv("TSAT_WIN0")) : (1u << 14);
   u32 win = win0;  // adaptive candidate window (grows on clean waves, shrinks on dependencies)
   bool stopped = false;
   if (resume) {  // a chained single-CTA launch returned here (run_rules_chain)
@@ -2610,8 +2633,8 @@ void run_rule_wave(Engine& e, int ri, int filter_mode, int allow_self, i64 n_max
       continue;
     }
     // adapt the window: dependencies every k combos -> evaluate ~2k ahead
-    if (ncommit_cand < ncand) win = std::max<u32>(64u, std::min<u32>(2u * ncommit_cand + 32u, 1u << 22));
-    else win = std::min<u32>(win * 4u, 1u << 22);
+    if (ncommit_cand < ncand) win = std::max<u32>(64u, std::min<u32>(2u * ncommit_cand + 32u, wave_win_max()));
+    else win = std::min<u32>(win * wave_grow(), wave_win_max());
     if (hazard) {
       e.phase_ms[9] += 1;  // hazards
       // exact sequential path for exactly the hazard combo
@@ -2699,7 +2722,7 @@ void run_rules_chain(Engine& e, const std::vector<int>& rules, const std::vector
   }
   e.ensure_nodes((u64)CTA_WIN * maxR + 2, (u64)CTA_WIN * maxK + 2);
   ensure_cand_bufs(e, B, CTA_WIN, maxR);
-  static const u32 win0 = getenv("TSAT_WIN0") ? (u32)atoi(getenv("TSAT_WIN0")) : (1u << 12);
+  static const u32 win0 = getenv("TSAT_WIN0") ? (u32)atoi(getenv("TSAT_WIN0")) : (1u << 14);
   for (size_t k = 0; k < K; k++) {
     CtaCtl& c = hc[k];
     memset(&c, 0, sizeof(c));
